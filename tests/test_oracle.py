@@ -1,0 +1,219 @@
+"""Pins for the CPU oracle (``-m "not gpu"``).
+
+Each test ties ``oracle/`` to something other than itself: values printed in
+SPEC/PAPER worked examples (tests/golden/), closed forms, textbook special
+cases, an exactly-rounded brute force, or a library routine (numpy / torch
+float64).  Chosen so a dropped term, wrong sign/index or transposed operand
+fails at least one of them (see the 'mutants' test at the bottom).
+"""
+import json
+import math
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import oracle
+from seeded_inputs import MODE_INT, MODE_UNIFORM, gen_f32
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _golden(name):
+    with open(os.path.join(GOLDEN, name)) as f:
+        return json.load(f)
+
+
+# ---------------------------------------------------------------- matmul ----
+
+def test_spec_2x2_worked_example():
+    g = _golden("spec_2x2_matmul.json")
+    C, D = oracle.matmul(np.array(g["A"], float), np.array(g["B"], float))
+    assert C.tolist() == g["C"]
+    # all entries positive, so sum |a||b| equals the product itself
+    assert D.tolist() == g["C"]
+
+
+def test_identity_and_permutation_closed_forms():
+    rng = np.random.default_rng(1)
+    A = rng.standard_normal((7, 5))
+    C, _ = oracle.matmul(A, np.eye(5))
+    assert np.array_equal(C, A)                       # A I = A
+    C, _ = oracle.matmul(np.eye(7), A)
+    assert np.array_equal(C, A)                       # I A = A
+    perm = rng.permutation(5)
+    Pm = np.zeros((5, 5))
+    Pm[perm, np.arange(5)] = 1.0                      # column j of A P = column perm[j] of A
+    C, _ = oracle.matmul(A, Pm)
+    assert np.array_equal(C, A[:, perm])
+
+
+def test_all_ones_and_rank1_closed_forms():
+    M, N, K = 6, 9, 13
+    C, D = oracle.matmul(np.ones((M, K)), np.ones((K, N)))
+    assert np.all(C == K) and np.all(D == K)
+    u = np.arange(1, M + 1, dtype=float) * (-1) ** np.arange(M)
+    v = np.arange(2, N + 2, dtype=float)
+    A = np.repeat(u[:, None], K, axis=1)              # A[i,k] = u_i
+    B = np.repeat(v[None, :], K, axis=0)              # B[k,j] = v_j
+    C, D = oracle.matmul(A, B)
+    assert np.array_equal(C, K * np.outer(u, v))
+    assert np.array_equal(D, K * np.outer(np.abs(u), np.abs(v)))
+
+
+def test_brute_force_exact_on_integer_data():
+    """Exact Python-integer brute force, non-square shapes (catches transposes)."""
+    for (M, N, K) in [(1, 1, 1), (3, 4, 5), (5, 3, 7), (8, 2, 9)]:
+        A = gen_f32(11, M * K, MODE_INT).reshape(M, K).astype(int)
+        B = gen_f32(12, K * N, MODE_INT).reshape(K, N).astype(int)
+        C, D = oracle.matmul(A.astype(float), B.astype(float))
+        for i in range(M):
+            for j in range(N):
+                assert C[i, j] == sum(int(A[i, k]) * int(B[k, j]) for k in range(K))
+                assert D[i, j] == sum(abs(int(A[i, k])) * abs(int(B[k, j])) for k in range(K))
+
+
+def test_exactly_rounded_sum_on_float_data():
+    """fp64 summation error bound: |C - exact| <= K * 2^-53 * D (summation only;
+    products of fp32 inputs are exact in fp64)."""
+    M, N, K = 4, 5, 257
+    A = gen_f32(21, M * K).reshape(M, K).astype(np.float64)
+    B = gen_f32(22, K * N).reshape(K, N).astype(np.float64)
+    C, D = oracle.matmul(A, B)
+    for i in range(M):
+        for j in range(N):
+            exact = sum(Fraction(A[i, k]) * Fraction(B[k, j]) for k in range(K))
+            assert abs(Fraction(C[i, j]) - exact) <= Fraction(K) * Fraction(2) ** -53 * Fraction(D[i, j])
+            assert D[i, j] == pytest.approx(math.fsum(abs(A[i, k] * B[k, j]) for k in range(K)), rel=1e-14)
+
+
+def test_numpy_float64_matmul_agrees():
+    M, N, K = 33, 47, 129
+    A = gen_f32(31, M * K).reshape(M, K).astype(np.float64)
+    B = gen_f32(32, K * N).reshape(K, N).astype(np.float64)
+    C, D = oracle.matmul(A, B)
+    ref = A @ B
+    assert np.max(np.abs(C - ref) / D) < 1e-14
+    assert np.allclose(D, np.abs(A) @ np.abs(B), rtol=1e-14, atol=0)
+
+
+def test_paper_fig2_shape_256x258x512_integer():
+    """The paper's running example I=256, J=258, K=512, integer data,
+    checked against exact integer numpy matmul (int64 has no rounding)."""
+    A = gen_f32(41, 256 * 512, MODE_INT).reshape(256, 512)
+    B = gen_f32(42, 512 * 258, MODE_INT).reshape(512, 258)
+    C, _ = oracle.matmul(A, B)
+    assert np.array_equal(C.astype(np.int64), A.astype(np.int64) @ B.astype(np.int64))
+
+
+# ---------------------------------------------------------------- conv2d ----
+
+def test_conv_output_shapes_golden():
+    g = _golden("conv_shapes.json")
+    for c in g["cases"]:
+        P, Q = oracle.conv_out_hw(c["H"], c["W"], c["R"], c["S"], (c["stride"],) * 2, (c["pad"],) * 2)
+        assert (P, Q) == (c["P"], c["Q"])
+
+
+def test_conv_delta_kernel_is_identity():
+    x = gen_f32(51, 2 * 5 * 6 * 3).reshape(2, 5, 6, 3).astype(np.float64)
+    w = np.zeros((3, 3, 3, 3))
+    for c in range(3):
+        w[1, 1, c, c] = 1.0                            # w[r,s,c,f] = [r=1][s=1][c=f]
+    y, _ = oracle.conv2d(x, w, (1, 1), (1, 1))
+    assert np.array_equal(y, x)
+
+
+def test_conv_all_ones_padding_closed_form():
+    """All-ones x, w, 3x3, pad 1: interior 9C, edges 6C, corners 4C."""
+    N, H, W, C, F = 1, 5, 7, 4, 2
+    y, D = oracle.conv2d(np.ones((N, H, W, C)), np.ones((3, 3, C, F)), (1, 1), (1, 1))
+    expect = np.full((H, W), 9.0 * C)
+    expect[0, :] = expect[-1, :] = 6.0 * C
+    expect[:, 0] = expect[:, -1] = 6.0 * C
+    expect[0, 0] = expect[0, -1] = expect[-1, 0] = expect[-1, -1] = 4.0 * C
+    for f in range(F):
+        assert np.array_equal(y[0, :, :, f], expect)
+    assert np.array_equal(D, y)
+
+
+def test_conv_1x1_equals_matmul():
+    N, H, W, C, F = 2, 3, 4, 5, 6
+    x = gen_f32(61, N * H * W * C, MODE_INT).reshape(N, H, W, C).astype(np.float64)
+    w = gen_f32(62, C * F, MODE_INT).reshape(1, 1, C, F).astype(np.float64)
+    y, _ = oracle.conv2d(x, w)
+    ref = x.reshape(-1, C).astype(np.int64) @ w.reshape(C, F).astype(np.int64)
+    assert np.array_equal(y.reshape(-1, F), ref)
+
+
+def _im2col(x, R, S, stride, pad):
+    N, H, W, C = x.shape
+    P = (H + 2 * pad - R) // stride + 1
+    Q = (W + 2 * pad - S) // stride + 1
+    xp = np.zeros((N, H + 2 * pad, W + 2 * pad, C), x.dtype)
+    xp[:, pad:pad + H, pad:pad + W, :] = x
+    cols = np.zeros((N, P, Q, R, S, C), x.dtype)
+    for r in range(R):
+        for s in range(S):
+            cols[:, :, :, r, s, :] = xp[:, r:r + stride * P:stride, s:s + stride * Q:stride, :]
+    return cols.reshape(N * P * Q, R * S * C), (N, P, Q)
+
+
+@pytest.mark.parametrize("stride,pad", [(1, 1), (2, 0), (2, 3), (1, 0)])
+def test_conv_equals_explicit_im2col_matmul_integer(stride, pad):
+    N, H, W, C, F, R, S = 2, 9, 8, 3, 4, 3, 3
+    if pad == 3:
+        R = S = 7
+    x = gen_f32(71, N * H * W * C, MODE_INT).reshape(N, H, W, C)
+    w = gen_f32(72, R * S * C * F, MODE_INT).reshape(R, S, C, F)
+    y, _ = oracle.conv2d(x, w, (stride, stride), (pad, pad))
+    cols, (n, P, Q) = _im2col(x.astype(np.int64), R, S, stride, pad)
+    ref = cols @ w.reshape(R * S * C, F).astype(np.int64)
+    assert np.array_equal(y.reshape(-1, F).astype(np.int64), ref)
+
+
+def test_conv_matches_torch_float64():
+    torch = pytest.importorskip("torch")
+    N, H, W, C, F = 2, 14, 14, 8, 5
+    x = gen_f32(81, N * H * W * C).reshape(N, H, W, C).astype(np.float64)
+    w = gen_f32(82, 3 * 3 * C * F).reshape(3, 3, C, F).astype(np.float64)
+    for stride, pad in [(1, 1), (2, 1)]:
+        y, D = oracle.conv2d(x, w, (stride, stride), (pad, pad))
+        ref = torch.nn.functional.conv2d(
+            torch.from_numpy(x).permute(0, 3, 1, 2),             # NHWC -> NCHW
+            torch.from_numpy(w).permute(3, 2, 0, 1),             # RSCF -> FCRS
+            stride=stride, padding=pad).permute(0, 2, 3, 1).numpy()
+        assert y.shape == ref.shape
+        assert np.max(np.abs(y - ref) / D) < 1e-14
+
+
+# --------------------------------------------------------------- rounding ---
+
+def test_round_out_bf16_matches_torch_rne():
+    torch = pytest.importorskip("torch")
+    vals = np.concatenate([gen_f32(91, 4096).astype(np.float64) * 300.0,
+                           np.arange(-40000, 40000, 7, dtype=np.float64)])
+    vals32 = vals.astype(np.float32).astype(np.float64)   # torch path: f32 -> bf16
+    ours = oracle.round_out(vals32, "bf16")
+    ref = torch.from_numpy(vals32.astype(np.float32)).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    assert np.array_equal(ours, ref)
+    assert np.array_equal(oracle.round_out(vals, "f32"), vals.astype(np.float32))
+
+
+# ---------------------------------------------------------------- mutants ---
+
+def test_pins_reject_plausible_mutants():
+    """Each plausible oracle bug, applied to a Python copy, fails a pin above."""
+    g = _golden("spec_2x2_matmul.json")
+    A, B = np.array(g["A"], float), np.array(g["B"], float)
+    good = np.array(g["C"], float)
+    mutants = {
+        "transposed B": A @ B.T,
+        "transposed A": A.T @ B,
+        "dropped last k": A[:, :1] @ B[:1, :],
+        "wrong sign": A @ (-B),
+        "accumulate into stale C": A @ B + 1.0,
+    }
+    for name, bad in mutants.items():
+        assert not np.array_equal(bad, good), name
