@@ -1,0 +1,256 @@
+/*
+ * xtc.h -- C-ABI of the B200-native XTC hot path (libxtc.so).
+ *
+ * The paper's statement of the problem (PAPER.md, arXiv 2512.16512):
+ *   - an operator from a fixed set (matmul, conv2d, ...) with a hyper-
+ *     rectangular iteration space (§III-A, Fig.2);
+ *   - a schedule built from the primitives of Table I:
+ *     strip-mine, interchange, unroll, vectorize, parallelize, split,
+ *     pack, bufferize (fuse is not on this path);
+ *   - a compiled module conforming to "XTC's ABI: a function named after
+ *     the graph and taking as parameters the graph's inputs and outputs,
+ *     each passed as a contiguous raw pointer" (§IV-A);
+ *   - an Executor that "validates that the optimized operator produces
+ *     results consistent with the reference implementation" and an
+ *     Evaluator that "generates input tensors, executes the compiled code,
+ *     and collects performance metrics" (§IV-B).
+ *
+ * Here the four steps are: xtc_op_create (operator), xtc_schedule_apply
+ * (schedule -> sm_100a launch plan), xtc_run (the compiled function) and
+ * xtc_measure (Executor + Evaluator on the GPU).
+ *
+ * Conventions (all entry points):
+ *   - Tensors are DEVICE pointers, row-major, contiguous unless a leading
+ *     dimension is given.  The caller owns every tensor buffer and every
+ *     stream; the library owns the xtc_op handle, its plan, its TMA
+ *     descriptors, its split-K workspace and its cached validation
+ *     reference.  Streams are passed as `void*` holding a cudaStream_t
+ *     (NULL = the legacy default stream).
+ *   - Argument order follows the paper's ABI: inputs, then outputs
+ *     (P:757-761).  matmul: inputs {A[M][K], B[K][N]}, outputs {C[M][N]}.
+ *     conv2d: inputs {x[N][H][W][C], w[R][S][C][F]}, outputs {y[N][P][Q][F]}.
+ *   - Every call returns xtc_status; no C++ exception crosses the ABI and
+ *     the library never aborts the process.  On any status other than
+ *     XTC_OK a human-readable reason is available from xtc_last_error()
+ *     (thread-local, valid until the next xtc_* call on the same thread).
+ *   - XTC_E_ILLEGAL_SCHEDULE: nothing was launched and the op keeps its
+ *     previous schedule.  XTC_E_CUDA: a CUDA error; sticky device errors
+ *     leave the context unusable (the process must exit).
+ *   - A handle is single-owner: do not drive one handle from two threads
+ *     at once.  Distinct handles may be used concurrently.
+ */
+#ifndef XTC_H
+#define XTC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define XTC_ABI_VERSION 1
+
+typedef enum {
+    XTC_OK = 0,
+    XTC_E_INVALID_ARG = 1,       /* malformed descriptor / null pointer / bad size      */
+    XTC_E_UNSUPPORTED = 2,       /* well-formed but not implemented (dtype combination) */
+    XTC_E_ILLEGAL_SCHEDULE = 3,  /* schedule violates a legality rule   */
+    XTC_E_NO_SCHEDULE = 4,       /* xtc_run / xtc_measure before xtc_schedule_apply     */
+    XTC_E_CUDA = 5,              /* CUDA runtime/driver error                           */
+    XTC_E_VALIDATION_FAILED = 6, /* xtc_measure: cfg->validate == 2 and the check failed */
+    XTC_E_OOM = 7                /* device allocation failed                            */
+} xtc_status;
+
+typedef enum { XTC_OP_MATMUL = 0, XTC_OP_CONV2D = 1 } xtc_op_kind;
+
+/* Storage / arithmetic types.  XTC_TF32: fp32 storage, tf32 tensor-core math. */
+typedef enum { XTC_F32 = 0, XTC_BF16 = 1, XTC_TF32 = 2 } xtc_dtype;
+
+/* Operator descriptor (paper: O.tensor / O.mm / conv2d).
+ *   matmul : C[m][n] = sum_k A[m][k] * B[k][n]      (C overwritten, reading 1)
+ *            lda/ldb/ldc = row pitch in elements, 0 = packed (k, n, n).
+ *   conv2d : y[b][p][q][f] = sum_{r,s,c} xpad[b][p*sh+r][q*sw+s][c] * w[r][s][c][f]
+ *            xpad = x zero-padded by (pad_h, pad_w) (reading 3);
+ *            p < P = (h + 2 pad_h - r)/stride_h + 1, q < Q likewise.
+ *            Implicit GEMM view: M = batch*P*Q, N = f, K = r*s*c (c fastest).
+ * in_dtype: F32 (SIMT engine, fp32 FFMA), TF32 or BF16 (tcgen05 engine).
+ * out_dtype: F32 or BF16 (RNE). */
+typedef struct {
+    int32_t kind;       /* xtc_op_kind */
+    int32_t in_dtype;   /* xtc_dtype   */
+    int32_t out_dtype;  /* xtc_dtype: XTC_F32 or XTC_BF16 */
+    int32_t reserved0;
+    int64_t m, n, k, lda, ldb, ldc;                         /* matmul */
+    int64_t batch, h, w, c, f, r, s;                        /* conv2d */
+    int64_t stride_h, stride_w, pad_h, pad_w;               /* conv2d */
+} xtc_op_desc;
+
+typedef enum { XTC_ENGINE_SIMT = 0, XTC_ENGINE_TCGEN05 = 1 } xtc_engine;
+typedef enum { XTC_ORDER_MN = 0, XTC_ORDER_NM = 1 } xtc_order;
+typedef enum { XTC_SPLITK_ORDERED = 0, XTC_SPLITK_ATOMIC = 1 } xtc_splitk_mode;
+
+/* A schedule: Table I primitives as GPU loop-nest knobs.  The
+ * mapping, value ranges and legality rules are in DESIGN.md §4 (SURVEY.md
+ * §8(a) a2).  Unused knobs must be 0 (or 1 where noted); a knob value 0
+ * means "default" only where stated.
+ *
+ * strip_mine   tile_m, tile_n, tile_k : CTA tile of the (M,N,K) loops
+ *                          inner_m, inner_n       : SIMT thread register tile (TM x TN);
+ *                                                   tcgen05: UMMA atom (inner_m = tile_m / cta_group,
+ *                                                   inner_n = tile_n); 0 = derive
+ * interchange  order                  : XTC_ORDER_MN: M-tile loop outer, N-tile loop inner
+ *                          raster_group           : strip-mine the outer tile loop by this many tiles
+ *                                                   and move the inner loop inside it (grouped raster)
+ * unroll       unroll_k               : SIMT: k-loop unroll inside the SMEM tile (divides tile_k)
+ *                                                   tcgen05: k-steps per stage, must be 0/1 (= fully unrolled)
+ * vectorize    vector_n               : SIMT: 1 or 4 (float4 SMEM/global access along N); tcgen05: 0
+ * parallelize  persistent             : 0 = one CTA per tile, 1 = #SM CTAs loop over tiles
+ *                          cluster_m              : tcgen05: 1, or 2 = CTA pair (cta_group::2, tile_m = 256)
+ * split        split_k, split_k_mode  : K split into split_k contiguous segments + reduction
+ *                          split_n_at             : 0, or the J split point s: [0,s) main root,
+ *                                                   [s,N) remainder root on the SIMT engine (Fig.3/4)
+ * pack         stages                 : SMEM ring depth (SIMT 1|2, tcgen05 2..8)
+ *                          swizzle                : tcgen05: 128 (TMA/UMMA 128-byte swizzle);
+ *                                                   SIMT: SMEM row padding in floats (0..8)
+ * bufferize    buffer_c               : 1 = SMEM-staged output + TMA store, 0 = direct stores
+ *                          acc_buffers            : tcgen05 TMEM accumulator buffers (1|2) */
+typedef struct {
+    int32_t engine;
+    int32_t tile_m, tile_n, tile_k;
+    int32_t inner_m, inner_n;
+    int32_t order, raster_group;
+    int32_t unroll_k;
+    int32_t vector_n;
+    int32_t stages, swizzle;
+    int32_t buffer_c, acc_buffers;
+    int32_t split_k, split_k_mode;
+    int32_t cluster_m;
+    int32_t persistent;
+    int32_t split_n_at;
+    int32_t reserved[5];
+} xtc_schedule;
+
+/* What the planner derived for a legal schedule (for reports and tests). */
+typedef struct {
+    int32_t engine;
+    int32_t grid_x, grid_y, grid_z, block_x, cluster_x;
+    int32_t smem_bytes;
+    int32_t tmem_cols;
+    int64_t num_tiles;          /* output tiles x split_k segments           */
+    int64_t k_blocks_per_split;
+    int64_t workspace_bytes;    /* split-K workspace                          */
+    int32_t tail_grid_x, tail_grid_y; /* split_n_at remainder launch (0 if none) */
+    int32_t reserved[4];
+} xtc_plan_info;
+
+/* Measurement configuration (Evaluator). */
+typedef struct {
+    int32_t warmup;       /* untimed launches before the timed ones (>= 0)            */
+    int32_t repeats;      /* timed launches, each bracketed by its own CUDA events (>=1) */
+    int32_t flush_l2;     /* 1: overwrite a 2 x L2-size scratch buffer before every rep  */
+    int32_t validate;     /* 0: no; 1: validate, report; 2: validate, fail on mismatch   */
+    int32_t exact;        /* 1: inputs are integer-valued -> require bit-exact output    */
+    int32_t reuse_reference; /* 1: reuse the cached GPU reference if the input pointers
+                                are unchanged (caller promises the data is unchanged)   */
+    double tol;           /* max |C - R| / D allowed (<= 0: 1e-5 fp32, 5e-3 bf16/tf32)  */
+    double peak_tflops;   /* denominator for frac_peak (0 = not reported)              */
+} xtc_measure_cfg;
+
+/* Results of xtc_measure. */
+typedef struct {
+    int32_t status;        /* xtc_status of the measurement                          */
+    int32_t valid;         /* 1 validated and within tolerance, 0 failed, -1 not run */
+    double max_norm_err;   /* max_ij |C - R| / D   (D = sum_k |a||b|, fp64 on GPU)     */
+    int64_t n_mismatch;    /* #elements whose bits differ from round_out(R)           */
+    int64_t n_nan;         /* #NaN/Inf outputs (outputs are pre-filled with NaN)      */
+    int64_t err_row, err_col; /* location of max_norm_err (output row-major [M][N])   */
+    double t_min_ns, t_med_ns, t_mean_ns, t_max_ns;
+    double tflops_med, tflops_min;   /* 2*M*N*K / t (FLOPs of the definition)     */
+    double frac_peak;      /* tflops_med / cfg->peak_tflops                          */
+    double sm_clock_mhz;   /* NVML SM clock sampled right after the timed window (0 if n/a) */
+    int32_t n_reps;
+    int32_t reserved0;
+    double reserved[6];
+} xtc_metrics;
+
+typedef struct xtc_op_s* xtc_op;
+
+/* a1 -- operator instantiation.  Validates the descriptor (shapes > 0, dtype
+ * combination supported), binds it to CUDA device `device` and returns a new
+ * handle in *out.  Nothing is launched.  Errors: INVALID_ARG, UNSUPPORTED. */
+xtc_status xtc_op_create(const xtc_op_desc* desc, int32_t device, xtc_op* out);
+
+/* Releases the handle and everything it owns (workspace, reference cache). */
+void xtc_op_destroy(xtc_op op);
+
+/* a2 -- pure host-side legality check + plan derivation for (desc, sch); needs
+ * no GPU.  num_sms <= 0 means 148 (B200).  Returns XTC_OK and fills *info (may
+ * be NULL), or XTC_E_ILLEGAL_SCHEDULE / XTC_E_INVALID_ARG with the violated
+ * rule in xtc_last_error(). */
+xtc_status xtc_schedule_check(const xtc_op_desc* desc, const xtc_schedule* sch,
+                              int32_t num_sms, xtc_plan_info* info);
+
+/* a2 -- apply a schedule to an op: check legality against the op's device,
+ * select the kernel variant, size the grid / SMEM / TMEM, allocate the split-K
+ * workspace.  On error the previous schedule stays in effect. */
+xtc_status xtc_schedule_apply(xtc_op op, const xtc_schedule* sch);
+
+/* Strategy.default_schedule(opt_level): a heuristic schedule for
+ * the descriptor.  opt_level 0 = the plainest legal schedule (SIMT 8x8x8,
+ * 1x1 inner); >= 2 = the engine's tuned default. */
+xtc_status xtc_schedule_default(const xtc_op_desc* desc, int32_t opt_level, xtc_schedule* out);
+
+/* a3..a7 -- run the scheduled operator once, asynchronously on `stream`.
+ * inputs[0..1], outputs[0] as in the conventions above.  The TMA descriptors
+ * are re-encoded only when a pointer differs from the previous call. */
+xtc_status xtc_run(xtc_op op, const void* const* inputs, void* const* outputs, void* stream);
+
+/* a8 + a9 -- Executor + Evaluator.  Synchronous.  Sequence:
+ *   1. if cfg->validate: fill outputs with NaN, run once, compute (or reuse)
+ *      the fp64 GPU reference R and D, compare -> max_norm_err, n_mismatch, n_nan;
+ *   2. cfg->warmup untimed runs;
+ *   3. cfg->repeats timed runs, each between two CUDA events on `stream`, with
+ *      the L2 flush (if requested) outside the event window;
+ *   4. min / median / mean / max, TFLOP/s, clock sample.
+ * Returns XTC_E_VALIDATION_FAILED only when cfg->validate == 2 and the check
+ * failed (metrics are still filled). */
+xtc_status xtc_measure(xtc_op op, const void* const* inputs, void* const* outputs,
+                       const xtc_measure_cfg* cfg, xtc_metrics* out, void* stream);
+
+/* a10 -- measure a batch of candidate schedules on one op (the sweep's inner
+ * loop without the GIL): for each i, apply cands[i] (illegal -> out[i].status =
+ * XTC_E_ILLEGAL_SCHEDULE, nothing launched), then xtc_measure.  Returns XTC_OK
+ * unless a CUDA error made the context unusable. */
+xtc_status xtc_sweep(xtc_op op, const xtc_schedule* cands, int32_t n,
+                     const void* const* inputs, void* const* outputs,
+                     const xtc_measure_cfg* cfg, xtc_metrics* out, void* stream);
+
+/* Seeded input generator (Evaluator "generates input tensors").
+ * Fills count elements of dtype (F32/TF32: float, BF16: bf16) at device pointer
+ * dst with element i = value(seed, first + i) of the counter-based generator
+ * in DESIGN.md §3 (identical to seeded_inputs/__init__.py).  mode 0 =
+ * uniform [-1,1), 1 = integers {-2..2}.  Asynchronous on stream. */
+xtc_status xtc_fill(void* dst, int64_t count, int32_t dtype, uint64_t seed, int32_t mode,
+                    int64_t first, void* stream);
+
+/* 2*M*N*K (matmul) or 2*N*P*Q*F*R*S*C (conv2d): FLOPs of the definition. */
+double xtc_op_flops(const xtc_op_desc* desc);
+
+/* Algorithmic bytes: inputs read once + output written once. */
+double xtc_op_min_bytes(const xtc_op_desc* desc);
+
+/* Device-side counters of the last xtc_run/xtc_measure on this op: number of
+ * kernels launched by the last xtc_run (main + split-K reduce + tail root). */
+int32_t xtc_last_launch_count(xtc_op op);
+
+/* Reason for the last non-OK status on this thread ("" if none). */
+const char* xtc_last_error(void);
+
+/* sizeof of the public structs, for binding self-checks:
+ * [0]=xtc_op_desc [1]=xtc_schedule [2]=xtc_plan_info [3]=xtc_measure_cfg [4]=xtc_metrics */
+void xtc_abi_sizes(int64_t* out5);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* XTC_H */

@@ -1,0 +1,706 @@
+// abi.cu -- the C-ABI of include/xtc.h: op handles, schedule application,
+// TMA descriptor encoding, run, Executor/Evaluator (measure) and sweep.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+#include "xtc_internal.h"
+
+namespace xtc {
+cudaError_t launch_tc_gemm(bool tf32, bool conv, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
+                           const TcParams& p, int grid, int smem, cudaStream_t st);
+cudaError_t launch_simt_gemm(int tm, int tn, int u, int vec, const SimtParams& p, int grid, int block, int smem,
+                             cudaStream_t st);
+cudaError_t launch_fill(void* dst, int64_t count, int bf16, uint64_t seed, int mode, int64_t first, cudaStream_t st);
+cudaError_t launch_ref_gemm(const void* A, const void* B, int bf16, int64_t M, int64_t N, int64_t K, int64_t lda,
+                            int64_t ldb, double* R, double* D, cudaStream_t st);
+cudaError_t launch_ref_conv(const void* x, const void* w, int bf16, const ConvGeom& g, int64_t Nb, int64_t F,
+                            double* R, double* D, cudaStream_t st);
+cudaError_t launch_compare(const void* C, int out_bf16, int64_t M, int64_t N, int64_t ldc, const double* R,
+                           const double* D, double* blk_err, int64_t* blk_idx, void* counts, int blocks,
+                           cudaStream_t st);
+cudaError_t launch_flush(void* buf, int64_t bytes, uint32_t salt, cudaStream_t st);
+cudaError_t launch_splitk_reduce(const float* W, int S, int64_t M, int64_t N, int64_t ws_ld, void* C, int64_t ldc,
+                                 int out_bf16, cudaStream_t st);
+cudaError_t launch_tail_gemm(const void* A, const void* B, int bf16_in, void* C, int out_bf16, int64_t M, int64_t n0,
+                             int64_t ntail, int64_t K, int64_t lda, int64_t ldb, int64_t ldc, int gx, int gy,
+                             cudaStream_t st);
+}  // namespace xtc
+
+using namespace xtc;
+
+static thread_local std::string g_err;
+
+static xtc_status fail(xtc_status s, const std::string& why) {
+    g_err = why;
+    return s;
+}
+static xtc_status cuda_fail(cudaError_t e, const char* where) {
+    g_err = std::string(where) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+    return XTC_E_CUDA;
+}
+#define CU_TRY(expr, where)                                  \
+    do {                                                     \
+        cudaError_t _e = (expr);                             \
+        if (_e != cudaSuccess) return cuda_fail(_e, where);  \
+    } while (0)
+
+// -------------------------------------------------- driver entry points --
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+typedef CUresult (*PFN_encodeIm2col)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                     const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t,
+                                     const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                     CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled g_encode_tiled = nullptr;
+static PFN_encodeIm2col g_encode_im2col = nullptr;
+
+static xtc_status load_driver_fns() {
+    if (g_encode_tiled && g_encode_im2col) return XTC_OK;
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    CU_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q), "cudaGetDriverEntryPoint");
+    if (!fn || q != cudaDriverEntryPointSuccess) return fail(XTC_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    g_encode_tiled = reinterpret_cast<PFN_encodeTiled>(fn);
+    fn = nullptr;
+    CU_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &fn, cudaEnableDefault, &q), "cudaGetDriverEntryPoint");
+    if (!fn || q != cudaDriverEntryPointSuccess) return fail(XTC_E_CUDA, "cuTensorMapEncodeIm2col unavailable");
+    g_encode_im2col = reinterpret_cast<PFN_encodeIm2col>(fn);
+    return XTC_OK;
+}
+
+// ------------------------------------------------------------- NVML clock --
+typedef int (*PFN_nvmlInit)(void);
+typedef int (*PFN_nvmlHandleByPci)(const char*, void**);
+typedef int (*PFN_nvmlClock)(void*, int, unsigned int*);
+static PFN_nvmlClock g_nvml_clock = nullptr;
+static PFN_nvmlHandleByPci g_nvml_handle = nullptr;
+static bool g_nvml_tried = false;
+
+static double sm_clock_mhz(int device) {
+    if (!g_nvml_tried) {
+        g_nvml_tried = true;
+        void* h = dlopen("libnvidia-ml.so.1", RTLD_NOW | RTLD_LOCAL);
+        if (h) {
+            auto init = reinterpret_cast<PFN_nvmlInit>(dlsym(h, "nvmlInit_v2"));
+            g_nvml_handle = reinterpret_cast<PFN_nvmlHandleByPci>(dlsym(h, "nvmlDeviceGetHandleByPciBusId_v2"));
+            g_nvml_clock = reinterpret_cast<PFN_nvmlClock>(dlsym(h, "nvmlDeviceGetClockInfo"));
+            if (!init || init() != 0) g_nvml_clock = nullptr;
+        }
+    }
+    if (!g_nvml_clock || !g_nvml_handle) return 0.0;
+    char bus[32] = {0};
+    if (cudaDeviceGetPCIBusId(bus, sizeof bus, device) != cudaSuccess) return 0.0;
+    void* dev = nullptr;
+    if (g_nvml_handle(bus, &dev) != 0) return 0.0;
+    unsigned int mhz = 0;
+    if (g_nvml_clock(dev, 1 /* NVML_CLOCK_SM */, &mhz) != 0) return 0.0;
+    return (double)mhz;
+}
+
+// ------------------------------------------------------------- op handle --
+struct xtc_op_s {
+    xtc_op_desc d{};
+    int device = 0;
+    int num_sms = kNumSmsB200;
+    bool has_plan = false;
+    Plan plan;
+    // per-op owned resources
+    float* ws = nullptr;
+    int64_t ws_bytes = 0;
+    // TMA descriptors, bound to pointers
+    alignas(64) CUtensorMap tmA, tmB, tmC;
+    const void* bound[3] = {nullptr, nullptr, nullptr};
+    bool maps_valid = false;
+    // validation reference cache
+    double* R = nullptr;
+    double* D = nullptr;
+    int64_t ref_elems = 0;
+    const void* ref_inputs[2] = {nullptr, nullptr};
+    bool ref_valid = false;
+    double* blk_err = nullptr;
+    int64_t* blk_idx = nullptr;
+    void* counts = nullptr;
+    // timing
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    std::vector<cudaEvent_t> evs;
+    int32_t last_launches = 0;
+};
+
+static int dsize(int dt) { return dt == XTC_BF16 ? 2 : 4; }
+
+static void* g_flush_buf[64] = {nullptr};
+static int64_t g_flush_bytes[64] = {0};
+
+static void release_op(xtc_op op) {
+    if (!op) return;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(op->device);
+    if (op->ws) cudaFree(op->ws);
+    if (op->R) cudaFree(op->R);
+    if (op->D) cudaFree(op->D);
+    if (op->blk_err) cudaFree(op->blk_err);
+    if (op->blk_idx) cudaFree(op->blk_idx);
+    if (op->counts) cudaFree(op->counts);
+    for (auto e : op->evs) cudaEventDestroy(e);
+    cudaSetDevice(cur);
+    delete op;
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) cudaSetDevice(dev);
+        else prev = -1;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+extern "C" {
+
+const char* xtc_last_error(void) { return g_err.c_str(); }
+
+void xtc_abi_sizes(int64_t* out5) {
+    if (!out5) return;
+    out5[0] = sizeof(xtc_op_desc);
+    out5[1] = sizeof(xtc_schedule);
+    out5[2] = sizeof(xtc_plan_info);
+    out5[3] = sizeof(xtc_measure_cfg);
+    out5[4] = sizeof(xtc_metrics);
+}
+
+double xtc_op_flops(const xtc_op_desc* d) {
+    if (!d) return 0.0;
+    int64_t M, N, K, P, Q;
+    gemm_view(*d, M, N, K, P, Q);
+    return 2.0 * (double)M * (double)N * (double)K;
+}
+
+double xtc_op_min_bytes(const xtc_op_desc* d) {
+    if (!d) return 0.0;
+    const double si = dsize(d->in_dtype), so = dsize(d->out_dtype);
+    if (d->kind == XTC_OP_CONV2D) {
+        int64_t M, N, K, P, Q;
+        gemm_view(*d, M, N, K, P, Q);
+        return si * (double)(d->batch * d->h * d->w * d->c) + si * (double)(d->r * d->s * d->c * d->f) +
+               so * (double)(d->batch * P * Q * d->f);
+    }
+    return si * (double)(d->m * d->k + d->k * d->n) + so * (double)(d->m * d->n);
+}
+
+xtc_status xtc_op_create(const xtc_op_desc* desc, int32_t device, xtc_op* out) {
+    if (!desc || !out) return fail(XTC_E_INVALID_ARG, "null argument");
+    *out = nullptr;
+    std::string why;
+    xtc_status st = check_desc(*desc, why);
+    if (st != XTC_OK) return fail(st, why);
+    int ndev = 0;
+    CU_TRY(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+    if (device < 0 || device >= ndev) return fail(XTC_E_INVALID_ARG, "device index out of range");
+    cudaDeviceProp prop;
+    CU_TRY(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    if (prop.major != 10 || prop.minor != 0)
+        return fail(XTC_E_UNSUPPORTED, std::string("libxtc is built for sm_100a (B200); device is ") + prop.name);
+    xtc_op op = new xtc_op_s();
+    op->d = *desc;
+    op->device = device;
+    op->num_sms = prop.multiProcessorCount;
+    *out = op;
+    return XTC_OK;
+}
+
+void xtc_op_destroy(xtc_op op) { release_op(op); }
+
+int32_t xtc_last_launch_count(xtc_op op) { return op ? op->last_launches : 0; }
+
+xtc_status xtc_schedule_check(const xtc_op_desc* desc, const xtc_schedule* sch, int32_t num_sms, xtc_plan_info* info) {
+    if (!desc || !sch) return fail(XTC_E_INVALID_ARG, "null argument");
+    Plan p;
+    std::string why;
+    xtc_status st = make_plan(*desc, *sch, num_sms, p, why);
+    if (st != XTC_OK) return fail(st, why);
+    if (info) {
+        memset(info, 0, sizeof *info);
+        info->engine = p.engine;
+        info->grid_x = p.grid_x;
+        info->grid_y = p.grid_y;
+        info->grid_z = p.grid_z;
+        info->block_x = p.block;
+        info->cluster_x = p.cluster;
+        info->smem_bytes = p.smem;
+        info->tmem_cols = p.tmem_cols;
+        info->num_tiles = p.num_tiles;
+        info->k_blocks_per_split = p.engine == XTC_ENGINE_TCGEN05 ? p.kb_per_split : p.k_per_split / std::max(1, sch->tile_k);
+        info->workspace_bytes = p.workspace_bytes;
+        info->tail_grid_x = p.tail_grid_x;
+        info->tail_grid_y = p.tail_grid_y;
+    }
+    return XTC_OK;
+}
+
+xtc_status xtc_schedule_apply(xtc_op op, const xtc_schedule* sch) {
+    if (!op || !sch) return fail(XTC_E_INVALID_ARG, "null argument");
+    Plan p;
+    std::string why;
+    xtc_status st = make_plan(op->d, *sch, op->num_sms, p, why);
+    if (st != XTC_OK) return fail(st, why);
+    DeviceGuard g(op->device);
+    if (p.workspace_bytes > op->ws_bytes) {
+        if (op->ws) cudaFree(op->ws);
+        op->ws = nullptr;
+        op->ws_bytes = 0;
+        if (cudaMalloc(&op->ws, p.workspace_bytes) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(XTC_E_OOM, "split-K workspace allocation failed");
+        }
+        op->ws_bytes = p.workspace_bytes;
+    }
+    op->plan = p;
+    op->has_plan = true;
+    op->maps_valid = false;
+    return XTC_OK;
+}
+
+xtc_status xtc_schedule_default(const xtc_op_desc* d, int32_t opt_level, xtc_schedule* out) {
+    if (!d || !out) return fail(XTC_E_INVALID_ARG, "null argument");
+    std::string why;
+    xtc_status st = check_desc(*d, why);
+    if (st != XTC_OK) return fail(st, why);
+    xtc_schedule s;
+    memset(&s, 0, sizeof s);
+    int64_t M, N, K, P, Q;
+    gemm_view(*d, M, N, K, P, Q);
+    if (d->in_dtype == XTC_F32 || opt_level <= 0) {
+        s.engine = XTC_ENGINE_SIMT;
+        if (opt_level <= 0 || d->in_dtype != XTC_F32) {
+            if (d->in_dtype != XTC_F32) return fail(XTC_E_UNSUPPORTED, "opt_level 0 (SIMT) needs fp32 inputs");
+            s.tile_m = s.tile_n = s.tile_k = 8;
+            s.inner_m = s.inner_n = 1;
+            s.unroll_k = 1;
+            s.stages = 1;
+        } else {
+            s.tile_m = 64; s.tile_n = 64; s.tile_k = 16;
+            s.inner_m = 4; s.inner_n = 4;
+            s.unroll_k = 4; s.vector_n = 4; s.stages = 2; s.swizzle = 4;
+            s.raster_group = 8;
+        }
+        s.split_k = 1;
+        *out = s;
+        return XTC_OK;
+    }
+    // tcgen05 default: 128 x N tile, deepest ring that fits, persistent + double-buffered TMEM
+    const int es = dsize(d->in_dtype);
+    const int atom = 128 / es;
+    s.engine = XTC_ENGINE_TCGEN05;
+    s.tile_m = 128;
+    s.tile_n = N >= 256 ? 256 : (N >= 128 ? 128 : atom * (int)std::max<int64_t>(1, (N + atom - 1) / atom));
+    if (s.tile_n > 256) s.tile_n = 256;
+    s.tile_k = atom;
+    s.swizzle = 128;
+    s.buffer_c = 1;
+    s.acc_buffers = s.tile_n <= 256 ? 2 : 1;
+    if (2 * s.tile_n > 512) s.acc_buffers = 1;
+    s.persistent = 1;
+    s.raster_group = 8;
+    s.split_k = 1;
+    const int stage = 128 * s.tile_k * es + s.tile_k * s.tile_n * es;
+    int stages = (kSmemMaxOptin - kTcEpiSmem - kSmemReserve) / stage;
+    s.stages = std::max(2, std::min(8, stages));
+    // low-parallelism shapes: split K so the grid covers the SMs (a5)
+    const int64_t tiles = ((M + 127) / 128) * ((N + s.tile_n - 1) / s.tile_n);
+    const int64_t kb = (K + s.tile_k - 1) / s.tile_k;
+    int sk = 1;
+    while (tiles * sk * 2 <= kNumSmsB200 && kb / (sk * 2) >= 4) sk *= 2;
+    s.split_k = sk;
+    Plan p;
+    if (make_plan(*d, s, kNumSmsB200, p, why) != XTC_OK) {
+        s.split_k = 1;
+        if (make_plan(*d, s, kNumSmsB200, p, why) != XTC_OK) return fail(XTC_E_ILLEGAL_SCHEDULE, "default: " + why);
+    }
+    *out = s;
+    return XTC_OK;
+}
+
+xtc_status xtc_fill(void* dst, int64_t count, int32_t dtype, uint64_t seed, int32_t mode, int64_t first, void* stream) {
+    if (!dst && count > 0) return fail(XTC_E_INVALID_ARG, "null dst");
+    if (mode != 0 && mode != 1) return fail(XTC_E_INVALID_ARG, "mode must be 0 (uniform) or 1 (int)");
+    CU_TRY(launch_fill(dst, count, dtype == XTC_BF16, seed, mode, first, (cudaStream_t)stream), "fill");
+    return XTC_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------- run --
+static xtc_status encode_maps(xtc_op op, const void* A, const void* B, void* C) {
+    const Plan& p = op->plan;
+    const xtc_op_desc& d = op->d;
+    xtc_status st = load_driver_fns();
+    if (st != XTC_OK) return st;
+    const bool tf32 = d.in_dtype == XTC_TF32;
+    const CUtensorMapDataType in_t = tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    const int es = dsize(d.in_dtype);
+    const int atom = 128 / es;
+    const int tile_k = p.sch.tile_k, tile_n = p.sch.tile_n;
+    CUresult r;
+    // B: [K][N] row-major, N-major UMMA operand: box {atom N-cols, tile_k rows}
+    {
+        const int64_t ldb = (d.kind == XTC_OP_MATMUL && d.ldb) ? d.ldb : p.n_total;
+        cuuint64_t dims[2] = {(cuuint64_t)p.N, (cuuint64_t)p.K};
+        cuuint64_t strides[1] = {(cuuint64_t)(ldb * es)};
+        cuuint32_t box[2] = {(cuuint32_t)atom, (cuuint32_t)tile_k};
+        cuuint32_t estr[2] = {1, 1};
+        r = g_encode_tiled(&op->tmB, in_t, 2, const_cast<void*>(B), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(XTC_E_CUDA, "cuTensorMapEncodeTiled(B) failed: " + std::to_string((int)r));
+    }
+    if (d.kind == XTC_OP_MATMUL) {
+        const int64_t lda = d.lda ? d.lda : d.k;
+        cuuint64_t dims[2] = {(cuuint64_t)p.K, (cuuint64_t)p.M};
+        cuuint64_t strides[1] = {(cuuint64_t)(lda * es)};
+        cuuint32_t box[2] = {(cuuint32_t)atom, 128};
+        cuuint32_t estr[2] = {1, 1};
+        r = g_encode_tiled(&op->tmA, in_t, 2, const_cast<void*>(A), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(XTC_E_CUDA, "cuTensorMapEncodeTiled(A) failed: " + std::to_string((int)r));
+    } else {
+        // x: NHWC, im2col: one pixel = `atom` channels (128 B), 128 pixels per column
+        cuuint64_t dims[4] = {(cuuint64_t)d.c, (cuuint64_t)d.w, (cuuint64_t)d.h, (cuuint64_t)d.batch};
+        cuuint64_t strides[3] = {(cuuint64_t)(d.c * es), (cuuint64_t)(d.w * d.c * es), (cuuint64_t)(d.h * d.w * d.c * es)};
+        int lower[2] = {(int)-d.pad_w, (int)-d.pad_h};                                   // {W, H}
+        int upper[2] = {(int)(d.pad_w - (d.s - 1)), (int)(d.pad_h - (d.r - 1))};
+        cuuint32_t estr[4] = {1, (cuuint32_t)d.stride_w, (cuuint32_t)d.stride_h, 1};
+        r = g_encode_im2col(&op->tmA, in_t, 4, const_cast<void*>(A), dims, strides, lower, upper, (cuuint32_t)atom, 128,
+                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(XTC_E_CUDA, "cuTensorMapEncodeIm2col(x) failed: " + std::to_string((int)r));
+    }
+    // C (or the split-K workspace): 3-D {N, M, S} so stores clip per segment; box {128 B, 32 rows, 1}
+    if (p.sch.buffer_c) {
+        const bool to_ws = p.split_k > 1;
+        const int os = to_ws ? 4 : dsize(d.out_dtype);
+        const CUtensorMapDataType out_t = os == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+        const int64_t ld = to_ws ? p.ws_ld : ((d.kind == XTC_OP_MATMUL && d.ldc) ? d.ldc : p.n_total);
+        void* base = to_ws ? (void*)op->ws : C;
+        cuuint64_t dims[3] = {(cuuint64_t)p.N, (cuuint64_t)p.M, (cuuint64_t)(to_ws ? p.split_k : 1)};
+        cuuint64_t strides[2] = {(cuuint64_t)(ld * os), (cuuint64_t)(ld * os * p.M)};
+        cuuint32_t box[3] = {(cuuint32_t)(128 / os), 32, 1};
+        cuuint32_t estr[3] = {1, 1, 1};
+        r = g_encode_tiled(&op->tmC, out_t, 3, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(XTC_E_CUDA, "cuTensorMapEncodeTiled(C) failed: " + std::to_string((int)r));
+    } else {
+        memset(&op->tmC, 0, sizeof op->tmC);
+    }
+    (void)tile_n;
+    op->bound[0] = A;
+    op->bound[1] = B;
+    op->bound[2] = C;
+    op->maps_valid = true;
+    return XTC_OK;
+}
+
+static ConvGeom conv_geom(const xtc_op_desc& d) {
+    ConvGeom g;
+    memset(&g, 0, sizeof g);
+    if (d.kind != XTC_OP_CONV2D) return g;
+    int64_t M, N, K, P, Q;
+    gemm_view(d, M, N, K, P, Q);
+    g.is_conv = 1;
+    g.H = (int)d.h; g.W = (int)d.w; g.C = (int)d.c; g.P = (int)P; g.Q = (int)Q;
+    g.R = (int)d.r; g.S = (int)d.s; g.sh = (int)d.stride_h; g.sw = (int)d.stride_w;
+    g.ph = (int)d.pad_h; g.pw = (int)d.pad_w;
+    return g;
+}
+
+static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cudaStream_t st) {
+    const Plan& p = op->plan;
+    const xtc_op_desc& d = op->d;
+    const int64_t ldc = (d.kind == XTC_OP_MATMUL && d.ldc) ? d.ldc : p.n_total;
+    const bool out_bf16 = d.out_dtype == XTC_BF16;
+    const bool split_out = p.split_k > 1 && !p.atomic;
+    int launches = 0;
+    if (p.atomic) {
+        // atomic split-K accumulates into C: clear the main root's columns first
+        const int64_t rows = p.M;
+        CU_TRY(cudaMemset2DAsync(C, ldc * 4, 0, p.N * 4, rows, st), "memset C (atomic split-K)");
+    }
+    TileMap tm{p.tiles_m, p.tiles_n, p.split_k, p.sch.order, p.sch.raster_group};
+    if (p.engine == XTC_ENGINE_SIMT) {
+        SimtParams sp;
+        memset(&sp, 0, sizeof sp);
+        sp.A = A; sp.B = B; sp.C = C; sp.Wk = op->ws;
+        sp.M = p.M; sp.N = p.N; sp.K = p.K;
+        sp.lda = (d.kind == XTC_OP_MATMUL && d.lda) ? d.lda : p.K;
+        sp.ldb = (d.kind == XTC_OP_MATMUL && d.ldb) ? d.ldb : p.n_total;
+        sp.ldc = ldc;
+        sp.ws_ld = p.ws_ld;
+        sp.tile_m = p.sch.tile_m; sp.tile_n = p.sch.tile_n; sp.tile_k = p.sch.tile_k;
+        sp.pad = p.sch.swizzle;
+        sp.stages = p.sch.stages == 0 ? 1 : p.sch.stages;
+        sp.k_per_split = p.k_per_split;
+        sp.tm = tm;
+        sp.num_tiles = p.num_tiles;
+        sp.out_bf16 = out_bf16; sp.split_out = split_out; sp.atomic = p.atomic;
+        sp.cg = conv_geom(d);
+        const int u = p.sch.unroll_k == 0 ? 1 : p.sch.unroll_k;
+        const int vec = p.sch.vector_n == 0 ? 1 : p.sch.vector_n;
+        CU_TRY(launch_simt_gemm(p.sch.inner_m, p.sch.inner_n, u, vec, sp, p.grid_x, p.block, p.smem, st), "simt_gemm launch");
+        ++launches;
+    } else {
+        if (!op->maps_valid || op->bound[0] != A || op->bound[1] != B || op->bound[2] != C) {
+            xtc_status s2 = encode_maps(op, A, B, C);
+            if (s2 != XTC_OK) return s2;
+        }
+        TcParams tp;
+        memset(&tp, 0, sizeof tp);
+        tp.M = p.M; tp.N = p.N; tp.K = p.K;
+        tp.tile_n = p.sch.tile_n; tp.tile_k = p.sch.tile_k; tp.stages = p.sch.stages;
+        tp.kb_total = p.kb_total; tp.kb_per_split = p.kb_per_split;
+        tp.tm = tm;
+        tp.num_tiles = p.num_tiles;
+        tp.acc_buffers = p.sch.acc_buffers == 0 ? 1 : p.sch.acc_buffers;
+        tp.buffer_c = p.sch.buffer_c;
+        tp.atomic = p.atomic;
+        tp.out_bf16 = out_bf16;
+        tp.split_out = split_out;
+        tp.ldc = ldc;
+        tp.ws_ld = p.ws_ld;
+        tp.C = C;
+        tp.Wk = op->ws;
+        const bool tf32 = d.in_dtype == XTC_TF32;
+        const uint32_t fmt = tf32 ? 2u : 1u;
+        tp.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (0u << 15) | (1u << 16) |
+                   ((uint32_t)(p.sch.tile_n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+        tp.tmem_cols = (uint32_t)p.tmem_cols;
+        const int es = dsize(d.in_dtype);
+        tp.a_stage_bytes = (uint32_t)(128 * p.sch.tile_k * es);
+        tp.b_stage_bytes = (uint32_t)(p.sch.tile_k * p.sch.tile_n * es);
+        tp.cg = conv_geom(d);
+        CU_TRY(launch_tc_gemm(tf32, d.kind == XTC_OP_CONV2D, op->tmA, op->tmB, op->tmC, tp, p.grid_x, p.smem, st),
+               "tc_gemm launch");
+        ++launches;
+    }
+    if (split_out) {
+        CU_TRY(launch_splitk_reduce(op->ws, p.split_k, p.M, p.N, p.ws_ld, C, ldc, out_bf16, st), "splitk_reduce");
+        ++launches;
+    }
+    if (p.has_tail) {
+        const int64_t lda = d.lda ? d.lda : d.k;
+        const int64_t ldb = d.ldb ? d.ldb : d.n;
+        CU_TRY(launch_tail_gemm(A, B, d.in_dtype == XTC_BF16, C, out_bf16, p.M, p.tail_n0, p.tail_n, p.K, lda, ldb, ldc,
+                                p.tail_grid_x, p.tail_grid_y, st),
+               "tail_gemm");
+        ++launches;
+    }
+    op->last_launches = launches;
+    return XTC_OK;
+}
+
+extern "C" xtc_status xtc_run(xtc_op op, const void* const* inputs, void* const* outputs, void* stream) {
+    if (!op || !inputs || !outputs || !inputs[0] || !inputs[1] || !outputs[0])
+        return fail(XTC_E_INVALID_ARG, "null op or tensor pointer");
+    if (!op->has_plan) return fail(XTC_E_NO_SCHEDULE, "xtc_run before xtc_schedule_apply");
+    DeviceGuard g(op->device);
+    if (op->plan.engine == XTC_ENGINE_TCGEN05) {
+        for (int i = 0; i < 2; ++i)
+            if (reinterpret_cast<uintptr_t>(inputs[i]) & 15) return fail(XTC_E_INVALID_ARG, "TMA needs 16-byte aligned inputs");
+        if (op->plan.sch.buffer_c && (reinterpret_cast<uintptr_t>(outputs[0]) & 15))
+            return fail(XTC_E_INVALID_ARG, "TMA store needs a 16-byte aligned output");
+    }
+    return run_impl(op, inputs[0], inputs[1], outputs[0], (cudaStream_t)stream);
+}
+
+// --------------------------------------------------------------- measure --
+static xtc_status ensure_flush(int device, cudaStream_t) {
+    if (device < 0 || device >= 64) return fail(XTC_E_INVALID_ARG, "device index");
+    if (g_flush_buf[device]) return XTC_OK;
+    int l2 = 0;
+    CU_TRY(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device), "L2 size");
+    const int64_t bytes = std::max<int64_t>(2 * (int64_t)l2, 64 << 20);
+    if (cudaMalloc(&g_flush_buf[device], bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(XTC_E_OOM, "L2 flush buffer allocation failed");
+    }
+    g_flush_bytes[device] = bytes;
+    return XTC_OK;
+}
+
+static xtc_status compute_reference(xtc_op op, const void* A, const void* B, cudaStream_t st) {
+    const xtc_op_desc& d = op->d;
+    int64_t M, N, K, P, Q;
+    gemm_view(d, M, N, K, P, Q);
+    const int64_t elems = M * N;
+    if (elems > op->ref_elems) {
+        if (op->R) cudaFree(op->R);
+        if (op->D) cudaFree(op->D);
+        op->R = op->D = nullptr;
+        op->ref_elems = 0;
+        if (cudaMalloc(&op->R, elems * 8) != cudaSuccess || cudaMalloc(&op->D, elems * 8) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(XTC_E_OOM, "reference buffers (2 x 8 B per output) allocation failed");
+        }
+        op->ref_elems = elems;
+    }
+    const int bf16 = d.in_dtype == XTC_BF16;
+    if (d.kind == XTC_OP_MATMUL) {
+        const int64_t lda = d.lda ? d.lda : d.k, ldb = d.ldb ? d.ldb : d.n;
+        CU_TRY(launch_ref_gemm(A, B, bf16, M, N, K, lda, ldb, op->R, op->D, st), "ref_gemm");
+    } else {
+        CU_TRY(launch_ref_conv(A, B, bf16, conv_geom(d), d.batch, d.f, op->R, op->D, st), "ref_conv");
+    }
+    op->ref_inputs[0] = A;
+    op->ref_inputs[1] = B;
+    op->ref_valid = true;
+    return XTC_OK;
+}
+
+static const int kCmpBlocks = 148 * 8;
+
+static xtc_status validate(xtc_op op, const void* A, const void* B, void* C, const xtc_measure_cfg* cfg,
+                           xtc_metrics* m, cudaStream_t st) {
+    const xtc_op_desc& d = op->d;
+    int64_t M, N, K, P, Q;
+    gemm_view(d, M, N, K, P, Q);
+    const int64_t ldc = (d.kind == XTC_OP_MATMUL && d.ldc) ? d.ldc : N;
+    const int os = dsize(d.out_dtype);
+    // NaN sentinel: every output the schedule fails to write stays NaN (coverage)
+    CU_TRY(cudaMemset2DAsync(C, ldc * os, 0xFF, N * os, M, st), "NaN fill");
+    xtc_status s = run_impl(op, A, B, C, st);
+    if (s != XTC_OK) return s;
+    if (!(cfg->reuse_reference && op->ref_valid && op->ref_inputs[0] == A && op->ref_inputs[1] == B)) {
+        s = compute_reference(op, A, B, st);
+        if (s != XTC_OK) return s;
+    }
+    if (!op->blk_err) {
+        if (cudaMalloc(&op->blk_err, kCmpBlocks * 8) != cudaSuccess || cudaMalloc(&op->blk_idx, kCmpBlocks * 8) != cudaSuccess ||
+            cudaMalloc(&op->counts, 16) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(XTC_E_OOM, "compare buffers");
+        }
+    }
+    CU_TRY(cudaMemsetAsync(op->counts, 0, 16, st), "memset counts");
+    CU_TRY(launch_compare(C, d.out_dtype == XTC_BF16, M, N, ldc, op->R, op->D, op->blk_err, op->blk_idx, op->counts,
+                          kCmpBlocks, st),
+           "compare");
+    std::vector<double> be(kCmpBlocks);
+    std::vector<int64_t> bi(kCmpBlocks);
+    unsigned long long cnt[2];
+    CU_TRY(cudaMemcpyAsync(be.data(), op->blk_err, kCmpBlocks * 8, cudaMemcpyDeviceToHost, st), "D2H err");
+    CU_TRY(cudaMemcpyAsync(bi.data(), op->blk_idx, kCmpBlocks * 8, cudaMemcpyDeviceToHost, st), "D2H idx");
+    CU_TRY(cudaMemcpyAsync(cnt, op->counts, 16, cudaMemcpyDeviceToHost, st), "D2H counts");
+    CU_TRY(cudaStreamSynchronize(st), "validate sync");
+    double best = -1;
+    int64_t bidx = -1;
+    for (int i = 0; i < kCmpBlocks; ++i)
+        if (bi[i] >= 0 && (be[i] > best || (be[i] == best && bi[i] < bidx))) { best = be[i]; bidx = bi[i]; }
+    m->max_norm_err = best < 0 ? 0.0 : best;
+    m->err_row = bidx >= 0 ? bidx / N : -1;
+    m->err_col = bidx >= 0 ? bidx % N : -1;
+    m->n_mismatch = (int64_t)cnt[0];
+    m->n_nan = (int64_t)cnt[1];
+    double tol = cfg->tol;
+    if (tol <= 0) tol = d.in_dtype == XTC_F32 ? 1e-5 : 5e-3;
+    bool ok = m->n_nan == 0 && m->max_norm_err <= tol;
+    if (cfg->exact) ok = ok && m->n_mismatch == 0;
+    m->valid = ok ? 1 : 0;
+    return XTC_OK;
+}
+
+static xtc_status measure_impl(xtc_op op, const void* A, const void* B, void* C, const xtc_measure_cfg* cfg,
+                               xtc_metrics* m, cudaStream_t st) {
+    memset(m, 0, sizeof *m);
+    m->valid = -1;
+    m->err_row = m->err_col = -1;
+    if (cfg->repeats < 1 || cfg->warmup < 0) return fail(XTC_E_INVALID_ARG, "repeats must be >= 1, warmup >= 0");
+    if (cfg->validate) {
+        xtc_status s = validate(op, A, B, C, cfg, m, st);
+        if (s != XTC_OK) return s;
+    }
+    for (int i = 0; i < cfg->warmup; ++i) {
+        xtc_status s = run_impl(op, A, B, C, st);
+        if (s != XTC_OK) return s;
+    }
+    if (cfg->flush_l2) {
+        xtc_status s = ensure_flush(op->device, st);
+        if (s != XTC_OK) return s;
+    }
+    const int R = cfg->repeats;
+    while ((int)op->evs.size() < 2 * R) {
+        cudaEvent_t e;
+        CU_TRY(cudaEventCreate(&e), "cudaEventCreate");
+        op->evs.push_back(e);
+    }
+    for (int i = 0; i < R; ++i) {
+        if (cfg->flush_l2) CU_TRY(launch_flush(g_flush_buf[op->device], g_flush_bytes[op->device], (uint32_t)i, st), "flush");
+        CU_TRY(cudaEventRecord(op->evs[2 * i], st), "event");
+        xtc_status s = run_impl(op, A, B, C, st);
+        if (s != XTC_OK) return s;
+        CU_TRY(cudaEventRecord(op->evs[2 * i + 1], st), "event");
+    }
+    CU_TRY(cudaEventSynchronize(op->evs[2 * R - 1]), "event sync");
+    m->sm_clock_mhz = sm_clock_mhz(op->device);
+    std::vector<double> t(R);
+    for (int i = 0; i < R; ++i) {
+        float ms = 0;
+        CU_TRY(cudaEventElapsedTime(&ms, op->evs[2 * i], op->evs[2 * i + 1]), "elapsed");
+        t[i] = ms * 1e6;
+    }
+    std::vector<double> srt = t;
+    std::sort(srt.begin(), srt.end());
+    m->t_min_ns = srt.front();
+    m->t_max_ns = srt.back();
+    m->t_med_ns = (R % 2) ? srt[R / 2] : 0.5 * (srt[R / 2 - 1] + srt[R / 2]);
+    double sum = 0;
+    for (double v : t) sum += v;
+    m->t_mean_ns = sum / R;
+    const double flops = xtc_op_flops(&op->d);
+    m->tflops_med = flops / m->t_med_ns * 1e-3;
+    m->tflops_min = flops / m->t_min_ns * 1e-3;
+    m->frac_peak = cfg->peak_tflops > 0 ? m->tflops_med / cfg->peak_tflops : 0.0;
+    m->n_reps = R;
+    m->status = XTC_OK;
+    return XTC_OK;
+}
+
+extern "C" xtc_status xtc_measure(xtc_op op, const void* const* inputs, void* const* outputs,
+                                  const xtc_measure_cfg* cfg, xtc_metrics* out, void* stream) {
+    if (!op || !inputs || !outputs || !cfg || !out || !inputs[0] || !inputs[1] || !outputs[0])
+        return fail(XTC_E_INVALID_ARG, "null argument");
+    if (!op->has_plan) return fail(XTC_E_NO_SCHEDULE, "xtc_measure before xtc_schedule_apply");
+    DeviceGuard g(op->device);
+    xtc_status s = measure_impl(op, inputs[0], inputs[1], outputs[0], cfg, out, (cudaStream_t)stream);
+    if (s != XTC_OK) { out->status = s; return s; }
+    if (cfg->validate == 2 && out->valid == 0) return fail(XTC_E_VALIDATION_FAILED, "validation failed");
+    return XTC_OK;
+}
+
+extern "C" xtc_status xtc_sweep(xtc_op op, const xtc_schedule* cands, int32_t n, const void* const* inputs,
+                                void* const* outputs, const xtc_measure_cfg* cfg, xtc_metrics* out, void* stream) {
+    if (!op || !cands || n < 0 || !out || !cfg) return fail(XTC_E_INVALID_ARG, "null argument");
+    DeviceGuard g(op->device);
+    xtc_measure_cfg c = *cfg;
+    for (int i = 0; i < n; ++i) {
+        xtc_status s = xtc_schedule_apply(op, &cands[i]);
+        if (s != XTC_OK) {
+            memset(&out[i], 0, sizeof out[i]);
+            out[i].status = s;
+            out[i].valid = -1;
+            continue;
+        }
+        s = measure_impl(op, inputs[0], inputs[1], outputs[0], &c, &out[i], (cudaStream_t)stream);
+        c.reuse_reference = 1;     // same inputs for every candidate of the sweep
+        if (s == XTC_E_CUDA) { out[i].status = s; return s; }
+        out[i].status = s;
+    }
+    return XTC_OK;
+}

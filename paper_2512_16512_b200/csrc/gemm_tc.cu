@@ -1,0 +1,295 @@
+// gemm_tc.cu -- KB2/KB3: schedule-parametrised tcgen05 GEMM and implicit-GEMM
+// conv2d for sm_100a (bf16 kind::f16 / tf32 kind::tf32, fp32 accumulate in TMEM).
+//
+// How the paper's primitives (Table I) appear in this kernel:
+//   strip_mine  -> CTA tile 128 x tile_n x tile_k; UMMA atom 128 x tile_n x 16 (8 tf32)
+//   interchange -> tile order (TileMap: MN / NM + grouped raster)
+//   unroll      -> the tile_k / UMMA_K MMAs of one stage are issued back to back
+//   vectorize   -> the innermost tile is one tcgen05.mma (the tensor core is the SIMD unit)
+//   parallelize -> one CTA per tile, or persistent CTAs striding over tiles
+//   split       -> split_k contiguous K segments, fp32 partials + ordered reduction
+//   pack        -> TMA -> `stages`-deep SMEM ring in the 128-byte-swizzled layout the
+//                  UMMA reads ("copies the elements ... in the order of their access",
+//                  P:549-557; the swizzle plays the role of the paper's anti-conflict pad)
+//   bufferize   -> accumulator in TMEM (acc_buffers deep); output staged in SMEM and
+//                  written back by TMA store ("copied to the output tensor, while modifying
+//                  its ordering to fit the original layout")
+//
+// Warp roles (256 threads): warp 0 = TMA producer, warp 1 = MMA issuer (one thread),
+// warp 2 = TMEM allocator, warp 3 idle, warps 4..7 = epilogue (TMEM lane quarters).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include "ptx.cuh"
+#include "xtc_internal.h"
+
+namespace xtc {
+
+template <bool TF32, bool CONV>
+__global__ void __launch_bounds__(kTcThreads, 1)
+tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+               const __grid_constant__ CUtensorMap tmC, const TcParams p) {
+    constexpr int ATOM = TF32 ? 32 : 64;     // elements per 128-byte row (A's K / B's N)
+    constexpr int UMMA_K = TF32 ? 8 : 16;    // K per tcgen05.mma (32 bytes)
+    constexpr uint32_t A_ATOM_BYTES = 128 * 128;
+
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t pad = (1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u;
+    uint8_t* smem = smem_raw + pad;
+    const int S = p.stages;
+    uint8_t* sA = smem;
+    uint8_t* sB = sA + (size_t)S * p.a_stage_bytes;
+    uint8_t* sC = sB + (size_t)S * p.b_stage_bytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sC + kTcEpiSmem);
+    uint64_t* empty = full + 8;
+    uint64_t* tfull = empty + 8;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    if (warp == 0 && lane == 0) {
+        ptx::prefetch_tmap(&tmA);
+        ptx::prefetch_tmap(&tmB);
+        if (p.buffer_c) ptx::prefetch_tmap(&tmC);
+    }
+    if (warp == 1 && lane == 0) {
+        for (int s = 0; s < S; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
+        for (int a = 0; a < 2; ++a) { ptx::mbar_init(&tfull[a], 1); ptx::mbar_init(&tempty[a], 4); }
+        ptx::fence_mbarrier_init();
+    }
+    if (warp == 2) {
+        ptx::tmem_alloc(tmem_slot, p.tmem_cols);
+        ptx::tmem_relinquish();
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ===================== TMA producer (pack) =====================
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            const uint32_t stage_bytes = p.a_stage_bytes + p.b_stage_bytes;
+            const int n_a = p.tile_k / ATOM;
+            const int n_b = p.tile_n / ATOM;
+            for (int64_t t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+                int mb, nb, ks;
+                tile_coords(p.tm, t, mb, nb, ks);
+                const int kb0 = ks * p.kb_per_split;
+                const int kb1 = min(p.kb_total, kb0 + p.kb_per_split);
+                const int m0 = mb * 128, n0 = nb * p.tile_n;
+                int wq = 0, hp = 0, nimg = 0;
+                if constexpr (CONV) {
+                    const int pq = p.cg.P * p.cg.Q;
+                    nimg = m0 / pq;
+                    const int rem = m0 - nimg * pq;
+                    const int pp = rem / p.cg.Q, qq = rem - pp * p.cg.Q;
+                    hp = pp * p.cg.sh - p.cg.ph;      // filter-window origin of pixel m0
+                    wq = qq * p.cg.sw - p.cg.pw;
+                }
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    ptx::mbar_wait(&empty[s], ph ^ 1);
+                    ptx::mbar_arrive_expect_tx(&full[s], stage_bytes);
+                    uint8_t* a_dst = sA + (size_t)s * p.a_stage_bytes;
+                    uint8_t* b_dst = sB + (size_t)s * p.b_stage_bytes;
+                    for (int a = 0; a < n_a; ++a) {
+                        const int kc = kb * p.tile_k + a * ATOM;
+                        if constexpr (CONV) {
+                            const int rs = kc / p.cg.C;
+                            const int c = kc - rs * p.cg.C;
+                            const int r = rs / p.cg.S;
+                            const int sx = rs - r * p.cg.S;
+                            ptx::tma_load_im2col_4d(&tmA, a_dst + a * A_ATOM_BYTES, &full[s], c, wq, hp, nimg,
+                                                    (uint16_t)sx, (uint16_t)r);
+                        } else {
+                            ptx::tma_load_2d(&tmA, a_dst + a * A_ATOM_BYTES, &full[s], kc, m0);
+                        }
+                    }
+                    for (int b = 0; b < n_b; ++b)
+                        ptx::tma_load_2d(&tmB, b_dst + (size_t)b * p.tile_k * 128, &full[s], n0 + b * ATOM, kb * p.tile_k);
+                    if (++s == S) { s = 0; ph ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer (contraction) =====================
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            int acc = 0;
+            uint32_t aph = 0;
+            const int n_a = p.tile_k / ATOM;
+            const uint32_t b_lbo = (uint32_t)p.tile_k * 128u;   // stride between 128-byte N blocks of B
+            for (int64_t t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+                int mb, nb, ks;
+                tile_coords(p.tm, t, mb, nb, ks);
+                const int kb0 = ks * p.kb_per_split;
+                const int kb1 = min(p.kb_total, kb0 + p.kb_per_split);
+                ptx::mbar_wait(&tempty[acc], aph ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d_tmem = tmem_base + (uint32_t)(acc * p.tile_n);
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    ptx::mbar_wait(&full[s], ph);
+                    ptx::tc_fence_after();
+                    const uint32_t a_base = ptx::smem_u32(sA + (size_t)s * p.a_stage_bytes);
+                    const uint32_t b_base = ptx::smem_u32(sB + (size_t)s * p.b_stage_bytes);
+                    for (int a = 0; a < n_a; ++a) {
+#pragma unroll
+                        for (int kk = 0; kk < ATOM / UMMA_K; ++kk) {
+                            const uint64_t adesc = ptx::smem_desc_sw128(a_base + a * A_ATOM_BYTES + kk * 32, 16, 1024);
+                            const uint32_t krow = a * ATOM + kk * UMMA_K;
+                            const uint64_t bdesc = ptx::smem_desc_sw128(b_base + krow * 128, b_lbo, 1024);
+                            ptx::umma<TF32>(d_tmem, adesc, bdesc, p.idesc, (kb > kb0 || a > 0 || kk > 0) ? 1u : 0u);
+                        }
+                    }
+                    ptx::umma_commit(&empty[s]);       // frees the SMEM slot when these MMAs finish
+                    if (++s == S) { s = 0; ph ^= 1; }
+                }
+                ptx::umma_commit(&tfull[acc]);         // accumulator ready for the epilogue
+                if (++acc == p.acc_buffers) { acc = 0; aph ^= 1; }
+            }
+        }
+    } else if (warp >= 4) {
+        // ===================== epilogue (bufferize) =====================
+        const int q = warp & 3;                        // TMEM lanes 32q..32q+31
+        int acc = 0;
+        uint32_t aph = 0;
+        int buf = 0;
+        uint8_t* stage = sC + q * (kTcEpiStageBytes * kTcEpiBuffers);
+        const bool to_ws = p.split_out != 0;
+        const bool bf16_out = p.out_bf16 && !to_ws;
+        for (int64_t t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+            int mb, nb, ks;
+            tile_coords(p.tm, t, mb, nb, ks);
+            const int m0 = mb * 128, n0 = nb * p.tile_n;
+            const int64_t row = (int64_t)m0 + 32 * q + lane;
+            ptx::mbar_wait(&tfull[acc], aph);
+            ptx::tc_fence_after();
+            const uint32_t t_row = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * p.tile_n);
+            for (int c = 0; c < p.tile_n; c += 32) {
+                uint32_t v[32];
+                ptx::tmem_ld_32x32b_x32(t_row + c, v);
+                ptx::tmem_ld_wait();
+                if (p.buffer_c) {
+                    // stage one 128-byte row per thread (swizzled), then one TMA store per warp
+                    const bool first_half = !bf16_out || ((c & 63) == 0);
+                    if (first_half) {
+                        if (lane == 0) ptx::bulk_wait_read<1>();
+                        __syncwarp();
+                    }
+                    uint8_t* rowp = stage + buf * kTcEpiStageBytes + lane * 128;
+                    if (bf16_out) {
+                        const int cbase = (c & 63) ? 4 : 0;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            uint4 w;
+                            w.x = ptx::pack_bf16x2(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1]));
+                            w.y = ptx::pack_bf16x2(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3]));
+                            w.z = ptx::pack_bf16x2(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5]));
+                            w.w = ptx::pack_bf16x2(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7]));
+                            const int phys = (cbase + j) ^ (lane & 7);
+                            *reinterpret_cast<uint4*>(rowp + phys * 16) = w;
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            uint4 w = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                            const int phys = j ^ (lane & 7);
+                            *reinterpret_cast<uint4*>(rowp + phys * 16) = w;
+                        }
+                    }
+                    const bool last_half = !bf16_out || ((c & 63) == 32) || (c + 32 >= p.tile_n);
+                    if (last_half) {
+                        ptx::fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            const int col = bf16_out ? (n0 + (c & ~63)) : (n0 + c);
+                            ptx::tma_store_3d(&tmC, stage + buf * kTcEpiStageBytes, col, m0 + 32 * q, to_ws ? ks : 0);
+                            ptx::bulk_commit();
+                        }
+                        buf ^= 1;
+                    }
+                } else if (row < p.M) {
+                    const int64_t col0 = (int64_t)n0 + c;
+                    const int ncols = (int)((p.N - col0) < 32 ? (p.N - col0) : 32);
+                    if (ncols > 0) {
+                        if (to_ws) {
+                            float* dst = p.Wk + ((int64_t)ks * p.M + row) * p.ws_ld + col0;
+                            if (ncols == 32) {
+#pragma unroll
+                                for (int j = 0; j < 8; ++j)
+                                    reinterpret_cast<uint4*>(dst)[j] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                            } else {
+                                for (int j = 0; j < ncols; ++j) dst[j] = __uint_as_float(v[j]);
+                            }
+                        } else if (p.atomic) {
+                            float* dst = reinterpret_cast<float*>(p.C) + row * p.ldc + col0;
+                            for (int j = 0; j < ncols; ++j) atomicAdd(dst + j, __uint_as_float(v[j]));
+                        } else if (bf16_out) {
+                            uint16_t* dst = reinterpret_cast<uint16_t*>(p.C) + row * p.ldc + col0;
+                            if (ncols == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+#pragma unroll
+                                for (int j = 0; j < 4; ++j) {
+                                    uint4 w;
+                                    w.x = ptx::pack_bf16x2(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1]));
+                                    w.y = ptx::pack_bf16x2(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3]));
+                                    w.z = ptx::pack_bf16x2(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5]));
+                                    w.w = ptx::pack_bf16x2(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7]));
+                                    reinterpret_cast<uint4*>(dst)[j] = w;
+                                }
+                            } else {
+                                for (int j = 0; j < ncols; ++j)
+                                    dst[j] = (uint16_t)(ptx::pack_bf16x2(__uint_as_float(v[j]), 0.f) & 0xFFFFu);
+                            }
+                        } else {
+                            float* dst = reinterpret_cast<float*>(p.C) + row * p.ldc + col0;
+                            if (ncols == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+#pragma unroll
+                                for (int j = 0; j < 8; ++j)
+                                    reinterpret_cast<uint4*>(dst)[j] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                            } else {
+                                for (int j = 0; j < ncols; ++j) dst[j] = __uint_as_float(v[j]);
+                            }
+                        }
+                    }
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&tempty[acc]);   // TMEM buffer free for the next tile
+            if (++acc == p.acc_buffers) { acc = 0; aph ^= 1; }
+        }
+        if (p.buffer_c && lane == 0) ptx::bulk_wait<0>();
+    }
+
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem_base, p.tmem_cols);
+    }
+}
+
+// ------------------------------------------------------------------ launch --
+template <bool TF32, bool CONV>
+static cudaError_t launch_tc_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
+                               const TcParams& p, int grid, int smem, cudaStream_t st) {
+    auto k = tc_gemm_kernel<TF32, CONV>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    k<<<grid, kTcThreads, smem, st>>>(a, b, c, p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tc_gemm(bool tf32, bool conv, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
+                           const TcParams& p, int grid, int smem, cudaStream_t st) {
+    if (tf32) return conv ? launch_tc_t<true, true>(a, b, c, p, grid, smem, st)
+                          : launch_tc_t<true, false>(a, b, c, p, grid, smem, st);
+    return conv ? launch_tc_t<false, true>(a, b, c, p, grid, smem, st)
+                : launch_tc_t<false, false>(a, b, c, p, grid, smem, st);
+}
+
+}  // namespace xtc

@@ -1,0 +1,268 @@
+// harness.cu -- on-chip validation and measurement kernels (a8, a9), plus the
+// split-K reduction (a5), the split_n_at remainder root and the seeded filler.
+//
+//   KB5 splitk_reduce : C = sum_{s=0}^{S-1} W[s] in ascending s (deterministic)
+//   KB6 ref_gemm/conv : R and D = sum |a||b| in fp64, one output per thread
+//                       ("validates that the optimized operator produces results
+//                       consistent with the reference implementation")
+//   KB7 compare       : max |C-R|/D (+argmax), #bit mismatches vs round_out(R), #NaN/Inf
+//   KB8 l2_flush      : overwrite a scratch buffer >= 2 x L2 between timed reps
+//   KB9 fill          : counter-based generator, same definition as
+//                       seeded_inputs/__init__.py, implemented independently here
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include "xtc_internal.h"
+
+namespace xtc {
+
+// ------------------------------------------------------------------ fill --
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+    uint64_t z = x + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__global__ void fill_kernel(void* dst, int64_t count, int bf16, uint64_t seed, int mode, int64_t first) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t h = splitmix64(seed * 0xD1B54A32D192ED03ull + (uint64_t)(first + i));
+        float v;
+        if (mode == 1) v = (float)((int)((h >> 32) % 5ull) - 2);
+        else v = (float)((double)(h >> 40) * (1.0 / 8388608.0) - 1.0);
+        if (bf16) static_cast<__nv_bfloat16*>(dst)[i] = __float2bfloat16_rn(v);
+        else static_cast<float*>(dst)[i] = v;
+    }
+}
+
+cudaError_t launch_fill(void* dst, int64_t count, int bf16, uint64_t seed, int mode, int64_t first, cudaStream_t st) {
+    if (count <= 0) return cudaSuccess;
+    int64_t blocks = (count + 255) / 256;
+    if (blocks > 148 * 64) blocks = 148 * 64;
+    fill_kernel<<<(int)blocks, 256, 0, st>>>(dst, count, bf16, seed, mode, first);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------- input loads --
+__device__ __forceinline__ double ld_in(const void* p, int64_t i, int bf16) {
+    if (bf16) return (double)__bfloat162float(static_cast<const __nv_bfloat16*>(p)[i]);
+    return (double)static_cast<const float*>(p)[i];
+}
+
+// ------------------------------------------------------- fp64 reference --
+// 32x32 output tile per 256-thread block, 4 outputs per thread, k staged in SMEM.
+__global__ void __launch_bounds__(256) ref_gemm_f64_kernel(const void* A, const void* B, int bf16, int64_t M, int64_t N,
+                                                           int64_t K, int64_t lda, int64_t ldb, double* R, double* D) {
+    __shared__ double As[32][33];
+    __shared__ double Bs[32][33];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // ty 0..7
+    const int64_t m0 = (int64_t)blockIdx.y * 32, n0 = (int64_t)blockIdx.x * 32;
+    double s[4] = {0, 0, 0, 0}, d[4] = {0, 0, 0, 0};
+    for (int64_t k0 = 0; k0 < K; k0 += 32) {
+        for (int r = ty; r < 32; r += 8) {
+            const int64_t m = m0 + r, k = k0 + tx;
+            As[r][tx] = (m < M && k < K) ? ld_in(A, m * lda + k, bf16) : 0.0;
+            const int64_t kb = k0 + r, n = n0 + tx;
+            Bs[r][tx] = (kb < K && n < N) ? ld_in(B, kb * ldb + n, bf16) : 0.0;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int kk = 0; kk < 32; ++kk) {
+            const double b = Bs[kk][tx];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const double a = As[ty + 8 * i][kk];
+                s[i] = fma(a, b, s[i]);
+                d[i] = fma(fabs(a), fabs(b), d[i]);
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int64_t m = m0 + ty + 8 * i, n = n0 + tx;
+        if (m < M && n < N) { R[m * N + n] = s[i]; D[m * N + n] = d[i]; }
+    }
+}
+
+__global__ void ref_conv_f64_kernel(const void* x, const void* w, int bf16, ConvGeom g, int64_t Nb, int64_t F,
+                                    double* R, double* D) {
+    const int64_t total = Nb * g.P * g.Q * F;
+    for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total; o += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t f = o % F;
+        const int64_t pix = o / F;
+        const int q = (int)(pix % g.Q);
+        const int p = (int)((pix / g.Q) % g.P);
+        const int64_t n = pix / ((int64_t)g.P * g.Q);
+        double s = 0, d = 0;
+        for (int r = 0; r < g.R; ++r) {
+            const int h = p * g.sh + r - g.ph;
+            if (h < 0 || h >= g.H) continue;
+            for (int sx = 0; sx < g.S; ++sx) {
+                const int ww = q * g.sw + sx - g.pw;
+                if (ww < 0 || ww >= g.W) continue;
+                const int64_t xb = ((n * g.H + h) * g.W + ww) * g.C;
+                const int64_t wb = ((int64_t)(r * g.S + sx) * g.C) * F + f;
+                for (int c = 0; c < g.C; ++c) {
+                    const double a = ld_in(x, xb + c, bf16), b = ld_in(w, wb + (int64_t)c * F, bf16);
+                    s = fma(a, b, s);
+                    d = fma(fabs(a), fabs(b), d);
+                }
+            }
+        }
+        R[o] = s;
+        D[o] = d;
+    }
+}
+
+cudaError_t launch_ref_gemm(const void* A, const void* B, int bf16, int64_t M, int64_t N, int64_t K, int64_t lda,
+                            int64_t ldb, double* R, double* D, cudaStream_t st) {
+    dim3 grid((unsigned)((N + 31) / 32), (unsigned)((M + 31) / 32));
+    ref_gemm_f64_kernel<<<grid, 256, 0, st>>>(A, B, bf16, M, N, K, lda, ldb, R, D);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ref_conv(const void* x, const void* w, int bf16, const ConvGeom& g, int64_t Nb, int64_t F,
+                            double* R, double* D, cudaStream_t st) {
+    ref_conv_f64_kernel<<<148 * 16, 256, 0, st>>>(x, w, bf16, g, Nb, F, R, D);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- compare --
+struct CmpOut {
+    unsigned long long n_mismatch, n_nan;
+};
+
+__global__ void compare_kernel(const void* C, int out_bf16, int64_t M, int64_t N, int64_t ldc, const double* R,
+                               const double* D, double* blk_err, int64_t* blk_idx, CmpOut* out) {
+    double best = -1.0;
+    int64_t best_i = -1;
+    unsigned long long mism = 0, nan = 0;
+    const int64_t total = M * N;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t m = i / N, n = i - m * N;
+        const double r = R[i], d = D[i];
+        double c;
+        bool bits_ok;
+        if (out_bf16) {
+            const __nv_bfloat16 cv = static_cast<const __nv_bfloat16*>(C)[m * ldc + n];
+            c = (double)__bfloat162float(cv);
+            const __nv_bfloat16 rr = __float2bfloat16_rn(__double2float_rn(r));
+            bits_ok = __bfloat16_as_ushort(cv) == __bfloat16_as_ushort(rr);
+        } else {
+            const float cv = static_cast<const float*>(C)[m * ldc + n];
+            c = (double)cv;
+            bits_ok = __float_as_uint(cv) == __float_as_uint(__double2float_rn(r));
+        }
+        double e;
+        if (isnan(c) || isinf(c)) { ++nan; e = INFINITY; }
+        else e = (d > 0) ? fabs(c - r) / d : (c == r ? 0.0 : INFINITY);
+        if (!bits_ok) ++mism;
+        if (e > best) { best = e; best_i = i; }
+    }
+    // block reduce (max with index; counts by atomics)
+    __shared__ double se[256];
+    __shared__ int64_t si[256];
+    se[threadIdx.x] = best;
+    si[threadIdx.x] = best_i;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) {
+            const double o = se[threadIdx.x + w];
+            const int64_t oi = si[threadIdx.x + w];
+            if (o > se[threadIdx.x] || (o == se[threadIdx.x] && oi >= 0 && (si[threadIdx.x] < 0 || oi < si[threadIdx.x]))) {
+                se[threadIdx.x] = o;
+                si[threadIdx.x] = oi;
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) { blk_err[blockIdx.x] = se[0]; blk_idx[blockIdx.x] = si[0]; }
+    if (mism) atomicAdd(&out->n_mismatch, mism);
+    if (nan) atomicAdd(&out->n_nan, nan);
+}
+
+cudaError_t launch_compare(const void* C, int out_bf16, int64_t M, int64_t N, int64_t ldc, const double* R,
+                           const double* D, double* blk_err, int64_t* blk_idx, void* counts, int blocks,
+                           cudaStream_t st) {
+    compare_kernel<<<blocks, 256, 0, st>>>(C, out_bf16, M, N, ldc, R, D, blk_err, blk_idx, static_cast<CmpOut*>(counts));
+    return cudaGetLastError();
+}
+
+// --------------------------------------------------------------- L2 flush --
+__global__ void flush_kernel(uint4* buf, int64_t n16, uint32_t salt) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x)
+        buf[i] = make_uint4(salt, (uint32_t)i, salt ^ 0x5a5a5a5au, (uint32_t)(i >> 32));
+}
+
+cudaError_t launch_flush(void* buf, int64_t bytes, uint32_t salt, cudaStream_t st) {
+    flush_kernel<<<148 * 8, 512, 0, st>>>(static_cast<uint4*>(buf), bytes / 16, salt);
+    return cudaGetLastError();
+}
+
+// ----------------------------------------------------------- split-K reduce --
+__global__ void splitk_reduce_kernel(const float* __restrict__ W, int S, int64_t M, int64_t N, int64_t ws_ld,
+                                     void* C, int64_t ldc, int out_bf16) {
+    const int64_t groups_per_row = (N + 3) / 4;
+    const int64_t total = M * groups_per_row;
+    const int64_t plane = M * ws_ld;
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t m = g / groups_per_row;
+        const int64_t n = (g - m * groups_per_row) * 4;
+        const float4* src = reinterpret_cast<const float4*>(W + m * ws_ld + n);
+        float4 acc = src[0];
+        for (int s = 1; s < S; ++s) {                 // ascending s: deterministic order
+            const float4 v = *reinterpret_cast<const float4*>(W + s * plane + m * ws_ld + n);
+            acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+        const float a[4] = {acc.x, acc.y, acc.z, acc.w};
+        const int cnt = (int)((N - n) < 4 ? (N - n) : 4);
+        for (int j = 0; j < cnt; ++j) {
+            if (out_bf16) static_cast<__nv_bfloat16*>(C)[m * ldc + n + j] = __float2bfloat16_rn(a[j]);
+            else static_cast<float*>(C)[m * ldc + n + j] = a[j];
+        }
+    }
+}
+
+cudaError_t launch_splitk_reduce(const float* W, int S, int64_t M, int64_t N, int64_t ws_ld, void* C, int64_t ldc,
+                                 int out_bf16, cudaStream_t st) {
+    int64_t total = M * ((N + 3) / 4);
+    int64_t blocks = (total + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    splitk_reduce_kernel<<<(int)blocks, 256, 0, st>>>(W, S, M, N, ws_ld, C, ldc, out_bf16);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------- split_n_at remainder root --
+// The paper's scalar remainder loop (Fig.3 lines 33-35): one output
+// per thread, ascending k, fp32 FMA.
+__global__ void tail_gemm_kernel(const void* A, const void* B, int bf16_in, void* C, int out_bf16, int64_t M,
+                                 int64_t n0, int64_t ntail, int64_t K, int64_t lda, int64_t ldb, int64_t ldc) {
+    const int64_t j = (int64_t)blockIdx.x * 16 + (threadIdx.x & 15);
+    const int64_t i = (int64_t)blockIdx.y * 16 + (threadIdx.x >> 4);
+    if (i >= M || j >= ntail) return;
+    const int64_t col = n0 + j;
+    float s = 0.f;
+    for (int64_t k = 0; k < K; ++k) {
+        float a, b;
+        if (bf16_in) {
+            a = __bfloat162float(static_cast<const __nv_bfloat16*>(A)[i * lda + k]);
+            b = __bfloat162float(static_cast<const __nv_bfloat16*>(B)[k * ldb + col]);
+        } else {
+            a = static_cast<const float*>(A)[i * lda + k];
+            b = static_cast<const float*>(B)[k * ldb + col];
+        }
+        s = fmaf(a, b, s);
+    }
+    if (out_bf16) static_cast<__nv_bfloat16*>(C)[i * ldc + col] = __float2bfloat16_rn(s);
+    else static_cast<float*>(C)[i * ldc + col] = s;
+}
+
+cudaError_t launch_tail_gemm(const void* A, const void* B, int bf16_in, void* C, int out_bf16, int64_t M, int64_t n0,
+                             int64_t ntail, int64_t K, int64_t lda, int64_t ldb, int64_t ldc, int gx, int gy,
+                             cudaStream_t st) {
+    tail_gemm_kernel<<<dim3(gx, gy), 256, 0, st>>>(A, B, bf16_in, C, out_bf16, M, n0, ntail, K, lda, ldb, ldc);
+    return cudaGetLastError();
+}
+
+}  // namespace xtc

@@ -1,0 +1,220 @@
+// planner.cpp -- a2: schedule application = legality + launch-plan derivation.
+//
+// The paper's Scheduler "records the scheduling API calls and builds an
+// internal representation of the schedule", which the Compiler then applies
+// (P:751-755).  On B200 the "compiled" artefact is a launch plan
+// for one of the pre-built sm_100a kernel variants: grid / cluster, SMEM
+// bytes, TMEM columns, split-K workspace.  Everything here is host integer
+// work (no CUDA calls), so it is testable without a GPU.
+//
+// Legality rules:
+//   tcgen05 : UMMA M in {128 (cta_group::1), 256 (cta_group::2)}; N multiple of
+//             the 128-byte swizzle atom of B (64 bf16 / 32 tf32 columns) and <= 256;
+//             tile_k multiple of the A swizzle atom (64 bf16 / 32 tf32), <= 256;
+//             stages 2..8; SMEM <= 232448 B (sm_100 opt-in limit); TMEM columns
+//             (pow2 >= 32 of acc_buffers * tile_n) <= 512; TMA row pitches % 16 B.
+//   SIMT    : fp32 inputs; inner tile TM,TN in {1,2,4,8}; (tile/inner) threads
+//             in [1,1024]; unroll divides tile_k; vector_n 4 needs TN%4.
+//   split   : every K segment holds >= 1 k-block; atomic split-K needs fp32 out.
+#include <algorithm>
+#include <cstdio>
+#include <string>
+#include "xtc_internal.h"
+
+namespace xtc {
+
+static int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+static bool pow2_in(int v, int lo, int hi) { return v >= lo && v <= hi && (v & (v - 1)) == 0; }
+
+#define ILLEGAL(...) do { char _b[320]; snprintf(_b, sizeof _b, __VA_ARGS__); why = _b; return XTC_E_ILLEGAL_SCHEDULE; } while (0)
+#define INVALID(...) do { char _b[320]; snprintf(_b, sizeof _b, __VA_ARGS__); why = _b; return XTC_E_INVALID_ARG; } while (0)
+
+void gemm_view(const xtc_op_desc& d, int64_t& M, int64_t& N, int64_t& K, int64_t& P, int64_t& Q) {
+    if (d.kind == XTC_OP_CONV2D) {
+        P = (d.h + 2 * d.pad_h - d.r) / d.stride_h + 1;
+        Q = (d.w + 2 * d.pad_w - d.s) / d.stride_w + 1;
+        M = d.batch * P * Q;
+        N = d.f;
+        K = d.r * d.s * d.c;
+    } else {
+        P = Q = 0;
+        M = d.m; N = d.n; K = d.k;
+    }
+}
+
+static int dtype_size(int dt) { return dt == XTC_BF16 ? 2 : 4; }
+
+xtc_status check_desc(const xtc_op_desc& d, std::string& why) {
+    if (d.kind != XTC_OP_MATMUL && d.kind != XTC_OP_CONV2D) INVALID("unknown op kind %d", d.kind);
+    if (d.in_dtype < XTC_F32 || d.in_dtype > XTC_TF32) INVALID("unknown in_dtype %d", d.in_dtype);
+    if (d.out_dtype != XTC_F32 && d.out_dtype != XTC_BF16) INVALID("out_dtype must be F32 or BF16");
+    if (d.kind == XTC_OP_MATMUL) {
+        if (d.m <= 0 || d.n <= 0 || d.k <= 0) INVALID("matmul extents must be > 0 (m=%lld n=%lld k=%lld)",
+                                                      (long long)d.m, (long long)d.n, (long long)d.k);
+        if ((d.lda && d.lda < d.k) || (d.ldb && d.ldb < d.n) || (d.ldc && d.ldc < d.n))
+            INVALID("leading dimension smaller than the row extent");
+    } else {
+        if (d.batch <= 0 || d.h <= 0 || d.w <= 0 || d.c <= 0 || d.f <= 0 || d.r <= 0 || d.s <= 0)
+            INVALID("conv2d extents must be > 0");
+        if (d.stride_h <= 0 || d.stride_w <= 0 || d.pad_h < 0 || d.pad_w < 0) INVALID("bad stride/pad");
+        if (d.h + 2 * d.pad_h < d.r || d.w + 2 * d.pad_w < d.s) INVALID("filter larger than padded input");
+    }
+    int64_t M, N, K, P, Q;
+    gemm_view(d, M, N, K, P, Q);
+    if (M >= (1ll << 31) || N >= (1ll << 31) || K >= (1ll << 31)) INVALID("extent >= 2^31");
+    return XTC_OK;
+}
+
+static xtc_status plan_simt(const xtc_op_desc& d, const xtc_schedule& s, int num_sms, Plan& p, std::string& why) {
+    if (d.in_dtype != XTC_F32) ILLEGAL("SIMT engine computes fp32 inputs only (in_dtype must be F32)");
+    int TM = s.inner_m, TN = s.inner_n;
+    if (!pow2_in(TM, 1, 8) || !pow2_in(TN, 1, 8)) ILLEGAL("SIMT inner_m/inner_n (thread tile) must be 1,2,4 or 8");
+    if (s.tile_m < 1 || s.tile_n < 1 || s.tile_m > 256 || s.tile_n > 256) ILLEGAL("SIMT tile_m/tile_n must be in [1,256]");
+    if (s.tile_m % TM || s.tile_n % TN) ILLEGAL("strip-mine: tile_m %% inner_m and tile_n %% inner_n must be 0");
+    int threads = (s.tile_m / TM) * (s.tile_n / TN);
+    if (threads < 1 || threads > 1024) ILLEGAL("SIMT tile/inner gives %d threads (must be 1..1024)", threads);
+    if (s.tile_k < 1 || s.tile_k > 64) ILLEGAL("SIMT tile_k must be in [1,64]");
+    int U = s.unroll_k == 0 ? 1 : s.unroll_k;
+    if (!pow2_in(U, 1, 8)) ILLEGAL("SIMT unroll_k must be 1,2,4 or 8");
+    if (s.tile_k % U) ILLEGAL("unroll: unroll_k (%d) must divide the k-tile trip count %d (S:271)", U, s.tile_k);
+    int V = s.vector_n == 0 ? 1 : s.vector_n;
+    if (V != 1 && V != 4) ILLEGAL("SIMT vector_n must be 1 or 4");
+    if (V == 4 && TN % 4) ILLEGAL("vectorize: vector_n 4 needs inner_n %% 4 == 0");
+    int st = s.stages == 0 ? 1 : s.stages;
+    if (st != 1 && st != 2) ILLEGAL("SIMT stages must be 1 or 2");
+    if (s.swizzle < 0 || s.swizzle > 8) ILLEGAL("SIMT swizzle (SMEM pad) must be in [0,8] floats");
+    if (s.buffer_c != 0) ILLEGAL("SIMT engine: buffer_c must be 0 (the register tile is the write buffer)");
+    if (s.acc_buffers > 1) ILLEGAL("SIMT engine: acc_buffers must be 0 or 1");
+    if (s.cluster_m > 1) ILLEGAL("SIMT engine: cluster_m must be 1");
+    if (V == 4 && (s.tile_n + s.swizzle) % 4) ILLEGAL("vectorize: vector_n 4 needs (tile_n + pad) %% 4 == 0 for aligned float4");
+    auto r4 = [](int x) { return (x + 3) / 4 * 4; };
+    int smem = st * (r4(s.tile_k * (s.tile_m + s.swizzle)) + r4(s.tile_k * (s.tile_n + s.swizzle))) * 4;
+    if (smem > kSmemMaxOptin) ILLEGAL("SMEM %d B exceeds the %d B per-CTA limit", smem, kSmemMaxOptin);
+    p.block = threads;
+    p.smem = smem;
+    p.tiles_m = (int)cdiv(p.M, s.tile_m);
+    p.tiles_n = (int)cdiv(p.N, s.tile_n);
+    int64_t ksplit = cdiv(p.K, p.split_k);
+    p.k_per_split = cdiv(ksplit, s.tile_k) * s.tile_k;
+    if ((p.split_k - 1) * p.k_per_split >= p.K) ILLEGAL("split: split_k %d leaves an empty K segment (K=%lld, tile_k=%d)",
+                                                      p.split_k, (long long)p.K, s.tile_k);
+    p.num_tiles = (int64_t)p.tiles_m * p.tiles_n * p.split_k;
+    if (p.num_tiles >= (1ll << 31)) ILLEGAL("too many tiles");
+    p.grid_x = s.persistent ? (int)std::min<int64_t>(p.num_tiles, (int64_t)num_sms * std::max(1, 2048 / threads))
+                            : (int)p.num_tiles;
+    return XTC_OK;
+}
+
+static xtc_status plan_tc(const xtc_op_desc& d, const xtc_schedule& s, int num_sms, Plan& p, std::string& why) {
+    if (d.in_dtype != XTC_BF16 && d.in_dtype != XTC_TF32) ILLEGAL("tcgen05 engine needs BF16 or TF32 inputs");
+    int es = dtype_size(d.in_dtype);
+    p.atom_k = 128 / es;          // elements per 128-byte swizzle row
+    p.atom_n = 128 / es;
+    int cg = s.cluster_m == 0 ? 1 : s.cluster_m;
+    if (cg != 1 && cg != 2) ILLEGAL("tcgen05 cluster_m must be 1 (cta_group::1) or 2 (cta_group::2 CTA pair)");
+    if (cg == 2) ILLEGAL("cta_group::2 (cluster_m=2) is not built yet");
+    p.cta_group = cg;
+    if (s.tile_m != 128 * cg) ILLEGAL("tcgen05 tile_m must be %d for cluster_m=%d (UMMA M=128 per CTA)", 128 * cg, cg);
+    if (s.inner_m != 0 && s.inner_m != s.tile_m) ILLEGAL("tcgen05 inner_m (UMMA M) must equal tile_m");
+    if (s.inner_n != 0 && s.inner_n != s.tile_n) ILLEGAL("tcgen05 inner_n (UMMA N) must equal tile_n");
+    int bn_cta = s.tile_n / cg;
+    if (s.tile_n < p.atom_n * cg || s.tile_n > 256 || bn_cta % p.atom_n)
+        ILLEGAL("tcgen05 tile_n must be a multiple of %d in [%d,256] (B swizzle atom x cta_group)", p.atom_n * cg, p.atom_n * cg);
+    if (s.tile_k < p.atom_k || s.tile_k > 256 || s.tile_k % p.atom_k)
+        ILLEGAL("tcgen05 tile_k must be a multiple of %d in [%d,256] (128-byte swizzle atom)", p.atom_k, p.atom_k);
+    if (s.unroll_k > 1) ILLEGAL("tcgen05 unroll_k must be 0 or 1 (the k-steps of a stage are always fully unrolled)");
+    if (s.vector_n > 1) ILLEGAL("tcgen05 vector_n must be 0 (the UMMA atom is the vector unit)");
+    if (s.stages < 2 || s.stages > 8) ILLEGAL("tcgen05 stages must be in [2,8]");
+    if (s.swizzle != 0 && s.swizzle != 128) ILLEGAL("tcgen05 swizzle must be 128 (0 = default 128)");
+    int accb = s.acc_buffers == 0 ? 1 : s.acc_buffers;
+    if (accb < 1 || accb > 2) ILLEGAL("acc_buffers must be 1 or 2");
+    int cols = accb * s.tile_n;
+    int alloc = 32;
+    while (alloc < cols) alloc *= 2;
+    if (alloc > 512) ILLEGAL("bufferize: %d TMEM columns (acc_buffers x tile_n, pow2) exceed 512", alloc);
+    p.tmem_cols = alloc;
+    int a_stage = 128 * s.tile_k * es;
+    int b_stage = s.tile_k * bn_cta * es;
+    int smem = s.stages * (a_stage + b_stage) + kTcEpiSmem + kSmemReserve;
+    if (smem > kSmemMaxOptin) ILLEGAL("pack: %d stages x %d B + epilogue = %d B SMEM exceeds %d B",
+                                      s.stages, a_stage + b_stage, smem, kSmemMaxOptin);
+    p.smem = smem;
+    // TMA pitch / alignment rules (cuda.h cuTensorMapEncodeTiled: strides % 16 B)
+    int os = dtype_size(d.out_dtype);
+    if (d.kind == XTC_OP_MATMUL) {
+        int64_t lda = d.lda ? d.lda : d.k, ldb = d.ldb ? d.ldb : d.n;
+        if ((lda * es) % 16 || (ldb * es) % 16) ILLEGAL("TMA needs 16-byte row pitch for A and B (lda, ldb)");
+    } else {
+        if (d.c % p.atom_k) ILLEGAL("tcgen05 conv2d needs C %% %d == 0 (one 128-byte channel block per im2col load)", p.atom_k);
+        if ((d.f * es) % 16) ILLEGAL("TMA needs 16-byte row pitch for the RSCF filter");
+        if (p.K % s.tile_k) ILLEGAL("tcgen05 conv2d needs R*S*C %% tile_k == 0");
+        if (d.stride_h > 8 || d.stride_w > 8) ILLEGAL("im2col TMA traversal stride must be <= 8");
+        if (d.pad_h > 127 || d.pad_w > 127 || d.r > 128 || d.s > 128) ILLEGAL("im2col corner offsets out of [-128,127]");
+    }
+    p.tiles_m = (int)cdiv(p.M, s.tile_m);
+    p.tiles_n = (int)cdiv(p.N, s.tile_n);
+    p.kb_total = (int)cdiv(p.K, s.tile_k);
+    p.kb_per_split = (int)cdiv(p.kb_total, p.split_k);
+    if ((int64_t)(p.split_k - 1) * p.kb_per_split >= p.kb_total)
+        ILLEGAL("split: split_k %d leaves an empty K segment (%d k-blocks of %d)", p.split_k, p.kb_total, s.tile_k);
+    p.k_per_split = (int64_t)p.kb_per_split * s.tile_k;
+    p.num_tiles = (int64_t)p.tiles_m * p.tiles_n * p.split_k;
+    if (p.num_tiles >= (1ll << 31)) ILLEGAL("too many tiles");
+    if (s.buffer_c) {
+        int64_t ldc = (d.kind == XTC_OP_MATMUL && d.ldc) ? d.ldc : p.n_total;
+        if (p.split_k == 1 && (ldc * os) % 16) ILLEGAL("bufferize: TMA store needs a 16-byte output row pitch");
+    }
+    if (s.buffer_c && d.out_dtype == XTC_BF16 && p.split_k == 1 && s.tile_n % 64)
+        ILLEGAL("bufferize: bf16 TMA-store staging needs tile_n %% 64 == 0");
+    if (p.atomic && s.buffer_c) ILLEGAL("atomic split-K uses direct red.global stores: buffer_c must be 0");
+    p.block = kTcThreads;
+    p.cluster = cg;
+    p.grid_x = s.persistent ? (int)std::min<int64_t>(p.num_tiles, num_sms) : (int)p.num_tiles;
+    if (p.grid_x % cg) p.grid_x += cg - p.grid_x % cg;
+    return XTC_OK;
+}
+
+xtc_status make_plan(const xtc_op_desc& d, const xtc_schedule& s, int num_sms, Plan& p, std::string& why) {
+    xtc_status st = check_desc(d, why);
+    if (st != XTC_OK) return st;
+    if (num_sms <= 0) num_sms = kNumSmsB200;
+    p = Plan();
+    p.sch = s;
+    p.engine = s.engine;
+    int64_t M, N, K, P, Q;
+    gemm_view(d, M, N, K, P, Q);
+    p.M = M; p.N = N; p.K = K; p.n_total = N;
+    if (s.order != XTC_ORDER_MN && s.order != XTC_ORDER_NM) ILLEGAL("interchange: order must be 0 (MN) or 1 (NM)");
+    if (s.raster_group < 0 || s.raster_group > 64) ILLEGAL("raster_group must be in [0,64]");
+    if (s.persistent != 0 && s.persistent != 1) ILLEGAL("persistent must be 0 or 1");
+    p.split_k = s.split_k == 0 ? 1 : s.split_k;
+    if (p.split_k < 1 || p.split_k > 64) ILLEGAL("split_k must be in [1,64]");
+    if (s.split_k_mode != XTC_SPLITK_ORDERED && s.split_k_mode != XTC_SPLITK_ATOMIC) ILLEGAL("unknown split_k_mode");
+    p.atomic = (p.split_k > 1 && s.split_k_mode == XTC_SPLITK_ATOMIC);
+    if (p.atomic && d.out_dtype != XTC_F32) ILLEGAL("atomic split-K needs fp32 output");
+    if (s.split_n_at) {
+        if (s.split_n_at < 0 || s.split_n_at >= N) ILLEGAL("split: split_n_at %d must be in (0, N=%lld)", s.split_n_at, (long long)N);
+        if (d.kind != XTC_OP_MATMUL) ILLEGAL("split_n_at is defined for matmul only");
+        p.has_tail = true;
+        p.tail_n0 = s.split_n_at;
+        p.tail_n = N - s.split_n_at;
+        p.N = s.split_n_at;
+        // remainder root: SIMT 16x16 tiles, 1x1 inner (the paper's scalar remainder loop)
+        p.tail_grid_x = (int)cdiv(p.tail_n, 16);
+        p.tail_grid_y = (int)cdiv(M, 16);
+        if (d.in_dtype != XTC_F32 && d.in_dtype != XTC_BF16 && d.in_dtype != XTC_TF32) ILLEGAL("bad dtype");
+    }
+    for (int i = 0; i < 5; ++i)
+        if (s.reserved[i]) ILLEGAL("reserved schedule fields must be 0");
+    if (s.engine == XTC_ENGINE_SIMT) st = plan_simt(d, s, num_sms, p, why);
+    else if (s.engine == XTC_ENGINE_TCGEN05) st = plan_tc(d, s, num_sms, p, why);
+    else ILLEGAL("unknown engine %d", s.engine);
+    if (st != XTC_OK) return st;
+    if (p.split_k > 1 && !p.atomic) {
+        p.ws_ld = cdiv(p.N, 4) * 4;
+        p.workspace_bytes = (int64_t)p.split_k * p.M * p.ws_ld * 4;
+    }
+    return XTC_OK;
+}
+
+}  // namespace xtc

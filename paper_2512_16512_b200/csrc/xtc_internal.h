@@ -1,0 +1,110 @@
+// xtc_internal.h -- types shared by the planner (host) and the sm_100a kernels.
+// Not part of the public ABI (include/xtc.h is).
+#pragma once
+#include <stdint.h>
+#include <string>
+#include "../../include/xtc.h"
+
+#ifdef __CUDACC__
+#define XTC_HD __host__ __device__ __forceinline__
+#else
+#define XTC_HD inline
+#endif
+
+namespace xtc {
+
+constexpr int kNumSmsB200 = 148;
+constexpr int kSmemMaxOptin = 232448;       // sm_100: (228 - 1) KB per CTA (opt-in)
+constexpr int kSmemReserve = 2048;          // barriers + alignment slack in the tcgen05 kernel
+constexpr int kTcThreads = 256;             // warp0 TMA, warp1 MMA, warp2 TMEM alloc, warp3 idle, warps4-7 epilogue
+constexpr int kTcEpiStageBytes = 4096;      // one warp's 32 rows x 128 B output staging chunk
+constexpr int kTcEpiBuffers = 2;            // double-buffered per warp
+constexpr int kTcEpiSmem = 4 * kTcEpiStageBytes * kTcEpiBuffers;
+
+// Tile-order mapping: the schedule's interchange + grouped raster.
+// Linear tile id -> (split segment ks, tile row mb, tile col nb).
+// order MN: the M-tile loop is outer, the N-tile loop inner; raster_group G
+// strip-mines the outer loop by G and moves the inner loop inside the strip.
+struct TileMap {
+    int32_t tiles_m, tiles_n, split_k, order, group;
+};
+
+XTC_HD void tile_coords(const TileMap& t, int64_t id, int& mb, int& nb, int& ks) {
+    int64_t per = (int64_t)t.tiles_m * t.tiles_n;
+    ks = (int)(id / per);
+    int64_t r = id - (int64_t)ks * per;
+    int outer_n = (t.order == XTC_ORDER_MN) ? t.tiles_m : t.tiles_n;   // extent of outer loop
+    int inner_n = (t.order == XTC_ORDER_MN) ? t.tiles_n : t.tiles_m;
+    int G = t.group < 1 ? 1 : t.group;
+    int64_t strip = (int64_t)G * inner_n;
+    int g = (int)(r / strip);
+    int64_t w = r - (int64_t)g * strip;
+    int rows = outer_n - g * G;
+    if (rows > G) rows = G;
+    int inner = (int)(w / rows);
+    int outer = g * G + (int)(w - (int64_t)inner * rows);
+    if (t.order == XTC_ORDER_MN) { mb = outer; nb = inner; } else { nb = outer; mb = inner; }
+}
+
+// ------------------------------------------------------------------ plans --
+struct Plan {
+    xtc_schedule sch{};
+    int engine = 0;
+    // GEMM view of the main root
+    int64_t M = 0, N = 0, K = 0;        // N = columns of the main root (split_n_at or full N)
+    int64_t n_total = 0;
+    int32_t tiles_m = 0, tiles_n = 0, split_k = 1;
+    int64_t num_tiles = 0;              // tiles_m * tiles_n * split_k
+    int64_t k_per_split = 0;            // SIMT: K elements per segment (multiple of tile_k)
+    int32_t kb_total = 0, kb_per_split = 0;   // tcgen05: k-blocks of tile_k
+    int32_t grid_x = 1, grid_y = 1, grid_z = 1, block = 1, cluster = 1;
+    int32_t smem = 0, tmem_cols = 0;
+    int32_t cta_group = 1;
+    int32_t atom_k = 0, atom_n = 0;     // tcgen05: elements per 128-byte swizzle row
+    int64_t ws_ld = 0;                  // split-K workspace row pitch (floats)
+    int64_t workspace_bytes = 0;
+    bool atomic = false;
+    // split_n_at remainder root (SIMT, fixed 16x16x16 1x1 tile)
+    bool has_tail = false;
+    int64_t tail_n0 = 0, tail_n = 0;
+    int32_t tail_grid_x = 0, tail_grid_y = 0;
+};
+
+// Host-only: legality + plan derivation.  Returns XTC_OK or an error with reason.
+xtc_status make_plan(const xtc_op_desc& d, const xtc_schedule& s, int num_sms, Plan& p, std::string& why);
+xtc_status check_desc(const xtc_op_desc& d, std::string& why);
+void gemm_view(const xtc_op_desc& d, int64_t& M, int64_t& N, int64_t& K, int64_t& P, int64_t& Q);
+
+// ------------------------------------------------------- kernel parameters --
+struct ConvGeom {
+    int32_t is_conv;
+    int32_t H, W, C, P, Q, R, S, sh, sw, ph, pw;
+};
+
+struct SimtParams {
+    const void* A; const void* B; void* C; float* Wk;
+    int64_t M, N, K, lda, ldb, ldc, ws_ld;
+    int32_t tile_m, tile_n, tile_k, pad, stages;
+    int64_t k_per_split;
+    TileMap tm;
+    int64_t num_tiles;
+    int32_t out_bf16, split_out, atomic;
+    ConvGeom cg;
+};
+
+struct TcParams {
+    int64_t M, N, K;
+    int32_t tile_n, tile_k, stages;
+    int32_t kb_total, kb_per_split;
+    TileMap tm;
+    int64_t num_tiles;
+    int32_t acc_buffers, buffer_c, atomic, out_bf16, split_out;
+    int64_t ldc, ws_ld;
+    void* C; float* Wk;
+    uint32_t idesc;
+    uint32_t tmem_cols;
+    uint32_t a_stage_bytes, b_stage_bytes;
+    ConvGeom cg;
+};
+
+}  // namespace xtc

@@ -1,0 +1,165 @@
+"""-m gpu: the CUDA path (through the C-ABI) against the CPU oracle."""
+import numpy as np
+import pytest
+import torch
+
+import paper_2512_16512_b200 as xtc
+from seeded_inputs import MODE_INT, MODE_UNIFORM, gen_tensor
+from gpu_util import (TORCH_DT, check_against_oracle, dev_tensor, oracle_conv, oracle_matmul, run_matmul,
+                      to_numpy_out)
+
+pytestmark = pytest.mark.gpu
+
+S = xtc.schedule
+
+
+# ------------------------------------------------------------- generator --
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("mode", [MODE_UNIFORM, MODE_INT])
+def test_gpu_generator_matches_seeded_inputs(dtype, mode):
+    t = dev_tensor((1000, 37), dtype, 123, mode)
+    got = to_numpy_out(t, dtype)
+    want = gen_tensor(123, (1000, 37), dtype, mode)
+    assert np.array_equal(got.view(np.uint16 if dtype == "bf16" else np.uint32),
+                          want.view(np.uint16 if dtype == "bf16" else np.uint32))
+
+
+# ------------------------------------------------------- config 1 (SIMT) --
+CONFIG1 = dict(engine=0, tile_m=8, tile_n=8, tile_k=8, inner_m=1, inner_n=1, unroll_k=1, stages=1, order=0)
+
+
+@pytest.mark.parametrize("mode", [MODE_INT, MODE_UNIFORM])
+def test_config1_fp32_32cube_tile8_ijk(mode):
+    err, m = run_matmul(32, 32, 32, "f32", "f32", S(**CONFIG1), mode)
+    assert m.t_med_ns > 0
+
+
+SIMT_SCHEDS = [
+    dict(engine=0, tile_m=64, tile_n=64, tile_k=16, inner_m=4, inner_n=4, unroll_k=4, vector_n=4, stages=2, swizzle=4),
+    dict(engine=0, tile_m=32, tile_n=64, tile_k=8, inner_m=2, inner_n=4, unroll_k=2, vector_n=1, stages=1, swizzle=1,
+         order=1, raster_group=2),
+    dict(engine=0, tile_m=128, tile_n=64, tile_k=32, inner_m=8, inner_n=8, unroll_k=8, vector_n=4, stages=2, swizzle=4,
+         persistent=1),
+    dict(engine=0, tile_m=16, tile_n=16, tile_k=16, inner_m=1, inner_n=1, unroll_k=4, stages=2, split_k=3),
+    dict(engine=0, tile_m=16, tile_n=16, tile_k=16, inner_m=1, inner_n=2, split_k=4, split_k_mode=1),
+]
+
+
+@pytest.mark.parametrize("sch", SIMT_SCHEDS)
+def test_simt_schedules_integer_bit_exact(sch):
+    run_matmul(200, 136, 328, "f32", "f32", S(**sch), MODE_INT)
+
+
+@pytest.mark.parametrize("sch", SIMT_SCHEDS[:3])
+def test_simt_schedules_float_tolerance(sch):
+    err, _ = run_matmul(256, 192, 512, "f32", "f32", S(**sch), MODE_UNIFORM)
+    assert err <= 1e-5
+
+
+def test_paper_fig4_split_j_at_256_remainder():
+    """The paper's running example: I=256, J=258, K=512 with J split at 256,
+    K1=4, J1=16 register tile: main root SIMT with a
+    16-wide thread tile, remainder root [256,258) scalar."""
+    sch = S(engine=0, tile_m=16, tile_n=128, tile_k=4, inner_m=1, inner_n=8, unroll_k=4, vector_n=4, stages=1,
+            split_n_at=256)
+    run_matmul(256, 258, 512, "f32", "f32", sch, MODE_INT)
+    run_matmul(256, 258, 512, "f32", "f32", sch, MODE_UNIFORM)
+
+
+def test_simt_bf16_output():
+    run_matmul(96, 80, 64, "f32", "bf16", S(engine=0, tile_m=32, tile_n=16, tile_k=8, inner_m=2, inner_n=2),
+               MODE_INT)
+
+
+# --------------------------------------------------------- tcgen05 bf16 --
+def tc(**kw):
+    base = dict(engine=1, tile_m=128, tile_n=128, tile_k=64, stages=4, swizzle=128, buffer_c=1, acc_buffers=1)
+    base.update(kw)
+    return S(**base)
+
+
+TC_SCHEDS = [
+    dict(),
+    dict(tile_n=64, stages=2),
+    dict(tile_n=256, stages=3, acc_buffers=2, persistent=1),
+    dict(tile_n=192, tile_k=128, stages=2, buffer_c=0),
+    dict(tile_n=128, persistent=1, acc_buffers=2, raster_group=4, order=1),
+    dict(tile_n=128, split_k=3),
+    dict(tile_n=64, split_k=2, buffer_c=0),
+]
+
+
+@pytest.mark.parametrize("sch", TC_SCHEDS)
+def test_tc_bf16_integer_bit_exact(sch):
+    run_matmul(256, 512, 384, "bf16", "bf16", tc(**sch), MODE_INT)
+
+
+@pytest.mark.parametrize("sch", TC_SCHEDS[:5])
+def test_tc_bf16_f32_out_integer(sch):
+    run_matmul(256, 256, 256, "bf16", "f32", tc(**sch), MODE_INT)
+
+
+def test_tc_bf16_ragged_tails():
+    # M, N, K not multiples of the tile: TMA zero-fill on loads, clipping on stores
+    run_matmul(300, 328, 200, "bf16", "bf16", tc(tile_n=128), MODE_INT)
+    run_matmul(300, 328, 200, "bf16", "f32", tc(tile_n=64, buffer_c=0, persistent=1, acc_buffers=2), MODE_INT)
+
+
+@pytest.mark.parametrize("size", [512, 1024])
+def test_tc_bf16_float_tolerance(size):
+    err, m = run_matmul(size, size, size, "bf16", "bf16", tc(tile_n=256, stages=3, acc_buffers=2, persistent=1),
+                        MODE_UNIFORM)
+    assert err <= 5e-3
+
+
+def test_tc_atomic_split_k():
+    run_matmul(256, 256, 512, "bf16", "f32", tc(tile_n=128, split_k=4, split_k_mode=1, buffer_c=0), MODE_INT)
+
+
+# ---------------------------------------------------------- tcgen05 tf32 --
+@pytest.mark.parametrize("sch", [dict(tile_k=32, tile_n=128), dict(tile_k=64, tile_n=96, stages=3, buffer_c=0),
+                                 dict(tile_k=32, tile_n=256, persistent=1, acc_buffers=2)])
+def test_tc_tf32_integer_and_float(sch):
+    run_matmul(256, 384, 256, "tf32", "f32", tc(**sch), MODE_INT)
+    err, _ = run_matmul(256, 384, 256, "tf32", "f32", tc(**sch), MODE_UNIFORM)
+    assert err <= 5e-3
+
+
+# ------------------------------------------------------------------ conv --
+def run_conv(d, in_dtype, out_dtype, sch, mode, seed=10):
+    x = dev_tensor((d.batch, d.h, d.w, d.c), in_dtype, seed, mode)
+    w = dev_tensor((d.r, d.s, d.c, d.f), in_dtype, seed + 1, mode)
+    M, N, K = xtc.gemm_view(d)
+    y = torch.full((M, N), float("nan"), dtype=TORCH_DT[out_dtype], device="cuda:0")
+    op = xtc.Op(d).apply(sch)
+    op.run(x, w, y)
+    torch.cuda.synchronize()
+    O, D = oracle_conv(d, in_dtype, mode, seed, seed + 1)
+    exact = mode == MODE_INT
+    tol = 1e-5 if in_dtype == "f32" else 5e-3
+    err = check_against_oracle(y, O, D, out_dtype, exact, tol)
+    m = op.measure(x, w, y, xtc.measure_cfg(warmup=1, repeats=2, validate=1, exact=int(exact), tol=tol))
+    assert m.valid == 1, m.as_dict()
+    return err
+
+
+@pytest.mark.parametrize("shape", [(2, 56, 56, 64, 64), (3, 14, 14, 256, 256)])
+@pytest.mark.parametrize("mode", [MODE_INT, MODE_UNIFORM])
+def test_tc_conv_resnet_layers(shape, mode):
+    b, h, w, c, f = shape
+    d = xtc.conv2d_desc(b, h, w, c, f, 3, 3, 1, 1, "bf16", "bf16")
+    run_conv(d, "bf16", "bf16", tc(tile_n=min(f, 256), tile_k=64, stages=4, persistent=1, acc_buffers=2), mode)
+
+
+def test_tc_conv_split_k_and_stride2():
+    d = xtc.conv2d_desc(2, 14, 14, 256, 256, 3, 3, 1, 1, "bf16", "bf16")
+    run_conv(d, "bf16", "bf16", tc(tile_n=128, split_k=3), MODE_INT)
+    d2 = xtc.conv2d_desc(2, 15, 17, 64, 128, 3, 3, 2, 1, "bf16", "f32")
+    run_conv(d2, "bf16", "f32", tc(tile_n=128, buffer_c=0), MODE_INT)
+
+
+def test_simt_conv_fp32():
+    d = xtc.conv2d_desc(2, 14, 14, 16, 32, 3, 3, 1, 1, "f32", "f32")
+    sch = S(engine=0, tile_m=64, tile_n=32, tile_k=16, inner_m=4, inner_n=4, unroll_k=4, vector_n=4, stages=2)
+    run_conv(d, "f32", "f32", sch, MODE_INT)
+    run_conv(d, "f32", "f32", sch, MODE_UNIFORM)
