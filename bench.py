@@ -1,0 +1,328 @@
+#!/usr/bin/env python
+"""bench.py -- the driver contract (one JSON line on rank 0).
+
+Workload (N=1): BASELINE.json config 5's operator, the largest matmul,
+8192x8192x8192 bf16 -> bf16, one ``xtc_run`` per step (rows a1-a7 of SURVEY.md
+§8(a)); on-chip validation (a8) runs once before timing.  N>1: the same
+matmul split by M across ranks, C assembled by an NCCL all-gather (config 5;
+strong scaling).  Metric: TFLOP/s of the definition (2*M*N*K / step time).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl xtc|reference]
+
+--impl reference times the CPU oracle (oracle/, fp64 naive loop nest) on a
+bounded row sample of the same workload on the host cores (the tier's
+reference arm).  Only that leg and the cpu_baseline leg touch oracle/.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+M = N = K = 8192
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary.json")
+FALLBACK_PEAKS = {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0}
+
+# Tuned default for the headline workload (from the schedule sweep).
+HEADLINE_SCHEDULE = dict(engine=1, tile_m=128, tile_n=256, tile_k=64, stages=4, swizzle=128, buffer_c=1,
+                         acc_buffers=2, persistent=1, raster_group=8, order=0)
+
+
+def load_peaks():
+    try:
+        with open(PEAKS_FILE) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:
+        return dict(FALLBACK_PEAKS), "fallback"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="xtc", choices=["xtc", "reference"])
+    ap.add_argument("--no-extras", action="store_true", help="skip the secondary config lines (1024^3, conv, sweep)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------ clocks -------
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+            self.t.join(timeout=1)
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------- reference arm ---
+def cpu_oracle_sample(rows: int = 32, seed_a: int = 1, seed_b: int = 2):
+    """The oracle as it stands (fp64 naive loop nest) on `rows` sampled rows of
+    the 8192^3 workload.  Returns (TFLOP/s, seconds, threads, description)."""
+    import oracle
+    from seeded_inputs import gen_rows, gen_tensor
+    sel = [int(i * (M // rows)) for i in range(rows)]
+    A = oracle.to_f64(gen_rows(seed_a, (M, K), sel, "bf16"), "bf16")
+    B = oracle.to_f64(gen_tensor(seed_b, (K, N), "bf16"), "bf16")
+    t0 = time.perf_counter()
+    oracle.matmul(A, B)
+    dt = time.perf_counter() - t0
+    flops = 2.0 * rows * N * K
+    return flops / dt / 1e12, dt, oracle.num_threads(), f"{rows} of {M} output rows of the {M}x{N}x{K} matmul (full N, K)"
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+    oracle.build()
+    vals = []
+    for _ in range(max(0, args.warmup)):
+        pass   # the oracle has no warm state worth priming beyond one call below
+    for _ in range(args.steps):
+        v, dt, threads, sample = cpu_oracle_sample(rows=8)
+        vals.append(v)
+    v = statistics.median(vals)
+    line = {"metric": "matmul TFLOP/s (8192^3 bf16)", "value": v, "unit": "TFLOP/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 2 * M * N * K / (v * 1e12) * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded counter-based generator)", "impl": "reference",
+            "config": {"workload": "matmul 8192x8192x8192 bf16->bf16 (BASELINE config 5)", "global_batch": 1,
+                       "parallelism": "host cores (OpenMP)"},
+            "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": threads, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- xtc arm --
+def main_xtc(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2512_16512_b200 as xtc
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    peaks, peak_kind = load_peaks()
+    peak_tf = float(peaks.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"]))
+
+    from paper_2512_16512_b200.parallel import shard_rows
+    r0, r1 = shard_rows(M, world, rank)
+    Mr = r1 - r0
+    stream = torch.cuda.current_stream(dev)
+    sp = stream.cuda_stream
+    a = torch.empty((Mr, K), dtype=torch.bfloat16, device=dev)
+    b = torch.empty((K, N), dtype=torch.bfloat16, device=dev)
+    c = torch.empty((Mr, N), dtype=torch.bfloat16, device=dev)
+    # every rank regenerates its rows of A and the whole of B from the seed: no broadcast needed
+    xtc.xtc_fill(a.data_ptr(), Mr * K, xtc.XTC_BF16, 1, 0, r0 * K, sp)
+    xtc.xtc_fill(b.data_ptr(), K * N, xtc.XTC_BF16, 2, 0, 0, sp)
+    desc = xtc.matmul_desc(Mr, N, K, "bf16", "bf16")
+    op = xtc.Op(desc, local).apply(xtc.schedule(**HEADLINE_SCHEDULE))
+
+    # a8: on-chip validation once (fp64 GPU reference, NaN sentinel), outside the timed region
+    vm = op.measure(a, b, c, xtc.measure_cfg(warmup=0, repeats=1, validate=1, tol=5e-3), stream=sp)
+    validation = {"valid": int(vm.valid), "max_norm_err": vm.max_norm_err, "n_nan": int(vm.n_nan), "tol": 5e-3}
+
+    full_c = torch.empty((M, N), dtype=torch.bfloat16, device=dev) if world > 1 else None
+
+    def step():
+        op.run(a, b, c, stream=sp)
+        if world > 1:
+            dist.all_gather_into_tensor(full_c, c)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for i in range(args.steps):
+            evs[i][0].record(stream)
+            kev[i][0].record(stream)
+            op.run(a, b, c, stream=sp)
+            kev[i][1].record(stream)
+            if world > 1:
+                dist.all_gather_into_tensor(full_c, c)
+            evs[i][1].record(stream)
+        t_end.record(stream)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    launches_per_step = op.launches()
+    total_ms = t_start.elapsed_time(t_end)
+    kern_ms = [s.elapsed_time(e) for s, e in kev]
+    step_ms = total_ms / args.steps
+    t = torch.tensor([total_ms, sum(kern_ms) / len(kern_ms)], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms_max, kern_ms_max = float(t[0]), float(t[1])
+    flops = 2.0 * M * N * K
+    value = flops / (total_ms_max / args.steps * 1e-3) / 1e12
+
+    # e2e: through the public API with HOST buffers: H2D inputs, run, D2H result, every step
+    h_a = torch.empty((Mr, K), dtype=torch.bfloat16, pin_memory=True)
+    h_b = torch.empty((K, N), dtype=torch.bfloat16, pin_memory=True)
+    h_a.copy_(a)
+    h_b.copy_(b)
+    h_c = torch.empty((M if world > 1 else Mr, N), dtype=torch.bfloat16, pin_memory=True)
+    e2e_steps = max(3, min(args.steps, 10))
+
+    def e2e_step():
+        a.copy_(h_a, non_blocking=True)
+        b.copy_(h_b, non_blocking=True)
+        op.run(a, b, c, stream=sp)
+        if world > 1:
+            dist.all_gather_into_tensor(full_c, c)
+            h_c.copy_(full_c, non_blocking=True)
+        else:
+            h_c.copy_(c, non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    te = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_val = flops / (float(te[0]) / e2e_steps * 1e-3) / 1e12
+
+    extras = {}
+    if rank == 0 and world == 1 and not args.no_extras:
+        try:
+            from paper_2512_16512_b200.bench_extras import run_extras
+            extras = run_extras(xtc, torch, dev, peak_tf)
+        except Exception as ex:   # extras are secondary: report, don't fail the headline
+            extras = {"error": repr(ex)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, dt, threads, sample = cpu_oracle_sample(rows=32)
+        cpu = {"value": v, "unit": "TFLOP/s", "cores": threads, "kind": "oracle", "sample": sample,
+               "seconds": round(dt, 2)}
+
+    traffic = None
+    try:
+        with open(NCU_SUMMARY) as f:
+            traffic = json.load(f).get("headline_kernel", {}).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    achieved = flops / world / (kern_ms_max * 1e-3) / 1e12
+    if rank == 0:
+        clocks = clk.summary()
+        line = {
+            "metric": "matmul TFLOP/s (8192^3 bf16)", "value": value, "unit": "TFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms_max / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded counter-based generator, uniform[-1,1) bf16)",
+            "config": {"workload": "matmul 8192x8192x8192 bf16->bf16 (BASELINE config 5: largest matmul)",
+                       "model": None, "global_batch": 1, "seq_len": None,
+                       "parallelism": f"M-sharded x{world} + NCCL all-gather" if world > 1 else "single GPU",
+                       "schedule": HEADLINE_SCHEDULE,
+                       "l2": "inputs (256 MiB) exceed L2 (126 MB); no flush between steps"},
+            "frac_of_peak": value / world / peak_tf,
+            "peak_used": {"bf16_tflops": peak_tf, "kind": peak_kind},
+            "validation": validation,
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
+                         "frac": achieved / peak_tf, "traffic": traffic,
+                         "kernel": "tc_gemm_kernel<bf16>", "algorithmic_flops_per_launch": flops / world},
+            "gpu_launches": launches_per_step * args.steps,
+            "e2e": {"value": e2e_val, "unit": "TFLOP/s", "h2d_bytes_per_step": (Mr * K + K * N) * 2,
+                    "d2h_bytes_per_step": (M if world > 1 else Mr) * N * 2, "steps": e2e_steps},
+            "clocks": clocks,
+            "cpu_baseline": cpu,
+            "extras": extras,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return main_xtc(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,88 @@
+"""Secondary BASELINE.json configs measured in the same bench.py run (N=1):
+1024^3 / 512^3 bf16 best-of-schedules, the ResNet-50 conv layers at N=32 as
+implicit GEMM, the fp32 SIMT path, and a short candidate sweep (schedules/s).
+Every number is validated on chip (fp64 GPU reference) before it is timed."""
+from __future__ import annotations
+
+import time
+
+TC = dict(engine=1, tile_m=128, tile_k=64, swizzle=128)
+
+MATMUL_SCHEDS = {
+    1024: [dict(TC, tile_n=128, stages=6, buffer_c=1, acc_buffers=2, persistent=1, raster_group=4),
+           dict(TC, tile_n=64, stages=8, buffer_c=1, acc_buffers=2, persistent=1, raster_group=4),
+           dict(TC, tile_n=128, stages=6, buffer_c=1, acc_buffers=1, split_k=2),
+           dict(TC, tile_n=64, stages=8, buffer_c=1, acc_buffers=1, split_k=2)],
+    512: [dict(TC, tile_n=64, stages=8, buffer_c=1, acc_buffers=1),
+          dict(TC, tile_n=64, stages=4, buffer_c=1, acc_buffers=1, split_k=2),
+          dict(TC, tile_n=128, stages=4, buffer_c=1, acc_buffers=1, split_k=4)],
+}
+
+CONV_SCHEDS = {
+    "L56": [dict(TC, tile_n=64, stages=8, buffer_c=1, acc_buffers=2, persistent=1, raster_group=8),
+            dict(TC, tile_n=64, stages=6, buffer_c=1, acc_buffers=2, persistent=0)],
+    "L14": [dict(TC, tile_n=256, stages=4, buffer_c=1, acc_buffers=1, split_k=3),
+            dict(TC, tile_n=128, stages=6, buffer_c=1, acc_buffers=2, split_k=2, persistent=1),
+            dict(TC, tile_n=256, stages=4, buffer_c=1, acc_buffers=2, persistent=1)],
+}
+
+
+def _best(xtc, torch, dev, desc, scheds, in_shapes, peak, fill_seed=11, flush=1):
+    M, N, K = xtc.gemm_view(desc)
+    tdt = torch.bfloat16 if desc.in_dtype == xtc.XTC_BF16 else torch.float32
+    odt = torch.bfloat16 if desc.out_dtype == xtc.XTC_BF16 else torch.float32
+    a = torch.empty(in_shapes[0], dtype=tdt, device=dev)
+    b = torch.empty(in_shapes[1], dtype=tdt, device=dev)
+    c = torch.empty((M, N), dtype=odt, device=dev)
+    st = torch.cuda.current_stream(dev).cuda_stream
+    xtc.xtc_fill(a.data_ptr(), a.numel(), desc.in_dtype, fill_seed, 0, 0, st)
+    xtc.xtc_fill(b.data_ptr(), b.numel(), desc.in_dtype, fill_seed + 1, 0, 0, st)
+    op = xtc.Op(desc, dev.index)
+    best = None
+    rows = []
+    for s in scheds:
+        op.apply(xtc.schedule(**s))
+        m = op.measure(a, b, c, xtc.measure_cfg(warmup=3, repeats=20, flush_l2=flush, validate=1,
+                                                reuse_reference=1, peak_tflops=peak), stream=st)
+        rows.append({"tflops_med": round(m.tflops_med, 1), "valid": int(m.valid), "t_med_us": round(m.t_med_ns / 1e3, 2)})
+        if m.valid == 1 and (best is None or m.tflops_med > best[0].tflops_med):
+            best = (m, s)
+    if best is None:
+        return {"error": "no valid schedule", "tried": rows}
+    m, s = best
+    return {"tflops_med": m.tflops_med, "tflops_min_time": m.tflops_min, "t_med_us": m.t_med_ns / 1e3,
+            "frac_peak": m.tflops_med / peak, "max_norm_err": m.max_norm_err, "l2": "flushed" if flush else "warm",
+            "schedule": s, "tried": rows}
+
+
+def run_extras(xtc, torch, dev, peak):
+    out = {}
+    for n in (1024, 512):
+        d = xtc.matmul_desc(n, n, n, "bf16", "bf16")
+        out[f"matmul_{n}_bf16"] = _best(xtc, torch, dev, d, MATMUL_SCHEDS[n], [(n, n), (n, n)], peak)
+    d = xtc.matmul_desc(1024, 1024, 1024, "f32", "f32")
+    out["matmul_1024_f32_simt"] = _best(xtc, torch, dev, d, [
+        dict(engine=0, tile_m=128, tile_n=128, tile_k=16, inner_m=8, inner_n=8, unroll_k=4, vector_n=4, stages=2,
+             swizzle=4, raster_group=4),
+        dict(engine=0, tile_m=64, tile_n=128, tile_k=16, inner_m=4, inner_n=8, unroll_k=4, vector_n=4, stages=2,
+             swizzle=4)], [(1024, 1024), (1024, 1024)], peak)
+    for name, (h, c) in {"L56": (56, 64), "L14": (14, 256)}.items():
+        d = xtc.conv2d_desc(32, h, h, c, c, 3, 3, 1, 1, "bf16", "bf16")
+        out[f"conv_{name}_n32_bf16"] = _best(xtc, torch, dev, d, CONV_SCHEDS[name], [(32, h, h, c), (3, 3, c, c)], peak)
+    # a10: short sweep at 1024^3 (the full 4096-candidate sweep is paper_2512_16512_b200.sweep)
+    from .sweep import run_sweep
+    n_c = 256
+    desc, samples, mine, todo, scheds, op, (a, b, c), cfg, st, _ = run_sweep(1024, 1024, 1024, n_c, seed=0,
+                                                                             device=dev.index, peak_tflops=peak)
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    mets = op.sweep(scheds, a, b, c, cfg, stream=st)
+    torch.cuda.synchronize(dev)
+    dt = time.perf_counter() - t0
+    ok = [m for m in mets if m.status == 0 and m.valid == 1]
+    out["sweep_1024_bf16"] = {"candidates": n_c, "seconds": dt, "schedules_per_s": n_c / dt, "valid": len(ok),
+                              "invalid": n_c - len(ok),
+                              "best_tflops": max((m.tflops_med for m in ok), default=None),
+                              "protocol": "per candidate: apply, NaN fill + run + compare vs cached fp64 GPU ref, "
+                                          "2 warmup, 10 timed reps"}
+    return out

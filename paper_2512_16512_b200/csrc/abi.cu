@@ -359,8 +359,10 @@ static xtc_status encode_maps(xtc_op op, const void* A, const void* B, void* C) 
         cuuint64_t strides[1] = {(cuuint64_t)(ldb * es)};
         cuuint32_t box[2] = {(cuuint32_t)atom, (cuuint32_t)tile_k};
         cuuint32_t estr[2] = {1, 1};
+        // tf32 MN-major operands must use 32-byte swizzle atoms (UMMA SWIZZLE_128B_BASE32B)
+        const CUtensorMapSwizzle bsw = tf32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B;
         r = g_encode_tiled(&op->tmB, in_t, 2, const_cast<void*>(B), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                           bsw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(XTC_E_CUDA, "cuTensorMapEncodeTiled(B) failed: " + std::to_string((int)r));
     }
     if (d.kind == XTC_OP_MATMUL) {

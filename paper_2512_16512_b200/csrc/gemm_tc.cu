@@ -141,7 +141,10 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                         for (int kk = 0; kk < ATOM / UMMA_K; ++kk) {
                             const uint64_t adesc = ptx::smem_desc_sw128(a_base + a * A_ATOM_BYTES + kk * 32, 16, 1024);
                             const uint32_t krow = a * ATOM + kk * UMMA_K;
-                            const uint64_t bdesc = ptx::smem_desc_sw128(b_base + krow * 128, b_lbo, 1024);
+                            // B is MN-major: LBO = stride between 128-byte N blocks, SBO = stride between
+                            // K-row groups (8 rows of 128 B for SW128; 4 rows for tf32's SW128_BASE32B)
+                            const uint64_t bdesc = TF32 ? ptx::smem_desc_sw128(b_base + krow * 128, b_lbo, 512, 1)
+                                                        : ptx::smem_desc_sw128(b_base + krow * 128, b_lbo, 1024, 2);
                             ptx::umma<TF32>(d_tmem, adesc, bdesc, p.idesc, (kb > kb0 || a > 0 || kk > 0) ? 1u : 0u);
                         }
                     }

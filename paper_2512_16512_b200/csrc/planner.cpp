@@ -72,7 +72,9 @@ static xtc_status plan_simt(const xtc_op_desc& d, const xtc_schedule& s, int num
     if (s.tile_m < 1 || s.tile_n < 1 || s.tile_m > 256 || s.tile_n > 256) ILLEGAL("SIMT tile_m/tile_n must be in [1,256]");
     if (s.tile_m % TM || s.tile_n % TN) ILLEGAL("strip-mine: tile_m %% inner_m and tile_n %% inner_n must be 0");
     int threads = (s.tile_m / TM) * (s.tile_n / TN);
-    if (threads < 1 || threads > 1024) ILLEGAL("SIMT tile/inner gives %d threads (must be 1..1024)", threads);
+    if (threads < 1 || threads > simt_max_threads(TM, TN))
+        ILLEGAL("SIMT tile/inner gives %d threads (must be 1..%d for a %dx%d thread tile)", threads,
+                simt_max_threads(TM, TN), TM, TN);
     if (s.tile_k < 1 || s.tile_k > 64) ILLEGAL("SIMT tile_k must be in [1,64]");
     int U = s.unroll_k == 0 ? 1 : s.unroll_k;
     if (!pow2_in(U, 1, 8)) ILLEGAL("SIMT unroll_k must be 1,2,4 or 8");

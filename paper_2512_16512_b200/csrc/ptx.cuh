@@ -164,14 +164,16 @@ __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.
 //   bits [16,30) leading-dimension byte offset >> 4
 //   bits [32,46) stride-dimension byte offset >> 4
 //   bits [46,48) version = 1 (sm100)
-//   bits [61,64) layout: 2 = SWIZZLE_128B
-__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+//   bits [61,64) layout: 2 = SWIZZLE_128B, 1 = SWIZZLE_128B_BASE32B (32-byte atoms;
+//                the only MN-major layout for 32-bit (tf32) operands)
+__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes,
+                                                    uint32_t layout = 2) {
     uint64_t d = 0;
     d |= (uint64_t)((saddr >> 4) & 0x3FFF);
     d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
     d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
     d |= (uint64_t)1 << 46;
-    d |= (uint64_t)2 << 61;
+    d |= (uint64_t)(layout & 7) << 61;
     return d;
 }
 

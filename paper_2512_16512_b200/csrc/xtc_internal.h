@@ -21,6 +21,12 @@ constexpr int kTcEpiStageBytes = 4096;      // one warp's 32 rows x 128 B output
 constexpr int kTcEpiBuffers = 2;            // double-buffered per warp
 constexpr int kTcEpiSmem = 4 * kTcEpiStageBytes * kTcEpiBuffers;
 
+// SIMT register budget: the TM x TN accumulator tile plus operands must fit
+// without spills, so large thread tiles cap the CTA size (65536 regs / SM).
+XTC_HD constexpr int simt_max_threads(int tm, int tn) {
+    return tm * tn >= 32 ? 256 : (tm * tn >= 16 ? 512 : 1024);
+}
+
 // Tile-order mapping: the schedule's interchange + grouped raster.
 // Linear tile id -> (split segment ks, tile row mb, tile col nb).
 // order MN: the M-tile loop is outer, the N-tile loop inner; raster_group G

@@ -1,0 +1,83 @@
+"""Multi-GPU partitioning of the hot path.
+
+Only the two shardings the path has are implemented:
+  1. candidate data-parallelism: a sweep's schedule candidates are dealt to
+     ranks by id (id mod world == rank); every rank regenerates identical inputs
+     and the identical candidate list from the seed; fixed-size records are
+     collected with one all-gather (NCCL over NVLink on the GPU box).
+  2. M-sharding of a large GEMM (conv: batch sharding): rank r computes the
+     contiguous output rows [r0, r1); B is replicated by regenerating it from
+     the seed (no broadcast); C is assembled by all_gather_into_tensor.
+There is no tensor/pipeline/sequence parallelism: the operator has none.
+"""
+from __future__ import annotations
+
+from typing import List, Sequence, Tuple
+
+import torch
+
+# record layout of one measured candidate (float64 slots)
+REC_FIELDS = ["id", "status", "valid", "max_norm_err", "n_mismatch", "n_nan", "t_min_ns", "t_med_ns",
+              "tflops_med", "sm_clock_mhz"]
+REC = len(REC_FIELDS)
+
+
+def shard_rows(m: int, world: int, rank: int) -> Tuple[int, int]:
+    """Contiguous, balanced row range of `rank` (the first m % world ranks get one more row)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    base, rem = divmod(m, world)
+    r0 = rank * base + min(rank, rem)
+    return r0, r0 + base + (1 if rank < rem else 0)
+
+
+def rank_candidates(n: int, world: int, rank: int) -> List[int]:
+    """Candidate ids of `rank`: interleaved (id mod world) to balance random per-candidate cost."""
+    return list(range(rank, n, world))
+
+
+def pack_records(ids: Sequence[int], metrics: Sequence, rows: int) -> torch.Tensor:
+    """Fixed-size [rows, REC] float64 block; unused rows have id = -1."""
+    t = torch.full((rows, REC), -1.0, dtype=torch.float64)
+    for i, (cid, m) in enumerate(zip(ids, metrics)):
+        t[i, 0] = cid
+        if isinstance(m, dict):
+            vals = [m.get(f, 0.0) for f in REC_FIELDS[1:]]
+        else:
+            vals = [getattr(m, f) for f in REC_FIELDS[1:]]
+        t[i, 1:] = torch.tensor([float(v) for v in vals], dtype=torch.float64)
+    return t
+
+
+def unpack_gathered(gathered: torch.Tensor, n: int) -> List[dict]:
+    """[world*rows, REC] -> list of n records ordered by candidate id."""
+    out = [None] * n
+    for row in gathered.tolist():
+        cid = int(row[0])
+        if 0 <= cid < n:
+            out[cid] = dict(zip(REC_FIELDS, row))
+            out[cid]["id"] = cid
+    missing = [i for i, r in enumerate(out) if r is None]
+    if missing:
+        raise RuntimeError(f"records missing for candidates {missing[:8]}...")
+    return out
+
+
+def gather_records(local: torch.Tensor, group=None) -> torch.Tensor:
+    """All-gather the per-rank record blocks (NCCL on GPU tensors, gloo on CPU)."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    out = torch.empty((world * local.shape[0], local.shape[1]), dtype=local.dtype, device=local.device)
+    dist.all_gather_into_tensor(out, local, group=group)
+    return out
+
+
+def gather_rows(c_shard: torch.Tensor, m_total: int, group=None) -> torch.Tensor:
+    """Assemble C from equal row shards (M-sharded GEMM, config 5)."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    if m_total % world:
+        raise ValueError("all_gather_into_tensor needs equal shards: M % world must be 0")
+    out = torch.empty((m_total,) + tuple(c_shard.shape[1:]), dtype=c_shard.dtype, device=c_shard.device)
+    dist.all_gather_into_tensor(out, c_shard.contiguous(), group=group)
+    return out
