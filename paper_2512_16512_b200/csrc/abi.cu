@@ -12,7 +12,7 @@
 #include "xtc_internal.h"
 
 namespace xtc {
-cudaError_t launch_tc_gemm(bool tf32, bool conv, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
+cudaError_t launch_tc_gemm(bool tf32, bool conv, int cta_group, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
                            const TcParams& p, int grid, int smem, cudaStream_t st);
 cudaError_t launch_simt_gemm(int tm, int tn, int u, int vec, const SimtParams& p, int grid, int block, int smem,
                              cudaStream_t st);
@@ -482,13 +482,13 @@ static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cud
         const bool tf32 = d.in_dtype == XTC_TF32;
         const uint32_t fmt = tf32 ? 2u : 1u;
         tp.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (0u << 15) | (1u << 16) |
-                   ((uint32_t)(p.sch.tile_n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+                   ((uint32_t)(p.sch.tile_n >> 3) << 17) | ((uint32_t)((128 * p.cta_group) >> 4) << 24);
         tp.tmem_cols = (uint32_t)p.tmem_cols;
         const int es = dsize(d.in_dtype);
         tp.a_stage_bytes = (uint32_t)(128 * p.sch.tile_k * es);
-        tp.b_stage_bytes = (uint32_t)(p.sch.tile_k * p.sch.tile_n * es);
+        tp.b_stage_bytes = (uint32_t)(p.sch.tile_k * (p.sch.tile_n / p.cta_group) * es);
         tp.cg = conv_geom(d);
-        CU_TRY(launch_tc_gemm(tf32, d.kind == XTC_OP_CONV2D, op->tmA, op->tmB, op->tmC, tp, p.grid_x, p.smem, st),
+        CU_TRY(launch_tc_gemm(tf32, d.kind == XTC_OP_CONV2D, p.cta_group, op->tmA, op->tmB, op->tmC, tp, p.grid_x, p.smem, st),
                "tc_gemm launch");
         ++launches;
     }

@@ -2,11 +2,13 @@
 // conv2d for sm_100a (bf16 kind::f16 / tf32 kind::tf32, fp32 accumulate in TMEM).
 //
 // How the paper's primitives (Table I) appear in this kernel:
-//   strip_mine  -> CTA tile 128 x tile_n x tile_k; UMMA atom 128 x tile_n x 16 (8 tf32)
+//   strip_mine  -> CTA tile 128 x tile_n x tile_k (CTA pair: 256 x tile_n); UMMA atom
+//                  (128|256) x tile_n x 16 (8 for tf32)
 //   interchange -> tile order (TileMap: MN / NM + grouped raster)
 //   unroll      -> the tile_k / UMMA_K MMAs of one stage are issued back to back
 //   vectorize   -> the innermost tile is one tcgen05.mma (the tensor core is the SIMD unit)
-//   parallelize -> one CTA per tile, or persistent CTAs striding over tiles
+//   parallelize -> one CTA (pair) per tile, or persistent CTAs striding over tiles;
+//                  cluster_m = 2 pairs two SMs on one 256-row tile (cta_group::2)
 //   split       -> split_k contiguous K segments, fp32 partials + ordered reduction
 //   pack        -> TMA -> `stages`-deep SMEM ring in the 128-byte-swizzled layout the
 //                  UMMA reads ("copies the elements ... in the order of their access",
@@ -15,8 +17,15 @@
 //                  written back by TMA store ("copied to the output tensor, while modifying
 //                  its ordering to fit the original layout")
 //
-// Warp roles (256 threads): warp 0 = TMA producer, warp 1 = MMA issuer (one thread),
-// warp 2 = TMEM allocator, warp 3 idle, warps 4..7 = epilogue (TMEM lane quarters).
+// Warp roles (256 threads): warp 0 = TMA producer, warp 1 = MMA issuer (one thread;
+// leader CTA only for pairs), warp 2 = TMEM allocator, warp 3 idle, warps 4..7 =
+// epilogue (TMEM lane quarters).
+//
+// CTA pair (CG = 2): each CTA loads its own 128 rows of A and its tile_n/2 columns
+// of B; both CTAs' TMA bytes are counted on the LEADER's full barrier; the leader's
+// single thread issues cta_group::2 MMAs (M = 256) whose commits are multicast to
+// the empty / tmem-full barriers of both CTAs; each CTA's epilogue drains its own
+// 128 TMEM lanes and arrives on the leader's tmem-empty barrier.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include "ptx.cuh"
@@ -24,13 +33,14 @@
 
 namespace xtc {
 
-template <bool TF32, bool CONV>
+template <bool TF32, bool CONV, int CG>
 __global__ void __launch_bounds__(kTcThreads, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmC, const TcParams p) {
     constexpr int ATOM = TF32 ? 32 : 64;     // elements per 128-byte row (A's K / B's N)
     constexpr int UMMA_K = TF32 ? 8 : 16;    // K per tcgen05.mma (32 bytes)
     constexpr uint32_t A_ATOM_BYTES = 128 * 128;
+    constexpr int TILE_M = 128 * CG;
 
     extern __shared__ uint8_t smem_raw[];
     const uint32_t pad = (1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u;
@@ -47,6 +57,10 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    const uint32_t rank = (CG == 2) ? ptx::cluster_ctarank() : 0u;
+    const int64_t cluster_id = blockIdx.x / CG;
+    const int64_t num_clusters = gridDim.x / CG;
+    const int bn_cta = p.tile_n / CG;        // B columns this CTA loads
 
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tmA);
@@ -55,15 +69,15 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     }
     if (warp == 1 && lane == 0) {
         for (int s = 0; s < S; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
-        for (int a = 0; a < 2; ++a) { ptx::mbar_init(&tfull[a], 1); ptx::mbar_init(&tempty[a], 4); }
+        for (int a = 0; a < 2; ++a) { ptx::mbar_init(&tfull[a], 1); ptx::mbar_init(&tempty[a], 4 * CG); }
         ptx::fence_mbarrier_init();
     }
     if (warp == 2) {
-        ptx::tmem_alloc(tmem_slot, p.tmem_cols);
-        ptx::tmem_relinquish();
+        ptx::tmem_alloc<CG>(tmem_slot, p.tmem_cols);
+        ptx::tmem_relinquish<CG>();
     }
     ptx::tc_fence_before();
-    __syncthreads();
+    if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
@@ -74,13 +88,14 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             uint32_t ph = 0;
             const uint32_t stage_bytes = p.a_stage_bytes + p.b_stage_bytes;
             const int n_a = p.tile_k / ATOM;
-            const int n_b = p.tile_n / ATOM;
-            for (int64_t t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+            const int n_b = bn_cta / ATOM;
+            for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters) {
                 int mb, nb, ks;
                 tile_coords(p.tm, t, mb, nb, ks);
                 const int kb0 = ks * p.kb_per_split;
                 const int kb1 = min(p.kb_total, kb0 + p.kb_per_split);
-                const int m0 = mb * 128, n0 = nb * p.tile_n;
+                const int m0 = mb * TILE_M + 128 * (int)rank;     // this CTA's 128 rows
+                const int n0 = nb * p.tile_n + bn_cta * (int)rank;  // this CTA's B columns
                 int wq = 0, hp = 0, nimg = 0;
                 if constexpr (CONV) {
                     const int pq = p.cg.P * p.cg.Q;
@@ -92,7 +107,13 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 }
                 for (int kb = kb0; kb < kb1; ++kb) {
                     ptx::mbar_wait(&empty[s], ph ^ 1);
-                    ptx::mbar_arrive_expect_tx(&full[s], stage_bytes);
+                    uint32_t bar_c = 0;
+                    if constexpr (CG == 2) {
+                        if (rank == 0) ptx::mbar_arrive_expect_tx(&full[s], 2 * stage_bytes);
+                        bar_c = ptx::mapa_shared(ptx::smem_u32(&full[s]), 0);
+                    } else {
+                        ptx::mbar_arrive_expect_tx(&full[s], stage_bytes);
+                    }
                     uint8_t* a_dst = sA + (size_t)s * p.a_stage_bytes;
                     uint8_t* b_dst = sB + (size_t)s * p.b_stage_bytes;
                     for (int a = 0; a < n_a; ++a) {
@@ -102,28 +123,36 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                             const int c = kc - rs * p.cg.C;
                             const int r = rs / p.cg.S;
                             const int sx = rs - r * p.cg.S;
-                            ptx::tma_load_im2col_4d(&tmA, a_dst + a * A_ATOM_BYTES, &full[s], c, wq, hp, nimg,
-                                                    (uint16_t)sx, (uint16_t)r);
+                            if constexpr (CG == 2)
+                                ptx::tma_load_im2col_4d_pair(&tmA, a_dst + a * A_ATOM_BYTES, bar_c, c, wq, hp, nimg,
+                                                             (uint16_t)sx, (uint16_t)r);
+                            else
+                                ptx::tma_load_im2col_4d(&tmA, a_dst + a * A_ATOM_BYTES, &full[s], c, wq, hp, nimg,
+                                                        (uint16_t)sx, (uint16_t)r);
                         } else {
-                            ptx::tma_load_2d(&tmA, a_dst + a * A_ATOM_BYTES, &full[s], kc, m0);
+                            if constexpr (CG == 2) ptx::tma_load_2d_pair(&tmA, a_dst + a * A_ATOM_BYTES, bar_c, kc, m0);
+                            else ptx::tma_load_2d(&tmA, a_dst + a * A_ATOM_BYTES, &full[s], kc, m0);
                         }
                     }
-                    for (int b = 0; b < n_b; ++b)
-                        ptx::tma_load_2d(&tmB, b_dst + (size_t)b * p.tile_k * 128, &full[s], n0 + b * ATOM, kb * p.tile_k);
+                    for (int b = 0; b < n_b; ++b) {
+                        uint8_t* dst = b_dst + (size_t)b * p.tile_k * 128;
+                        if constexpr (CG == 2) ptx::tma_load_2d_pair(&tmB, dst, bar_c, n0 + b * ATOM, kb * p.tile_k);
+                        else ptx::tma_load_2d(&tmB, dst, &full[s], n0 + b * ATOM, kb * p.tile_k);
+                    }
                     if (++s == S) { s = 0; ph ^= 1; }
                 }
             }
         }
     } else if (warp == 1) {
         // ===================== MMA issuer (contraction) =====================
-        if (lane == 0) {
+        if (lane == 0 && rank == 0) {
             int s = 0;
             uint32_t ph = 0;
             int acc = 0;
             uint32_t aph = 0;
             const int n_a = p.tile_k / ATOM;
             const uint32_t b_lbo = (uint32_t)p.tile_k * 128u;   // stride between 128-byte N blocks of B
-            for (int64_t t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+            for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters) {
                 int mb, nb, ks;
                 tile_coords(p.tm, t, mb, nb, ks);
                 const int kb0 = ks * p.kb_per_split;
@@ -145,13 +174,13 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                             // K-row groups (8 rows of 128 B for SW128; 4 rows for tf32's SW128_BASE32B)
                             const uint64_t bdesc = TF32 ? ptx::smem_desc_sw128(b_base + krow * 128, b_lbo, 512, 1)
                                                         : ptx::smem_desc_sw128(b_base + krow * 128, b_lbo, 1024, 2);
-                            ptx::umma<TF32>(d_tmem, adesc, bdesc, p.idesc, (kb > kb0 || a > 0 || kk > 0) ? 1u : 0u);
+                            ptx::umma<TF32, CG>(d_tmem, adesc, bdesc, p.idesc, (kb > kb0 || a > 0 || kk > 0) ? 1u : 0u);
                         }
                     }
-                    ptx::umma_commit(&empty[s]);       // frees the SMEM slot when these MMAs finish
+                    ptx::umma_commit<CG>(&empty[s]);   // frees the SMEM slot(s) when these MMAs finish
                     if (++s == S) { s = 0; ph ^= 1; }
                 }
-                ptx::umma_commit(&tfull[acc]);         // accumulator ready for the epilogue
+                ptx::umma_commit<CG>(&tfull[acc]);     // accumulator ready for the epilogue(s)
                 if (++acc == p.acc_buffers) { acc = 0; aph ^= 1; }
             }
         }
@@ -164,10 +193,10 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         uint8_t* stage = sC + q * (kTcEpiStageBytes * kTcEpiBuffers);
         const bool to_ws = p.split_out != 0;
         const bool bf16_out = p.out_bf16 && !to_ws;
-        for (int64_t t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters) {
             int mb, nb, ks;
             tile_coords(p.tm, t, mb, nb, ks);
-            const int m0 = mb * 128, n0 = nb * p.tile_n;
+            const int m0 = mb * TILE_M + 128 * (int)rank, n0 = nb * p.tile_n;
             const int64_t row = (int64_t)m0 + 32 * q + lane;
             ptx::mbar_wait(&tfull[acc], aph);
             ptx::tc_fence_after();
@@ -262,37 +291,64 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             }
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&tempty[acc]);   // TMEM buffer free for the next tile
+            if (lane == 0) {                           // TMEM buffer free for the next tile
+                if constexpr (CG == 2) ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&tempty[acc]), 0));
+                else ptx::mbar_arrive(&tempty[acc]);
+            }
             if (++acc == p.acc_buffers) { acc = 0; aph ^= 1; }
         }
         if (p.buffer_c && lane == 0) ptx::bulk_wait<0>();
     }
 
     ptx::tc_fence_before();
-    __syncthreads();
+    if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
     if (warp == 2) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc(tmem_base, p.tmem_cols);
+        ptx::tmem_dealloc<CG>(tmem_base, p.tmem_cols);
     }
 }
 
 // ------------------------------------------------------------------ launch --
-template <bool TF32, bool CONV>
+template <bool TF32, bool CONV, int CG>
 static cudaError_t launch_tc_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
                                const TcParams& p, int grid, int smem, cudaStream_t st) {
-    auto k = tc_gemm_kernel<TF32, CONV>;
+    auto k = tc_gemm_kernel<TF32, CONV, CG>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    k<<<grid, kTcThreads, smem, st>>>(a, b, c, p);
+    if constexpr (CG == 1) {
+        k<<<grid, kTcThreads, smem, st>>>(a, b, c, p);
+    } else {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(kTcThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = CG;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, k, a, b, c, p);
+        if (e != cudaSuccess) return e;
+    }
     return cudaGetLastError();
 }
 
-cudaError_t launch_tc_gemm(bool tf32, bool conv, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
-                           const TcParams& p, int grid, int smem, cudaStream_t st) {
-    if (tf32) return conv ? launch_tc_t<true, true>(a, b, c, p, grid, smem, st)
-                          : launch_tc_t<true, false>(a, b, c, p, grid, smem, st);
-    return conv ? launch_tc_t<false, true>(a, b, c, p, grid, smem, st)
-                : launch_tc_t<false, false>(a, b, c, p, grid, smem, st);
+template <int CG>
+static cudaError_t launch_tc_cg(bool tf32, bool conv, const CUtensorMap& a, const CUtensorMap& b,
+                                const CUtensorMap& c, const TcParams& p, int grid, int smem, cudaStream_t st) {
+    if (tf32) return conv ? launch_tc_t<true, true, CG>(a, b, c, p, grid, smem, st)
+                          : launch_tc_t<true, false, CG>(a, b, c, p, grid, smem, st);
+    return conv ? launch_tc_t<false, true, CG>(a, b, c, p, grid, smem, st)
+                : launch_tc_t<false, false, CG>(a, b, c, p, grid, smem, st);
+}
+
+cudaError_t launch_tc_gemm(bool tf32, bool conv, int cta_group, const CUtensorMap& a, const CUtensorMap& b,
+                           const CUtensorMap& c, const TcParams& p, int grid, int smem, cudaStream_t st) {
+    if (cta_group == 2) return launch_tc_cg<2>(tf32, conv, a, b, c, p, grid, smem, st);
+    return launch_tc_cg<1>(tf32, conv, a, b, c, p, grid, smem, st);
 }
 
 }  // namespace xtc

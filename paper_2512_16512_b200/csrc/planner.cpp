@@ -114,7 +114,6 @@ static xtc_status plan_tc(const xtc_op_desc& d, const xtc_schedule& s, int num_s
     p.atom_n = 128 / es;
     int cg = s.cluster_m == 0 ? 1 : s.cluster_m;
     if (cg != 1 && cg != 2) ILLEGAL("tcgen05 cluster_m must be 1 (cta_group::1) or 2 (cta_group::2 CTA pair)");
-    if (cg == 2) ILLEGAL("cta_group::2 (cluster_m=2) is not built yet");
     p.cta_group = cg;
     if (s.tile_m != 128 * cg) ILLEGAL("tcgen05 tile_m must be %d for cluster_m=%d (UMMA M=128 per CTA)", 128 * cg, cg);
     if (s.inner_m != 0 && s.inner_m != s.tile_m) ILLEGAL("tcgen05 inner_m (UMMA M) must equal tile_m");
@@ -171,8 +170,9 @@ static xtc_status plan_tc(const xtc_op_desc& d, const xtc_schedule& s, int num_s
     if (p.atomic && s.buffer_c) ILLEGAL("atomic split-K uses direct red.global stores: buffer_c must be 0");
     p.block = kTcThreads;
     p.cluster = cg;
-    p.grid_x = s.persistent ? (int)std::min<int64_t>(p.num_tiles, num_sms) : (int)p.num_tiles;
-    if (p.grid_x % cg) p.grid_x += cg - p.grid_x % cg;
+    // one CTA (pair) per tile, or a persistent grid of at most one CTA per SM
+    const int64_t ctas = p.num_tiles * cg;
+    p.grid_x = s.persistent ? (int)std::min<int64_t>(ctas, num_sms - num_sms % cg) : (int)ctas;
     return XTC_OK;
 }
 

@@ -163,3 +163,38 @@ def test_simt_conv_fp32():
     sch = S(engine=0, tile_m=64, tile_n=32, tile_k=16, inner_m=4, inner_n=4, unroll_k=4, vector_n=4, stages=2)
     run_conv(d, "f32", "f32", sch, MODE_INT)
     run_conv(d, "f32", "f32", sch, MODE_UNIFORM)
+
+
+# ------------------------------------------------- CTA pair (cta_group::2) --
+PAIR_SCHEDS = [
+    dict(tile_m=256, cluster_m=2, tile_n=256, stages=4, acc_buffers=2, persistent=1),
+    dict(tile_m=256, cluster_m=2, tile_n=128, stages=6, acc_buffers=2, persistent=0),
+    dict(tile_m=256, cluster_m=2, tile_n=256, tile_k=128, stages=2, buffer_c=0),
+    dict(tile_m=256, cluster_m=2, tile_n=128, split_k=3, persistent=1, acc_buffers=2, order=1, raster_group=2),
+]
+
+
+@pytest.mark.parametrize("sch", PAIR_SCHEDS)
+def test_tc_pair_bf16_integer_bit_exact(sch):
+    run_matmul(512, 512, 384, "bf16", "bf16", tc(**sch), MODE_INT)
+
+
+def test_tc_pair_ragged_and_float():
+    run_matmul(300, 328, 200, "bf16", "f32", tc(**PAIR_SCHEDS[0]), MODE_INT)
+    err, _ = run_matmul(1024, 1024, 1024, "bf16", "bf16", tc(**PAIR_SCHEDS[0]), MODE_UNIFORM)
+    assert err <= 5e-3
+
+
+def test_tc_pair_tf32():
+    sch = tc(tile_m=256, cluster_m=2, tile_n=128, tile_k=32, stages=4, persistent=1, acc_buffers=2)
+    run_matmul(512, 256, 256, "tf32", "f32", sch, MODE_INT)
+    err, _ = run_matmul(512, 256, 256, "tf32", "f32", sch, MODE_UNIFORM)
+    assert err <= 5e-3
+
+
+@pytest.mark.parametrize("shape", [(2, 56, 56, 64, 128), (3, 14, 14, 256, 256)])
+def test_tc_pair_conv(shape):
+    b, h, w, c, f = shape
+    d = xtc.conv2d_desc(b, h, w, c, f, 3, 3, 1, 1, "bf16", "bf16")
+    run_conv(d, "bf16", "bf16", tc(tile_m=256, cluster_m=2, tile_n=128, stages=4, persistent=1, acc_buffers=2),
+             MODE_INT)
