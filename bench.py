@@ -32,8 +32,8 @@ NCU_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary.json")
 FALLBACK_PEAKS = {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0}
 
 # Tuned default for the headline workload (from the schedule sweep).
-HEADLINE_SCHEDULE = dict(engine=1, tile_m=128, tile_n=256, tile_k=64, stages=4, swizzle=128, buffer_c=1,
-                         acc_buffers=2, persistent=1, raster_group=8, order=0)
+HEADLINE_SCHEDULE = dict(engine=1, tile_m=256, tile_n=256, tile_k=64, stages=6, swizzle=128, buffer_c=1,
+                         acc_buffers=2, persistent=1, raster_group=16, order=0, cluster_m=2)
 
 
 def load_peaks():

@@ -25,6 +25,7 @@ cudaError_t launch_compare(const void* C, int out_bf16, int64_t M, int64_t N, in
                            const double* D, double* blk_err, int64_t* blk_idx, void* counts, int blocks,
                            cudaStream_t st);
 cudaError_t launch_flush(void* buf, int64_t bytes, uint32_t salt, cudaStream_t st);
+cudaError_t launch_delay(uint64_t ns, cudaStream_t st);
 cudaError_t launch_splitk_reduce(const float* W, int S, int64_t M, int64_t N, int64_t ws_ld, void* C, int64_t ldc,
                                  int out_bf16, cudaStream_t st);
 cudaError_t launch_tail_gemm(const void* A, const void* B, int bf16_in, void* C, int out_bf16, int64_t M, int64_t n0,
@@ -642,6 +643,8 @@ static xtc_status measure_impl(xtc_op op, const void* A, const void* B, void* C,
         CU_TRY(cudaEventCreate(&e), "cudaEventCreate");
         op->evs.push_back(e);
     }
+    // keep the GPU busy while the reps are enqueued (budget ~20 us of host work per rep)
+    CU_TRY(launch_delay(std::min<uint64_t>(20000ull * (uint64_t)R + 50000ull, 20000000ull), st), "delay");
     for (int i = 0; i < R; ++i) {
         if (cfg->flush_l2) CU_TRY(launch_flush(g_flush_buf[op->device], g_flush_bytes[op->device], (uint32_t)i, st), "flush");
         CU_TRY(cudaEventRecord(op->evs[2 * i], st), "event");

@@ -164,7 +164,7 @@ template <int TM, int TN, int U, int VEC>
 static cudaError_t launch_simt_t(const SimtParams& p, int grid, int block, int smem, cudaStream_t st) {
     auto k = simt_gemm_kernel<TM, TN, U, VEC>;
     if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaError_t e = ensure_smem_attr(k, smem);
         if (e != cudaSuccess) return e;
     }
     k<<<grid, block, smem, st>>>(p);

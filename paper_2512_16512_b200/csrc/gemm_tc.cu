@@ -313,7 +313,7 @@ template <bool TF32, bool CONV, int CG>
 static cudaError_t launch_tc_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
                                const TcParams& p, int grid, int smem, cudaStream_t st) {
     auto k = tc_gemm_kernel<TF32, CONV, CG>;
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = ensure_smem_attr(k, smem);
     if (e != cudaSuccess) return e;
     if constexpr (CG == 1) {
         k<<<grid, kTcThreads, smem, st>>>(a, b, c, p);

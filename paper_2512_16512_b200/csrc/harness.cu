@@ -190,13 +190,38 @@ cudaError_t launch_compare(const void* C, int out_bf16, int64_t M, int64_t N, in
 }
 
 // --------------------------------------------------------------- L2 flush --
-__global__ void flush_kernel(uint4* buf, int64_t n16, uint32_t salt) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x)
-        buf[i] = make_uint4(salt, (uint32_t)i, salt ^ 0x5a5a5a5au, (uint32_t)(i >> 32));
+// Streams through a buffer >= 2 x L2 with loads, leaving L2 full of CLEAN lines
+// of that buffer: the next kernel finds none of its data cached and pays no
+// write-back of dirty flush lines (a store-based flush would bill the next
+// kernel for evicting ~L2-size of dirty data).  The store is never taken; it
+// only keeps the loads alive.
+__global__ void flush_kernel(const uint4* __restrict__ buf, int64_t n16, uint32_t salt, uint32_t* sink) {
+    uint32_t acc = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint4 v = __ldcg(buf + i);
+        acc ^= v.x ^ v.y ^ v.z ^ v.w;
+    }
+    if (acc == salt + 0x9E3779B9u) sink[0] = acc;
+}
+
+// Device-side delay: keeps the stream busy while the host enqueues the timed
+// reps, so per-rep CUDA events bracket GPU execution, not host submission.
+__global__ void delay_kernel(uint64_t ns) {
+    uint64_t t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    uint64_t t = t0;
+    while (t - t0 < ns) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+}
+
+cudaError_t launch_delay(uint64_t ns, cudaStream_t st) {
+    delay_kernel<<<1, 32, 0, st>>>(ns);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_flush(void* buf, int64_t bytes, uint32_t salt, cudaStream_t st) {
-    flush_kernel<<<148 * 8, 512, 0, st>>>(static_cast<uint4*>(buf), bytes / 16, salt);
+    // the last 16 bytes of the buffer serve as the (never written) sink
+    flush_kernel<<<148 * 8, 512, 0, st>>>(static_cast<const uint4*>(buf), bytes / 16 - 1, salt,
+                                          reinterpret_cast<uint32_t*>(static_cast<char*>(buf) + bytes - 16));
     return cudaGetLastError();
 }
 

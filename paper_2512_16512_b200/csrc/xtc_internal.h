@@ -4,6 +4,7 @@
 #include <stdint.h>
 #include <string>
 #include "../../include/xtc.h"
+#include <cuda_runtime.h>
 
 #ifdef __CUDACC__
 #define XTC_HD __host__ __device__ __forceinline__
@@ -20,6 +21,21 @@ constexpr int kTcThreads = 256;             // warp0 TMA, warp1 MMA, warp2 TMEM 
 constexpr int kTcEpiStageBytes = 4096;      // one warp's 32 rows x 128 B output staging chunk
 constexpr int kTcEpiBuffers = 2;            // double-buffered per warp
 constexpr int kTcEpiSmem = 4 * kTcEpiStageBytes * kTcEpiBuffers;
+
+// cudaFuncSetAttribute is a driver round trip: set the dynamic-SMEM opt-in once
+// per kernel variant and device, not on every launch (sweeps launch thousands).
+template <typename F>
+inline cudaError_t ensure_smem_attr(F* kernel, int smem) {
+    static int set_bytes[64] = {0};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (smem <= set_bytes[dev]) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess) set_bytes[dev] = smem;
+    return e;
+}
 
 // SIMT register budget: the TM x TN accumulator tile plus operands must fit
 // without spills, so large thread tiles cap the CTA size (65536 regs / SM).
