@@ -7,6 +7,8 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 #include "xtc_internal.h"
@@ -36,6 +38,22 @@ cudaError_t launch_tail_gemm(const void* A, const void* B, int bf16_in, void* C,
 using namespace xtc;
 
 static thread_local std::string g_err;
+
+namespace xtc {
+cudaError_t ensure_smem_attr_impl(const void* kernel, int smem) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, int> set_bytes;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(mu);
+    int& have = set_bytes[{kernel, dev}];
+    if (smem <= have) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess) have = smem;
+    return e;
+}
+}  // namespace xtc
 
 static xtc_status fail(xtc_status s, const std::string& why) {
     g_err = why;

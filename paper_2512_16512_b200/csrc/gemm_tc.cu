@@ -49,7 +49,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     uint8_t* sA = smem;
     uint8_t* sB = sA + (size_t)S * p.a_stage_bytes;
     uint8_t* sC = sB + (size_t)S * p.b_stage_bytes;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sC + kTcEpiSmem);
+    uint64_t* full = reinterpret_cast<uint64_t*>(sC + (p.buffer_c ? kTcEpiSmem : 0));
     uint64_t* empty = full + 8;
     uint64_t* tfull = empty + 8;
     uint64_t* tempty = tfull + 2;

@@ -136,7 +136,7 @@ static xtc_status plan_tc(const xtc_op_desc& d, const xtc_schedule& s, int num_s
     p.tmem_cols = alloc;
     int a_stage = 128 * s.tile_k * es;
     int b_stage = s.tile_k * bn_cta * es;
-    int smem = s.stages * (a_stage + b_stage) + kTcEpiSmem + kSmemReserve;
+    int smem = s.stages * (a_stage + b_stage) + (s.buffer_c ? kTcEpiSmem : 0) + kSmemReserve;
     if (smem > kSmemMaxOptin) ILLEGAL("pack: %d stages x %d B + epilogue = %d B SMEM exceeds %d B",
                                       s.stages, a_stage + b_stage, smem, kSmemMaxOptin);
     p.smem = smem;

@@ -24,17 +24,11 @@ constexpr int kTcEpiSmem = 4 * kTcEpiStageBytes * kTcEpiBuffers;
 
 // cudaFuncSetAttribute is a driver round trip: set the dynamic-SMEM opt-in once
 // per kernel variant and device, not on every launch (sweeps launch thousands).
+cudaError_t ensure_smem_attr_impl(const void* kernel, int smem);   // keyed by (kernel, device)
+
 template <typename F>
 inline cudaError_t ensure_smem_attr(F* kernel, int smem) {
-    static int set_bytes[64] = {0};
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return e;
-    if (dev < 0 || dev >= 64) dev = 0;
-    if (smem <= set_bytes[dev]) return cudaSuccess;
-    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e == cudaSuccess) set_bytes[dev] = smem;
-    return e;
+    return ensure_smem_attr_impl(reinterpret_cast<const void*>(kernel), smem);
 }
 
 // SIMT register budget: the TM x TN accumulator tile plus operands must fit
