@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -28,6 +29,8 @@ cudaError_t launch_compare(const void* C, int out_bf16, int64_t M, int64_t N, in
                            cudaStream_t st);
 cudaError_t launch_flush(void* buf, int64_t bytes, uint32_t salt, cudaStream_t st);
 cudaError_t launch_delay(uint64_t ns, cudaStream_t st);
+cudaError_t launch_fault(void* C, int out_bf16, int64_t M, int64_t N, int64_t ldc, int kind, int64_t row, int64_t col,
+                         cudaStream_t st);
 cudaError_t launch_splitk_reduce(const float* W, int S, int64_t M, int64_t N, int64_t ws_ld, void* C, int64_t ldc,
                                  int out_bf16, cudaStream_t st);
 cudaError_t launch_tail_gemm(const void* A, const void* B, int bf16_in, void* C, int out_bf16, int64_t M, int64_t n0,
@@ -151,6 +154,10 @@ struct xtc_op_s {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     std::vector<cudaEvent_t> evs;
     int32_t last_launches = 0;
+    // fault injection for harness tests (XTC_DEBUG_FAULT=kind, XTC_DEBUG_FAULT_AT=row,col):
+    // 1 = perturb one output, 2 = leave one output unwritten (NaN), 3 = drop a 32x32 block (zeros)
+    int fault = 0;
+    int64_t fault_row = 0, fault_col = 0;
 };
 
 static int dsize(int dt) { return dt == XTC_BF16 ? 2 : 4; }
@@ -234,6 +241,13 @@ xtc_status xtc_op_create(const xtc_op_desc* desc, int32_t device, xtc_op* out) {
     op->d = *desc;
     op->device = device;
     op->num_sms = prop.multiProcessorCount;
+    if (const char* f = getenv("XTC_DEBUG_FAULT")) {
+        op->fault = atoi(f);
+        if (const char* at = getenv("XTC_DEBUG_FAULT_AT")) {
+            long long r = 0, c = 0;
+            if (sscanf(at, "%lld,%lld", &r, &c) == 2) { op->fault_row = r; op->fault_col = c; }
+        }
+    }
     *out = op;
     return XTC_OK;
 }
@@ -521,6 +535,10 @@ static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cud
         CU_TRY(launch_tail_gemm(A, B, d.in_dtype == XTC_BF16, C, out_bf16, p.M, p.tail_n0, p.tail_n, p.K, lda, ldb, ldc,
                                 p.tail_grid_x, p.tail_grid_y, st),
                "tail_gemm");
+        ++launches;
+    }
+    if (op->fault) {
+        CU_TRY(launch_fault(C, out_bf16, p.M, p.n_total, ldc, op->fault, op->fault_row, op->fault_col, st), "fault");
         ++launches;
     }
     op->last_launches = launches;

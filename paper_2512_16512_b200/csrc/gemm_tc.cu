@@ -83,7 +83,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 
     if (warp == 0) {
         // ===================== TMA producer (pack) =====================
-        if (lane == 0) {
+        {
             int s = 0;
             uint32_t ph = 0;
             const uint32_t stage_bytes = p.a_stage_bytes + p.b_stage_bytes;
@@ -107,6 +107,10 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 }
                 for (int kb = kb0; kb < kb1; ++kb) {
                     ptx::mbar_wait(&empty[s], ph ^ 1);
+                    if (!ptx::elect_one()) {           // one lane issues; the warp stays converged
+                        if (++s == S) { s = 0; ph ^= 1; }
+                        continue;
+                    }
                     uint32_t bar_c = 0;
                     if constexpr (CG == 2) {
                         if (rank == 0) ptx::mbar_arrive_expect_tx(&full[s], 2 * stage_bytes);
@@ -145,13 +149,24 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         }
     } else if (warp == 1) {
         // ===================== MMA issuer (contraction) =====================
-        if (lane == 0 && rank == 0) {
+        // The whole warp runs the loop (its values are warp-uniform, so they live in
+        // uniform registers); one elected lane issues the MMAs and the commits.
+        if (rank == 0) {
             int s = 0;
             uint32_t ph = 0;
             int acc = 0;
             uint32_t aph = 0;
             const int n_a = p.tile_k / ATOM;
             const uint32_t b_lbo = (uint32_t)p.tile_k * 128u;   // stride between 128-byte N blocks of B
+            // Descriptors of stage 0; stage s and each k-step only advance the 14-bit
+            // start-address field (address >> 4), which never carries out of the field
+            // because the whole SMEM window is < 256 KB.
+            const uint64_t adesc0 = ptx::smem_desc_sw128(ptx::smem_u32(sA), 16, 1024);
+            // B is MN-major: LBO = stride between 128-byte N blocks, SBO = stride between
+            // K-row groups (8 rows of 128 B for SW128; 4 rows for tf32's SW128_BASE32B)
+            const uint64_t bdesc0 = TF32 ? ptx::smem_desc_sw128(ptx::smem_u32(sB), b_lbo, 512, 1)
+                                         : ptx::smem_desc_sw128(ptx::smem_u32(sB), b_lbo, 1024, 2);
+            const uint32_t a_stage16 = p.a_stage_bytes >> 4, b_stage16 = p.b_stage_bytes >> 4;
             for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters) {
                 int mb, nb, ks;
                 tile_coords(p.tm, t, mb, nb, ks);
@@ -163,24 +178,25 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 for (int kb = kb0; kb < kb1; ++kb) {
                     ptx::mbar_wait(&full[s], ph);
                     ptx::tc_fence_after();
-                    const uint32_t a_base = ptx::smem_u32(sA + (size_t)s * p.a_stage_bytes);
-                    const uint32_t b_base = ptx::smem_u32(sB + (size_t)s * p.b_stage_bytes);
-                    for (int a = 0; a < n_a; ++a) {
+                    if (ptx::elect_one()) {
+                        const uint64_t ad = adesc0 + (uint64_t)(s * a_stage16);
+                        const uint64_t bd = bdesc0 + (uint64_t)(s * b_stage16);
+                        for (int a = 0; a < n_a; ++a) {
 #pragma unroll
-                        for (int kk = 0; kk < ATOM / UMMA_K; ++kk) {
-                            const uint64_t adesc = ptx::smem_desc_sw128(a_base + a * A_ATOM_BYTES + kk * 32, 16, 1024);
-                            const uint32_t krow = a * ATOM + kk * UMMA_K;
-                            // B is MN-major: LBO = stride between 128-byte N blocks, SBO = stride between
-                            // K-row groups (8 rows of 128 B for SW128; 4 rows for tf32's SW128_BASE32B)
-                            const uint64_t bdesc = TF32 ? ptx::smem_desc_sw128(b_base + krow * 128, b_lbo, 512, 1)
-                                                        : ptx::smem_desc_sw128(b_base + krow * 128, b_lbo, 1024, 2);
-                            ptx::umma<TF32, CG>(d_tmem, adesc, bdesc, p.idesc, (kb > kb0 || a > 0 || kk > 0) ? 1u : 0u);
+                            for (int kk = 0; kk < ATOM / UMMA_K; ++kk) {
+                                const uint32_t krow = a * ATOM + kk * UMMA_K;
+                                ptx::umma<TF32, CG>(d_tmem, ad + (uint64_t)((a * A_ATOM_BYTES + kk * 32) >> 4),
+                                                    bd + (uint64_t)(krow * 8), p.idesc,
+                                                    (kb > kb0 || a > 0 || kk > 0) ? 1u : 0u);
+                            }
                         }
+                        ptx::umma_commit<CG>(&empty[s]);   // frees the SMEM slot(s) when these MMAs finish
                     }
-                    ptx::umma_commit<CG>(&empty[s]);   // frees the SMEM slot(s) when these MMAs finish
+                    __syncwarp();
                     if (++s == S) { s = 0; ph ^= 1; }
                 }
-                ptx::umma_commit<CG>(&tfull[acc]);     // accumulator ready for the epilogue(s)
+                if (ptx::elect_one()) ptx::umma_commit<CG>(&tfull[acc]);   // accumulator ready for the epilogue(s)
+                __syncwarp();
                 if (++acc == p.acc_buffers) { acc = 0; aph ^= 1; }
             }
         }

@@ -213,6 +213,32 @@ __global__ void delay_kernel(uint64_t ns) {
     while (t - t0 < ns) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
 }
 
+// ------------------------------------------------- fault injection (tests) --
+// kind 1: C[row][col] += 1 (a wrong value); 2: C[row][col] = NaN (an output the
+// schedule "forgot" to write); 3: a 32x32 block at (row, col) zeroed (a dropped tile).
+__global__ void fault_kernel(void* C, int out_bf16, int64_t M, int64_t N, int64_t ldc, int kind, int64_t row,
+                             int64_t col) {
+    const int64_t r = row + (kind == 3 ? threadIdx.x / 32 : 0);
+    const int64_t c = col + (kind == 3 ? threadIdx.x % 32 : 0);
+    if (kind != 3 && threadIdx.x) return;
+    if (r >= M || c >= N) return;
+    const int64_t i = r * ldc + c;
+    if (out_bf16) {
+        __nv_bfloat16* p = static_cast<__nv_bfloat16*>(C) + i;
+        const float v = __bfloat162float(*p);
+        *p = __float2bfloat16_rn(kind == 1 ? v + 1.0f : kind == 2 ? __int_as_float(0x7fc00000) : 0.0f);
+    } else {
+        float* p = static_cast<float*>(C) + i;
+        *p = kind == 1 ? *p + 1.0f : kind == 2 ? __int_as_float(0x7fc00000) : 0.0f;
+    }
+}
+
+cudaError_t launch_fault(void* C, int out_bf16, int64_t M, int64_t N, int64_t ldc, int kind, int64_t row, int64_t col,
+                         cudaStream_t st) {
+    fault_kernel<<<1, 1024, 0, st>>>(C, out_bf16, M, N, ldc, kind, row, col);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_delay(uint64_t ns, cudaStream_t st) {
     delay_kernel<<<1, 32, 0, st>>>(ns);
     return cudaGetLastError();

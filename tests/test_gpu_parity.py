@@ -198,3 +198,60 @@ def test_tc_pair_conv(shape):
     d = xtc.conv2d_desc(b, h, w, c, f, 3, 3, 1, 1, "bf16", "bf16")
     run_conv(d, "bf16", "bf16", tc(tile_m=256, cluster_m=2, tile_n=128, stages=4, persistent=1, acc_buffers=2),
              MODE_INT)
+
+
+# ------------------------------------------------------- fault injection --
+@pytest.mark.parametrize("kind,expect", [(1, "value"), (2, "nan"), (3, "block")])
+@pytest.mark.parametrize("in_dtype", ["bf16", "f32"])
+def test_validation_catches_injected_faults(monkeypatch, kind, expect, in_dtype):
+    """SPEC S:524 / SURVEY T4: a corrupted, unwritten or dropped output must fail
+    on-chip validation and be located."""
+    monkeypatch.setenv("XTC_DEBUG_FAULT", str(kind))
+    monkeypatch.setenv("XTC_DEBUG_FAULT_AT", "70,37")
+    M = N = K = 128
+    desc = xtc.matmul_desc(M, N, K, in_dtype, "f32")
+    a = dev_tensor((M, K), in_dtype, 3, MODE_INT)
+    b = dev_tensor((K, N), in_dtype, 4, MODE_INT)
+    c = torch.empty((M, N), dtype=torch.float32, device="cuda:0")
+    sch = tc(tile_n=128) if in_dtype == "bf16" else S(engine=0, tile_m=32, tile_n=32, tile_k=8, inner_m=2, inner_n=2)
+    op = xtc.Op(desc).apply(sch)
+    m = op.measure(a, b, c, xtc.measure_cfg(warmup=0, repeats=1, validate=1, exact=1))
+    assert m.valid == 0
+    if expect == "nan":
+        assert m.n_nan == 1 and (m.err_row, m.err_col) == (70, 37)
+    elif expect == "value":
+        assert m.n_mismatch == 1 and (m.err_row, m.err_col) == (70, 37) and m.max_norm_err > 0
+    else:
+        assert m.n_mismatch >= 1 and 70 <= m.err_row < 102 and 37 <= m.err_col < 69
+    # validate=2 turns the failure into a status
+    with pytest.raises(xtc.XtcError):
+        xtc._check(xtc.lib().xtc_measure(op.handle, xtc._ptrs([a.data_ptr(), b.data_ptr()]), xtc._ptrs([c.data_ptr()]),
+                                         xtc.ctypes.byref(xtc.measure_cfg(warmup=0, repeats=1, validate=2, exact=1)),
+                                         xtc.ctypes.byref(xtc.xtc_metrics()), xtc.c_void_p(0)))
+
+
+def test_illegal_schedule_launches_nothing():
+    desc = xtc.matmul_desc(256, 256, 256, "bf16", "bf16")
+    op = xtc.Op(desc).apply(tc())
+    with pytest.raises(xtc.XtcError) as e:
+        op.apply(tc(tile_n=100))
+    assert e.value.status == xtc.XTC_E_ILLEGAL_SCHEDULE
+    # the previous (legal) schedule is still in effect
+    a = dev_tensor((256, 256), "bf16", 1, MODE_INT)
+    b = dev_tensor((256, 256), "bf16", 2, MODE_INT)
+    c = torch.empty((256, 256), dtype=torch.bfloat16, device="cuda:0")
+    m = op.measure(a, b, c, xtc.measure_cfg(warmup=0, repeats=2, validate=1, exact=1))
+    assert m.valid == 1
+
+
+def test_sweep_records_and_illegal_candidates():
+    desc = xtc.matmul_desc(512, 512, 512, "bf16", "bf16")
+    a = dev_tensor((512, 512), "bf16", 1, MODE_INT)
+    b = dev_tensor((512, 512), "bf16", 2, MODE_INT)
+    c = torch.empty((512, 512), dtype=torch.bfloat16, device="cuda:0")
+    cands = [tc(tile_n=128), tc(tile_n=100), tc(tile_m=256, cluster_m=2, tile_n=256, persistent=1, acc_buffers=2),
+             S(engine=0, tile_m=32, tile_n=32, tile_k=8, inner_m=2, inner_n=2)]
+    recs = xtc.Op(desc).sweep(cands, a, b, c, xtc.measure_cfg(warmup=1, repeats=3, validate=1, exact=1))
+    assert [r.status for r in recs] == [0, xtc.XTC_E_ILLEGAL_SCHEDULE, 0, xtc.XTC_E_ILLEGAL_SCHEDULE]
+    assert recs[0].valid == 1 and recs[2].valid == 1 and recs[1].valid == -1
+    assert recs[0].tflops_med > 0 and recs[0].t_min_ns <= recs[0].t_med_ns <= recs[0].t_max_ns
