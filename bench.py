@@ -32,7 +32,7 @@ NCU_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary.json")
 FALLBACK_PEAKS = {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0}
 
 # Tuned default for the headline workload (from the schedule sweep).
-HEADLINE_SCHEDULE = dict(engine=1, tile_m=256, tile_n=256, tile_k=64, stages=6, swizzle=128, buffer_c=1,
+HEADLINE_SCHEDULE = dict(engine=1, tile_m=256, tile_n=256, tile_k=128, stages=3, swizzle=128, buffer_c=1,
                          acc_buffers=2, persistent=1, raster_group=16, order=0, cluster_m=2)
 
 
@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--impl", default="xtc", choices=["xtc", "reference"])
     ap.add_argument("--no-extras", action="store_true", help="skip the secondary config lines (1024^3, conv, sweep)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sweep-candidates", type=int, default=1024)
     return ap.parse_args()
 
 
@@ -156,6 +157,39 @@ def run_reference(args):
             "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+# ---------------------------------------------------------------- sweep ----
+def sharded_sweep(xtc, torch, dist, dev, world, rank, n_cand, peak_tf):
+    """Candidates dealt by id % world; each rank measures its share through
+    xtc_sweep (C++ loop: apply, NaN-fill + validate vs cached fp64 GPU reference,
+    2 warmup, 10 timed reps); fixed-size records all-gathered.  Timed with CUDA
+    events from a post-setup barrier to the end of the gather, max over ranks."""
+    from paper_2512_16512_b200.parallel import gather_records, pack_records, unpack_gathered
+    from paper_2512_16512_b200.sweep import run_sweep
+    _, samples, mine, todo, scheds, op, (a, b, c), cfg, sp, _ = run_sweep(
+        1024, 1024, 1024, n_cand, seed=0, world=world, rank=rank, device=dev.index, peak_tflops=peak_tf)
+    rows = (n_cand + world - 1) // world
+    stream = torch.cuda.current_stream(dev)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    mets = op.sweep(scheds, a, b, c, cfg, stream=sp)
+    local = pack_records(todo, mets, rows).to(dev)
+    gathered = gather_records(local) if world > 1 else local
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    t = torch.tensor([e0.elapsed_time(e1) * 1e-3], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    recs = unpack_gathered(gathered.cpu(), n_cand)
+    ok = [r for r in recs if int(r["status"]) == 0 and int(r["valid"]) == 1]
+    best = max(ok, key=lambda r: r["tflops_med"]) if ok else None
+    return {"candidates": n_cand, "ranks": world, "seconds": float(t[0]), "schedules_per_s": n_cand / float(t[0]),
+            "valid": len(ok), "invalid": n_cand - len(ok), "best_tflops": best["tflops_med"] if best else None,
+            "best_id": int(best["id"]) if best else None, "space": "GpuStrategy(TC_SLOTS) legal set, seed 0"}
 
 
 # ---------------------------------------------------------------- xtc arm --
@@ -269,6 +303,11 @@ def main_xtc(args):
     e2e_val = flops / (float(te[0]) / e2e_steps * 1e-3) / 1e12
 
     extras = {}
+    if not args.no_extras:
+        # config 4 (scaled down): a seeded candidate sweep at 1024^3 dealt across the ranks,
+        # records all-gathered over NCCL; device-timed, max over ranks
+        extras["sweep_1024_bf16_sharded"] = sharded_sweep(xtc, torch, dist, dev, world, rank, args.sweep_candidates,
+                                                          peak_tf)
     if rank == 0 and world == 1 and not args.no_extras:
         try:
             from paper_2512_16512_b200.bench_extras import run_extras

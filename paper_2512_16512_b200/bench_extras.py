@@ -69,20 +69,4 @@ def run_extras(xtc, torch, dev, peak):
     for name, (h, c) in {"L56": (56, 64), "L14": (14, 256)}.items():
         d = xtc.conv2d_desc(32, h, h, c, c, 3, 3, 1, 1, "bf16", "bf16")
         out[f"conv_{name}_n32_bf16"] = _best(xtc, torch, dev, d, CONV_SCHEDS[name], [(32, h, h, c), (3, 3, c, c)], peak)
-    # a10: short sweep at 1024^3 (the full 4096-candidate sweep is paper_2512_16512_b200.sweep)
-    from .sweep import run_sweep
-    n_c = 256
-    desc, samples, mine, todo, scheds, op, (a, b, c), cfg, st, _ = run_sweep(1024, 1024, 1024, n_c, seed=0,
-                                                                             device=dev.index, peak_tflops=peak)
-    torch.cuda.synchronize(dev)
-    t0 = time.perf_counter()
-    mets = op.sweep(scheds, a, b, c, cfg, stream=st)
-    torch.cuda.synchronize(dev)
-    dt = time.perf_counter() - t0
-    ok = [m for m in mets if m.status == 0 and m.valid == 1]
-    out["sweep_1024_bf16"] = {"candidates": n_c, "seconds": dt, "schedules_per_s": n_c / dt, "valid": len(ok),
-                              "invalid": n_c - len(ok),
-                              "best_tflops": max((m.tflops_med for m in ok), default=None),
-                              "protocol": "per candidate: apply, NaN fill + run + compare vs cached fp64 GPU ref, "
-                                          "2 warmup, 10 timed reps"}
     return out

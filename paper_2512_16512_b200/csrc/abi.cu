@@ -679,8 +679,9 @@ static xtc_status measure_impl(xtc_op op, const void* A, const void* B, void* C,
         CU_TRY(cudaEventCreate(&e), "cudaEventCreate");
         op->evs.push_back(e);
     }
-    // keep the GPU busy while the reps are enqueued (budget ~20 us of host work per rep)
-    CU_TRY(launch_delay(std::min<uint64_t>(20000ull * (uint64_t)R + 50000ull, 20000000ull), st), "delay");
+    // keep the GPU busy while the reps are enqueued (host enqueue is ~3-6 us per rep
+    // with cached launch attributes; budget 8 us per rep + 20 us)
+    CU_TRY(launch_delay(std::min<uint64_t>(8000ull * (uint64_t)R + 20000ull, 20000000ull), st), "delay");
     for (int i = 0; i < R; ++i) {
         if (cfg->flush_l2) CU_TRY(launch_flush(g_flush_buf[op->device], g_flush_bytes[op->device], (uint32_t)i, st), "flush");
         CU_TRY(cudaEventRecord(op->evs[2 * i], st), "event");

@@ -84,6 +84,7 @@ def prt_tiles(sample: Sequence[int], n_pdims: int = 2, p_levels: int = 3, r_leve
 # P UMMA atom | R UMMA k-steps | P instruction tile.  Slots below are the
 # free choices of that sketch.
 TC_SLOTS = {
+    "cluster_m": [1, 2],          # parallelize: 1 CTA (tile_m 128) or a CTA pair (tile_m 256)
     "tile_n": [64, 128, 192, 256],
     "tile_k": [64, 128],
     "stages": [2, 3, 4, 5, 6, 7, 8],
@@ -126,12 +127,16 @@ class GpuStrategy:
             return dict(engine=XTC_ENGINE_TCGEN05, tile_m=128, swizzle=128)
         return dict(engine=XTC_ENGINE_SIMT)
 
+    def _kw(self, names, values) -> Dict[str, int]:
+        kw = self._base()
+        kw.update({n: int(v) for n, v in zip(names, values)})
+        if self.engine == XTC_ENGINE_TCGEN05:
+            kw["tile_m"] = 128 * max(1, kw.get("cluster_m", 1))    # UMMA M = 128 per CTA
+        return kw
+
     def generate(self, sample: Sequence[int]) -> xtc_schedule:
         """Sample (flat vector in slot order) -> schedule (the planner input)."""
-        kw = self._base()
-        for (name, _), v in zip(self.slots.items(), sample):
-            kw[name] = int(v)
-        return schedule(**kw)
+        return schedule(**self._kw(list(self.slots), sample))
 
     def _divisible(self, kw) -> bool:
         if not self.exact_divisors:
@@ -148,8 +153,7 @@ class GpuStrategy:
             names = list(self.slots)
             legal = []
             for combo in itertools.product(*(self.slots[n] for n in names)):
-                kw = self._base()
-                kw.update(zip(names, combo))
+                kw = self._kw(names, combo)
                 if not self._divisible(kw):
                     continue
                 st, _, _ = xtc_schedule_check(self.desc, schedule(**kw), self.num_sms)
