@@ -311,7 +311,7 @@ def main_xtc(args):
     if rank == 0 and world == 1 and not args.no_extras:
         try:
             from paper_2512_16512_b200.bench_extras import run_extras
-            extras = run_extras(xtc, torch, dev, peak_tf)
+            extras.update(run_extras(xtc, torch, dev, peak_tf))
         except Exception as ex:   # extras are secondary: report, don't fail the headline
             extras = {"error": repr(ex)}
 
