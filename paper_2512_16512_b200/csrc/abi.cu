@@ -158,6 +158,10 @@ struct xtc_op_s {
     // 1 = perturb one output, 2 = leave one output unwritten (NaN), 3 = drop a 32x32 block (zeros)
     int fault = 0;
     int64_t fault_row = 0, fault_col = 0;
+    // device trace (XTC_TRACE=path): per-launch %globaltimer stamps of the first CTAs,
+    // appended to `path` as one JSON line per tcgen05 launch (synchronises; diagnostics only)
+    std::string trace_path;
+    uint64_t* trace_dev = nullptr;
 };
 
 static int dsize(int dt) { return dt == XTC_BF16 ? 2 : 4; }
@@ -176,6 +180,7 @@ static void release_op(xtc_op op) {
     if (op->blk_err) cudaFree(op->blk_err);
     if (op->blk_idx) cudaFree(op->blk_idx);
     if (op->counts) cudaFree(op->counts);
+    if (op->trace_dev) cudaFree(op->trace_dev);
     for (auto e : op->evs) cudaEventDestroy(e);
     cudaSetDevice(cur);
     delete op;
@@ -241,6 +246,7 @@ xtc_status xtc_op_create(const xtc_op_desc* desc, int32_t device, xtc_op* out) {
     op->d = *desc;
     op->device = device;
     op->num_sms = prop.multiProcessorCount;
+    if (const char* tp = getenv("XTC_TRACE")) op->trace_path = tp;
     if (const char* f = getenv("XTC_DEBUG_FAULT")) {
         op->fault = atoi(f);
         if (const char* at = getenv("XTC_DEBUG_FAULT_AT")) {
@@ -487,6 +493,12 @@ static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cud
         sp.num_tiles = p.num_tiles;
         sp.out_bf16 = out_bf16; sp.split_out = split_out; sp.atomic = p.atomic;
         sp.cg = conv_geom(d);
+        {
+            const int BM = sp.tile_m, BN = sp.tile_n, BK = sp.tile_k, pad = sp.pad;
+            const bool aligned = ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0;
+            sp.fast = (d.kind == XTC_OP_MATMUL) && aligned && sp.lda % 4 == 0 && sp.ldb % 4 == 0 && BK % 4 == 0 &&
+                      BN % 4 == 0 && pad % 4 == 0 && (BM + pad) % 4 == 0 && BM * (BK / 4) <= 4 * p.block;
+        }
         const int u = p.sch.unroll_k == 0 ? 1 : p.sch.unroll_k;
         const int vec = p.sch.vector_n == 0 ? 1 : p.sch.vector_n;
         CU_TRY(launch_simt_gemm(p.sch.inner_m, p.sch.inner_n, u, vec, sp, p.grid_x, p.block, p.smem, st), "simt_gemm launch");
@@ -521,9 +533,29 @@ static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cud
         tp.a_stage_bytes = (uint32_t)(128 * p.sch.tile_k * es);
         tp.b_stage_bytes = (uint32_t)(p.sch.tile_k * (p.sch.tile_n / p.cta_group) * es);
         tp.cg = conv_geom(d);
+        const size_t trace_bytes = (size_t)kTraceCtas * kTraceSlots * 8;
+        if (!op->trace_path.empty()) {
+            if (!op->trace_dev) CU_TRY(cudaMalloc(&op->trace_dev, trace_bytes), "trace alloc");
+            CU_TRY(cudaMemsetAsync(op->trace_dev, 0, trace_bytes, st), "trace clear");
+            tp.trace = op->trace_dev;
+        }
         CU_TRY(launch_tc_gemm(tf32, d.kind == XTC_OP_CONV2D, p.cta_group, op->tmA, op->tmB, op->tmC, tp, p.grid_x, p.smem, st),
                "tc_gemm launch");
         ++launches;
+        if (tp.trace) {
+            std::vector<uint64_t> h((size_t)kTraceCtas * kTraceSlots);
+            CU_TRY(cudaMemcpyAsync(h.data(), op->trace_dev, trace_bytes, cudaMemcpyDeviceToHost, st), "trace D2H");
+            CU_TRY(cudaStreamSynchronize(st), "trace sync");
+            if (FILE* f = fopen(op->trace_path.c_str(), "a")) {
+                fprintf(f, "{\"M\":%lld,\"N\":%lld,\"K\":%lld,\"tile_n\":%d,\"tile_k\":%d,\"stages\":%d,\"cta_group\":%d,"
+                           "\"grid\":%d,\"num_tiles\":%lld,\"kb_per_split\":%d,\"slots\":%d,\"kK\":%d,\"kT\":%d,\"t\":[",
+                        (long long)p.M, (long long)p.N, (long long)p.K, p.sch.tile_n, p.sch.tile_k, p.sch.stages,
+                        p.cta_group, p.grid_x, (long long)p.num_tiles, p.kb_per_split, kTraceSlots, kTraceK, kTraceTiles);
+                for (size_t i = 0; i < h.size(); ++i) fprintf(f, "%s%llu", i ? "," : "", (unsigned long long)h[i]);
+                fprintf(f, "]}\n");
+                fclose(f);
+            }
+        }
     }
     if (split_out) {
         CU_TRY(launch_splitk_reduce(op->ws, p.split_k, p.M, p.N, p.ws_ld, C, ldc, out_bf16, st), "splitk_reduce");

@@ -93,6 +93,131 @@ __global__ void __launch_bounds__(simt_max_threads(TM, TN)) simt_gemm_kernel(con
             }
         };
 
+        auto compute = [&](const float* As, const float* Bs) {
+            for (int kk = 0; kk < BK; kk += U) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    float a[TM], b[TN];
+                    const float* ar = As + (kk + u) * lda_s + ty * TM;
+                    if constexpr (TM % 4 == 0) {
+                        if (p.fast) {                       // lda_s % 4 == 0: 16-byte A fragment reads
+#pragma unroll
+                            for (int i = 0; i < TM / 4; ++i) {
+                                const float4 v4 = *reinterpret_cast<const float4*>(ar + 4 * i);
+                                a[4 * i] = v4.x; a[4 * i + 1] = v4.y; a[4 * i + 2] = v4.z; a[4 * i + 3] = v4.w;
+                            }
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < TM; ++i) a[i] = ar[i];
+                        }
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < TM; ++i) a[i] = ar[i];
+                    }
+                    const float* br = Bs + (kk + u) * ldb_s;
+                    if constexpr (VEC == 4) {
+#pragma unroll
+                        for (int j = 0; j < TN / 4; ++j) {
+                            const float4 v4 = *reinterpret_cast<const float4*>(br + tx * TN + 4 * j);
+                            b[4 * j] = v4.x; b[4 * j + 1] = v4.y; b[4 * j + 2] = v4.z; b[4 * j + 3] = v4.w;
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < TN; ++j) b[j] = br[tx + j * tx_n];
+                    }
+#pragma unroll
+                    for (int i = 0; i < TM; ++i)
+#pragma unroll
+                        for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+                }
+            }
+        };
+
+        if (p.fast) {
+            // Vectorised pack (aligned matmul): B k-rows by 16-byte cp.async (partial vectors
+            // zero-filled via src-size), A by 16-byte register loads along K transposed into
+            // As[k][m]; the next k-tile is fetched while the current one is computed.
+            const float* Ag = static_cast<const float*>(p.A);
+            const int vra = BK / 4, vrb = BN / 4;
+            float4 ra[4];
+            auto load_a_regs = [&](int kt) {
+                const int64_t k0 = k_begin + (int64_t)kt * BK;
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const int v = tid + r * nthr;
+                    ra[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (v < BM * vra) {
+                        const int i = v / vra, kq = v - i * vra;
+                        const int64_t m = m0 + i, k = k0 + 4 * kq;
+                        if (m < p.M) {
+                            const float* src = Ag + m * p.lda + k;
+                            if (k + 3 < k_end) ra[r] = *reinterpret_cast<const float4*>(src);
+                            else {
+                                if (k < k_end) ra[r].x = src[0];
+                                if (k + 1 < k_end) ra[r].y = src[1];
+                                if (k + 2 < k_end) ra[r].z = src[2];
+                            }
+                        }
+                    }
+                }
+            };
+            auto store_a_regs = [&](float* As) {
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const int v = tid + r * nthr;
+                    if (v < BM * vra) {
+                        const int i = v / vra, kq = v - i * vra;
+                        float* d = As + (4 * kq) * lda_s + i;
+                        d[0] = ra[r].x; d[lda_s] = ra[r].y; d[2 * lda_s] = ra[r].z; d[3 * lda_s] = ra[r].w;
+                    }
+                }
+            };
+            auto load_b_async = [&](int kt, float* Bs) {
+                const int64_t k0 = k_begin + (int64_t)kt * BK;
+                for (int v = tid; v < BK * vrb; v += nthr) {
+                    const int kk = v / vrb, jq = v - kk * vrb;
+                    const int64_t k = k0 + kk, n = n0 + 4 * jq;
+                    int bytes = 0;
+                    if (k < k_end && n < p.N) bytes = (int)(p.N - n >= 4 ? 16 : 4 * (p.N - n));
+                    const float* src = bytes ? Bg + k * p.ldb + n : Bg;
+                    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(Bs + kk * ldb_s + 4 * jq));
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(bytes) : "memory");
+                }
+            };
+            if (nk > 0) {
+                load_b_async(0, sm + a_sz);
+                cp_async_commit();
+                load_a_regs(0);
+                store_a_regs(sm);
+                cp_async_wait<0>();
+                __syncthreads();
+            }
+            for (int kt = 0; kt < nk; ++kt) {
+                const int cur = (p.stages == 2) ? (kt & 1) : 0;
+                float* As = sm + cur * (a_sz + b_sz);
+                const bool more = kt + 1 < nk;
+                if (p.stages == 2 && more) {
+                    float* An = sm + (cur ^ 1) * (a_sz + b_sz);
+                    load_b_async(kt + 1, An + a_sz);
+                    cp_async_commit();
+                    load_a_regs(kt + 1);
+                    compute(As, As + a_sz);
+                    store_a_regs(An);
+                    cp_async_wait<0>();
+                } else {
+                    compute(As, As + a_sz);
+                    if (more) {                           // single buffer: refill after everyone is done
+                        __syncthreads();
+                        load_b_async(kt + 1, As + a_sz);
+                        cp_async_commit();
+                        load_a_regs(kt + 1);
+                        store_a_regs(As);
+                        cp_async_wait<0>();
+                    }
+                }
+                __syncthreads();
+            }
+        } else {
         if (p.stages == 2 && nk > 0) { load_tile(0, sm, sm + a_sz, true); cp_async_commit(); }
         for (int kt = 0; kt < nk; ++kt) {
             float* As;
@@ -115,31 +240,9 @@ __global__ void __launch_bounds__(simt_max_threads(TM, TN)) simt_gemm_kernel(con
                 load_tile(kt, As, Bs, false);
             }
             __syncthreads();
-            for (int kk = 0; kk < BK; kk += U) {
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    float a[TM], b[TN];
-                    const float* ar = As + (kk + u) * lda_s + ty * TM;
-#pragma unroll
-                    for (int i = 0; i < TM; ++i) a[i] = ar[i];
-                    const float* br = Bs + (kk + u) * ldb_s;
-                    if constexpr (VEC == 4) {
-#pragma unroll
-                        for (int j = 0; j < TN / 4; ++j) {
-                            const float4 v4 = *reinterpret_cast<const float4*>(br + tx * TN + 4 * j);
-                            b[4 * j] = v4.x; b[4 * j + 1] = v4.y; b[4 * j + 2] = v4.z; b[4 * j + 3] = v4.w;
-                        }
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < TN; ++j) b[j] = br[tx + j * tx_n];
-                    }
-#pragma unroll
-                    for (int i = 0; i < TM; ++i)
-#pragma unroll
-                        for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
-                }
-            }
+            compute(As, Bs);
             __syncthreads();
+        }
         }
 
 #pragma unroll

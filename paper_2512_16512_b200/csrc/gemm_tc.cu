@@ -55,6 +55,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
+    if (p.trace && blockIdx.x < kTraceCtas && threadIdx.x == 0)
+        p.trace[(size_t)blockIdx.x * kTraceSlots] = ptx::globaltimer();
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const uint32_t rank = (CG == 2) ? ptx::cluster_ctarank() : 0u;
@@ -80,6 +82,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    uint64_t* const trace = (p.trace && blockIdx.x < kTraceCtas) ? p.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
+    if (trace && threadIdx.x == 0) trace[1] = ptx::globaltimer();
+    int trace_k = 0;       // per-role counters (each role only touches its own slots)
 
     if (warp == 0) {
         // ===================== TMA producer (pack) =====================
@@ -107,6 +112,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 }
                 for (int kb = kb0; kb < kb1; ++kb) {
                     ptx::mbar_wait(&empty[s], ph ^ 1);
+                    if (trace && lane == 0 && trace_k < kTraceK) trace[8 + trace_k++] = ptx::globaltimer();
                     if (!ptx::elect_one()) {           // one lane issues; the warp stays converged
                         if (++s == S) { s = 0; ph ^= 1; }
                         continue;
@@ -177,6 +183,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 const uint32_t d_tmem = tmem_base + (uint32_t)(acc * p.tile_n);
                 for (int kb = kb0; kb < kb1; ++kb) {
                     ptx::mbar_wait(&full[s], ph);
+                    if (trace && lane == 0 && trace_k < kTraceK) trace[8 + kTraceK + trace_k++] = ptx::globaltimer();
                     ptx::tc_fence_after();
                     if (ptx::elect_one()) {
                         const uint64_t ad = adesc0 + (uint64_t)(s * a_stage16);
@@ -215,6 +222,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             const int m0 = mb * TILE_M + 128 * (int)rank, n0 = nb * p.tile_n;
             const int64_t row = (int64_t)m0 + 32 * q + lane;
             ptx::mbar_wait(&tfull[acc], aph);
+            if (trace && warp == 4 && lane == 0 && trace_k < kTraceTiles) trace[8 + 2 * kTraceK + 2 * trace_k] = ptx::globaltimer();
             ptx::tc_fence_after();
             const uint32_t t_row = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * p.tile_n);
             for (int c = 0; c < p.tile_n; c += 32) {
@@ -307,6 +315,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             }
             ptx::tc_fence_before();
             __syncwarp();
+            if (trace && warp == 4 && lane == 0 && trace_k < kTraceTiles) trace[8 + 2 * kTraceK + 2 * trace_k++ + 1] = ptx::globaltimer();
             if (lane == 0) {                           // TMEM buffer free for the next tile
                 if constexpr (CG == 2) ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&tempty[acc]), 0));
                 else ptx::mbar_arrive(&tempty[acc]);

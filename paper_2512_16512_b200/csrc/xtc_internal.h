@@ -105,6 +105,7 @@ struct SimtParams {
     TileMap tm;
     int64_t num_tiles;
     int32_t out_bf16, split_out, atomic;
+    int32_t fast;        // aligned matmul: 16-byte vectorised pack + float4 A fragments
     ConvGeom cg;
 };
 
@@ -121,6 +122,14 @@ struct TcParams {
     uint32_t tmem_cols;
     uint32_t a_stage_bytes, b_stage_bytes;
     ConvGeom cg;
+    // Diagnostics (XTC_TRACE): %globaltimer stamps for CTAs < kTraceCtas, laid out
+    // [cta][kTraceSlots]: slot 0 kernel entry, 1 setup done; producer issue of k-block i at
+    // 8+i, MMA full-wait done at 8+kTraceK+i, epilogue tile j start/end at 8+2kTraceK+2j(+1).
+    uint64_t* trace;
 };
+constexpr int kTraceCtas = 4;
+constexpr int kTraceK = 96;
+constexpr int kTraceTiles = 16;
+constexpr int kTraceSlots = 8 + 2 * kTraceK + 2 * kTraceTiles;
 
 }  // namespace xtc
