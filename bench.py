@@ -201,10 +201,19 @@ def main_xtc(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # XTC_BENCH_DIST=gloo-shared: single-GPU rehearsal of the multi-rank path (all ranks
+    # on device 0, gloo collectives through host copies); never used for reported numbers
+    rehearsal = os.environ.get("XTC_BENCH_DIST", "") == "gloo-shared"
+    if rehearsal:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if rehearsal:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+    from paper_2512_16512_b200.parallel import gather_rows
     peaks, peak_kind = load_peaks()
     peak_tf = float(peaks.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"]))
 
@@ -231,7 +240,7 @@ def main_xtc(args):
     def step():
         op.run(a, b, c, stream=sp)
         if world > 1:
-            dist.all_gather_into_tensor(full_c, c)
+            gather_rows(c, M, out=full_c)
 
     for _ in range(args.warmup):
         step()
@@ -251,7 +260,7 @@ def main_xtc(args):
             op.run(a, b, c, stream=sp)
             kev[i][1].record(stream)
             if world > 1:
-                dist.all_gather_into_tensor(full_c, c)
+                gather_rows(c, M, out=full_c)
             evs[i][1].record(stream)
         t_end.record(stream)
         torch.cuda.synchronize(dev)
@@ -282,7 +291,7 @@ def main_xtc(args):
         b.copy_(h_b, non_blocking=True)
         op.run(a, b, c, stream=sp)
         if world > 1:
-            dist.all_gather_into_tensor(full_c, c)
+            gather_rows(c, M, out=full_c)
             h_c.copy_(full_c, non_blocking=True)
         else:
             h_c.copy_(c, non_blocking=True)

@@ -113,10 +113,10 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 for (int kb = kb0; kb < kb1; ++kb) {
                     ptx::mbar_wait(&empty[s], ph ^ 1);
                     if (trace && lane == 0 && trace_k < kTraceK) trace[8 + trace_k++] = ptx::globaltimer();
-                    if (!ptx::elect_one()) {           // one lane issues; the warp stays converged
-                        if (++s == S) { s = 0; ph ^= 1; }
-                        continue;
-                    }
+                    // One lane issues while the other 31 wait at __syncwarp below: letting them
+                    // run ahead into the next try_wait would suspend the warp (divergent paths
+                    // of a warp are serialised) and throttle the issuing lane.
+                    if (ptx::elect_one()) {
                     uint32_t bar_c = 0;
                     if constexpr (CG == 2) {
                         if (rank == 0) ptx::mbar_arrive_expect_tx(&full[s], 2 * stage_bytes);
@@ -149,6 +149,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                         if constexpr (CG == 2) ptx::tma_load_2d_pair(&tmB, dst, bar_c, n0 + b * ATOM, kb * p.tile_k);
                         else ptx::tma_load_2d(&tmB, dst, &full[s], n0 + b * ATOM, kb * p.tile_k);
                     }
+                    }   // elected lane
+                    __syncwarp();
                     if (++s == S) { s = 0; ph ^= 1; }
                 }
             }

@@ -63,21 +63,35 @@ def unpack_gathered(gathered: torch.Tensor, n: int) -> List[dict]:
     return out
 
 
+def _all_gather(out: torch.Tensor, local: torch.Tensor, group=None) -> None:
+    """all_gather_into_tensor; NCCL gathers device tensors in place over NVLink.  The
+    gloo backend (CPU tests, or the single-GPU rehearsal of the multi-rank bench)
+    gathers through host copies."""
+    import torch.distributed as dist
+    if dist.get_backend(group) == "gloo" and local.is_cuda:
+        host = torch.empty(out.shape, dtype=out.dtype)
+        dist.all_gather_into_tensor(host, local.cpu(), group=group)
+        out.copy_(host)
+    else:
+        dist.all_gather_into_tensor(out, local, group=group)
+
+
 def gather_records(local: torch.Tensor, group=None) -> torch.Tensor:
     """All-gather the per-rank record blocks (NCCL on GPU tensors, gloo on CPU)."""
     import torch.distributed as dist
     world = dist.get_world_size(group)
     out = torch.empty((world * local.shape[0], local.shape[1]), dtype=local.dtype, device=local.device)
-    dist.all_gather_into_tensor(out, local, group=group)
+    _all_gather(out, local, group)
     return out
 
 
-def gather_rows(c_shard: torch.Tensor, m_total: int, group=None) -> torch.Tensor:
+def gather_rows(c_shard: torch.Tensor, m_total: int, group=None, out: torch.Tensor = None) -> torch.Tensor:
     """Assemble C from equal row shards (M-sharded GEMM, config 5)."""
     import torch.distributed as dist
     world = dist.get_world_size(group)
     if m_total % world:
         raise ValueError("all_gather_into_tensor needs equal shards: M % world must be 0")
-    out = torch.empty((m_total,) + tuple(c_shard.shape[1:]), dtype=c_shard.dtype, device=c_shard.device)
-    dist.all_gather_into_tensor(out, c_shard.contiguous(), group=group)
+    if out is None:
+        out = torch.empty((m_total,) + tuple(c_shard.shape[1:]), dtype=c_shard.dtype, device=c_shard.device)
+    _all_gather(out, c_shard.contiguous(), group)
     return out

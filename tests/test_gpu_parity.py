@@ -255,3 +255,23 @@ def test_sweep_records_and_illegal_candidates():
     assert [r.status for r in recs] == [0, xtc.XTC_E_ILLEGAL_SCHEDULE, 0, xtc.XTC_E_ILLEGAL_SCHEDULE]
     assert recs[0].valid == 1 and recs[2].valid == 1 and recs[1].valid == -1
     assert recs[0].tflops_med > 0 and recs[0].t_min_ns <= recs[0].t_med_ns <= recs[0].t_max_ns
+
+
+# ------------------------------------------- multi-rank bench rehearsal --
+def test_bench_two_rank_rehearsal_on_one_gpu(tmp_path):
+    """The N>1 bench path (M-sharded GEMM + all-gather + sharded sweep + max-over-ranks
+    timing) run end to end with 2 ranks sharing one GPU over gloo."""
+    import json, os, subprocess, sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, XTC_BENCH_DIST="gloo-shared")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(root, "bench.py"), "--gpus", "2",
+           "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--sweep-candidates", "32"]
+    out = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    rec = json.loads(lines[0])
+    assert rec["n_gpus"] == 2 and rec["validation"]["valid"] == 1 and rec["value"] > 0
+    sw = rec["extras"]["sweep_1024_bf16_sharded"]
+    assert sw["ranks"] == 2 and sw["candidates"] == 32 and sw["valid"] + sw["invalid"] == 32
