@@ -89,7 +89,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     if (warp == 0) {
         // ===================== TMA producer (pack) =====================
         {
-            int s = 0;
+            int s = 0, filled = 0;
             uint32_t ph = 0;
             const uint32_t stage_bytes = p.a_stage_bytes + p.b_stage_bytes;
             const int n_a = p.tile_k / ATOM;
@@ -111,7 +111,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                     wq = qq * p.cg.sw - p.cg.pw;
                 }
                 for (int kb = kb0; kb < kb1; ++kb) {
-                    ptx::mbar_wait(&empty[s], ph ^ 1);
+                    if (filled < S) ++filled;                  // the first S slots start free
+                    else ptx::mbar_wait(&empty[s], ph ^ 1);
                     if (trace && lane == 0 && trace_k < kTraceK) trace[8 + trace_k++] = ptx::globaltimer();
                     // One lane issues while the other 31 wait at __syncwarp below: letting them
                     // run ahead into the next try_wait would suspend the warp (divergent paths
