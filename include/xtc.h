@@ -112,6 +112,8 @@ typedef enum { XTC_SPLITK_ORDERED = 0, XTC_SPLITK_ATOMIC = 1 } xtc_splitk_mode;
  * pack         stages                 : SMEM ring depth (SIMT 1|2, tcgen05 2..8)
  *                          swizzle                : tcgen05: 128 (TMA/UMMA 128-byte swizzle);
  *                                                   SIMT: SMEM row padding in floats (0..8)
+ *                          pack_warps             : tcgen05: warps issuing the TMA copies (1..3; 0 = 1);
+ *                                                   warp w owns every pack_warps-th k-block of the ring
  * bufferize    buffer_c               : 1 = SMEM-staged output + TMA store, 0 = direct stores
  *                          acc_buffers            : tcgen05 TMEM accumulator buffers (1|2) */
 typedef struct {
@@ -127,7 +129,8 @@ typedef struct {
     int32_t cluster_m;
     int32_t persistent;
     int32_t split_n_at;
-    int32_t reserved[5];
+    int32_t pack_warps;
+    int32_t reserved[4];
 } xtc_schedule;
 
 /* What the planner derived for a legal schedule (for reports and tests). */

@@ -86,11 +86,14 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     if (trace && threadIdx.x == 0) trace[1] = ptx::globaltimer();
     int trace_k = 0;       // per-role counters (each role only touches its own slots)
 
-    if (warp == 0) {
-        // ===================== TMA producer (pack) =====================
+    if (warp == 0 || ((warp == 2 || warp == 3) && warp - 1 < p.pack_warps)) {
+        // ===================== TMA producer(s) (pack) =====================
+        // pack_warps producers (warps 0, 2, 3) share the ring: the g-th k-block of this
+        // CTA's tile sequence uses slot g % S and is issued by producer g % pack_warps.
         {
-            int s = 0, filled = 0;
-            uint32_t ph = 0;
+            const int pw = warp == 0 ? 0 : warp - 1;
+            const int P = p.pack_warps;
+            int64_t g = 0;
             const uint32_t stage_bytes = p.a_stage_bytes + p.b_stage_bytes;
             const int n_a = p.tile_k / ATOM;
             const int n_b = bn_cta / ATOM;
@@ -111,9 +114,14 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                     wq = qq * p.cg.sw - p.cg.pw;
                 }
                 for (int kb = kb0; kb < kb1; ++kb) {
-                    if (filled < S) ++filled;                  // the first S slots start free
-                    else ptx::mbar_wait(&empty[s], ph ^ 1);
-                    if (trace && lane == 0 && trace_k < kTraceK) trace[8 + trace_k++] = ptx::globaltimer();
+                    const int s = (int)(g % S);
+                    const int64_t use = g / S;                 // how many times slot s was filled before
+                    const bool mine = (g % P) == pw;
+                    trace_k = g < kTraceK ? (int)g : kTraceK;
+                    ++g;
+                    if (!mine) continue;                       // warp-uniform
+                    if (use > 0) ptx::mbar_wait(&empty[s], (uint32_t)((use & 1) ^ 1));   // first fill: slot free
+                    if (trace && lane == 0 && trace_k < kTraceK) trace[8 + trace_k] = ptx::globaltimer();
                     // One lane issues while the other 31 wait at __syncwarp below: letting them
                     // run ahead into the next try_wait would suspend the warp (divergent paths
                     // of a warp are serialised) and throttle the issuing lane.
@@ -152,7 +160,6 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                     }
                     }   // elected lane
                     __syncwarp();
-                    if (++s == S) { s = 0; ph ^= 1; }
                 }
             }
         }

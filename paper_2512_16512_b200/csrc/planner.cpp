@@ -88,6 +88,7 @@ static xtc_status plan_simt(const xtc_op_desc& d, const xtc_schedule& s, int num
     if (s.buffer_c != 0) ILLEGAL("SIMT engine: buffer_c must be 0 (the register tile is the write buffer)");
     if (s.acc_buffers > 1) ILLEGAL("SIMT engine: acc_buffers must be 0 or 1");
     if (s.cluster_m > 1) ILLEGAL("SIMT engine: cluster_m must be 1");
+    if (s.pack_warps > 1) ILLEGAL("SIMT engine: pack_warps must be 0 or 1 (all threads pack)");
     if (V == 4 && (s.tile_n + s.swizzle) % 4) ILLEGAL("vectorize: vector_n 4 needs (tile_n + pad) %% 4 == 0 for aligned float4");
     auto r4 = [](int x) { return (x + 3) / 4 * 4; };
     int smem = st * (r4(s.tile_k * (s.tile_m + s.swizzle)) + r4(s.tile_k * (s.tile_n + s.swizzle))) * 4;
@@ -124,6 +125,7 @@ static xtc_status plan_tc(const xtc_op_desc& d, const xtc_schedule& s, int num_s
     if (s.tile_k < p.atom_k || s.tile_k > 256 || s.tile_k % p.atom_k)
         ILLEGAL("tcgen05 tile_k must be a multiple of %d in [%d,256] (128-byte swizzle atom)", p.atom_k, p.atom_k);
     if (s.unroll_k > 1) ILLEGAL("tcgen05 unroll_k must be 0 or 1 (the k-steps of a stage are always fully unrolled)");
+    if (s.pack_warps < 0 || s.pack_warps > 3) ILLEGAL("pack: pack_warps (TMA-issuing warps) must be in [0,3]");
     if (s.vector_n > 1) ILLEGAL("tcgen05 vector_n must be 0 (the UMMA atom is the vector unit)");
     if (s.stages < 2 || s.stages > 8) ILLEGAL("tcgen05 stages must be in [2,8]");
     if (s.swizzle != 0 && s.swizzle != 128) ILLEGAL("tcgen05 swizzle must be 128 (0 = default 128)");
@@ -206,7 +208,7 @@ xtc_status make_plan(const xtc_op_desc& d, const xtc_schedule& s, int num_sms, P
         p.tail_grid_y = (int)cdiv(M, 16);
         if (d.in_dtype != XTC_F32 && d.in_dtype != XTC_BF16 && d.in_dtype != XTC_TF32) ILLEGAL("bad dtype");
     }
-    for (int i = 0; i < 5; ++i)
+    for (int i = 0; i < 4; ++i)
         if (s.reserved[i]) ILLEGAL("reserved schedule fields must be 0");
     if (s.engine == XTC_ENGINE_SIMT) st = plan_simt(d, s, num_sms, p, why);
     else if (s.engine == XTC_ENGINE_TCGEN05) st = plan_tc(d, s, num_sms, p, why);

@@ -116,6 +116,7 @@ struct TcParams {
     TileMap tm;
     int64_t num_tiles;
     int32_t acc_buffers, buffer_c, atomic, out_bf16, split_out;
+    int32_t pack_warps;      // 1..3 TMA-issuing warps (warps 0, 2, 3)
     int64_t ldc, ws_ld;
     void* C; float* Wk;
     uint32_t idesc;

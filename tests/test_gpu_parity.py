@@ -275,3 +275,14 @@ def test_bench_two_rank_rehearsal_on_one_gpu(tmp_path):
     assert rec["n_gpus"] == 2 and rec["validation"]["valid"] == 1 and rec["value"] > 0
     sw = rec["extras"]["sweep_1024_bf16_sharded"]
     assert sw["ranks"] == 2 and sw["candidates"] == 32 and sw["valid"] + sw["invalid"] == 32
+
+
+@pytest.mark.parametrize("pw", [2, 3])
+def test_tc_pack_warps(pw):
+    """pack with 2-3 TMA-issuing warps (k-blocks dealt round-robin over the ring)."""
+    run_matmul(256, 512, 640, "bf16", "bf16", tc(tile_n=128, stages=5, pack_warps=pw, persistent=1, acc_buffers=2),
+               MODE_INT)
+    run_matmul(512, 512, 384, "bf16", "bf16", tc(tile_m=256, cluster_m=2, tile_n=256, tile_k=128, stages=3,
+                                                 pack_warps=pw, persistent=1, acc_buffers=2), MODE_INT)
+    d = xtc.conv2d_desc(2, 56, 56, 64, 64, 3, 3, 1, 1, "bf16", "bf16")
+    run_conv(d, "bf16", "bf16", tc(tile_n=64, stages=8, pack_warps=pw, persistent=1, acc_buffers=2), MODE_INT)

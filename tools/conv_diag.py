@@ -23,16 +23,17 @@ def bench(desc, shapes, sch, reps=30):
 
 TC = dict(engine=1, tile_m=128, tile_k=64, swizzle=128, buffer_c=1)
 P2 = dict(TC, tile_m=256, cluster_m=2)
-for name, (B, H, C, F) in {"L56": (32, 56, 64, 64), "L14": (32, 14, 256, 256)}.items():
-    d = xtc.conv2d_desc(B, H, H, C, F)
-    M, N, K = xtc.gemm_view(d)
-    dm = xtc.matmul_desc(M, N, K, "bf16", "bf16")
-    scheds = [dict(TC, tile_n=min(F, 256), stages=8 if F == 64 else 4, acc_buffers=2, persistent=1, raster_group=8),
-              dict(TC, tile_n=min(F, 256), stages=6, acc_buffers=2, persistent=0),
-              dict(TC, tile_n=min(F, 256), tile_k=128, stages=4 if F == 64 else 2, acc_buffers=2, persistent=1)]
-    if F >= 128:
-        scheds += [dict(P2, tile_n=256, tile_k=128, stages=3, acc_buffers=2, persistent=1, split_k=s) for s in (1, 2, 3)]
-        scheds += [dict(TC, tile_n=256, stages=4, acc_buffers=1, split_k=3), dict(TC, tile_n=128, stages=6, acc_buffers=2, split_k=2, persistent=1)]
-    for s in scheds:
-        print(json.dumps({"layer": name, "sch": {k: v for k, v in s.items() if k not in ("engine", "swizzle")},
-                          "conv": bench(d, [(B, H, H, C), (3, 3, C, F)], s), "gemm_same_shape": bench(dm, [(M, K), (K, N)], s)}), flush=True)
+if __name__ == "__main__":
+  for name, (B, H, C, F) in {"L56": (32, 56, 64, 64), "L14": (32, 14, 256, 256)}.items():
+      d = xtc.conv2d_desc(B, H, H, C, F)
+      M, N, K = xtc.gemm_view(d)
+      dm = xtc.matmul_desc(M, N, K, "bf16", "bf16")
+      scheds = [dict(TC, tile_n=min(F, 256), stages=8 if F == 64 else 4, acc_buffers=2, persistent=1, raster_group=8),
+                dict(TC, tile_n=min(F, 256), stages=6, acc_buffers=2, persistent=0),
+                dict(TC, tile_n=min(F, 256), tile_k=128, stages=4 if F == 64 else 2, acc_buffers=2, persistent=1)]
+      if F >= 128:
+          scheds += [dict(P2, tile_n=256, tile_k=128, stages=3, acc_buffers=2, persistent=1, split_k=s) for s in (1, 2, 3)]
+          scheds += [dict(TC, tile_n=256, stages=4, acc_buffers=1, split_k=3), dict(TC, tile_n=128, stages=6, acc_buffers=2, split_k=2, persistent=1)]
+      for s in scheds:
+          print(json.dumps({"layer": name, "sch": {k: v for k, v in s.items() if k not in ("engine", "swizzle")},
+                            "conv": bench(d, [(B, H, H, C), (3, 3, C, F)], s), "gemm_same_shape": bench(dm, [(M, K), (K, N)], s)}), flush=True)
