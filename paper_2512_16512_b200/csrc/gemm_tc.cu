@@ -93,7 +93,10 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         {
             const int pw = warp == 0 ? 0 : warp - 1;
             const int P = p.pack_warps;
-            int64_t g = 0;
+            int g = 0;                    // k-blocks seen (trace index)
+            int s = 0, rr = 0;            // slot g % S, producer g % P (incremental: no divisions)
+            uint32_t use_par = 0;         // parity of (g / S)
+            bool first_round = true;      // g < S: slot never filled before
             const uint32_t stage_bytes = p.a_stage_bytes + p.b_stage_bytes;
             const int n_a = p.tile_k / ATOM;
             const int n_b = bn_cta / ATOM;
@@ -114,27 +117,30 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                     wq = qq * p.cg.sw - p.cg.pw;
                 }
                 for (int kb = kb0; kb < kb1; ++kb) {
-                    const int s = (int)(g % S);
-                    const int64_t use = g / S;                 // how many times slot s was filled before
-                    const bool mine = (g % P) == pw;
-                    trace_k = g < kTraceK ? (int)g : kTraceK;
+                    const int cs = s;
+                    const uint32_t cpar = use_par;
+                    const bool mine = rr == pw, fresh = first_round;
+                    trace_k = g < kTraceK ? g : kTraceK;
                     ++g;
+                    if (++rr == P) rr = 0;
+                    if (++s == S) { s = 0; use_par ^= 1u; first_round = false; }
                     if (!mine) continue;                       // warp-uniform
-                    if (use > 0) ptx::mbar_wait(&empty[s], (uint32_t)((use & 1) ^ 1));   // first fill: slot free
+                    if (!fresh) ptx::mbar_wait(&empty[cs], cpar ^ 1u);   // first fill: the slot is free
                     if (trace && lane == 0 && trace_k < kTraceK) trace[8 + trace_k] = ptx::globaltimer();
                     // One lane issues while the other 31 wait at __syncwarp below: letting them
                     // run ahead into the next try_wait would suspend the warp (divergent paths
                     // of a warp are serialised) and throttle the issuing lane.
                     if (ptx::elect_one()) {
                     uint32_t bar_c = 0;
+                    uint64_t* const fb = &full[cs];
                     if constexpr (CG == 2) {
-                        if (rank == 0) ptx::mbar_arrive_expect_tx(&full[s], 2 * stage_bytes);
-                        bar_c = ptx::mapa_shared(ptx::smem_u32(&full[s]), 0);
+                        if (rank == 0) ptx::mbar_arrive_expect_tx(fb, 2 * stage_bytes);
+                        bar_c = ptx::mapa_shared(ptx::smem_u32(fb), 0);
                     } else {
-                        ptx::mbar_arrive_expect_tx(&full[s], stage_bytes);
+                        ptx::mbar_arrive_expect_tx(fb, stage_bytes);
                     }
-                    uint8_t* a_dst = sA + (size_t)s * p.a_stage_bytes;
-                    uint8_t* b_dst = sB + (size_t)s * p.b_stage_bytes;
+                    uint8_t* a_dst = sA + (size_t)cs * p.a_stage_bytes;
+                    uint8_t* b_dst = sB + (size_t)cs * p.b_stage_bytes;
                     for (int a = 0; a < n_a; ++a) {
                         const int kc = kb * p.tile_k + a * ATOM;
                         if constexpr (CONV) {
@@ -146,17 +152,17 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                                 ptx::tma_load_im2col_4d_pair(&tmA, a_dst + a * A_ATOM_BYTES, bar_c, c, wq, hp, nimg,
                                                              (uint16_t)sx, (uint16_t)r);
                             else
-                                ptx::tma_load_im2col_4d(&tmA, a_dst + a * A_ATOM_BYTES, &full[s], c, wq, hp, nimg,
+                                ptx::tma_load_im2col_4d(&tmA, a_dst + a * A_ATOM_BYTES, fb, c, wq, hp, nimg,
                                                         (uint16_t)sx, (uint16_t)r);
                         } else {
                             if constexpr (CG == 2) ptx::tma_load_2d_pair(&tmA, a_dst + a * A_ATOM_BYTES, bar_c, kc, m0);
-                            else ptx::tma_load_2d(&tmA, a_dst + a * A_ATOM_BYTES, &full[s], kc, m0);
+                            else ptx::tma_load_2d(&tmA, a_dst + a * A_ATOM_BYTES, fb, kc, m0);
                         }
                     }
                     for (int b = 0; b < n_b; ++b) {
                         uint8_t* dst = b_dst + (size_t)b * p.tile_k * 128;
                         if constexpr (CG == 2) ptx::tma_load_2d_pair(&tmB, dst, bar_c, n0 + b * ATOM, kb * p.tile_k);
-                        else ptx::tma_load_2d(&tmB, dst, &full[s], n0 + b * ATOM, kb * p.tile_k);
+                        else ptx::tma_load_2d(&tmB, dst, fb, n0 + b * ATOM, kb * p.tile_k);
                     }
                     }   // elected lane
                     __syncwarp();
