@@ -45,21 +45,25 @@ struct TileMap {
     int32_t tiles_m, tiles_n, split_k, order, group;
 };
 
-XTC_HD void tile_coords(const TileMap& t, int64_t id, int& mb, int& nb, int& ks) {
-    int64_t per = (int64_t)t.tiles_m * t.tiles_n;
-    ks = (int)(id / per);
-    int64_t r = id - (int64_t)ks * per;
-    int outer_n = (t.order == XTC_ORDER_MN) ? t.tiles_m : t.tiles_n;   // extent of outer loop
-    int inner_n = (t.order == XTC_ORDER_MN) ? t.tiles_n : t.tiles_m;
-    int G = t.group < 1 ? 1 : t.group;
-    int64_t strip = (int64_t)G * inner_n;
-    int g = (int)(r / strip);
-    int64_t w = r - (int64_t)g * strip;
-    int rows = outer_n - g * G;
+// 32-bit unsigned arithmetic: the planner caps the tile count below 2^31, and 64-bit
+// integer division is a long software sequence on the GPU (every role calls this per tile).
+XTC_HD void tile_coords(const TileMap& t, int64_t id64, int& mb, int& nb, int& ks) {
+    const uint32_t id = (uint32_t)id64;
+    const uint32_t per = (uint32_t)t.tiles_m * (uint32_t)t.tiles_n;
+    const uint32_t k = id / per;
+    const uint32_t r = id - k * per;
+    const uint32_t outer_n = (t.order == XTC_ORDER_MN) ? t.tiles_m : t.tiles_n;   // extent of outer loop
+    const uint32_t inner_n = (t.order == XTC_ORDER_MN) ? t.tiles_n : t.tiles_m;
+    const uint32_t G = t.group < 1 ? 1u : (uint32_t)t.group;
+    const uint32_t strip = G * inner_n;
+    const uint32_t g = r / strip;
+    const uint32_t w = r - g * strip;
+    uint32_t rows = outer_n - g * G;
     if (rows > G) rows = G;
-    int inner = (int)(w / rows);
-    int outer = g * G + (int)(w - (int64_t)inner * rows);
-    if (t.order == XTC_ORDER_MN) { mb = outer; nb = inner; } else { nb = outer; mb = inner; }
+    const uint32_t inner = w / rows;
+    const uint32_t outer = g * G + (w - inner * rows);
+    ks = (int)k;
+    if (t.order == XTC_ORDER_MN) { mb = (int)outer; nb = (int)inner; } else { nb = (int)outer; mb = (int)inner; }
 }
 
 // ------------------------------------------------------------------ plans --
