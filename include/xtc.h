@@ -114,6 +114,9 @@ typedef enum { XTC_SPLITK_ORDERED = 0, XTC_SPLITK_ATOMIC = 1 } xtc_splitk_mode;
  *                                                   SIMT: SMEM row padding in floats (0..8)
  *                          pack_warps             : tcgen05: warps issuing the TMA copies (1..3; 0 = 1);
  *                                                   warp w owns every pack_warps-th k-block of the ring
+ *                          b_resident             : tcgen05: 1 = pack all of B once per CTA at the outermost
+ *                                                   loop (needs a single N tile and split_k 1); the ring
+ *                                                   then streams A only
  * bufferize    buffer_c               : 1 = SMEM-staged output + TMA store, 0 = direct stores
  *                          acc_buffers            : tcgen05 TMEM accumulator buffers (1|2) */
 typedef struct {
@@ -130,7 +133,8 @@ typedef struct {
     int32_t persistent;
     int32_t split_n_at;
     int32_t pack_warps;
-    int32_t reserved[4];
+    int32_t b_resident;
+    int32_t reserved[3];
 } xtc_schedule;
 
 /* What the planner derived for a legal schedule (for reports and tests). */

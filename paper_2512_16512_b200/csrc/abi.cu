@@ -517,6 +517,7 @@ static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cud
         tp.num_tiles = p.num_tiles;
         tp.acc_buffers = p.sch.acc_buffers == 0 ? 1 : p.sch.acc_buffers;
         tp.pack_warps = p.sch.pack_warps == 0 ? 1 : p.sch.pack_warps;
+        tp.b_resident = p.sch.b_resident;
         tp.buffer_c = p.sch.buffer_c;
         tp.atomic = p.atomic;
         tp.out_bf16 = out_bf16;

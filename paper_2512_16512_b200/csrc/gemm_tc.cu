@@ -46,14 +46,18 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const uint32_t pad = (1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u;
     uint8_t* smem = smem_raw + pad;
     const int S = p.stages;
-    uint8_t* sA = smem;
+    // [resident B (b_resident only)][A ring][B ring (unless resident)][epilogue staging][barriers]
+    const bool b_res = p.b_resident != 0;
+    uint8_t* sBres = smem;
+    uint8_t* sA = smem + (b_res ? (size_t)p.kb_total * p.b_stage_bytes : 0);
     uint8_t* sB = sA + (size_t)S * p.a_stage_bytes;
-    uint8_t* sC = sB + (size_t)S * p.b_stage_bytes;
+    uint8_t* sC = sB + (b_res ? 0 : (size_t)S * p.b_stage_bytes);
     uint64_t* full = reinterpret_cast<uint64_t*>(sC + (p.buffer_c ? kTcEpiSmem : 0));
     uint64_t* empty = full + 8;
     uint64_t* tfull = empty + 8;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* bfull = tempty + 2;            // resident B landed
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
 
     if (p.trace && blockIdx.x < kTraceCtas && threadIdx.x == 0)
         p.trace[(size_t)blockIdx.x * kTraceSlots] = ptx::globaltimer();
@@ -72,6 +76,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     if (warp == 1 && lane == 0) {
         for (int s = 0; s < S; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
         for (int a = 0; a < 2; ++a) { ptx::mbar_init(&tfull[a], 1); ptx::mbar_init(&tempty[a], 4 * CG); }
+        ptx::mbar_init(bfull, 1);
         ptx::fence_mbarrier_init();
     }
     if (warp == 2) {
@@ -97,9 +102,30 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             int s = 0, rr = 0;            // slot g % S, producer g % P (incremental: no divisions)
             uint32_t use_par = 0;         // parity of (g / S)
             bool first_round = true;      // g < S: slot never filled before
-            const uint32_t stage_bytes = p.a_stage_bytes + p.b_stage_bytes;
+            const uint32_t stage_bytes = p.a_stage_bytes + (b_res ? 0u : p.b_stage_bytes);
             const int n_a = p.tile_k / ATOM;
             const int n_b = bn_cta / ATOM;
+            if (b_res && pw == 0) {
+                // pack B once: every k-block of this CTA's B columns (single N tile, split_k 1)
+                if (ptx::elect_one()) {
+                    const uint32_t all = (uint32_t)p.kb_total * p.b_stage_bytes;
+                    uint32_t bar_c = 0;
+                    if constexpr (CG == 2) {
+                        if (rank == 0) ptx::mbar_arrive_expect_tx(bfull, 2 * all);
+                        bar_c = ptx::mapa_shared(ptx::smem_u32(bfull), 0);
+                    } else {
+                        ptx::mbar_arrive_expect_tx(bfull, all);
+                    }
+                    const int nc = bn_cta * (int)rank;
+                    for (int kb = 0; kb < p.kb_total; ++kb)
+                        for (int b = 0; b < n_b; ++b) {
+                            uint8_t* dst = sBres + (size_t)kb * p.b_stage_bytes + (size_t)b * p.tile_k * 128;
+                            if constexpr (CG == 2) ptx::tma_load_2d_pair(&tmB, dst, bar_c, nc + b * ATOM, kb * p.tile_k);
+                            else ptx::tma_load_2d(&tmB, dst, bfull, nc + b * ATOM, kb * p.tile_k);
+                        }
+                }
+                __syncwarp();
+            }
             for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters) {
                 int mb, nb, ks;
                 tile_coords(p.tm, t, mb, nb, ks);
@@ -159,7 +185,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                             else ptx::tma_load_2d(&tmA, a_dst + a * A_ATOM_BYTES, fb, kc, m0);
                         }
                     }
-                    for (int b = 0; b < n_b; ++b) {
+                    for (int b = 0; b < (b_res ? 0 : n_b); ++b) {
                         uint8_t* dst = b_dst + (size_t)b * p.tile_k * 128;
                         if constexpr (CG == 2) ptx::tma_load_2d_pair(&tmB, dst, bar_c, n0 + b * ATOM, kb * p.tile_k);
                         else ptx::tma_load_2d(&tmB, dst, fb, n0 + b * ATOM, kb * p.tile_k);
@@ -186,9 +212,11 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             const uint64_t adesc0 = ptx::smem_desc_sw128(ptx::smem_u32(sA), 16, 1024);
             // B is MN-major: LBO = stride between 128-byte N blocks, SBO = stride between
             // K-row groups (8 rows of 128 B for SW128; 4 rows for tf32's SW128_BASE32B)
-            const uint64_t bdesc0 = TF32 ? ptx::smem_desc_sw128(ptx::smem_u32(sB), b_lbo, 512, 1)
-                                         : ptx::smem_desc_sw128(ptx::smem_u32(sB), b_lbo, 1024, 2);
+            uint8_t* const b_base_ptr = b_res ? sBres : sB;
+            const uint64_t bdesc0 = TF32 ? ptx::smem_desc_sw128(ptx::smem_u32(b_base_ptr), b_lbo, 512, 1)
+                                         : ptx::smem_desc_sw128(ptx::smem_u32(b_base_ptr), b_lbo, 1024, 2);
             const uint32_t a_stage16 = p.a_stage_bytes >> 4, b_stage16 = p.b_stage_bytes >> 4;
+            if (b_res) ptx::mbar_wait(bfull, 0);     // resident B has landed (in both CTAs for a pair)
             for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters) {
                 int mb, nb, ks;
                 tile_coords(p.tm, t, mb, nb, ks);
@@ -203,7 +231,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                     ptx::tc_fence_after();
                     if (ptx::elect_one()) {
                         const uint64_t ad = adesc0 + (uint64_t)(s * a_stage16);
-                        const uint64_t bd = bdesc0 + (uint64_t)(s * b_stage16);
+                        const uint64_t bd = bdesc0 + (uint64_t)((b_res ? kb : s) * b_stage16);
                         for (int a = 0; a < n_a; ++a) {
 #pragma unroll
                             for (int kk = 0; kk < ATOM / UMMA_K; ++kk) {

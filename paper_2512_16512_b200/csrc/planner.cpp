@@ -89,6 +89,7 @@ static xtc_status plan_simt(const xtc_op_desc& d, const xtc_schedule& s, int num
     if (s.acc_buffers > 1) ILLEGAL("SIMT engine: acc_buffers must be 0 or 1");
     if (s.cluster_m > 1) ILLEGAL("SIMT engine: cluster_m must be 1");
     if (s.pack_warps > 1) ILLEGAL("SIMT engine: pack_warps must be 0 or 1 (all threads pack)");
+    if (s.b_resident) ILLEGAL("SIMT engine: b_resident must be 0");
     if (V == 4 && (s.tile_n + s.swizzle) % 4) ILLEGAL("vectorize: vector_n 4 needs (tile_n + pad) %% 4 == 0 for aligned float4");
     auto r4 = [](int x) { return (x + 3) / 4 * 4; };
     int smem = st * (r4(s.tile_k * (s.tile_m + s.swizzle)) + r4(s.tile_k * (s.tile_n + s.swizzle))) * 4;
@@ -138,9 +139,24 @@ static xtc_status plan_tc(const xtc_op_desc& d, const xtc_schedule& s, int num_s
     p.tmem_cols = alloc;
     int a_stage = 128 * s.tile_k * es;
     int b_stage = s.tile_k * bn_cta * es;
-    int smem = s.stages * (a_stage + b_stage) + (s.buffer_c ? kTcEpiSmem : 0) + kSmemReserve;
-    if (smem > kSmemMaxOptin) ILLEGAL("pack: %d stages x %d B + epilogue = %d B SMEM exceeds %d B",
-                                      s.stages, a_stage + b_stage, smem, kSmemMaxOptin);
+    int smem = 0;
+    if (s.b_resident) {
+        // pack B once per CTA (outermost loop level): all k-blocks of B stay in SMEM
+        if (s.b_resident != 1) ILLEGAL("b_resident must be 0 or 1");
+        if (cdiv(p.N, s.tile_n) != 1) ILLEGAL("pack: b_resident needs a single N tile (N <= tile_n)");
+        if (p.split_k != 1) ILLEGAL("pack: b_resident needs split_k 1");
+        const int64_t kbt = cdiv(p.K, s.tile_k);
+        const int64_t b_all = kbt * b_stage;
+        const int64_t tot = b_all + (int64_t)s.stages * a_stage + (s.buffer_c ? kTcEpiSmem : 0) + kSmemReserve;
+        if (tot > kSmemMaxOptin)
+            ILLEGAL("pack: resident B (%lld B) + %d A stages + epilogue = %lld B SMEM exceeds %d B", (long long)b_all,
+                    s.stages, (long long)tot, kSmemMaxOptin);
+        smem = (int)tot;
+    } else {
+        smem = s.stages * (a_stage + b_stage) + (s.buffer_c ? kTcEpiSmem : 0) + kSmemReserve;
+        if (smem > kSmemMaxOptin) ILLEGAL("pack: %d stages x %d B + epilogue = %d B SMEM exceeds %d B",
+                                          s.stages, a_stage + b_stage, smem, kSmemMaxOptin);
+    }
     p.smem = smem;
     // TMA pitch / alignment rules (cuda.h cuTensorMapEncodeTiled: strides % 16 B)
     int os = dtype_size(d.out_dtype);
@@ -208,7 +224,7 @@ xtc_status make_plan(const xtc_op_desc& d, const xtc_schedule& s, int num_sms, P
         p.tail_grid_y = (int)cdiv(M, 16);
         if (d.in_dtype != XTC_F32 && d.in_dtype != XTC_BF16 && d.in_dtype != XTC_TF32) ILLEGAL("bad dtype");
     }
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 3; ++i)
         if (s.reserved[i]) ILLEGAL("reserved schedule fields must be 0");
     if (s.engine == XTC_ENGINE_SIMT) st = plan_simt(d, s, num_sms, p, why);
     else if (s.engine == XTC_ENGINE_TCGEN05) st = plan_tc(d, s, num_sms, p, why);

@@ -121,6 +121,7 @@ struct TcParams {
     int64_t num_tiles;
     int32_t acc_buffers, buffer_c, atomic, out_bf16, split_out;
     int32_t pack_warps;      // 1..3 TMA-issuing warps (warps 0, 2, 3)
+    int32_t b_resident;      // all of B packed once per CTA (kb_total x b_stage_bytes before the A ring)
     int64_t ldc, ws_ld;
     void* C; float* Wk;
     uint32_t idesc;

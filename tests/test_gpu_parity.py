@@ -286,3 +286,16 @@ def test_tc_pack_warps(pw):
                                                  pack_warps=pw, persistent=1, acc_buffers=2), MODE_INT)
     d = xtc.conv2d_desc(2, 56, 56, 64, 64, 3, 3, 1, 1, "bf16", "bf16")
     run_conv(d, "bf16", "bf16", tc(tile_n=64, stages=8, pack_warps=pw, persistent=1, acc_buffers=2), MODE_INT)
+
+
+def test_tc_b_resident():
+    """pack of B at the outermost loop level (whole B resident in SMEM, ring streams A)."""
+    run_matmul(512, 64, 576, "bf16", "bf16", tc(tile_n=64, stages=6, b_resident=1, persistent=1, acc_buffers=2,
+                                                pack_warps=2), MODE_INT)
+    run_matmul(640, 256, 256, "bf16", "f32", tc(tile_m=256, cluster_m=2, tile_n=256, stages=3, b_resident=1,
+                                                persistent=1, acc_buffers=2), MODE_INT)
+    d = xtc.conv2d_desc(2, 56, 56, 64, 64, 3, 3, 1, 1, "bf16", "bf16")
+    run_conv(d, "bf16", "bf16", tc(tile_n=64, stages=7, b_resident=1, persistent=1, acc_buffers=2, pack_warps=3),
+             MODE_INT)
+    run_conv(d, "bf16", "bf16", tc(tile_n=64, stages=7, b_resident=1, persistent=1, acc_buffers=2, pack_warps=3),
+             MODE_UNIFORM)
