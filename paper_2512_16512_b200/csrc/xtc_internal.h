@@ -133,7 +133,7 @@ struct TcParams {
     // 8+i, MMA full-wait done at 8+kTraceK+i, epilogue tile j start/end at 8+2kTraceK+2j(+1).
     uint64_t* trace;
 };
-constexpr int kTraceCtas = 4;
+constexpr int kTraceCtas = 160;          // >= #SMs: the whole persistent grid
 constexpr int kTraceK = 96;
 constexpr int kTraceTiles = 16;
 constexpr int kTraceSlots = 8 + 2 * kTraceK + 2 * kTraceTiles;
