@@ -299,3 +299,57 @@ def test_tc_b_resident():
              MODE_INT)
     run_conv(d, "bf16", "bf16", tc(tile_n=64, stages=7, b_resident=1, persistent=1, acc_buffers=2, pack_warps=3),
              MODE_UNIFORM)
+
+
+# --------------------------------------------------- schedule invariance --
+def _invariance(desc, in_dtype, out_dtype, cands, seed=5):
+    M, N, K = xtc.gemm_view(desc)
+    a = dev_tensor((M, K), in_dtype, seed, MODE_INT)
+    b = dev_tensor((K, N), in_dtype, seed + 1, MODE_INT)
+    c = torch.empty((M, N), dtype=TORCH_DT[out_dtype], device="cuda:0")
+    op = xtc.Op(desc)
+    recs = op.sweep(cands, a, b, c, xtc.measure_cfg(warmup=0, repeats=1, validate=1, exact=1))
+    bad = [(i, r.status, r.valid, r.n_mismatch, r.n_nan) for i, r in enumerate(recs)
+           if r.status != 0 or r.valid != 1 or r.n_mismatch != 0]
+    assert not bad, bad[:5]
+    # the on-chip reference itself equals the oracle: check the last candidate's output
+    O, D = oracle_matmul(M, N, K, in_dtype, MODE_INT, seed, seed + 1)
+    check_against_oracle(c, O, D, out_dtype, True, 0.0)
+    return len(recs)
+
+
+def test_schedule_invariance_tcgen05_sampled():
+    """BASELINE north_star: every legal schedule gives bit-identical results on
+    small-integer inputs.  128 draws from the legal tcgen05 design space (both CTA
+    shapes, split-K, raster orders, epilogue modes, persistence) plus pack_warps /
+    b_resident variants."""
+    from paper_2512_16512_b200.strategy import GpuStrategy
+    desc = xtc.matmul_desc(512, 512, 512, "bf16", "bf16")
+    st = GpuStrategy(desc, exact_divisors=False)
+    cands = [st.generate(s) for s in st.sample(128, seed=11)]
+    extra = []
+    for i, c in enumerate(cands[:32]):
+        d = c.as_dict()
+        d["pack_warps"] = 1 + i % 3
+        extra.append(xtc.schedule(**d))
+    n = _invariance(desc, "bf16", "bf16", cands + extra)
+    assert n == 160
+
+
+def test_schedule_invariance_simt_sampled():
+    from paper_2512_16512_b200.strategy import GpuStrategy
+    desc = xtc.matmul_desc(200, 136, 328, "f32", "f32")
+    st = GpuStrategy(desc, engine=xtc.XTC_ENGINE_SIMT, exact_divisors=False)
+    cands = [st.generate(s) for s in st.sample(96, seed=12)]
+    assert _invariance(desc, "f32", "f32", cands) == 96
+
+
+@pytest.mark.parametrize("mnk", [(130, 130, 131), (96, 132, 100), (64, 64, 4)])
+def test_simt_fast_and_generic_pack_paths(mnk):
+    """Aligned shapes take the vectorised pack (16-byte loads, partial vectors zero-filled);
+    odd pitches fall back to the scalar pack.  Both must be exact."""
+    M, N, K = mnk
+    for stages in (1, 2):
+        sch = S(engine=0, tile_m=64, tile_n=64, tile_k=16, inner_m=4, inner_n=4, unroll_k=4, vector_n=4,
+                stages=stages, swizzle=4)
+        run_matmul(M, N, K, "f32", "f32", sch, MODE_INT)
