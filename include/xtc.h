@@ -74,12 +74,18 @@ typedef enum { XTC_F32 = 0, XTC_BF16 = 1, XTC_TF32 = 2 } xtc_dtype;
  *            p < P = (h + 2 pad_h - r)/stride_h + 1, q < Q likewise.
  *            Implicit GEMM view: M = batch*P*Q, N = f, K = r*s*c (c fastest).
  * in_dtype: F32 (SIMT engine, fp32 FFMA), TF32 or BF16 (tcgen05 engine).
- * out_dtype: F32 or BF16 (RNE). */
+ * out_dtype: F32 or BF16 (RNE).
+ * consumer: elementwise consumer op applied to the result (the paper's graph
+ *   matmul -> relu, Fig.9): XTC_CONSUMER_NONE or XTC_CONSUMER_RELU
+ *   (out = max(result, 0), rounded once to out_dtype).  Whether it runs fused
+ *   into the contraction's epilogue or as its own pass is the schedule's
+ *   `fuse` knob. */
+typedef enum { XTC_CONSUMER_NONE = 0, XTC_CONSUMER_RELU = 1 } xtc_consumer;
 typedef struct {
     int32_t kind;       /* xtc_op_kind */
     int32_t in_dtype;   /* xtc_dtype   */
     int32_t out_dtype;  /* xtc_dtype: XTC_F32 or XTC_BF16 */
-    int32_t reserved0;
+    int32_t consumer;   /* xtc_consumer */
     int64_t m, n, k, lda, ldb, ldc;                         /* matmul */
     int64_t batch, h, w, c, f, r, s;                        /* conv2d */
     int64_t stride_h, stride_w, pad_h, pad_w;               /* conv2d */
@@ -118,7 +124,10 @@ typedef enum { XTC_SPLITK_ORDERED = 0, XTC_SPLITK_ATOMIC = 1 } xtc_splitk_mode;
  *                                                   loop (needs a single N tile and split_k 1); the ring
  *                                                   then streams A only
  * bufferize    buffer_c               : 1 = SMEM-staged output + TMA store, 0 = direct stores
- *                          acc_buffers            : tcgen05 TMEM accumulator buffers (1|2) */
+ *                          acc_buffers            : tcgen05 TMEM accumulator buffers (1|2)
+ * fuse         fuse                   : 1 = the op's consumer (relu) is applied in the producer's
+ *                                                   epilogue (or in the split-K reduction); 0 = it runs as a
+ *                                                   separate elementwise pass over the output */
 typedef struct {
     int32_t engine;
     int32_t tile_m, tile_n, tile_k;
@@ -134,7 +143,8 @@ typedef struct {
     int32_t split_n_at;
     int32_t pack_warps;
     int32_t b_resident;
-    int32_t reserved[3];
+    int32_t fuse;
+    int32_t reserved[2];
 } xtc_schedule;
 
 /* What the planner derived for a legal schedule (for reports and tests). */

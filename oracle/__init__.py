@@ -103,6 +103,13 @@ def conv2d(x: np.ndarray, w: np.ndarray, stride=(1, 1), pad=(0, 0)):
     return y, D
 
 
+def relu(O: np.ndarray) -> np.ndarray:
+    """The relu consumer op of the paper's graphs (Fig.9 matmul -> relu):
+    elementwise max(x, 0) on the fp64 result, applied before round_out.
+    Pinned by SPEC S:63: relu([-1, 0, 2]) = [0, 0, 2]."""
+    return np.maximum(np.asarray(O, dtype=np.float64), 0.0)
+
+
 def round_out(O: np.ndarray, out_dtype: str) -> np.ndarray:
     """round_out of SURVEY.md §8(c): fp32 output -> float32(O) (RN);
     bf16 output -> RNE to bf16, returned as uint16 bit patterns.

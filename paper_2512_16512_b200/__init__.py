@@ -28,12 +28,14 @@ XTC_F32, XTC_BF16, XTC_TF32 = 0, 1, 2
 XTC_ENGINE_SIMT, XTC_ENGINE_TCGEN05 = 0, 1
 XTC_ORDER_MN, XTC_ORDER_NM = 0, 1
 XTC_SPLITK_ORDERED, XTC_SPLITK_ATOMIC = 0, 1
+XTC_CONSUMER_NONE, XTC_CONSUMER_RELU = 0, 1
 DTYPES = {"f32": XTC_F32, "bf16": XTC_BF16, "tf32": XTC_TF32}
+CONSUMERS = {None: XTC_CONSUMER_NONE, "none": XTC_CONSUMER_NONE, "relu": XTC_CONSUMER_RELU}
 
 
 # ------------------------------------------------------------- structs -----
 class xtc_op_desc(Structure):
-    _fields_ = [("kind", c_int32), ("in_dtype", c_int32), ("out_dtype", c_int32), ("reserved0", c_int32),
+    _fields_ = [("kind", c_int32), ("in_dtype", c_int32), ("out_dtype", c_int32), ("consumer", c_int32),
                 ("m", c_int64), ("n", c_int64), ("k", c_int64), ("lda", c_int64), ("ldb", c_int64), ("ldc", c_int64),
                 ("batch", c_int64), ("h", c_int64), ("w", c_int64), ("c", c_int64), ("f", c_int64),
                 ("r", c_int64), ("s", c_int64),
@@ -42,11 +44,11 @@ class xtc_op_desc(Structure):
 
 SCHEDULE_FIELDS = ["engine", "tile_m", "tile_n", "tile_k", "inner_m", "inner_n", "order", "raster_group",
                    "unroll_k", "vector_n", "stages", "swizzle", "buffer_c", "acc_buffers", "split_k",
-                   "split_k_mode", "cluster_m", "persistent", "split_n_at", "pack_warps", "b_resident"]
+                   "split_k_mode", "cluster_m", "persistent", "split_n_at", "pack_warps", "b_resident", "fuse"]
 
 
 class xtc_schedule(Structure):
-    _fields_ = [(f, c_int32) for f in SCHEDULE_FIELDS] + [("reserved", c_int32 * 3)]
+    _fields_ = [(f, c_int32) for f in SCHEDULE_FIELDS] + [("reserved", c_int32 * 2)]
 
     def as_dict(self):
         return {f: int(getattr(self, f)) for f in SCHEDULE_FIELDS}
@@ -211,20 +213,23 @@ def xtc_last_launch_count(op) -> int:
 
 
 # ------------------------------------------------------------ helpers ------
-def matmul_desc(m, n, k, in_dtype="bf16", out_dtype="bf16", lda=0, ldb=0, ldc=0) -> xtc_op_desc:
+def matmul_desc(m, n, k, in_dtype="bf16", out_dtype="bf16", lda=0, ldb=0, ldc=0, consumer=None) -> xtc_op_desc:
     d = xtc_op_desc()
     d.kind = XTC_OP_MATMUL
     d.in_dtype = DTYPES[in_dtype]
     d.out_dtype = DTYPES[out_dtype]
+    d.consumer = CONSUMERS[consumer]
     d.m, d.n, d.k, d.lda, d.ldb, d.ldc = m, n, k, lda, ldb, ldc
     return d
 
 
-def conv2d_desc(batch, h, w, c, f, r=3, s=3, stride=1, pad=1, in_dtype="bf16", out_dtype="bf16") -> xtc_op_desc:
+def conv2d_desc(batch, h, w, c, f, r=3, s=3, stride=1, pad=1, in_dtype="bf16", out_dtype="bf16",
+                consumer=None) -> xtc_op_desc:
     d = xtc_op_desc()
     d.kind = XTC_OP_CONV2D
     d.in_dtype = DTYPES[in_dtype]
     d.out_dtype = DTYPES[out_dtype]
+    d.consumer = CONSUMERS[consumer]
     d.batch, d.h, d.w, d.c, d.f, d.r, d.s = batch, h, w, c, f, r, s
     d.stride_h = d.stride_w = stride
     d.pad_h = d.pad_w = pad

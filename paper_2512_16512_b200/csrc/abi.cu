@@ -24,17 +24,18 @@ cudaError_t launch_ref_gemm(const void* A, const void* B, int bf16, int64_t M, i
                             int64_t ldb, double* R, double* D, cudaStream_t st);
 cudaError_t launch_ref_conv(const void* x, const void* w, int bf16, const ConvGeom& g, int64_t Nb, int64_t F,
                             double* R, double* D, cudaStream_t st);
-cudaError_t launch_compare(const void* C, int out_bf16, int64_t M, int64_t N, int64_t ldc, const double* R,
+cudaError_t launch_compare(const void* C, int out_bf16, int relu, int64_t M, int64_t N, int64_t ldc, const double* R,
                            const double* D, double* blk_err, int64_t* blk_idx, void* counts, int blocks,
                            cudaStream_t st);
+cudaError_t launch_relu(void* C, int out_bf16, int64_t M, int64_t N, int64_t ldc, cudaStream_t st);
 cudaError_t launch_flush(void* buf, int64_t bytes, uint32_t salt, cudaStream_t st);
 cudaError_t launch_delay(uint64_t ns, cudaStream_t st);
 cudaError_t launch_fault(void* C, int out_bf16, int64_t M, int64_t N, int64_t ldc, int kind, int64_t row, int64_t col,
                          cudaStream_t st);
 cudaError_t launch_splitk_reduce(const float* W, int S, int64_t M, int64_t N, int64_t ws_ld, void* C, int64_t ldc,
-                                 int out_bf16, cudaStream_t st);
-cudaError_t launch_tail_gemm(const void* A, const void* B, int bf16_in, void* C, int out_bf16, int64_t M, int64_t n0,
-                             int64_t ntail, int64_t K, int64_t lda, int64_t ldb, int64_t ldc, int gx, int gy,
+                                 int out_bf16, int relu, cudaStream_t st);
+cudaError_t launch_tail_gemm(const void* A, const void* B, int bf16_in, void* C, int out_bf16, int relu, int64_t M,
+                             int64_t n0, int64_t ntail, int64_t K, int64_t lda, int64_t ldb, int64_t ldc, int gx, int gy,
                              cudaStream_t st);
 }  // namespace xtc
 
@@ -499,6 +500,7 @@ static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cud
             sp.fast = (d.kind == XTC_OP_MATMUL) && aligned && sp.lda % 4 == 0 && sp.ldb % 4 == 0 && BK % 4 == 0 &&
                       BN % 4 == 0 && pad % 4 == 0 && (BM + pad) % 4 == 0 && BM * (BK / 4) <= 4 * p.block;
         }
+        sp.relu = p.relu_epi;
         const int u = p.sch.unroll_k == 0 ? 1 : p.sch.unroll_k;
         const int vec = p.sch.vector_n == 0 ? 1 : p.sch.vector_n;
         CU_TRY(launch_simt_gemm(p.sch.inner_m, p.sch.inner_n, u, vec, sp, p.grid_x, p.block, p.smem, st), "simt_gemm launch");
@@ -518,6 +520,7 @@ static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cud
         tp.acc_buffers = p.sch.acc_buffers == 0 ? 1 : p.sch.acc_buffers;
         tp.pack_warps = p.sch.pack_warps == 0 ? 1 : p.sch.pack_warps;
         tp.b_resident = p.sch.b_resident;
+        tp.relu = p.relu_epi;
         tp.buffer_c = p.sch.buffer_c;
         tp.atomic = p.atomic;
         tp.out_bf16 = out_bf16;
@@ -560,15 +563,20 @@ static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cud
         }
     }
     if (split_out) {
-        CU_TRY(launch_splitk_reduce(op->ws, p.split_k, p.M, p.N, p.ws_ld, C, ldc, out_bf16, st), "splitk_reduce");
+        CU_TRY(launch_splitk_reduce(op->ws, p.split_k, p.M, p.N, p.ws_ld, C, ldc, out_bf16, p.relu_reduce, st),
+               "splitk_reduce");
         ++launches;
     }
     if (p.has_tail) {
         const int64_t lda = d.lda ? d.lda : d.k;
         const int64_t ldb = d.ldb ? d.ldb : d.n;
-        CU_TRY(launch_tail_gemm(A, B, d.in_dtype == XTC_BF16, C, out_bf16, p.M, p.tail_n0, p.tail_n, p.K, lda, ldb, ldc,
-                                p.tail_grid_x, p.tail_grid_y, st),
+        CU_TRY(launch_tail_gemm(A, B, d.in_dtype == XTC_BF16, C, out_bf16, p.relu_epi || p.relu_reduce, p.M, p.tail_n0,
+                                p.tail_n, p.K, lda, ldb, ldc, p.tail_grid_x, p.tail_grid_y, st),
                "tail_gemm");
+        ++launches;
+    }
+    if (p.relu_pass) {                       // fuse = 0: the consumer as its own pass
+        CU_TRY(launch_relu(C, out_bf16, p.M, p.n_total, ldc, st), "relu");
         ++launches;
     }
     if (op->fault) {
@@ -662,7 +670,8 @@ static xtc_status validate(xtc_op op, const void* A, const void* B, void* C, con
         }
     }
     CU_TRY(cudaMemsetAsync(op->counts, 0, 16, st), "memset counts");
-    CU_TRY(launch_compare(C, d.out_dtype == XTC_BF16, M, N, ldc, op->R, op->D, op->blk_err, op->blk_idx, op->counts,
+    CU_TRY(launch_compare(C, d.out_dtype == XTC_BF16, d.consumer == XTC_CONSUMER_RELU, M, N, ldc, op->R, op->D,
+                          op->blk_err, op->blk_idx, op->counts,
                           kCmpBlocks, st),
            "compare");
     std::vector<double> be(kCmpBlocks);

@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(simt_max_threads(TM, TN)) simt_gemm_kernel(con
             for (int j = 0; j < TN; ++j) {
                 const int64_t col = n0 + (VEC == 4 ? tx * TN + j : tx + j * tx_n);
                 if (col >= p.N) continue;
-                const float v = acc[i][j];
+                const float v = p.relu ? fmaxf(acc[i][j], 0.f) : acc[i][j];   // fused consumer
                 if (p.split_out) p.Wk[((int64_t)ks * p.M + row) * p.ws_ld + col] = v;
                 else if (p.atomic) atomicAdd(static_cast<float*>(p.C) + row * p.ldc + col, v);
                 else if (p.out_bf16) static_cast<__nv_bfloat16*>(p.C)[row * p.ldc + col] = __float2bfloat16_rn(v);

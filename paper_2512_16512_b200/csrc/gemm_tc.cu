@@ -273,6 +273,10 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 uint32_t v[32];
                 ptx::tmem_ld_32x32b_x32(t_row + c, v);
                 ptx::tmem_ld_wait();
+                if (p.relu) {                      // fused consumer: relu before rounding
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(fmaxf(__uint_as_float(v[j]), 0.f));
+                }
                 if (p.buffer_c) {
                     // stage one 128-byte row per thread (swizzled), then one TMA store per warp
                     const bool first_half = !bf16_out || ((c & 63) == 0);

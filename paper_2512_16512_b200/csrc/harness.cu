@@ -133,15 +133,16 @@ struct CmpOut {
     unsigned long long n_mismatch, n_nan;
 };
 
-__global__ void compare_kernel(const void* C, int out_bf16, int64_t M, int64_t N, int64_t ldc, const double* R,
-                               const double* D, double* blk_err, int64_t* blk_idx, CmpOut* out) {
+__global__ void compare_kernel(const void* C, int out_bf16, int relu, int64_t M, int64_t N, int64_t ldc,
+                               const double* R, const double* D, double* blk_err, int64_t* blk_idx, CmpOut* out) {
     double best = -1.0;
     int64_t best_i = -1;
     unsigned long long mism = 0, nan = 0;
     const int64_t total = M * N;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t m = i / N, n = i - m * N;
-        const double r = R[i], d = D[i];
+        // the reference of the consumer op: relu(R); D stays the normaliser (|relu a - relu b| <= |a - b|)
+        const double r = relu ? fmax(R[i], 0.0) : R[i], d = D[i];
         double c;
         bool bits_ok;
         if (out_bf16) {
@@ -182,10 +183,35 @@ __global__ void compare_kernel(const void* C, int out_bf16, int64_t M, int64_t N
     if (nan) atomicAdd(&out->n_nan, nan);
 }
 
-cudaError_t launch_compare(const void* C, int out_bf16, int64_t M, int64_t N, int64_t ldc, const double* R,
+cudaError_t launch_compare(const void* C, int out_bf16, int relu, int64_t M, int64_t N, int64_t ldc, const double* R,
                            const double* D, double* blk_err, int64_t* blk_idx, void* counts, int blocks,
                            cudaStream_t st) {
-    compare_kernel<<<blocks, 256, 0, st>>>(C, out_bf16, M, N, ldc, R, D, blk_err, blk_idx, static_cast<CmpOut*>(counts));
+    compare_kernel<<<blocks, 256, 0, st>>>(C, out_bf16, relu, M, N, ldc, R, D, blk_err, blk_idx,
+                                           static_cast<CmpOut*>(counts));
+    return cudaGetLastError();
+}
+
+// --------------------------------------------- unfused consumer (fuse = 0) --
+// relu as its own elementwise pass over the output (the paper's separate graph op);
+// one read + one write of C.
+__global__ void relu_kernel(void* C, int out_bf16, int64_t M, int64_t N, int64_t ldc) {
+    const int64_t total = M * N;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t m = i / N, n = i - m * N;
+        if (out_bf16) {
+            __nv_bfloat16* p = static_cast<__nv_bfloat16*>(C) + m * ldc + n;
+            if (__bfloat162float(*p) < 0.f) *p = __float2bfloat16_rn(0.f);
+        } else {
+            float* p = static_cast<float*>(C) + m * ldc + n;
+            *p = fmaxf(*p, 0.f);
+        }
+    }
+}
+
+cudaError_t launch_relu(void* C, int out_bf16, int64_t M, int64_t N, int64_t ldc, cudaStream_t st) {
+    int64_t blocks = (M * N + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    relu_kernel<<<(int)blocks, 256, 0, st>>>(C, out_bf16, M, N, ldc);
     return cudaGetLastError();
 }
 
@@ -253,7 +279,7 @@ cudaError_t launch_flush(void* buf, int64_t bytes, uint32_t salt, cudaStream_t s
 
 // ----------------------------------------------------------- split-K reduce --
 __global__ void splitk_reduce_kernel(const float* __restrict__ W, int S, int64_t M, int64_t N, int64_t ws_ld,
-                                     void* C, int64_t ldc, int out_bf16) {
+                                     void* C, int64_t ldc, int out_bf16, int relu) {
     const int64_t groups_per_row = (N + 3) / 4;
     const int64_t total = M * groups_per_row;
     const int64_t plane = M * ws_ld;
@@ -266,7 +292,9 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ W, int S, int64_t
             const float4 v = *reinterpret_cast<const float4*>(W + s * plane + m * ws_ld + n);
             acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
         }
-        const float a[4] = {acc.x, acc.y, acc.z, acc.w};
+        float a[4] = {acc.x, acc.y, acc.z, acc.w};
+        if (relu)                                      // fused consumer on the complete sums
+            for (int j = 0; j < 4; ++j) a[j] = fmaxf(a[j], 0.f);
         const int cnt = (int)((N - n) < 4 ? (N - n) : 4);
         for (int j = 0; j < cnt; ++j) {
             if (out_bf16) static_cast<__nv_bfloat16*>(C)[m * ldc + n + j] = __float2bfloat16_rn(a[j]);
@@ -276,19 +304,20 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ W, int S, int64_t
 }
 
 cudaError_t launch_splitk_reduce(const float* W, int S, int64_t M, int64_t N, int64_t ws_ld, void* C, int64_t ldc,
-                                 int out_bf16, cudaStream_t st) {
+                                 int out_bf16, int relu, cudaStream_t st) {
     int64_t total = M * ((N + 3) / 4);
     int64_t blocks = (total + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
-    splitk_reduce_kernel<<<(int)blocks, 256, 0, st>>>(W, S, M, N, ws_ld, C, ldc, out_bf16);
+    splitk_reduce_kernel<<<(int)blocks, 256, 0, st>>>(W, S, M, N, ws_ld, C, ldc, out_bf16, relu);
     return cudaGetLastError();
 }
 
 // ---------------------------------------------- split_n_at remainder root --
 // The paper's scalar remainder loop (Fig.3 lines 33-35): one output
 // per thread, ascending k, fp32 FMA.
-__global__ void tail_gemm_kernel(const void* A, const void* B, int bf16_in, void* C, int out_bf16, int64_t M,
-                                 int64_t n0, int64_t ntail, int64_t K, int64_t lda, int64_t ldb, int64_t ldc) {
+__global__ void tail_gemm_kernel(const void* A, const void* B, int bf16_in, void* C, int out_bf16, int relu,
+                                 int64_t M, int64_t n0, int64_t ntail, int64_t K, int64_t lda, int64_t ldb,
+                                 int64_t ldc) {
     const int64_t j = (int64_t)blockIdx.x * 16 + (threadIdx.x & 15);
     const int64_t i = (int64_t)blockIdx.y * 16 + (threadIdx.x >> 4);
     if (i >= M || j >= ntail) return;
@@ -305,14 +334,15 @@ __global__ void tail_gemm_kernel(const void* A, const void* B, int bf16_in, void
         }
         s = fmaf(a, b, s);
     }
+    if (relu) s = fmaxf(s, 0.f);
     if (out_bf16) static_cast<__nv_bfloat16*>(C)[i * ldc + col] = __float2bfloat16_rn(s);
     else static_cast<float*>(C)[i * ldc + col] = s;
 }
 
-cudaError_t launch_tail_gemm(const void* A, const void* B, int bf16_in, void* C, int out_bf16, int64_t M, int64_t n0,
-                             int64_t ntail, int64_t K, int64_t lda, int64_t ldb, int64_t ldc, int gx, int gy,
+cudaError_t launch_tail_gemm(const void* A, const void* B, int bf16_in, void* C, int out_bf16, int relu, int64_t M,
+                             int64_t n0, int64_t ntail, int64_t K, int64_t lda, int64_t ldb, int64_t ldc, int gx, int gy,
                              cudaStream_t st) {
-    tail_gemm_kernel<<<dim3(gx, gy), 256, 0, st>>>(A, B, bf16_in, C, out_bf16, M, n0, ntail, K, lda, ldb, ldc);
+    tail_gemm_kernel<<<dim3(gx, gy), 256, 0, st>>>(A, B, bf16_in, C, out_bf16, relu, M, n0, ntail, K, lda, ldb, ldc);
     return cudaGetLastError();
 }
 

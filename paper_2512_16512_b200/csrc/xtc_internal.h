@@ -85,6 +85,9 @@ struct Plan {
     int64_t workspace_bytes = 0;
     bool atomic = false;
     // split_n_at remainder root (SIMT, fixed 16x16x16 1x1 tile)
+    // consumer (relu) placement: fused in the epilogue, fused in the split-K reduction,
+    // or a separate pass (fuse = 0)
+    bool relu_epi = false, relu_reduce = false, relu_pass = false;
     bool has_tail = false;
     int64_t tail_n0 = 0, tail_n = 0;
     int32_t tail_grid_x = 0, tail_grid_y = 0;
@@ -110,6 +113,7 @@ struct SimtParams {
     int64_t num_tiles;
     int32_t out_bf16, split_out, atomic;
     int32_t fast;        // aligned matmul: 16-byte vectorised pack + float4 A fragments
+    int32_t relu;        // fused consumer in the epilogue
     ConvGeom cg;
 };
 
@@ -122,6 +126,7 @@ struct TcParams {
     int32_t acc_buffers, buffer_c, atomic, out_bf16, split_out;
     int32_t pack_warps;      // 1..3 TMA-issuing warps (warps 0, 2, 3)
     int32_t b_resident;      // all of B packed once per CTA (kb_total x b_stage_bytes before the A ring)
+    int32_t relu;            // fused consumer in the epilogue
     int64_t ldc, ws_ld;
     void* C; float* Wk;
     uint32_t idesc;

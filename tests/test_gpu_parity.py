@@ -353,3 +353,53 @@ def test_simt_fast_and_generic_pack_paths(mnk):
         sch = S(engine=0, tile_m=64, tile_n=64, tile_k=16, inner_m=4, inner_n=4, unroll_k=4, vector_n=4,
                 stages=stages, swizzle=4)
         run_matmul(M, N, K, "f32", "f32", sch, MODE_INT)
+
+
+# ------------------------------------------------------- fuse (relu) --
+def run_matmul_relu(M, N, K, in_dtype, out_dtype, sch, mode, seed=21):
+    desc = xtc.matmul_desc(M, N, K, in_dtype, out_dtype, consumer="relu")
+    a = dev_tensor((M, K), in_dtype, seed, mode)
+    b = dev_tensor((K, N), in_dtype, seed + 1, mode)
+    c = torch.full((M, N), float("nan"), dtype=TORCH_DT[out_dtype], device="cuda:0")
+    op = xtc.Op(desc).apply(sch)
+    op.run(a, b, c)
+    torch.cuda.synchronize()
+    O, D = oracle_matmul(M, N, K, in_dtype, mode, seed, seed + 1)
+    exact = mode == MODE_INT
+    tol = 1e-5 if in_dtype == "f32" else 5e-3
+    import oracle as _o
+    check_against_oracle(c, _o.relu(O), D, out_dtype, exact, tol)
+    m = op.measure(a, b, c, xtc.measure_cfg(warmup=0, repeats=2, validate=1, exact=int(exact), tol=tol))
+    assert m.valid == 1, m.as_dict()
+    return op.launches()
+
+
+@pytest.mark.parametrize("fuse", [0, 1])
+def test_fuse_relu_tcgen05(fuse):
+    n1 = run_matmul_relu(256, 384, 320, "bf16", "bf16", tc(tile_n=128, fuse=fuse), MODE_INT)
+    assert n1 == (1 if fuse else 2)            # fused: one kernel; unfused: GEMM + relu pass
+    run_matmul_relu(256, 384, 320, "bf16", "f32", tc(tile_n=128, split_k=2, fuse=fuse), MODE_INT)
+    run_matmul_relu(512, 256, 256, "bf16", "bf16", tc(tile_m=256, cluster_m=2, tile_n=256, fuse=fuse, persistent=1,
+                                                      acc_buffers=2), MODE_UNIFORM)
+
+
+def test_fuse_relu_atomic_splitk_unfused_and_simt_and_tail():
+    run_matmul_relu(256, 256, 512, "bf16", "f32", tc(tile_n=128, split_k=4, split_k_mode=1, buffer_c=0, fuse=0),
+                    MODE_INT)
+    run_matmul_relu(200, 136, 328, "f32", "f32", S(engine=0, tile_m=32, tile_n=32, tile_k=8, inner_m=2, inner_n=2,
+                                                   fuse=1), MODE_INT)
+    run_matmul_relu(256, 258, 512, "f32", "f32", S(engine=0, tile_m=16, tile_n=128, tile_k=4, inner_m=1, inner_n=8,
+                                                   unroll_k=4, vector_n=4, split_n_at=256, fuse=1), MODE_INT)
+
+
+def test_fuse_relu_conv():
+    d = xtc.conv2d_desc(2, 14, 14, 64, 128, 3, 3, 1, 1, "bf16", "bf16", consumer="relu")
+    x = dev_tensor((2, 14, 14, 64), "bf16", 30, MODE_INT)
+    w = dev_tensor((3, 3, 64, 128), "bf16", 31, MODE_INT)
+    y = torch.empty((2 * 14 * 14, 128), dtype=torch.bfloat16, device="cuda:0")
+    op = xtc.Op(d).apply(tc(tile_n=128, fuse=1))
+    op.run(x, w, y)
+    torch.cuda.synchronize()
+    O, D = oracle_conv(d, "bf16", MODE_INT, 30, 31)
+    import oracle as _o
+    check_against_oracle(y, _o.relu(O), D, "bf16", True, 0.0)

@@ -201,3 +201,18 @@ def test_gpu_strategy_sampling_is_seeded_and_legal():
         s = st.generate(smp)
         code, _, why = xtc.xtc_schedule_check(MM, s)
         assert code == xtc.XTC_OK, why
+
+
+def test_fuse_legality():
+    d = xtc.matmul_desc(256, 256, 256, "bf16", "f32", consumer="relu")
+    st, _, why = chk(d, **dict(TCB, split_k=2, split_k_mode=1, buffer_c=0, fuse=1))
+    assert st == xtc.XTC_E_ILLEGAL_SCHEDULE and "atomic" in why
+    for kw in (dict(fuse=1), dict(fuse=0), dict(split_k=2, fuse=1), dict(split_k=2, split_k_mode=1, buffer_c=0, fuse=0)):
+        args = dict(TCB)
+        args.update(kw)
+        st, _, why = chk(d, **args)
+        assert st == xtc.XTC_OK, (kw, why)
+    bad = xtc.matmul_desc(64, 64, 64, "bf16", "f32")
+    bad.consumer = 7
+    st, _, why = xtc.xtc_schedule_check(bad, S(**TCB))
+    assert st == xtc.XTC_E_INVALID_ARG

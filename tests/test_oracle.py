@@ -217,3 +217,13 @@ def test_pins_reject_plausible_mutants():
     }
     for name, bad in mutants.items():
         assert not np.array_equal(bad, good), name
+
+
+def test_relu_spec_worked_example():
+    g = _golden("spec_relu.json")
+    assert oracle.relu(np.array(g["x"], float)).tolist() == g["y"]
+    # relu(matmul) closed form on a rank-1 product with mixed signs: K * max(u_i v_j, 0)
+    u = np.array([1.0, -2.0, 3.0])
+    v = np.array([-1.0, 2.0])
+    C, _ = oracle.matmul(np.repeat(u[:, None], 4, 1), np.repeat(v[None, :], 4, 0))
+    assert np.array_equal(oracle.relu(C), 4 * np.maximum(np.outer(u, v), 0))
