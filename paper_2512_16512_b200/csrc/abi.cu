@@ -142,6 +142,7 @@ struct xtc_op_s {
     alignas(64) CUtensorMap tmA, tmB, tmC;
     const void* bound[3] = {nullptr, nullptr, nullptr};
     bool maps_valid = false;
+    bool a3d = false, b3d = false;   // tmA / tmB encoded as 3-D (one TMA per stage)
     // validation reference cache
     double* R = nullptr;
     double* D = nullptr;
@@ -392,28 +393,61 @@ static xtc_status encode_maps(xtc_op op, const void* A, const void* B, void* C) 
     const int atom = 128 / es;
     const int tile_k = p.sch.tile_k, tile_n = p.sch.tile_n;
     CUresult r;
-    // B: [K][N] row-major, N-major UMMA operand: box {atom N-cols, tile_k rows}
+    const bool allow3d = getenv("XTC_NO_3D_TMA") == nullptr;
+    // B: [K][N] row-major, N-major UMMA operand.  3-D view {atom, K, N/atom} (strides ldb, 128 B):
+    // one box {atom, tile_k, bn_cta/atom} per stage lands as [n-block][k][128 B].  Only when N is a
+    // multiple of the atom (else the last block would read into the next row instead of zero-filling).
     {
         const int64_t ldb = (d.kind == XTC_OP_MATMUL && d.ldb) ? d.ldb : p.n_total;
-        cuuint64_t dims[2] = {(cuuint64_t)p.N, (cuuint64_t)p.K};
-        cuuint64_t strides[1] = {(cuuint64_t)(ldb * es)};
-        cuuint32_t box[2] = {(cuuint32_t)atom, (cuuint32_t)tile_k};
-        cuuint32_t estr[2] = {1, 1};
         // tf32 MN-major operands must use 32-byte swizzle atoms (UMMA SWIZZLE_128B_BASE32B)
         const CUtensorMapSwizzle bsw = tf32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B;
-        r = g_encode_tiled(&op->tmB, in_t, 2, const_cast<void*>(B), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           bsw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS) return fail(XTC_E_CUDA, "cuTensorMapEncodeTiled(B) failed: " + std::to_string((int)r));
+        op->b3d = false;
+        if (allow3d && p.N % atom == 0) {
+            cuuint64_t dims[3] = {(cuuint64_t)atom, (cuuint64_t)p.K, (cuuint64_t)(p.N / atom)};
+            cuuint64_t strides[2] = {(cuuint64_t)(ldb * es), (cuuint64_t)(atom * es)};
+            cuuint32_t box[3] = {(cuuint32_t)atom, (cuuint32_t)tile_k, (cuuint32_t)(tile_n / p.cta_group / atom)};
+            cuuint32_t estr[3] = {1, 1, 1};
+            r = g_encode_tiled(&op->tmB, in_t, 3, const_cast<void*>(B), dims, strides, box, estr,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, bsw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            op->b3d = (r == CUDA_SUCCESS);
+        }
+        if (!op->b3d) {
+            cuuint64_t dims[2] = {(cuuint64_t)p.N, (cuuint64_t)p.K};
+            cuuint64_t strides[1] = {(cuuint64_t)(ldb * es)};
+            cuuint32_t box[2] = {(cuuint32_t)atom, (cuuint32_t)tile_k};
+            cuuint32_t estr[2] = {1, 1};
+            r = g_encode_tiled(&op->tmB, in_t, 2, const_cast<void*>(B), dims, strides, box, estr,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, bsw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) return fail(XTC_E_CUDA, "cuTensorMapEncodeTiled(B) failed: " + std::to_string((int)r));
+        }
     }
+    op->a3d = false;
     if (d.kind == XTC_OP_MATMUL) {
+        // A: [M][K] K-major.  3-D view {atom, M, K/atom} (strides lda, 128 B): one box
+        // {atom, 128, tile_k/atom} per stage lands as [k-atom][row][128 B] (needs K % atom == 0).
         const int64_t lda = d.lda ? d.lda : d.k;
-        cuuint64_t dims[2] = {(cuuint64_t)p.K, (cuuint64_t)p.M};
-        cuuint64_t strides[1] = {(cuuint64_t)(lda * es)};
-        cuuint32_t box[2] = {(cuuint32_t)atom, 128};
-        cuuint32_t estr[2] = {1, 1};
-        r = g_encode_tiled(&op->tmA, in_t, 2, const_cast<void*>(A), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS) return fail(XTC_E_CUDA, "cuTensorMapEncodeTiled(A) failed: " + std::to_string((int)r));
+        if (allow3d && p.K % atom == 0) {
+            cuuint64_t dims[3] = {(cuuint64_t)atom, (cuuint64_t)p.M, (cuuint64_t)(p.K / atom)};
+            cuuint64_t strides[2] = {(cuuint64_t)(lda * es), (cuuint64_t)(atom * es)};
+            cuuint32_t box[3] = {(cuuint32_t)atom, 128, (cuuint32_t)(tile_k / atom)};
+            cuuint32_t estr[3] = {1, 1, 1};
+            r = g_encode_tiled(&op->tmA, in_t, 3, const_cast<void*>(A), dims, strides, box, estr,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            op->a3d = (r == CUDA_SUCCESS);
+        }
+        if (!op->a3d) {
+            cuuint64_t dims[2] = {(cuuint64_t)p.K, (cuuint64_t)p.M};
+            cuuint64_t strides[1] = {(cuuint64_t)(lda * es)};
+            cuuint32_t box[2] = {(cuuint32_t)atom, 128};
+            cuuint32_t estr[2] = {1, 1};
+            r = g_encode_tiled(&op->tmA, in_t, 2, const_cast<void*>(A), dims, strides, box, estr,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) return fail(XTC_E_CUDA, "cuTensorMapEncodeTiled(A) failed: " + std::to_string((int)r));
+        }
     } else {
         // x: NHWC, im2col: one pixel = `atom` channels (128 B), 128 pixels per column
         cuuint64_t dims[4] = {(cuuint64_t)d.c, (cuuint64_t)d.w, (cuuint64_t)d.h, (cuuint64_t)d.batch};
@@ -521,6 +555,8 @@ static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cud
         tp.pack_warps = p.sch.pack_warps == 0 ? 1 : p.sch.pack_warps;
         tp.b_resident = p.sch.b_resident;
         tp.relu = p.relu_epi;
+        tp.a3d = op->a3d;
+        tp.b3d = op->b3d;
         tp.buffer_c = p.sch.buffer_c;
         tp.atomic = p.atomic;
         tp.out_bf16 = out_bf16;

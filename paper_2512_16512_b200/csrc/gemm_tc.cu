@@ -118,6 +118,11 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                     }
                     const int nc = bn_cta * (int)rank;
                     for (int kb = 0; kb < p.kb_total; ++kb)
+                        if (p.b3d) {
+                            uint8_t* dst = sBres + (size_t)kb * p.b_stage_bytes;
+                            if constexpr (CG == 2) ptx::tma_load_3d_pair(&tmB, dst, bar_c, 0, kb * p.tile_k, nc / ATOM);
+                            else ptx::tma_load_3d(&tmB, dst, bfull, 0, kb * p.tile_k, nc / ATOM);
+                        } else
                         for (int b = 0; b < n_b; ++b) {
                             uint8_t* dst = sBres + (size_t)kb * p.b_stage_bytes + (size_t)b * p.tile_k * 128;
                             if constexpr (CG == 2) ptx::tma_load_2d_pair(&tmB, dst, bar_c, nc + b * ATOM, kb * p.tile_k);
@@ -167,7 +172,15 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                     }
                     uint8_t* a_dst = sA + (size_t)cs * p.a_stage_bytes;
                     uint8_t* b_dst = sB + (size_t)cs * p.b_stage_bytes;
-                    for (int a = 0; a < n_a; ++a) {
+                    // 3-D maps: one TMA moves all atoms of the stage ({atom, rows, atom index} box
+                    // lands as [atom][rows][128 B], the layout the UMMA descriptors walk)
+                    const bool a_one = !CONV && p.a3d;
+                    if (a_one) {
+                        const int ka = kb * (p.tile_k / ATOM);
+                        if constexpr (CG == 2) ptx::tma_load_3d_pair(&tmA, a_dst, bar_c, 0, m0, ka);
+                        else ptx::tma_load_3d(&tmA, a_dst, fb, 0, m0, ka);
+                    }
+                    for (int a = 0; a < (a_one ? 0 : n_a); ++a) {
                         const int kc = kb * p.tile_k + a * ATOM;
                         if constexpr (CONV) {
                             const int rs = kc / p.cg.C;
@@ -185,7 +198,11 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                             else ptx::tma_load_2d(&tmA, a_dst + a * A_ATOM_BYTES, fb, kc, m0);
                         }
                     }
-                    for (int b = 0; b < (b_res ? 0 : n_b); ++b) {
+                    if (!b_res && p.b3d) {
+                        if constexpr (CG == 2) ptx::tma_load_3d_pair(&tmB, b_dst, bar_c, 0, kb * p.tile_k, n0 / ATOM);
+                        else ptx::tma_load_3d(&tmB, b_dst, fb, 0, kb * p.tile_k, n0 / ATOM);
+                    }
+                    for (int b = 0; b < ((b_res || p.b3d) ? 0 : n_b); ++b) {
                         uint8_t* dst = b_dst + (size_t)b * p.tile_k * 128;
                         if constexpr (CG == 2) ptx::tma_load_2d_pair(&tmB, dst, bar_c, n0 + b * ATOM, kb * p.tile_k);
                         else ptx::tma_load_2d(&tmB, dst, fb, n0 + b * ATOM, kb * p.tile_k);

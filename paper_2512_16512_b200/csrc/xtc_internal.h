@@ -127,6 +127,7 @@ struct TcParams {
     int32_t pack_warps;      // 1..3 TMA-issuing warps (warps 0, 2, 3)
     int32_t b_resident;      // all of B packed once per CTA (kb_total x b_stage_bytes before the A ring)
     int32_t relu;            // fused consumer in the epilogue
+    int32_t a3d, b3d;        // one 3-D TMA per stage for all 128-B atoms of A / B (tmA / tmB are 3-D maps)
     int64_t ldc, ws_ld;
     void* C; float* Wk;
     uint32_t idesc;
