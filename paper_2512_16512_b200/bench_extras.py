@@ -71,9 +71,9 @@ def run_extras(xtc, torch, dev, peak):
         out[f"matmul_{n}_bf16"] = _best(xtc, torch, dev, d, MATMUL_SCHEDS[n], [(n, n), (n, n)], peak)
     d = xtc.matmul_desc(1024, 1024, 1024, "f32", "f32")
     simt = _best(xtc, torch, dev, d, SIMT_SCHEDS, [(1024, 1024), (1024, 1024)], peak)
-    # the fp32 path's own ceiling: 148 SM x 128 FFMA lanes x 2 FLOP x 1.965 GHz
+    # the fp32 path's own ceiling, measured: 72.5 TF/s FFMA (profiles/r01_ffma_peak.txt)
     if "tflops_med" in simt:
-        simt["frac_fp32_simt_peak"] = simt["tflops_med"] / 74.4
+        simt["frac_fp32_simt_peak"] = simt["tflops_med"] / 72.5
     out["matmul_1024_f32_simt"] = simt
     for name, (h, c) in {"L56": (56, 64), "L14": (14, 256)}.items():
         d = xtc.conv2d_desc(32, h, h, c, c, 3, 3, 1, 1, "bf16", "bf16")
