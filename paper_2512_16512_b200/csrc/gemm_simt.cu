@@ -49,7 +49,7 @@ __device__ __forceinline__ const float* a_elem(const SimtParams& p, int64_t m, i
 }
 
 template <int TM, int TN, int U, int VEC>
-__global__ void __launch_bounds__(simt_max_threads(TM, TN)) simt_gemm_kernel(const SimtParams p) {
+__global__ void __launch_bounds__(simt_max_threads(TM, TN), simt_min_blocks(TM, TN)) simt_gemm_kernel(const SimtParams p) {
     extern __shared__ __align__(16) float sm[];
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int BM = p.tile_m, BN = p.tile_n, BK = p.tile_k;

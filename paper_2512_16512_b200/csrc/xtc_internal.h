@@ -36,6 +36,9 @@ inline cudaError_t ensure_smem_attr(F* kernel, int smem) {
 XTC_HD constexpr int simt_max_threads(int tm, int tn) {
     return tm * tn >= 32 ? 256 : (tm * tn >= 16 ? 512 : 1024);
 }
+// Register-tiled variants ask for two resident CTAs per SM (<= 128 regs/thread for the
+// 256-thread 8x8 tiles): one CTA leaves 2 warps per scheduler, too few to hide LDS latency.
+XTC_HD constexpr int simt_min_blocks(int tm, int tn) { return tm * tn >= 16 ? 2 : 1; }
 
 // Tile-order mapping: the schedule's interchange + grouped raster.
 // Linear tile id -> (split segment ks, tile row mb, tile col nb).
