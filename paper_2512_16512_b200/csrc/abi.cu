@@ -556,6 +556,7 @@ static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cud
         tp.b_resident = p.sch.b_resident;
         tp.relu = p.relu_epi;
         tp.a3d = op->a3d;
+        tp.debug_skip_mma = getenv("XTC_DEBUG_SKIP_MMA") != nullptr;   // diagnostics: output invalid
         tp.b3d = op->b3d;
         tp.buffer_c = p.sch.buffer_c;
         tp.atomic = p.atomic;

@@ -249,7 +249,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                     if (ptx::elect_one()) {
                         const uint64_t ad = adesc0 + (uint64_t)(s * a_stage16);
                         const uint64_t bd = bdesc0 + (uint64_t)((b_res ? kb : s) * b_stage16);
-                        for (int a = 0; a < n_a; ++a) {
+                        for (int a = 0; a < (p.debug_skip_mma ? 0 : n_a); ++a) {
 #pragma unroll
                             for (int kk = 0; kk < ATOM / UMMA_K; ++kk) {
                                 const uint32_t krow = a * ATOM + kk * UMMA_K;

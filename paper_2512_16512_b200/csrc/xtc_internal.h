@@ -38,7 +38,7 @@ XTC_HD constexpr int simt_max_threads(int tm, int tn) {
 }
 // Register-tiled variants ask for two resident CTAs per SM (<= 128 regs/thread for the
 // 256-thread 8x8 tiles): one CTA leaves 2 warps per scheduler, too few to hide LDS latency.
-XTC_HD constexpr int simt_min_blocks(int tm, int tn) { return tm * tn >= 16 ? 2 : 1; }
+XTC_HD constexpr int simt_min_blocks(int tm, int tn) { return tm * tn >= 32 ? 2 : 1; }
 
 // Tile-order mapping: the schedule's interchange + grouped raster.
 // Linear tile id -> (split segment ks, tile row mb, tile col nb).
@@ -131,6 +131,7 @@ struct TcParams {
     int32_t b_resident;      // all of B packed once per CTA (kb_total x b_stage_bytes before the A ring)
     int32_t relu;            // fused consumer in the epilogue
     int32_t a3d, b3d;        // one 3-D TMA per stage for all 128-B atoms of A / B (tmA / tmB are 3-D maps)
+    int32_t debug_skip_mma;  // diagnostics only (XTC_DEBUG_SKIP_MMA): commits without MMAs, output invalid
     int64_t ldc, ws_ld;
     void* C; float* Wk;
     uint32_t idesc;
