@@ -33,6 +33,8 @@ SIMT_SCHEDS = [
          swizzle=4),
     dict(engine=0, tile_m=64, tile_n=128, tile_k=16, inner_m=4, inner_n=8, unroll_k=4, vector_n=4, stages=2,
          swizzle=4),
+    dict(engine=0, tile_m=128, tile_n=64, tile_k=32, inner_m=8, inner_n=4, unroll_k=8, vector_n=4, stages=2,
+         swizzle=4),
 ]
 
 
@@ -78,4 +80,15 @@ def run_extras(xtc, torch, dev, peak):
     for name, (h, c) in {"L56": (56, 64), "L14": (14, 256)}.items():
         d = xtc.conv2d_desc(32, h, h, c, c, 3, 3, 1, 1, "bf16", "bf16")
         out[f"conv_{name}_n32_bf16"] = _best(xtc, torch, dev, d, CONV_SCHEDS[name], [(32, h, h, c), (3, 3, c, c)], peak)
+    # BASELINE config 3 spans batch N = 1..32: smaller batches are parallelism-bound, so the
+    # candidate list adds split-K (a5) there
+    scan = {}
+    for name, (h, c) in {"L56": (56, 64), "L14": (14, 256)}.items():
+        for nb in (1, 8):
+            d = xtc.conv2d_desc(nb, h, h, c, c, 3, 3, 1, 1, "bf16", "bf16")
+            cands = list(CONV_SCHEDS[name]) + [dict(TC, tile_n=min(c, 256), stages=4, buffer_c=1, acc_buffers=1,
+                                                     split_k=sk, pack_warps=2) for sk in (2, 3)]
+            r = _best(xtc, torch, dev, d, cands, [(nb, h, h, c), (3, 3, c, c)], peak)
+            scan[f"{name}_n{nb}"] = {k: r.get(k) for k in ("tflops_med", "t_med_us", "schedule", "error")}
+    out["conv_batch_scan_bf16"] = scan
     return out

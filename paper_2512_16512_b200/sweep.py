@@ -19,15 +19,18 @@ import time
 
 import torch
 
-from . import (Op, XTC_BF16, XTC_ENGINE_TCGEN05, matmul_desc, measure_cfg, xtc_fill)
+from . import (DTYPES, Op, XTC_ENGINE_SIMT, XTC_ENGINE_TCGEN05, matmul_desc, measure_cfg, xtc_fill)
 from .parallel import REC_FIELDS, gather_records, pack_records, rank_candidates, unpack_gathered
 from .strategy import GpuStrategy
 
+TORCH_DT = {"bf16": torch.bfloat16, "f32": torch.float32, "tf32": torch.float32}
+
 
 def run_sweep(m, n, k, candidates, seed=0, world=1, rank=0, device=0, warmup=2, repeats=10, validate=1,
-              peak_tflops=0.0, resume_path=None, in_dtype="bf16", out_dtype="bf16"):
+              peak_tflops=0.0, resume_path=None, in_dtype="bf16", out_dtype="bf16", engine=XTC_ENGINE_TCGEN05):
+    """engine XTC_ENGINE_SIMT sweeps the fp32 register-tiled engine (in_dtype f32)."""
     desc = matmul_desc(m, n, k, in_dtype, out_dtype)
-    strat = GpuStrategy(desc, XTC_ENGINE_TCGEN05)
+    strat = GpuStrategy(desc, engine)
     samples = strat.sample(candidates, seed=seed)
     mine = rank_candidates(len(samples), world, rank)
     done = {}
@@ -39,12 +42,12 @@ def run_sweep(m, n, k, candidates, seed=0, world=1, rank=0, device=0, warmup=2, 
                     done[r["id"]] = r
     todo = [i for i in mine if i not in done]
     dev = torch.device("cuda", device)
-    a = torch.empty((m, k), dtype=torch.bfloat16, device=dev)
-    b = torch.empty((k, n), dtype=torch.bfloat16, device=dev)
-    c = torch.empty((m, n), dtype=torch.bfloat16, device=dev)
+    a = torch.empty((m, k), dtype=TORCH_DT[in_dtype], device=dev)
+    b = torch.empty((k, n), dtype=TORCH_DT[in_dtype], device=dev)
+    c = torch.empty((m, n), dtype=TORCH_DT[out_dtype], device=dev)
     st = torch.cuda.current_stream(dev).cuda_stream
-    xtc_fill(a.data_ptr(), m * k, XTC_BF16, seed + 1, 0, 0, st)
-    xtc_fill(b.data_ptr(), k * n, XTC_BF16, seed + 2, 0, 0, st)
+    xtc_fill(a.data_ptr(), m * k, DTYPES[in_dtype], seed + 1, 0, 0, st)
+    xtc_fill(b.data_ptr(), k * n, DTYPES[in_dtype], seed + 2, 0, 0, st)
     op = Op(desc, device)
     cfg = measure_cfg(warmup=warmup, repeats=repeats, validate=validate, reuse_reference=1,
                       peak_tflops=peak_tflops)
@@ -67,7 +70,12 @@ def main():
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--resume", default=None)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--engine", default="tcgen05", choices=["tcgen05", "simt"])
+    ap.add_argument("--dtype", default=None, help="input dtype (default bf16 for tcgen05, f32 for simt)")
     args = ap.parse_args()
+    engine = XTC_ENGINE_SIMT if args.engine == "simt" else XTC_ENGINE_TCGEN05
+    in_dt = args.dtype or ("f32" if engine == XTC_ENGINE_SIMT else "bf16")
+    out_dt = "f32" if in_dt in ("f32", "tf32") else "bf16"
     import torch.distributed as dist
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -77,7 +85,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     desc, samples, mine, todo, scheds, op, (a, b, c), cfg, st, done = run_sweep(
         args.m, args.n, args.k, args.candidates, args.seed, world, rank, local, args.warmup, args.repeats,
-        resume_path=args.resume)
+        resume_path=args.resume, in_dtype=in_dt, out_dtype=out_dt, engine=engine)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -102,10 +110,12 @@ def main():
     if rank == 0:
         ok = [r for r in all_recs if int(r["status"]) == 0 and int(r["valid"]) == 1]
         best = max(ok, key=lambda r: r["tflops_med"]) if ok else None
-        out = {"candidates": len(samples), "world": world, "seconds": float(dtt[0]),
+        out = {"candidates": len(samples), "world": world, "engine": args.engine, "dtype": in_dt,
+               "shape": [args.m, args.n, args.k], "seconds": float(dtt[0]),
                "schedules_per_s": len(samples) / float(dtt[0]), "valid": len(ok),
                "best": {"id": best["id"], "tflops_med": best["tflops_med"],
-                        "schedule": dict(zip(list(GpuStrategy(desc).slots), samples[int(best["id"])]))} if best else None}
+                        "schedule": dict(zip(list(GpuStrategy(desc, engine).slots), samples[int(best["id"])]))}
+               if best else None}
         print(json.dumps(out), flush=True)
         if args.out:
             with open(args.out, "w") as f:
