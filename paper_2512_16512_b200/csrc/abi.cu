@@ -28,6 +28,8 @@ cudaError_t launch_compare(const void* C, int out_bf16, int relu, int64_t M, int
                            const double* D, double* blk_err, int64_t* blk_idx, void* counts, int blocks,
                            cudaStream_t st);
 cudaError_t launch_relu(void* C, int out_bf16, int64_t M, int64_t N, int64_t ldc, cudaStream_t st);
+cudaError_t launch_compare_finalize(const double* blk_err, const int64_t* blk_idx, int blocks, void* counts,
+                                    double* slot, cudaStream_t st);
 cudaError_t launch_flush(void* buf, int64_t bytes, uint32_t salt, cudaStream_t st);
 cudaError_t launch_delay(uint64_t ns, cudaStream_t st);
 cudaError_t launch_fault(void* C, int out_bf16, int64_t M, int64_t N, int64_t ldc, int kind, int64_t row, int64_t col,
@@ -808,21 +810,183 @@ extern "C" xtc_status xtc_measure(xtc_op op, const void* const* inputs, void* co
 
 extern "C" xtc_status xtc_sweep(xtc_op op, const xtc_schedule* cands, int32_t n, const void* const* inputs,
                                 void* const* outputs, const xtc_measure_cfg* cfg, xtc_metrics* out, void* stream) {
-    if (!op || !cands || n < 0 || !out || !cfg) return fail(XTC_E_INVALID_ARG, "null argument");
+    if (!op || !cands || n < 0 || !out || !cfg || !inputs || !outputs) return fail(XTC_E_INVALID_ARG, "null argument");
+    if (cfg->repeats < 1 || cfg->warmup < 0) return fail(XTC_E_INVALID_ARG, "repeats must be >= 1, warmup >= 0");
     DeviceGuard g(op->device);
-    xtc_measure_cfg c = *cfg;
+    cudaStream_t st = (cudaStream_t)stream;
+    const void* A = inputs[0];
+    const void* B = inputs[1];
+    void* C = outputs[0];
+    const xtc_op_desc& d = op->d;
+    int64_t M, N, K, P, Q;
+    gemm_view(d, M, N, K, P, Q);
+    const int64_t ldc = (d.kind == XTC_OP_MATMUL && d.ldc) ? d.ldc : N;
+    const int os = dsize(d.out_dtype);
+    const int R = cfg->repeats;
+    double tol = cfg->tol;
+    if (tol <= 0) tol = d.in_dtype == XTC_F32 ? 1e-5 : 5e-3;
+
+    // 1. plan every candidate on the host; illegal ones launch nothing
+    std::vector<Plan> plans(n);
+    std::vector<char> legal(n, 0);
+    int64_t ws_max = 0;
     for (int i = 0; i < n; ++i) {
-        xtc_status s = xtc_schedule_apply(op, &cands[i]);
-        if (s != XTC_OK) {
-            memset(&out[i], 0, sizeof out[i]);
-            out[i].status = s;
-            out[i].valid = -1;
-            continue;
-        }
-        s = measure_impl(op, inputs[0], inputs[1], outputs[0], &c, &out[i], (cudaStream_t)stream);
-        c.reuse_reference = 1;     // same inputs for every candidate of the sweep
-        if (s == XTC_E_CUDA) { out[i].status = s; return s; }
+        memset(&out[i], 0, sizeof out[i]);
+        out[i].valid = -1;
+        out[i].err_row = out[i].err_col = -1;
+        std::string why;
+        xtc_status s = make_plan(d, cands[i], op->num_sms, plans[i], why);
         out[i].status = s;
+        if (s == XTC_OK) {
+            legal[i] = 1;
+            ws_max = std::max(ws_max, plans[i].workspace_bytes);
+        }
     }
+    // 2. resources sized once for the whole sweep: no allocation (an implicit device
+    //    synchronisation) between candidates
+    if (ws_max > op->ws_bytes) {
+        if (op->ws) cudaFree(op->ws);
+        op->ws = nullptr;
+        op->ws_bytes = 0;
+        if (cudaMalloc(&op->ws, ws_max) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(XTC_E_OOM, "split-K workspace allocation failed");
+        }
+        op->ws_bytes = ws_max;
+    }
+    if (cfg->flush_l2) {
+        xtc_status s = ensure_flush(op->device, st);
+        if (s != XTC_OK) return s;
+    }
+    if (cfg->validate) {
+        if (!(cfg->reuse_reference && op->ref_valid && op->ref_inputs[0] == A && op->ref_inputs[1] == B)) {
+            xtc_status s = compute_reference(op, A, B, st);
+            if (s != XTC_OK) return s;
+        }
+        if (!op->blk_err) {
+            if (cudaMalloc(&op->blk_err, kCmpBlocks * 8) != cudaSuccess ||
+                cudaMalloc(&op->blk_idx, kCmpBlocks * 8) != cudaSuccess || cudaMalloc(&op->counts, 16) != cudaSuccess) {
+                cudaGetLastError();
+                return fail(XTC_E_OOM, "compare buffers");
+            }
+        }
+        CU_TRY(cudaMemsetAsync(op->counts, 0, 16, st), "memset counts");
+    }
+    // 3. chunks of candidates enqueued back to back, one synchronisation per chunk: the host
+    //    stays ahead of the GPU, so the per-rep events bracket GPU work only (no delay kernel)
+    const int CH = 64;
+    double* slots = nullptr;
+    if (cfg->validate && cudaMalloc(&slots, (size_t)CH * 4 * sizeof(double)) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(XTC_E_OOM, "sweep validation slots");
+    }
+    std::vector<cudaEvent_t> ev((size_t)CH * 2 * R);
+    for (auto& e : ev)
+        if (cudaEventCreate(&e) != cudaSuccess) {
+            if (slots) cudaFree(slots);
+            return cuda_fail(cudaGetLastError(), "cudaEventCreate");
+        }
+    auto cleanup = [&]() {
+        for (auto e : ev) cudaEventDestroy(e);
+        if (slots) cudaFree(slots);
+    };
+    const bool had_plan = op->has_plan;
+    Plan saved = op->plan;
+    const double flops = xtc_op_flops(&d);
+    std::vector<double> hslots((size_t)CH * 4);
+    for (int c0 = 0; c0 < n; c0 += CH) {
+        const int c1 = std::min(n, c0 + CH);
+        for (int i = c0; i < c1; ++i) {
+            if (!legal[i]) continue;
+            op->plan = plans[i];
+            op->has_plan = true;
+            op->maps_valid = false;           // TMA boxes depend on the schedule
+            xtc_status s = XTC_OK;
+            if (cfg->validate) {
+                if (cudaMemset2DAsync(C, ldc * os, 0xFF, N * os, M, st) != cudaSuccess) s = XTC_E_CUDA;
+                if (s == XTC_OK) s = run_impl(op, A, B, C, st);
+                if (s == XTC_OK && (launch_compare(C, d.out_dtype == XTC_BF16, d.consumer == XTC_CONSUMER_RELU, M, N,
+                                                   ldc, op->R, op->D, op->blk_err, op->blk_idx, op->counts, kCmpBlocks,
+                                                   st) != cudaSuccess ||
+                                    launch_compare_finalize(op->blk_err, op->blk_idx, kCmpBlocks, op->counts,
+                                                            slots + (size_t)(i - c0) * 4, st) != cudaSuccess))
+                    s = XTC_E_CUDA;
+            }
+            for (int w = 0; s == XTC_OK && w < cfg->warmup; ++w) s = run_impl(op, A, B, C, st);
+            for (int r = 0; s == XTC_OK && r < R; ++r) {
+                if (cfg->flush_l2 &&
+                    launch_flush(g_flush_buf[op->device], g_flush_bytes[op->device], (uint32_t)r, st) != cudaSuccess) {
+                    s = XTC_E_CUDA;
+                    break;
+                }
+                cudaEventRecord(ev[((size_t)(i - c0) * R + r) * 2], st);
+                s = run_impl(op, A, B, C, st);
+                cudaEventRecord(ev[((size_t)(i - c0) * R + r) * 2 + 1], st);
+            }
+            out[i].status = s;
+            if (s == XTC_E_CUDA) {
+                cleanup();
+                return s;
+            }
+        }
+        if (cudaStreamSynchronize(st) != cudaSuccess) {
+            cleanup();
+            return cuda_fail(cudaGetLastError(), "sweep chunk sync");
+        }
+        const double clk = sm_clock_mhz(op->device);
+        if (cfg->validate &&
+            cudaMemcpy(hslots.data(), slots, (size_t)(c1 - c0) * 4 * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess) {
+            cleanup();
+            return cuda_fail(cudaGetLastError(), "sweep slots D2H");
+        }
+        for (int i = c0; i < c1; ++i) {
+            if (!legal[i] || out[i].status != XTC_OK) continue;
+            xtc_metrics& m = out[i];
+            if (cfg->validate) {
+                const double* sl = &hslots[(size_t)(i - c0) * 4];
+                m.max_norm_err = sl[0];
+                const int64_t idx = (int64_t)sl[1];
+                m.err_row = idx >= 0 ? idx / N : -1;
+                m.err_col = idx >= 0 ? idx % N : -1;
+                m.n_mismatch = (int64_t)sl[2];
+                m.n_nan = (int64_t)sl[3];
+                bool ok = m.n_nan == 0 && m.max_norm_err <= tol;
+                if (cfg->exact) ok = ok && m.n_mismatch == 0;
+                m.valid = ok ? 1 : 0;
+            }
+            std::vector<double> t(R);
+            for (int r = 0; r < R; ++r) {
+                float ms = 0;
+                cudaEventElapsedTime(&ms, ev[((size_t)(i - c0) * R + r) * 2], ev[((size_t)(i - c0) * R + r) * 2 + 1]);
+                t[r] = ms * 1e6;
+            }
+            std::vector<double> srt = t;
+            std::sort(srt.begin(), srt.end());
+            m.t_min_ns = srt.front();
+            m.t_max_ns = srt.back();
+            m.t_med_ns = (R % 2) ? srt[R / 2] : 0.5 * (srt[R / 2 - 1] + srt[R / 2]);
+            double sum = 0;
+            for (double v : t) sum += v;
+            m.t_mean_ns = sum / R;
+            m.tflops_med = flops / m.t_med_ns * 1e-3;
+            m.tflops_min = flops / m.t_min_ns * 1e-3;
+            m.frac_peak = cfg->peak_tflops > 0 ? m.tflops_med / cfg->peak_tflops : 0.0;
+            m.sm_clock_mhz = clk;
+            m.n_reps = R;
+        }
+    }
+    cleanup();
+    // the op keeps the last legal candidate's schedule (or its previous one if none was legal)
+    int last = -1;
+    for (int i = n - 1; i >= 0; --i)
+        if (legal[i]) { last = i; break; }
+    if (last >= 0) {
+        op->plan = plans[last];
+        op->has_plan = true;
+    } else {
+        op->plan = saved;
+        op->has_plan = had_plan;
+    }
+    op->maps_valid = false;
     return XTC_OK;
 }

@@ -191,6 +191,50 @@ cudaError_t launch_compare(const void* C, int out_bf16, int relu, int64_t M, int
     return cudaGetLastError();
 }
 
+// Device-side end of the compare (used by the asynchronous sweep): one block reduces
+// the per-block (max err, index) partials and the counters into `slot`
+// {max_err, (double)index, (double)n_mismatch, (double)n_nan}, then clears the counters.
+__global__ void compare_finalize_kernel(const double* blk_err, const int64_t* blk_idx, int blocks, CmpOut* counts,
+                                        double* slot) {
+    __shared__ double se[256];
+    __shared__ int64_t si[256];
+    double best = -1.0;
+    int64_t bi = -1;
+    for (int i = threadIdx.x; i < blocks; i += blockDim.x) {
+        const double e = blk_err[i];
+        const int64_t x = blk_idx[i];
+        if (x >= 0 && (e > best || (e == best && (bi < 0 || x < bi)))) { best = e; bi = x; }
+    }
+    se[threadIdx.x] = best;
+    si[threadIdx.x] = bi;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) {
+            const double o = se[threadIdx.x + w];
+            const int64_t oi = si[threadIdx.x + w];
+            if (oi >= 0 && (o > se[threadIdx.x] || (o == se[threadIdx.x] && (si[threadIdx.x] < 0 || oi < si[threadIdx.x])))) {
+                se[threadIdx.x] = o;
+                si[threadIdx.x] = oi;
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        slot[0] = se[0] < 0 ? 0.0 : se[0];
+        slot[1] = (double)si[0];
+        slot[2] = (double)counts->n_mismatch;
+        slot[3] = (double)counts->n_nan;
+        counts->n_mismatch = 0;
+        counts->n_nan = 0;
+    }
+}
+
+cudaError_t launch_compare_finalize(const double* blk_err, const int64_t* blk_idx, int blocks, void* counts,
+                                    double* slot, cudaStream_t st) {
+    compare_finalize_kernel<<<1, 256, 0, st>>>(blk_err, blk_idx, blocks, static_cast<CmpOut*>(counts), slot);
+    return cudaGetLastError();
+}
+
 // --------------------------------------------- unfused consumer (fuse = 0) --
 // relu as its own elementwise pass over the output (the paper's separate graph op);
 // one read + one write of C.
