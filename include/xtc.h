@@ -171,6 +171,12 @@ typedef struct {
                                 are unchanged (caller promises the data is unchanged)   */
     double tol;           /* max |C - R| / D allowed (<= 0: 1e-5 fp32, 5e-3 bf16/tf32)  */
     double peak_tflops;   /* denominator for frac_peak (0 = not reported)              */
+    /* Hardware counters by human-readable name: NULL or a
+     * comma-separated list of up to 8 Nsight-Compute metric names, each optionally
+     * prefixed "gpu." (e.g. "gpu.dram__bytes_read.sum,gpu.sm__throughput.avg.pct_of_peak_sustained_elapsed").
+     * Collected by the CUPTI range profiler in a separate replay pass AFTER the timed
+     * reps (one range around one xtc_run), never inside the timed region. */
+    const char* counters;
 } xtc_measure_cfg;
 
 /* Results of xtc_measure. */
@@ -186,8 +192,10 @@ typedef struct {
     double frac_peak;      /* tflops_med / cfg->peak_tflops                          */
     double sm_clock_mhz;   /* NVML SM clock sampled right after the timed window (0 if n/a) */
     int32_t n_reps;
-    int32_t reserved0;
-    double reserved[6];
+    int32_t n_counters;    /* values in counters[] (in cfg->counters order); -1: CUPTI, the device
+                              or a metric name unavailable -- the measurement itself is still
+                              XTC_OK and xtc_last_error() says why */
+    double counters[8];
 } xtc_metrics;
 
 typedef struct xtc_op_s* xtc_op;

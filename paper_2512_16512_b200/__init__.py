@@ -63,7 +63,8 @@ class xtc_plan_info(Structure):
 
 class xtc_measure_cfg(Structure):
     _fields_ = [("warmup", c_int32), ("repeats", c_int32), ("flush_l2", c_int32), ("validate", c_int32),
-                ("exact", c_int32), ("reuse_reference", c_int32), ("tol", c_double), ("peak_tflops", c_double)]
+                ("exact", c_int32), ("reuse_reference", c_int32), ("tol", c_double), ("peak_tflops", c_double),
+                ("counters", ctypes.c_char_p)]
 
 
 class xtc_metrics(Structure):
@@ -71,11 +72,25 @@ class xtc_metrics(Structure):
                 ("n_nan", c_int64), ("err_row", c_int64), ("err_col", c_int64),
                 ("t_min_ns", c_double), ("t_med_ns", c_double), ("t_mean_ns", c_double), ("t_max_ns", c_double),
                 ("tflops_med", c_double), ("tflops_min", c_double), ("frac_peak", c_double),
-                ("sm_clock_mhz", c_double), ("n_reps", c_int32), ("reserved0", c_int32), ("reserved", c_double * 6)]
+                ("sm_clock_mhz", c_double), ("n_reps", c_int32), ("n_counters", c_int32), ("counters", c_double * 8)]
 
     def as_dict(self):
         return {f: (getattr(self, f) if not isinstance(getattr(self, f), ctypes.Array) else None)
                 for f, _ in self._fields_ if not f.startswith("reserved")}
+
+    def counter_values(self, names) -> dict:
+        """{name: value} for the names passed in measure_cfg(counters=...); {} if CUPTI was
+        unavailable (n_counters == -1) or none were requested."""
+        names = _counter_names(names)
+        return {n: self.counters[i] for i, n in enumerate(names[:max(self.n_counters, 0)])}
+
+
+def _counter_names(names) -> list:
+    if not names:
+        return []
+    if isinstance(names, str):
+        names = names.split(",")
+    return [n.strip() for n in names if n.strip()]
 
 
 xtc_op = c_void_p
@@ -254,11 +269,15 @@ def schedule(**kw) -> xtc_schedule:
 
 
 def measure_cfg(warmup=2, repeats=10, flush_l2=0, validate=1, exact=0, reuse_reference=0, tol=0.0,
-                peak_tflops=0.0) -> xtc_measure_cfg:
+                peak_tflops=0.0, counters=None) -> xtc_measure_cfg:
+    """counters: None, a comma-separated string or a list of metric names (optionally
+    "gpu."-prefixed), collected in a separate CUPTI pass after the timed reps."""
     c = xtc_measure_cfg()
     c.warmup, c.repeats, c.flush_l2, c.validate, c.exact, c.reuse_reference = (
         warmup, repeats, flush_l2, validate, exact, reuse_reference)
     c.tol, c.peak_tflops = tol, peak_tflops
+    names = _counter_names(counters)
+    c.counters = ",".join(names).encode() if names else None
     return c
 
 

@@ -792,6 +792,33 @@ static xtc_status measure_impl(xtc_op op, const void* A, const void* B, void* C,
     m->tflops_min = flops / m->t_min_ns * 1e-3;
     m->frac_peak = cfg->peak_tflops > 0 ? m->tflops_med / cfg->peak_tflops : 0.0;
     m->n_reps = R;
+    if (cfg->counters && *cfg->counters) {
+        // separate pass, after the timed region: one range = one operator call
+        std::vector<std::string> names = split_counter_names(cfg->counters);
+        if (names.size() > 8) return fail(XTC_E_INVALID_ARG, "at most 8 counters per measurement");
+        for (int i = 0; i < 8; ++i) m->counters[i] = std::nan("");
+        std::vector<double> vals;
+        std::string why;
+        xtc_status rs = XTC_OK;
+        auto prepare = [&] {  // same cache state as the timed reps: flushed before each replay
+            if (cfg->flush_l2 &&
+                launch_flush(g_flush_buf[op->device], g_flush_bytes[op->device], 0u, st) != cudaSuccess)
+                return false;
+            return cudaStreamSynchronize(st) == cudaSuccess;
+        };
+        auto once = [&] {
+            rs = run_impl(op, A, B, C, st);
+            return rs == XTC_OK && cudaStreamSynchronize(st) == cudaSuccess;
+        };
+        if (!names.empty() && collect_counters(op->device, names, prepare, once, vals, why)) {
+            m->n_counters = (int32_t)names.size();
+            for (size_t i = 0; i < names.size(); ++i) m->counters[i] = vals[i];
+        } else {
+            if (rs != XTC_OK) return rs;
+            m->n_counters = -1;
+            g_err = "counters unavailable: " + why;  // documented: readable although the status is XTC_OK
+        }
+    }
     m->status = XTC_OK;
     return XTC_OK;
 }

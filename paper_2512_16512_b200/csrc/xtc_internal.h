@@ -2,7 +2,9 @@
 // Not part of the public ABI (include/xtc.h is).
 #pragma once
 #include <stdint.h>
+#include <functional>
 #include <string>
+#include <vector>
 #include "../../include/xtc.h"
 #include <cuda_runtime.h>
 
@@ -147,5 +149,13 @@ constexpr int kTraceCtas = 160;          // >= #SMs: the whole persistent grid
 constexpr int kTraceK = 96;
 constexpr int kTraceTiles = 16;
 constexpr int kTraceSlots = 8 + 2 * kTraceK + 2 * kTraceTiles;
+
+// counters.cpp: named hardware counters through the CUPTI range profiler (dlopen'ed).
+// split_counter_names strips the "gpu." prefix; collect_counters wraps one range around
+// run_once() (replayed once per counter pass, each replay preceded by prepare() outside the range) and returns false with `why` when CUPTI,
+// the device or a metric name is unavailable.
+std::vector<std::string> split_counter_names(const char* list);
+bool collect_counters(int device, const std::vector<std::string>& names, const std::function<bool()>& prepare,
+                      const std::function<bool()>& run_once, std::vector<double>& values, std::string& why);
 
 }  // namespace xtc

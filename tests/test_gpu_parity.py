@@ -257,6 +257,44 @@ def test_sweep_records_and_illegal_candidates():
     assert recs[0].tflops_med > 0 and recs[0].t_min_ns <= recs[0].t_med_ns <= recs[0].t_max_ns
 
 
+# ----------------------------------------------- named hardware counters --
+def test_measure_named_counters():
+    """a9 counters by name: collected by CUPTI in a pass after the
+    timed reps.  Pinned to physics: after an L2 flush every byte of A and B must come from
+    DRAM at least once, the kernel time must agree with the event timing, and the timed
+    numbers / validation are unaffected by the extra pass."""
+    n = 2048
+    desc = xtc.matmul_desc(n, n, n, "bf16", "bf16")
+    a = dev_tensor((n, n), "bf16", 1, MODE_UNIFORM)
+    b = dev_tensor((n, n), "bf16", 2, MODE_UNIFORM)
+    c = torch.empty((n, n), dtype=torch.bfloat16, device="cuda:0")
+    op = xtc.Op(desc)
+    op.apply(tc(tile_n=256, stages=4, persistent=1, acc_buffers=2))
+    names = ["gpu.dram__bytes_read.sum", "gpu__time_duration.sum", "dram__bytes_write.sum"]
+    m = op.measure(a, b, c, xtc.measure_cfg(warmup=2, repeats=5, flush_l2=1, validate=1, counters=names))
+    assert m.valid == 1 and m.n_reps == 5
+    assert m.n_counters == 3, xtc.xtc_last_error()
+    v = m.counter_values(names)
+    compulsory = 2 * n * n * 2                       # A + B in bf16
+    assert compulsory <= v["gpu.dram__bytes_read.sum"] <= 8 * compulsory
+    assert 0 <= v["dram__bytes_write.sum"] <= 4 * n * n * 2
+    assert 0.5 * m.t_min_ns <= v["gpu__time_duration.sum"] <= 3.0 * m.t_max_ns
+
+
+def test_measure_unknown_counter_is_unavailable_not_failure():
+    desc = xtc.matmul_desc(256, 256, 256, "bf16", "bf16")
+    a = dev_tensor((256, 256), "bf16", 1, MODE_INT)
+    b = dev_tensor((256, 256), "bf16", 2, MODE_INT)
+    c = torch.empty((256, 256), dtype=torch.bfloat16, device="cuda:0")
+    op = xtc.Op(desc)
+    op.apply(tc())
+    m = op.measure(a, b, c, xtc.measure_cfg(warmup=0, repeats=2, validate=1, exact=1,
+                                            counters="gpu.no_such__metric.sum"))
+    assert m.valid == 1 and m.t_med_ns > 0
+    assert m.n_counters == -1 and "counters unavailable" in xtc.xtc_last_error()
+    assert m.counter_values("gpu.no_such__metric.sum") == {}
+
+
 # ------------------------------------------- multi-rank bench rehearsal --
 def test_bench_two_rank_rehearsal_on_one_gpu(tmp_path):
     """The N>1 bench path (M-sharded GEMM + all-gather + sharded sweep + max-over-ranks
