@@ -123,7 +123,13 @@ typedef enum { XTC_SPLITK_ORDERED = 0, XTC_SPLITK_ATOMIC = 1 } xtc_splitk_mode;
  *                          b_resident             : tcgen05: 1 = pack all of B once per CTA at the outermost
  *                                                   loop (needs a single N tile and split_k 1); the ring
  *                                                   then streams A only
- * bufferize    buffer_c               : 1 = SMEM-staged output + TMA store, 0 = direct stores
+ *                          pack_halo              : tcgen05 conv2d, stride 1: 1 = pack the input at the
+ *                                                   output-tile level instead of per k-block -- one haloed
+ *                                                   NHWC patch (tile rows + R-1 rows, Wp >= Q+S-1 pixel
+ *                                                   slots) per tile, every filter tap (r, s) read as a
+ *                                                   row-shifted view of it; tile_m = 128 or 256 virtual
+ *                                                   rows (128/Wp output rows each), cluster_m 1, split_k 1
+ * bufferize    buffer_c             : 1 = SMEM-staged output + TMA store, 0 = direct stores
  *                          acc_buffers            : tcgen05 TMEM accumulator buffers (1|2)
  * fuse         fuse                   : 1 = the op's consumer (relu) is applied in the producer's
  *                                                   epilogue (or in the split-K reduction); 0 = it runs as a
@@ -144,7 +150,8 @@ typedef struct {
     int32_t pack_warps;
     int32_t b_resident;
     int32_t fuse;
-    int32_t reserved[2];
+    int32_t pack_halo;
+    int32_t reserved[1];
 } xtc_schedule;
 
 /* What the planner derived for a legal schedule (for reports and tests). */

@@ -17,6 +17,8 @@
 namespace xtc {
 cudaError_t launch_tc_gemm(bool tf32, bool conv, int cta_group, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
                            const TcParams& p, int grid, int smem, cudaStream_t st);
+cudaError_t launch_tc_conv_halo(bool tf32, const CUtensorMap& x, const CUtensorMap& b, const CUtensorMap& y,
+                                const TcParams& p, int grid, int smem, cudaStream_t st);
 cudaError_t launch_simt_gemm(int tm, int tn, int u, int vec, const SimtParams& p, int grid, int block, int smem,
                              cudaStream_t st);
 cudaError_t launch_fill(void* dst, int64_t count, int bf16, uint64_t seed, int mode, int64_t first, cudaStream_t st);
@@ -450,6 +452,17 @@ static xtc_status encode_maps(xtc_op op, const void* A, const void* B, void* C) 
                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
             if (r != CUDA_SUCCESS) return fail(XTC_E_CUDA, "cuTensorMapEncodeTiled(A) failed: " + std::to_string((int)r));
         }
+    } else if (p.halo) {
+        // x: NHWC, tiled 4-D {C, W, H, N}; box {atom channels, Wp slots, patch rows, 1} = one
+        // channel plane of the haloed patch, [row][slot][128 B] in SMEM
+        cuuint64_t dims[4] = {(cuuint64_t)d.c, (cuuint64_t)d.w, (cuuint64_t)d.h, (cuuint64_t)d.batch};
+        cuuint64_t strides[3] = {(cuuint64_t)(d.c * es), (cuuint64_t)(d.w * d.c * es), (cuuint64_t)(d.h * d.w * d.c * es)};
+        cuuint32_t box[4] = {(cuuint32_t)atom, (cuuint32_t)p.halo_wp, (cuuint32_t)p.halo_pr, 1};
+        cuuint32_t estr[4] = {1, 1, 1, 1};
+        r = g_encode_tiled(&op->tmA, in_t, 4, const_cast<void*>(A), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(XTC_E_CUDA, "cuTensorMapEncodeTiled(x patch) failed: " + std::to_string((int)r));
     } else {
         // x: NHWC, im2col: one pixel = `atom` channels (128 B), 128 pixels per column
         cuuint64_t dims[4] = {(cuuint64_t)d.c, (cuuint64_t)d.w, (cuuint64_t)d.h, (cuuint64_t)d.batch};
@@ -463,7 +476,22 @@ static xtc_status encode_maps(xtc_op op, const void* A, const void* B, void* C) 
         if (r != CUDA_SUCCESS) return fail(XTC_E_CUDA, "cuTensorMapEncodeIm2col(x) failed: " + std::to_string((int)r));
     }
     // C (or the split-K workspace): 3-D {N, M, S} so stores clip per segment; box {128 B, 32 rows, 1}
-    if (p.sch.buffer_c) {
+    if (p.sch.buffer_c && p.halo) {
+        // y: NPQF as 4-D {F, Q, P, N}; one epilogue warp's 32 virtual rows = box {128 B, min(Wp,32)
+        // slots, max(1,32/Wp) rows, 1}; slots q >= Q and rows p >= P are clipped
+        int64_t M_, N_, K_, P, Q;
+        gemm_view(d, M_, N_, K_, P, Q);
+        const int os = dsize(d.out_dtype);
+        const CUtensorMapDataType out_t = os == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+        cuuint64_t dims[4] = {(cuuint64_t)d.f, (cuuint64_t)Q, (cuuint64_t)P, (cuuint64_t)d.batch};
+        cuuint64_t strides[3] = {(cuuint64_t)(d.f * os), (cuuint64_t)(Q * d.f * os), (cuuint64_t)(P * Q * d.f * os)};
+        const int wq = p.halo_wp < 32 ? p.halo_wp : 32;
+        cuuint32_t box[4] = {(cuuint32_t)(128 / os), (cuuint32_t)wq, (cuuint32_t)(32 / wq), 1};
+        cuuint32_t estr[4] = {1, 1, 1, 1};
+        r = g_encode_tiled(&op->tmC, out_t, 4, C, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(XTC_E_CUDA, "cuTensorMapEncodeTiled(y) failed: " + std::to_string((int)r));
+    } else if (p.sch.buffer_c) {
         const bool to_ws = p.split_k > 1;
         const int os = to_ws ? 4 : dsize(d.out_dtype);
         const CUtensorMapDataType out_t = os == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
@@ -559,6 +587,7 @@ static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cud
         tp.relu = p.relu_epi;
         tp.a3d = op->a3d;
         tp.debug_skip_mma = getenv("XTC_DEBUG_SKIP_MMA") != nullptr;   // diagnostics: output invalid
+        if (const char* sk = getenv("XTC_DEBUG_SKIP")) tp.debug_skip_mma = atoi(sk);   // bitmask, see TcParams
         tp.b3d = op->b3d;
         tp.buffer_c = p.sch.buffer_c;
         tp.atomic = p.atomic;
@@ -583,9 +612,23 @@ static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cud
             CU_TRY(cudaMemsetAsync(op->trace_dev, 0, trace_bytes, st), "trace clear");
             tp.trace = op->trace_dev;
         }
-        CU_TRY(launch_tc_gemm(tf32, d.kind == XTC_OP_CONV2D, p.cta_group, op->tmA, op->tmB, op->tmC, tp, p.grid_x, p.smem, st),
-               "tc_gemm launch");
-        ++launches;
+        if (p.halo) {
+            tp.wp = p.halo_wp;
+            tp.rt = p.halo_rt;
+            tp.msub = p.halo_msub;
+            tp.planes = p.halo_planes;
+            tp.nbuf = p.halo_nbuf;
+            tp.tpi = p.halo_tpi;
+            tp.patch_bytes = (uint32_t)p.halo_patch_bytes;
+            tp.plane_bytes = (uint32_t)(p.halo_patch_bytes / p.halo_planes);
+            CU_TRY(launch_tc_conv_halo(tf32, op->tmA, op->tmB, op->tmC, tp, p.grid_x, p.smem, st), "conv_halo launch");
+            ++launches;
+        } else {
+            CU_TRY(launch_tc_gemm(tf32, d.kind == XTC_OP_CONV2D, p.cta_group, op->tmA, op->tmB, op->tmC, tp, p.grid_x,
+                                  p.smem, st),
+                   "tc_gemm launch");
+            ++launches;
+        }
         if (tp.trace) {
             std::vector<uint64_t> h((size_t)kTraceCtas * kTraceSlots);
             CU_TRY(cudaMemcpyAsync(h.data(), op->trace_dev, trace_bytes, cudaMemcpyDeviceToHost, st), "trace D2H");

@@ -1,0 +1,418 @@
+// conv_halo.cu -- KB3h: stride-1 conv2d as implicit GEMM with the input packed once per
+// output tile (schedule knob pack_halo = 1), sm_100a tcgen05 (bf16 kind::f16 / tf32).
+//
+// The paper's pack primitive copies "the elements used below a given loop
+// level ... in the order of their access".  The im2col kernel (gemm_tc.cu) packs at the
+// k-block level: every filter tap (r, s) re-loads a 128 x C pixel block through the TMA
+// im2col unit, 9 loads per tile for a 3x3 filter.  Here the pack sits at the output-tile
+// level, above the (r, s, c) reduction loops: the tile's input window (tile rows + R - 1
+// rows of Wp pixel slots, zero-filled outside the image by TMA) is loaded once, and tap
+// (r, s) of virtual row v is patch row v + r*Wp + s -- the UMMA A operand of that tap is
+// the patch advanced by (r*Wp + s) 128-byte rows.  The 128-byte swizzle is anchored to
+// absolute SMEM addresses, so such views need no descriptor base offset
+// (profiles/r01_umma_row_shift_microtest.txt).
+//
+// Virtual rows: a 128-row UMMA tile is 128/Wp output rows x Wp slots, Wp the power of two
+// >= Q + S - 1.  Slots q >= Q and rows p >= P hold don't-care values and are never
+// written: the TMA store box {f, q, p, n} is clipped at the tensor edges, direct stores
+// test the bounds.
+//
+// Warp roles (256 threads): warp 0 = patch producer, warp 3 = B (filter) producer (ring,
+// or the whole filter once with b_resident), warp 1 = MMA issuer, warp 2 = TMEM
+// allocator, warps 4..7 = epilogue (TMEM lane quarters).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include "ptx.cuh"
+#include "xtc_internal.h"
+
+namespace xtc {
+
+template <bool TF32, int MSUB>
+__global__ void __launch_bounds__(kTcThreads, 1)
+tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmB,
+                    const __grid_constant__ CUtensorMap tmY, const TcParams p) {
+    constexpr int ATOM = TF32 ? 32 : 64;     // channels per 128-byte row
+    constexpr int UMMA_K = TF32 ? 8 : 16;
+
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t pad = (1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u;
+    uint8_t* smem = smem_raw + pad;
+    const bool b_res = p.b_resident != 0;
+    const int S = p.stages;
+    // [B: all k-blocks (b_resident) or an S-stage ring][patch buffers][epilogue staging][barriers]
+    uint8_t* sB = smem;
+    uint8_t* sP = sB + (size_t)(b_res ? p.kb_total : S) * p.b_stage_bytes;
+    uint8_t* sC = sP + (size_t)p.nbuf * p.patch_bytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sC + (p.buffer_c ? kTcEpiSmem : 0));
+    uint64_t* empty = full + 8;
+    uint64_t* pfull = empty + 8;
+    uint64_t* pempty = pfull + kHaloMaxPatchBufs;
+    uint64_t* tfull = pempty + kHaloMaxPatchBufs;
+    uint64_t* tempty = tfull + 2;
+    uint64_t* bfull = tempty + 2;                // resident filter: one barrier per k-block
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + kHaloMaxResidentKb);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    // XTC_TRACE (diagnostics): slot 0 entry, 1 setup done, 2 exit; 8+j patch j issued,
+    // 8+kTraceK+j patch j seen by the MMA warp, 8+2kTraceK+2j(+1) epilogue of tile j start/end
+    uint64_t* const trace = (p.trace && blockIdx.x < kTraceCtas) ? p.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
+    if (trace && threadIdx.x == 0) trace[0] = ptx::globaltimer();
+    if (warp == 0 && lane == 0) {
+        ptx::prefetch_tmap(&tmX);
+        ptx::prefetch_tmap(&tmB);
+        if (p.buffer_c) ptx::prefetch_tmap(&tmY);
+    }
+    if (warp == 1 && lane == 0) {
+        for (int s = 0; s < S; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
+        for (int i = 0; i < kHaloMaxPatchBufs; ++i) {
+            ptx::mbar_init(&pfull[i], 1);
+            ptx::mbar_init(&pempty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            ptx::mbar_init(&tfull[i], 1);
+            ptx::mbar_init(&tempty[i], 4);
+        }
+        for (int i = 0; i < kHaloMaxResidentKb; ++i) ptx::mbar_init(&bfull[i], 1);
+        ptx::fence_mbarrier_init();
+    }
+    if (warp == 2) {
+        ptx::tmem_alloc<1>(tmem_slot, p.tmem_cols);
+        ptx::tmem_relinquish<1>();
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const int acc_cols = MSUB * p.tile_n;        // TMEM columns of one accumulator buffer
+    if (trace && threadIdx.x == 0) trace[1] = ptx::globaltimer();
+    int tj = 0;                                  // per-role tile counter for the trace
+
+    // tile id -> (image, first output row, first output channel)
+    auto decode = [&](int64_t t, int& nimg, int& p0, int& n0) {
+        int mb, nb, ks;
+        tile_coords(p.tm, t, mb, nb, ks);
+        nimg = mb / p.tpi;
+        p0 = (mb - nimg * p.tpi) * p.rt * MSUB;
+        n0 = nb * p.tile_n;
+    };
+    auto load_b = [&](uint8_t* dst, uint64_t* bar, int kb, int n0) {
+        if (p.b3d) {
+            ptx::tma_load_3d(&tmB, dst, bar, 0, kb * p.tile_k, n0 / ATOM);
+        } else {
+            for (int b = 0; b < p.tile_n / ATOM; ++b)
+                ptx::tma_load_2d(&tmB, dst + (size_t)b * p.tile_k * 128, bar, n0 + b * ATOM, kb * p.tile_k);
+        }
+    };
+
+    if (warp == 0) {
+        // ===================== patch producer (pack at the tile level) =====================
+        int pb = 0;
+        uint32_t use_par = 0;
+        bool first_round = true;
+        for (int64_t t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+            int nimg, p0, n0;
+            decode(t, nimg, p0, n0);
+            const int cb = pb;
+            const uint32_t cpar = use_par;
+            const bool fresh = first_round;
+            if (++pb == p.nbuf) { pb = 0; use_par ^= 1u; first_round = false; }
+            if (!fresh) {
+                if (p.debug_skip_mma & 128) ptx::mbar_wait_sleep(&pempty[cb], cpar ^ 1u);
+                else ptx::mbar_wait(&pempty[cb], cpar ^ 1u);
+            }
+            if (trace && lane == 0 && tj < kTraceK) trace[8 + tj] = ptx::globaltimer();
+            ++tj;
+            if (p.debug_skip_mma & 2) {
+                if (ptx::elect_one()) ptx::mbar_arrive(&pfull[cb]);
+            } else if (ptx::elect_one()) {
+                ptx::mbar_arrive_expect_tx(&pfull[cb], p.patch_bytes);
+                uint8_t* dst = sP + (size_t)cb * p.patch_bytes;
+                // box {ATOM channels, Wp slots, rows, 1} at (plane, -pad_w, p0 - pad_h, n): the zero
+                // padding and the slots beyond the image are TMA's out-of-bounds zero fill
+                for (int pl = 0; pl < p.planes; ++pl)
+                    ptx::tma_load_4d(&tmX, dst + (size_t)pl * p.plane_bytes, &pfull[cb], pl * ATOM, -p.cg.pw,
+                                     p0 - p.cg.ph, nimg);
+            }
+            __syncwarp();
+        }
+    } else if (warp == 3) {
+        // ===================== filter (B) producer =====================
+        if (b_res) {
+            if (ptx::elect_one()) {
+                // one barrier per k-block: the first tile's MMAs start when k-block 0 lands
+                for (int kb = 0; kb < p.kb_total; ++kb) {
+                    ptx::mbar_arrive_expect_tx(&bfull[kb], p.b_stage_bytes);
+                    load_b(sB + (size_t)kb * p.b_stage_bytes, &bfull[kb], kb, 0);
+                }
+            }
+            __syncwarp();
+        } else {
+            int s = 0;
+            uint32_t use_par = 0;
+            bool first_round = true;
+            for (int64_t t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+                int nimg, p0, n0;
+                decode(t, nimg, p0, n0);
+                for (int kb = 0; kb < p.kb_total; ++kb) {
+                    const int cs = s;
+                    const uint32_t cpar = use_par;
+                    const bool fresh = first_round;
+                    if (++s == S) { s = 0; use_par ^= 1u; first_round = false; }
+                    if (!fresh) ptx::mbar_wait(&empty[cs], cpar ^ 1u);
+                    if (ptx::elect_one()) {
+                        ptx::mbar_arrive_expect_tx(&full[cs], p.b_stage_bytes);
+                        load_b(sB + (size_t)cs * p.b_stage_bytes, &full[cs], kb, n0);
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer (contraction over r, s, c) =====================
+        int s = 0, acc = 0, pb = 0;
+        uint32_t ph = 0, aph = 0, pph = 0;
+        const uint32_t b_lbo = (uint32_t)p.tile_k * 128u;
+        const uint64_t adesc0 = ptx::smem_desc_sw128(ptx::smem_u32(sP), 16, 1024);
+        const uint64_t bdesc0 = TF32 ? ptx::smem_desc_sw128(ptx::smem_u32(sB), b_lbo, 512, 1)
+                                     : ptx::smem_desc_sw128(ptx::smem_u32(sB), b_lbo, 1024, 2);
+        // Every loop bound and stride in registers, and ONE elected lane runs the whole tile
+        // (ring waits, UMMAs, commits) -- the warp reconverges once per tile, not per k-block.
+        // Every loop bound and stride is pinned in a register, ONE elected lane runs the whole
+        // tile (ring waits, UMMAs, commits), and an atom's MSUB x (ATOM/UMMA_K) UMMAs are
+        // straight-line code: the issue loop is a handful of instructions per 128-byte atom
+        // (short N=64 UMMAs take only ~48 cycles each, so issue overhead is exposed).
+        const uint32_t b_stage16 = ptx::pin(p.b_stage_bytes >> 4);
+        const uint32_t plane16 = ptx::pin(p.plane_bytes >> 4);
+        const uint32_t patch16 = ptx::pin(p.patch_bytes >> 4);
+        const int n_atoms = ptx::pin(p.tile_k / ATOM);
+        const int R_S = ptx::pin(p.cg.S), planes = ptx::pin(p.planes);
+        const uint32_t tile_n = ptx::pin((uint32_t)p.tile_n);
+        // A offset change (16-byte units) when the atom index wraps the channel planes, and
+        // when it also wraps the filter columns (next filter row: + Wp rows)
+        const uint32_t d_plane = plane16;
+        const uint32_t d_col = ptx::pin(8u - (uint32_t)(p.planes - 1) * plane16);
+        const uint32_t d_row = ptx::pin((uint32_t)p.wp * 8u - (uint32_t)(p.planes - 1) * plane16 -
+                                        (uint32_t)(p.cg.S - 1) * 8u);
+        const int kb_total = ptx::pin((p.debug_skip_mma & 33) ? 0 : p.kb_total);
+        const int Sring = ptx::pin(S);
+        const uint32_t idesc = ptx::pin(p.idesc);
+        const bool plain_arrive = (p.debug_skip_mma & 16) != 0;
+        const bool wait_tempty = !(p.debug_skip_mma & 64);
+        const int nbuf = p.nbuf, accb = p.acc_buffers;
+        bool b_landed = false;                        // resident filter fully in SMEM (after the first tile)
+        if (b_res && (p.debug_skip_mma & 256)) {      // diagnostics: wait for the whole filter up front
+            for (int kb = 0; kb < p.kb_total; ++kb) ptx::mbar_wait(&bfull[kb], 0);
+            b_landed = true;
+        }
+        for (int64_t t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+            if (wait_tempty) ptx::mbar_wait(&tempty[acc], aph ^ 1u);
+            ptx::mbar_wait(&pfull[pb], pph);
+            if (trace && lane == 0 && tj < kTraceK) trace[8 + kTraceK + tj] = ptx::globaltimer();
+            ++tj;
+            ptx::tc_fence_after();
+            if (ptx::elect_one()) {
+                const uint32_t d0 = tmem_base + (uint32_t)(acc * acc_cols);
+                const uint64_t apatch = adesc0 + (uint64_t)((uint32_t)pb * patch16);
+                // the next 128-byte atom: channel plane pl, filter column sx, A offset aoff
+                // (16-byte units) = pl*plane16 + (r*Wp + sx)*8
+                int sx = 0, pl = 0;
+                uint32_t aoff = 0;
+                uint32_t accf = 0;                    // 0 for the tile's first UMMA (overwrite)
+                auto atom = [&](uint64_t bd) {
+                    const uint64_t ad = apatch + (uint64_t)aoff;
+#pragma unroll
+                    for (int ms = 0; ms < MSUB; ++ms)
+#pragma unroll
+                        for (int kk = 0; kk < ATOM / UMMA_K; ++kk)
+                            ptx::umma<TF32, 1>(d0 + (uint32_t)ms * tile_n, ad + (uint64_t)(ms * 1024 + kk * 2),
+                                               bd + (uint64_t)(kk * UMMA_K * 8), idesc, kk ? 1u : accf);
+                    accf = 1u;
+                    const bool pw = ++pl == planes;             // plane wraps: next filter column
+                    pl = pw ? 0 : pl;
+                    sx += pw ? 1 : 0;
+                    const bool sw = sx == R_S;                  // column wraps: next filter row
+                    sx = sw ? 0 : sx;
+                    aoff += pw ? (sw ? d_row : d_col) : d_plane;
+                };
+                if (b_res) {
+                    // resident filter: k-block kb of B at kb * b_stage16, atom a at a*ATOM rows
+                    for (int kb = 0; kb < kb_total; ++kb) {
+                        if (!b_landed) {
+                            ptx::mbar_wait(&bfull[kb], 0);
+                            ptx::tc_fence_after();
+                        }
+                        const uint64_t bd = bdesc0 + (uint64_t)((uint32_t)kb * b_stage16);
+                        for (int a = 0; a < n_atoms; ++a) atom(bd + (uint64_t)(a * ATOM * 8));
+                    }
+                } else {
+                    int s1 = s;
+                    uint32_t ph1 = ph;
+                    for (int kb = 0; kb < kb_total; ++kb) {
+                        ptx::mbar_wait(&full[s1], ph1);
+                        ptx::tc_fence_after();
+                        const uint64_t bd = bdesc0 + (uint64_t)((uint32_t)s1 * b_stage16);
+                        for (int a = 0; a < n_atoms; ++a) atom(bd + (uint64_t)(a * ATOM * 8));
+                        ptx::umma_commit<1>(&empty[s1]);
+                        if (++s1 == Sring) { s1 = 0; ph1 ^= 1u; }
+                    }
+                }
+                if (plain_arrive) {                   // diagnostics: plain arrives (valid only without MMAs)
+                    ptx::mbar_arrive(&pempty[pb]);
+                    ptx::mbar_arrive(&tfull[acc]);
+                } else {
+                    ptx::umma_commit<1>(&pempty[pb]);     // patch buffer free once these MMAs finish
+                    ptx::umma_commit<1>(&tfull[acc]);
+                }
+            }
+            __syncwarp();
+            if (!b_res)                               // every lane advances the ring by kb_total slots
+                for (int kb = 0; kb < kb_total; ++kb)
+                    if (++s == S) { s = 0; ph ^= 1u; }
+            (void)nbuf; (void)accb;
+            b_landed = b_landed || kb_total > 0;
+            if (++pb == p.nbuf) { pb = 0; pph ^= 1u; }
+            if (++acc == p.acc_buffers) { acc = 0; aph ^= 1u; }
+        }
+    } else if (warp >= 4) {
+        // ===================== epilogue (bufferize) =====================
+        const int q = warp & 3;
+        int acc = 0, buf = 0;
+        uint32_t aph = 0;
+        uint8_t* stage = sC + q * (kTcEpiStageBytes * kTcEpiBuffers);
+        const bool bf16_out = p.out_bf16 != 0;
+        const int P = p.cg.P, Q = p.cg.Q;
+        for (int64_t t = blockIdx.x; t < ((p.debug_skip_mma & 64) ? 0 : p.num_tiles); t += gridDim.x) {
+            int nimg, p0, n0;
+            decode(t, nimg, p0, n0);
+            if (p.debug_skip_mma & 128) ptx::mbar_wait_sleep(&tfull[acc], aph);
+            else ptx::mbar_wait(&tfull[acc], aph);
+            if (trace && warp == 4 && lane == 0 && tj < kTraceTiles) trace[8 + 2 * kTraceK + 2 * tj] = ptx::globaltimer();
+            ptx::tc_fence_after();
+            for (int ms = 0; ms < ((p.debug_skip_mma & 8) ? 0 : MSUB); ++ms) {
+                const int v0 = ms * 128 + 32 * q;              // first virtual row of this warp
+                const int prow0 = p0 + v0 / p.wp, q0 = v0 % p.wp;
+                const int v = v0 + lane;
+                const int prow = p0 + v / p.wp, qcol = v % p.wp;
+                const bool valid = prow < P && qcol < Q;
+                const bool any_valid = prow0 < P;              // rows grow with the lane index
+                const uint32_t t_row = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * acc_cols + ms * p.tile_n);
+                for (int c = 0; c < p.tile_n; c += 32) {
+                    uint32_t vals[32];
+                    ptx::tmem_ld_32x32b_x32(t_row + c, vals);
+                    ptx::tmem_ld_wait();
+                    if (!any_valid || (p.debug_skip_mma & 4)) continue;   // warp-uniform
+                    if (p.relu) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) vals[j] = __float_as_uint(fmaxf(__uint_as_float(vals[j]), 0.f));
+                    }
+                    if (p.buffer_c) {
+                        // one 128-byte staging row per thread (virtual row order = the TMA box's
+                        // [p][q] order), then one clipped 4-D TMA store per warp
+                        const bool first_half = !bf16_out || ((c & 63) == 0);
+                        if (first_half) {
+                            if (lane == 0) ptx::bulk_wait_read<1>();
+                            __syncwarp();
+                        }
+                        uint8_t* rowp = stage + buf * kTcEpiStageBytes + lane * 128;
+                        if (bf16_out) {
+                            const int cbase = (c & 63) ? 4 : 0;
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                uint4 w;
+                                w.x = ptx::pack_bf16x2(__uint_as_float(vals[8 * j + 0]), __uint_as_float(vals[8 * j + 1]));
+                                w.y = ptx::pack_bf16x2(__uint_as_float(vals[8 * j + 2]), __uint_as_float(vals[8 * j + 3]));
+                                w.z = ptx::pack_bf16x2(__uint_as_float(vals[8 * j + 4]), __uint_as_float(vals[8 * j + 5]));
+                                w.w = ptx::pack_bf16x2(__uint_as_float(vals[8 * j + 6]), __uint_as_float(vals[8 * j + 7]));
+                                *reinterpret_cast<uint4*>(rowp + (((cbase + j) ^ (lane & 7)) * 16)) = w;
+                            }
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 8; ++j)
+                                *reinterpret_cast<uint4*>(rowp + ((j ^ (lane & 7)) * 16)) =
+                                    make_uint4(vals[4 * j], vals[4 * j + 1], vals[4 * j + 2], vals[4 * j + 3]);
+                        }
+                        const bool last_half = !bf16_out || ((c & 63) == 32) || (c + 32 >= p.tile_n);
+                        if (last_half) {
+                            ptx::fence_proxy_async_smem();
+                            __syncwarp();
+                            if (lane == 0) {
+                                const int col = bf16_out ? (n0 + (c & ~63)) : (n0 + c);
+                                ptx::tma_store_4d(&tmY, stage + buf * kTcEpiStageBytes, col, q0, prow0, nimg);
+                                ptx::bulk_commit();
+                            }
+                            buf ^= 1;
+                        }
+                    } else if (valid) {
+                        const int64_t m = ((int64_t)nimg * P + prow) * Q + qcol;
+                        const int64_t col0 = (int64_t)n0 + c;
+                        const int ncols = (int)((p.N - col0) < 32 ? (p.N - col0) : 32);
+                        if (bf16_out) {
+                            uint16_t* dst = reinterpret_cast<uint16_t*>(p.C) + m * p.ldc + col0;
+                            if (ncols == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+#pragma unroll
+                                for (int j = 0; j < 4; ++j) {
+                                    uint4 w;
+                                    w.x = ptx::pack_bf16x2(__uint_as_float(vals[8 * j + 0]), __uint_as_float(vals[8 * j + 1]));
+                                    w.y = ptx::pack_bf16x2(__uint_as_float(vals[8 * j + 2]), __uint_as_float(vals[8 * j + 3]));
+                                    w.z = ptx::pack_bf16x2(__uint_as_float(vals[8 * j + 4]), __uint_as_float(vals[8 * j + 5]));
+                                    w.w = ptx::pack_bf16x2(__uint_as_float(vals[8 * j + 6]), __uint_as_float(vals[8 * j + 7]));
+                                    reinterpret_cast<uint4*>(dst)[j] = w;
+                                }
+                            } else {
+                                for (int j = 0; j < ncols; ++j)
+                                    dst[j] = (uint16_t)(ptx::pack_bf16x2(__uint_as_float(vals[j]), 0.f) & 0xFFFFu);
+                            }
+                        } else {
+                            float* dst = reinterpret_cast<float*>(p.C) + m * p.ldc + col0;
+                            if (ncols == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+#pragma unroll
+                                for (int j = 0; j < 8; ++j)
+                                    reinterpret_cast<uint4*>(dst)[j] =
+                                        make_uint4(vals[4 * j], vals[4 * j + 1], vals[4 * j + 2], vals[4 * j + 3]);
+                            } else {
+                                for (int j = 0; j < ncols; ++j) dst[j] = __uint_as_float(vals[j]);
+                            }
+                        }
+                    }
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (trace && warp == 4 && lane == 0 && tj < kTraceTiles) trace[8 + 2 * kTraceK + 2 * tj + 1] = ptx::globaltimer();
+            ++tj;
+            if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+            if (++acc == p.acc_buffers) { acc = 0; aph ^= 1u; }
+        }
+        if (p.buffer_c && lane == 0) ptx::bulk_wait<0>();
+    }
+
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (trace && threadIdx.x == 0) trace[2] = ptx::globaltimer();
+    if (warp == 2) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<1>(tmem_base, p.tmem_cols);
+    }
+}
+
+template <bool TF32, int MSUB>
+static cudaError_t launch_halo_t(const CUtensorMap& x, const CUtensorMap& b, const CUtensorMap& y, const TcParams& p,
+                                 int grid, int smem, cudaStream_t st) {
+    auto k = tc_conv_halo_kernel<TF32, MSUB>;
+    cudaError_t e = ensure_smem_attr(k, smem);
+    if (e != cudaSuccess) return e;
+    k<<<grid, kTcThreads, smem, st>>>(x, b, y, p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tc_conv_halo(bool tf32, const CUtensorMap& x, const CUtensorMap& b, const CUtensorMap& y,
+                                const TcParams& p, int grid, int smem, cudaStream_t st) {
+    // MSUB (128-row UMMA tiles per patch) is a template parameter: the per-atom UMMA
+    // sequence is straight-line code
+    if (p.msub == 2)
+        return tf32 ? launch_halo_t<true, 2>(x, b, y, p, grid, smem, st) : launch_halo_t<false, 2>(x, b, y, p, grid, smem, st);
+    return tf32 ? launch_halo_t<true, 1>(x, b, y, p, grid, smem, st) : launch_halo_t<false, 1>(x, b, y, p, grid, smem, st);
+}
+
+}  // namespace xtc

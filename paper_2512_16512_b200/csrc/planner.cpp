@@ -91,6 +91,7 @@ static xtc_status plan_simt(const xtc_op_desc& d, const xtc_schedule& s, int num
     if (s.cluster_m > 1) ILLEGAL("SIMT engine: cluster_m must be 1");
     if (s.pack_warps > 1) ILLEGAL("SIMT engine: pack_warps must be 0 or 1 (all threads pack)");
     if (s.b_resident) ILLEGAL("SIMT engine: b_resident must be 0");
+    if (s.pack_halo) ILLEGAL("SIMT engine: pack_halo must be 0");
     if (V == 4 && (s.tile_n + s.swizzle) % 4) ILLEGAL("vectorize: vector_n 4 needs (tile_n + pad) %% 4 == 0 for aligned float4");
     auto r4 = [](int x) { return (x + 3) / 4 * 4; };
     int smem = st * (r4(s.tile_k * (s.tile_m + s.swizzle)) + r4(s.tile_k * (s.tile_n + s.swizzle))) * 4;
@@ -110,8 +111,104 @@ static xtc_status plan_simt(const xtc_op_desc& d, const xtc_schedule& s, int num
     return XTC_OK;
 }
 
+// pack at the output-tile level for stride-1 conv2d (pack_halo = 1).  A tile is tile_m
+// "virtual rows" = (tile_m / Wp) output rows x Wp pixel slots, Wp = the power of two
+// >= max(8, Q + S - 1) dividing 128; slots q >= Q and rows p >= P are computed on
+// don't-care data and never stored.  The patch holds tile rows + R - 1 input rows of Wp
+// pixels starting at (p0 - pad_h, -pad_w) for every 128-byte channel plane; TMA
+// zero-fills everything outside the image (the zero padding).  Tap (r, s) of virtual row
+// v reads patch row v + r*Wp + s, so each UMMA's A operand is the patch advanced by
+// (r*Wp + s) 128-byte rows (profiles/r01_umma_row_shift_microtest.txt).
+static xtc_status plan_tc_halo(const xtc_op_desc& d, const xtc_schedule& s, int num_sms, Plan& p, std::string& why) {
+    const int es = dtype_size(d.in_dtype), os = dtype_size(d.out_dtype);
+    if (d.kind != XTC_OP_CONV2D) ILLEGAL("pack_halo applies to conv2d only");
+    if (s.pack_halo != 1) ILLEGAL("pack_halo must be 0 or 1");
+    if (d.stride_h != 1 || d.stride_w != 1) ILLEGAL("pack_halo needs stride 1 (taps must be row shifts of one patch)");
+    if (s.cluster_m > 1) ILLEGAL("pack_halo: cluster_m must be 1");
+    if (p.split_k != 1) ILLEGAL("pack_halo: split_k must be 1");
+    if (s.pack_warps > 1) ILLEGAL("pack_halo: pack_warps must be 0 or 1 (warp 0 packs patches, warp 3 the B ring)");
+    if (s.tile_m != 128 && s.tile_m != 256) ILLEGAL("pack_halo: tile_m must be 128 or 256 (1 or 2 UMMA M-tiles per patch)");
+    if (s.inner_m != 0 && s.inner_m != 128) ILLEGAL("pack_halo: inner_m (UMMA M) must be 128");
+    if (s.inner_n != 0 && s.inner_n != s.tile_n) ILLEGAL("tcgen05 inner_n (UMMA N) must equal tile_n");
+    if (s.tile_n < p.atom_n || s.tile_n > 256 || s.tile_n % p.atom_n)
+        ILLEGAL("tcgen05 tile_n must be a multiple of %d in [%d,256]", p.atom_n, p.atom_n);
+    if (s.tile_k < p.atom_k || s.tile_k > 256 || s.tile_k % p.atom_k)
+        ILLEGAL("tcgen05 tile_k must be a multiple of %d in [%d,256] (128-byte swizzle atom)", p.atom_k, p.atom_k);
+    if (s.unroll_k > 1) ILLEGAL("tcgen05 unroll_k must be 0 or 1");
+    if (s.vector_n > 1) ILLEGAL("tcgen05 vector_n must be 0");
+    if (s.stages < 2 || s.stages > 8) ILLEGAL("tcgen05 stages must be in [2,8]");
+    if (s.swizzle != 0 && s.swizzle != 128) ILLEGAL("tcgen05 swizzle must be 128 (0 = default 128)");
+    if (d.c % p.atom_k) ILLEGAL("tcgen05 conv2d needs C %% %d == 0", p.atom_k);
+    if ((d.f * es) % 16 || (d.f * os) % 16) ILLEGAL("TMA needs 16-byte row pitch for the filter and the output");
+    if (p.K % s.tile_k) ILLEGAL("tcgen05 conv2d needs R*S*C %% tile_k == 0");
+    int64_t P, Q, M_, N_, K_;
+    gemm_view(d, M_, N_, K_, P, Q);
+    int wp = 8;
+    while (wp < Q + d.s - 1) wp *= 2;
+    if (wp > 128) ILLEGAL("pack_halo: Q + S - 1 = %lld pixel slots exceed one 128-row UMMA tile", (long long)(Q + d.s - 1));
+    const int msub = s.tile_m / 128;
+    const int rt = 128 / wp;                               // output rows per UMMA M-tile
+    const int64_t pr = (int64_t)msub * rt + d.r - 1;       // patch rows
+    if (pr > 256) ILLEGAL("pack_halo: %lld patch rows exceed the 256-row TMA box", (long long)pr);
+    const int accb = s.acc_buffers == 0 ? 1 : s.acc_buffers;
+    if (accb < 1 || accb > 2) ILLEGAL("acc_buffers must be 1 or 2");
+    int alloc = 32;
+    while (alloc < accb * msub * s.tile_n) alloc *= 2;
+    if (alloc > 512) ILLEGAL("bufferize: %d TMEM columns (acc_buffers x tile_m/128 x tile_n) exceed 512", alloc);
+    p.tmem_cols = alloc;
+    const int64_t planes = d.c / p.atom_k;
+    const int64_t patch = planes * pr * wp * 128;
+    const int64_t b_stage = (int64_t)s.tile_k * s.tile_n * es;
+    p.tiles_n = (int)cdiv(N_, s.tile_n);
+    p.kb_total = (int)cdiv(K_, s.tile_k);
+    int64_t b_bytes;
+    if (s.b_resident) {
+        if (s.b_resident != 1) ILLEGAL("b_resident must be 0 or 1");
+        if (p.tiles_n != 1) ILLEGAL("pack: b_resident needs a single N tile (N <= tile_n)");
+        if (p.kb_total > kHaloMaxResidentKb)
+            ILLEGAL("pack_halo: b_resident supports at most %d k-blocks (one barrier each)", kHaloMaxResidentKb);
+        b_bytes = p.kb_total * b_stage;
+    } else {
+        b_bytes = s.stages * b_stage;
+    }
+    const int64_t fixed = b_bytes + (s.buffer_c ? kTcEpiSmem : 0) + kSmemReserve;
+    // two patch buffers when they fit: measured on B200, a third buffer in flight slows the
+    // tile (its TMA writes compete with the UMMA operand reads for the SMEM port)
+    int nbuf = 2;
+    if (const char* e = getenv("XTC_HALO_NBUF")) nbuf = std::max(1, std::min(kHaloMaxPatchBufs, atoi(e)));   // diagnostics
+    while (nbuf > 1 && fixed + nbuf * patch > kSmemMaxOptin) --nbuf;
+    if (fixed + nbuf * patch > kSmemMaxOptin)
+        ILLEGAL("pack_halo: patch %lld B + B operand %lld B + epilogue exceed %d B SMEM", (long long)patch,
+                (long long)b_bytes, kSmemMaxOptin);
+    if (s.buffer_c && d.out_dtype == XTC_BF16 && s.tile_n % 64) ILLEGAL("bufferize: bf16 TMA-store staging needs tile_n %% 64 == 0");
+    p.smem = (int)(fixed + nbuf * patch);
+    p.halo = true;
+    p.halo_wp = wp;
+    p.halo_rt = rt;
+    p.halo_msub = msub;
+    p.halo_pr = (int)pr;
+    p.halo_planes = (int)planes;
+    p.halo_nbuf = nbuf;
+    p.halo_patch_bytes = patch;
+    p.halo_tpi = (int)cdiv(P, (int64_t)rt * msub);
+    p.tiles_m = (int)(d.batch * p.halo_tpi);
+    p.kb_per_split = p.kb_total;
+    p.k_per_split = (int64_t)p.kb_per_split * s.tile_k;
+    p.num_tiles = (int64_t)p.tiles_m * p.tiles_n;
+    if (p.num_tiles >= (1ll << 31)) ILLEGAL("too many tiles");
+    p.cta_group = 1;
+    p.block = kTcThreads;
+    p.cluster = 1;
+    p.grid_x = s.persistent ? (int)std::min<int64_t>(p.num_tiles, num_sms) : (int)p.num_tiles;
+    return XTC_OK;
+}
+
 static xtc_status plan_tc(const xtc_op_desc& d, const xtc_schedule& s, int num_sms, Plan& p, std::string& why) {
     if (d.in_dtype != XTC_BF16 && d.in_dtype != XTC_TF32) ILLEGAL("tcgen05 engine needs BF16 or TF32 inputs");
+    if (s.pack_halo) {
+        p.atom_k = p.atom_n = 128 / dtype_size(d.in_dtype);
+        return plan_tc_halo(d, s, num_sms, p, why);
+    }
     int es = dtype_size(d.in_dtype);
     p.atom_k = 128 / es;          // elements per 128-byte swizzle row
     p.atom_n = 128 / es;
@@ -225,8 +322,7 @@ xtc_status make_plan(const xtc_op_desc& d, const xtc_schedule& s, int num_sms, P
         p.tail_grid_y = (int)cdiv(M, 16);
         if (d.in_dtype != XTC_F32 && d.in_dtype != XTC_BF16 && d.in_dtype != XTC_TF32) ILLEGAL("bad dtype");
     }
-    for (int i = 0; i < 2; ++i)
-        if (s.reserved[i]) ILLEGAL("reserved schedule fields must be 0");
+    if (s.reserved[0]) ILLEGAL("reserved schedule fields must be 0");
     // fuse: the consumer runs in the producer's epilogue, in the split-K
     // reduction (which produces the complete sums), or as its own elementwise pass
     if (s.fuse != 0 && s.fuse != 1) ILLEGAL("fuse must be 0 or 1");

@@ -65,6 +65,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     }
 }
 
+// Wait for waiters off the critical path (epilogue, producers of far-ahead stages): back
+// off with nanosleep between polls so spinning warps do not crowd the issue slots and the
+// shared sync/MIO path of the warp that feeds the tensor core.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    uint32_t addr = smem_u32(bar);
+    if (mbar_try_wait(addr, parity)) return;
+    uint64_t t0 = globaltimer();
+    uint32_t n = 0;
+    while (!mbar_try_wait(addr, parity)) {
+        __nanosleep(64);
+        if ((++n & 1023u) == 0 && globaltimer() - t0 > XTC_WATCHDOG_NS) {
+            printf("xtc watchdog: mbarrier wait timed out (block %d thread %d parity %u)\n",
+                   blockIdx.x, threadIdx.x, parity);
+            __trap();
+        }
+    }
+}
+
 // ---------------------------------------------------------------- TMA ----
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* m) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
@@ -104,6 +122,26 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* m, const void* s
     asm volatile(
         "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];"
         ::"l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+
+// 4-D tiled (not im2col) load / store: the haloed conv patch {c, w, h, n} and the NPQF
+// output box {f, q, p, n}; out-of-bounds elements are zero-filled on load, clipped on store.
+__device__ __forceinline__ void tma_load_4d(const CUtensorMap* m, void* dst, uint64_t* bar, int32_t c0, int32_t c1,
+                                            int32_t c2, int32_t c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2];"
+        ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2),
+          "r"(c3)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* m, const void* src, int32_t c0, int32_t c1, int32_t c2,
+                                             int32_t c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];"
+        ::"l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
         : "memory");
 }
 
@@ -267,6 +305,19 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     uint32_t r;
     asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
     return r;
+}
+
+// Pin a loop-invariant value in a register: the compiler otherwise re-loads kernel
+// parameters from the constant bank inside hot loops (a dependent LDC -> compare -> branch
+// chain per use), which dominates a single-thread MMA-issue loop with short UMMAs.
+template <typename T>
+__device__ __forceinline__ T pin(T v) {
+    static_assert(sizeof(T) == 4, "pin: 32-bit values");
+    uint32_t u;
+    memcpy(&u, &v, 4);
+    asm volatile("" : "+r"(u));
+    memcpy(&v, &u, 4);
+    return v;
 }
 
 __device__ __forceinline__ uint32_t elect_one() {

@@ -23,6 +23,8 @@ constexpr int kTcThreads = 256;             // warp0 TMA, warp1 MMA, warp2 TMEM 
 constexpr int kTcEpiStageBytes = 4096;      // one warp's 32 rows x 128 B output staging chunk
 constexpr int kTcEpiBuffers = 2;            // double-buffered per warp
 constexpr int kTcEpiSmem = 4 * kTcEpiStageBytes * kTcEpiBuffers;
+constexpr int kHaloMaxPatchBufs = 4;        // conv_halo: patch buffers (planner fits as many as SMEM allows)
+constexpr int kHaloMaxResidentKb = 32;      // conv_halo: resident-filter k-blocks (one mbarrier each)
 
 // cudaFuncSetAttribute is a driver round trip: set the dynamic-SMEM opt-in once
 // per kernel variant and device, not on every launch (sweeps launch thousands).
@@ -96,6 +98,12 @@ struct Plan {
     bool has_tail = false;
     int64_t tail_n0 = 0, tail_n = 0;
     int32_t tail_grid_x = 0, tail_grid_y = 0;
+    // pack_halo conv (planner.cpp plan_tc_halo): Wp pixel slots per output row, rt output
+    // rows per 128-row UMMA tile, msub UMMA tiles per CTA tile, pr patch rows, planes
+    // 128-byte channel planes, nbuf patch buffers, tpi tiles per image
+    bool halo = false;
+    int32_t halo_wp = 0, halo_rt = 0, halo_msub = 0, halo_pr = 0, halo_planes = 0, halo_nbuf = 0, halo_tpi = 0;
+    int64_t halo_patch_bytes = 0;
 };
 
 // Host-only: legality + plan derivation.  Returns XTC_OK or an error with reason.
@@ -133,13 +141,17 @@ struct TcParams {
     int32_t b_resident;      // all of B packed once per CTA (kb_total x b_stage_bytes before the A ring)
     int32_t relu;            // fused consumer in the epilogue
     int32_t a3d, b3d;        // one 3-D TMA per stage for all 128-B atoms of A / B (tmA / tmB are 3-D maps)
-    int32_t debug_skip_mma;  // diagnostics only (XTC_DEBUG_SKIP_MMA): commits without MMAs, output invalid
+    int32_t debug_skip_mma;  // diagnostics only, output invalid: XTC_DEBUG_SKIP_MMA, or XTC_DEBUG_SKIP=mask
+                             // (conv_halo: 1 no MMAs, 2 no patch TMA, 4 no output stores)
     int64_t ldc, ws_ld;
     void* C; float* Wk;
     uint32_t idesc;
     uint32_t tmem_cols;
     uint32_t a_stage_bytes, b_stage_bytes;
     ConvGeom cg;
+    // pack_halo conv only (see Plan)
+    int32_t wp, rt, msub, planes, nbuf, tpi;
+    uint32_t patch_bytes, plane_bytes;
     // Diagnostics (XTC_TRACE): %globaltimer stamps for CTAs < kTraceCtas, laid out
     // [cta][kTraceSlots]: slot 0 kernel entry, 1 setup done; producer issue of k-block i at
     // 8+i, MMA full-wait done at 8+kTraceK+i, epilogue tile j start/end at 8+2kTraceK+2j(+1).

@@ -158,6 +158,50 @@ def test_tc_conv_split_k_and_stride2():
     run_conv(d2, "bf16", "f32", tc(tile_n=128, buffer_c=0), MODE_INT)
 
 
+# pack_halo: the input packed once per output tile, filter taps as row-shifted views
+HALO_CASES = [
+    # (batch, h, w, c, f, r, s, pad, in, out, schedule overrides)            Wp  rows/UMMA tile
+    ((2, 56, 56, 64, 64, 3, 3, 1, "bf16", "bf16"), dict(tile_n=64, b_resident=1, stages=2)),               # 64  2
+    ((2, 56, 56, 64, 64, 3, 3, 1, "bf16", "bf16"), dict(tile_m=256, tile_n=64, b_resident=1, stages=2)),   # 64  2x2
+    ((3, 14, 14, 256, 256, 3, 3, 1, "bf16", "bf16"), dict(tile_n=128, stages=4)),                          # 16  8
+    ((3, 14, 14, 256, 256, 3, 3, 1, "bf16", "bf16"), dict(tile_n=256, tile_k=64, stages=2, buffer_c=0)),
+    ((2, 9, 13, 64, 64, 3, 3, 1, "bf16", "f32"), dict(tile_n=64, stages=3)),                               # 16  ragged
+    ((1, 20, 20, 64, 128, 5, 5, 2, "bf16", "bf16"), dict(tile_n=128, stages=3, acc_buffers=1)),            # 32  4
+    ((2, 7, 7, 128, 64, 1, 1, 0, "bf16", "bf16"), dict(tile_n=64, stages=2, tile_m=256)),                  # 8   16x2
+    ((1, 10, 10, 64, 64, 3, 3, 0, "bf16", "f32"), dict(tile_n=64, stages=2, buffer_c=0)),                  # 16  pad 0
+    ((1, 3, 100, 64, 64, 3, 3, 1, "bf16", "bf16"), dict(tile_n=64, stages=2)),                             # 128 1
+    ((2, 14, 14, 64, 64, 3, 3, 1, "tf32", "f32"), dict(tile_n=64, tile_k=32, stages=4)),                   # tf32: 2 planes
+]
+
+
+@pytest.mark.parametrize("case", HALO_CASES, ids=[f"{c[0][:8]}-{i}" for i, c in enumerate(HALO_CASES)])
+@pytest.mark.parametrize("mode", [MODE_INT, MODE_UNIFORM])
+def test_tc_conv_pack_halo(case, mode):
+    (b, h, w, c, f, r, s, pad, idt, odt), kw = case
+    d = xtc.conv2d_desc(b, h, w, c, f, r, s, 1, pad, idt, odt)
+    base = dict(pack_halo=1, tile_m=128, tile_k=64, persistent=1, acc_buffers=2, buffer_c=1)
+    base.update(kw)
+    run_conv(d, idt, odt, tc(**base), mode)
+
+
+def run_conv_relu(d, sch, seed=30):
+    import oracle as _o
+    x = dev_tensor((d.batch, d.h, d.w, d.c), "bf16", seed, MODE_INT)
+    w = dev_tensor((d.r, d.s, d.c, d.f), "bf16", seed + 1, MODE_INT)
+    M, N, K = xtc.gemm_view(d)
+    y = torch.full((M, N), float("nan"), dtype=torch.bfloat16, device="cuda:0")
+    xtc.Op(d).apply(sch).run(x, w, y)
+    torch.cuda.synchronize()
+    O, D = oracle_conv(d, "bf16", MODE_INT, seed, seed + 1)
+    check_against_oracle(y, _o.relu(O), D, "bf16", True, 0.0)
+
+
+def test_tc_conv_pack_halo_fused_relu_and_grid_modes():
+    d = xtc.conv2d_desc(2, 56, 56, 64, 64, 3, 3, 1, 1, "bf16", "bf16", consumer="relu")
+    for extra in (dict(fuse=1, persistent=1), dict(fuse=1, persistent=0, acc_buffers=1), dict(fuse=0)):
+        run_conv_relu(d, tc(pack_halo=1, tile_n=64, stages=3, **extra))
+
+
 def test_simt_conv_fp32():
     d = xtc.conv2d_desc(2, 14, 14, 16, 32, 3, 3, 1, 1, "f32", "f32")
     sch = S(engine=0, tile_m=64, tile_n=32, tile_k=16, inner_m=4, inner_n=4, unroll_k=4, vector_n=4, stages=2)

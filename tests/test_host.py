@@ -136,6 +136,48 @@ def test_conv_legality_and_plan():
     assert st == xtc.XTC_E_ILLEGAL_SCHEDULE
 
 
+HALO = dict(engine=1, tile_m=128, tile_n=64, tile_k=64, stages=2, buffer_c=1, acc_buffers=2, persistent=1,
+            pack_halo=1)
+
+
+def test_pack_halo_plan():
+    """Tile counts follow from Wp = pow2 >= Q+S-1 slots and 128/Wp output rows per UMMA tile."""
+    l56 = xtc.conv2d_desc(32, 56, 56, 64, 64)
+    st, info, why = chk(l56, **dict(HALO, b_resident=1))
+    assert st == xtc.XTC_OK, why
+    assert info.num_tiles == 32 * 28 and info.grid_x == 148 and info.tmem_cols == 128
+    # resident filter 9 x 8 KiB + 2 patches of 4 rows x 64 slots x 128 B + epilogue staging
+    assert info.smem_bytes == 9 * 8192 + 2 * 4 * 64 * 128 + 32768 + 2048
+    st, info, why = chk(l56, **dict(HALO, tile_m=256, b_resident=1))
+    assert st == xtc.XTC_OK and info.num_tiles == 32 * 14 and info.tmem_cols == 256, why
+    l14 = xtc.conv2d_desc(32, 14, 14, 256, 256)
+    st, info, why = chk(l14, **dict(HALO, tile_n=128, stages=4))
+    assert st == xtc.XTC_OK and info.num_tiles == 32 * 2 * 2, why
+    one = xtc.conv2d_desc(2, 7, 7, 128, 64, 1, 1, 1, 0)        # 1x1: Wp = 8, 16 rows per tile
+    st, info, why = chk(one, **HALO)
+    assert st == xtc.XTC_OK and info.num_tiles == 2, why
+
+
+@pytest.mark.parametrize("desc,kw,frag", [
+    (xtc.conv2d_desc(2, 15, 17, 64, 128, 3, 3, 2, 1), {}, "stride 1"),
+    (xtc.matmul_desc(256, 256, 256), {}, "conv2d only"),
+    (xtc.conv2d_desc(2, 56, 56, 64, 64), dict(cluster_m=2, tile_m=256), "cluster_m"),
+    (xtc.conv2d_desc(2, 56, 56, 64, 64), dict(split_k=3), "split_k"),
+    (xtc.conv2d_desc(2, 56, 56, 64, 64), dict(pack_warps=2), "pack_warps"),
+    (xtc.conv2d_desc(1, 4, 200, 64, 64), {}, "slots"),
+    (xtc.conv2d_desc(2, 56, 56, 64, 64), dict(tile_m=384), "tile_m"),
+    (xtc.conv2d_desc(2, 56, 56, 64, 64), dict(pack_halo=2), "pack_halo"),
+    (xtc.conv2d_desc(2, 56, 56, 256, 256), dict(tile_m=256, tile_n=256, acc_buffers=1, stages=8), "SMEM"),
+])
+def test_pack_halo_legality(desc, kw, frag):
+    args = dict(HALO)
+    args.update(kw)
+    st, _, why = chk(desc, **args)
+    assert st == xtc.XTC_E_ILLEGAL_SCHEDULE and frag in why, (st, why)
+    st, _, why = chk(desc, engine=0, tile_m=32, tile_n=32, tile_k=8, inner_m=2, inner_n=2, pack_halo=1)
+    assert st != xtc.XTC_OK
+
+
 def test_default_schedules_are_legal():
     for d in (MM, xtc.matmul_desc(8192, 8192, 8192), xtc.conv2d_desc(32, 56, 56, 64, 64),
               xtc.conv2d_desc(32, 14, 14, 256, 256), xtc.matmul_desc(32, 32, 32, "f32", "f32"),
