@@ -200,11 +200,8 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
         const bool plain_arrive = (p.debug_skip_mma & 16) != 0;
         const bool wait_tempty = !(p.debug_skip_mma & 64);
         const int nbuf = p.nbuf, accb = p.acc_buffers;
-        bool b_landed = false;                        // resident filter fully in SMEM (after the first tile)
-        if (b_res && (p.debug_skip_mma & 256)) {      // diagnostics: wait for the whole filter up front
+        if (b_res)                                    // the resident filter (per-k-block barriers)
             for (int kb = 0; kb < p.kb_total; ++kb) ptx::mbar_wait(&bfull[kb], 0);
-            b_landed = true;
-        }
         for (int64_t t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
             if (wait_tempty) ptx::mbar_wait(&tempty[acc], aph ^ 1u);
             ptx::mbar_wait(&pfull[pb], pph);
@@ -238,10 +235,6 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
                 if (b_res) {
                     // resident filter: k-block kb of B at kb * b_stage16, atom a at a*ATOM rows
                     for (int kb = 0; kb < kb_total; ++kb) {
-                        if (!b_landed) {
-                            ptx::mbar_wait(&bfull[kb], 0);
-                            ptx::tc_fence_after();
-                        }
                         const uint64_t bd = bdesc0 + (uint64_t)((uint32_t)kb * b_stage16);
                         for (int a = 0; a < n_atoms; ++a) atom(bd + (uint64_t)(a * ATOM * 8));
                     }
@@ -270,7 +263,6 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
                 for (int kb = 0; kb < kb_total; ++kb)
                     if (++s == S) { s = 0; ph ^= 1u; }
             (void)nbuf; (void)accb;
-            b_landed = b_landed || kb_total > 0;
             if (++pb == p.nbuf) { pb = 0; pph ^= 1u; }
             if (++acc == p.acc_buffers) { acc = 0; aph ^= 1u; }
         }

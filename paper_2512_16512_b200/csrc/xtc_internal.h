@@ -23,7 +23,7 @@ constexpr int kTcThreads = 256;             // warp0 TMA, warp1 MMA, warp2 TMEM 
 constexpr int kTcEpiStageBytes = 4096;      // one warp's 32 rows x 128 B output staging chunk
 constexpr int kTcEpiBuffers = 2;            // double-buffered per warp
 constexpr int kTcEpiSmem = 4 * kTcEpiStageBytes * kTcEpiBuffers;
-constexpr int kHaloMaxPatchBufs = 4;        // conv_halo: patch buffers (planner fits as many as SMEM allows)
+constexpr int kHaloMaxPatchBufs = 2;        // conv_halo: patch buffers (at most; the planner fits what SMEM allows)
 constexpr int kHaloMaxResidentKb = 32;      // conv_halo: resident-filter k-blocks (one mbarrier each)
 
 // cudaFuncSetAttribute is a driver round trip: set the dynamic-SMEM opt-in once
