@@ -28,6 +28,7 @@
 // 128 TMEM lanes and arrives on the leader's tmem-empty barrier.
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <type_traits>
 #include "ptx.cuh"
 #include "xtc_internal.h"
 
@@ -214,14 +215,12 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         }
     } else if (warp == 1) {
         // ===================== MMA issuer (contraction) =====================
-        // The whole warp runs the loop (its values are warp-uniform, so they live in
-        // uniform registers); one elected lane issues the MMAs and the commits.
+        // One elected lane runs each tile's whole k-loop (stage waits, UMMAs, commits); the
+        // warp reconverges once per tile.  Loop bounds and strides are pinned in registers
+        // and the atoms of a stage are a compile-time count (NA), so a stage is straight-line
+        // code: with short UMMAs (N = 64: ~48 cycles) any per-stage branch or constant-bank
+        // reload shows up directly in the tile time (profiles/r01_conv_halo_ab.txt).
         if (rank == 0) {
-            int s = 0;
-            uint32_t ph = 0;
-            int acc = 0;
-            uint32_t aph = 0;
-            const int n_a = p.tile_k / ATOM;
             const uint32_t b_lbo = (uint32_t)p.tile_k * 128u;   // stride between 128-byte N blocks of B
             // Descriptors of stage 0; stage s and each k-step only advance the 14-bit
             // start-address field (address >> 4), which never carries out of the field
@@ -232,41 +231,71 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             uint8_t* const b_base_ptr = b_res ? sBres : sB;
             const uint64_t bdesc0 = TF32 ? ptx::smem_desc_sw128(ptx::smem_u32(b_base_ptr), b_lbo, 512, 1)
                                          : ptx::smem_desc_sw128(ptx::smem_u32(b_base_ptr), b_lbo, 1024, 2);
-            const uint32_t a_stage16 = p.a_stage_bytes >> 4, b_stage16 = p.b_stage_bytes >> 4;
+            const uint32_t a_stage16 = ptx::pin(p.a_stage_bytes >> 4), b_stage16 = ptx::pin(p.b_stage_bytes >> 4);
+            const uint32_t idesc = ptx::pin(p.idesc);
+            const int Sring = ptx::pin(S), accb = ptx::pin(p.acc_buffers), tile_n = ptx::pin(p.tile_n);
+            const int kb_per = ptx::pin(p.kb_per_split), kb_tot = ptx::pin(p.kb_total);
+            const uint32_t b_res_u = ptx::pin((uint32_t)(b_res ? 1 : 0));
             if (b_res) ptx::mbar_wait(bfull, 0);     // resident B has landed (in both CTAs for a pair)
-            for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters) {
-                int mb, nb, ks;
-                tile_coords(p.tm, t, mb, nb, ks);
-                const int kb0 = ks * p.kb_per_split;
-                const int kb1 = min(p.kb_total, kb0 + p.kb_per_split);
-                ptx::mbar_wait(&tempty[acc], aph ^ 1);
-                ptx::tc_fence_after();
-                const uint32_t d_tmem = tmem_base + (uint32_t)(acc * p.tile_n);
-                for (int kb = kb0; kb < kb1; ++kb) {
-                    ptx::mbar_wait(&full[s], ph);
-                    if (trace && lane == 0 && trace_k < kTraceK) trace[8 + kTraceK + trace_k++] = ptx::globaltimer();
+            // NA > 0: atoms per stage known at compile time; NA == 0: none (diagnostics);
+            // NA < 0: runtime count n_a (other tile_k, and the traced variant)
+            auto mma_loop = [&](auto na_c, auto trace_c) {
+                constexpr int NA = decltype(na_c)::value;
+                constexpr bool TR = decltype(trace_c)::value;
+                const int n_a = NA >= 0 ? NA : ptx::pin(p.tile_k / ATOM);
+                int s = 0, acc = 0, tk = 0;
+                uint32_t ph = 0, aph = 0;
+                for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters) {
+                    int mb, nb, ks;
+                    tile_coords(p.tm, t, mb, nb, ks);
+                    const int kb0 = ks * kb_per;
+                    const int kb1 = min(kb_tot, kb0 + kb_per);
+                    ptx::mbar_wait(&tempty[acc], aph ^ 1);
                     ptx::tc_fence_after();
                     if (ptx::elect_one()) {
-                        const uint64_t ad = adesc0 + (uint64_t)(s * a_stage16);
-                        const uint64_t bd = bdesc0 + (uint64_t)((b_res ? kb : s) * b_stage16);
-                        for (int a = 0; a < (p.debug_skip_mma ? 0 : n_a); ++a) {
-#pragma unroll
-                            for (int kk = 0; kk < ATOM / UMMA_K; ++kk) {
-                                const uint32_t krow = a * ATOM + kk * UMMA_K;
-                                ptx::umma<TF32, CG>(d_tmem, ad + (uint64_t)((a * A_ATOM_BYTES + kk * 32) >> 4),
-                                                    bd + (uint64_t)(krow * 8), p.idesc,
-                                                    (kb > kb0 || a > 0 || kk > 0) ? 1u : 0u);
+                        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * tile_n);
+                        int s1 = s, tk1 = tk;
+                        uint32_t ph1 = ph;
+                        for (int kb = kb0; kb < kb1; ++kb) {
+                            ptx::mbar_wait(&full[s1], ph1);
+                            if constexpr (TR) {
+                                if (tk1 < kTraceK) trace[8 + kTraceK + tk1] = ptx::globaltimer();
+                                ++tk1;
                             }
+                            ptx::tc_fence_after();
+                            const uint64_t ad = adesc0 + (uint64_t)((uint32_t)s1 * a_stage16);
+                            const uint64_t bd = bdesc0 + (uint64_t)((b_res_u ? (uint32_t)kb : (uint32_t)s1) * b_stage16);
+                            const uint32_t acc0 = kb > kb0 ? 1u : 0u;
+#pragma unroll
+                            for (int a = 0; a < (NA >= 0 ? NA : n_a); ++a) {
+#pragma unroll
+                                for (int kk = 0; kk < ATOM / UMMA_K; ++kk) {
+                                    const uint32_t krow = a * ATOM + kk * UMMA_K;
+                                    ptx::umma<TF32, CG>(d_tmem, ad + (uint64_t)((a * A_ATOM_BYTES + kk * 32) >> 4),
+                                                        bd + (uint64_t)(krow * 8), idesc, (a > 0 || kk > 0) ? 1u : acc0);
+                                }
+                            }
+                            ptx::umma_commit<CG>(&empty[s1]);   // frees the SMEM slot(s) when these MMAs finish
+                            if (++s1 == Sring) { s1 = 0; ph1 ^= 1u; }
                         }
-                        ptx::umma_commit<CG>(&empty[s]);   // frees the SMEM slot(s) when these MMAs finish
+                        ptx::umma_commit<CG>(&tfull[acc]);      // accumulator ready for the epilogue(s)
                     }
                     __syncwarp();
-                    if (++s == S) { s = 0; ph ^= 1; }
+                    for (int kb = kb0; kb < kb1; ++kb)           // every lane tracks the ring position
+                        if (++s == Sring) { s = 0; ph ^= 1u; }
+                    if constexpr (TR) tk += kb1 - kb0;
+                    if (++acc == accb) { acc = 0; aph ^= 1u; }
                 }
-                if (ptx::elect_one()) ptx::umma_commit<CG>(&tfull[acc]);   // accumulator ready for the epilogue(s)
-                __syncwarp();
-                if (++acc == p.acc_buffers) { acc = 0; aph ^= 1; }
-            }
+            };
+            using T0 = std::integral_constant<bool, false>;
+            using T1 = std::integral_constant<bool, true>;
+            const int n_a = p.tile_k / ATOM;
+            if (trace) mma_loop(std::integral_constant<int, -1>{}, T1{});
+            else if (p.debug_skip_mma) mma_loop(std::integral_constant<int, 0>{}, T0{});
+            else if (n_a == 1) mma_loop(std::integral_constant<int, 1>{}, T0{});
+            else if (n_a == 2) mma_loop(std::integral_constant<int, 2>{}, T0{});
+            else if (n_a == 4) mma_loop(std::integral_constant<int, 4>{}, T0{});
+            else mma_loop(std::integral_constant<int, -1>{}, T0{});
         }
     } else if (warp >= 4) {
         // ===================== epilogue (bufferize) =====================

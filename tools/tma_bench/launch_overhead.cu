@@ -22,28 +22,37 @@ __global__ void k_delay(unsigned long long ns) {
     while (ptx::globaltimer() - t0 < ns) {}
 }
 
-template <bool TMEM, bool MAPS>
+// TMEM: 0 none, 1 alloc+relinquish+dealloc, 2 alloc+dealloc (no relinquish), 3 alloc 32 cols,
+// 4 relinquish only, 5 alloc+relinquish+dealloc with no fences
+template <int TMEM, bool MAPS>
 __global__ void __launch_bounds__(256, 1) k_empty(const __grid_constant__ Maps m, int* sink) {
     extern __shared__ uint8_t smem[];
     __shared__ uint32_t slot;
+    const uint32_t cols = TMEM == 3 ? 32 : 256;
     if constexpr (MAPS) {
         if (threadIdx.x == 0) { ptx::prefetch_tmap(&m.a); ptx::prefetch_tmap(&m.b); ptx::prefetch_tmap(&m.c); }
     }
-    if constexpr (TMEM) {
-        if ((threadIdx.x >> 5) == 2) { ptx::tmem_alloc<1>(&slot, 256); ptx::tmem_relinquish<1>(); }
-        ptx::tc_fence_before();
+    if constexpr (TMEM != 0) {
+        if ((threadIdx.x >> 5) == 2) {
+            if (TMEM != 4) ptx::tmem_alloc<1>(&slot, cols);
+            if (TMEM != 2) ptx::tmem_relinquish<1>();
+        }
+        if (TMEM != 5) ptx::tc_fence_before();
         __syncthreads();
-        ptx::tc_fence_after();
+        if (TMEM != 5) ptx::tc_fence_after();
     }
     if (threadIdx.x == 0 && blockIdx.x == 100000) sink[0] = smem[0];
-    if constexpr (TMEM) {
-        ptx::tc_fence_before();
+    if constexpr (TMEM != 0) {
+        if (TMEM != 5) ptx::tc_fence_before();
         __syncthreads();
-        if ((threadIdx.x >> 5) == 2) { ptx::tc_fence_after(); ptx::tmem_dealloc<1>(slot, 256); }
+        if ((threadIdx.x >> 5) == 2 && TMEM != 4) {
+            if (TMEM != 5) ptx::tc_fence_after();
+            ptx::tmem_dealloc<1>(slot, cols);
+        }
     }
 }
 
-template <bool TMEM, bool MAPS>
+template <int TMEM, bool MAPS>
 static void run(const char* name, int grid, int smem, int* sink, const Maps& m) {
     auto k = k_empty<TMEM, MAPS>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -80,13 +89,15 @@ int main() {
     cudaMalloc(&sink, 4);
     Maps m;
     memset(&m, 0, sizeof m);
-    for (int grid : {148, 25}) {
-        run<false, false>("empty", grid, 0, sink, m);
-        run<false, false>("empty", grid, 100 * 1024, sink, m);
-        run<false, false>("empty", grid, 206 * 1024, sink, m);
-        run<false, true>("3 tensormap params", grid, 206 * 1024, sink, m);
-        run<true, false>("tmem alloc/dealloc", grid, 206 * 1024, sink, m);
-        run<true, true>("tmem + tensormaps", grid, 206 * 1024, sink, m);
+    for (int grid : {148}) {
+        run<0, false>("empty", grid, 206 * 1024, sink, m);
+        run<1, false>("alloc+relinquish+dealloc", grid, 206 * 1024, sink, m);
+        run<2, false>("alloc+dealloc", grid, 206 * 1024, sink, m);
+        run<3, false>("alloc 32 cols", grid, 206 * 1024, sink, m);
+        run<4, false>("relinquish only", grid, 206 * 1024, sink, m);
+        run<5, false>("no tcgen05 fences", grid, 206 * 1024, sink, m);
+        run<0, false>("empty 0 smem", grid, 0, sink, m);
+        run<1, false>("alloc.. 0 smem", grid, 0, sink, m);
     }
     return 0;
 }
