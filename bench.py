@@ -344,6 +344,24 @@ def main_xtc(args):
         dist.all_reduce(v, op=dist.ReduceOp.MIN)
         validation["valid_all_ranks"] = int(v[0])
 
+    # a9 hardware counters by name for the headline kernel (CUPTI range profiler, a replay
+    # pass of its own after the timed region): live DRAM traffic and tensor-pipe activity
+    live = None
+    if rank == 0:
+        names = ["gpu.dram__bytes_read.sum", "gpu.dram__bytes_write.sum",
+                 "gpu.sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"]
+        try:
+            cm = op.measure(a, b, c, xtc.measure_cfg(warmup=1, repeats=1, validate=0, counters=names), stream=sp)
+            cv = cm.counter_values(names)
+            if cv:
+                live = {"dram_bytes_per_launch": cv[names[0]] + cv[names[1]],
+                        "tensor_pipe_active_pct": cv[names[2]],
+                        "source": "CUPTI range profiler via xtc_measure(counters=...), separate pass after timing"}
+            else:
+                live = {"unavailable": xtc.xtc_last_error()}
+        except Exception as ex:
+            live = {"unavailable": repr(ex)}
+
     extras = {}
     if not args.no_extras:
         # config 4 (scaled down): a seeded candidate sweep at 1024^3 dealt across the ranks,
@@ -387,7 +405,10 @@ def main_xtc(args):
             "validation": validation,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                          "frac": achieved / peak_tf, "traffic": traffic,
-                         "kernel": "tc_gemm_kernel<bf16>", "algorithmic_flops_per_launch": flops / world},
+                         "kernel": "tc_gemm_kernel<bf16>", "algorithmic_flops_per_launch": flops / world,
+                         "algorithmic_bytes_per_launch": (Mr * K + K * N + Mr * N) * 2,
+                         "traffic_source": "ncu --set full capture committed under profiles/ (ncu_summary.json)",
+                         "live_counters": live},
             "gpu_launches": launches_per_step * args.steps,
             "e2e": {"value": e2e_val, "unit": "TFLOP/s", "h2d_bytes_per_step": (Mr * K + K * N) * 2,
                     "d2h_bytes_per_step": (M if world > 1 else Mr) * N * 2, "steps": e2e_steps,

@@ -19,10 +19,17 @@ MATMUL_SCHEDS = {
           dict(TC, tile_n=64, tile_k=128, stages=4, buffer_c=1, acc_buffers=1, pack_warps=2)],
 }
 
+HALO = dict(TC, pack_halo=1, buffer_c=1, acc_buffers=2, persistent=1)
+
 CONV_SCHEDS = {
-    "L56": [dict(TC, tile_n=64, stages=8, buffer_c=1, acc_buffers=2, persistent=1, raster_group=8, pack_warps=3),
+    # pack_halo (input packed once per output tile) first; the im2col schedules stay as candidates
+    "L56": [dict(HALO, tile_n=64, stages=2, b_resident=1),
+            dict(HALO, tile_m=256, tile_n=64, stages=2, b_resident=1),
+            dict(TC, tile_n=64, stages=8, buffer_c=1, acc_buffers=2, persistent=1, raster_group=8, pack_warps=3),
             dict(TC, tile_n=64, stages=7, buffer_c=1, acc_buffers=2, persistent=1, pack_warps=3, b_resident=1)],
-    "L14": [dict(PAIR, tile_n=256, tile_k=128, stages=3, buffer_c=1, acc_buffers=2, persistent=1, pack_warps=2),
+    "L14": [dict(HALO, tile_n=128, tile_k=128, stages=3),
+            dict(HALO, tile_n=128, stages=4),
+            dict(PAIR, tile_n=256, tile_k=128, stages=3, buffer_c=1, acc_buffers=2, persistent=1, pack_warps=2),
             dict(TC, tile_n=256, stages=4, buffer_c=1, acc_buffers=2, persistent=1, pack_warps=2),
             dict(TC, tile_n=256, stages=4, buffer_c=1, acc_buffers=1, split_k=3, pack_warps=2)],
 }
@@ -88,6 +95,8 @@ def run_extras(xtc, torch, dev, peak):
             d = xtc.conv2d_desc(nb, h, h, c, c, 3, 3, 1, 1, "bf16", "bf16")
             cands = list(CONV_SCHEDS[name]) + [dict(TC, tile_n=min(c, 256), stages=4, buffer_c=1, acc_buffers=1,
                                                      split_k=sk, pack_warps=2) for sk in (2, 3)]
+            if name == "L14":   # few tiles at small batch: narrower halo tiles spread over more SMs
+                cands.append(dict(HALO, tile_n=64, tile_k=128, stages=4))
             r = _best(xtc, torch, dev, d, cands, [(nb, h, h, c), (3, 3, c, c)], peak)
             scan[f"{name}_n{nb}"] = {k: r.get(k) for k in ("tflops_med", "t_med_us", "schedule", "error")}
     out["conv_batch_scan_bf16"] = scan
