@@ -192,6 +192,58 @@ def sharded_sweep(xtc, torch, dist, dev, world, rank, n_cand, peak_tf):
             "best_id": int(best["id"]) if best else None, "space": "GpuStrategy(TC_SLOTS) legal set, seed 0"}
 
 
+def sharded_conv(xtc, torch, dist, dev, world, rank, peak_tf, steps=10):
+    """SURVEY §8(e) mode 3: the batched conv (L56, N=32) split by batch, y all-gathered.
+    Every rank regenerates its own images from the seed (the generator's `first` offset
+    makes the shard equal to the global tensor's slice) and the whole filter.  A step is
+    the local conv + the all-gather of y; device-timed from a barrier, max over ranks.
+    The local conv alone (median of xtc_measure reps) is reported beside it."""
+    from paper_2512_16512_b200.bench_extras import CONV_SCHEDS
+    from paper_2512_16512_b200.parallel import gather_rows, shard_rows
+    NB, H, C = 32, 56, 64
+    n0, n1 = shard_rows(NB, world, rank)
+    nb = n1 - n0
+    d = xtc.conv2d_desc(nb, H, H, C, C, 3, 3, 1, 1, "bf16", "bf16")
+    M, N, K = xtc.gemm_view(d)
+    x = torch.empty((nb, H, H, C), dtype=torch.bfloat16, device=dev)
+    w = torch.empty((3, 3, C, C), dtype=torch.bfloat16, device=dev)
+    y = torch.empty((M, N), dtype=torch.bfloat16, device=dev)
+    y_all = torch.empty((M * world, N), dtype=torch.bfloat16, device=dev)
+    st = torch.cuda.current_stream(dev)
+    xtc.xtc_fill(x.data_ptr(), x.numel(), xtc.XTC_BF16, 5, 0, n0 * H * H * C, st.cuda_stream)
+    xtc.xtc_fill(w.data_ptr(), w.numel(), xtc.XTC_BF16, 6, 0, 0, st.cuda_stream)
+    op = xtc.Op(d, dev.index).apply(xtc.schedule(**CONV_SCHEDS["L56"][0]))
+    m = op.measure(x, w, y, xtc.measure_cfg(warmup=3, repeats=20, validate=1, tol=5e-3, peak_tflops=peak_tf),
+                   stream=st.cuda_stream)
+    flops = xtc.xtc_op_flops(d)
+    for _ in range(3):
+        op.run(x, w, y, stream=st.cuda_stream)
+        if world > 1:
+            gather_rows(y, M * world, out=y_all)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(steps):
+        op.run(x, w, y, stream=st.cuda_stream)
+        if world > 1:
+            gather_rows(y, M * world, out=y_all)
+    e1.record(st)
+    torch.cuda.synchronize(dev)
+    t = torch.tensor([e0.elapsed_time(e1) * 1e-3 / steps], device=dev, dtype=torch.float64)
+    valid = torch.tensor([int(m.valid)], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(valid, op=dist.ReduceOp.MIN)
+    return {"workload": "conv L56 32x56x56x64 -> 64 (3x3 s1 p1) bf16, batch split across ranks",
+            "ranks": world, "images_per_rank": nb, "valid_all_ranks": int(valid[0]),
+            "local_conv_us_med": m.t_med_ns / 1e3, "local_conv_tflops": m.tflops_med,
+            "step_us": float(t[0]) * 1e6, "step_tflops_all_ranks": flops * world / float(t[0]) / 1e12,
+            "schedule": CONV_SCHEDS["L56"][0],
+            "note": "launch-bound at N=32 (SURVEY §8e): reported, not expected to scale"}
+
+
 # ---------------------------------------------------------------- xtc arm --
 def main_xtc(args):
     import torch
@@ -368,6 +420,7 @@ def main_xtc(args):
         # records all-gathered over NCCL; device-timed, max over ranks
         extras["sweep_1024_bf16_sharded"] = sharded_sweep(xtc, torch, dist, dev, world, rank, args.sweep_candidates,
                                                           peak_tf)
+        extras["conv_L56_batch_sharded"] = sharded_conv(xtc, torch, dist, dev, world, rank, peak_tf)
     if rank == 0 and world == 1 and not args.no_extras:
         try:
             from paper_2512_16512_b200.bench_extras import run_extras

@@ -202,6 +202,31 @@ def test_tc_conv_pack_halo_fused_relu_and_grid_modes():
         run_conv_relu(d, tc(pack_halo=1, tile_n=64, stages=3, **extra))
 
 
+# ------------------------------------------------ the paper's §VI-B workloads --
+@pytest.mark.parametrize("mode", [MODE_INT, MODE_UNIFORM])
+def test_paper_tu_matmul_512x128x1024(mode):
+    """[512,128] x [128,1024] (Fig.11): tcgen05 bf16 and SIMT fp32 schedules."""
+    for sch in (tc(tile_n=64, tile_k=64, stages=2), tc(tile_n=128, tile_k=128, stages=2, persistent=1, acc_buffers=2),
+                tc(tile_m=256, cluster_m=2, tile_n=256, tile_k=64, stages=2)):
+        err, _ = run_matmul(512, 1024, 128, "bf16", "bf16", sch, mode)
+        assert err <= 5e-3
+    err, _ = run_matmul(512, 1024, 128, "f32", "f32", S(engine=0, tile_m=64, tile_n=64, tile_k=16, inner_m=4,
+                                                          inner_n=4, unroll_k=4, vector_n=4, stages=2, swizzle=4), mode)
+    assert err <= 1e-5
+
+
+@pytest.mark.parametrize("mode", [MODE_INT, MODE_UNIFORM])
+def test_paper_stem_conv_7x7_stride2(mode):
+    """[112,112,16] x [7,7,3] step 2 (reading 4): 224x224x3 -> 112x112x16, pad 3.  C = 3 gives a 6-byte
+    pixel pitch (no TMA), so it runs on the SIMT engine; K = 147 is ragged for every tile_k."""
+    d = xtc.conv2d_desc(1, 224, 224, 3, 16, 7, 7, 2, 3, "f32", "f32")
+    assert xtc.gemm_view(d) == (112 * 112, 16, 147)
+    for sch in (S(engine=0, tile_m=64, tile_n=16, tile_k=8, inner_m=4, inner_n=2, unroll_k=2, stages=1),
+                S(engine=0, tile_m=64, tile_n=16, tile_k=21, inner_m=4, inner_n=4, stages=2, vector_n=4, swizzle=4)):
+        err = run_conv(d, "f32", "f32", sch, mode)
+        assert err <= 1e-5
+
+
 def test_simt_conv_fp32():
     d = xtc.conv2d_desc(2, 14, 14, 16, 32, 3, 3, 1, 1, "f32", "f32")
     sch = S(engine=0, tile_m=64, tile_n=32, tile_k=16, inner_m=4, inner_n=4, unroll_k=4, vector_n=4, stages=2)
@@ -357,6 +382,8 @@ def test_bench_two_rank_rehearsal_on_one_gpu(tmp_path):
     assert rec["n_gpus"] == 2 and rec["validation"]["valid"] == 1 and rec["value"] > 0
     sw = rec["extras"]["sweep_1024_bf16_sharded"]
     assert sw["ranks"] == 2 and sw["candidates"] == 32 and sw["valid"] + sw["invalid"] == 32
+    cv = rec["extras"]["conv_L56_batch_sharded"]
+    assert cv["ranks"] == 2 and cv["images_per_rank"] == 16 and cv["valid_all_ranks"] == 1 and cv["step_us"] > 0
 
 
 @pytest.mark.parametrize("pw", [2, 3])
