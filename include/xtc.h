@@ -75,12 +75,18 @@ typedef enum { XTC_F32 = 0, XTC_BF16 = 1, XTC_TF32 = 2 } xtc_dtype;
  *            Implicit GEMM view: M = batch*P*Q, N = f, K = r*s*c (c fastest).
  * in_dtype: F32 (SIMT engine, fp32 FFMA), TF32 or BF16 (tcgen05 engine).
  * out_dtype: F32 or BF16 (RNE).
- * consumer: elementwise consumer op applied to the result (the paper's graph
- *   matmul -> relu, Fig.9): XTC_CONSUMER_NONE or XTC_CONSUMER_RELU
- *   (out = max(result, 0), rounded once to out_dtype).  Whether it runs fused
- *   into the contraction's epilogue or as its own pass is the schedule's
- *   `fuse` knob. */
-typedef enum { XTC_CONSUMER_NONE = 0, XTC_CONSUMER_RELU = 1 } xtc_consumer;
+ * consumer: elementwise consumer ops applied to the result (the paper's graph
+ *   matmul -> relu, Fig.9; fuse), a bitmask of
+ *     XTC_CONSUMER_RELU       out = max(v, 0)
+ *     XTC_CONSUMER_BIAS       v += bias[n]  (bias = inputs[2]: fp32, one value per
+ *                             output column n / output channel f, device memory)
+ *     XTC_CONSUMER_ACCUMULATE v += C_old    (beta = 1: the output is also an input,
+ *                             Fig.2's C[i][j] += ...; reading 1's NEXT flag)
+ *   applied as out = round_out(relu(C_old + A*B + bias)), rounded once.  Whether
+ *   they run fused into the contraction's epilogue (or split-K reduction) or as
+ *   their own pass is the schedule's `fuse` knob (accumulate must be fused). */
+typedef enum { XTC_CONSUMER_NONE = 0, XTC_CONSUMER_RELU = 1, XTC_CONSUMER_BIAS = 2,
+               XTC_CONSUMER_ACCUMULATE = 4 } xtc_consumer;
 typedef struct {
     int32_t kind;       /* xtc_op_kind */
     int32_t in_dtype;   /* xtc_dtype   */
@@ -233,13 +239,19 @@ xtc_status xtc_schedule_apply(xtc_op op, const xtc_schedule* sch);
 xtc_status xtc_schedule_default(const xtc_op_desc* desc, int32_t opt_level, xtc_schedule* out);
 
 /* a3..a7 -- run the scheduled operator once, asynchronously on `stream`.
- * inputs[0..1], outputs[0] as in the conventions above.  The TMA descriptors
- * are re-encoded only when a pointer differs from the previous call. */
+ * inputs[0..1], outputs[0] as in the conventions above; inputs[2] = the fp32
+ * bias (n or f values) when the consumer has XTC_CONSUMER_BIAS (NULL ->
+ * XTC_E_INVALID_ARG).  With XTC_CONSUMER_ACCUMULATE, outputs[0] is read too.
+ * The TMA descriptors are re-encoded only when a pointer differs from the
+ * previous call. */
 xtc_status xtc_run(xtc_op op, const void* const* inputs, void* const* outputs, void* stream);
 
 /* a8 + a9 -- Executor + Evaluator.  Synchronous.  Sequence:
  *   1. if cfg->validate: fill outputs with NaN, run once, compute (or reuse)
  *      the fp64 GPU reference R and D, compare -> max_norm_err, n_mismatch, n_nan;
+ *      the reference includes the consumer (C_old + R + bias, relu; with
+ *      ACCUMULATE the output is snapshotted instead of NaN-filled, and every
+ *      timed run keeps accumulating into it);
  *   2. cfg->warmup untimed runs;
  *   3. cfg->repeats timed runs, each between two CUDA events on `stream`, with
  *      the L2 flush (if requested) outside the event window;

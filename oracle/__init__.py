@@ -110,6 +110,20 @@ def relu(O: np.ndarray) -> np.ndarray:
     return np.maximum(np.asarray(O, dtype=np.float64), 0.0)
 
 
+def consume(O: np.ndarray, relu_: bool = False, bias=None, c_old=None) -> np.ndarray:
+    """The fused consumer of the contraction (fuse), in fp64 and
+    in this order: C_old + O (the accumulate flag, Fig.2's `C[i][j] +=`), + bias[n]
+    broadcast over rows, then relu (above); round_out follows once.  Pinned in
+    tests/test_oracle.py by [A | 1]·[B ; biasᵀ] and [A | I]·[B ; C_old] (both textbook
+    block-matrix identities computed through `matmul`) and a hand example."""
+    R = np.asarray(O, dtype=np.float64).copy()
+    if c_old is not None:
+        R = R + np.asarray(c_old, dtype=np.float64)
+    if bias is not None:
+        R = R + np.asarray(bias, dtype=np.float64)[None, :]
+    return relu(R) if relu_ else R
+
+
 def round_out(O: np.ndarray, out_dtype: str) -> np.ndarray:
     """round_out of SURVEY.md §8(c): fp32 output -> float32(O) (RN);
     bf16 output -> RNE to bf16, returned as uint16 bit patterns.

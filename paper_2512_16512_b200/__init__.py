@@ -28,9 +28,20 @@ XTC_F32, XTC_BF16, XTC_TF32 = 0, 1, 2
 XTC_ENGINE_SIMT, XTC_ENGINE_TCGEN05 = 0, 1
 XTC_ORDER_MN, XTC_ORDER_NM = 0, 1
 XTC_SPLITK_ORDERED, XTC_SPLITK_ATOMIC = 0, 1
-XTC_CONSUMER_NONE, XTC_CONSUMER_RELU = 0, 1
+XTC_CONSUMER_NONE, XTC_CONSUMER_RELU, XTC_CONSUMER_BIAS, XTC_CONSUMER_ACCUMULATE = 0, 1, 2, 4
 DTYPES = {"f32": XTC_F32, "bf16": XTC_BF16, "tf32": XTC_TF32}
-CONSUMERS = {None: XTC_CONSUMER_NONE, "none": XTC_CONSUMER_NONE, "relu": XTC_CONSUMER_RELU}
+CONSUMERS = {None: XTC_CONSUMER_NONE, "none": XTC_CONSUMER_NONE, "relu": XTC_CONSUMER_RELU,
+             "bias": XTC_CONSUMER_BIAS, "accumulate": XTC_CONSUMER_ACCUMULATE}
+
+
+def consumer_bits(consumer) -> int:
+    """None / an int bitmask / a name / '+'-joined names ('bias+relu', 'accumulate+bias+relu')."""
+    if consumer is None or isinstance(consumer, int):
+        return int(consumer or 0)
+    bits = 0
+    for part in str(consumer).split("+"):
+        bits |= CONSUMERS[part.strip()]
+    return bits
 
 
 # ------------------------------------------------------------- structs -----
@@ -234,7 +245,7 @@ def matmul_desc(m, n, k, in_dtype="bf16", out_dtype="bf16", lda=0, ldb=0, ldc=0,
     d.kind = XTC_OP_MATMUL
     d.in_dtype = DTYPES[in_dtype]
     d.out_dtype = DTYPES[out_dtype]
-    d.consumer = CONSUMERS[consumer]
+    d.consumer = consumer_bits(consumer)
     d.m, d.n, d.k, d.lda, d.ldb, d.ldc = m, n, k, lda, ldb, ldc
     return d
 
@@ -245,7 +256,7 @@ def conv2d_desc(batch, h, w, c, f, r=3, s=3, stride=1, pad=1, in_dtype="bf16", o
     d.kind = XTC_OP_CONV2D
     d.in_dtype = DTYPES[in_dtype]
     d.out_dtype = DTYPES[out_dtype]
-    d.consumer = CONSUMERS[consumer]
+    d.consumer = consumer_bits(consumer)
     d.batch, d.h, d.w, d.c, d.f, d.r, d.s = batch, h, w, c, f, r, s
     d.stride_h = d.stride_w = stride
     d.pad_h = d.pad_w = pad
@@ -310,16 +321,21 @@ class Op:
         import torch
         return torch.cuda.current_stream().cuda_stream
 
-    def run(self, a, b, c, stream=None) -> None:
-        xtc_run(self.handle, [a.data_ptr(), b.data_ptr()], [c.data_ptr()], self._stream(stream))
+    @staticmethod
+    def _inputs(a, b, bias):
+        # inputs[2] = the fp32 bias of an XTC_CONSUMER_BIAS consumer (include/xtc.h)
+        return [a.data_ptr(), b.data_ptr()] + ([bias.data_ptr()] if bias is not None else [None])
 
-    def measure(self, a, b, c, cfg: xtc_measure_cfg = None, stream=None) -> xtc_metrics:
-        cfg = cfg or measure_cfg()
-        return xtc_measure(self.handle, [a.data_ptr(), b.data_ptr()], [c.data_ptr()], cfg, self._stream(stream))
+    def run(self, a, b, c, stream=None, bias=None) -> None:
+        xtc_run(self.handle, self._inputs(a, b, bias), [c.data_ptr()], self._stream(stream))
 
-    def sweep(self, cands, a, b, c, cfg: xtc_measure_cfg = None, stream=None):
+    def measure(self, a, b, c, cfg: xtc_measure_cfg = None, stream=None, bias=None) -> xtc_metrics:
         cfg = cfg or measure_cfg()
-        return xtc_sweep(self.handle, cands, [a.data_ptr(), b.data_ptr()], [c.data_ptr()], cfg, self._stream(stream))
+        return xtc_measure(self.handle, self._inputs(a, b, bias), [c.data_ptr()], cfg, self._stream(stream))
+
+    def sweep(self, cands, a, b, c, cfg: xtc_measure_cfg = None, stream=None, bias=None):
+        cfg = cfg or measure_cfg()
+        return xtc_sweep(self.handle, cands, self._inputs(a, b, bias), [c.data_ptr()], cfg, self._stream(stream))
 
     def launches(self) -> int:
         return xtc_last_launch_count(self.handle)

@@ -26,10 +26,11 @@ cudaError_t launch_ref_gemm(const void* A, const void* B, int bf16, int64_t M, i
                             int64_t ldb, double* R, double* D, cudaStream_t st);
 cudaError_t launch_ref_conv(const void* x, const void* w, int bf16, const ConvGeom& g, int64_t Nb, int64_t F,
                             double* R, double* D, cudaStream_t st);
-cudaError_t launch_compare(const void* C, int out_bf16, int relu, int64_t M, int64_t N, int64_t ldc, const double* R,
-                           const double* D, double* blk_err, int64_t* blk_idx, void* counts, int blocks,
+cudaError_t launch_compare(const void* C, int out_bf16, const CmpConsumer& cc, int64_t M, int64_t N, int64_t ldc,
+                           const double* R, const double* D, double* blk_err, int64_t* blk_idx, void* counts, int blocks,
                            cudaStream_t st);
-cudaError_t launch_relu(void* C, int out_bf16, int64_t M, int64_t N, int64_t ldc, cudaStream_t st);
+cudaError_t launch_consumer_pass(void* C, int out_bf16, int64_t M, int64_t N, int64_t ldc, int cons,
+                                 const float* bias, cudaStream_t st);
 cudaError_t launch_compare_finalize(const double* blk_err, const int64_t* blk_idx, int blocks, void* counts,
                                     double* slot, cudaStream_t st);
 cudaError_t launch_flush(void* buf, int64_t bytes, uint32_t salt, cudaStream_t st);
@@ -37,10 +38,10 @@ cudaError_t launch_delay(uint64_t ns, cudaStream_t st);
 cudaError_t launch_fault(void* C, int out_bf16, int64_t M, int64_t N, int64_t ldc, int kind, int64_t row, int64_t col,
                          cudaStream_t st);
 cudaError_t launch_splitk_reduce(const float* W, int S, int64_t M, int64_t N, int64_t ws_ld, void* C, int64_t ldc,
-                                 int out_bf16, int relu, cudaStream_t st);
-cudaError_t launch_tail_gemm(const void* A, const void* B, int bf16_in, void* C, int out_bf16, int relu, int64_t M,
-                             int64_t n0, int64_t ntail, int64_t K, int64_t lda, int64_t ldb, int64_t ldc, int gx, int gy,
-                             cudaStream_t st);
+                                 int out_bf16, int cons, const float* bias, cudaStream_t st);
+cudaError_t launch_tail_gemm(const void* A, const void* B, int bf16_in, void* C, int out_bf16, int cons,
+                             const float* bias, int64_t M, int64_t n0, int64_t ntail, int64_t K, int64_t lda, int64_t ldb,
+                             int64_t ldc, int gx, int gy, cudaStream_t st);
 }  // namespace xtc
 
 using namespace xtc;
@@ -156,6 +157,11 @@ struct xtc_op_s {
     double* blk_err = nullptr;
     int64_t* blk_idx = nullptr;
     void* counts = nullptr;
+    // consumer inputs of the current call: the bias (inputs[2]) and, for accumulate-mode
+    // validation, a snapshot of the output taken before the validated run
+    const float* bias = nullptr;
+    void* c_old = nullptr;
+    int64_t c_old_bytes = 0;
     // timing
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     std::vector<cudaEvent_t> evs;
@@ -186,6 +192,7 @@ static void release_op(xtc_op op) {
     if (op->blk_err) cudaFree(op->blk_err);
     if (op->blk_idx) cudaFree(op->blk_idx);
     if (op->counts) cudaFree(op->counts);
+    if (op->c_old) cudaFree(op->c_old);
     if (op->trace_dev) cudaFree(op->trace_dev);
     for (auto e : op->evs) cudaEventDestroy(e);
     cudaSetDevice(cur);
@@ -535,8 +542,9 @@ static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cud
     const bool out_bf16 = d.out_dtype == XTC_BF16;
     const bool split_out = p.split_k > 1 && !p.atomic;
     int launches = 0;
-    if (p.atomic) {
-        // atomic split-K accumulates into C: clear the main root's columns first
+    if (p.atomic && !(d.consumer & XTC_CONSUMER_ACCUMULATE)) {
+        // atomic split-K accumulates into C: clear the main root's columns first (unless the
+        // consumer is C += A*B, which is exactly what the atomics do)
         const int64_t rows = p.M;
         CU_TRY(cudaMemset2DAsync(C, ldc * 4, 0, p.N * 4, rows, st), "memset C (atomic split-K)");
     }
@@ -564,7 +572,8 @@ static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cud
             sp.fast = (d.kind == XTC_OP_MATMUL) && aligned && sp.lda % 4 == 0 && sp.ldb % 4 == 0 && BK % 4 == 0 &&
                       BN % 4 == 0 && pad % 4 == 0 && (BM + pad) % 4 == 0 && BM * (BK / 4) <= 4 * p.block;
         }
-        sp.relu = p.relu_epi;
+        sp.cons = p.cons_epi;
+        sp.bias = op->bias;
         const int u = p.sch.unroll_k == 0 ? 1 : p.sch.unroll_k;
         const int vec = p.sch.vector_n == 0 ? 1 : p.sch.vector_n;
         CU_TRY(launch_simt_gemm(p.sch.inner_m, p.sch.inner_n, u, vec, sp, p.grid_x, p.block, p.smem, st), "simt_gemm launch");
@@ -584,7 +593,8 @@ static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cud
         tp.acc_buffers = p.sch.acc_buffers == 0 ? 1 : p.sch.acc_buffers;
         tp.pack_warps = p.sch.pack_warps == 0 ? 1 : p.sch.pack_warps;
         tp.b_resident = p.sch.b_resident;
-        tp.relu = p.relu_epi;
+        tp.cons = p.cons_epi;
+        tp.bias = op->bias;
         tp.a3d = op->a3d;
         tp.debug_skip_mma = getenv("XTC_DEBUG_SKIP_MMA") != nullptr;   // diagnostics: output invalid
         if (const char* sk = getenv("XTC_DEBUG_SKIP")) tp.debug_skip_mma = atoi(sk);   // bitmask, see TcParams
@@ -645,20 +655,20 @@ static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cud
         }
     }
     if (split_out) {
-        CU_TRY(launch_splitk_reduce(op->ws, p.split_k, p.M, p.N, p.ws_ld, C, ldc, out_bf16, p.relu_reduce, st),
+        CU_TRY(launch_splitk_reduce(op->ws, p.split_k, p.M, p.N, p.ws_ld, C, ldc, out_bf16, p.cons_reduce, op->bias, st),
                "splitk_reduce");
         ++launches;
     }
     if (p.has_tail) {
         const int64_t lda = d.lda ? d.lda : d.k;
         const int64_t ldb = d.ldb ? d.ldb : d.n;
-        CU_TRY(launch_tail_gemm(A, B, d.in_dtype == XTC_BF16, C, out_bf16, p.relu_epi || p.relu_reduce, p.M, p.tail_n0,
+        CU_TRY(launch_tail_gemm(A, B, d.in_dtype == XTC_BF16, C, out_bf16, p.cons_tail, op->bias, p.M, p.tail_n0,
                                 p.tail_n, p.K, lda, ldb, ldc, p.tail_grid_x, p.tail_grid_y, st),
                "tail_gemm");
         ++launches;
     }
-    if (p.relu_pass) {                       // fuse = 0: the consumer as its own pass
-        CU_TRY(launch_relu(C, out_bf16, p.M, p.n_total, ldc, st), "relu");
+    if (p.cons_pass) {                       // fuse = 0: the consumer as its own pass
+        CU_TRY(launch_consumer_pass(C, out_bf16, p.M, p.n_total, ldc, p.cons_pass, op->bias, st), "consumer pass");
         ++launches;
     }
     if (op->fault) {
@@ -669,10 +679,21 @@ static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cud
     return XTC_OK;
 }
 
+// inputs[2] is the bias when the consumer has XTC_CONSUMER_BIAS (only then is it read)
+static xtc_status bind_bias(xtc_op op, const void* const* inputs) {
+    op->bias = nullptr;
+    if (op->d.consumer & XTC_CONSUMER_BIAS) {
+        if (!inputs[2]) return fail(XTC_E_INVALID_ARG, "consumer XTC_CONSUMER_BIAS needs inputs[2] (fp32 bias)");
+        op->bias = static_cast<const float*>(inputs[2]);
+    }
+    return XTC_OK;
+}
+
 extern "C" xtc_status xtc_run(xtc_op op, const void* const* inputs, void* const* outputs, void* stream) {
     if (!op || !inputs || !outputs || !inputs[0] || !inputs[1] || !outputs[0])
         return fail(XTC_E_INVALID_ARG, "null op or tensor pointer");
     if (!op->has_plan) return fail(XTC_E_NO_SCHEDULE, "xtc_run before xtc_schedule_apply");
+    if (bind_bias(op, inputs) != XTC_OK) return XTC_E_INVALID_ARG;
     DeviceGuard g(op->device);
     if (op->plan.engine == XTC_ENGINE_TCGEN05) {
         for (int i = 0; i < 2; ++i)
@@ -729,6 +750,23 @@ static xtc_status compute_reference(xtc_op op, const void* A, const void* B, cud
 
 static const int kCmpBlocks = 148 * 8;
 
+// Copy the output (M rows of N elements, pitch ldc) into the op's snapshot buffer (same layout).
+static xtc_status snapshot_output(xtc_op op, const void* C, int64_t M, int64_t N, int64_t ldc, int os, cudaStream_t st) {
+    const int64_t bytes = M * ldc * os;
+    if (op->c_old_bytes < bytes) {
+        if (op->c_old) cudaFree(op->c_old);
+        op->c_old = nullptr;
+        op->c_old_bytes = 0;
+        if (cudaMalloc(&op->c_old, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(XTC_E_OOM, "accumulate snapshot");
+        }
+        op->c_old_bytes = bytes;
+    }
+    CU_TRY(cudaMemcpy2DAsync(op->c_old, ldc * os, C, ldc * os, N * os, M, cudaMemcpyDeviceToDevice, st), "snapshot C");
+    return XTC_OK;
+}
+
 static xtc_status validate(xtc_op op, const void* A, const void* B, void* C, const xtc_measure_cfg* cfg,
                            xtc_metrics* m, cudaStream_t st) {
     const xtc_op_desc& d = op->d;
@@ -736,8 +774,16 @@ static xtc_status validate(xtc_op op, const void* A, const void* B, void* C, con
     gemm_view(d, M, N, K, P, Q);
     const int64_t ldc = (d.kind == XTC_OP_MATMUL && d.ldc) ? d.ldc : N;
     const int os = dsize(d.out_dtype);
-    // NaN sentinel: every output the schedule fails to write stays NaN (coverage)
-    CU_TRY(cudaMemset2DAsync(C, ldc * os, 0xFF, N * os, M, st), "NaN fill");
+    CmpConsumer cc{d.consumer, op->bias, nullptr};
+    if (d.consumer & XTC_CONSUMER_ACCUMULATE) {
+        // C is an input: snapshot it (the reference is C_old + A*B ...) instead of the sentinel
+        xtc_status s0 = snapshot_output(op, C, M, N, ldc, os, st);
+        if (s0 != XTC_OK) return s0;
+        cc.c_old = op->c_old;
+    } else {
+        // NaN sentinel: every output the schedule fails to write stays NaN (coverage)
+        CU_TRY(cudaMemset2DAsync(C, ldc * os, 0xFF, N * os, M, st), "NaN fill");
+    }
     xtc_status s = run_impl(op, A, B, C, st);
     if (s != XTC_OK) return s;
     if (!(cfg->reuse_reference && op->ref_valid && op->ref_inputs[0] == A && op->ref_inputs[1] == B)) {
@@ -752,9 +798,8 @@ static xtc_status validate(xtc_op op, const void* A, const void* B, void* C, con
         }
     }
     CU_TRY(cudaMemsetAsync(op->counts, 0, 16, st), "memset counts");
-    CU_TRY(launch_compare(C, d.out_dtype == XTC_BF16, d.consumer == XTC_CONSUMER_RELU, M, N, ldc, op->R, op->D,
-                          op->blk_err, op->blk_idx, op->counts,
-                          kCmpBlocks, st),
+    CU_TRY(launch_compare(C, d.out_dtype == XTC_BF16, cc, M, N, ldc, op->R, op->D, op->blk_err, op->blk_idx,
+                          op->counts, kCmpBlocks, st),
            "compare");
     std::vector<double> be(kCmpBlocks);
     std::vector<int64_t> bi(kCmpBlocks);
@@ -871,6 +916,7 @@ extern "C" xtc_status xtc_measure(xtc_op op, const void* const* inputs, void* co
     if (!op || !inputs || !outputs || !cfg || !out || !inputs[0] || !inputs[1] || !outputs[0])
         return fail(XTC_E_INVALID_ARG, "null argument");
     if (!op->has_plan) return fail(XTC_E_NO_SCHEDULE, "xtc_measure before xtc_schedule_apply");
+    if (bind_bias(op, inputs) != XTC_OK) return XTC_E_INVALID_ARG;
     DeviceGuard g(op->device);
     xtc_status s = measure_impl(op, inputs[0], inputs[1], outputs[0], cfg, out, (cudaStream_t)stream);
     if (s != XTC_OK) { out->status = s; return s; }
@@ -882,6 +928,7 @@ extern "C" xtc_status xtc_sweep(xtc_op op, const xtc_schedule* cands, int32_t n,
                                 void* const* outputs, const xtc_measure_cfg* cfg, xtc_metrics* out, void* stream) {
     if (!op || !cands || n < 0 || !out || !cfg || !inputs || !outputs) return fail(XTC_E_INVALID_ARG, "null argument");
     if (cfg->repeats < 1 || cfg->warmup < 0) return fail(XTC_E_INVALID_ARG, "repeats must be >= 1, warmup >= 0");
+    if (bind_bias(op, inputs) != XTC_OK) return XTC_E_INVALID_ARG;
     DeviceGuard g(op->device);
     cudaStream_t st = (cudaStream_t)stream;
     const void* A = inputs[0];
@@ -942,6 +989,13 @@ extern "C" xtc_status xtc_sweep(xtc_op op, const xtc_schedule* cands, int32_t n,
         }
         CU_TRY(cudaMemsetAsync(op->counts, 0, 16, st), "memset counts");
     }
+    // accumulate: the output is an input; every candidate is validated from the same C_old
+    const bool accum = (d.consumer & XTC_CONSUMER_ACCUMULATE) != 0;
+    if (cfg->validate && accum) {
+        xtc_status s = snapshot_output(op, C, M, N, ldc, os, st);
+        if (s != XTC_OK) return s;
+    }
+    const CmpConsumer cc{d.consumer, op->bias, accum ? op->c_old : nullptr};
     // 3. chunks of candidates enqueued back to back, one synchronisation per chunk: the host
     //    stays ahead of the GPU, so the per-rep events bracket GPU work only (no delay kernel)
     const int CH = 64;
@@ -973,11 +1027,13 @@ extern "C" xtc_status xtc_sweep(xtc_op op, const xtc_schedule* cands, int32_t n,
             op->maps_valid = false;           // TMA boxes depend on the schedule
             xtc_status s = XTC_OK;
             if (cfg->validate) {
-                if (cudaMemset2DAsync(C, ldc * os, 0xFF, N * os, M, st) != cudaSuccess) s = XTC_E_CUDA;
+                const cudaError_t pre =
+                    accum ? cudaMemcpy2DAsync(C, ldc * os, op->c_old, ldc * os, N * os, M, cudaMemcpyDeviceToDevice, st)
+                          : cudaMemset2DAsync(C, ldc * os, 0xFF, N * os, M, st);   // NaN sentinel
+                if (pre != cudaSuccess) s = XTC_E_CUDA;
                 if (s == XTC_OK) s = run_impl(op, A, B, C, st);
-                if (s == XTC_OK && (launch_compare(C, d.out_dtype == XTC_BF16, d.consumer == XTC_CONSUMER_RELU, M, N,
-                                                   ldc, op->R, op->D, op->blk_err, op->blk_idx, op->counts, kCmpBlocks,
-                                                   st) != cudaSuccess ||
+                if (s == XTC_OK && (launch_compare(C, d.out_dtype == XTC_BF16, cc, M, N, ldc, op->R, op->D, op->blk_err,
+                                                   op->blk_idx, op->counts, kCmpBlocks, st) != cudaSuccess ||
                                     launch_compare_finalize(op->blk_err, op->blk_idx, kCmpBlocks, op->counts,
                                                             slots + (size_t)(i - c0) * 4, st) != cudaSuccess))
                     s = XTC_E_CUDA;

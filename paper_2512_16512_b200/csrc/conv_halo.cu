@@ -22,6 +22,7 @@
 // allocator, warps 4..7 = epilogue (TMEM lane quarters).
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include "consumer.cuh"
 #include "ptx.cuh"
 #include "xtc_internal.h"
 
@@ -294,9 +295,11 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
                     ptx::tmem_ld_32x32b_x32(t_row + c, vals);
                     ptx::tmem_ld_wait();
                     if (!any_valid || (p.debug_skip_mma & 4)) continue;   // warp-uniform
-                    if (p.relu) {
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) vals[j] = __float_as_uint(fmaxf(__uint_as_float(vals[j]), 0.f));
+                    if (p.cons && valid) {            // fused consumer before the rounding
+                        const int64_t m = ((int64_t)nimg * P + prow) * Q + qcol;
+                        const int64_t cc = (int64_t)n0 + c;
+                        const int nc = (int)((p.N - cc) < 32 ? (p.N - cc) : 32);
+                        if (nc > 0) apply_consumer32(vals, p.cons, p.bias, p.C, bf16_out, m, p.ldc, cc, nc);
                     }
                     if (p.buffer_c) {
                         // one 128-byte staging row per thread (virtual row order = the TMA box's

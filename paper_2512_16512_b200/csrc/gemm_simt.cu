@@ -253,7 +253,15 @@ __global__ void __launch_bounds__(simt_max_threads(TM, TN), simt_min_blocks(TM, 
             for (int j = 0; j < TN; ++j) {
                 const int64_t col = n0 + (VEC == 4 ? tx * TN + j : tx + j * tx_n);
                 if (col >= p.N) continue;
-                const float v = p.relu ? fmaxf(acc[i][j], 0.f) : acc[i][j];   // fused consumer
+                float v = acc[i][j];
+                if (p.cons) {                                  // fused consumer
+                    const int64_t o = row * p.ldc + col;
+                    if ((p.cons & XTC_CONSUMER_ACCUMULATE) && !p.atomic)   // atomics add onto C anyway
+                        v += p.out_bf16 ? __bfloat162float(static_cast<const __nv_bfloat16*>(p.C)[o])
+                                        : static_cast<const float*>(p.C)[o];
+                    if ((p.cons & XTC_CONSUMER_BIAS) && (!p.atomic || ks == 0)) v += __ldg(p.bias + col);
+                    if (p.cons & XTC_CONSUMER_RELU) v = fmaxf(v, 0.f);
+                }
                 if (p.split_out) p.Wk[((int64_t)ks * p.M + row) * p.ws_ld + col] = v;
                 else if (p.atomic) atomicAdd(static_cast<float*>(p.C) + row * p.ldc + col, v);
                 else if (p.out_bf16) static_cast<__nv_bfloat16*>(p.C)[row * p.ldc + col] = __float2bfloat16_rn(v);

@@ -29,6 +29,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <type_traits>
+#include "consumer.cuh"
 #include "ptx.cuh"
 #include "xtc_internal.h"
 
@@ -319,9 +320,12 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 uint32_t v[32];
                 ptx::tmem_ld_32x32b_x32(t_row + c, v);
                 ptx::tmem_ld_wait();
-                if (p.relu) {                      // fused consumer: relu before rounding
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(fmaxf(__uint_as_float(v[j]), 0.f));
+                if (p.cons && row < p.M) {         // fused consumer before the rounding
+                    const int64_t cc = (int64_t)n0 + c;
+                    const int nc = (int)((p.N - cc) < 32 ? (p.N - cc) : 32);
+                    // atomic split-K: C is accumulated in place, the first segment adds the bias
+                    if (nc > 0) apply_consumer32(v, p.cons, p.bias, p.C, bf16_out, row, p.ldc, cc, nc, !p.atomic,
+                                                 !p.atomic || ks == 0);
                 }
                 if (p.buffer_c) {
                     // stage one 128-byte row per thread (swizzled), then one TMA store per warp

@@ -133,7 +133,7 @@ struct CmpOut {
     unsigned long long n_mismatch, n_nan;
 };
 
-__global__ void compare_kernel(const void* C, int out_bf16, int relu, int64_t M, int64_t N, int64_t ldc,
+__global__ void compare_kernel(const void* C, int out_bf16, CmpConsumer cc, int64_t M, int64_t N, int64_t ldc,
                                const double* R, const double* D, double* blk_err, int64_t* blk_idx, CmpOut* out) {
     double best = -1.0;
     int64_t best_i = -1;
@@ -141,8 +141,21 @@ __global__ void compare_kernel(const void* C, int out_bf16, int relu, int64_t M,
     const int64_t total = M * N;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t m = i / N, n = i - m * N;
-        // the reference of the consumer op: relu(R); D stays the normaliser (|relu a - relu b| <= |a - b|)
-        const double r = relu ? fmax(R[i], 0.0) : R[i], d = D[i];
+        // the reference of the consumer op: relu(C_old + R + bias); the normaliser gains |C_old| + |bias|
+        // (relu is 1-Lipschitz: |relu a - relu b| <= |a - b|)
+        double r = R[i], d = D[i];
+        if (cc.cons & XTC_CONSUMER_ACCUMULATE) {
+            const int64_t o = m * ldc + n;
+            const double old = out_bf16 ? (double)__bfloat162float(static_cast<const __nv_bfloat16*>(cc.c_old)[o])
+                                        : (double)static_cast<const float*>(cc.c_old)[o];
+            r += old;
+            d += fabs(old);
+        }
+        if (cc.cons & XTC_CONSUMER_BIAS) {
+            r += (double)cc.bias[n];
+            d += fabs((double)cc.bias[n]);
+        }
+        if (cc.cons & XTC_CONSUMER_RELU) r = fmax(r, 0.0);
         double c;
         bool bits_ok;
         if (out_bf16) {
@@ -183,10 +196,10 @@ __global__ void compare_kernel(const void* C, int out_bf16, int relu, int64_t M,
     if (nan) atomicAdd(&out->n_nan, nan);
 }
 
-cudaError_t launch_compare(const void* C, int out_bf16, int relu, int64_t M, int64_t N, int64_t ldc, const double* R,
-                           const double* D, double* blk_err, int64_t* blk_idx, void* counts, int blocks,
+cudaError_t launch_compare(const void* C, int out_bf16, const CmpConsumer& cc, int64_t M, int64_t N, int64_t ldc,
+                           const double* R, const double* D, double* blk_err, int64_t* blk_idx, void* counts, int blocks,
                            cudaStream_t st) {
-    compare_kernel<<<blocks, 256, 0, st>>>(C, out_bf16, relu, M, N, ldc, R, D, blk_err, blk_idx,
+    compare_kernel<<<blocks, 256, 0, st>>>(C, out_bf16, cc, M, N, ldc, R, D, blk_err, blk_idx,
                                            static_cast<CmpOut*>(counts));
     return cudaGetLastError();
 }
@@ -235,27 +248,40 @@ cudaError_t launch_compare_finalize(const double* blk_err, const int64_t* blk_id
     return cudaGetLastError();
 }
 
+// The consumer (include/xtc.h xtc_consumer) on one complete sum v of output (m, col):
+// relu(C_old + v + bias[col]).  The caller reads C_old from C before overwriting it.
+__device__ __forceinline__ float consume(float v, int cons, const float* bias, const void* C, int out_bf16,
+                                         int64_t off, int64_t col) {
+    if (cons & XTC_CONSUMER_ACCUMULATE)
+        v += out_bf16 ? __bfloat162float(static_cast<const __nv_bfloat16*>(C)[off]) : static_cast<const float*>(C)[off];
+    if (cons & XTC_CONSUMER_BIAS) v += bias[col];
+    if (cons & XTC_CONSUMER_RELU) v = fmaxf(v, 0.f);
+    return v;
+}
+
 // --------------------------------------------- unfused consumer (fuse = 0) --
-// relu as its own elementwise pass over the output (the paper's separate graph op);
-// one read + one write of C.
-__global__ void relu_kernel(void* C, int out_bf16, int64_t M, int64_t N, int64_t ldc) {
+// bias / relu as their own elementwise pass over the output (the paper's separate graph
+// ops); one read + one write of C.  (Accumulate is never unfused: C would be gone.)
+__global__ void consumer_pass_kernel(void* C, int out_bf16, int64_t M, int64_t N, int64_t ldc, int cons,
+                                     const float* bias) {
     const int64_t total = M * N;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t m = i / N, n = i - m * N;
+        const int64_t m = i / N, n = i - m * N, o = m * ldc + n;
         if (out_bf16) {
-            __nv_bfloat16* p = static_cast<__nv_bfloat16*>(C) + m * ldc + n;
-            if (__bfloat162float(*p) < 0.f) *p = __float2bfloat16_rn(0.f);
+            __nv_bfloat16* p = static_cast<__nv_bfloat16*>(C) + o;
+            *p = __float2bfloat16_rn(consume(__bfloat162float(*p), cons, bias, C, out_bf16, o, n));
         } else {
-            float* p = static_cast<float*>(C) + m * ldc + n;
-            *p = fmaxf(*p, 0.f);
+            float* p = static_cast<float*>(C) + o;
+            *p = consume(*p, cons, bias, C, out_bf16, o, n);
         }
     }
 }
 
-cudaError_t launch_relu(void* C, int out_bf16, int64_t M, int64_t N, int64_t ldc, cudaStream_t st) {
+cudaError_t launch_consumer_pass(void* C, int out_bf16, int64_t M, int64_t N, int64_t ldc, int cons,
+                                 const float* bias, cudaStream_t st) {
     int64_t blocks = (M * N + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
-    relu_kernel<<<(int)blocks, 256, 0, st>>>(C, out_bf16, M, N, ldc);
+    consumer_pass_kernel<<<(int)blocks, 256, 0, st>>>(C, out_bf16, M, N, ldc, cons & ~XTC_CONSUMER_ACCUMULATE, bias);
     return cudaGetLastError();
 }
 
@@ -323,7 +349,7 @@ cudaError_t launch_flush(void* buf, int64_t bytes, uint32_t salt, cudaStream_t s
 
 // ----------------------------------------------------------- split-K reduce --
 __global__ void splitk_reduce_kernel(const float* __restrict__ W, int S, int64_t M, int64_t N, int64_t ws_ld,
-                                     void* C, int64_t ldc, int out_bf16, int relu) {
+                                     void* C, int64_t ldc, int out_bf16, int cons, const float* bias) {
     const int64_t groups_per_row = (N + 3) / 4;
     const int64_t total = M * groups_per_row;
     const int64_t plane = M * ws_ld;
@@ -337,9 +363,9 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ W, int S, int64_t
             acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
         }
         float a[4] = {acc.x, acc.y, acc.z, acc.w};
-        if (relu)                                      // fused consumer on the complete sums
-            for (int j = 0; j < 4; ++j) a[j] = fmaxf(a[j], 0.f);
         const int cnt = (int)((N - n) < 4 ? (N - n) : 4);
+        if (cons)                                      // fused consumer on the complete sums
+            for (int j = 0; j < cnt; ++j) a[j] = consume(a[j], cons, bias, C, out_bf16, m * ldc + n + j, n + j);
         for (int j = 0; j < cnt; ++j) {
             if (out_bf16) static_cast<__nv_bfloat16*>(C)[m * ldc + n + j] = __float2bfloat16_rn(a[j]);
             else static_cast<float*>(C)[m * ldc + n + j] = a[j];
@@ -348,18 +374,19 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ W, int S, int64_t
 }
 
 cudaError_t launch_splitk_reduce(const float* W, int S, int64_t M, int64_t N, int64_t ws_ld, void* C, int64_t ldc,
-                                 int out_bf16, int relu, cudaStream_t st) {
+                                 int out_bf16, int cons, const float* bias, cudaStream_t st) {
     int64_t total = M * ((N + 3) / 4);
     int64_t blocks = (total + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
-    splitk_reduce_kernel<<<(int)blocks, 256, 0, st>>>(W, S, M, N, ws_ld, C, ldc, out_bf16, relu);
+    splitk_reduce_kernel<<<(int)blocks, 256, 0, st>>>(W, S, M, N, ws_ld, C, ldc, out_bf16, cons, bias);
     return cudaGetLastError();
 }
 
 // ---------------------------------------------- split_n_at remainder root --
 // The paper's scalar remainder loop (Fig.3 lines 33-35): one output
 // per thread, ascending k, fp32 FMA.
-__global__ void tail_gemm_kernel(const void* A, const void* B, int bf16_in, void* C, int out_bf16, int relu,
+__global__ void tail_gemm_kernel(const void* A, const void* B, int bf16_in, void* C, int out_bf16, int cons,
+                                 const float* bias,
                                  int64_t M, int64_t n0, int64_t ntail, int64_t K, int64_t lda, int64_t ldb,
                                  int64_t ldc) {
     const int64_t j = (int64_t)blockIdx.x * 16 + (threadIdx.x & 15);
@@ -378,15 +405,16 @@ __global__ void tail_gemm_kernel(const void* A, const void* B, int bf16_in, void
         }
         s = fmaf(a, b, s);
     }
-    if (relu) s = fmaxf(s, 0.f);
+    if (cons) s = consume(s, cons, bias, C, out_bf16, i * ldc + col, col);
     if (out_bf16) static_cast<__nv_bfloat16*>(C)[i * ldc + col] = __float2bfloat16_rn(s);
     else static_cast<float*>(C)[i * ldc + col] = s;
 }
 
-cudaError_t launch_tail_gemm(const void* A, const void* B, int bf16_in, void* C, int out_bf16, int relu, int64_t M,
-                             int64_t n0, int64_t ntail, int64_t K, int64_t lda, int64_t ldb, int64_t ldc, int gx, int gy,
-                             cudaStream_t st) {
-    tail_gemm_kernel<<<dim3(gx, gy), 256, 0, st>>>(A, B, bf16_in, C, out_bf16, relu, M, n0, ntail, K, lda, ldb, ldc);
+cudaError_t launch_tail_gemm(const void* A, const void* B, int bf16_in, void* C, int out_bf16, int cons,
+                             const float* bias, int64_t M, int64_t n0, int64_t ntail, int64_t K, int64_t lda, int64_t ldb,
+                             int64_t ldc, int gx, int gy, cudaStream_t st) {
+    tail_gemm_kernel<<<dim3(gx, gy), 256, 0, st>>>(A, B, bf16_in, C, out_bf16, cons, bias, M, n0, ntail, K, lda, ldb,
+                                                   ldc);
     return cudaGetLastError();
 }
 

@@ -48,7 +48,8 @@ xtc_status check_desc(const xtc_op_desc& d, std::string& why) {
     if (d.kind != XTC_OP_MATMUL && d.kind != XTC_OP_CONV2D) INVALID("unknown op kind %d", d.kind);
     if (d.in_dtype < XTC_F32 || d.in_dtype > XTC_TF32) INVALID("unknown in_dtype %d", d.in_dtype);
     if (d.out_dtype != XTC_F32 && d.out_dtype != XTC_BF16) INVALID("out_dtype must be F32 or BF16");
-    if (d.consumer != XTC_CONSUMER_NONE && d.consumer != XTC_CONSUMER_RELU) INVALID("unknown consumer %d", d.consumer);
+    if (d.consumer & ~(XTC_CONSUMER_RELU | XTC_CONSUMER_BIAS | XTC_CONSUMER_ACCUMULATE))
+        INVALID("unknown consumer bits 0x%x", d.consumer);
     if (d.kind == XTC_OP_MATMUL) {
         if (d.m <= 0 || d.n <= 0 || d.k <= 0) INVALID("matmul extents must be > 0 (m=%lld n=%lld k=%lld)",
                                                       (long long)d.m, (long long)d.n, (long long)d.k);
@@ -326,11 +327,16 @@ xtc_status make_plan(const xtc_op_desc& d, const xtc_schedule& s, int num_sms, P
     // fuse: the consumer runs in the producer's epilogue, in the split-K
     // reduction (which produces the complete sums), or as its own elementwise pass
     if (s.fuse != 0 && s.fuse != 1) ILLEGAL("fuse must be 0 or 1");
-    if (d.consumer == XTC_CONSUMER_RELU) {
-        if (s.fuse && p.atomic) ILLEGAL("fuse: relu cannot be fused with atomic split-K (partial sums)");
-        p.relu_epi = s.fuse && p.split_k == 1;
-        p.relu_reduce = s.fuse && p.split_k > 1;
-        p.relu_pass = !s.fuse;
+    if (d.consumer) {
+        if (s.fuse && p.atomic && (d.consumer & XTC_CONSUMER_RELU))
+            ILLEGAL("fuse: relu cannot be fused with atomic split-K (partial sums)");
+        if (!s.fuse && (d.consumer & XTC_CONSUMER_ACCUMULATE))
+            ILLEGAL("fuse: accumulate must be fused (an unfused C += A*B would need a temporary for A*B)");
+        // atomic split-K: the first K segment adds the bias, accumulate = C is not cleared
+        p.cons_epi = (s.fuse && (p.split_k == 1 || p.atomic)) ? d.consumer : 0;
+        p.cons_reduce = (s.fuse && p.split_k > 1 && !p.atomic) ? d.consumer : 0;
+        p.cons_pass = s.fuse ? 0 : d.consumer;
+        p.cons_tail = s.fuse ? d.consumer : 0;
     }
     if (s.engine == XTC_ENGINE_SIMT) st = plan_simt(d, s, num_sms, p, why);
     else if (s.engine == XTC_ENGINE_TCGEN05) st = plan_tc(d, s, num_sms, p, why);

@@ -92,9 +92,9 @@ struct Plan {
     int64_t workspace_bytes = 0;
     bool atomic = false;
     // split_n_at remainder root (SIMT, fixed 16x16x16 1x1 tile)
-    // consumer (relu) placement: fused in the epilogue, fused in the split-K reduction,
-    // or a separate pass (fuse = 0)
-    bool relu_epi = false, relu_reduce = false, relu_pass = false;
+    // consumer (XTC_CONSUMER_* bits) placement: fused in the epilogue, fused in the split-K
+    // reduction, in the split_n_at remainder root, or a separate pass (fuse = 0)
+    int32_t cons_epi = 0, cons_reduce = 0, cons_pass = 0, cons_tail = 0;
     bool has_tail = false;
     int64_t tail_n0 = 0, tail_n = 0;
     int32_t tail_grid_x = 0, tail_grid_y = 0;
@@ -126,7 +126,8 @@ struct SimtParams {
     int64_t num_tiles;
     int32_t out_bf16, split_out, atomic;
     int32_t fast;        // aligned matmul: 16-byte vectorised pack + float4 A fragments
-    int32_t relu;        // fused consumer in the epilogue
+    int32_t cons;        // fused consumer bits (XTC_CONSUMER_*) applied in the epilogue
+    const float* bias;   // XTC_CONSUMER_BIAS: one fp32 value per output column
     ConvGeom cg;
 };
 
@@ -139,7 +140,8 @@ struct TcParams {
     int32_t acc_buffers, buffer_c, atomic, out_bf16, split_out;
     int32_t pack_warps;      // 1..3 TMA-issuing warps (warps 0, 2, 3)
     int32_t b_resident;      // all of B packed once per CTA (kb_total x b_stage_bytes before the A ring)
-    int32_t relu;            // fused consumer in the epilogue
+    int32_t cons;            // fused consumer bits (XTC_CONSUMER_*) applied in the epilogue
+    const float* bias;       // XTC_CONSUMER_BIAS: one fp32 value per output column
     int32_t a3d, b3d;        // one 3-D TMA per stage for all 128-B atoms of A / B (tmA / tmB are 3-D maps)
     int32_t debug_skip_mma;  // diagnostics only, output invalid: XTC_DEBUG_SKIP_MMA, or XTC_DEBUG_SKIP=mask
                              // (conv_halo: 1 no MMAs, 2 no patch TMA, 4 no output stores)
@@ -161,6 +163,14 @@ constexpr int kTraceCtas = 160;          // >= #SMs: the whole persistent grid
 constexpr int kTraceK = 96;
 constexpr int kTraceTiles = 16;
 constexpr int kTraceSlots = 8 + 2 * kTraceK + 2 * kTraceTiles;
+
+// Validation of the consumer (harness.cu compare_kernel): bits, bias, and the snapshot of
+// the output taken before the validated run (XTC_CONSUMER_ACCUMULATE; same layout as C).
+struct CmpConsumer {
+    int32_t cons;
+    const float* bias;
+    const void* c_old;
+};
 
 // counters.cpp: named hardware counters through the CUPTI range profiler (dlopen'ed).
 // split_counter_names strips the "gpu." prefix; collect_counters wraps one range around

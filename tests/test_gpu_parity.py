@@ -5,7 +5,7 @@ import torch
 
 import paper_2512_16512_b200 as xtc
 from seeded_inputs import MODE_INT, MODE_UNIFORM, gen_tensor
-from gpu_util import (TORCH_DT, check_against_oracle, dev_tensor, oracle_conv, oracle_matmul, run_matmul,
+from gpu_util import (TORCH_DT, check_against_oracle, dev_tensor, oracle_conv, oracle_matmul, out_as_f64, run_matmul,
                       to_numpy_out)
 
 pytestmark = pytest.mark.gpu
@@ -512,3 +512,105 @@ def test_fuse_relu_conv():
     O, D = oracle_conv(d, "bf16", MODE_INT, 30, 31)
     import oracle as _o
     check_against_oracle(y, _o.relu(O), D, "bf16", True, 0.0)
+
+
+# ------------------------------------------------- consumers: bias / accumulate --
+def run_consumer(d, sch, cons, in_dtype, out_dtype, mode, seed=40):
+    """One run of `sch` with the consumer bits `cons` (include/xtc.h) against
+    oracle.consume(oracle result, relu, bias, C_old); then the library's own validation."""
+    import oracle as _o
+    from seeded_inputs import gen_tensor as _gen
+    d.consumer = xtc.consumer_bits(cons)
+    is_conv = d.kind == xtc.XTC_OP_CONV2D
+    M, N, K = xtc.gemm_view(d)
+    if is_conv:
+        a = dev_tensor((d.batch, d.h, d.w, d.c), in_dtype, seed, mode)
+        b = dev_tensor((d.r, d.s, d.c, d.f), in_dtype, seed + 1, mode)
+        O, D = oracle_conv(d, in_dtype, mode, seed, seed + 1)
+    else:
+        a = dev_tensor((M, K), in_dtype, seed, mode)
+        b = dev_tensor((K, N), in_dtype, seed + 1, mode)
+        O, D = oracle_matmul(M, N, K, in_dtype, mode, seed, seed + 1)
+    bits = d.consumer
+    bias = dev_tensor((N,), "f32", seed + 7, mode) if bits & xtc.XTC_CONSUMER_BIAS else None
+    if bits & xtc.XTC_CONSUMER_ACCUMULATE:
+        c = dev_tensor((M, N), out_dtype, seed + 9, mode)
+    else:
+        c = torch.full((M, N), float("nan"), dtype=TORCH_DT[out_dtype], device="cuda:0")
+    c_old = out_as_f64(to_numpy_out(c, out_dtype), out_dtype).reshape(M, N) if bits & xtc.XTC_CONSUMER_ACCUMULATE else None
+    bias_np = _gen(seed + 7, (N,), "f32", mode).astype(np.float64) if bias is not None else None
+    op = xtc.Op(d).apply(sch)
+    op.run(a, b, c, bias=bias)
+    torch.cuda.synchronize()
+    want = _o.consume(O, bool(bits & xtc.XTC_CONSUMER_RELU), bias_np, c_old)
+    Dn = D + (np.abs(c_old) if c_old is not None else 0) + (np.abs(bias_np)[None, :] if bias_np is not None else 0)
+    exact = mode == MODE_INT
+    tol = 1e-5 if in_dtype == "f32" else 5e-3
+    check_against_oracle(c, want, Dn, out_dtype, exact, tol)
+    m = op.measure(a, b, c, xtc.measure_cfg(warmup=1, repeats=2, validate=1, exact=int(exact), tol=tol), bias=bias)
+    assert m.valid == 1, m.as_dict()
+    return op
+
+
+CONS = ["bias", "accumulate", "bias+relu", "accumulate+bias+relu"]
+
+
+@pytest.mark.parametrize("cons", CONS)
+@pytest.mark.parametrize("mode", [MODE_INT, MODE_UNIFORM])
+def test_consumer_tcgen05_epilogue(cons, mode):
+    d = lambda: xtc.matmul_desc(256, 320, 192, "bf16", "bf16")
+    run_consumer(d(), tc(tile_n=64, fuse=1), cons, "bf16", "bf16", mode)                       # TMA-store epilogue
+    run_consumer(d(), tc(tile_n=64, fuse=1, buffer_c=0), cons, "bf16", "bf16", mode)           # direct stores
+    run_consumer(xtc.matmul_desc(256, 320, 192, "bf16", "f32"), tc(tile_n=64, fuse=1, persistent=1, acc_buffers=2),
+                 cons, "bf16", "f32", mode)
+    run_consumer(xtc.matmul_desc(512, 512, 256, "bf16", "bf16"),
+                 tc(tile_m=256, cluster_m=2, tile_n=256, fuse=1, persistent=1, acc_buffers=2), cons, "bf16", "bf16", mode)
+
+
+@pytest.mark.parametrize("cons", CONS)
+def test_consumer_split_k_ordered_atomic_and_tail(cons):
+    run_consumer(xtc.matmul_desc(256, 256, 512, "bf16", "bf16"), tc(tile_n=128, split_k=4, fuse=1), cons,
+                 "bf16", "bf16", MODE_INT)                                                    # in the reduction
+    if "relu" not in cons:                                                                    # relu + atomics: illegal
+        run_consumer(xtc.matmul_desc(256, 256, 512, "bf16", "f32"),
+                     tc(tile_n=128, split_k=4, split_k_mode=1, buffer_c=0, fuse=1), cons, "bf16", "f32", MODE_INT)
+        run_consumer(xtc.matmul_desc(128, 96, 256, "f32", "f32"),
+                     S(engine=0, tile_m=32, tile_n=32, tile_k=8, inner_m=2, inner_n=2, split_k=4, split_k_mode=1,
+                       fuse=1), cons, "f32", "f32", MODE_INT)
+    run_consumer(xtc.matmul_desc(256, 258, 512, "f32", "f32"),                                  # split_n_at remainder root
+                 S(engine=0, tile_m=16, tile_n=128, tile_k=4, inner_m=1, inner_n=8, unroll_k=4, vector_n=4, stages=1,
+                   split_n_at=256, fuse=1), cons, "f32", "f32", MODE_INT)
+
+
+@pytest.mark.parametrize("cons", CONS)
+def test_consumer_conv_simt_and_unfused(cons):
+    run_consumer(xtc.conv2d_desc(2, 14, 14, 64, 128, 3, 3, 1, 1, "bf16", "bf16"), tc(tile_n=128, fuse=1), cons,
+                 "bf16", "bf16", MODE_INT)                                                    # im2col conv
+    run_consumer(xtc.conv2d_desc(2, 56, 56, 64, 64, 3, 3, 1, 1, "bf16", "bf16"),
+                 tc(pack_halo=1, tile_n=64, stages=2, b_resident=1, persistent=1, acc_buffers=2, fuse=1), cons,
+                 "bf16", "bf16", MODE_INT)                                                    # halo conv, TMA store
+    run_consumer(xtc.conv2d_desc(1, 9, 13, 64, 64, 3, 3, 1, 1, "bf16", "f32"),
+                 tc(pack_halo=1, tile_n=64, stages=3, buffer_c=0, fuse=1), cons, "bf16", "f32", MODE_INT)
+    run_consumer(xtc.matmul_desc(200, 136, 328, "f32", "f32"),
+                 S(engine=0, tile_m=64, tile_n=64, tile_k=16, inner_m=4, inner_n=4, unroll_k=4, vector_n=4, stages=2,
+                   swizzle=4, fuse=1), cons, "f32", "f32", MODE_UNIFORM)
+    if "accumulate" not in cons:                                                              # unfused: its own pass
+        run_consumer(xtc.matmul_desc(256, 384, 320, "bf16", "bf16"), tc(tile_n=128, fuse=0), cons, "bf16", "bf16",
+                     MODE_INT)
+
+
+def test_consumer_bias_pointer_required_and_sweep_with_accumulate():
+    d = xtc.matmul_desc(256, 256, 256, "bf16", "bf16", consumer="bias")
+    a = dev_tensor((256, 256), "bf16", 1, MODE_INT)
+    b = dev_tensor((256, 256), "bf16", 2, MODE_INT)
+    c = torch.empty((256, 256), dtype=torch.bfloat16, device="cuda:0")
+    op = xtc.Op(d).apply(tc())
+    with pytest.raises(xtc.XtcError, match="INVALID_ARG"):
+        op.run(a, b, c)
+    d2 = xtc.matmul_desc(256, 256, 256, "bf16", "f32", consumer="accumulate+bias")
+    bias = dev_tensor((256,), "f32", 3, MODE_INT)
+    c2 = dev_tensor((256, 256), "f32", 4, MODE_INT)
+    recs = xtc.Op(d2).sweep([tc(tile_n=128, fuse=1), tc(tile_n=64, split_k=2, fuse=1),
+                             tc(tile_n=128, split_k=2, split_k_mode=1, buffer_c=0, fuse=1)], a, b, c2,
+                            xtc.measure_cfg(warmup=1, repeats=2, validate=1, exact=1), bias=bias)
+    assert [r.valid for r in recs] == [1, 1, 1], [r.as_dict() for r in recs]

@@ -178,6 +178,22 @@ def test_pack_halo_legality(desc, kw, frag):
     assert st != xtc.XTC_OK
 
 
+def test_consumer_bitmask_legality():
+    """bias / accumulate: accumulate must be fused; relu cannot ride atomic split-K."""
+    acc = xtc.matmul_desc(256, 256, 256, "bf16", "f32", consumer="accumulate+bias")
+    st, _, why = chk(acc, **dict(TCB, fuse=0))
+    assert st == xtc.XTC_E_ILLEGAL_SCHEDULE and "accumulate must be fused" in why
+    for kw in (dict(fuse=1), dict(fuse=1, split_k=2), dict(fuse=1, split_k=2, split_k_mode=1, buffer_c=0)):
+        st, _, why = chk(acc, **dict(TCB, **kw))
+        assert st == xtc.XTC_OK, (kw, why)
+    br = xtc.matmul_desc(256, 256, 256, "bf16", "f32", consumer="bias+relu")
+    st, _, why = chk(br, **dict(TCB, fuse=1, split_k=2, split_k_mode=1, buffer_c=0))
+    assert st == xtc.XTC_E_ILLEGAL_SCHEDULE and "atomic" in why
+    st, _, why = chk(br, **dict(TCB, fuse=0))
+    assert st == xtc.XTC_OK, why
+    assert xtc.consumer_bits("accumulate+bias+relu") == 7 and xtc.consumer_bits(None) == 0
+
+
 def test_default_schedules_are_legal():
     for d in (MM, xtc.matmul_desc(8192, 8192, 8192), xtc.conv2d_desc(32, 56, 56, 64, 64),
               xtc.conv2d_desc(32, 14, 14, 256, 256), xtc.matmul_desc(32, 32, 32, "f32", "f32"),
@@ -255,6 +271,6 @@ def test_fuse_legality():
         st, _, why = chk(d, **args)
         assert st == xtc.XTC_OK, (kw, why)
     bad = xtc.matmul_desc(64, 64, 64, "bf16", "f32")
-    bad.consumer = 7
+    bad.consumer = 8                                  # not an XTC_CONSUMER_* bit
     st, _, why = xtc.xtc_schedule_check(bad, S(**TCB))
     assert st == xtc.XTC_E_INVALID_ARG

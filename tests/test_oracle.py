@@ -227,3 +227,37 @@ def test_relu_spec_worked_example():
     v = np.array([-1.0, 2.0])
     C, _ = oracle.matmul(np.repeat(u[:, None], 4, 1), np.repeat(v[None, :], 4, 0))
     assert np.array_equal(oracle.relu(C), 4 * np.maximum(np.outer(u, v), 0))
+
+
+# --------------------------------------------- consumer: bias / accumulate --
+def test_consume_bias_is_an_augmented_matmul():
+    """C + 1·biasᵀ = [A | 1] · [B ; biasᵀ] (block-matrix identity, computed through matmul)."""
+    rng = np.random.default_rng(3)
+    A = rng.integers(-2, 3, (7, 5)).astype(np.float64)
+    B = rng.integers(-2, 3, (5, 6)).astype(np.float64)
+    bias = rng.integers(-9, 10, 6).astype(np.float64)
+    C, _ = oracle.matmul(A, B)
+    aug, _ = oracle.matmul(np.hstack([A, np.ones((7, 1))]), np.vstack([B, bias[None, :]]))
+    assert np.array_equal(oracle.consume(C, bias=bias), aug)
+
+
+def test_consume_accumulate_is_an_augmented_matmul():
+    """C_old + A·B = [A | I] · [B ; C_old] (Fig.2's C[i][j] += ...)."""
+    rng = np.random.default_rng(4)
+    A = rng.integers(-2, 3, (6, 4)).astype(np.float64)
+    B = rng.integers(-2, 3, (4, 5)).astype(np.float64)
+    Cold = rng.integers(-20, 21, (6, 5)).astype(np.float64)
+    C, _ = oracle.matmul(A, B)
+    aug, _ = oracle.matmul(np.hstack([A, np.eye(6)]), np.vstack([B, Cold]))
+    assert np.array_equal(oracle.consume(C, c_old=Cold), aug)
+
+
+def test_consume_order_hand_example():
+    """relu is applied last, after C_old and bias: relu([[-3, 1]] + [[1, 0]] + [2, -5]) = [[0, 0]],
+    while without relu = [[0, -4]]; and with A = 0 the output is relu(C_old + bias) broadcast."""
+    O = np.array([[-3.0, 1.0]])
+    assert oracle.consume(O, relu_=True, bias=[2.0, -5.0], c_old=[[1.0, 0.0]]).tolist() == [[0.0, 0.0]]
+    assert oracle.consume(O, relu_=False, bias=[2.0, -5.0], c_old=[[1.0, 0.0]]).tolist() == [[0.0, -4.0]]
+    assert oracle.consume(O, relu_=True, bias=[2.0, 5.0]).tolist() == [[0.0, 6.0]]
+    Z, _ = oracle.matmul(np.zeros((3, 4)), np.ones((4, 2)))
+    assert oracle.consume(Z, relu_=True, bias=[-1.0, 7.0]).tolist() == [[0.0, 7.0]] * 3
