@@ -274,3 +274,21 @@ def test_fuse_legality():
     bad.consumer = 8                                  # not an XTC_CONSUMER_* bit
     st, _, why = xtc.xtc_schedule_check(bad, S(**TCB))
     assert st == xtc.XTC_E_INVALID_ARG
+
+
+# ------------------------------------------------------- traffic model (N3) ----
+def test_traffic_model_closed_forms():
+    from paper_2512_16512_b200.model import predicted_l2_bytes
+    d = xtc.matmul_desc(1024, 1024, 1024, "bf16", "bf16")
+    # 128x128 tiles: A and B each streamed N/128 resp. M/128 times -> 2 * 1024^3 * 2 B / 128
+    p = predicted_l2_bytes(d, S(**dict(TCB, tile_n=128)))
+    assert p["loads"] == 2 * 1024 ** 3 * 2 / 128 and p["outputs"] == 1024 * 1024 * 2 and p["partials"] == 0
+    # a CTA pair (tile_m 256) with tile_n 256 halves the operand traffic of 128x128
+    p2 = predicted_l2_bytes(d, S(**dict(TCB, tile_m=256, cluster_m=2, tile_n=256)))
+    assert p2["loads"] == p["loads"] / 2
+    # split-K does not change the operand loads, adds S fp32 planes written and read
+    p3 = predicted_l2_bytes(d, S(**dict(TCB, tile_n=128, split_k=4)))
+    assert p3["loads"] == p["loads"] and p3["partials"] == 2 * 4 * 1024 * 1024 * 4
+    # ragged: M = 300 -> 3 tiles of 128 rows are loaded in full boxes
+    pr = predicted_l2_bytes(xtc.matmul_desc(300, 128, 64, "bf16", "bf16"), S(**dict(TCB, tile_n=128)))
+    assert pr["loads"] == 3 * 1 * 64 * (128 + 128) * 2
