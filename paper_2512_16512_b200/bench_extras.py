@@ -34,6 +34,10 @@ CONV_SCHEDS = {
             dict(TC, tile_n=256, stages=4, buffer_c=1, acc_buffers=1, split_k=3, pack_warps=2)],
 }
 
+SPLIT3_SCHEDS = [dict(TC, tile_n=128, tile_k=32, stages=3, buffer_c=1, split_k=2),
+                 dict(TC, tile_n=128, tile_k=32, stages=3, buffer_c=1),
+                 dict(TC, tile_n=256, tile_k=32, stages=2, buffer_c=1, persistent=1, acc_buffers=2)]
+
 SIMT_SCHEDS = [
     dict(engine=0, tile_m=64, tile_n=64, tile_k=16, inner_m=4, inner_n=4, unroll_k=4, vector_n=4, stages=2, swizzle=4),
     dict(engine=0, tile_m=128, tile_n=64, tile_k=16, inner_m=8, inner_n=4, unroll_k=4, vector_n=4, stages=2,
@@ -59,7 +63,11 @@ def _best(xtc, torch, dev, desc, scheds, in_shapes, peak, fill_seed=11, flush=1)
     best = None
     rows = []
     for s in scheds:
-        op.apply(xtc.schedule(**s))
+        try:
+            op.apply(xtc.schedule(**s))
+        except xtc.XtcError as e:                  # illegal for this shape: recorded, not measured
+            rows.append({"illegal": str(e)[:160]})
+            continue
         m = op.measure(a, b, c, xtc.measure_cfg(warmup=3, repeats=20, flush_l2=flush, validate=1,
                                                 reuse_reference=1, peak_tflops=peak), stream=st)
         rows.append({"tflops_med": round(m.tflops_med, 1), "valid": int(m.valid), "t_med_us": round(m.t_med_ns / 1e3, 2)})
@@ -84,6 +92,14 @@ def run_extras(xtc, torch, dev, peak):
     if "tflops_med" in simt:
         simt["frac_fp32_simt_peak"] = simt["tflops_med"] / 72.5
     out["matmul_1024_f32_simt"] = simt
+    # the same fp32 configs on the tensor cores: the 3xTF32 split (validated at the fp32 1e-5 bar);
+    # its ceiling is a third of the tf32 rate (half the bf16 peak) = peak / 6
+    for n in (1024, 512):
+        d = xtc.matmul_desc(n, n, n, "f32", "f32")
+        r = _best(xtc, torch, dev, d, SPLIT3_SCHEDS, [(n, n), (n, n)], peak)
+        if "tflops_med" in r:
+            r["frac_3xtf32_peak"] = r["tflops_med"] / (peak / 6)
+        out[f"matmul_{n}_f32_3xtf32"] = r
     for name, (h, c) in {"L56": (56, 64), "L14": (14, 256)}.items():
         d = xtc.conv2d_desc(32, h, h, c, c, 3, 3, 1, 1, "bf16", "bf16")
         out[f"conv_{name}_n32_bf16"] = _best(xtc, torch, dev, d, CONV_SCHEDS[name], [(32, h, h, c), (3, 3, c, c)], peak)

@@ -398,7 +398,7 @@ static xtc_status encode_maps(xtc_op op, const void* A, const void* B, void* C) 
     const xtc_op_desc& d = op->d;
     xtc_status st = load_driver_fns();
     if (st != XTC_OK) return st;
-    const bool tf32 = d.in_dtype == XTC_TF32;
+    const bool tf32 = d.in_dtype == XTC_TF32 || p.split3;     // fp32 storage (tf32 or the 3xTF32 split)
     const CUtensorMapDataType in_t = tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
     const int es = dsize(d.in_dtype);
     const int atom = 128 / es;
@@ -607,7 +607,7 @@ static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cud
         tp.ws_ld = p.ws_ld;
         tp.C = C;
         tp.Wk = op->ws;
-        const bool tf32 = d.in_dtype == XTC_TF32;
+        const bool tf32 = d.in_dtype == XTC_TF32 || p.split3;     // 3xTF32: kind::tf32 on fp32 storage
         const uint32_t fmt = tf32 ? 2u : 1u;
         tp.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (0u << 15) | (1u << 16) |
                    ((uint32_t)(p.sch.tile_n >> 3) << 17) | ((uint32_t)((128 * p.cta_group) >> 4) << 24);
@@ -615,6 +615,7 @@ static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cud
         const int es = dsize(d.in_dtype);
         tp.a_stage_bytes = (uint32_t)(128 * p.sch.tile_k * es);
         tp.b_stage_bytes = (uint32_t)(p.sch.tile_k * (p.sch.tile_n / p.cta_group) * es);
+        tp.lo_off = p.split3 ? (uint32_t)(p.sch.stages * (tp.a_stage_bytes + tp.b_stage_bytes)) : 0u;
         tp.cg = conv_geom(d);
         const size_t trace_bytes = (size_t)kTraceCtas * kTraceSlots * 8;
         if (!op->trace_path.empty()) {

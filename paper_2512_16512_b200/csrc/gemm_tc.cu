@@ -35,7 +35,7 @@
 
 namespace xtc {
 
-template <bool TF32, bool CONV, int CG>
+template <bool TF32, bool CONV, int CG, bool SPLIT3>
 __global__ void __launch_bounds__(kTcThreads, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmC, const TcParams p) {
@@ -53,13 +53,15 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     uint8_t* sBres = smem;
     uint8_t* sA = smem + (b_res ? (size_t)p.kb_total * p.b_stage_bytes : 0);
     uint8_t* sB = sA + (size_t)S * p.a_stage_bytes;
-    uint8_t* sC = sB + (b_res ? 0 : (size_t)S * p.b_stage_bytes);
+    // SPLIT3 (3xTF32): the lo rings (A_lo, B_lo) follow the B ring, p.lo_off bytes after their hi rings
+    uint8_t* sC = sB + (b_res ? 0 : (size_t)S * p.b_stage_bytes) + (SPLIT3 ? (size_t)p.lo_off : 0);
     uint64_t* full = reinterpret_cast<uint64_t*>(sC + (p.buffer_c ? kTcEpiSmem : 0));
     uint64_t* empty = full + 8;
     uint64_t* tfull = empty + 8;
     uint64_t* tempty = tfull + 2;
     uint64_t* bfull = tempty + 2;            // resident B landed
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
+    uint64_t* split = bfull + 1;             // SPLIT3: lo parts of stage s written (warps 2 and 3)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(split + 8);
 
     if (p.trace && blockIdx.x < kTraceCtas && threadIdx.x == 0)
         p.trace[(size_t)blockIdx.x * kTraceSlots] = ptx::globaltimer();
@@ -79,6 +81,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         for (int s = 0; s < S; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
         for (int a = 0; a < 2; ++a) { ptx::mbar_init(&tfull[a], 1); ptx::mbar_init(&tempty[a], 4 * CG); }
         ptx::mbar_init(bfull, 1);
+        if constexpr (SPLIT3) for (int s = 0; s < S; ++s) ptx::mbar_init(&split[s], 2);
         ptx::fence_mbarrier_init();
     }
     if (warp == 2) {
@@ -214,6 +217,42 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 }
             }
         }
+    } else if (SPLIT3 && (warp == 2 || warp == 3)) {
+        // ===================== 3xTF32 split: lo = a - tf32(a) =====================
+        // kind::tf32 reads the hi part of an fp32 operand (the low 13 mantissa bits are
+        // ignored); the lo part is written at the same offsets of the lo rings, so it
+        // inherits the swizzled layout.  Warps 2 and 3 share each stage's A and B tiles.
+        int s = 0;
+        uint32_t ph = 0;
+        const uint32_t lo_off = p.lo_off;
+        auto split_buf = [&](uint8_t* hi, uint32_t bytes) {
+            const uint4* src = reinterpret_cast<const uint4*>(hi);
+            uint4* dst = reinterpret_cast<uint4*>(hi + lo_off);
+            for (uint32_t i = (uint32_t)((warp - 2) * 32 + lane); i < bytes / 16; i += 64) {
+                const uint4 x = src[i];
+                uint4 l;
+                l.x = __float_as_uint(__uint_as_float(x.x) - __uint_as_float(x.x & 0xFFFFE000u));
+                l.y = __float_as_uint(__uint_as_float(x.y) - __uint_as_float(x.y & 0xFFFFE000u));
+                l.z = __float_as_uint(__uint_as_float(x.z) - __uint_as_float(x.z & 0xFFFFE000u));
+                l.w = __float_as_uint(__uint_as_float(x.w) - __uint_as_float(x.w & 0xFFFFE000u));
+                dst[i] = l;
+            }
+        };
+        for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters) {
+            int mb, nb, ks;
+            tile_coords(p.tm, t, mb, nb, ks);
+            const int kb0 = ks * p.kb_per_split;
+            const int kb1 = min(p.kb_total, kb0 + p.kb_per_split);
+            for (int kb = kb0; kb < kb1; ++kb) {
+                ptx::mbar_wait(&full[s], ph);
+                split_buf(sA + (size_t)s * p.a_stage_bytes, p.a_stage_bytes);
+                split_buf(sB + (size_t)s * p.b_stage_bytes, p.b_stage_bytes);
+                ptx::fence_proxy_async_smem();       // generic-proxy stores -> visible to the tensor core
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&split[s]);
+                if (++s == S) { s = 0; ph ^= 1u; }
+            }
+        }
     } else if (warp == 1) {
         // ===================== MMA issuer (contraction) =====================
         // One elected lane runs each tile's whole k-loop (stage waits, UMMAs, commits); the
@@ -237,6 +276,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             const int Sring = ptx::pin(S), accb = ptx::pin(p.acc_buffers), tile_n = ptx::pin(p.tile_n);
             const int kb_per = ptx::pin(p.kb_per_split), kb_tot = ptx::pin(p.kb_total);
             const uint32_t b_res_u = ptx::pin((uint32_t)(b_res ? 1 : 0));
+            const uint32_t lo16 = ptx::pin(p.lo_off >> 4);     // SPLIT3: hi stage -> lo stage (16-byte units)
             if (b_res) ptx::mbar_wait(bfull, 0);     // resident B has landed (in both CTAs for a pair)
             // NA > 0: atoms per stage known at compile time; NA == 0: none (diagnostics);
             // NA < 0: runtime count n_a (other tile_k, and the traced variant)
@@ -259,6 +299,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                         uint32_t ph1 = ph;
                         for (int kb = kb0; kb < kb1; ++kb) {
                             ptx::mbar_wait(&full[s1], ph1);
+                            if constexpr (SPLIT3) ptx::mbar_wait(&split[s1], ph1);   // lo parts written
                             if constexpr (TR) {
                                 if (tk1 < kTraceK) trace[8 + kTraceK + tk1] = ptx::globaltimer();
                                 ++tk1;
@@ -267,14 +308,25 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                             const uint64_t ad = adesc0 + (uint64_t)((uint32_t)s1 * a_stage16);
                             const uint64_t bd = bdesc0 + (uint64_t)((b_res_u ? (uint32_t)kb : (uint32_t)s1) * b_stage16);
                             const uint32_t acc0 = kb > kb0 ? 1u : 0u;
+                            auto pass = [&](uint64_t ad_, uint64_t bd_, uint32_t first) {
 #pragma unroll
-                            for (int a = 0; a < (NA >= 0 ? NA : n_a); ++a) {
+                                for (int a = 0; a < (NA >= 0 ? NA : n_a); ++a) {
 #pragma unroll
-                                for (int kk = 0; kk < ATOM / UMMA_K; ++kk) {
-                                    const uint32_t krow = a * ATOM + kk * UMMA_K;
-                                    ptx::umma<TF32, CG>(d_tmem, ad + (uint64_t)((a * A_ATOM_BYTES + kk * 32) >> 4),
-                                                        bd + (uint64_t)(krow * 8), idesc, (a > 0 || kk > 0) ? 1u : acc0);
+                                    for (int kk = 0; kk < ATOM / UMMA_K; ++kk) {
+                                        const uint32_t krow = a * ATOM + kk * UMMA_K;
+                                        ptx::umma<TF32, CG>(d_tmem, ad_ + (uint64_t)((a * A_ATOM_BYTES + kk * 32) >> 4),
+                                                            bd_ + (uint64_t)(krow * 8), idesc,
+                                                            (a > 0 || kk > 0) ? 1u : first);
+                                    }
                                 }
+                            };
+                            if constexpr (SPLIT3) {
+                                // small terms first: hi*lo + lo*hi, then hi*hi
+                                pass(ad, bd + (uint64_t)lo16, acc0);
+                                pass(ad + (uint64_t)lo16, bd, 1u);
+                                pass(ad, bd, 1u);
+                            } else {
+                                pass(ad, bd, acc0);
                             }
                             ptx::umma_commit<CG>(&empty[s1]);   // frees the SMEM slot(s) when these MMAs finish
                             if (++s1 == Sring) { s1 = 0; ph1 ^= 1u; }
@@ -433,10 +485,10 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 }
 
 // ------------------------------------------------------------------ launch --
-template <bool TF32, bool CONV, int CG>
+template <bool TF32, bool CONV, int CG, bool SPLIT3 = false>
 static cudaError_t launch_tc_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
                                const TcParams& p, int grid, int smem, cudaStream_t st) {
-    auto k = tc_gemm_kernel<TF32, CONV, CG>;
+    auto k = tc_gemm_kernel<TF32, CONV, CG, SPLIT3>;
     cudaError_t e = ensure_smem_attr(k, smem);
     if (e != cudaSuccess) return e;
     if constexpr (CG == 1) {
@@ -471,6 +523,7 @@ static cudaError_t launch_tc_cg(bool tf32, bool conv, const CUtensorMap& a, cons
 
 cudaError_t launch_tc_gemm(bool tf32, bool conv, int cta_group, const CUtensorMap& a, const CUtensorMap& b,
                            const CUtensorMap& c, const TcParams& p, int grid, int smem, cudaStream_t st) {
+    if (p.lo_off) return launch_tc_t<true, false, 1, true>(a, b, c, p, grid, smem, st);   // 3xTF32 split (fp32)
     if (cta_group == 2) return launch_tc_cg<2>(tf32, conv, a, b, c, p, grid, smem, st);
     return launch_tc_cg<1>(tf32, conv, a, b, c, p, grid, smem, st);
 }

@@ -205,7 +205,19 @@ static xtc_status plan_tc_halo(const xtc_op_desc& d, const xtc_schedule& s, int 
 }
 
 static xtc_status plan_tc(const xtc_op_desc& d, const xtc_schedule& s, int num_sms, Plan& p, std::string& why) {
-    if (d.in_dtype != XTC_BF16 && d.in_dtype != XTC_TF32) ILLEGAL("tcgen05 engine needs BF16 or TF32 inputs");
+    // F32 inputs on the tensor cores: the 3xTF32 split, fp32-accurate:
+    // a = hi + lo with hi = a truncated to tf32 (what kind::tf32 reads) and lo = a - hi
+    // (exact in fp32); C = hi*lo + lo*hi + hi*hi.  Matmul, 1-CTA, single TMA producer.
+    p.split3 = d.in_dtype == XTC_F32;
+    if (p.split3) {
+        if (d.kind != XTC_OP_MATMUL) ILLEGAL("tcgen05 fp32 (3xTF32 split) is defined for matmul only");
+        if (s.pack_halo) ILLEGAL("tcgen05 fp32 (3xTF32 split): pack_halo must be 0");
+        if (s.cluster_m > 1) ILLEGAL("tcgen05 fp32 (3xTF32 split): cluster_m must be 1");
+        if (s.pack_warps > 1) ILLEGAL("tcgen05 fp32 (3xTF32 split): pack_warps must be 0 or 1 (warps 2-3 split)");
+        if (s.b_resident) ILLEGAL("tcgen05 fp32 (3xTF32 split): b_resident must be 0");
+    } else if (d.in_dtype != XTC_BF16 && d.in_dtype != XTC_TF32) {
+        ILLEGAL("tcgen05 engine needs BF16, TF32 or F32 (3xTF32 split) inputs");
+    }
     if (s.pack_halo) {
         p.atom_k = p.atom_n = 128 / dtype_size(d.in_dtype);
         return plan_tc_halo(d, s, num_sms, p, why);
@@ -252,9 +264,11 @@ static xtc_status plan_tc(const xtc_op_desc& d, const xtc_schedule& s, int num_s
                     s.stages, (long long)tot, kSmemMaxOptin);
         smem = (int)tot;
     } else {
-        smem = s.stages * (a_stage + b_stage) + (s.buffer_c ? kTcEpiSmem : 0) + kSmemReserve;
+        // 3xTF32: every stage also holds the lo parts of its A and B tiles
+        const int per_stage = (a_stage + b_stage) * (p.split3 ? 2 : 1);
+        smem = s.stages * per_stage + (s.buffer_c ? kTcEpiSmem : 0) + kSmemReserve;
         if (smem > kSmemMaxOptin) ILLEGAL("pack: %d stages x %d B + epilogue = %d B SMEM exceeds %d B",
-                                          s.stages, a_stage + b_stage, smem, kSmemMaxOptin);
+                                          s.stages, per_stage, smem, kSmemMaxOptin);
     }
     p.smem = smem;
     // TMA pitch / alignment rules (cuda.h cuTensorMapEncodeTiled: strides % 16 B)

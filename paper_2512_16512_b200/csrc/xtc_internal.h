@@ -87,6 +87,7 @@ struct Plan {
     int32_t grid_x = 1, grid_y = 1, grid_z = 1, block = 1, cluster = 1;
     int32_t smem = 0, tmem_cols = 0;
     int32_t cta_group = 1;
+    bool split3 = false;                // tcgen05 with F32 inputs: 3xTF32 split (hi*lo + lo*hi + hi*hi)
     int32_t atom_k = 0, atom_n = 0;     // tcgen05: elements per 128-byte swizzle row
     int64_t ws_ld = 0;                  // split-K workspace row pitch (floats)
     int64_t workspace_bytes = 0;
@@ -150,6 +151,7 @@ struct TcParams {
     uint32_t idesc;
     uint32_t tmem_cols;
     uint32_t a_stage_bytes, b_stage_bytes;
+    uint32_t lo_off;         // 3xTF32: byte offset from a hi stage (A or B ring) to its lo copy
     ConvGeom cg;
     // pack_halo conv only (see Plan)
     int32_t wp, rt, msub, planes, nbuf, tpi;

@@ -116,6 +116,27 @@ def test_tc_atomic_split_k():
     run_matmul(256, 256, 512, "bf16", "f32", tc(tile_n=128, split_k=4, split_k_mode=1, buffer_c=0), MODE_INT)
 
 
+# ------------------------------------------------- tcgen05 fp32 (3xTF32) --
+SPLIT3_SCHEDS = [dict(tile_k=32, tile_n=128, stages=3), dict(tile_k=32, tile_n=256, stages=2, persistent=1,
+                                                             acc_buffers=2),
+                 dict(tile_k=64, tile_n=64, stages=2, buffer_c=0), dict(tile_k=32, tile_n=128, stages=3, split_k=2)]
+
+
+@pytest.mark.parametrize("sch", SPLIT3_SCHEDS)
+def test_tc_fp32_3xtf32_at_the_fp32_tolerance(sch):
+    """fp32 inputs on the tensor cores (a = hi + lo, C = hi*lo + lo*hi + hi*hi) meet the fp32
+    bar of BASELINE (max |C - O| / D <= 1e-5), and are bit-exact on integer data."""
+    run_matmul(256, 384, 320, "f32", "f32", tc(**sch), MODE_INT)
+    err, _ = run_matmul(256, 384, 1024, "f32", "f32", tc(**sch), MODE_UNIFORM, tol=1e-5)
+    assert err <= 1e-5
+
+
+def test_tc_fp32_3xtf32_ragged_and_bf16_out():
+    err, _ = run_matmul(300, 328, 200, "f32", "f32", tc(tile_k=32, tile_n=128, stages=3), MODE_UNIFORM, tol=1e-5)
+    assert err <= 1e-5
+    run_matmul(256, 256, 256, "f32", "bf16", tc(tile_k=32, tile_n=128, stages=3), MODE_INT)
+
+
 # ---------------------------------------------------------- tcgen05 tf32 --
 @pytest.mark.parametrize("sch", [dict(tile_k=32, tile_n=128), dict(tile_k=64, tile_n=96, stages=3, buffer_c=0),
                                  dict(tile_k=32, tile_n=256, persistent=1, acc_buffers=2)])

@@ -93,10 +93,16 @@ def test_tc_legality(kw, frag):
         assert st == xtc.XTC_E_ILLEGAL_SCHEDULE and frag in why, (st, why)
 
 
-def test_tc_rejects_fp32_inputs_and_simt_rejects_bf16():
+def test_tc_fp32_is_the_3xtf32_split_and_simt_rejects_bf16():
     d32 = xtc.matmul_desc(256, 256, 256, "f32", "f32")
-    st, _, why = chk(d32, **TCB)
-    assert st == xtc.XTC_E_ILLEGAL_SCHEDULE and "BF16 or TF32" in why
+    st, info, why = chk(d32, **dict(TCB, tile_k=32, stages=3))
+    assert st == xtc.XTC_OK, why
+    assert info.smem_bytes == 3 * 2 * (128 * 32 * 4 + 32 * 128 * 4) + 32768 + 2048   # hi + lo per stage
+    for kw, frag in ((dict(tile_m=256, cluster_m=2, tile_n=256), "cluster_m"), (dict(pack_warps=2), "pack_warps")):
+        st, _, why = chk(d32, **dict(TCB, tile_k=32, stages=2, **kw))
+        assert st == xtc.XTC_E_ILLEGAL_SCHEDULE and frag in why, why
+    st, _, why = chk(xtc.conv2d_desc(1, 14, 14, 64, 64, 3, 3, 1, 1, "f32", "f32"), **dict(TCB, tile_k=32, stages=2))
+    assert st == xtc.XTC_E_ILLEGAL_SCHEDULE and "matmul only" in why
     st, _, why = chk(MM, engine=0, tile_m=16, tile_n=16, tile_k=8, inner_m=1, inner_n=1)
     assert st == xtc.XTC_E_ILLEGAL_SCHEDULE and "fp32" in why
 
