@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--no-extras", action="store_true", help="skip the secondary config lines (1024^3, conv, sweep)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sweep-candidates", type=int, default=1024)
+    ap.add_argument("--overlap-chunks", type=int, default=4,
+                    help="N>1: block-cyclic row chunks per rank, each all-gathered while the next computes")
     return ap.parse_args()
 
 
@@ -274,24 +276,56 @@ def main_xtc(args):
     Mr = r1 - r0
     stream = torch.cuda.current_stream(dev)
     sp = stream.cuda_stream
+    # N > 1 (chunked overlap): the rank's rows are CH chunks of Mc rows dealt
+    # block-cyclically (chunk j of rank r = global rows (j*W + r)*Mc ...), so chunk j gathered
+    # from every rank lands contiguously in C; chunk j's all-gather runs on NCCL's stream while
+    # chunk j+1 is computed.
+    CH = args.overlap_chunks if world > 1 else 1
+    if CH > 1 and M % (world * CH):
+        CH = 1
+    Mc = Mr // CH
     a = torch.empty((Mr, K), dtype=torch.bfloat16, device=dev)
     b = torch.empty((K, N), dtype=torch.bfloat16, device=dev)
     c = torch.empty((Mr, N), dtype=torch.bfloat16, device=dev)
     # every rank regenerates its rows of A and the whole of B from the seed: no broadcast needed
-    xtc.xtc_fill(a.data_ptr(), Mr * K, xtc.XTC_BF16, 1, 0, r0 * K, sp)
+    if CH > 1:
+        for j in range(CH):
+            g0 = (j * world + rank) * Mc
+            xtc.xtc_fill(a[j * Mc].data_ptr(), Mc * K, xtc.XTC_BF16, 1, 0, g0 * K, sp)
+    else:
+        xtc.xtc_fill(a.data_ptr(), Mr * K, xtc.XTC_BF16, 1, 0, r0 * K, sp)
     xtc.xtc_fill(b.data_ptr(), K * N, xtc.XTC_BF16, 2, 0, 0, sp)
     desc = xtc.matmul_desc(Mr, N, K, "bf16", "bf16")
     op = xtc.Op(desc, local).apply(xtc.schedule(**HEADLINE_SCHEDULE))
+    chunk_ops = [xtc.Op(xtc.matmul_desc(Mc, N, K, "bf16", "bf16"), local).apply(xtc.schedule(**HEADLINE_SCHEDULE))
+                 for _ in range(CH)] if CH > 1 else [op]
+    async_nccl = world > 1 and not rehearsal
 
     # a8 (on-chip validation: fp64 GPU reference, NaN sentinel) runs once AFTER the timed
     # region: its ~0.1 s fp64 reference kernel would otherwise heat the part right before timing
 
     full_c = torch.empty((M, N), dtype=torch.bfloat16, device=dev) if world > 1 else None
 
+    def compute_and_gather(kev_pair=None):
+        handles = []
+        if kev_pair is not None:
+            kev_pair[0].record(stream)
+        for j in range(CH):
+            cj = c[j * Mc:(j + 1) * Mc]
+            chunk_ops[j].run(a[j * Mc:(j + 1) * Mc], b, cj, stream=sp)
+            if world > 1:
+                out = full_c[j * world * Mc:(j + 1) * world * Mc] if CH > 1 else full_c
+                if async_nccl:
+                    handles.append(dist.all_gather_into_tensor(out, cj, async_op=True))
+                else:
+                    gather_rows(cj, out.shape[0], out=out)
+        if kev_pair is not None:
+            kev_pair[1].record(stream)
+        for h in handles:                           # the compute stream waits for every gather
+            h.wait()
+
     def step():
-        op.run(a, b, c, stream=sp)
-        if world > 1:
-            gather_rows(c, M, out=full_c)
+        compute_and_gather()
 
     for _ in range(args.warmup):
         step()
@@ -307,18 +341,14 @@ def main_xtc(args):
         t_start.record(stream)
         for i in range(args.steps):
             evs[i][0].record(stream)
-            kev[i][0].record(stream)
-            op.run(a, b, c, stream=sp)
-            kev[i][1].record(stream)
-            if world > 1:
-                gather_rows(c, M, out=full_c)
+            compute_and_gather(kev[i])
             evs[i][1].record(stream)
         t_end.record(stream)
         torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    launches_per_step = op.launches()
+    launches_per_step = sum(o.launches() for o in chunk_ops)
     total_ms = t_start.elapsed_time(t_end)
     kern_ms = [s.elapsed_time(e) for s, e in kev]
     step_ms = total_ms / args.steps
@@ -388,13 +418,23 @@ def main_xtc(args):
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_val = flops / (float(te[0]) / e2e_steps * 1e-3) / 1e12
 
-    vm = op.measure(a, b, c, xtc.measure_cfg(warmup=0, repeats=1, validate=1, tol=5e-3), stream=sp)
-    validation = {"valid": int(vm.valid), "max_norm_err": vm.max_norm_err, "n_nan": int(vm.n_nan), "tol": 5e-3,
-                  "n_mismatch_vs_rne_of_ref": int(vm.n_mismatch), "when": "after the timed region, same inputs"}
+    vms = [o.measure(a[j * Mc:(j + 1) * Mc], b, c[j * Mc:(j + 1) * Mc],
+                     xtc.measure_cfg(warmup=0, repeats=1, validate=1, tol=5e-3), stream=sp)
+           for j, o in enumerate(chunk_ops)]
+    validation = {"valid": int(min(vm.valid for vm in vms)), "max_norm_err": max(vm.max_norm_err for vm in vms),
+                  "n_nan": int(sum(vm.n_nan for vm in vms)), "tol": 5e-3,
+                  "n_mismatch_vs_rne_of_ref": int(sum(vm.n_mismatch for vm in vms)),
+                  "when": "after the timed region, same inputs"}
     if world > 1:
-        v = torch.tensor([validation["valid"]], device=dev)
+        # the assembled C holds this rank's chunks at their global rows
+        compute_and_gather()
+        torch.cuda.synchronize(dev)
+        ok = all(torch.equal(full_c[(j * world + rank) * Mc:(j * world + rank + 1) * Mc] if CH > 1 else
+                             full_c[r0:r1], c[j * Mc:(j + 1) * Mc] if CH > 1 else c) for j in range(CH))
+        v = torch.tensor([validation["valid"], int(ok)], device=dev)
         dist.all_reduce(v, op=dist.ReduceOp.MIN)
         validation["valid_all_ranks"] = int(v[0])
+        validation["gather_consistent_all_ranks"] = int(v[1])
 
     # a9 hardware counters by name for the headline kernel (CUPTI range profiler, a replay
     # pass of its own after the timed region): live DRAM traffic and tensor-pipe activity
@@ -450,7 +490,8 @@ def main_xtc(args):
             "data": "synthetic (seeded counter-based generator, uniform[-1,1) bf16)",
             "config": {"workload": "matmul 8192x8192x8192 bf16->bf16 (BASELINE config 5: largest matmul)",
                        "model": None, "global_batch": 1, "seq_len": None,
-                       "parallelism": f"M-sharded x{world} + NCCL all-gather" if world > 1 else "single GPU",
+                       "parallelism": (f"M-sharded x{world}, {CH} block-cyclic chunks per rank, each NCCL "
+                                       f"all-gather overlapping the next chunk's GEMM") if world > 1 else "single GPU",
                        "schedule": HEADLINE_SCHEDULE,
                        "l2": "inputs (256 MiB) exceed L2 (126 MB); no flush between steps"},
             "frac_of_peak": value / world / peak_tf,

@@ -401,6 +401,7 @@ def test_bench_two_rank_rehearsal_on_one_gpu(tmp_path):
     assert len(lines) == 1, out.stdout[-2000:]
     rec = json.loads(lines[0])
     assert rec["n_gpus"] == 2 and rec["validation"]["valid"] == 1 and rec["value"] > 0
+    assert rec["validation"]["valid_all_ranks"] == 1 and rec["validation"]["gather_consistent_all_ranks"] == 1
     sw = rec["extras"]["sweep_1024_bf16_sharded"]
     assert sw["ranks"] == 2 and sw["candidates"] == 32 and sw["valid"] + sw["invalid"] == 32
     cv = rec["extras"]["conv_L56_batch_sharded"]

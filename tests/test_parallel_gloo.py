@@ -45,6 +45,19 @@ def _worker(rank, world, port, q):
         full = gather_rows(torch.from_numpy(C_r), M)
         want, _ = oracle.matmul(A.astype(np.float64), B.astype(np.float64))
         assert np.array_equal(full.numpy(), want)
+        # 3) the overlapped form (bench.py N>1): CH block-cyclic chunks of Mc rows per rank, chunk j
+        #    of rank r = global rows (j*W + r)*Mc ...; gathering chunk by chunk assembles C in order
+        CH = 4
+        Mc = M // (world * CH)
+        rows_mine = np.concatenate([np.arange((j * world + rank) * Mc, (j * world + rank + 1) * Mc)
+                                    for j in range(CH)])
+        C_bc, _ = oracle.matmul(A[rows_mine].astype(np.float64), B.astype(np.float64))
+        C_bc = torch.from_numpy(C_bc)
+        full_bc = torch.empty((M, N), dtype=C_bc.dtype)
+        for j in range(CH):
+            gather_rows(C_bc[j * Mc:(j + 1) * Mc].contiguous(), world * Mc,
+                        out=full_bc[j * world * Mc:(j + 1) * world * Mc])
+        assert np.array_equal(full_bc.numpy(), want)
         q.put((rank, "ok"))
     except Exception as e:  # pragma: no cover
         q.put((rank, repr(e)))
