@@ -416,7 +416,9 @@ static xtc_status encode_maps(xtc_op op, const void* A, const void* B, void* C) 
         if (allow3d && p.N % atom == 0) {
             cuuint64_t dims[3] = {(cuuint64_t)atom, (cuuint64_t)p.K, (cuuint64_t)(p.N / atom)};
             cuuint64_t strides[2] = {(cuuint64_t)(ldb * es), (cuuint64_t)(atom * es)};
-            cuuint32_t box[3] = {(cuuint32_t)atom, (cuuint32_t)tile_k, (cuuint32_t)(tile_n / p.cta_group / atom)};
+            // each CTA of a pair (or of a halo multicast cluster) loads its share of the N blocks
+            const int b_share = p.halo ? p.halo_cl : p.cta_group;
+            cuuint32_t box[3] = {(cuuint32_t)atom, (cuuint32_t)tile_k, (cuuint32_t)(tile_n / b_share / atom)};
             cuuint32_t estr[3] = {1, 1, 1};
             r = g_encode_tiled(&op->tmB, in_t, 3, const_cast<void*>(B), dims, strides, box, estr,
                                CU_TENSOR_MAP_INTERLEAVE_NONE, bsw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -630,6 +632,7 @@ static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cud
             tp.planes = p.halo_planes;
             tp.nbuf = p.halo_nbuf;
             tp.tpi = p.halo_tpi;
+            tp.cl = p.halo_cl;
             tp.patch_bytes = (uint32_t)p.halo_patch_bytes;
             tp.plane_bytes = (uint32_t)(p.halo_patch_bytes / p.halo_planes);
             CU_TRY(launch_tc_conv_halo(tf32, op->tmA, op->tmB, op->tmC, tp, p.grid_x, p.smem, st), "conv_halo launch");

@@ -28,7 +28,7 @@
 
 namespace xtc {
 
-template <bool TF32, int MSUB>
+template <bool TF32, int MSUB, int CL>
 __global__ void __launch_bounds__(kTcThreads, 1)
 tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmY, const TcParams p) {
@@ -55,6 +55,11 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    // CL = 2: a cluster of two CTAs on M tiles 2j, 2j+1 (same N tile) shares the filter ring:
+    // each fetches half of every stage and TMA-multicasts it to both
+    const uint32_t rank = (CL == 2) ? ptx::cluster_ctarank() : 0u;
+    const int64_t cluster_id = blockIdx.x / CL;
+    const int64_t num_clusters = gridDim.x / CL;
     // XTC_TRACE (diagnostics): slot 0 entry, 1 setup done, 2 exit; 8+j patch j issued,
     // 8+kTraceK+j patch j seen by the MMA warp, 8+2kTraceK+2j(+1) epilogue of tile j start/end
     uint64_t* const trace = (p.trace && blockIdx.x < kTraceCtas) ? p.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
@@ -65,7 +70,8 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
         if (p.buffer_c) ptx::prefetch_tmap(&tmY);
     }
     if (warp == 1 && lane == 0) {
-        for (int s = 0; s < S; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
+        // a multicast stage is free only when the MMAs of every CTA in the cluster have read it
+        for (int s = 0; s < S; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], CL); }
         for (int i = 0; i < kHaloMaxPatchBufs; ++i) {
             ptx::mbar_init(&pfull[i], 1);
             ptx::mbar_init(&pempty[i], 1);
@@ -82,7 +88,7 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
         ptx::tmem_relinquish<1>();
     }
     ptx::tc_fence_before();
-    __syncthreads();
+    if constexpr (CL == 2) ptx::cluster_sync(); else __syncthreads();   // peers' barriers exist before multicasts
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const int acc_cols = MSUB * p.tile_n;        // TMEM columns of one accumulator buffer
@@ -93,6 +99,7 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
     auto decode = [&](int64_t t, int& nimg, int& p0, int& n0) {
         int mb, nb, ks;
         tile_coords(p.tm, t, mb, nb, ks);
+        mb = mb * CL + (int)rank;                    // CL = 2: the loop runs over M-tile pairs
         nimg = mb / p.tpi;
         p0 = (mb - nimg * p.tpi) * p.rt * MSUB;
         n0 = nb * p.tile_n;
@@ -111,7 +118,7 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
         int pb = 0;
         uint32_t use_par = 0;
         bool first_round = true;
-        for (int64_t t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters) {
             int nimg, p0, n0;
             decode(t, nimg, p0, n0);
             const int cb = pb;
@@ -152,7 +159,7 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
             int s = 0;
             uint32_t use_par = 0;
             bool first_round = true;
-            for (int64_t t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+            for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters) {
                 int nimg, p0, n0;
                 decode(t, nimg, p0, n0);
                 for (int kb = 0; kb < p.kb_total; ++kb) {
@@ -162,8 +169,16 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
                     if (++s == S) { s = 0; use_par ^= 1u; first_round = false; }
                     if (!fresh) ptx::mbar_wait(&empty[cs], cpar ^ 1u);
                     if (ptx::elect_one()) {
-                        ptx::mbar_arrive_expect_tx(&full[cs], p.b_stage_bytes);
-                        load_b(sB + (size_t)cs * p.b_stage_bytes, &full[cs], kb, n0);
+                        ptx::mbar_arrive_expect_tx(&full[cs], p.b_stage_bytes);   // both halves land here
+                        if constexpr (CL == 2) {
+                            // my half of the stage's 128-byte N blocks, written into both CTAs
+                            const int half = p.tile_n / ATOM / 2;
+                            ptx::tma_load_3d_multicast(&tmB, sB + (size_t)cs * p.b_stage_bytes +
+                                                                 (size_t)rank * half * p.tile_k * 128,
+                                                       &full[cs], 0, kb * p.tile_k, n0 / ATOM + (int)rank * half, 0x3);
+                        } else {
+                            load_b(sB + (size_t)cs * p.b_stage_bytes, &full[cs], kb, n0);
+                        }
                     }
                     __syncwarp();
                 }
@@ -203,7 +218,7 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
         const int nbuf = p.nbuf, accb = p.acc_buffers;
         if (b_res)                                    // the resident filter (per-k-block barriers)
             for (int kb = 0; kb < p.kb_total; ++kb) ptx::mbar_wait(&bfull[kb], 0);
-        for (int64_t t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters) {
             if (wait_tempty) ptx::mbar_wait(&tempty[acc], aph ^ 1u);
             ptx::mbar_wait(&pfull[pb], pph);
             if (trace && lane == 0 && tj < kTraceK) trace[8 + kTraceK + tj] = ptx::globaltimer();
@@ -247,7 +262,8 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
                         ptx::tc_fence_after();
                         const uint64_t bd = bdesc0 + (uint64_t)((uint32_t)s1 * b_stage16);
                         for (int a = 0; a < n_atoms; ++a) atom(bd + (uint64_t)(a * ATOM * 8));
-                        ptx::umma_commit<1>(&empty[s1]);
+                        if constexpr (CL == 2) ptx::umma_commit_multicast(&empty[s1], 0x3);
+                        else ptx::umma_commit<1>(&empty[s1]);
                         if (++s1 == Sring) { s1 = 0; ph1 ^= 1u; }
                     }
                 }
@@ -275,7 +291,7 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
         uint8_t* stage = sC + q * (kTcEpiStageBytes * kTcEpiBuffers);
         const bool bf16_out = p.out_bf16 != 0;
         const int P = p.cg.P, Q = p.cg.Q;
-        for (int64_t t = blockIdx.x; t < ((p.debug_skip_mma & 64) ? 0 : p.num_tiles); t += gridDim.x) {
+        for (int64_t t = cluster_id; t < ((p.debug_skip_mma & 64) ? 0 : p.num_tiles); t += num_clusters) {
             int nimg, p0, n0;
             decode(t, nimg, p0, n0);
             if (p.debug_skip_mma & 128) ptx::mbar_wait_sleep(&tfull[acc], aph);
@@ -383,7 +399,7 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
     }
 
     ptx::tc_fence_before();
-    __syncthreads();
+    if constexpr (CL == 2) ptx::cluster_sync(); else __syncthreads();   // no CTA exits while a peer may still signal it
     if (trace && threadIdx.x == 0) trace[2] = ptx::globaltimer();
     if (warp == 2) {
         ptx::tc_fence_after();
@@ -391,14 +407,38 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
     }
 }
 
-template <bool TF32, int MSUB>
+template <bool TF32, int MSUB, int CL>
 static cudaError_t launch_halo_t(const CUtensorMap& x, const CUtensorMap& b, const CUtensorMap& y, const TcParams& p,
                                  int grid, int smem, cudaStream_t st) {
-    auto k = tc_conv_halo_kernel<TF32, MSUB>;
+    auto k = tc_conv_halo_kernel<TF32, MSUB, CL>;
     cudaError_t e = ensure_smem_attr(k, smem);
     if (e != cudaSuccess) return e;
-    k<<<grid, kTcThreads, smem, st>>>(x, b, y, p);
+    if constexpr (CL == 1) {
+        k<<<grid, kTcThreads, smem, st>>>(x, b, y, p);
+    } else {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(kTcThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = CL;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, k, x, b, y, p);
+        if (e != cudaSuccess) return e;
+    }
     return cudaGetLastError();
+}
+
+template <bool TF32, int MSUB>
+static cudaError_t launch_halo_cl(const CUtensorMap& x, const CUtensorMap& b, const CUtensorMap& y, const TcParams& p,
+                                  int grid, int smem, cudaStream_t st) {
+    return p.cl == 2 ? launch_halo_t<TF32, MSUB, 2>(x, b, y, p, grid, smem, st)
+                     : launch_halo_t<TF32, MSUB, 1>(x, b, y, p, grid, smem, st);
 }
 
 cudaError_t launch_tc_conv_halo(bool tf32, const CUtensorMap& x, const CUtensorMap& b, const CUtensorMap& y,
@@ -406,8 +446,8 @@ cudaError_t launch_tc_conv_halo(bool tf32, const CUtensorMap& x, const CUtensorM
     // MSUB (128-row UMMA tiles per patch) is a template parameter: the per-atom UMMA
     // sequence is straight-line code
     if (p.msub == 2)
-        return tf32 ? launch_halo_t<true, 2>(x, b, y, p, grid, smem, st) : launch_halo_t<false, 2>(x, b, y, p, grid, smem, st);
-    return tf32 ? launch_halo_t<true, 1>(x, b, y, p, grid, smem, st) : launch_halo_t<false, 1>(x, b, y, p, grid, smem, st);
+        return tf32 ? launch_halo_cl<true, 2>(x, b, y, p, grid, smem, st) : launch_halo_cl<false, 2>(x, b, y, p, grid, smem, st);
+    return tf32 ? launch_halo_cl<true, 1>(x, b, y, p, grid, smem, st) : launch_halo_cl<false, 1>(x, b, y, p, grid, smem, st);
 }
 
 }  // namespace xtc

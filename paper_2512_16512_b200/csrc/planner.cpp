@@ -125,7 +125,10 @@ static xtc_status plan_tc_halo(const xtc_op_desc& d, const xtc_schedule& s, int 
     if (d.kind != XTC_OP_CONV2D) ILLEGAL("pack_halo applies to conv2d only");
     if (s.pack_halo != 1) ILLEGAL("pack_halo must be 0 or 1");
     if (d.stride_h != 1 || d.stride_w != 1) ILLEGAL("pack_halo needs stride 1 (taps must be row shifts of one patch)");
-    if (s.cluster_m > 1) ILLEGAL("pack_halo: cluster_m must be 1");
+    // cluster_m = 2: two CTAs on adjacent M tiles (same N tile) each fetch half of every filter
+    // stage and TMA-multicast it to both (the filter stream per SM is halved)
+    const int hcl = s.cluster_m == 0 ? 1 : s.cluster_m;
+    if (hcl != 1 && hcl != 2) ILLEGAL("pack_halo: cluster_m must be 1 or 2 (filter multicast pair)");
     if (p.split_k != 1) ILLEGAL("pack_halo: split_k must be 1");
     if (s.pack_warps > 1) ILLEGAL("pack_halo: pack_warps must be 0 or 1 (warp 0 packs patches, warp 3 the B ring)");
     if (s.tile_m != 128 && s.tile_m != 256) ILLEGAL("pack_halo: tile_m must be 128 or 256 (1 or 2 UMMA M-tiles per patch)");
@@ -193,14 +196,23 @@ static xtc_status plan_tc_halo(const xtc_op_desc& d, const xtc_schedule& s, int 
     p.halo_patch_bytes = patch;
     p.halo_tpi = (int)cdiv(P, (int64_t)rt * msub);
     p.tiles_m = (int)(d.batch * p.halo_tpi);
+    if (hcl == 2) {
+        if (s.b_resident) ILLEGAL("pack_halo: cluster_m 2 multicasts the filter ring; b_resident must be 0");
+        if ((s.tile_n / p.atom_n) % 2) ILLEGAL("pack_halo: cluster_m 2 needs an even number of 128-byte filter blocks (tile_n)");
+        if (p.tiles_m % 2) ILLEGAL("pack_halo: cluster_m 2 needs an even number of M tiles (%d)", p.tiles_m);
+        if (d.f % p.atom_n) ILLEGAL("pack_halo: cluster_m 2 needs F %% %d == 0 (3-D filter TMA)", p.atom_n);
+        p.tiles_m /= 2;                                 // the tile loop runs over M-tile pairs
+    }
+    p.halo_cl = hcl;
     p.kb_per_split = p.kb_total;
     p.k_per_split = (int64_t)p.kb_per_split * s.tile_k;
     p.num_tiles = (int64_t)p.tiles_m * p.tiles_n;
     if (p.num_tiles >= (1ll << 31)) ILLEGAL("too many tiles");
     p.cta_group = 1;
     p.block = kTcThreads;
-    p.cluster = 1;
-    p.grid_x = s.persistent ? (int)std::min<int64_t>(p.num_tiles, num_sms) : (int)p.num_tiles;
+    p.cluster = hcl;
+    const int64_t ctas = p.num_tiles * hcl;
+    p.grid_x = s.persistent ? (int)std::min<int64_t>(ctas, num_sms - num_sms % hcl) : (int)ctas;
     return XTC_OK;
 }
 

@@ -268,6 +268,26 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
                      ::"r"(smem_u32(bar)), "h"((uint16_t)0x3) : "memory");
 }
 
+// cta_group::1 MMAs whose completion must be seen by every CTA in `mask` (the barrier at the
+// same offset in each): a stage multicast into several CTAs is free only when all of them
+// have consumed it.
+__device__ __forceinline__ void umma_commit_multicast(uint64_t* bar, uint16_t mask) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                 ::"r"(smem_u32(bar)), "h"(mask) : "memory");
+}
+
+// 3-D tiled TMA load written to the same SMEM offset (and completing the same-offset
+// mbarrier) in every CTA of `mask`.
+__device__ __forceinline__ void tma_load_3d_multicast(const CUtensorMap* m, void* dst, uint64_t* bar, int32_t c0,
+                                                      int32_t c1, int32_t c2, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%3, %4, %5}], [%2], %6;"
+        ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2),
+          "h"(mask)
+        : "memory");
+}
+
 // 32 lanes x 32 columns of 32-bit accumulator -> 32 registers per thread.
 __device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&v)[32]) {
     asm volatile(

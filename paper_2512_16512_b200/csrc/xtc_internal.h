@@ -104,6 +104,7 @@ struct Plan {
     // 128-byte channel planes, nbuf patch buffers, tpi tiles per image
     bool halo = false;
     int32_t halo_wp = 0, halo_rt = 0, halo_msub = 0, halo_pr = 0, halo_planes = 0, halo_nbuf = 0, halo_tpi = 0;
+    int32_t halo_cl = 1;                // CTAs per cluster sharing the filter stream (TMA multicast)
     int64_t halo_patch_bytes = 0;
 };
 
@@ -154,7 +155,7 @@ struct TcParams {
     uint32_t lo_off;         // 3xTF32: byte offset from a hi stage (A or B ring) to its lo copy
     ConvGeom cg;
     // pack_halo conv only (see Plan)
-    int32_t wp, rt, msub, planes, nbuf, tpi;
+    int32_t wp, rt, msub, planes, nbuf, tpi, cl;
     uint32_t patch_bytes, plane_bytes;
     // Diagnostics (XTC_TRACE): %globaltimer stamps for CTAs < kTraceCtas, laid out
     // [cta][kTraceSlots]: slot 0 kernel entry, 1 setup done; producer issue of k-block i at

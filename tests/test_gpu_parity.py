@@ -192,6 +192,9 @@ HALO_CASES = [
     ((1, 10, 10, 64, 64, 3, 3, 0, "bf16", "f32"), dict(tile_n=64, stages=2, buffer_c=0)),                  # 16  pad 0
     ((1, 3, 100, 64, 64, 3, 3, 1, "bf16", "bf16"), dict(tile_n=64, stages=2)),                             # 128 1
     ((2, 14, 14, 64, 64, 3, 3, 1, "tf32", "f32"), dict(tile_n=64, tile_k=32, stages=4)),                   # tf32: 2 planes
+    # cluster_m 2: the filter stream shared by two CTAs through TMA multicast
+    ((3, 14, 14, 256, 256, 3, 3, 1, "bf16", "bf16"), dict(cluster_m=2, tile_n=128, tile_k=128, stages=3)),
+    ((2, 28, 28, 64, 256, 3, 3, 1, "bf16", "f32"), dict(cluster_m=2, tile_n=256, stages=3, persistent=0, buffer_c=0)),
 ]
 
 

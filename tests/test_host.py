@@ -167,7 +167,10 @@ def test_pack_halo_plan():
 @pytest.mark.parametrize("desc,kw,frag", [
     (xtc.conv2d_desc(2, 15, 17, 64, 128, 3, 3, 2, 1), {}, "stride 1"),
     (xtc.matmul_desc(256, 256, 256), {}, "conv2d only"),
-    (xtc.conv2d_desc(2, 56, 56, 64, 64), dict(cluster_m=2, tile_m=256), "cluster_m"),
+    (xtc.conv2d_desc(2, 56, 56, 64, 64), dict(cluster_m=4), "cluster_m"),
+    (xtc.conv2d_desc(2, 56, 56, 64, 64), dict(cluster_m=2, b_resident=1), "b_resident"),
+    (xtc.conv2d_desc(2, 56, 56, 64, 64), dict(cluster_m=2), "even number of 128-byte filter blocks"),
+    (xtc.conv2d_desc(1, 14, 14, 256, 256), dict(cluster_m=2, tile_n=128, tile_m=256), "even number of M tiles"),
     (xtc.conv2d_desc(2, 56, 56, 64, 64), dict(split_k=3), "split_k"),
     (xtc.conv2d_desc(2, 56, 56, 64, 64), dict(pack_warps=2), "pack_warps"),
     (xtc.conv2d_desc(1, 4, 200, 64, 64), {}, "slots"),
