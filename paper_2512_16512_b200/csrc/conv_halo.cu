@@ -96,8 +96,8 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
     int tj = 0;                                  // per-role tile counter for the trace
 
     // tile id -> (image, first output row, first output channel)
-    auto decode = [&](int64_t t, int& nimg, int& p0, int& n0) {
-        int mb, nb, ks;
+    auto decode = [&](int64_t t, int& nimg, int& p0, int& n0, int& ks) {
+        int mb, nb;
         tile_coords(p.tm, t, mb, nb, ks);
         mb = mb * CL + (int)rank;                    // CL = 2: the loop runs over M-tile pairs
         nimg = mb / p.tpi;
@@ -120,7 +120,8 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
         bool first_round = true;
         for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters) {
             int nimg, p0, n0;
-            decode(t, nimg, p0, n0);
+            int ks;
+            decode(t, nimg, p0, n0, ks);
             const int cb = pb;
             const uint32_t cpar = use_par;
             const bool fresh = first_round;
@@ -161,8 +162,10 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
             bool first_round = true;
             for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters) {
                 int nimg, p0, n0;
-                decode(t, nimg, p0, n0);
-                for (int kb = 0; kb < p.kb_total; ++kb) {
+                int ks;
+                decode(t, nimg, p0, n0, ks);
+                const int kb0 = ks * p.kb_per_split, kb1 = min(p.kb_total, kb0 + p.kb_per_split);
+                for (int kb = kb0; kb < kb1; ++kb) {
                     const int cs = s;
                     const uint32_t cpar = use_par;
                     const bool fresh = first_round;
@@ -224,13 +227,21 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
             if (trace && lane == 0 && tj < kTraceK) trace[8 + kTraceK + tj] = ptx::globaltimer();
             ++tj;
             ptx::tc_fence_after();
+            int kb0, kb1;                             // this tile's K segment (split_k)
+            {
+                int mb_, nb_, ks_;
+                tile_coords(p.tm, t, mb_, nb_, ks_);
+                kb0 = ks_ * p.kb_per_split;
+                kb1 = min(kb_total, kb0 + p.kb_per_split);
+            }
             if (ptx::elect_one()) {
                 const uint32_t d0 = tmem_base + (uint32_t)(acc * acc_cols);
                 const uint64_t apatch = adesc0 + (uint64_t)((uint32_t)pb * patch16);
                 // the next 128-byte atom: channel plane pl, filter column sx, A offset aoff
-                // (16-byte units) = pl*plane16 + (r*Wp + sx)*8
-                int sx = 0, pl = 0;
-                uint32_t aoff = 0;
+                // (16-byte units) = pl*plane16 + (r*Wp + sx)*8, starting at the segment's first atom
+                const int j0 = kb0 * n_atoms, tap0 = j0 / planes;
+                int pl = j0 - tap0 * planes, sx = tap0 % R_S;
+                uint32_t aoff = (uint32_t)pl * plane16 + (uint32_t)((tap0 / R_S) * p.wp + sx) * 8u;
                 uint32_t accf = 0;                    // 0 for the tile's first UMMA (overwrite)
                 auto atom = [&](uint64_t bd) {
                     const uint64_t ad = apatch + (uint64_t)aoff;
@@ -250,14 +261,14 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
                 };
                 if (b_res) {
                     // resident filter: k-block kb of B at kb * b_stage16, atom a at a*ATOM rows
-                    for (int kb = 0; kb < kb_total; ++kb) {
+                    for (int kb = kb0; kb < kb1; ++kb) {
                         const uint64_t bd = bdesc0 + (uint64_t)((uint32_t)kb * b_stage16);
                         for (int a = 0; a < n_atoms; ++a) atom(bd + (uint64_t)(a * ATOM * 8));
                     }
                 } else {
                     int s1 = s;
                     uint32_t ph1 = ph;
-                    for (int kb = 0; kb < kb_total; ++kb) {
+                    for (int kb = kb0; kb < kb1; ++kb) {
                         ptx::mbar_wait(&full[s1], ph1);
                         ptx::tc_fence_after();
                         const uint64_t bd = bdesc0 + (uint64_t)((uint32_t)s1 * b_stage16);
@@ -276,8 +287,8 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
                 }
             }
             __syncwarp();
-            if (!b_res)                               // every lane advances the ring by kb_total slots
-                for (int kb = 0; kb < kb_total; ++kb)
+            if (!b_res)                               // every lane advances the ring by the segment's slots
+                for (int kb = kb0; kb < kb1; ++kb)
                     if (++s == S) { s = 0; ph ^= 1u; }
             (void)nbuf; (void)accb;
             if (++pb == p.nbuf) { pb = 0; pph ^= 1u; }
@@ -293,7 +304,8 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
         const int P = p.cg.P, Q = p.cg.Q;
         for (int64_t t = cluster_id; t < ((p.debug_skip_mma & 64) ? 0 : p.num_tiles); t += num_clusters) {
             int nimg, p0, n0;
-            decode(t, nimg, p0, n0);
+            int ks;
+            decode(t, nimg, p0, n0, ks);
             if (p.debug_skip_mma & 128) ptx::mbar_wait_sleep(&tfull[acc], aph);
             else ptx::mbar_wait(&tfull[acc], aph);
             if (trace && warp == 4 && lane == 0 && tj < kTraceTiles) trace[8 + 2 * kTraceK + 2 * tj] = ptx::globaltimer();
@@ -358,7 +370,10 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
                         const int64_t m = ((int64_t)nimg * P + prow) * Q + qcol;
                         const int64_t col0 = (int64_t)n0 + c;
                         const int ncols = (int)((p.N - col0) < 32 ? (p.N - col0) : 32);
-                        if (bf16_out) {
+                        if (p.split_out) {                  // split_k: this segment's fp32 partial sums
+                            float* dst = p.Wk + ((int64_t)ks * p.M + m) * p.ws_ld + col0;
+                            for (int j = 0; j < ncols; ++j) dst[j] = __uint_as_float(vals[j]);
+                        } else if (bf16_out) {
                             uint16_t* dst = reinterpret_cast<uint16_t*>(p.C) + m * p.ldc + col0;
                             if (ncols == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
 #pragma unroll

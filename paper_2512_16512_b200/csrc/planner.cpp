@@ -129,7 +129,10 @@ static xtc_status plan_tc_halo(const xtc_op_desc& d, const xtc_schedule& s, int 
     // stage and TMA-multicast it to both (the filter stream per SM is halved)
     const int hcl = s.cluster_m == 0 ? 1 : s.cluster_m;
     if (hcl != 1 && hcl != 2) ILLEGAL("pack_halo: cluster_m must be 1 or 2 (filter multicast pair)");
-    if (p.split_k != 1) ILLEGAL("pack_halo: split_k must be 1");
+    // split: K segments (runs of filter taps / channel planes) as their own CTAs; fp32 partials
+    // written by direct stores, summed in ascending segment order by the reduction kernel
+    if (p.split_k > 1 && p.atomic) ILLEGAL("pack_halo: split_k needs the ordered reduction (split_k_mode 0)");
+    if (p.split_k > 1 && s.buffer_c) ILLEGAL("pack_halo: split_k writes fp32 partials with direct stores (buffer_c 0)");
     if (s.pack_warps > 1) ILLEGAL("pack_halo: pack_warps must be 0 or 1 (warp 0 packs patches, warp 3 the B ring)");
     if (s.tile_m != 128 && s.tile_m != 256) ILLEGAL("pack_halo: tile_m must be 128 or 256 (1 or 2 UMMA M-tiles per patch)");
     if (s.inner_m != 0 && s.inner_m != 128) ILLEGAL("pack_halo: inner_m (UMMA M) must be 128");
@@ -204,9 +207,11 @@ static xtc_status plan_tc_halo(const xtc_op_desc& d, const xtc_schedule& s, int 
         p.tiles_m /= 2;                                 // the tile loop runs over M-tile pairs
     }
     p.halo_cl = hcl;
-    p.kb_per_split = p.kb_total;
+    p.kb_per_split = (int)cdiv(p.kb_total, p.split_k);
+    if ((int64_t)(p.split_k - 1) * p.kb_per_split >= p.kb_total)
+        ILLEGAL("split: split_k %d leaves an empty K segment (%d k-blocks of %d)", p.split_k, p.kb_total, s.tile_k);
     p.k_per_split = (int64_t)p.kb_per_split * s.tile_k;
-    p.num_tiles = (int64_t)p.tiles_m * p.tiles_n;
+    p.num_tiles = (int64_t)p.tiles_m * p.tiles_n * p.split_k;
     if (p.num_tiles >= (1ll << 31)) ILLEGAL("too many tiles");
     p.cta_group = 1;
     p.block = kTcThreads;

@@ -195,6 +195,10 @@ HALO_CASES = [
     # cluster_m 2: the filter stream shared by two CTAs through TMA multicast
     ((3, 14, 14, 256, 256, 3, 3, 1, "bf16", "bf16"), dict(cluster_m=2, tile_n=128, tile_k=128, stages=3)),
     ((2, 28, 28, 64, 256, 3, 3, 1, "bf16", "f32"), dict(cluster_m=2, tile_n=256, stages=3, persistent=0, buffer_c=0)),
+    # split_k: K segments (runs of taps / channel planes) as CTAs, ordered reduction
+    ((1, 14, 14, 256, 256, 3, 3, 1, "bf16", "bf16"), dict(tile_n=128, stages=4, split_k=3, buffer_c=0)),
+    ((1, 14, 14, 256, 256, 3, 3, 1, "bf16", "bf16"), dict(tile_n=128, stages=4, split_k=9, buffer_c=0)),
+    ((1, 56, 56, 64, 64, 3, 3, 1, "bf16", "f32"), dict(tile_n=64, stages=2, split_k=3, buffer_c=0, b_resident=1)),
 ]
 
 
@@ -622,6 +626,12 @@ def test_consumer_conv_simt_and_unfused(cons):
     if "accumulate" not in cons:                                                              # unfused: its own pass
         run_consumer(xtc.matmul_desc(256, 384, 320, "bf16", "bf16"), tc(tile_n=128, fuse=0), cons, "bf16", "bf16",
                      MODE_INT)
+
+
+def test_consumer_halo_split_k_in_the_reduction():
+    run_consumer(xtc.conv2d_desc(1, 14, 14, 256, 256, 3, 3, 1, 1, "bf16", "bf16"),
+                 tc(pack_halo=1, tile_n=128, stages=4, split_k=4, buffer_c=0, fuse=1), "bias+relu", "bf16", "bf16",
+                 MODE_INT)
 
 
 def test_consumer_bias_pointer_required_and_sweep_with_accumulate():

@@ -171,7 +171,8 @@ def test_pack_halo_plan():
     (xtc.conv2d_desc(2, 56, 56, 64, 64), dict(cluster_m=2, b_resident=1), "b_resident"),
     (xtc.conv2d_desc(2, 56, 56, 64, 64), dict(cluster_m=2), "even number of 128-byte filter blocks"),
     (xtc.conv2d_desc(1, 14, 14, 256, 256), dict(cluster_m=2, tile_n=128, tile_m=256), "even number of M tiles"),
-    (xtc.conv2d_desc(2, 56, 56, 64, 64), dict(split_k=3), "split_k"),
+    (xtc.conv2d_desc(2, 56, 56, 64, 64), dict(split_k=3), "buffer_c 0"),
+    (xtc.conv2d_desc(2, 56, 56, 64, 64), dict(split_k=10, buffer_c=0), "empty K segment"),
     (xtc.conv2d_desc(2, 56, 56, 64, 64), dict(pack_warps=2), "pack_warps"),
     (xtc.conv2d_desc(1, 4, 200, 64, 64), {}, "slots"),
     (xtc.conv2d_desc(2, 56, 56, 64, 64), dict(tile_m=384), "tile_m"),
