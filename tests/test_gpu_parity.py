@@ -375,7 +375,10 @@ def test_measure_named_counters():
     compulsory = 2 * n * n * 2                       # A + B in bf16
     assert compulsory <= v["gpu.dram__bytes_read.sum"] <= 8 * compulsory
     assert 0 <= v["dram__bytes_write.sum"] <= 4 * n * n * 2
-    assert 0.5 * m.t_min_ns <= v["gpu__time_duration.sum"] <= 3.0 * m.t_max_ns
+    # the user range is pushed/popped on the host around the call, so its duration also
+    # holds the launch's submission latency (tens of us under CUPTI's replay): the upper
+    # bound allows that, the lower bound pins that the kernel itself is inside the range
+    assert 0.5 * m.t_min_ns <= v["gpu__time_duration.sum"] <= 3.0 * m.t_max_ns + 200e3
 
 
 def test_measure_unknown_counter_is_unavailable_not_failure():
