@@ -247,6 +247,38 @@ def sharded_conv(xtc, torch, dist, dev, world, rank, peak_tf, steps=10):
 
 
 # ---------------------------------------------------------------- xtc arm --
+def cublas_same_protocol(torch, stream, a, b, c, op, sp, steps, flops, rounds=3):
+    """Context only (library code, not the product): cuBLAS (torch.matmul) on the same
+    8192^3 bf16 operands under the headline's protocol -- `steps` back-to-back launches
+    between two events -- interleaved block by block with the XTC kernel so that both see
+    the same power-capped clock.  MEASURED_PEAKS' bf16 figure is a best-of-10 burst."""
+    c_ref = torch.empty_like(c)
+
+    def block(fn):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / steps
+
+    ours = lambda: op.run(a, b, c, stream=sp)
+    lib = lambda: torch.matmul(a, b, out=c_ref)
+    lib()
+    torch.cuda.synchronize()
+    t_x, t_l = [], []
+    for _ in range(rounds):
+        t_l.append(block(lib))
+        t_x.append(block(ours))
+    same = bool(torch.equal(c, c_ref))
+    mx, ml = sorted(t_x)[len(t_x) // 2], sorted(t_l)[len(t_l) // 2]
+    return {"xtc_tflops": flops / (mx * 1e-3) / 1e12, "cublas_tflops": flops / (ml * 1e-3) / 1e12,
+            "xtc_over_cublas": ml / mx, "ms_per_step": {"xtc": t_x, "cublas": t_l},
+            "outputs_bitwise_equal": same,
+            "protocol": f"{rounds} interleaved blocks of {steps} back-to-back launches each (cuBLAS block first)"}
+
+
 def main_xtc(args):
     import torch
     import torch.distributed as dist
@@ -462,6 +494,7 @@ def main_xtc(args):
                                                           peak_tf)
         extras["conv_L56_batch_sharded"] = sharded_conv(xtc, torch, dist, dev, world, rank, peak_tf)
     if rank == 0 and world == 1 and not args.no_extras:
+        extras["cublas_same_protocol"] = cublas_same_protocol(torch, stream, a, b, c, op, sp, args.steps, flops)
         try:
             from paper_2512_16512_b200.bench_extras import run_extras
             extras.update(run_extras(xtc, torch, dev, peak_tf))

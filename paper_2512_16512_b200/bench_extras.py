@@ -27,7 +27,9 @@ CONV_SCHEDS = {
             dict(HALO, tile_m=256, tile_n=64, stages=2, b_resident=1),
             dict(TC, tile_n=64, stages=8, buffer_c=1, acc_buffers=2, persistent=1, raster_group=8, pack_warps=3),
             dict(TC, tile_n=64, stages=7, buffer_c=1, acc_buffers=2, persistent=1, pack_warps=3, b_resident=1)],
-    "L14": [dict(HALO, tile_n=128, tile_k=128, stages=3),
+    "L14": [dict(HALO, tile_m=256, cluster_m=2, inner_m=256, tile_n=128, tile_k=128, stages=3),
+            dict(HALO, tile_m=256, cluster_m=2, inner_m=256, tile_n=256, tile_k=128, stages=3),
+            dict(HALO, tile_n=128, tile_k=128, stages=3),
             dict(HALO, tile_n=128, stages=4),
             dict(PAIR, tile_n=256, tile_k=128, stages=3, buffer_c=1, acc_buffers=2, persistent=1, pack_warps=2),
             dict(TC, tile_n=256, stages=4, buffer_c=1, acc_buffers=2, persistent=1, pack_warps=2),

@@ -600,6 +600,7 @@ static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cud
         tp.a3d = op->a3d;
         tp.debug_skip_mma = getenv("XTC_DEBUG_SKIP_MMA") != nullptr;   // diagnostics: output invalid
         if (const char* sk = getenv("XTC_DEBUG_SKIP")) tp.debug_skip_mma = atoi(sk);   // bitmask, see TcParams
+        tp.debug_late_alloc = getenv("XTC_DEBUG_LATE_ALLOC") != nullptr && atoi(getenv("XTC_DEBUG_LATE_ALLOC")) != 0;
         tp.b3d = op->b3d;
         tp.buffer_c = p.sch.buffer_c;
         tp.atomic = p.atomic;
@@ -633,6 +634,7 @@ static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cud
             tp.nbuf = p.halo_nbuf;
             tp.tpi = p.halo_tpi;
             tp.cl = p.halo_cl;
+            tp.pair = p.halo_pair ? 1 : 0;
             tp.patch_bytes = (uint32_t)p.halo_patch_bytes;
             tp.plane_bytes = (uint32_t)(p.halo_patch_bytes / p.halo_planes);
             CU_TRY(launch_tc_conv_halo(tf32, op->tmA, op->tmB, op->tmC, tp, p.grid_x, p.smem, st), "conv_halo launch");

@@ -28,7 +28,7 @@
 
 namespace xtc {
 
-template <bool TF32, int MSUB, int CL>
+template <bool TF32, int MSUB, int CL, bool PAIR = false>
 __global__ void __launch_bounds__(kTcThreads, 1)
 tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmY, const TcParams p) {
@@ -56,7 +56,14 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     // CL = 2: a cluster of two CTAs on M tiles 2j, 2j+1 (same N tile) shares the filter ring:
-    // each fetches half of every stage and TMA-multicasts it to both
+    // each fetches half of every stage and TMA-multicasts it to both.
+    // PAIR (CL = 2, inner_m 256): the same two CTAs form a cta_group::2 pair.  Each packs its
+    // own patch and half of the filter columns, all completing on the leader's barriers; the
+    // leader (rank 0) issues M = 256 UMMAs (A rows from both patches, B columns from both
+    // filter halves, at identical SMEM offsets) whose commits are multicast to both CTAs, and
+    // both epilogues drain their own TMEM, then arrive on the leader's tempty.
+    static_assert(!PAIR || (CL == 2 && MSUB == 1), "the CTA pair is a 2-CTA cluster, one UMMA tile per CTA");
+    constexpr int CG = PAIR ? 2 : 1;
     const uint32_t rank = (CL == 2) ? ptx::cluster_ctarank() : 0u;
     const int64_t cluster_id = blockIdx.x / CL;
     const int64_t num_clusters = gridDim.x / CL;
@@ -71,26 +78,40 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
     }
     if (warp == 1 && lane == 0) {
         // a multicast stage is free only when the MMAs of every CTA in the cluster have read it
-        for (int s = 0; s < S; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], CL); }
+        for (int s = 0; s < S; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], PAIR ? 1 : CL); }
         for (int i = 0; i < kHaloMaxPatchBufs; ++i) {
             ptx::mbar_init(&pfull[i], 1);
             ptx::mbar_init(&pempty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(&tfull[i], 1);
-            ptx::mbar_init(&tempty[i], 4);
+            ptx::mbar_init(&tempty[i], 4 * CG);
         }
         for (int i = 0; i < kHaloMaxResidentKb; ++i) ptx::mbar_init(&bfull[i], 1);
         ptx::fence_mbarrier_init();
     }
-    if (warp == 2) {
-        ptx::tmem_alloc<1>(tmem_slot, p.tmem_cols);
-        ptx::tmem_relinquish<1>();
+    // barriers first (peers' barriers exist before multicasts); the TMEM allocation is then
+    // taken by warp 2 while warps 0 and 3 already issue the patch and filter loads, and only
+    // the TMEM users (warps 1, 4..7) wait for it on the named barrier kTmemBar
+    if (warp == 2 && p.debug_late_alloc) {
+        ptx::tmem_alloc<CG>(tmem_slot, p.tmem_cols);
+        ptx::tmem_relinquish<CG>();
+        ptx::tc_fence_before();
     }
-    ptx::tc_fence_before();
-    if constexpr (CL == 2) ptx::cluster_sync(); else __syncthreads();   // peers' barriers exist before multicasts
-    ptx::tc_fence_after();
-    const uint32_t tmem_base = *tmem_slot;
+    if constexpr (CL == 2) ptx::cluster_sync(); else __syncthreads();
+    if (warp == 2 && p.debug_late_alloc) {
+        ptx::named_bar_arrive(ptx::kTmemBar, ptx::kTmemBarThreads);
+    } else if (warp == 2) {
+        ptx::tmem_alloc<CG>(tmem_slot, p.tmem_cols);
+        ptx::tmem_relinquish<CG>();
+        ptx::tc_fence_before();
+        ptx::named_bar_arrive(ptx::kTmemBar, ptx::kTmemBarThreads);
+    }
+    auto tmem_address = [&]() -> uint32_t {
+        ptx::named_bar_sync(ptx::kTmemBar, ptx::kTmemBarThreads);
+        ptx::tc_fence_after();
+        return *reinterpret_cast<volatile uint32_t*>(tmem_slot);
+    };
     const int acc_cols = MSUB * p.tile_n;        // TMEM columns of one accumulator buffer
     if (trace && threadIdx.x == 0) trace[1] = ptx::globaltimer();
     int tj = 0;                                  // per-role tile counter for the trace
@@ -110,6 +131,16 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
         } else {
             for (int b = 0; b < p.tile_n / ATOM; ++b)
                 ptx::tma_load_2d(&tmB, dst + (size_t)b * p.tile_k * 128, bar, n0 + b * ATOM, kb * p.tile_k);
+        }
+    };
+    // PAIR: this CTA's half of the filter columns (128-byte blocks nblk0 ...), completing on the
+    // leader's barrier bar_c
+    auto load_b_pair = [&](uint8_t* dst, uint32_t bar_c, int kb, int nblk0) {
+        if (p.b3d) {
+            ptx::tma_load_3d_pair(&tmB, dst, bar_c, 0, kb * p.tile_k, nblk0);
+        } else {
+            for (int b = 0; b < p.tile_n / ATOM / 2; ++b)
+                ptx::tma_load_2d_pair(&tmB, dst + (size_t)b * p.tile_k * 128, bar_c, (nblk0 + b) * ATOM, kb * p.tile_k);
         }
     };
 
@@ -135,13 +166,21 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
             if (p.debug_skip_mma & 2) {
                 if (ptx::elect_one()) ptx::mbar_arrive(&pfull[cb]);
             } else if (ptx::elect_one()) {
-                ptx::mbar_arrive_expect_tx(&pfull[cb], p.patch_bytes);
                 uint8_t* dst = sP + (size_t)cb * p.patch_bytes;
                 // box {ATOM channels, Wp slots, rows, 1} at (plane, -pad_w, p0 - pad_h, n): the zero
                 // padding and the slots beyond the image are TMA's out-of-bounds zero fill
-                for (int pl = 0; pl < p.planes; ++pl)
-                    ptx::tma_load_4d(&tmX, dst + (size_t)pl * p.plane_bytes, &pfull[cb], pl * ATOM, -p.cg.pw,
-                                     p0 - p.cg.ph, nimg);
+                if constexpr (PAIR) {                 // both patches complete on the leader's barrier
+                    if (rank == 0) ptx::mbar_arrive_expect_tx(&pfull[cb], 2 * p.patch_bytes);
+                    const uint32_t bar_c = ptx::mapa_shared(ptx::smem_u32(&pfull[cb]), 0);
+                    for (int pl = 0; pl < p.planes; ++pl)
+                        ptx::tma_load_4d_pair(&tmX, dst + (size_t)pl * p.plane_bytes, bar_c, pl * ATOM, -p.cg.pw,
+                                              p0 - p.cg.ph, nimg);
+                } else {
+                    ptx::mbar_arrive_expect_tx(&pfull[cb], p.patch_bytes);
+                    for (int pl = 0; pl < p.planes; ++pl)
+                        ptx::tma_load_4d(&tmX, dst + (size_t)pl * p.plane_bytes, &pfull[cb], pl * ATOM, -p.cg.pw,
+                                         p0 - p.cg.ph, nimg);
+                }
             }
             __syncwarp();
         }
@@ -151,8 +190,14 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
             if (ptx::elect_one()) {
                 // one barrier per k-block: the first tile's MMAs start when k-block 0 lands
                 for (int kb = 0; kb < p.kb_total; ++kb) {
-                    ptx::mbar_arrive_expect_tx(&bfull[kb], p.b_stage_bytes);
-                    load_b(sB + (size_t)kb * p.b_stage_bytes, &bfull[kb], kb, 0);
+                    if constexpr (PAIR) {             // my half of the columns, on the leader's barrier
+                        if (rank == 0) ptx::mbar_arrive_expect_tx(&bfull[kb], 2 * p.b_stage_bytes);
+                        load_b_pair(sB + (size_t)kb * p.b_stage_bytes, ptx::mapa_shared(ptx::smem_u32(&bfull[kb]), 0),
+                                    kb, (int)rank * (p.tile_n / ATOM / 2));
+                    } else {
+                        ptx::mbar_arrive_expect_tx(&bfull[kb], p.b_stage_bytes);
+                        load_b(sB + (size_t)kb * p.b_stage_bytes, &bfull[kb], kb, 0);
+                    }
                 }
             }
             __syncwarp();
@@ -171,7 +216,11 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
                     const bool fresh = first_round;
                     if (++s == S) { s = 0; use_par ^= 1u; first_round = false; }
                     if (!fresh) ptx::mbar_wait(&empty[cs], cpar ^ 1u);
-                    if (ptx::elect_one()) {
+                    if (PAIR && ptx::elect_one()) {
+                        if (rank == 0) ptx::mbar_arrive_expect_tx(&full[cs], 2 * p.b_stage_bytes);
+                        load_b_pair(sB + (size_t)cs * p.b_stage_bytes, ptx::mapa_shared(ptx::smem_u32(&full[cs]), 0),
+                                    kb, n0 / ATOM + (int)rank * (p.tile_n / ATOM / 2));
+                    } else if (!PAIR && ptx::elect_one()) {
                         ptx::mbar_arrive_expect_tx(&full[cs], p.b_stage_bytes);   // both halves land here
                         if constexpr (CL == 2) {
                             // my half of the stage's 128-byte N blocks, written into both CTAs
@@ -189,6 +238,7 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
         }
     } else if (warp == 1) {
         // ===================== MMA issuer (contraction over r, s, c) =====================
+        const uint32_t tmem_base = tmem_address();
         int s = 0, acc = 0, pb = 0;
         uint32_t ph = 0, aph = 0, pph = 0;
         const uint32_t b_lbo = (uint32_t)p.tile_k * 128u;
@@ -219,9 +269,9 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
         const bool plain_arrive = (p.debug_skip_mma & 16) != 0;
         const bool wait_tempty = !(p.debug_skip_mma & 64);
         const int nbuf = p.nbuf, accb = p.acc_buffers;
-        if (b_res)                                    // the resident filter (per-k-block barriers)
+        if (b_res && !(PAIR && rank != 0))            // the resident filter (per-k-block barriers)
             for (int kb = 0; kb < p.kb_total; ++kb) ptx::mbar_wait(&bfull[kb], 0);
-        for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters) {
+        for (int64_t t = cluster_id; t < ((PAIR && rank != 0) ? 0 : p.num_tiles); t += num_clusters) {
             if (wait_tempty) ptx::mbar_wait(&tempty[acc], aph ^ 1u);
             ptx::mbar_wait(&pfull[pb], pph);
             if (trace && lane == 0 && tj < kTraceK) trace[8 + kTraceK + tj] = ptx::globaltimer();
@@ -249,7 +299,7 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
                     for (int ms = 0; ms < MSUB; ++ms)
 #pragma unroll
                         for (int kk = 0; kk < ATOM / UMMA_K; ++kk)
-                            ptx::umma<TF32, 1>(d0 + (uint32_t)ms * tile_n, ad + (uint64_t)(ms * 1024 + kk * 2),
+                            ptx::umma<TF32, CG>(d0 + (uint32_t)ms * tile_n, ad + (uint64_t)(ms * 1024 + kk * 2),
                                                bd + (uint64_t)(kk * UMMA_K * 8), idesc, kk ? 1u : accf);
                     accf = 1u;
                     const bool pw = ++pl == planes;             // plane wraps: next filter column
@@ -273,7 +323,8 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
                         ptx::tc_fence_after();
                         const uint64_t bd = bdesc0 + (uint64_t)((uint32_t)s1 * b_stage16);
                         for (int a = 0; a < n_atoms; ++a) atom(bd + (uint64_t)(a * ATOM * 8));
-                        if constexpr (CL == 2) ptx::umma_commit_multicast(&empty[s1], 0x3);
+                        if constexpr (PAIR) ptx::umma_commit<2>(&empty[s1]);
+                        else if constexpr (CL == 2) ptx::umma_commit_multicast(&empty[s1], 0x3);
                         else ptx::umma_commit<1>(&empty[s1]);
                         if (++s1 == Sring) { s1 = 0; ph1 ^= 1u; }
                     }
@@ -282,8 +333,8 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
                     ptx::mbar_arrive(&pempty[pb]);
                     ptx::mbar_arrive(&tfull[acc]);
                 } else {
-                    ptx::umma_commit<1>(&pempty[pb]);     // patch buffer free once these MMAs finish
-                    ptx::umma_commit<1>(&tfull[acc]);
+                    ptx::umma_commit<CG>(&pempty[pb]);    // patch buffer(s) free once these MMAs finish
+                    ptx::umma_commit<CG>(&tfull[acc]);
                 }
             }
             __syncwarp();
@@ -296,6 +347,7 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
         }
     } else if (warp >= 4) {
         // ===================== epilogue (bufferize) =====================
+        const uint32_t tmem_base = tmem_address();
         const int q = warp & 3;
         int acc = 0, buf = 0;
         uint32_t aph = 0;
@@ -407,7 +459,10 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
             __syncwarp();
             if (trace && warp == 4 && lane == 0 && tj < kTraceTiles) trace[8 + 2 * kTraceK + 2 * tj + 1] = ptx::globaltimer();
             ++tj;
-            if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+            if (lane == 0) {
+                if constexpr (PAIR) ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&tempty[acc]), 0));
+                else ptx::mbar_arrive(&tempty[acc]);
+            }
             if (++acc == p.acc_buffers) { acc = 0; aph ^= 1u; }
         }
         if (p.buffer_c && lane == 0) ptx::bulk_wait<0>();
@@ -418,14 +473,14 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
     if (trace && threadIdx.x == 0) trace[2] = ptx::globaltimer();
     if (warp == 2) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc<1>(tmem_base, p.tmem_cols);
+        ptx::tmem_dealloc<CG>(*reinterpret_cast<volatile uint32_t*>(tmem_slot), p.tmem_cols);
     }
 }
 
-template <bool TF32, int MSUB, int CL>
+template <bool TF32, int MSUB, int CL, bool PAIR = false>
 static cudaError_t launch_halo_t(const CUtensorMap& x, const CUtensorMap& b, const CUtensorMap& y, const TcParams& p,
                                  int grid, int smem, cudaStream_t st) {
-    auto k = tc_conv_halo_kernel<TF32, MSUB, CL>;
+    auto k = tc_conv_halo_kernel<TF32, MSUB, CL, PAIR>;
     cudaError_t e = ensure_smem_attr(k, smem);
     if (e != cudaSuccess) return e;
     if constexpr (CL == 1) {
@@ -460,6 +515,9 @@ cudaError_t launch_tc_conv_halo(bool tf32, const CUtensorMap& x, const CUtensorM
                                 const TcParams& p, int grid, int smem, cudaStream_t st) {
     // MSUB (128-row UMMA tiles per patch) is a template parameter: the per-atom UMMA
     // sequence is straight-line code
+    if (p.pair)
+        return tf32 ? launch_halo_t<true, 1, 2, true>(x, b, y, p, grid, smem, st)
+                    : launch_halo_t<false, 1, 2, true>(x, b, y, p, grid, smem, st);
     if (p.msub == 2)
         return tf32 ? launch_halo_cl<true, 2>(x, b, y, p, grid, smem, st) : launch_halo_cl<false, 2>(x, b, y, p, grid, smem, st);
     return tf32 ? launch_halo_cl<true, 1>(x, b, y, p, grid, smem, st) : launch_halo_cl<false, 1>(x, b, y, p, grid, smem, st);

@@ -84,14 +84,29 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         if constexpr (SPLIT3) for (int s = 0; s < S; ++s) ptx::mbar_init(&split[s], 2);
         ptx::fence_mbarrier_init();
     }
-    if (warp == 2) {
+    // Barriers first; the TMEM allocation (the first tcgen05 instruction, ~0.5-1 us on a cold
+    // SM) is then taken by warp 2 while the producers already issue the first (HBM-cold)
+    // stages.  Only the MMA issuer and the epilogue read the TMEM address: they wait on the
+    // named barrier kTmemBar, which warp 2 arrives on after the allocation.
+    if (warp == 2 && p.debug_late_alloc) {
         ptx::tmem_alloc<CG>(tmem_slot, p.tmem_cols);
         ptx::tmem_relinquish<CG>();
+        ptx::tc_fence_before();
     }
-    ptx::tc_fence_before();
     if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
-    ptx::tc_fence_after();
-    const uint32_t tmem_base = *tmem_slot;
+    if (warp == 2 && p.debug_late_alloc) {
+        ptx::named_bar_arrive(ptx::kTmemBar, ptx::kTmemBarThreads);
+    } else if (warp == 2) {
+        ptx::tmem_alloc<CG>(tmem_slot, p.tmem_cols);
+        ptx::tmem_relinquish<CG>();
+        ptx::tc_fence_before();
+        ptx::named_bar_arrive(ptx::kTmemBar, ptx::kTmemBarThreads);
+    }
+    auto tmem_address = [&]() -> uint32_t {     // warps 1 and 4..7, once, before any TMEM use
+        ptx::named_bar_sync(ptx::kTmemBar, ptx::kTmemBarThreads);
+        ptx::tc_fence_after();
+        return *reinterpret_cast<volatile uint32_t*>(tmem_slot);
+    };
     uint64_t* const trace = (p.trace && blockIdx.x < kTraceCtas) ? p.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
     if (trace && threadIdx.x == 0) trace[1] = ptx::globaltimer();
     int trace_k = 0;       // per-role counters (each role only touches its own slots)
@@ -255,6 +270,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         }
     } else if (warp == 1) {
         // ===================== MMA issuer (contraction) =====================
+        const uint32_t tmem_base = tmem_address();
         // One elected lane runs each tile's whole k-loop (stage waits, UMMAs, commits); the
         // warp reconverges once per tile.  Loop bounds and strides are pinned in registers
         // and the atoms of a stage are a compile-time count (NA), so a stage is straight-line
@@ -352,6 +368,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         }
     } else if (warp >= 4) {
         // ===================== epilogue (bufferize) =====================
+        const uint32_t tmem_base = tmem_address();
         const int q = warp & 3;                        // TMEM lanes 32q..32q+31
         int acc = 0;
         uint32_t aph = 0;
@@ -480,7 +497,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     if (trace && threadIdx.x == 0) trace[2] = ptx::globaltimer();
     if (warp == 2) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc<CG>(tmem_base, p.tmem_cols);
+        ptx::tmem_dealloc<CG>(*reinterpret_cast<volatile uint32_t*>(tmem_slot), p.tmem_cols);
     }
 }
 

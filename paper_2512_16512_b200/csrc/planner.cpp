@@ -135,7 +135,19 @@ static xtc_status plan_tc_halo(const xtc_op_desc& d, const xtc_schedule& s, int 
     if (p.split_k > 1 && s.buffer_c) ILLEGAL("pack_halo: split_k writes fp32 partials with direct stores (buffer_c 0)");
     if (s.pack_warps > 1) ILLEGAL("pack_halo: pack_warps must be 0 or 1 (warp 0 packs patches, warp 3 the B ring)");
     if (s.tile_m != 128 && s.tile_m != 256) ILLEGAL("pack_halo: tile_m must be 128 or 256 (1 or 2 UMMA M-tiles per patch)");
-    if (s.inner_m != 0 && s.inner_m != 128) ILLEGAL("pack_halo: inner_m (UMMA M) must be 128");
+    if (s.inner_m != 0 && s.inner_m != 128 && s.inner_m != 256) ILLEGAL("pack_halo: inner_m (UMMA M) must be 128 or 256");
+    // inner_m = 256: the UMMA atom spans a CTA pair (cta_group::2).  Each CTA packs the patch of
+    // its own 128-row M tile and half of the filter's N columns; the leader issues M = 256
+    // UMMAs whose A rows come from both patches and B columns from both filter halves (per
+    // SM: the operand reads of the B half and the filter TMA writes are halved)
+    const bool pair = s.inner_m == 256;
+    if (pair) {
+        if (hcl != 2 || s.tile_m != 256) ILLEGAL("pack_halo: inner_m 256 (CTA pair) needs cluster_m 2 and tile_m 256");
+        if (p.split_k > 1) ILLEGAL("pack_halo: the CTA pair (inner_m 256) needs split_k 1");
+        if (s.tile_n % (2 * p.atom_n))
+            ILLEGAL("pack_halo: the CTA pair needs tile_n %% %d == 0 (a 128-byte filter block per CTA)", 2 * p.atom_n);
+        if (d.f % p.atom_n) ILLEGAL("pack_halo: the CTA pair needs F %% %d == 0 (3-D filter TMA)", p.atom_n);
+    }
     if (s.inner_n != 0 && s.inner_n != s.tile_n) ILLEGAL("tcgen05 inner_n (UMMA N) must equal tile_n");
     if (s.tile_n < p.atom_n || s.tile_n > 256 || s.tile_n % p.atom_n)
         ILLEGAL("tcgen05 tile_n must be a multiple of %d in [%d,256]", p.atom_n, p.atom_n);
@@ -153,7 +165,7 @@ static xtc_status plan_tc_halo(const xtc_op_desc& d, const xtc_schedule& s, int 
     int wp = 8;
     while (wp < Q + d.s - 1) wp *= 2;
     if (wp > 128) ILLEGAL("pack_halo: Q + S - 1 = %lld pixel slots exceed one 128-row UMMA tile", (long long)(Q + d.s - 1));
-    const int msub = s.tile_m / 128;
+    const int msub = pair ? 1 : s.tile_m / 128;            // the pair: one 128-row UMMA tile per CTA
     const int rt = 128 / wp;                               // output rows per UMMA M-tile
     const int64_t pr = (int64_t)msub * rt + d.r - 1;       // patch rows
     if (pr > 256) ILLEGAL("pack_halo: %lld patch rows exceed the 256-row TMA box", (long long)pr);
@@ -165,7 +177,7 @@ static xtc_status plan_tc_halo(const xtc_op_desc& d, const xtc_schedule& s, int 
     p.tmem_cols = alloc;
     const int64_t planes = d.c / p.atom_k;
     const int64_t patch = planes * pr * wp * 128;
-    const int64_t b_stage = (int64_t)s.tile_k * s.tile_n * es;
+    const int64_t b_stage = (int64_t)s.tile_k * (pair ? s.tile_n / 2 : s.tile_n) * es;   // per CTA
     p.tiles_n = (int)cdiv(N_, s.tile_n);
     p.kb_total = (int)cdiv(K_, s.tile_k);
     int64_t b_bytes;
@@ -199,7 +211,10 @@ static xtc_status plan_tc_halo(const xtc_op_desc& d, const xtc_schedule& s, int 
     p.halo_patch_bytes = patch;
     p.halo_tpi = (int)cdiv(P, (int64_t)rt * msub);
     p.tiles_m = (int)(d.batch * p.halo_tpi);
-    if (hcl == 2) {
+    if (pair) {
+        if (p.tiles_m % 2) ILLEGAL("pack_halo: the CTA pair needs an even number of M tiles (%d)", p.tiles_m);
+        p.tiles_m /= 2;                                 // the tile loop runs over M-tile pairs
+    } else if (hcl == 2) {
         if (s.b_resident) ILLEGAL("pack_halo: cluster_m 2 multicasts the filter ring; b_resident must be 0");
         if ((s.tile_n / p.atom_n) % 2) ILLEGAL("pack_halo: cluster_m 2 needs an even number of 128-byte filter blocks (tile_n)");
         if (p.tiles_m % 2) ILLEGAL("pack_halo: cluster_m 2 needs an even number of M tiles (%d)", p.tiles_m);
@@ -213,7 +228,8 @@ static xtc_status plan_tc_halo(const xtc_op_desc& d, const xtc_schedule& s, int 
     p.k_per_split = (int64_t)p.kb_per_split * s.tile_k;
     p.num_tiles = (int64_t)p.tiles_m * p.tiles_n * p.split_k;
     if (p.num_tiles >= (1ll << 31)) ILLEGAL("too many tiles");
-    p.cta_group = 1;
+    p.halo_pair = pair;
+    p.cta_group = pair ? 2 : 1;                         // UMMA M = 128 * cta_group (abi.cu idesc)
     p.block = kTcThreads;
     p.cluster = hcl;
     const int64_t ctas = p.num_tiles * hcl;

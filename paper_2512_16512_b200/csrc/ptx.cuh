@@ -192,6 +192,15 @@ __device__ __forceinline__ void tma_load_3d_pair(const CUtensorMap* m, void* dst
         ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2)
         : "memory");
 }
+__device__ __forceinline__ void tma_load_4d_pair(const CUtensorMap* m, void* dst, uint32_t bar_cluster, int32_t c0,
+                                                 int32_t c1, int32_t c2, int32_t c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2];"
+        ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2),
+          "r"(c3)
+        : "memory");
+}
 __device__ __forceinline__ void tma_load_im2col_4d_pair(const CUtensorMap* m, void* dst, uint32_t bar_cluster,
                                                         int32_t c, int32_t w, int32_t h, int32_t n,
                                                         uint16_t off_w, uint16_t off_h) {
@@ -225,6 +234,16 @@ __device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
     else
         asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
 }
+// Named CTA barriers (id 0 is __syncthreads): the TMEM allocator arrives, the TMEM users
+// (MMA issuer + epilogue) sync, so the TMA producers never wait for the allocation.
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(uint32_t id, uint32_t n) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+constexpr uint32_t kTmemBar = 1;            // allocator (warp 2) + warp 1 + warps 4..7
+constexpr uint32_t kTmemBarThreads = 6 * 32;
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 

@@ -104,7 +104,8 @@ struct Plan {
     // 128-byte channel planes, nbuf patch buffers, tpi tiles per image
     bool halo = false;
     int32_t halo_wp = 0, halo_rt = 0, halo_msub = 0, halo_pr = 0, halo_planes = 0, halo_nbuf = 0, halo_tpi = 0;
-    int32_t halo_cl = 1;                // CTAs per cluster sharing the filter stream (TMA multicast)
+    int32_t halo_cl = 1;                // CTAs per cluster sharing the filter stream (TMA multicast, or a pair)
+    bool halo_pair = false;             // inner_m 256: cta_group::2 UMMAs (M = 256) over a CTA pair
     int64_t halo_patch_bytes = 0;
 };
 
@@ -145,6 +146,8 @@ struct TcParams {
     int32_t cons;            // fused consumer bits (XTC_CONSUMER_*) applied in the epilogue
     const float* bias;       // XTC_CONSUMER_BIAS: one fp32 value per output column
     int32_t a3d, b3d;        // one 3-D TMA per stage for all 128-B atoms of A / B (tmA / tmB are 3-D maps)
+    int32_t debug_late_alloc;  // diagnostics (A/B): XTC_DEBUG_LATE_ALLOC=1 allocates TMEM before the
+                               // prologue barrier, i.e. the producers wait for the allocation
     int32_t debug_skip_mma;  // diagnostics only, output invalid: XTC_DEBUG_SKIP_MMA, or XTC_DEBUG_SKIP=mask
                              // (conv_halo: 1 no MMAs, 2 no patch TMA, 4 no output stores)
     int64_t ldc, ws_ld;
@@ -155,7 +158,7 @@ struct TcParams {
     uint32_t lo_off;         // 3xTF32: byte offset from a hi stage (A or B ring) to its lo copy
     ConvGeom cg;
     // pack_halo conv only (see Plan)
-    int32_t wp, rt, msub, planes, nbuf, tpi, cl;
+    int32_t wp, rt, msub, planes, nbuf, tpi, cl, pair;
     uint32_t patch_bytes, plane_bytes;
     // Diagnostics (XTC_TRACE): %globaltimer stamps for CTAs < kTraceCtas, laid out
     // [cta][kTraceSlots]: slot 0 kernel entry, 1 setup done; producer issue of k-block i at

@@ -180,6 +180,7 @@ def test_tc_conv_split_k_and_stride2():
 
 
 # pack_halo: the input packed once per output tile, filter taps as row-shifted views
+PAIR_H = dict(tile_m=256, cluster_m=2, inner_m=256)
 HALO_CASES = [
     # (batch, h, w, c, f, r, s, pad, in, out, schedule overrides)            Wp  rows/UMMA tile
     ((2, 56, 56, 64, 64, 3, 3, 1, "bf16", "bf16"), dict(tile_n=64, b_resident=1, stages=2)),               # 64  2
@@ -195,6 +196,12 @@ HALO_CASES = [
     # cluster_m 2: the filter stream shared by two CTAs through TMA multicast
     ((3, 14, 14, 256, 256, 3, 3, 1, "bf16", "bf16"), dict(cluster_m=2, tile_n=128, tile_k=128, stages=3)),
     ((2, 28, 28, 64, 256, 3, 3, 1, "bf16", "f32"), dict(cluster_m=2, tile_n=256, stages=3, persistent=0, buffer_c=0)),
+    # inner_m 256: CTA pair (cta_group::2), M = 256 UMMAs over two CTAs' patches and filter halves
+    ((3, 14, 14, 256, 256, 3, 3, 1, "bf16", "bf16"), dict(PAIR_H, tile_n=128, tile_k=128, stages=3)),
+    ((2, 14, 14, 256, 256, 3, 3, 1, "bf16", "f32"), dict(PAIR_H, tile_n=256, stages=3, buffer_c=0, persistent=0)),
+    ((2, 28, 28, 64, 128, 3, 3, 1, "bf16", "bf16"), dict(PAIR_H, tile_n=128, stages=2, b_resident=1)),     # 32  4
+    ((2, 9, 13, 64, 128, 3, 3, 1, "bf16", "f32"), dict(PAIR_H, tile_n=128, stages=2, acc_buffers=1)),      # ragged
+    ((2, 14, 14, 64, 128, 3, 3, 1, "tf32", "f32"), dict(PAIR_H, tile_n=64, tile_k=32, stages=4)),          # tf32
     # split_k: K segments (runs of taps / channel planes) as CTAs, ordered reduction
     ((1, 14, 14, 256, 256, 3, 3, 1, "bf16", "bf16"), dict(tile_n=128, stages=4, split_k=3, buffer_c=0)),
     ((1, 14, 14, 256, 256, 3, 3, 1, "bf16", "bf16"), dict(tile_n=128, stages=4, split_k=9, buffer_c=0)),

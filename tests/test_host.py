@@ -159,6 +159,9 @@ def test_pack_halo_plan():
     l14 = xtc.conv2d_desc(32, 14, 14, 256, 256)
     st, info, why = chk(l14, **dict(HALO, tile_n=128, stages=4))
     assert st == xtc.XTC_OK and info.num_tiles == 32 * 2 * 2, why
+    # the CTA pair: the tile loop runs over M-tile pairs, two CTAs (one cluster) per pair tile
+    st, info, why = chk(l14, **dict(HALO, tile_m=256, cluster_m=2, inner_m=256, tile_n=128, tile_k=128, stages=3))
+    assert st == xtc.XTC_OK and info.num_tiles == 32 * 2 * 2 // 2 and info.cluster_x == 2, why
     one = xtc.conv2d_desc(2, 7, 7, 128, 64, 1, 1, 1, 0)        # 1x1: Wp = 8, 16 rows per tile
     st, info, why = chk(one, **HALO)
     assert st == xtc.XTC_OK and info.num_tiles == 2, why
@@ -171,6 +174,12 @@ def test_pack_halo_plan():
     (xtc.conv2d_desc(2, 56, 56, 64, 64), dict(cluster_m=2, b_resident=1), "b_resident"),
     (xtc.conv2d_desc(2, 56, 56, 64, 64), dict(cluster_m=2), "even number of 128-byte filter blocks"),
     (xtc.conv2d_desc(1, 14, 14, 256, 256), dict(cluster_m=2, tile_n=128, tile_m=256), "even number of M tiles"),
+    (xtc.conv2d_desc(2, 14, 14, 256, 256), dict(inner_m=256, tile_n=128), "cluster_m 2 and tile_m 256"),
+    (xtc.conv2d_desc(2, 56, 56, 64, 64), dict(inner_m=256, cluster_m=2, tile_m=256, tile_n=64), "tile_n % 128"),
+    (xtc.conv2d_desc(1, 7, 7, 256, 256), dict(inner_m=256, cluster_m=2, tile_m=256, tile_n=128), "even number of M tiles"),
+    (xtc.conv2d_desc(2, 14, 14, 256, 256), dict(inner_m=256, cluster_m=2, tile_m=256, tile_n=128, split_k=2,
+                                                buffer_c=0), "split_k 1"),
+    (xtc.conv2d_desc(2, 56, 56, 64, 64), dict(inner_m=64), "inner_m"),
     (xtc.conv2d_desc(2, 56, 56, 64, 64), dict(split_k=3), "buffer_c 0"),
     (xtc.conv2d_desc(2, 56, 56, 64, 64), dict(split_k=10, buffer_c=0), "empty K segment"),
     (xtc.conv2d_desc(2, 56, 56, 64, 64), dict(pack_warps=2), "pack_warps"),
