@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--sweep-candidates", type=int, default=1024)
     ap.add_argument("--overlap-chunks", type=int, default=4,
                     help="N>1: block-cyclic row chunks per rank, each all-gathered while the next computes")
+    ap.add_argument("--gather", default="fused", choices=["fused", "nccl"],
+                    help="N>1: 'fused' = the all-gather inside the GEMM epilogue (xtc_run_gather: TMA stores "
+                         "into every rank's symmetric-memory C over NVLink); 'nccl' = chunked NCCL overlap")
     return ap.parse_args()
 
 
@@ -315,6 +318,18 @@ def main_xtc(args):
     CH = args.overlap_chunks if world > 1 else 1
     if CH > 1 and M % (world * CH):
         CH = 1
+    # N > 1 with the gather fused into the GEMM: C lives in symmetric memory,
+    # every rank's epilogue stores its tiles into all W copies; no NCCL call on the data path.
+    # If the symmetric-memory rendezvous is unavailable the chunked NCCL overlap is used instead
+    # (another GPU path, reported in config.parallelism).
+    fused, fused_note = None, None
+    if world > 1 and not rehearsal and args.gather == "fused":
+        try:
+            from paper_2512_16512_b200.parallel import SymmetricOutput
+            fused = SymmetricOutput((M, N), torch.bfloat16, dev)
+            CH = 1
+        except Exception as ex:
+            fused_note = f"fused gather unavailable ({ex!r:.160}); NCCL chunked overlap used"
     Mc = Mr // CH
     a = torch.empty((Mr, K), dtype=torch.bfloat16, device=dev)
     b = torch.empty((K, N), dtype=torch.bfloat16, device=dev)
@@ -336,9 +351,17 @@ def main_xtc(args):
     # a8 (on-chip validation: fp64 GPU reference, NaN sentinel) runs once AFTER the timed
     # region: its ~0.1 s fp64 reference kernel would otherwise heat the part right before timing
 
-    full_c = torch.empty((M, N), dtype=torch.bfloat16, device=dev) if world > 1 else None
+    full_c = (fused.tensor if fused else torch.empty((M, N), dtype=torch.bfloat16, device=dev)) if world > 1 else None
 
     def compute_and_gather(kev_pair=None):
+        if fused:
+            if kev_pair is not None:
+                kev_pair[0].record(stream)
+            op.run_gather(a, b, fused.dests, r0, M, stream=sp)
+            if kev_pair is not None:
+                kev_pair[1].record(stream)
+            fused.barrier()                         # every rank's tiles have landed in every copy
+            return
         handles = []
         if kev_pair is not None:
             kev_pair[0].record(stream)
@@ -404,7 +427,8 @@ def main_xtc(args):
     e2e_steps = max(3, min(args.steps, 10))
     bufs = [(a, b, c, full_c, op)]
     a2, b2, c2 = torch.empty_like(a), torch.empty_like(b), torch.empty_like(c)
-    fc2 = torch.empty_like(full_c) if world > 1 else None
+    fused2 = SymmetricOutput((M, N), torch.bfloat16, dev) if fused else None
+    fc2 = (fused2.tensor if fused else torch.empty_like(full_c)) if world > 1 else None
     bufs.append((a2, b2, c2, fc2, xtc.Op(desc, local).apply(xtc.schedule(**HEADLINE_SCHEDULE))))
     s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
     ev_in = [torch.cuda.Event() for _ in range(2)]
@@ -424,9 +448,14 @@ def main_xtc(args):
             stream.wait_event(ev_in[j])
             if i >= 2:
                 stream.wait_event(ev_out[j])         # buffer j's result was copied out by step i-2
-            dop.run(da, db, dc, stream=sp)
-            if world > 1:
-                gather_rows(dc, M, out=dfc)
+            if fused:
+                fz = fused if j == 0 else fused2
+                dop.run_gather(da, db, fz.dests, r0, M, stream=sp)
+                fz.barrier()
+            else:
+                dop.run(da, db, dc, stream=sp)
+                if world > 1:
+                    gather_rows(dc, M, out=dfc)
             ev_comp[j].record(stream)
             s_out.wait_event(ev_comp[j])
             with torch.cuda.stream(s_out):
@@ -463,8 +492,24 @@ def main_xtc(args):
         torch.cuda.synchronize(dev)
         ok = all(torch.equal(full_c[(j * world + rank) * Mc:(j * world + rank + 1) * Mc] if CH > 1 else
                              full_c[r0:r1], c[j * Mc:(j + 1) * Mc] if CH > 1 else c) for j in range(CH))
-        v = torch.tensor([validation["valid"], int(ok)], device=dev)
-        dist.all_reduce(v, op=dist.ReduceOp.MIN)
+        # ... and every rank holds the same assembled C (checksums of the whole buffer agree)
+        from paper_2512_16512_b200.parallel import checksum_rows
+        cs = checksum_rows(full_c)
+        cs_all = [torch.empty_like(cs) for _ in range(world)]
+        if rehearsal:
+            cs_host = [torch.empty(2, dtype=torch.int64) for _ in range(world)]
+            dist.all_gather(cs_host, cs.cpu())
+            cs_all = cs_host
+        else:
+            dist.all_gather(cs_all, cs)
+        same = all(torch.equal(x.cpu(), cs_all[0].cpu()) for x in cs_all)
+        v = torch.tensor([validation["valid"], int(ok and same)], device=dev)
+        if rehearsal:
+            vh = v.cpu()
+            dist.all_reduce(vh, op=dist.ReduceOp.MIN)
+            v = vh
+        else:
+            dist.all_reduce(v, op=dist.ReduceOp.MIN)
         validation["valid_all_ranks"] = int(v[0])
         validation["gather_consistent_all_ranks"] = int(v[1])
 
@@ -523,8 +568,12 @@ def main_xtc(args):
             "data": "synthetic (seeded counter-based generator, uniform[-1,1) bf16)",
             "config": {"workload": "matmul 8192x8192x8192 bf16->bf16 (BASELINE config 5: largest matmul)",
                        "model": None, "global_batch": 1, "seq_len": None,
-                       "parallelism": (f"M-sharded x{world}, {CH} block-cyclic chunks per rank, each NCCL "
-                                       f"all-gather overlapping the next chunk's GEMM") if world > 1 else "single GPU",
+                       "parallelism": ((f"M-sharded x{world}, all-gather fused into the GEMM epilogue "
+                                        f"(xtc_run_gather: TMA stores into every rank's symmetric-memory C)")
+                                       if fused else
+                                       (f"M-sharded x{world}, {CH} block-cyclic chunks per rank, each NCCL "
+                                        f"all-gather overlapping the next chunk's GEMM"
+                                        + (f"; {fused_note}" if fused_note else ""))) if world > 1 else "single GPU",
                        "schedule": HEADLINE_SCHEDULE,
                        "l2": "inputs (256 MiB) exceed L2 (126 MB); no flush between steps"},
             "frac_of_peak": value / world / peak_tf,

@@ -246,6 +246,24 @@ xtc_status xtc_schedule_default(const xtc_op_desc* desc, int32_t opt_level, xtc_
  * previous call. */
 xtc_status xtc_run(xtc_op op, const void* const* inputs, void* const* outputs, void* stream);
 
+/* a3..a7 + §8(e) -- xtc_run of one M-shard of a matmul whose all-gather is
+ * fused into the epilogue (BASELINE config 5, "large matmul
+ * ... sharded by M ... NCCL all-gather", where the gather is the exchange step
+ * after the per-rank GEMM).  Every output tile staged in SMEM is written by TMA
+ * to EACH of the n_dest destinations: dests[d] is a device pointer (local, or
+ * a peer GPU's buffer mapped into this device's address space, e.g. CUDA IPC /
+ * symmetric memory over NVLink) to a row-major [dest_rows][N] output (row pitch
+ * desc.ldc if set, else N); this op's output row i lands at row row_offset + i
+ * of every destination.  The caller owns every buffer and must order the
+ * destinations' readers after this launch (a cross-device barrier for peers).
+ * Requires: tcgen05 engine, matmul, buffer_c = 1, split_k = 1, no split_n_at
+ * root, no separate consumer pass, no XTC_CONSUMER_ACCUMULATE, M a multiple of
+ * the CTA tile rows (a ragged last tile would overwrite a neighbour's rows),
+ * 1 <= n_dest <= 8, row_offset + M <= dest_rows, 16-byte aligned dests.
+ * Violations -> XTC_E_INVALID_ARG / XTC_E_UNSUPPORTED, nothing launched. */
+xtc_status xtc_run_gather(xtc_op op, const void* const* inputs, void* const* dests, int32_t n_dest,
+                          int64_t row_offset, int64_t dest_rows, void* stream);
+
 /* a8 + a9 -- Executor + Evaluator.  Synchronous.  Sequence:
  *   1. if cfg->validate: fill outputs with NaN, run once, compute (or reuse)
  *      the fp64 GPU reference R and D, compare -> max_norm_err, n_mismatch, n_nan;

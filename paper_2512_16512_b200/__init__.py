@@ -133,6 +133,7 @@ def lib():
         L.xtc_schedule_apply.argtypes = [xtc_op, P(xtc_schedule)]
         L.xtc_schedule_default.argtypes = [P(xtc_op_desc), c_int32, P(xtc_schedule)]
         L.xtc_run.argtypes = [xtc_op, P(c_void_p), P(c_void_p), c_void_p]
+        L.xtc_run_gather.argtypes = [xtc_op, P(c_void_p), P(c_void_p), c_int32, c_int64, c_int64, c_void_p]
         L.xtc_measure.argtypes = [xtc_op, P(c_void_p), P(c_void_p), P(xtc_measure_cfg), P(xtc_metrics), c_void_p]
         L.xtc_sweep.argtypes = [xtc_op, P(xtc_schedule), c_int32, P(c_void_p), P(c_void_p), P(xtc_measure_cfg),
                                 P(xtc_metrics), c_void_p]
@@ -147,7 +148,7 @@ def lib():
         L.xtc_abi_sizes.argtypes = [P(c_int64)]
         L.xtc_abi_sizes.restype = None
         for name in ("xtc_op_create", "xtc_schedule_check", "xtc_schedule_apply", "xtc_schedule_default",
-                     "xtc_run", "xtc_measure", "xtc_sweep", "xtc_fill"):
+                     "xtc_run", "xtc_run_gather", "xtc_measure", "xtc_sweep", "xtc_fill"):
             getattr(L, name).restype = c_int32
         sizes = (c_int64 * 5)()
         L.xtc_abi_sizes(sizes)
@@ -205,6 +206,13 @@ def _ptrs(ptrs):
 
 def xtc_run(op, inputs, outputs, stream=0) -> None:
     _check(lib().xtc_run(op, _ptrs(inputs), _ptrs(outputs), c_void_p(stream)))
+
+
+def xtc_run_gather(op, inputs, dests, row_offset, dest_rows, stream=0) -> None:
+    """xtc_run of an M-shard whose output tiles are TMA-stored to every pointer in ``dests``
+    (the all-gather fused into the epilogue; include/xtc.h)."""
+    _check(lib().xtc_run_gather(op, _ptrs(inputs), _ptrs(dests), len(dests), row_offset, dest_rows,
+                                c_void_p(stream)))
 
 
 def xtc_measure(op, inputs, outputs, cfg: xtc_measure_cfg, stream=0) -> xtc_metrics:
@@ -328,6 +336,11 @@ class Op:
 
     def run(self, a, b, c, stream=None, bias=None) -> None:
         xtc_run(self.handle, self._inputs(a, b, bias), [c.data_ptr()], self._stream(stream))
+
+    def run_gather(self, a, b, dests, row_offset, dest_rows, stream=None, bias=None) -> None:
+        """dests: device pointers (ints) of [dest_rows][N] outputs, local or peer-mapped."""
+        xtc_run_gather(self.handle, self._inputs(a, b, bias), list(dests), row_offset, dest_rows,
+                       self._stream(stream))
 
     def measure(self, a, b, c, cfg: xtc_measure_cfg = None, stream=None, bias=None) -> xtc_metrics:
         cfg = cfg or measure_cfg()

@@ -174,6 +174,13 @@ struct xtc_op_s {
     // appended to `path` as one JSON line per tcgen05 launch (synchronises; diagnostics only)
     std::string trace_path;
     uint64_t* trace_dev = nullptr;
+    // xtc_run_gather: destination tensor maps (host copy + device copy the kernel reads),
+    // bound to (dests, row count); re-encoded and re-uploaded only when these change
+    alignas(64) CUtensorMap gmaps[8];
+    void* gmaps_dev = nullptr;
+    const void* gbound[8] = {nullptr};
+    int32_t n_gbound = 0;
+    int64_t g_rows = 0;
 };
 
 static int dsize(int dt) { return dt == XTC_BF16 ? 2 : 4; }
@@ -194,6 +201,7 @@ static void release_op(xtc_op op) {
     if (op->counts) cudaFree(op->counts);
     if (op->c_old) cudaFree(op->c_old);
     if (op->trace_dev) cudaFree(op->trace_dev);
+    if (op->gmaps_dev) cudaFree(op->gmaps_dev);
     for (auto e : op->evs) cudaEventDestroy(e);
     cudaSetDevice(cur);
     delete op;
@@ -537,7 +545,13 @@ static ConvGeom conv_geom(const xtc_op_desc& d) {
     return g;
 }
 
-static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cudaStream_t st) {
+struct GatherArgs {            // xtc_run_gather: device tensor maps of the destinations
+    const void* maps;
+    int32_t n, row0;
+};
+
+static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cudaStream_t st,
+                           const GatherArgs* ga = nullptr) {
     const Plan& p = op->plan;
     const xtc_op_desc& d = op->d;
     const int64_t ldc = (d.kind == XTC_OP_MATMUL && d.ldc) ? d.ldc : p.n_total;
@@ -620,6 +634,11 @@ static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cud
         tp.b_stage_bytes = (uint32_t)(p.sch.tile_k * (p.sch.tile_n / p.cta_group) * es);
         tp.lo_off = p.split3 ? (uint32_t)(p.sch.stages * (tp.a_stage_bytes + tp.b_stage_bytes)) : 0u;
         tp.cg = conv_geom(d);
+        if (ga) {
+            tp.gather = ga->maps;
+            tp.n_gather = ga->n;
+            tp.gather_row0 = ga->row0;
+        }
         const size_t trace_bytes = (size_t)kTraceCtas * kTraceSlots * 8;
         if (!op->trace_path.empty()) {
             if (!op->trace_dev) CU_TRY(cudaMalloc(&op->trace_dev, trace_bytes), "trace alloc");
@@ -708,6 +727,62 @@ extern "C" xtc_status xtc_run(xtc_op op, const void* const* inputs, void* const*
             return fail(XTC_E_INVALID_ARG, "TMA store needs a 16-byte aligned output");
     }
     return run_impl(op, inputs[0], inputs[1], outputs[0], (cudaStream_t)stream);
+}
+
+extern "C" xtc_status xtc_run_gather(xtc_op op, const void* const* inputs, void* const* dests, int32_t n_dest,
+                                     int64_t row_offset, int64_t dest_rows, void* stream) {
+    if (!op || !inputs || !dests || !inputs[0] || !inputs[1]) return fail(XTC_E_INVALID_ARG, "null op or tensor pointer");
+    if (!op->has_plan) return fail(XTC_E_NO_SCHEDULE, "xtc_run_gather before xtc_schedule_apply");
+    if (n_dest < 1 || n_dest > 8) return fail(XTC_E_INVALID_ARG, "xtc_run_gather: n_dest must be in [1, 8]");
+    const Plan& p = op->plan;
+    const xtc_op_desc& d = op->d;
+    if (d.kind != XTC_OP_MATMUL || p.engine != XTC_ENGINE_TCGEN05 || !p.sch.buffer_c || p.split_k != 1 || p.halo ||
+        p.has_tail || p.cons_pass || p.split3 || (d.consumer & XTC_CONSUMER_ACCUMULATE))
+        return fail(XTC_E_UNSUPPORTED, "xtc_run_gather: needs a tcgen05 matmul schedule with buffer_c=1, split_k=1, "
+                                       "no split_n_at root, fused consumers other than accumulate");
+    const int64_t tile_rows = 128 * (int64_t)p.cta_group;
+    if (p.M % tile_rows) return fail(XTC_E_UNSUPPORTED, "xtc_run_gather: M must be a multiple of the CTA tile rows");
+    if (row_offset < 0 || row_offset + p.M > dest_rows || dest_rows > INT32_MAX)
+        return fail(XTC_E_INVALID_ARG, "xtc_run_gather: rows [row_offset, row_offset + M) must lie in [0, dest_rows)");
+    for (int i = 0; i < 2; ++i)
+        if (reinterpret_cast<uintptr_t>(inputs[i]) & 15) return fail(XTC_E_INVALID_ARG, "TMA needs 16-byte aligned inputs");
+    for (int i = 0; i < n_dest; ++i)
+        if (!dests[i] || (reinterpret_cast<uintptr_t>(dests[i]) & 15))
+            return fail(XTC_E_INVALID_ARG, "xtc_run_gather: null or unaligned destination");
+    if (bind_bias(op, inputs) != XTC_OK) return XTC_E_INVALID_ARG;
+    DeviceGuard g(op->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    const int os = dsize(d.out_dtype);
+    const int64_t ld = d.ldc ? d.ldc : p.n_total;
+    bool same = op->n_gbound == n_dest && op->g_rows == dest_rows;
+    for (int i = 0; same && i < n_dest; ++i) same = op->gbound[i] == dests[i];
+    if (!same) {
+        xtc_status s = load_driver_fns();
+        if (s != XTC_OK) return s;
+        const CUtensorMapDataType out_t = os == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+        for (int i = 0; i < n_dest; ++i) {
+            cuuint64_t dims[3] = {(cuuint64_t)p.N, (cuuint64_t)dest_rows, 1};
+            cuuint64_t strides[2] = {(cuuint64_t)(ld * os), (cuuint64_t)(ld * os * dest_rows)};
+            cuuint32_t box[3] = {(cuuint32_t)(128 / os), 32, 1};
+            cuuint32_t estr[3] = {1, 1, 1};
+            CUresult r = g_encode_tiled(&op->gmaps[i], out_t, 3, dests[i], dims, strides, box, estr,
+                                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                        CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS)
+                return fail(XTC_E_CUDA, "cuTensorMapEncodeTiled(gather dest) failed: " + std::to_string((int)r));
+        }
+        if (!op->gmaps_dev) CU_TRY(cudaMalloc(&op->gmaps_dev, sizeof op->gmaps), "gather maps alloc");
+        // pageable source: the call returns once the maps are staged, so op->gmaps may change afterwards
+        CU_TRY(cudaMemcpyAsync(op->gmaps_dev, op->gmaps, n_dest * sizeof(CUtensorMap), cudaMemcpyHostToDevice, st),
+               "gather maps upload");
+        for (int i = 0; i < 8; ++i) op->gbound[i] = i < n_dest ? dests[i] : nullptr;
+        op->n_gbound = n_dest;
+        op->g_rows = dest_rows;
+    }
+    // C (for the unused local map) = this shard's rows of the first destination
+    void* c_local = static_cast<uint8_t*>(dests[0]) + row_offset * ld * os;
+    GatherArgs ga{op->gmaps_dev, n_dest, (int32_t)row_offset};
+    return run_impl(op, inputs[0], inputs[1], c_local, st, &ga);
 }
 
 // --------------------------------------------------------------- measure --

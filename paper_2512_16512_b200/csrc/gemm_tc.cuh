@@ -1,0 +1,552 @@
+// gemm_tc.cuh -- KB2/KB3: schedule-parametrised tcgen05 GEMM and implicit-GEMM
+// conv2d for sm_100a (bf16 kind::f16 / tf32 kind::tf32, fp32 accumulate in TMEM).
+//
+// How the paper's primitives (Table I) appear in this kernel:
+//   strip_mine  -> CTA tile 128 x tile_n x tile_k (CTA pair: 256 x tile_n); UMMA atom
+//                  (128|256) x tile_n x 16 (8 for tf32)
+//   interchange -> tile order (TileMap: MN / NM + grouped raster)
+//   unroll      -> the tile_k / UMMA_K MMAs of one stage are issued back to back
+//   vectorize   -> the innermost tile is one tcgen05.mma (the tensor core is the SIMD unit)
+//   parallelize -> one CTA (pair) per tile, or persistent CTAs striding over tiles;
+//                  cluster_m = 2 pairs two SMs on one 256-row tile (cta_group::2)
+//   split       -> split_k contiguous K segments, fp32 partials + ordered reduction
+//   pack        -> TMA -> `stages`-deep SMEM ring in the 128-byte-swizzled layout the
+//                  UMMA reads ("copies the elements ... in the order of their access",
+//                  P:549-557; the swizzle plays the role of the paper's anti-conflict pad)
+//   bufferize   -> accumulator in TMEM (acc_buffers deep); output staged in SMEM and
+//                  written back by TMA store ("copied to the output tensor, while modifying
+//                  its ordering to fit the original layout")
+//
+// Warp roles (256 threads): warp 0 = TMA producer, warp 1 = MMA issuer (one thread;
+// leader CTA only for pairs), warp 2 = TMEM allocator, warp 3 idle, warps 4..7 =
+// epilogue (TMEM lane quarters).
+//
+// CTA pair (CG = 2): each CTA loads its own 128 rows of A and its tile_n/2 columns
+// of B; both CTAs' TMA bytes are counted on the LEADER's full barrier; the leader's
+// single thread issues cta_group::2 MMAs (M = 256) whose commits are multicast to
+// the empty / tmem-full barriers of both CTAs; each CTA's epilogue drains its own
+// 128 TMEM lanes and arrives on the leader's tmem-empty barrier.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <type_traits>
+#include "consumer.cuh"
+#include "ptx.cuh"
+#include "xtc_internal.h"
+
+namespace xtc {
+
+template <bool TF32, bool CONV, int CG, bool SPLIT3>
+__global__ void __launch_bounds__(kTcThreads, 1)
+tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+               const __grid_constant__ CUtensorMap tmC, const TcParams p) {
+    constexpr int ATOM = TF32 ? 32 : 64;     // elements per 128-byte row (A's K / B's N)
+    constexpr int UMMA_K = TF32 ? 8 : 16;    // K per tcgen05.mma (32 bytes)
+    constexpr uint32_t A_ATOM_BYTES = 128 * 128;
+    constexpr int TILE_M = 128 * CG;
+
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t pad = (1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u;
+    uint8_t* smem = smem_raw + pad;
+    const int S = p.stages;
+    // [resident B (b_resident only)][A ring][B ring (unless resident)][epilogue staging][barriers]
+    const bool b_res = p.b_resident != 0;
+    uint8_t* sBres = smem;
+    uint8_t* sA = smem + (b_res ? (size_t)p.kb_total * p.b_stage_bytes : 0);
+    uint8_t* sB = sA + (size_t)S * p.a_stage_bytes;
+    // SPLIT3 (3xTF32): the lo rings (A_lo, B_lo) follow the B ring, p.lo_off bytes after their hi rings
+    uint8_t* sC = sB + (b_res ? 0 : (size_t)S * p.b_stage_bytes) + (SPLIT3 ? (size_t)p.lo_off : 0);
+    uint64_t* full = reinterpret_cast<uint64_t*>(sC + (p.buffer_c ? kTcEpiSmem : 0));
+    uint64_t* empty = full + 8;
+    uint64_t* tfull = empty + 8;
+    uint64_t* tempty = tfull + 2;
+    uint64_t* bfull = tempty + 2;            // resident B landed
+    uint64_t* split = bfull + 1;             // SPLIT3: lo parts of stage s written (warps 2 and 3)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(split + 8);
+
+    if (p.trace && blockIdx.x < kTraceCtas && threadIdx.x == 0)
+        p.trace[(size_t)blockIdx.x * kTraceSlots] = ptx::globaltimer();
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t rank = (CG == 2) ? ptx::cluster_ctarank() : 0u;
+    const int64_t cluster_id = blockIdx.x / CG;
+    const int64_t num_clusters = gridDim.x / CG;
+    const int bn_cta = p.tile_n / CG;        // B columns this CTA loads
+
+    if (warp == 0 && lane == 0) {
+        ptx::prefetch_tmap(&tmA);
+        ptx::prefetch_tmap(&tmB);
+        if (p.buffer_c) ptx::prefetch_tmap(&tmC);
+    }
+    if (warp == 1 && lane == 0) {
+        for (int s = 0; s < S; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
+        for (int a = 0; a < 2; ++a) { ptx::mbar_init(&tfull[a], 1); ptx::mbar_init(&tempty[a], 4 * CG); }
+        ptx::mbar_init(bfull, 1);
+        if constexpr (SPLIT3) for (int s = 0; s < S; ++s) ptx::mbar_init(&split[s], 2);
+        ptx::fence_mbarrier_init();
+    }
+    // Barriers first; the TMEM allocation (the first tcgen05 instruction, ~0.5-1 us on a cold
+    // SM) is then taken by warp 2 while the producers already issue the first (HBM-cold)
+    // stages.  Only the MMA issuer and the epilogue read the TMEM address: they wait on the
+    // named barrier kTmemBar, which warp 2 arrives on after the allocation.
+    if (warp == 2 && p.debug_late_alloc) {
+        ptx::tmem_alloc<CG>(tmem_slot, p.tmem_cols);
+        ptx::tmem_relinquish<CG>();
+        ptx::tc_fence_before();
+    }
+    if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
+    if (warp == 2 && p.debug_late_alloc) {
+        ptx::named_bar_arrive(ptx::kTmemBar, ptx::kTmemBarThreads);
+    } else if (warp == 2) {
+        ptx::tmem_alloc<CG>(tmem_slot, p.tmem_cols);
+        ptx::tmem_relinquish<CG>();
+        ptx::tc_fence_before();
+        ptx::named_bar_arrive(ptx::kTmemBar, ptx::kTmemBarThreads);
+    }
+    auto tmem_address = [&]() -> uint32_t {     // warps 1 and 4..7, once, before any TMEM use
+        ptx::named_bar_sync(ptx::kTmemBar, ptx::kTmemBarThreads);
+        ptx::tc_fence_after();
+        return *reinterpret_cast<volatile uint32_t*>(tmem_slot);
+    };
+    uint64_t* const trace = (p.trace && blockIdx.x < kTraceCtas) ? p.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
+    if (trace && threadIdx.x == 0) trace[1] = ptx::globaltimer();
+    int trace_k = 0;       // per-role counters (each role only touches its own slots)
+
+    if (warp == 0 || ((warp == 2 || warp == 3) && warp - 1 < p.pack_warps)) {
+        // ===================== TMA producer(s) (pack) =====================
+        // pack_warps producers (warps 0, 2, 3) share the ring: the g-th k-block of this
+        // CTA's tile sequence uses slot g % S and is issued by producer g % pack_warps.
+        {
+            const int pw = warp == 0 ? 0 : warp - 1;
+            const int P = p.pack_warps;
+            int g = 0;                    // k-blocks seen (trace index)
+            int s = 0, rr = 0;            // slot g % S, producer g % P (incremental: no divisions)
+            uint32_t use_par = 0;         // parity of (g / S)
+            bool first_round = true;      // g < S: slot never filled before
+            const uint32_t stage_bytes = p.a_stage_bytes + (b_res ? 0u : p.b_stage_bytes);
+            const int n_a = p.tile_k / ATOM;
+            const int n_b = bn_cta / ATOM;
+            if (b_res && pw == 0) {
+                // pack B once: every k-block of this CTA's B columns (single N tile, split_k 1)
+                if (ptx::elect_one()) {
+                    const uint32_t all = (uint32_t)p.kb_total * p.b_stage_bytes;
+                    uint32_t bar_c = 0;
+                    if constexpr (CG == 2) {
+                        if (rank == 0) ptx::mbar_arrive_expect_tx(bfull, 2 * all);
+                        bar_c = ptx::mapa_shared(ptx::smem_u32(bfull), 0);
+                    } else {
+                        ptx::mbar_arrive_expect_tx(bfull, all);
+                    }
+                    const int nc = bn_cta * (int)rank;
+                    for (int kb = 0; kb < p.kb_total; ++kb)
+                        if (p.b3d) {
+                            uint8_t* dst = sBres + (size_t)kb * p.b_stage_bytes;
+                            if constexpr (CG == 2) ptx::tma_load_3d_pair(&tmB, dst, bar_c, 0, kb * p.tile_k, nc / ATOM);
+                            else ptx::tma_load_3d(&tmB, dst, bfull, 0, kb * p.tile_k, nc / ATOM);
+                        } else
+                        for (int b = 0; b < n_b; ++b) {
+                            uint8_t* dst = sBres + (size_t)kb * p.b_stage_bytes + (size_t)b * p.tile_k * 128;
+                            if constexpr (CG == 2) ptx::tma_load_2d_pair(&tmB, dst, bar_c, nc + b * ATOM, kb * p.tile_k);
+                            else ptx::tma_load_2d(&tmB, dst, bfull, nc + b * ATOM, kb * p.tile_k);
+                        }
+                }
+                __syncwarp();
+            }
+            for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters) {
+                int mb, nb, ks;
+                tile_coords(p.tm, t, mb, nb, ks);
+                const int kb0 = ks * p.kb_per_split;
+                const int kb1 = min(p.kb_total, kb0 + p.kb_per_split);
+                const int m0 = mb * TILE_M + 128 * (int)rank;     // this CTA's 128 rows
+                const int n0 = nb * p.tile_n + bn_cta * (int)rank;  // this CTA's B columns
+                int wq = 0, hp = 0, nimg = 0;
+                if constexpr (CONV) {
+                    const int pq = p.cg.P * p.cg.Q;
+                    nimg = m0 / pq;
+                    const int rem = m0 - nimg * pq;
+                    const int pp = rem / p.cg.Q, qq = rem - pp * p.cg.Q;
+                    hp = pp * p.cg.sh - p.cg.ph;      // filter-window origin of pixel m0
+                    wq = qq * p.cg.sw - p.cg.pw;
+                }
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    const int cs = s;
+                    const uint32_t cpar = use_par;
+                    const bool mine = rr == pw, fresh = first_round;
+                    trace_k = g < kTraceK ? g : kTraceK;
+                    ++g;
+                    if (++rr == P) rr = 0;
+                    if (++s == S) { s = 0; use_par ^= 1u; first_round = false; }
+                    if (!mine) continue;                       // warp-uniform
+                    if (!fresh) ptx::mbar_wait(&empty[cs], cpar ^ 1u);   // first fill: the slot is free
+                    if (trace && lane == 0 && trace_k < kTraceK) trace[8 + trace_k] = ptx::globaltimer();
+                    // One lane issues while the other 31 wait at __syncwarp below: letting them
+                    // run ahead into the next try_wait would suspend the warp (divergent paths
+                    // of a warp are serialised) and throttle the issuing lane.
+                    if (ptx::elect_one()) {
+                    uint32_t bar_c = 0;
+                    uint64_t* const fb = &full[cs];
+                    if constexpr (CG == 2) {
+                        if (rank == 0) ptx::mbar_arrive_expect_tx(fb, 2 * stage_bytes);
+                        bar_c = ptx::mapa_shared(ptx::smem_u32(fb), 0);
+                    } else {
+                        ptx::mbar_arrive_expect_tx(fb, stage_bytes);
+                    }
+                    uint8_t* a_dst = sA + (size_t)cs * p.a_stage_bytes;
+                    uint8_t* b_dst = sB + (size_t)cs * p.b_stage_bytes;
+                    // 3-D maps: one TMA moves all atoms of the stage ({atom, rows, atom index} box
+                    // lands as [atom][rows][128 B], the layout the UMMA descriptors walk)
+                    const bool a_one = !CONV && p.a3d;
+                    if (a_one) {
+                        const int ka = kb * (p.tile_k / ATOM);
+                        if constexpr (CG == 2) ptx::tma_load_3d_pair(&tmA, a_dst, bar_c, 0, m0, ka);
+                        else ptx::tma_load_3d(&tmA, a_dst, fb, 0, m0, ka);
+                    }
+                    for (int a = 0; a < (a_one ? 0 : n_a); ++a) {
+                        const int kc = kb * p.tile_k + a * ATOM;
+                        if constexpr (CONV) {
+                            const int rs = kc / p.cg.C;
+                            const int c = kc - rs * p.cg.C;
+                            const int r = rs / p.cg.S;
+                            const int sx = rs - r * p.cg.S;
+                            if constexpr (CG == 2)
+                                ptx::tma_load_im2col_4d_pair(&tmA, a_dst + a * A_ATOM_BYTES, bar_c, c, wq, hp, nimg,
+                                                             (uint16_t)sx, (uint16_t)r);
+                            else
+                                ptx::tma_load_im2col_4d(&tmA, a_dst + a * A_ATOM_BYTES, fb, c, wq, hp, nimg,
+                                                        (uint16_t)sx, (uint16_t)r);
+                        } else {
+                            if constexpr (CG == 2) ptx::tma_load_2d_pair(&tmA, a_dst + a * A_ATOM_BYTES, bar_c, kc, m0);
+                            else ptx::tma_load_2d(&tmA, a_dst + a * A_ATOM_BYTES, fb, kc, m0);
+                        }
+                    }
+                    if (!b_res && p.b3d) {
+                        if constexpr (CG == 2) ptx::tma_load_3d_pair(&tmB, b_dst, bar_c, 0, kb * p.tile_k, n0 / ATOM);
+                        else ptx::tma_load_3d(&tmB, b_dst, fb, 0, kb * p.tile_k, n0 / ATOM);
+                    }
+                    for (int b = 0; b < ((b_res || p.b3d) ? 0 : n_b); ++b) {
+                        uint8_t* dst = b_dst + (size_t)b * p.tile_k * 128;
+                        if constexpr (CG == 2) ptx::tma_load_2d_pair(&tmB, dst, bar_c, n0 + b * ATOM, kb * p.tile_k);
+                        else ptx::tma_load_2d(&tmB, dst, fb, n0 + b * ATOM, kb * p.tile_k);
+                    }
+                    }   // elected lane
+                    __syncwarp();
+                }
+            }
+        }
+    } else if (SPLIT3 && (warp == 2 || warp == 3)) {
+        // ===================== 3xTF32 split: lo = a - tf32(a) =====================
+        // kind::tf32 reads the hi part of an fp32 operand (the low 13 mantissa bits are
+        // ignored); the lo part is written at the same offsets of the lo rings, so it
+        // inherits the swizzled layout.  Warps 2 and 3 share each stage's A and B tiles.
+        int s = 0;
+        uint32_t ph = 0;
+        const uint32_t lo_off = p.lo_off;
+        auto split_buf = [&](uint8_t* hi, uint32_t bytes) {
+            const uint4* src = reinterpret_cast<const uint4*>(hi);
+            uint4* dst = reinterpret_cast<uint4*>(hi + lo_off);
+            for (uint32_t i = (uint32_t)((warp - 2) * 32 + lane); i < bytes / 16; i += 64) {
+                const uint4 x = src[i];
+                uint4 l;
+                l.x = __float_as_uint(__uint_as_float(x.x) - __uint_as_float(x.x & 0xFFFFE000u));
+                l.y = __float_as_uint(__uint_as_float(x.y) - __uint_as_float(x.y & 0xFFFFE000u));
+                l.z = __float_as_uint(__uint_as_float(x.z) - __uint_as_float(x.z & 0xFFFFE000u));
+                l.w = __float_as_uint(__uint_as_float(x.w) - __uint_as_float(x.w & 0xFFFFE000u));
+                dst[i] = l;
+            }
+        };
+        for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters) {
+            int mb, nb, ks;
+            tile_coords(p.tm, t, mb, nb, ks);
+            const int kb0 = ks * p.kb_per_split;
+            const int kb1 = min(p.kb_total, kb0 + p.kb_per_split);
+            for (int kb = kb0; kb < kb1; ++kb) {
+                ptx::mbar_wait(&full[s], ph);
+                split_buf(sA + (size_t)s * p.a_stage_bytes, p.a_stage_bytes);
+                split_buf(sB + (size_t)s * p.b_stage_bytes, p.b_stage_bytes);
+                ptx::fence_proxy_async_smem();       // generic-proxy stores -> visible to the tensor core
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&split[s]);
+                if (++s == S) { s = 0; ph ^= 1u; }
+            }
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer (contraction) =====================
+        const uint32_t tmem_base = tmem_address();
+        // One elected lane runs each tile's whole k-loop (stage waits, UMMAs, commits); the
+        // warp reconverges once per tile.  Loop bounds and strides are pinned in registers
+        // and the atoms of a stage are a compile-time count (NA), so a stage is straight-line
+        // code: with short UMMAs (N = 64: ~48 cycles) any per-stage branch or constant-bank
+        // reload shows up directly in the tile time (profiles/r01_conv_halo_ab.txt).
+        if (rank == 0) {
+            const uint32_t b_lbo = (uint32_t)p.tile_k * 128u;   // stride between 128-byte N blocks of B
+            // Descriptors of stage 0; stage s and each k-step only advance the 14-bit
+            // start-address field (address >> 4), which never carries out of the field
+            // because the whole SMEM window is < 256 KB.
+            const uint64_t adesc0 = ptx::smem_desc_sw128(ptx::smem_u32(sA), 16, 1024);
+            // B is MN-major: LBO = stride between 128-byte N blocks, SBO = stride between
+            // K-row groups (8 rows of 128 B for SW128; 4 rows for tf32's SW128_BASE32B)
+            uint8_t* const b_base_ptr = b_res ? sBres : sB;
+            const uint64_t bdesc0 = TF32 ? ptx::smem_desc_sw128(ptx::smem_u32(b_base_ptr), b_lbo, 512, 1)
+                                         : ptx::smem_desc_sw128(ptx::smem_u32(b_base_ptr), b_lbo, 1024, 2);
+            const uint32_t a_stage16 = ptx::pin(p.a_stage_bytes >> 4), b_stage16 = ptx::pin(p.b_stage_bytes >> 4);
+            const uint32_t idesc = ptx::pin(p.idesc);
+            const int Sring = ptx::pin(S), accb = ptx::pin(p.acc_buffers), tile_n = ptx::pin(p.tile_n);
+            const int kb_per = ptx::pin(p.kb_per_split), kb_tot = ptx::pin(p.kb_total);
+            const uint32_t b_res_u = ptx::pin((uint32_t)(b_res ? 1 : 0));
+            const uint32_t lo16 = ptx::pin(p.lo_off >> 4);     // SPLIT3: hi stage -> lo stage (16-byte units)
+            if (b_res) ptx::mbar_wait(bfull, 0);     // resident B has landed (in both CTAs for a pair)
+            // NA > 0: atoms per stage known at compile time; NA == 0: none (diagnostics);
+            // NA < 0: runtime count n_a (other tile_k, and the traced variant)
+            auto mma_loop = [&](auto na_c, auto trace_c) {
+                constexpr int NA = decltype(na_c)::value;
+                constexpr bool TR = decltype(trace_c)::value;
+                const int n_a = NA >= 0 ? NA : ptx::pin(p.tile_k / ATOM);
+                int s = 0, acc = 0, tk = 0;
+                uint32_t ph = 0, aph = 0;
+                for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters) {
+                    int mb, nb, ks;
+                    tile_coords(p.tm, t, mb, nb, ks);
+                    const int kb0 = ks * kb_per;
+                    const int kb1 = min(kb_tot, kb0 + kb_per);
+                    ptx::mbar_wait(&tempty[acc], aph ^ 1);
+                    ptx::tc_fence_after();
+                    if (ptx::elect_one()) {
+                        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * tile_n);
+                        int s1 = s, tk1 = tk;
+                        uint32_t ph1 = ph;
+                        for (int kb = kb0; kb < kb1; ++kb) {
+                            ptx::mbar_wait(&full[s1], ph1);
+                            if constexpr (SPLIT3) ptx::mbar_wait(&split[s1], ph1);   // lo parts written
+                            if constexpr (TR) {
+                                if (tk1 < kTraceK) trace[8 + kTraceK + tk1] = ptx::globaltimer();
+                                ++tk1;
+                            }
+                            ptx::tc_fence_after();
+                            const uint64_t ad = adesc0 + (uint64_t)((uint32_t)s1 * a_stage16);
+                            const uint64_t bd = bdesc0 + (uint64_t)((b_res_u ? (uint32_t)kb : (uint32_t)s1) * b_stage16);
+                            const uint32_t acc0 = kb > kb0 ? 1u : 0u;
+                            auto pass = [&](uint64_t ad_, uint64_t bd_, uint32_t first) {
+#pragma unroll
+                                for (int a = 0; a < (NA >= 0 ? NA : n_a); ++a) {
+#pragma unroll
+                                    for (int kk = 0; kk < ATOM / UMMA_K; ++kk) {
+                                        const uint32_t krow = a * ATOM + kk * UMMA_K;
+                                        ptx::umma<TF32, CG>(d_tmem, ad_ + (uint64_t)((a * A_ATOM_BYTES + kk * 32) >> 4),
+                                                            bd_ + (uint64_t)(krow * 8), idesc,
+                                                            (a > 0 || kk > 0) ? 1u : first);
+                                    }
+                                }
+                            };
+                            if constexpr (SPLIT3) {
+                                // small terms first: hi*lo + lo*hi, then hi*hi
+                                pass(ad, bd + (uint64_t)lo16, acc0);
+                                pass(ad + (uint64_t)lo16, bd, 1u);
+                                pass(ad, bd, 1u);
+                            } else {
+                                pass(ad, bd, acc0);
+                            }
+                            ptx::umma_commit<CG>(&empty[s1]);   // frees the SMEM slot(s) when these MMAs finish
+                            if (++s1 == Sring) { s1 = 0; ph1 ^= 1u; }
+                        }
+                        ptx::umma_commit<CG>(&tfull[acc]);      // accumulator ready for the epilogue(s)
+                    }
+                    __syncwarp();
+                    for (int kb = kb0; kb < kb1; ++kb)           // every lane tracks the ring position
+                        if (++s == Sring) { s = 0; ph ^= 1u; }
+                    if constexpr (TR) tk += kb1 - kb0;
+                    if (++acc == accb) { acc = 0; aph ^= 1u; }
+                }
+            };
+            using T0 = std::integral_constant<bool, false>;
+            using T1 = std::integral_constant<bool, true>;
+            const int n_a = p.tile_k / ATOM;
+            if (trace) mma_loop(std::integral_constant<int, -1>{}, T1{});
+            else if (p.debug_skip_mma) mma_loop(std::integral_constant<int, 0>{}, T0{});
+            else if (n_a == 1) mma_loop(std::integral_constant<int, 1>{}, T0{});
+            else if (n_a == 2) mma_loop(std::integral_constant<int, 2>{}, T0{});
+            else if (n_a == 4) mma_loop(std::integral_constant<int, 4>{}, T0{});
+            else mma_loop(std::integral_constant<int, -1>{}, T0{});
+        }
+    } else if (warp >= 4) {
+        // ===================== epilogue (bufferize) =====================
+        const uint32_t tmem_base = tmem_address();
+        const int q = warp & 3;                        // TMEM lanes 32q..32q+31
+        int acc = 0;
+        uint32_t aph = 0;
+        int buf = 0;
+        uint8_t* stage = sC + q * (kTcEpiStageBytes * kTcEpiBuffers);
+        if (p.n_gather && lane == 0)
+            for (int d = 0; d < p.n_gather; ++d) ptx::tmap_acquire(reinterpret_cast<const CUtensorMap*>(p.gather) + d);
+        const bool to_ws = p.split_out != 0;
+        const bool bf16_out = p.out_bf16 && !to_ws;
+        for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters) {
+            int mb, nb, ks;
+            tile_coords(p.tm, t, mb, nb, ks);
+            const int m0 = mb * TILE_M + 128 * (int)rank, n0 = nb * p.tile_n;
+            const int64_t row = (int64_t)m0 + 32 * q + lane;
+            ptx::mbar_wait(&tfull[acc], aph);
+            if (trace && warp == 4 && lane == 0 && trace_k < kTraceTiles) trace[8 + 2 * kTraceK + 2 * trace_k] = ptx::globaltimer();
+            ptx::tc_fence_after();
+            const uint32_t t_row = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * p.tile_n);
+            for (int c = 0; c < p.tile_n; c += 32) {
+                uint32_t v[32];
+                ptx::tmem_ld_32x32b_x32(t_row + c, v);
+                ptx::tmem_ld_wait();
+                if (p.cons && row < p.M) {         // fused consumer before the rounding
+                    const int64_t cc = (int64_t)n0 + c;
+                    const int nc = (int)((p.N - cc) < 32 ? (p.N - cc) : 32);
+                    // atomic split-K: C is accumulated in place, the first segment adds the bias
+                    if (nc > 0) apply_consumer32(v, p.cons, p.bias, p.C, bf16_out, row, p.ldc, cc, nc, !p.atomic,
+                                                 !p.atomic || ks == 0);
+                }
+                if (p.buffer_c) {
+                    // stage one 128-byte row per thread (swizzled), then one TMA store per warp
+                    const bool first_half = !bf16_out || ((c & 63) == 0);
+                    if (first_half) {
+                        if (lane == 0) ptx::bulk_wait_read<1>();
+                        __syncwarp();
+                    }
+                    uint8_t* rowp = stage + buf * kTcEpiStageBytes + lane * 128;
+                    if (bf16_out) {
+                        const int cbase = (c & 63) ? 4 : 0;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            uint4 w;
+                            w.x = ptx::pack_bf16x2(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1]));
+                            w.y = ptx::pack_bf16x2(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3]));
+                            w.z = ptx::pack_bf16x2(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5]));
+                            w.w = ptx::pack_bf16x2(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7]));
+                            const int phys = (cbase + j) ^ (lane & 7);
+                            *reinterpret_cast<uint4*>(rowp + phys * 16) = w;
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            uint4 w = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                            const int phys = j ^ (lane & 7);
+                            *reinterpret_cast<uint4*>(rowp + phys * 16) = w;
+                        }
+                    }
+                    const bool last_half = !bf16_out || ((c & 63) == 32) || (c + 32 >= p.tile_n);
+                    if (last_half) {
+                        ptx::fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            const int col = bf16_out ? (n0 + (c & ~63)) : (n0 + c);
+                            if (p.n_gather) {
+                                // fused all-gather: the staged chunk goes to every destination
+                                // (this rank's C and its peers'), one bulk group for all
+                                const CUtensorMap* gm = reinterpret_cast<const CUtensorMap*>(p.gather);
+                                for (int d = 0; d < p.n_gather; ++d)
+                                    ptx::tma_store_3d(gm + d, stage + buf * kTcEpiStageBytes, col,
+                                                      p.gather_row0 + m0 + 32 * q, 0);
+                            } else {
+                                ptx::tma_store_3d(&tmC, stage + buf * kTcEpiStageBytes, col, m0 + 32 * q, to_ws ? ks : 0);
+                            }
+                            ptx::bulk_commit();
+                        }
+                        buf ^= 1;
+                    }
+                } else if (row < p.M) {
+                    const int64_t col0 = (int64_t)n0 + c;
+                    const int ncols = (int)((p.N - col0) < 32 ? (p.N - col0) : 32);
+                    if (ncols > 0) {
+                        if (to_ws) {
+                            float* dst = p.Wk + ((int64_t)ks * p.M + row) * p.ws_ld + col0;
+                            if (ncols == 32) {
+#pragma unroll
+                                for (int j = 0; j < 8; ++j)
+                                    reinterpret_cast<uint4*>(dst)[j] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                            } else {
+                                for (int j = 0; j < ncols; ++j) dst[j] = __uint_as_float(v[j]);
+                            }
+                        } else if (p.atomic) {
+                            float* dst = reinterpret_cast<float*>(p.C) + row * p.ldc + col0;
+                            for (int j = 0; j < ncols; ++j) atomicAdd(dst + j, __uint_as_float(v[j]));
+                        } else if (bf16_out) {
+                            uint16_t* dst = reinterpret_cast<uint16_t*>(p.C) + row * p.ldc + col0;
+                            if (ncols == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+#pragma unroll
+                                for (int j = 0; j < 4; ++j) {
+                                    uint4 w;
+                                    w.x = ptx::pack_bf16x2(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1]));
+                                    w.y = ptx::pack_bf16x2(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3]));
+                                    w.z = ptx::pack_bf16x2(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5]));
+                                    w.w = ptx::pack_bf16x2(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7]));
+                                    reinterpret_cast<uint4*>(dst)[j] = w;
+                                }
+                            } else {
+                                for (int j = 0; j < ncols; ++j)
+                                    dst[j] = (uint16_t)(ptx::pack_bf16x2(__uint_as_float(v[j]), 0.f) & 0xFFFFu);
+                            }
+                        } else {
+                            float* dst = reinterpret_cast<float*>(p.C) + row * p.ldc + col0;
+                            if (ncols == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+#pragma unroll
+                                for (int j = 0; j < 8; ++j)
+                                    reinterpret_cast<uint4*>(dst)[j] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                            } else {
+                                for (int j = 0; j < ncols; ++j) dst[j] = __uint_as_float(v[j]);
+                            }
+                        }
+                    }
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (trace && warp == 4 && lane == 0 && trace_k < kTraceTiles) trace[8 + 2 * kTraceK + 2 * trace_k++ + 1] = ptx::globaltimer();
+            if (lane == 0) {                           // TMEM buffer free for the next tile
+                if constexpr (CG == 2) ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&tempty[acc]), 0));
+                else ptx::mbar_arrive(&tempty[acc]);
+            }
+            if (++acc == p.acc_buffers) { acc = 0; aph ^= 1; }
+        }
+        if (p.buffer_c && lane == 0) ptx::bulk_wait<0>();
+    }
+
+    ptx::tc_fence_before();
+    if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
+    if (trace && threadIdx.x == 0) trace[2] = ptx::globaltimer();
+    if (warp == 2) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<CG>(*reinterpret_cast<volatile uint32_t*>(tmem_slot), p.tmem_cols);
+    }
+}
+
+// ------------------------------------------------------------------ launch --
+template <bool TF32, bool CONV, int CG, bool SPLIT3>
+cudaError_t launch_tc_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
+                               const TcParams& p, int grid, int smem, cudaStream_t st) {
+    auto k = tc_gemm_kernel<TF32, CONV, CG, SPLIT3>;
+    cudaError_t e = ensure_smem_attr(k, smem);
+    if (e != cudaSuccess) return e;
+    if constexpr (CG == 1) {
+        k<<<grid, kTcThreads, smem, st>>>(a, b, c, p);
+    } else {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(kTcThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = CG;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, k, a, b, c, p);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaGetLastError();
+}
+
+// The variants are instantiated in their own translation units (gemm_tc_*.cu) so that
+// nvcc compiles them in parallel; gemm_tc.cu only dispatches.
+#define XTC_TC_VARIANT(TF32, CONV, CG, SPLIT3)                                                          \
+    template cudaError_t launch_tc_t<TF32, CONV, CG, SPLIT3>(const CUtensorMap&, const CUtensorMap&,   \
+                                                             const CUtensorMap&, const TcParams&, int, \
+                                                             int, cudaStream_t);
+#define XTC_TC_EXTERN(TF32, CONV, CG, SPLIT3) extern XTC_TC_VARIANT(TF32, CONV, CG, SPLIT3)
+
+}  // namespace xtc

@@ -1,0 +1,9 @@
+// gemm_tc_conv_bf16.cu -- instantiation of tc_gemm_kernel variants (see gemm_tc.cuh)
+#include "gemm_tc.cuh"
+
+namespace xtc {
+
+XTC_TC_VARIANT(false, true, 1, false)
+XTC_TC_VARIANT(false, true, 2, false)
+
+}  // namespace xtc

@@ -1,0 +1,9 @@
+// gemm_tc_mm_tf32.cu -- instantiation of tc_gemm_kernel variants (see gemm_tc.cuh)
+#include "gemm_tc.cuh"
+
+namespace xtc {
+
+XTC_TC_VARIANT(true, false, 1, false)
+XTC_TC_VARIANT(true, false, 2, false)
+
+}  // namespace xtc

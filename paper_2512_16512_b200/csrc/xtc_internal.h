@@ -164,6 +164,10 @@ struct TcParams {
     // [cta][kTraceSlots]: slot 0 kernel entry, 1 setup done; producer issue of k-block i at
     // 8+i, MMA full-wait done at 8+kTraceK+i, epilogue tile j start/end at 8+2kTraceK+2j(+1).
     uint64_t* trace;
+    // xtc_run_gather (fused all-gather): n_gather CUtensorMaps in device memory, one per
+    // destination ([dest_rows][N] each); output tile rows land at gather_row0 + row
+    const void* gather;
+    int32_t n_gather, gather_row0;
 };
 constexpr int kTraceCtas = 160;          // >= #SMs: the whole persistent grid
 constexpr int kTraceK = 96;

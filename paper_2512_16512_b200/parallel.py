@@ -8,6 +8,9 @@ Only the two shardings the path has are implemented:
   2. M-sharding of a large GEMM (conv: batch sharding): rank r computes the
      contiguous output rows [r0, r1); B is replicated by regenerating it from
      the seed (no broadcast); C is assembled by all_gather_into_tensor.
+     With the gather FUSED into the GEMM (xtc_run_gather), C is a
+     symmetric-memory buffer on every rank and each rank's epilogue TMA-stores its
+     tiles straight into every peer's copy over NVLink (no NCCL call on the data path).
 There is no tensor/pipeline/sequence parallelism: the operator has none.
 """
 from __future__ import annotations
@@ -94,4 +97,47 @@ def gather_rows(c_shard: torch.Tensor, m_total: int, group=None, out: torch.Tens
     if out is None:
         out = torch.empty((m_total,) + tuple(c_shard.shape[1:]), dtype=c_shard.dtype, device=c_shard.device)
     _all_gather(out, c_shard.contiguous(), group)
+    return out
+
+
+def rotated_destinations(ptrs: Sequence[int], rank: int) -> List[int]:
+    """Destination order of the fused all-gather for `rank`: its own buffer first, then the
+    peers r+1, r+2, ... (mod W), so at any moment the W ranks' stores target W different
+    GPUs instead of all starting on rank 0's buffer."""
+    w = len(ptrs)
+    if not 0 <= rank < w:
+        raise ValueError("rank out of range")
+    return [int(ptrs[(rank + i) % w]) for i in range(w)]
+
+
+class SymmetricOutput:
+    """C as a symmetric-memory tensor (torch.distributed._symmetric_memory: every rank's buffer
+    mapped into every peer's address space over NVLink).  ``dests`` are the device pointers
+    xtc_run_gather stores to (this rank's first); ``barrier()`` (on the current stream) orders
+    every rank's stores before any later read."""
+
+    def __init__(self, shape, dtype, device, group=None):
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+        group = group or dist.group.WORLD
+        self.tensor = symm.empty(*shape, dtype=dtype, device=device)
+        self.handle = symm.rendezvous(self.tensor, group)
+        self.dests = rotated_destinations(list(self.handle.buffer_ptrs), dist.get_rank(group))
+
+    def barrier(self):
+        self.handle.barrier(channel=0)
+
+
+def checksum_rows(c: torch.Tensor) -> torch.Tensor:
+    """Order-sensitive integer checksum of a 2-D tensor's bits (sum, and sum weighted by the
+    row index), computed in row blocks; equal on every rank iff the gathered copies agree
+    (up to checksum collisions)."""
+    bits = c.view(torch.int16 if c.element_size() == 2 else torch.int32)
+    out = torch.zeros(2, dtype=torch.int64, device=c.device)
+    step = max(1, (1 << 24) // max(1, c.shape[1]))
+    for r0 in range(0, c.shape[0], step):
+        x = bits[r0:r0 + step].to(torch.int64)
+        rows = torch.arange(r0 + 1, r0 + 1 + x.shape[0], device=c.device, dtype=torch.int64)[:, None]
+        out[0] += x.sum()
+        out[1] += (x * rows).sum()
     return out

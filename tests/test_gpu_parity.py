@@ -659,3 +659,75 @@ def test_consumer_bias_pointer_required_and_sweep_with_accumulate():
                              tc(tile_n=128, split_k=2, split_k_mode=1, buffer_c=0, fuse=1)], a, b, c2,
                             xtc.measure_cfg(warmup=1, repeats=2, validate=1, exact=1), bias=bias)
     assert [r.valid for r in recs] == [1, 1, 1], [r.as_dict() for r in recs]
+
+
+# ------------------------------------- fused all-gather (xtc_run_gather, N2) --
+GATHER_CASES = [
+    # (schedule, W virtual ranks, out dtype, N)
+    (dict(tile_n=128, stages=4, persistent=1, acc_buffers=2), 4, "bf16", 384),
+    (dict(tile_m=256, cluster_m=2, tile_n=256, tile_k=128, stages=3, persistent=1, acc_buffers=2,
+          raster_group=16), 4, "bf16", 512),
+    (dict(tile_n=64, stages=6), 8, "f32", 328),          # ragged N: every destination's store is clipped
+    (dict(tile_n=256, stages=3, acc_buffers=2, persistent=1), 1, "bf16", 256),
+]
+
+
+@pytest.mark.parametrize("sch,W,out,N", GATHER_CASES)
+@pytest.mark.parametrize("mode", [MODE_INT, MODE_UNIFORM])
+def test_run_gather_every_destination_holds_the_gathered_matmul(sch, W, out, N, mode):
+    """The M-sharded matmul with its all-gather fused into the epilogue, W ranks simulated on one
+    GPU: rank r's op computes rows [r*M/W, (r+1)*M/W) and TMA-stores each tile to all W
+    destinations.  Afterwards EVERY destination must equal the oracle's full C (bit-exact on
+    integers, <= 5e-3 of D on uniform data) -- the all-gather's result."""
+    M, K = 1024, 320
+    Ms = M // W
+    a = dev_tensor((M, K), "bf16", 11, mode)
+    b = dev_tensor((K, N), "bf16", 12, mode)
+    dests = [torch.full((M, N), float("nan"), dtype=TORCH_DT[out], device="cuda:0") for _ in range(W)]
+    ptrs = [d.data_ptr() for d in dests]
+    for r in range(W):
+        op = xtc.Op(xtc.matmul_desc(Ms, N, K, "bf16", out)).apply(tc(**sch))
+        op.run_gather(a[r * Ms:(r + 1) * Ms], b, ptrs, r * Ms, M)
+    torch.cuda.synchronize()
+    O, D = oracle_matmul(M, N, K, "bf16", mode, 11, 12)
+    for d in dests:
+        check_against_oracle(d, O, D, out, exact=(mode == MODE_INT), tol=5e-3)
+
+
+def test_run_gather_fused_relu_and_rerun_with_new_destinations():
+    """A fused consumer (relu) applies before the multi-destination store; a second call with
+    other destination pointers re-encodes the destination maps."""
+    M, N, K, W = 512, 256, 192, 2
+    Ms = M // W
+    a = dev_tensor((M, K), "bf16", 21, MODE_INT)
+    b = dev_tensor((K, N), "bf16", 22, MODE_INT)
+    ops = [xtc.Op(xtc.matmul_desc(Ms, N, K, "bf16", "bf16", consumer="relu")).apply(tc(tile_n=128, fuse=1))
+           for _ in range(W)]
+    O, D = oracle_matmul(M, N, K, "bf16", MODE_INT, 21, 22)
+    import oracle
+    O = oracle.relu(O)
+    for _ in range(2):
+        dests = [torch.full((M, N), float("nan"), dtype=torch.bfloat16, device="cuda:0") for _ in range(W)]
+        for r in range(W):
+            ops[r].run_gather(a[r * Ms:(r + 1) * Ms], b, [d.data_ptr() for d in dests], r * Ms, M)
+        torch.cuda.synchronize()
+        for d in dests:
+            check_against_oracle(d, O, D, "bf16", exact=True, tol=0)
+
+
+def test_run_gather_rejects_unsupported_schedules_and_ranges():
+    a = dev_tensor((256, 128), "bf16", 1, MODE_INT)
+    b = dev_tensor((128, 128), "bf16", 2, MODE_INT)
+    c = torch.zeros((512, 128), dtype=torch.bfloat16, device="cuda:0")
+    ok = xtc.Op(xtc.matmul_desc(256, 128, 128)).apply(tc(tile_n=128))
+    for bad in (dict(tile_n=128, split_k=2), dict(tile_n=128, buffer_c=0)):
+        op = xtc.Op(xtc.matmul_desc(256, 128, 128)).apply(tc(**bad))
+        with pytest.raises(xtc.XtcError):
+            op.run_gather(a, b, [c.data_ptr()], 0, 512)
+    with pytest.raises(xtc.XtcError):                       # rows past the destination
+        ok.run_gather(a, b, [c.data_ptr()], 384, 512)
+    with pytest.raises(xtc.XtcError):                       # more than 8 destinations
+        ok.run_gather(a, b, [c.data_ptr()] * 9, 0, 512)
+    ragged = xtc.Op(xtc.matmul_desc(200, 128, 128)).apply(tc(tile_n=128))
+    with pytest.raises(xtc.XtcError):                       # ragged shard would spill into a neighbour
+        ragged.run_gather(a[:200], b, [c.data_ptr()], 0, 512)

@@ -10,7 +10,8 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_2512_16512_b200.parallel import (REC_FIELDS, gather_records, gather_rows, pack_records,
-                                            rank_candidates, shard_rows, unpack_gathered)
+                                            rank_candidates, rotated_destinations, shard_rows, unpack_gathered,
+                                            checksum_rows)
 
 
 def _free_port():
@@ -58,6 +59,19 @@ def _worker(rank, world, port, q):
             gather_rows(C_bc[j * Mc:(j + 1) * Mc].contiguous(), world * Mc,
                         out=full_bc[j * world * Mc:(j + 1) * world * Mc])
         assert np.array_equal(full_bc.numpy(), want)
+        # 4) fused gather (xtc_run_gather, bench.py --gather fused): each rank stores to its own
+        #    buffer first, then to the peers in rotation; the consistency check compares
+        #    whole-buffer checksums across ranks
+        order = rotated_destinations([100 + r for r in range(world)], rank)
+        assert order[0] == 100 + rank and sorted(order) == [100 + r for r in range(world)]
+        c32 = torch.from_numpy(want.astype(np.float32))
+        cs = checksum_rows(c32)
+        cs_all = [torch.empty_like(cs) for _ in range(world)]
+        dist.all_gather(cs_all, cs)
+        assert all(torch.equal(x, cs_all[0]) for x in cs_all)
+        swapped = c32.clone()
+        swapped[[0, 1]] = swapped[[1, 0]]
+        assert not torch.equal(checksum_rows(swapped), cs)
         q.put((rank, "ok"))
     except Exception as e:  # pragma: no cover
         q.put((rank, repr(e)))
