@@ -295,6 +295,8 @@ def main_xtc(args):
     rehearsal = os.environ.get("XTC_BENCH_DIST", "") == "gloo-shared"
     if rehearsal:
         local = 0
+        # the ranks share device 0: let symmetric memory map one device's buffers twice
+        os.environ.setdefault("TORCH_SYMM_MEM_ALLOW_OVERLAPPING_DEVICES", "1")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -323,7 +325,7 @@ def main_xtc(args):
     # If the symmetric-memory rendezvous is unavailable the chunked NCCL overlap is used instead
     # (another GPU path, reported in config.parallelism).
     fused, fused_note = None, None
-    if world > 1 and not rehearsal and args.gather == "fused":
+    if world > 1 and args.gather == "fused":
         try:
             from paper_2512_16512_b200.parallel import SymmetricOutput
             fused = SymmetricOutput((M, N), torch.bfloat16, dev)

@@ -418,11 +418,21 @@ def test_bench_two_rank_rehearsal_on_one_gpu(tmp_path):
     assert len(lines) == 1, out.stdout[-2000:]
     rec = json.loads(lines[0])
     assert rec["n_gpus"] == 2 and rec["validation"]["valid"] == 1 and rec["value"] > 0
+    # the default N>1 gather is the fused one (xtc_run_gather into symmetric memory)
+    assert "fused into the GEMM epilogue" in rec["config"]["parallelism"], rec["config"]["parallelism"]
     assert rec["validation"]["valid_all_ranks"] == 1 and rec["validation"]["gather_consistent_all_ranks"] == 1
     sw = rec["extras"]["sweep_1024_bf16_sharded"]
     assert sw["ranks"] == 2 and sw["candidates"] == 32 and sw["valid"] + sw["invalid"] == 32
     cv = rec["extras"]["conv_L56_batch_sharded"]
     assert cv["ranks"] == 2 and cv["images_per_rank"] == 16 and cv["valid_all_ranks"] == 1 and cv["step_us"] > 0
+    # the NCCL-form (chunked all-gather overlap) path
+    cmd2 = [x if x != "--master-port=29533" else "--master-port=29534" for x in cmd[:-2]]
+    out = subprocess.run(cmd2 + ["--no-extras", "--gather", "nccl"], cwd=root, env=env, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    rec = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][0])
+    assert "block-cyclic chunks" in rec["config"]["parallelism"]
+    assert rec["validation"]["valid_all_ranks"] == 1 and rec["validation"]["gather_consistent_all_ranks"] == 1
 
 
 @pytest.mark.parametrize("pw", [2, 3])
