@@ -118,6 +118,11 @@ typedef enum { XTC_SPLITK_ORDERED = 0, XTC_SPLITK_ATOMIC = 1 } xtc_splitk_mode;
  * vectorize    vector_n               : SIMT: 1 or 4 (float4 SMEM/global access along N); tcgen05: 0
  * parallelize  persistent             : 0 = one CTA per tile, 1 = #SM CTAs loop over tiles
  *                          cluster_m              : tcgen05: 1, or 2 = CTA pair (cta_group::2, tile_m = 256)
+ *                          cluster_n              : tcgen05 matmul (cluster_m 1): 0/1, or 2 / 4 CTAs on adjacent
+ *                                                   N tiles of one M tile form a cluster; each TMA-loads
+ *                                                   1/cluster_n of the rows of every A stage and multicasts
+ *                                                   it to all of them (A leaves L2 once per cluster);
+ *                                                   needs tiles_n % cluster_n == 0, b_resident 0
  * split        split_k, split_k_mode  : K split into split_k contiguous segments + reduction
  *                          split_n_at             : 0, or the J split point s: [0,s) main root,
  *                                                   [s,N) remainder root on the SIMT engine (Fig.3/4)
@@ -157,7 +162,7 @@ typedef struct {
     int32_t b_resident;
     int32_t fuse;
     int32_t pack_halo;
-    int32_t reserved[1];
+    int32_t cluster_n;
 } xtc_schedule;
 
 /* What the planner derived for a legal schedule (for reports and tests). */

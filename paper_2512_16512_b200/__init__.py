@@ -56,11 +56,11 @@ class xtc_op_desc(Structure):
 SCHEDULE_FIELDS = ["engine", "tile_m", "tile_n", "tile_k", "inner_m", "inner_n", "order", "raster_group",
                    "unroll_k", "vector_n", "stages", "swizzle", "buffer_c", "acc_buffers", "split_k",
                    "split_k_mode", "cluster_m", "persistent", "split_n_at", "pack_warps", "b_resident", "fuse",
-                   "pack_halo"]
+                   "pack_halo", "cluster_n"]
 
 
 class xtc_schedule(Structure):
-    _fields_ = [(f, c_int32) for f in SCHEDULE_FIELDS] + [("reserved", c_int32 * 1)]
+    _fields_ = [(f, c_int32) for f in SCHEDULE_FIELDS]
 
     def as_dict(self):
         return {f: int(getattr(self, f)) for f in SCHEDULE_FIELDS}

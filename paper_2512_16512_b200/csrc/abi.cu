@@ -449,7 +449,9 @@ static xtc_status encode_maps(xtc_op op, const void* A, const void* B, void* C) 
         // A: [M][K] K-major.  3-D view {atom, M, K/atom} (strides lda, 128 B): one box
         // {atom, 128, tile_k/atom} per stage lands as [k-atom][row][128 B] (needs K % atom == 0).
         const int64_t lda = d.lda ? d.lda : d.k;
-        if (allow3d && p.K % atom == 0) {
+        // cluster_n: each CTA loads a 128/cluster_n-row slice of every A atom (2-D boxes)
+        const int a_rows = p.cluster_n > 1 ? 128 / p.cluster_n : 128;
+        if (allow3d && p.K % atom == 0 && p.cluster_n <= 1) {
             cuuint64_t dims[3] = {(cuuint64_t)atom, (cuuint64_t)p.M, (cuuint64_t)(p.K / atom)};
             cuuint64_t strides[2] = {(cuuint64_t)(lda * es), (cuuint64_t)(atom * es)};
             cuuint32_t box[3] = {(cuuint32_t)atom, 128, (cuuint32_t)(tile_k / atom)};
@@ -462,7 +464,7 @@ static xtc_status encode_maps(xtc_op op, const void* A, const void* B, void* C) 
         if (!op->a3d) {
             cuuint64_t dims[2] = {(cuuint64_t)p.K, (cuuint64_t)p.M};
             cuuint64_t strides[1] = {(cuuint64_t)(lda * es)};
-            cuuint32_t box[2] = {(cuuint32_t)atom, 128};
+            cuuint32_t box[2] = {(cuuint32_t)atom, (cuuint32_t)a_rows};
             cuuint32_t estr[2] = {1, 1};
             r = g_encode_tiled(&op->tmA, in_t, 2, const_cast<void*>(A), dims, strides, box, estr,
                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -564,7 +566,8 @@ static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cud
         const int64_t rows = p.M;
         CU_TRY(cudaMemset2DAsync(C, ldc * 4, 0, p.N * 4, rows, st), "memset C (atomic split-K)");
     }
-    TileMap tm{p.tiles_m, p.tiles_n, p.split_k, p.sch.order, p.sch.raster_group};
+    // cluster_n: the tile map walks cluster tiles (cluster_n adjacent N tiles of one M tile)
+    TileMap tm{p.tiles_m, p.tiles_n / (p.cluster_n > 1 ? p.cluster_n : 1), p.split_k, p.sch.order, p.sch.raster_group};
     if (p.engine == XTC_ENGINE_SIMT) {
         SimtParams sp;
         memset(&sp, 0, sizeof sp);
@@ -634,6 +637,7 @@ static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cud
         tp.b_stage_bytes = (uint32_t)(p.sch.tile_k * (p.sch.tile_n / p.cta_group) * es);
         tp.lo_off = p.split3 ? (uint32_t)(p.sch.stages * (tp.a_stage_bytes + tp.b_stage_bytes)) : 0u;
         tp.cg = conv_geom(d);
+        tp.cn = p.cluster_n > 1 ? p.cluster_n : 1;
         if (ga) {
             tp.gather = ga->maps;
             tp.n_gather = ga->n;

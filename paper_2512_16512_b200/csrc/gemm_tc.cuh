@@ -69,8 +69,14 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const uint32_t rank = (CG == 2) ? ptx::cluster_ctarank() : 0u;
-    const int64_t cluster_id = blockIdx.x / CG;
-    const int64_t num_clusters = gridDim.x / CG;
+    // cluster_n (CG = 1): cn CTAs on adjacent N tiles of one M tile; CTA crank loads rows
+    // [crank*128/cn, (crank+1)*128/cn) of every A stage and multicasts them to all cn CTAs
+    const int cn = CG == 1 ? p.cn : 1;
+    const bool mcast = cn > 1;
+    const uint32_t crank = mcast ? ptx::cluster_ctarank() : 0u;
+    const uint16_t cmask = (uint16_t)((1u << cn) - 1u);
+    const int64_t cluster_id = blockIdx.x / (CG * cn);
+    const int64_t num_clusters = gridDim.x / (CG * cn);
     const int bn_cta = p.tile_n / CG;        // B columns this CTA loads
 
     if (warp == 0 && lane == 0) {
@@ -79,7 +85,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         if (p.buffer_c) ptx::prefetch_tmap(&tmC);
     }
     if (warp == 1 && lane == 0) {
-        for (int s = 0; s < S; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
+        // a multicast stage is free when all cn CTAs' MMAs have consumed it (cn commit arrivals)
+        for (int s = 0; s < S; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], (uint32_t)cn); }
         for (int a = 0; a < 2; ++a) { ptx::mbar_init(&tfull[a], 1); ptx::mbar_init(&tempty[a], 4 * CG); }
         ptx::mbar_init(bfull, 1);
         if constexpr (SPLIT3) for (int s = 0; s < S; ++s) ptx::mbar_init(&split[s], 2);
@@ -94,7 +101,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         ptx::tmem_relinquish<CG>();
         ptx::tc_fence_before();
     }
-    if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
+    if (CG == 2 || mcast) ptx::cluster_sync(); else __syncthreads();
     if (warp == 2 && p.debug_late_alloc) {
         ptx::named_bar_arrive(ptx::kTmemBar, ptx::kTmemBarThreads);
     } else if (warp == 2) {
@@ -158,7 +165,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 const int kb0 = ks * p.kb_per_split;
                 const int kb1 = min(p.kb_total, kb0 + p.kb_per_split);
                 const int m0 = mb * TILE_M + 128 * (int)rank;     // this CTA's 128 rows
-                const int n0 = nb * p.tile_n + bn_cta * (int)rank;  // this CTA's B columns
+                const int n0 = (nb * cn + (int)crank) * p.tile_n + bn_cta * (int)rank;  // this CTA's B columns
                 int wq = 0, hp = 0, nimg = 0;
                 if constexpr (CONV) {
                     const int pq = p.cg.P * p.cg.Q;
@@ -196,12 +203,18 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                     // 3-D maps: one TMA moves all atoms of the stage ({atom, rows, atom index} box
                     // lands as [atom][rows][128 B], the layout the UMMA descriptors walk)
                     const bool a_one = !CONV && p.a3d;
-                    if (a_one) {
+                    if (mcast) {
+                        // this CTA's 128/cn-row slice of every A atom, into the same offset of all cn CTAs
+                        const int rows = 128 / cn;
+                        for (int a = 0; a < n_a; ++a)
+                            ptx::tma_load_2d_multicast(&tmA, a_dst + a * A_ATOM_BYTES + crank * rows * 128, fb,
+                                                       kb * p.tile_k + a * ATOM, m0 + (int)crank * rows, cmask);
+                    } else if (a_one) {
                         const int ka = kb * (p.tile_k / ATOM);
                         if constexpr (CG == 2) ptx::tma_load_3d_pair(&tmA, a_dst, bar_c, 0, m0, ka);
                         else ptx::tma_load_3d(&tmA, a_dst, fb, 0, m0, ka);
                     }
-                    for (int a = 0; a < (a_one ? 0 : n_a); ++a) {
+                    for (int a = 0; a < ((a_one || mcast) ? 0 : n_a); ++a) {
                         const int kc = kb * p.tile_k + a * ATOM;
                         if constexpr (CONV) {
                             const int rs = kc / p.cg.C;
@@ -297,9 +310,10 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             if (b_res) ptx::mbar_wait(bfull, 0);     // resident B has landed (in both CTAs for a pair)
             // NA > 0: atoms per stage known at compile time; NA == 0: none (diagnostics);
             // NA < 0: runtime count n_a (other tile_k, and the traced variant)
-            auto mma_loop = [&](auto na_c, auto trace_c) {
+            auto mma_loop = [&](auto na_c, auto trace_c, auto mc_c) {
                 constexpr int NA = decltype(na_c)::value;
                 constexpr bool TR = decltype(trace_c)::value;
+                constexpr bool MC = decltype(mc_c)::value;   // cluster_n: stage release multicast to the cluster
                 const int n_a = NA >= 0 ? NA : ptx::pin(p.tile_k / ATOM);
                 int s = 0, acc = 0, tk = 0;
                 uint32_t ph = 0, aph = 0;
@@ -345,7 +359,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                             } else {
                                 pass(ad, bd, acc0);
                             }
-                            ptx::umma_commit<CG>(&empty[s1]);   // frees the SMEM slot(s) when these MMAs finish
+                            if constexpr (MC) ptx::umma_commit_multicast(&empty[s1], cmask);   // ... in every CTA
+                            else ptx::umma_commit<CG>(&empty[s1]);   // frees the SMEM slot(s) when these MMAs finish
                             if (++s1 == Sring) { s1 = 0; ph1 ^= 1u; }
                         }
                         ptx::umma_commit<CG>(&tfull[acc]);      // accumulator ready for the epilogue(s)
@@ -360,12 +375,23 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             using T0 = std::integral_constant<bool, false>;
             using T1 = std::integral_constant<bool, true>;
             const int n_a = p.tile_k / ATOM;
-            if (trace) mma_loop(std::integral_constant<int, -1>{}, T1{});
-            else if (p.debug_skip_mma) mma_loop(std::integral_constant<int, 0>{}, T0{});
-            else if (n_a == 1) mma_loop(std::integral_constant<int, 1>{}, T0{});
-            else if (n_a == 2) mma_loop(std::integral_constant<int, 2>{}, T0{});
-            else if (n_a == 4) mma_loop(std::integral_constant<int, 4>{}, T0{});
-            else mma_loop(std::integral_constant<int, -1>{}, T0{});
+            bool issued = false;
+            if constexpr (CG == 1 && !CONV && !SPLIT3) {
+                if (mcast) {
+                    if (trace) mma_loop(std::integral_constant<int, -1>{}, T1{}, T1{});
+                    else if (n_a == 1) mma_loop(std::integral_constant<int, 1>{}, T0{}, T1{});
+                    else if (n_a == 2) mma_loop(std::integral_constant<int, 2>{}, T0{}, T1{});
+                    else mma_loop(std::integral_constant<int, -1>{}, T0{}, T1{});
+                    issued = true;
+                }
+            }
+            if (issued) {
+            } else if (trace) mma_loop(std::integral_constant<int, -1>{}, T1{}, T0{});
+            else if (p.debug_skip_mma) mma_loop(std::integral_constant<int, 0>{}, T0{}, T0{});
+            else if (n_a == 1) mma_loop(std::integral_constant<int, 1>{}, T0{}, T0{});
+            else if (n_a == 2) mma_loop(std::integral_constant<int, 2>{}, T0{}, T0{});
+            else if (n_a == 4) mma_loop(std::integral_constant<int, 4>{}, T0{}, T0{});
+            else mma_loop(std::integral_constant<int, -1>{}, T0{}, T0{});
         }
     } else if (warp >= 4) {
         // ===================== epilogue (bufferize) =====================
@@ -382,7 +408,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters) {
             int mb, nb, ks;
             tile_coords(p.tm, t, mb, nb, ks);
-            const int m0 = mb * TILE_M + 128 * (int)rank, n0 = nb * p.tile_n;
+            const int m0 = mb * TILE_M + 128 * (int)rank, n0 = (nb * cn + (int)crank) * p.tile_n;
             const int64_t row = (int64_t)m0 + 32 * q + lane;
             ptx::mbar_wait(&tfull[acc], aph);
             if (trace && warp == 4 && lane == 0 && trace_k < kTraceTiles) trace[8 + 2 * kTraceK + 2 * trace_k] = ptx::globaltimer();
@@ -505,7 +531,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     }
 
     ptx::tc_fence_before();
-    if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
+    // (cluster_n: no CTA may exit while a peer can still multicast into its SMEM / barriers)
+    if (CG == 2 || mcast) ptx::cluster_sync(); else __syncthreads();
     if (trace && threadIdx.x == 0) trace[2] = ptx::globaltimer();
     if (warp == 2) {
         ptx::tc_fence_after();
@@ -520,7 +547,7 @@ cudaError_t launch_tc_t(const CUtensorMap& a, const CUtensorMap& b, const CUtens
     auto k = tc_gemm_kernel<TF32, CONV, CG, SPLIT3>;
     cudaError_t e = ensure_smem_attr(k, smem);
     if (e != cudaSuccess) return e;
-    if constexpr (CG == 1) {
+    if (CG == 1 && p.cn <= 1) {
         k<<<grid, kTcThreads, smem, st>>>(a, b, c, p);
     } else {
         cudaLaunchConfig_t cfg = {};
@@ -530,7 +557,7 @@ cudaError_t launch_tc_t(const CUtensorMap& a, const CUtensorMap& b, const CUtens
         cfg.stream = st;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = CG;
+        attr[0].val.clusterDim.x = CG * (p.cn > 1 ? p.cn : 1);
         attr[0].val.clusterDim.y = 1;
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;

@@ -93,6 +93,7 @@ static xtc_status plan_simt(const xtc_op_desc& d, const xtc_schedule& s, int num
     if (s.pack_warps > 1) ILLEGAL("SIMT engine: pack_warps must be 0 or 1 (all threads pack)");
     if (s.b_resident) ILLEGAL("SIMT engine: b_resident must be 0");
     if (s.pack_halo) ILLEGAL("SIMT engine: pack_halo must be 0");
+    if (s.cluster_n > 1) ILLEGAL("SIMT engine: cluster_n must be 0 or 1");
     if (V == 4 && (s.tile_n + s.swizzle) % 4) ILLEGAL("vectorize: vector_n 4 needs (tile_n + pad) %% 4 == 0 for aligned float4");
     auto r4 = [](int x) { return (x + 3) / 4 * 4; };
     int smem = st * (r4(s.tile_k * (s.tile_m + s.swizzle)) + r4(s.tile_k * (s.tile_n + s.swizzle))) * 4;
@@ -252,6 +253,7 @@ static xtc_status plan_tc(const xtc_op_desc& d, const xtc_schedule& s, int num_s
         ILLEGAL("tcgen05 engine needs BF16, TF32 or F32 (3xTF32 split) inputs");
     }
     if (s.pack_halo) {
+        if (s.cluster_n > 1) ILLEGAL("pack_halo: cluster_n must be 0 or 1 (cluster_m multicasts the filter)");
         p.atom_k = p.atom_n = 128 / dtype_size(d.in_dtype);
         return plan_tc_halo(d, s, num_sms, p, why);
     }
@@ -334,6 +336,23 @@ static xtc_status plan_tc(const xtc_op_desc& d, const xtc_schedule& s, int num_s
     if (p.atomic && s.buffer_c) ILLEGAL("atomic split-K uses direct red.global stores: buffer_c must be 0");
     p.block = kTcThreads;
     p.cluster = cg;
+    // cluster_n: cn CTAs on adjacent N tiles of one M tile share every A stage by TMA multicast
+    // (each loads 128/cn of its rows); a "tile" of the tile map is then a cluster tile
+    const int cn = s.cluster_n == 0 ? 1 : s.cluster_n;
+    if (cn != 1) {
+        if (cn != 2 && cn != 4) ILLEGAL("parallelize: cluster_n must be 1, 2 or 4");
+        if (d.kind != XTC_OP_MATMUL) ILLEGAL("parallelize: cluster_n (A multicast) applies to matmul only");
+        if (cg != 1) ILLEGAL("parallelize: cluster_n needs cluster_m 1");
+        if (p.split3) ILLEGAL("parallelize: cluster_n needs bf16/tf32 inputs (not the 3xTF32 split)");
+        if (s.b_resident) ILLEGAL("parallelize: cluster_n needs b_resident 0");
+        if (p.tiles_n % cn) ILLEGAL("parallelize: cluster_n %d must divide the %d N tiles", cn, p.tiles_n);
+        p.cluster_n = cn;
+        p.cluster = cn;
+        p.num_tiles = (int64_t)p.tiles_m * (p.tiles_n / cn) * p.split_k;
+        const int64_t ctas = p.num_tiles * cn;
+        p.grid_x = s.persistent ? (int)std::min<int64_t>(ctas, num_sms - num_sms % cn) : (int)ctas;
+        return XTC_OK;
+    }
     // one CTA (pair) per tile, or a persistent grid of at most one CTA per SM
     const int64_t ctas = p.num_tiles * cg;
     p.grid_x = s.persistent ? (int)std::min<int64_t>(ctas, num_sms - num_sms % cg) : (int)ctas;
@@ -370,7 +389,6 @@ xtc_status make_plan(const xtc_op_desc& d, const xtc_schedule& s, int num_sms, P
         p.tail_grid_y = (int)cdiv(M, 16);
         if (d.in_dtype != XTC_F32 && d.in_dtype != XTC_BF16 && d.in_dtype != XTC_TF32) ILLEGAL("bad dtype");
     }
-    if (s.reserved[0]) ILLEGAL("reserved schedule fields must be 0");
     // fuse: the consumer runs in the producer's epilogue, in the split-K
     // reduction (which produces the complete sums), or as its own elementwise pass
     if (s.fuse != 0 && s.fuse != 1) ILLEGAL("fuse must be 0 or 1");

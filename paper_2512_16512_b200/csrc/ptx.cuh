@@ -301,6 +301,17 @@ __device__ __forceinline__ void umma_commit_multicast(uint64_t* bar, uint16_t ma
                  ::"r"(smem_u32(bar)), "h"(mask) : "memory");
 }
 
+// 2-D tiled TMA load written to the same SMEM offset (and completing the same-offset mbarrier)
+// in every CTA of `mask`.
+__device__ __forceinline__ void tma_load_2d_multicast(const CUtensorMap* m, void* dst, uint64_t* bar, int32_t c0,
+                                                      int32_t c1, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%3, %4}], [%2], %5;"
+        ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
+        : "memory");
+}
+
 // 3-D tiled TMA load written to the same SMEM offset (and completing the same-offset
 // mbarrier) in every CTA of `mask`.
 __device__ __forceinline__ void tma_load_3d_multicast(const CUtensorMap* m, void* dst, uint64_t* bar, int32_t c0,

@@ -741,3 +741,30 @@ def test_run_gather_rejects_unsupported_schedules_and_ranges():
     ragged = xtc.Op(xtc.matmul_desc(200, 128, 128)).apply(tc(tile_n=128))
     with pytest.raises(xtc.XtcError):                       # ragged shard would spill into a neighbour
         ragged.run_gather(a[:200], b, [c.data_ptr()], 0, 512)
+
+
+# ------------------------- cluster_n: A stages multicast across N-adjacent CTAs --
+CLUSTER_N_SCHEDS = [
+    dict(tile_n=64, stages=8, cluster_n=2),
+    dict(tile_n=64, stages=6, cluster_n=4, persistent=1, acc_buffers=2, raster_group=2),
+    dict(tile_n=128, tile_k=128, stages=3, cluster_n=2, persistent=1, acc_buffers=2, pack_warps=2),
+    dict(tile_n=64, stages=4, cluster_n=2, split_k=2),
+    dict(tile_n=64, stages=4, cluster_n=4, buffer_c=0, order=1),
+]
+
+
+@pytest.mark.parametrize("sch", CLUSTER_N_SCHEDS)
+def test_tc_cluster_n_multicast_integer_bit_exact(sch):
+    run_matmul(384, 512, 448, "bf16", "bf16", tc(**sch), MODE_INT)
+    run_matmul(300, 512, 200, "bf16", "f32", tc(**sch), MODE_INT)     # ragged M and K
+
+
+@pytest.mark.parametrize("size", [512, 1024])
+def test_tc_cluster_n_float_tolerance(size):
+    err, _ = run_matmul(size, size, size, "bf16", "bf16", tc(tile_n=64, stages=8, cluster_n=2, persistent=1,
+                                                             acc_buffers=2), MODE_UNIFORM)
+    assert err <= 5e-3
+
+
+def test_tc_cluster_n_tf32():
+    run_matmul(256, 256, 192, "tf32", "f32", tc(tile_n=64, tile_k=32, stages=6, cluster_n=2), MODE_INT)

@@ -311,3 +311,28 @@ def test_traffic_model_closed_forms():
     # ragged: M = 300 -> 3 tiles of 128 rows are loaded in full boxes
     pr = predicted_l2_bytes(xtc.matmul_desc(300, 128, 64, "bf16", "bf16"), S(**dict(TCB, tile_n=128)))
     assert pr["loads"] == 3 * 1 * 64 * (128 + 128) * 2
+
+
+def test_cluster_n_legality():
+    """cluster_n (A multicast across N-adjacent CTAs): legal values and the rules of include/xtc.h."""
+    d = xtc.matmul_desc(1024, 1024, 1024)
+    base = dict(engine=1, tile_m=128, tile_n=64, tile_k=64, stages=8, swizzle=128, buffer_c=1)
+    for cn in (0, 1, 2, 4):
+        st, info, why = xtc.xtc_schedule_check(d, xtc.schedule(**base, cluster_n=cn))
+        assert st == xtc.XTC_OK, why
+        if cn > 1:
+            assert info.cluster_x == cn and info.grid_x == 128 and info.num_tiles == 128 // cn
+    for bad in (dict(cluster_n=3), dict(cluster_n=8), dict(cluster_n=2, cluster_m=2, tile_m=256, tile_n=128),
+                dict(cluster_n=2, b_resident=1)):
+        st, _, why = xtc.xtc_schedule_check(d, xtc.schedule(**dict(base, **bad)))
+        assert st == xtc.XTC_E_ILLEGAL_SCHEDULE, bad
+    # N tiles not divisible by cluster_n
+    st, _, why = xtc.xtc_schedule_check(xtc.matmul_desc(1024, 192, 1024), xtc.schedule(**base, cluster_n=2))
+    assert st == xtc.XTC_E_ILLEGAL_SCHEDULE and "divide" in why
+    # SIMT and conv reject it
+    st, _, _ = xtc.xtc_schedule_check(d, xtc.schedule(engine=0, tile_m=64, tile_n=64, tile_k=16, inner_m=4,
+                                                      inner_n=4, cluster_n=2))
+    assert st == xtc.XTC_E_ILLEGAL_SCHEDULE
+    dc = xtc.conv2d_desc(2, 14, 14, 64, 64, 3, 3, 1, 1)
+    st, _, _ = xtc.xtc_schedule_check(dc, xtc.schedule(**base, cluster_n=2))
+    assert st == xtc.XTC_E_ILLEGAL_SCHEDULE
