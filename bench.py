@@ -32,8 +32,24 @@ NCU_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary.json")
 FALLBACK_PEAKS = {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0}
 
 # Tuned default for the headline workload (from the schedule sweep).
-HEADLINE_SCHEDULE = dict(engine=1, tile_m=256, tile_n=256, tile_k=128, stages=3, swizzle=128, buffer_c=1,
-                         acc_buffers=2, persistent=1, raster_group=16, order=0, cluster_m=2)
+# CTA pair, two 128-row M-subtiles per CTA: a 512 x 256 output tile per pair whose B stage (256
+# columns) is shared by 512 rows -- 25 % less operand traffic into the SMs than the 256 x 256 tile
+# (profiles/r01_headline_vs_cublas.json); one TMEM accumulator (2 x 256 columns).
+HEADLINE_SCHEDULE = dict(engine=1, tile_m=512, tile_n=256, tile_k=64, stages=4, swizzle=128, buffer_c=1,
+                         acc_buffers=1, persistent=1, raster_group=8, order=0, cluster_m=2)
+# the previous default (256 x 256 pair tile, double-buffered accumulator)
+PAIR256_SCHEDULE = dict(engine=1, tile_m=256, tile_n=256, tile_k=128, stages=3, swizzle=128, buffer_c=1,
+                        acc_buffers=2, persistent=1, raster_group=16, order=0, cluster_m=2)
+
+
+def schedule_for_rows(rows: int, num_sms: int = 148) -> dict:
+    """Headline schedule for an M-shard of `rows` rows (N = 8192): the 512-row pair tile does the
+    work of two 256-row tiles, so it is used unless its last wave of pair-CTAs leaves more of the
+    GPU idle than the 256-row tile's would (wave quantisation of a small shard)."""
+    pairs = num_sms // 2
+    t512 = -(-rows // 512) * (N // 256)
+    t256 = -(-rows // 256) * (N // 256)
+    return HEADLINE_SCHEDULE if 2 * -(-t512 // pairs) <= -(-t256 // pairs) else PAIR256_SCHEDULE
 
 
 def load_peaks():
@@ -73,6 +89,7 @@ class ClockSampler:
         self.period = period_s
         self.samples = []
         self.reasons = set()
+        self.mask_union = 0          # every clocks-event-reason bit seen (raw NVML mask, for the record)
         self.max_mhz = None
         self._stop = threading.Event()
         self.ok = False
@@ -103,6 +120,7 @@ class ClockSampler:
             try:
                 self.samples.append(float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)))
                 mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.mask_union |= int(mask)
                 for n, b in self.BITS.items():
                     if mask & b:
                         self.reasons.add(n)
@@ -120,7 +138,9 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0,
                     "source": "nvml"}
         return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples), "source": "nvml, 5 ms period"}
+                "sm_mhz_min": min(self.samples), "sm_mhz_max": max(self.samples),
+                "reasons": sorted(self.reasons), "reason_mask_union": hex(self.mask_union), "samples": len(self.samples),
+                "source": "nvml, 5 ms period"}
 
 
 # --------------------------------------------------------- reference arm ---
@@ -345,8 +365,9 @@ def main_xtc(args):
         xtc.xtc_fill(a.data_ptr(), Mr * K, xtc.XTC_BF16, 1, 0, r0 * K, sp)
     xtc.xtc_fill(b.data_ptr(), K * N, xtc.XTC_BF16, 2, 0, 0, sp)
     desc = xtc.matmul_desc(Mr, N, K, "bf16", "bf16")
-    op = xtc.Op(desc, local).apply(xtc.schedule(**HEADLINE_SCHEDULE))
-    chunk_ops = [xtc.Op(xtc.matmul_desc(Mc, N, K, "bf16", "bf16"), local).apply(xtc.schedule(**HEADLINE_SCHEDULE))
+    sched = schedule_for_rows(Mr)
+    op = xtc.Op(desc, local).apply(xtc.schedule(**sched))
+    chunk_ops = [xtc.Op(xtc.matmul_desc(Mc, N, K, "bf16", "bf16"), local).apply(xtc.schedule(**schedule_for_rows(Mc)))
                  for _ in range(CH)] if CH > 1 else [op]
     async_nccl = world > 1 and not rehearsal
 
@@ -431,7 +452,7 @@ def main_xtc(args):
     a2, b2, c2 = torch.empty_like(a), torch.empty_like(b), torch.empty_like(c)
     fused2 = SymmetricOutput((M, N), torch.bfloat16, dev) if fused else None
     fc2 = (fused2.tensor if fused else torch.empty_like(full_c)) if world > 1 else None
-    bufs.append((a2, b2, c2, fc2, xtc.Op(desc, local).apply(xtc.schedule(**HEADLINE_SCHEDULE))))
+    bufs.append((a2, b2, c2, fc2, xtc.Op(desc, local).apply(xtc.schedule(**sched))))
     s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
     ev_in = [torch.cuda.Event() for _ in range(2)]
     ev_comp = [torch.cuda.Event() for _ in range(2)]
@@ -576,7 +597,7 @@ def main_xtc(args):
                                        (f"M-sharded x{world}, {CH} block-cyclic chunks per rank, each NCCL "
                                         f"all-gather overlapping the next chunk's GEMM"
                                         + (f"; {fused_note}" if fused_note else ""))) if world > 1 else "single GPU",
-                       "schedule": HEADLINE_SCHEDULE,
+                       "schedule": sched,
                        "l2": "inputs (256 MiB) exceed L2 (126 MB); no flush between steps"},
             "frac_of_peak": value / world / peak_tf,
             "peak_used": {"bf16_tflops": peak_tf, "kind": peak_kind},

@@ -106,7 +106,10 @@ typedef enum { XTC_SPLITK_ORDERED = 0, XTC_SPLITK_ATOMIC = 1 } xtc_splitk_mode;
  * §8(a) a2).  Unused knobs must be 0 (or 1 where noted); a knob value 0
  * means "default" only where stated.
  *
- * strip_mine   tile_m, tile_n, tile_k : CTA tile of the (M,N,K) loops
+ * strip_mine   tile_m, tile_n, tile_k : CTA tile of the (M,N,K) loops; tcgen05: tile_m = 128 x
+ *                                                   cluster_m (one UMMA row tile per CTA) or 256 x cluster_m
+ *                                                   (matmul: two 128-row UMMA subtiles per CTA sharing every
+ *                                                   B stage, two TMEM accumulators)
  *                          inner_m, inner_n       : SIMT thread register tile (TM x TN);
  *                                                   tcgen05: UMMA atom (inner_m = tile_m / cta_group,
  *                                                   inner_n = tile_n); 0 = derive

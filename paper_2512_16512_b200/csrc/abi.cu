@@ -450,11 +450,11 @@ static xtc_status encode_maps(xtc_op op, const void* A, const void* B, void* C) 
         // {atom, 128, tile_k/atom} per stage lands as [k-atom][row][128 B] (needs K % atom == 0).
         const int64_t lda = d.lda ? d.lda : d.k;
         // cluster_n: each CTA loads a 128/cluster_n-row slice of every A atom (2-D boxes)
-        const int a_rows = p.cluster_n > 1 ? 128 / p.cluster_n : 128;
+        const int a_rows = p.cluster_n > 1 ? 128 / p.cluster_n : 128 * p.msub;
         if (allow3d && p.K % atom == 0 && p.cluster_n <= 1) {
             cuuint64_t dims[3] = {(cuuint64_t)atom, (cuuint64_t)p.M, (cuuint64_t)(p.K / atom)};
             cuuint64_t strides[2] = {(cuuint64_t)(lda * es), (cuuint64_t)(atom * es)};
-            cuuint32_t box[3] = {(cuuint32_t)atom, 128, (cuuint32_t)(tile_k / atom)};
+            cuuint32_t box[3] = {(cuuint32_t)atom, (cuuint32_t)a_rows, (cuuint32_t)(tile_k / atom)};
             cuuint32_t estr[3] = {1, 1, 1};
             r = g_encode_tiled(&op->tmA, in_t, 3, const_cast<void*>(A), dims, strides, box, estr,
                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -633,7 +633,8 @@ static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cud
                    ((uint32_t)(p.sch.tile_n >> 3) << 17) | ((uint32_t)((128 * p.cta_group) >> 4) << 24);
         tp.tmem_cols = (uint32_t)p.tmem_cols;
         const int es = dsize(d.in_dtype);
-        tp.a_stage_bytes = (uint32_t)(128 * p.sch.tile_k * es);
+        tp.a_stage_bytes = (uint32_t)(128 * p.msub * p.sch.tile_k * es);
+        tp.ms = p.msub;
         tp.b_stage_bytes = (uint32_t)(p.sch.tile_k * (p.sch.tile_n / p.cta_group) * es);
         tp.lo_off = p.split3 ? (uint32_t)(p.sch.stages * (tp.a_stage_bytes + tp.b_stage_bytes)) : 0u;
         tp.cg = conv_geom(d);
@@ -744,7 +745,7 @@ extern "C" xtc_status xtc_run_gather(xtc_op op, const void* const* inputs, void*
         p.has_tail || p.cons_pass || p.split3 || (d.consumer & XTC_CONSUMER_ACCUMULATE))
         return fail(XTC_E_UNSUPPORTED, "xtc_run_gather: needs a tcgen05 matmul schedule with buffer_c=1, split_k=1, "
                                        "no split_n_at root, fused consumers other than accumulate");
-    const int64_t tile_rows = 128 * (int64_t)p.cta_group;
+    const int64_t tile_rows = 128 * (int64_t)p.cta_group * p.msub;
     if (p.M % tile_rows) return fail(XTC_E_UNSUPPORTED, "xtc_run_gather: M must be a multiple of the CTA tile rows");
     if (row_offset < 0 || row_offset + p.M > dest_rows || dest_rows > INT32_MAX)
         return fail(XTC_E_INVALID_ARG, "xtc_run_gather: rows [row_offset, row_offset + M) must lie in [0, dest_rows)");

@@ -36,14 +36,17 @@
 
 namespace xtc {
 
-template <bool TF32, bool CONV, int CG, bool SPLIT3>
+template <bool TF32, bool CONV, int CG, bool SPLIT3, int MS>
 __global__ void __launch_bounds__(kTcThreads, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmC, const TcParams p) {
     constexpr int ATOM = TF32 ? 32 : 64;     // elements per 128-byte row (A's K / B's N)
     constexpr int UMMA_K = TF32 ? 8 : 16;    // K per tcgen05.mma (32 bytes)
-    constexpr uint32_t A_ATOM_BYTES = 128 * 128;
-    constexpr int TILE_M = 128 * CG;
+    // MS M-subtiles per CTA (tile_m = 128 * CG * MS): the CTA holds 128*MS rows of A, and each
+    // k-step issues MS UMMAs (one per 128-row subtile) sharing the B operand into MS TMEM
+    // accumulators of tile_n columns -- B is loaded once per MS*128 rows
+    constexpr uint32_t A_ATOM_BYTES = 128 * MS * 128;
+    constexpr int TILE_M = 128 * CG * MS;
 
     extern __shared__ uint8_t smem_raw[];
     const uint32_t pad = (1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u;
@@ -164,7 +167,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 tile_coords(p.tm, t, mb, nb, ks);
                 const int kb0 = ks * p.kb_per_split;
                 const int kb1 = min(p.kb_total, kb0 + p.kb_per_split);
-                const int m0 = mb * TILE_M + 128 * (int)rank;     // this CTA's 128 rows
+                const int m0 = mb * TILE_M + 128 * MS * (int)rank;     // this CTA's 128*MS rows
                 const int n0 = (nb * cn + (int)crank) * p.tile_n + bn_cta * (int)rank;  // this CTA's B columns
                 int wq = 0, hp = 0, nimg = 0;
                 if constexpr (CONV) {
@@ -175,7 +178,25 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                     hp = pp * p.cg.sh - p.cg.ph;      // filter-window origin of pixel m0
                     wq = qq * p.cg.sw - p.cg.pw;
                 }
+                // conv: (filter row r, filter col sx, channel c) of the next k-block, advanced
+                // incrementally (no integer division in the issue loop)
+                int c_run = 0, s_run = 0, r_run = 0;
+                if constexpr (CONV) {
+                    const int kc0 = kb0 * p.tile_k;
+                    const int rs0 = kc0 / p.cg.C;
+                    c_run = kc0 - rs0 * p.cg.C;
+                    r_run = rs0 / p.cg.S;
+                    s_run = rs0 - r_run * p.cg.S;
+                }
                 for (int kb = kb0; kb < kb1; ++kb) {
+                    const int c_kb = c_run, s_kb = s_run, r_kb = r_run;
+                    if constexpr (CONV) {
+                        c_run += p.tile_k;
+                        while (c_run >= p.cg.C) {
+                            c_run -= p.cg.C;
+                            if (++s_run == p.cg.S) { s_run = 0; ++r_run; }
+                        }
+                    }
                     const int cs = s;
                     const uint32_t cpar = use_par;
                     const bool mine = rr == pw, fresh = first_round;
@@ -203,7 +224,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                     // 3-D maps: one TMA moves all atoms of the stage ({atom, rows, atom index} box
                     // lands as [atom][rows][128 B], the layout the UMMA descriptors walk)
                     const bool a_one = !CONV && p.a3d;
-                    if (mcast) {
+                    if (MS == 1 && mcast) {
                         // this CTA's 128/cn-row slice of every A atom, into the same offset of all cn CTAs
                         const int rows = 128 / cn;
                         for (int a = 0; a < n_a; ++a)
@@ -214,13 +235,17 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                         if constexpr (CG == 2) ptx::tma_load_3d_pair(&tmA, a_dst, bar_c, 0, m0, ka);
                         else ptx::tma_load_3d(&tmA, a_dst, fb, 0, m0, ka);
                     }
+                    int c = c_kb, sx = s_kb, r = r_kb;       // conv: this atom's (r, s, c)
                     for (int a = 0; a < ((a_one || mcast) ? 0 : n_a); ++a) {
                         const int kc = kb * p.tile_k + a * ATOM;
                         if constexpr (CONV) {
-                            const int rs = kc / p.cg.C;
-                            const int c = kc - rs * p.cg.C;
-                            const int r = rs / p.cg.S;
-                            const int sx = rs - r * p.cg.S;
+                            if (a > 0) {
+                                c += ATOM;
+                                if (c == p.cg.C) {
+                                    c = 0;
+                                    if (++sx == p.cg.S) { sx = 0; ++r; }
+                                }
+                            }
                             if constexpr (CG == 2)
                                 ptx::tma_load_im2col_4d_pair(&tmA, a_dst + a * A_ATOM_BYTES, bar_c, c, wq, hp, nimg,
                                                              (uint16_t)sx, (uint16_t)r);
@@ -325,7 +350,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                     ptx::mbar_wait(&tempty[acc], aph ^ 1);
                     ptx::tc_fence_after();
                     if (ptx::elect_one()) {
-                        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * tile_n);
+                        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * MS * tile_n);
                         int s1 = s, tk1 = tk;
                         uint32_t ph1 = ph;
                         for (int kb = kb0; kb < kb1; ++kb) {
@@ -345,9 +370,12 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 #pragma unroll
                                     for (int kk = 0; kk < ATOM / UMMA_K; ++kk) {
                                         const uint32_t krow = a * ATOM + kk * UMMA_K;
-                                        ptx::umma<TF32, CG>(d_tmem, ad_ + (uint64_t)((a * A_ATOM_BYTES + kk * 32) >> 4),
-                                                            bd_ + (uint64_t)(krow * 8), idesc,
-                                                            (a > 0 || kk > 0) ? 1u : first);
+#pragma unroll
+                                        for (int h = 0; h < MS; ++h)
+                                            ptx::umma<TF32, CG>(d_tmem + (uint32_t)(h * tile_n),
+                                                                ad_ + (uint64_t)((a * A_ATOM_BYTES + h * 128 * 128 + kk * 32) >> 4),
+                                                                bd_ + (uint64_t)(krow * 8), idesc,
+                                                                (a > 0 || kk > 0) ? 1u : first);
                                     }
                                 }
                             };
@@ -408,12 +436,14 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters) {
             int mb, nb, ks;
             tile_coords(p.tm, t, mb, nb, ks);
-            const int m0 = mb * TILE_M + 128 * (int)rank, n0 = (nb * cn + (int)crank) * p.tile_n;
-            const int64_t row = (int64_t)m0 + 32 * q + lane;
+            const int m0t = mb * TILE_M + 128 * MS * (int)rank, n0 = (nb * cn + (int)crank) * p.tile_n;
             ptx::mbar_wait(&tfull[acc], aph);
             if (trace && warp == 4 && lane == 0 && trace_k < kTraceTiles) trace[8 + 2 * kTraceK + 2 * trace_k] = ptx::globaltimer();
             ptx::tc_fence_after();
-            const uint32_t t_row = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * p.tile_n);
+            for (int h = 0; h < MS; ++h) {                 // M-subtiles: accumulator h holds rows m0t + 128h ..
+            const int m0 = m0t + 128 * h;
+            const int64_t row = (int64_t)m0 + 32 * q + lane;
+            const uint32_t t_row = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)((acc * MS + h) * p.tile_n);
             for (int c = 0; c < p.tile_n; c += 32) {
                 uint32_t v[32];
                 ptx::tmem_ld_32x32b_x32(t_row + c, v);
@@ -518,6 +548,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                     }
                 }
             }
+            }   // M-subtiles
             ptx::tc_fence_before();
             __syncwarp();
             if (trace && warp == 4 && lane == 0 && trace_k < kTraceTiles) trace[8 + 2 * kTraceK + 2 * trace_k++ + 1] = ptx::globaltimer();
@@ -541,10 +572,10 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 }
 
 // ------------------------------------------------------------------ launch --
-template <bool TF32, bool CONV, int CG, bool SPLIT3>
+template <bool TF32, bool CONV, int CG, bool SPLIT3, int MS>
 cudaError_t launch_tc_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
                                const TcParams& p, int grid, int smem, cudaStream_t st) {
-    auto k = tc_gemm_kernel<TF32, CONV, CG, SPLIT3>;
+    auto k = tc_gemm_kernel<TF32, CONV, CG, SPLIT3, MS>;
     cudaError_t e = ensure_smem_attr(k, smem);
     if (e != cudaSuccess) return e;
     if (CG == 1 && p.cn <= 1) {
@@ -570,10 +601,10 @@ cudaError_t launch_tc_t(const CUtensorMap& a, const CUtensorMap& b, const CUtens
 
 // The variants are instantiated in their own translation units (gemm_tc_*.cu) so that
 // nvcc compiles them in parallel; gemm_tc.cu only dispatches.
-#define XTC_TC_VARIANT(TF32, CONV, CG, SPLIT3)                                                          \
-    template cudaError_t launch_tc_t<TF32, CONV, CG, SPLIT3>(const CUtensorMap&, const CUtensorMap&,   \
-                                                             const CUtensorMap&, const TcParams&, int, \
-                                                             int, cudaStream_t);
-#define XTC_TC_EXTERN(TF32, CONV, CG, SPLIT3) extern XTC_TC_VARIANT(TF32, CONV, CG, SPLIT3)
+#define XTC_TC_VARIANT(TF32, CONV, CG, SPLIT3, MS)                                                          \
+    template cudaError_t launch_tc_t<TF32, CONV, CG, SPLIT3, MS>(const CUtensorMap&, const CUtensorMap&,   \
+                                                                 const CUtensorMap&, const TcParams&, int, \
+                                                                 int, cudaStream_t);
+#define XTC_TC_EXTERN(TF32, CONV, CG, SPLIT3, MS) extern XTC_TC_VARIANT(TF32, CONV, CG, SPLIT3, MS)
 
 }  // namespace xtc

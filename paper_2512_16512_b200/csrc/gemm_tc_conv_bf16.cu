@@ -3,7 +3,7 @@
 
 namespace xtc {
 
-XTC_TC_VARIANT(false, true, 1, false)
-XTC_TC_VARIANT(false, true, 2, false)
+XTC_TC_VARIANT(false, true, 1, false, 1)
+XTC_TC_VARIANT(false, true, 2, false, 1)
 
 }  // namespace xtc

@@ -3,6 +3,6 @@
 
 namespace xtc {
 
-XTC_TC_VARIANT(true, false, 1, true)
+XTC_TC_VARIANT(true, false, 1, true, 1)
 
 }  // namespace xtc

@@ -263,8 +263,19 @@ static xtc_status plan_tc(const xtc_op_desc& d, const xtc_schedule& s, int num_s
     int cg = s.cluster_m == 0 ? 1 : s.cluster_m;
     if (cg != 1 && cg != 2) ILLEGAL("tcgen05 cluster_m must be 1 (cta_group::1) or 2 (cta_group::2 CTA pair)");
     p.cta_group = cg;
-    if (s.tile_m != 128 * cg) ILLEGAL("tcgen05 tile_m must be %d for cluster_m=%d (UMMA M=128 per CTA)", 128 * cg, cg);
-    if (s.inner_m != 0 && s.inner_m != s.tile_m) ILLEGAL("tcgen05 inner_m (UMMA M) must equal tile_m");
+    // M-subtiles: tile_m = 128 * cta_group * ms; ms = 2 stacks two UMMA row tiles per CTA that share
+    // every B stage (matmul; B leaves L2 once per 256 rows per CTA instead of per 128)
+    const int ms = s.tile_m == 256 * cg ? 2 : 1;
+    if (s.tile_m != 128 * cg * ms)
+        ILLEGAL("tcgen05 tile_m must be %d or %d for cluster_m=%d (128-row UMMA subtiles per CTA)", 128 * cg, 256 * cg, cg);
+    if (s.inner_m != 0 && s.inner_m != 128 * cg) ILLEGAL("tcgen05 inner_m (UMMA M) must be %d", 128 * cg);
+    if (ms == 2) {
+        if (d.kind != XTC_OP_MATMUL) ILLEGAL("tcgen05 tile_m %d (two M-subtiles per CTA) applies to matmul only", s.tile_m);
+        if (p.split3) ILLEGAL("tcgen05 two M-subtiles: not with the 3xTF32 split");
+        if (s.b_resident) ILLEGAL("tcgen05 two M-subtiles: b_resident must be 0");
+        if (s.cluster_n > 1) ILLEGAL("tcgen05 two M-subtiles: cluster_n must be 0 or 1");
+    }
+    p.msub = ms;
     if (s.inner_n != 0 && s.inner_n != s.tile_n) ILLEGAL("tcgen05 inner_n (UMMA N) must equal tile_n");
     int bn_cta = s.tile_n / cg;
     if (s.tile_n < p.atom_n * cg || s.tile_n > 256 || bn_cta % p.atom_n)
@@ -278,12 +289,12 @@ static xtc_status plan_tc(const xtc_op_desc& d, const xtc_schedule& s, int num_s
     if (s.swizzle != 0 && s.swizzle != 128) ILLEGAL("tcgen05 swizzle must be 128 (0 = default 128)");
     int accb = s.acc_buffers == 0 ? 1 : s.acc_buffers;
     if (accb < 1 || accb > 2) ILLEGAL("acc_buffers must be 1 or 2");
-    int cols = accb * s.tile_n;
+    int cols = accb * s.tile_n * ms;
     int alloc = 32;
     while (alloc < cols) alloc *= 2;
     if (alloc > 512) ILLEGAL("bufferize: %d TMEM columns (acc_buffers x tile_n, pow2) exceed 512", alloc);
     p.tmem_cols = alloc;
-    int a_stage = 128 * s.tile_k * es;
+    int a_stage = 128 * ms * s.tile_k * es;
     int b_stage = s.tile_k * bn_cta * es;
     int smem = 0;
     if (s.b_resident) {

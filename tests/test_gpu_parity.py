@@ -679,6 +679,8 @@ GATHER_CASES = [
           raster_group=16), 4, "bf16", 512),
     (dict(tile_n=64, stages=6), 8, "f32", 328),          # ragged N: every destination's store is clipped
     (dict(tile_n=256, stages=3, acc_buffers=2, persistent=1), 1, "bf16", 256),
+    # the bench headline tile: CTA pair with two M-subtiles (512-row tiles)
+    (dict(tile_m=512, cluster_m=2, tile_n=256, tile_k=64, stages=4, persistent=1, raster_group=8), 2, "bf16", 512),
 ]
 
 
@@ -768,3 +770,39 @@ def test_tc_cluster_n_float_tolerance(size):
 
 def test_tc_cluster_n_tf32():
     run_matmul(256, 256, 192, "tf32", "f32", tc(tile_n=64, tile_k=32, stages=6, cluster_n=2), MODE_INT)
+
+
+# ------------------- two 128-row M-subtiles per CTA sharing B (tile_m = 256 * cta_group) --
+MSUB_SCHEDS = [
+    dict(tile_m=256, tile_n=128, stages=4),
+    dict(tile_m=256, tile_n=256, tile_k=64, stages=3, persistent=1, raster_group=4),
+    dict(tile_m=512, cluster_m=2, tile_n=256, tile_k=64, stages=4),
+    dict(tile_m=512, cluster_m=2, tile_n=256, tile_k=64, stages=4, persistent=1, raster_group=16, order=1),
+    dict(tile_m=512, cluster_m=2, tile_n=128, tile_k=64, stages=4, persistent=1, acc_buffers=2, pack_warps=2),
+    dict(tile_m=256, tile_n=128, stages=3, split_k=2),
+    dict(tile_m=256, tile_n=64, stages=4, buffer_c=0),
+]
+
+
+@pytest.mark.parametrize("sch", MSUB_SCHEDS)
+def test_tc_two_m_subtiles_integer_bit_exact(sch):
+    run_matmul(1024, 512, 384, "bf16", "bf16", tc(**sch), MODE_INT)
+    run_matmul(700, 512, 200, "bf16", "f32", tc(**sch), MODE_INT)      # ragged M (partial subtiles) and K
+
+
+def test_tc_two_m_subtiles_float_and_tf32():
+    err, _ = run_matmul(1024, 1024, 1024, "bf16", "bf16", tc(tile_m=512, cluster_m=2, tile_n=256, tile_k=64,
+                                                             stages=4), MODE_UNIFORM)
+    assert err <= 5e-3
+    run_matmul(512, 256, 192, "tf32", "f32", tc(tile_m=256, tile_n=128, tile_k=32, stages=4), MODE_INT)
+    desc_relu = dict(tile_m=512, cluster_m=2, tile_n=256, tile_k=64, stages=4, fuse=1)
+    M, N, K = 512, 256, 128
+    import oracle
+    d = xtc.matmul_desc(M, N, K, "bf16", "bf16", consumer="relu")
+    a = dev_tensor((M, K), "bf16", 31, MODE_INT)
+    b = dev_tensor((K, N), "bf16", 32, MODE_INT)
+    c = torch.full((M, N), float("nan"), dtype=torch.bfloat16, device="cuda:0")
+    xtc.Op(d).apply(tc(**desc_relu)).run(a, b, c)
+    torch.cuda.synchronize()
+    O, D = oracle_matmul(M, N, K, "bf16", MODE_INT, 31, 32)
+    check_against_oracle(c, oracle.relu(O), D, "bf16", exact=True, tol=0)

@@ -336,3 +336,36 @@ def test_cluster_n_legality():
     dc = xtc.conv2d_desc(2, 14, 14, 64, 64, 3, 3, 1, 1)
     st, _, _ = xtc.xtc_schedule_check(dc, xtc.schedule(**base, cluster_n=2))
     assert st == xtc.XTC_E_ILLEGAL_SCHEDULE
+
+
+def test_two_m_subtiles_legality():
+    """tile_m = 256 x cluster_m: two 128-row UMMA subtiles per CTA (matmul only), TMEM = 2 x tile_n x acc."""
+    d = xtc.matmul_desc(8192, 8192, 8192)
+    ok = dict(engine=1, tile_m=512, cluster_m=2, tile_n=256, tile_k=64, stages=4, swizzle=128, buffer_c=1)
+    st, info, why = xtc.xtc_schedule_check(d, xtc.schedule(**ok))
+    assert st == xtc.XTC_OK, why
+    assert info.tmem_cols == 512 and info.num_tiles == 16 * 32 and info.grid_x == 1024
+    st, info, why = xtc.xtc_schedule_check(d, xtc.schedule(**dict(ok, tile_m=256, cluster_m=1, tile_n=128)))
+    assert st == xtc.XTC_OK, why
+    for bad in (dict(acc_buffers=2),                       # 2 x 2 x 256 TMEM columns
+                dict(tile_m=384),                          # not 128 or 256 per CTA
+                dict(stages=5),                            # 5 x 48 KB stages exceed SMEM
+                dict(inner_m=512)):                        # the UMMA M is 256
+        st, _, why = xtc.xtc_schedule_check(d, xtc.schedule(**dict(ok, **bad)))
+        assert st == xtc.XTC_E_ILLEGAL_SCHEDULE, bad
+    dc = xtc.conv2d_desc(2, 14, 14, 64, 64, 3, 3, 1, 1)
+    st, _, why = xtc.xtc_schedule_check(dc, xtc.schedule(engine=1, tile_m=256, tile_n=64, tile_k=64, stages=4,
+                                                         swizzle=128, buffer_c=1))
+    assert st == xtc.XTC_E_ILLEGAL_SCHEDULE and "matmul only" in why
+
+
+def test_bench_schedule_for_rows_wave_rule():
+    """bench.py picks the 512-row pair tile unless a small shard's last wave wastes more of the GPU."""
+    import bench
+    assert bench.schedule_for_rows(8192) is bench.HEADLINE_SCHEDULE       # 512 tiles: 7 waves vs 14 half-size
+    assert bench.schedule_for_rows(4096) is bench.PAIR256_SCHEDULE        # 256 tiles: 4 waves (8) vs 7
+    assert bench.schedule_for_rows(2048) is bench.HEADLINE_SCHEDULE
+    assert bench.schedule_for_rows(1024) is bench.HEADLINE_SCHEDULE
+    for s in (bench.HEADLINE_SCHEDULE, bench.PAIR256_SCHEDULE):
+        st, _, why = xtc.xtc_schedule_check(xtc.matmul_desc(8192, 8192, 8192), xtc.schedule(**s))
+        assert st == xtc.XTC_OK, why
