@@ -84,7 +84,9 @@ def prt_tiles(sample: Sequence[int], n_pdims: int = 2, p_levels: int = 3, r_leve
 # P UMMA atom | R UMMA k-steps | P instruction tile.  Slots below are the
 # free choices of that sketch.
 TC_SLOTS = {
-    "cluster_m": [1, 2],          # parallelize: 1 CTA (tile_m 128) or a CTA pair (tile_m 256)
+    "cluster_m": [1, 2],          # parallelize: 1 CTA or a CTA pair (cta_group::2)
+    "m_subtiles": [1, 2],         # strip_mine: 128-row UMMA subtiles per CTA (tile_m = 128 x cluster_m x this)
+    "cluster_n": [1, 2],          # parallelize: CTAs on adjacent N tiles sharing A stages by multicast
     "tile_n": [64, 128, 192, 256],
     "tile_k": [64, 128],
     "stages": [2, 3, 4, 5, 6, 7, 8],
@@ -131,7 +133,8 @@ class GpuStrategy:
         kw = self._base()
         kw.update({n: int(v) for n, v in zip(names, values)})
         if self.engine == XTC_ENGINE_TCGEN05:
-            kw["tile_m"] = 128 * max(1, kw.get("cluster_m", 1))    # UMMA M = 128 per CTA
+            # UMMA M = 128 per CTA; m_subtiles (a slot, not a schedule field) stacks 1 or 2 per CTA
+            kw["tile_m"] = 128 * max(1, kw.get("cluster_m", 1)) * max(1, kw.pop("m_subtiles", 1))
         return kw
 
     def generate(self, sample: Sequence[int]) -> xtc_schedule:
