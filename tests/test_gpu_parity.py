@@ -806,3 +806,29 @@ def test_tc_two_m_subtiles_float_and_tf32():
     torch.cuda.synchronize()
     O, D = oracle_matmul(M, N, K, "bf16", MODE_INT, 31, 32)
     check_against_oracle(c, oracle.relu(O), D, "bf16", exact=True, tol=0)
+
+
+# ------------------------------------------------------- degenerate shapes --
+@pytest.mark.parametrize("mnk", [(1, 1, 1), (1, 7, 3), (5, 1, 9), (3, 5, 1)])
+def test_simt_degenerate_shapes(mnk):
+    """Single rows/columns and a one-term reduction on the fp32 SIMT engine (bit-exact on integers)."""
+    M, N, K = mnk
+    run_matmul(M, N, K, "f32", "f32", S(engine=0, tile_m=8, tile_n=8, tile_k=8, inner_m=1, inner_n=1), MODE_INT)
+
+
+@pytest.mark.parametrize("mnk", [(1, 64, 64), (1, 8, 8), (130, 64, 8), (3, 200, 24)])
+@pytest.mark.parametrize("sch", [dict(tile_n=64, stages=2), dict(tile_m=256, cluster_m=2, tile_n=128, stages=2),
+                                 dict(tile_m=512, cluster_m=2, tile_n=256, tile_k=64, stages=4)])
+def test_tc_degenerate_shapes(mnk, sch):
+    """One output row, the narrowest TMA-legal N (8 bf16 = 16 B rows), K smaller than one k-block (TMA
+    zero-fills the rest of the box): one partial tile, every schedule family."""
+    M, N, K = mnk
+    run_matmul(M, N, K, "bf16", "bf16", tc(**sch), MODE_INT)
+
+
+def test_conv_degenerate_single_pixel():
+    """1x1 image, 3x3 filter with pad 1: only the centre tap meets data (P = Q = 1, M = batch)."""
+    d = xtc.conv2d_desc(3, 1, 1, 64, 64, 3, 3, 1, 1, "bf16", "f32")
+    run_conv(d, "bf16", "f32", tc(tile_n=64, stages=3), MODE_INT)
+    d = xtc.conv2d_desc(1, 1, 1, 64, 128, 1, 1, 1, 0, "bf16", "bf16")
+    run_conv(d, "bf16", "bf16", tc(tile_n=128, stages=2), MODE_INT)
