@@ -35,7 +35,9 @@ FALLBACK_PEAKS = {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_g
 # CTA pair, two 128-row M-subtiles per CTA: a 512 x 256 output tile per pair whose B stage (256
 # columns) is shared by 512 rows -- 25 % less operand traffic into the SMs than the 256 x 256 tile
 # (profiles/r01_headline_vs_cublas.json); one TMEM accumulator (2 x 256 columns).
-HEADLINE_SCHEDULE = dict(engine=1, tile_m=512, tile_n=256, tile_k=64, stages=4, swizzle=128, buffer_c=1,
+# Three 48 KB stages leave room for the 64 KB SMEM tile of the overlapped epilogue (TMEM is released
+# before the output's TMA stores, which then run under the next tile's MMAs).
+HEADLINE_SCHEDULE = dict(engine=1, tile_m=512, tile_n=256, tile_k=64, stages=3, swizzle=128, buffer_c=1,
                          acc_buffers=1, persistent=1, raster_group=8, order=0, cluster_m=2)
 # the previous default (256 x 256 pair tile, double-buffered accumulator)
 PAIR256_SCHEDULE = dict(engine=1, tile_m=256, tile_n=256, tile_k=128, stages=3, swizzle=128, buffer_c=1,

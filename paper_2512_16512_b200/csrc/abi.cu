@@ -635,6 +635,7 @@ static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cud
         const int es = dsize(d.in_dtype);
         tp.a_stage_bytes = (uint32_t)(128 * p.msub * p.sch.tile_k * es);
         tp.ms = p.msub;
+        tp.ovl = p.ovl ? 1 : 0;
         tp.b_stage_bytes = (uint32_t)(p.sch.tile_k * (p.sch.tile_n / p.cta_group) * es);
         tp.lo_off = p.split3 ? (uint32_t)(p.sch.stages * (tp.a_stage_bytes + tp.b_stage_bytes)) : 0u;
         tp.cg = conv_geom(d);

@@ -59,7 +59,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     uint8_t* sB = sA + (size_t)S * p.a_stage_bytes;
     // SPLIT3 (3xTF32): the lo rings (A_lo, B_lo) follow the B ring, p.lo_off bytes after their hi rings
     uint8_t* sC = sB + (b_res ? 0 : (size_t)S * p.b_stage_bytes) + (SPLIT3 ? (size_t)p.lo_off : 0);
-    uint64_t* full = reinterpret_cast<uint64_t*>(sC + (p.buffer_c ? kTcEpiSmem : 0));
+    uint64_t* full = reinterpret_cast<uint64_t*>(sC + (p.buffer_c ? (p.ovl ? 2 * kTcEpiSmem : kTcEpiSmem) : 0));
     uint64_t* empty = full + 8;
     uint64_t* tfull = empty + 8;
     uint64_t* tempty = tfull + 2;
@@ -440,6 +440,77 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             ptx::mbar_wait(&tfull[acc], aph);
             if (trace && warp == 4 && lane == 0 && trace_k < kTraceTiles) trace[8 + 2 * kTraceK + 2 * trace_k] = ptx::globaltimer();
             ptx::tc_fence_after();
+            if constexpr (MS == 2 && !CONV) {
+                if (p.ovl && p.n_gather == 0) {
+                    // ---- overlapped epilogue: TMEM -> SMEM tile (subtile 1) + registers (subtile 0),
+                    // TMEM released, then the TMA stores run while the next tile's MMAs do ----
+                    uint8_t* big = sC + q * (4 * kTcEpiStageBytes);    // 4 boxes [32 rows][128 B] = 256 columns
+                    if (lane == 0) ptx::bulk_wait_read<0>();          // the previous tile's stores have read it
+                    __syncwarp();
+                    const uint32_t t_q = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * 2 * 256);
+                    for (int c = 0; c < 256; c += 32) {
+                        uint32_t v[32];
+                        ptx::tmem_ld_32x32b_x32(t_q + (uint32_t)(256 + c), v);
+                        ptx::tmem_ld_wait();
+                        uint8_t* rowp = big + (c >> 6) * kTcEpiStageBytes + lane * 128;
+                        const int cbase = (c & 63) ? 4 : 0;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            uint4 w;
+                            w.x = ptx::pack_bf16x2(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1]));
+                            w.y = ptx::pack_bf16x2(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3]));
+                            w.z = ptx::pack_bf16x2(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5]));
+                            w.w = ptx::pack_bf16x2(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7]));
+                            *reinterpret_cast<uint4*>(rowp + (((cbase + j) ^ (lane & 7)) * 16)) = w;
+                        }
+                    }
+                    uint32_t R[8][16];                                   // subtile 0, packed bf16x2
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        uint32_t v[32];
+                        ptx::tmem_ld_32x32b_x32(t_q + (uint32_t)(32 * i), v);
+                        ptx::tmem_ld_wait();
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            R[i][j] = ptx::pack_bf16x2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+                    }
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) {                                     // TMEM free: the next tile's MMAs start
+                        if constexpr (CG == 2) ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&tempty[acc]), 0));
+                        else ptx::mbar_arrive(&tempty[acc]);
+                    }
+                    ptx::fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {                                     // subtile 1: rows m0t + 128 + 32q
+                        for (int b = 0; b < 4; ++b)
+                            ptx::tma_store_3d(&tmC, big + b * kTcEpiStageBytes, n0 + 64 * b, m0t + 128 + 32 * q, 0);
+                        ptx::bulk_commit();
+                        ptx::bulk_wait_read<0>();                        // ... have read the SMEM tile
+                    }
+                    __syncwarp();
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        uint8_t* rowp = big + (i >> 1) * kTcEpiStageBytes + lane * 128;
+                        const int cbase = (i & 1) ? 4 : 0;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const uint4 w = make_uint4(R[i][4 * j], R[i][4 * j + 1], R[i][4 * j + 2], R[i][4 * j + 3]);
+                            *reinterpret_cast<uint4*>(rowp + (((cbase + j) ^ (lane & 7)) * 16)) = w;
+                        }
+                    }
+                    ptx::fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {                                     // subtile 0: rows m0t + 32q
+                        for (int b = 0; b < 4; ++b)
+                            ptx::tma_store_3d(&tmC, big + b * kTcEpiStageBytes, n0 + 64 * b, m0t + 32 * q, 0);
+                        ptx::bulk_commit();
+                    }
+                    if (trace && warp == 4 && lane == 0 && trace_k < kTraceTiles) trace[8 + 2 * kTraceK + 2 * trace_k++ + 1] = ptx::globaltimer();
+                    if (++acc == p.acc_buffers) { acc = 0; aph ^= 1; }
+                    continue;
+                }
+            }
             for (int h = 0; h < MS; ++h) {                 // M-subtiles: accumulator h holds rows m0t + 128h ..
             const int m0 = m0t + 128 * h;
             const int64_t row = (int64_t)m0 + 32 * q + lane;

@@ -106,6 +106,7 @@ struct Plan {
     int32_t halo_wp = 0, halo_rt = 0, halo_msub = 0, halo_pr = 0, halo_planes = 0, halo_nbuf = 0, halo_tpi = 0;
     int32_t halo_cl = 1;                // CTAs per cluster sharing the filter stream (TMA multicast, or a pair)
     bool halo_pair = false;             // inner_m 256: cta_group::2 UMMAs (M = 256) over a CTA pair
+    bool ovl = false;                   // overlapped epilogue (see TcParams::ovl); 64 KB epilogue SMEM
     int32_t msub = 1;                   // tcgen05 matmul: 128-row M-subtiles per CTA (tile_m = 128*cta_group*msub)
     int32_t cluster_n = 1;              // tcgen05 matmul: CTAs on adjacent N tiles sharing A by multicast;
                                         // tiles (num_tiles) then count cluster tiles of cluster_n N tiles
@@ -164,6 +165,8 @@ struct TcParams {
     int32_t wp, rt, msub, planes, nbuf, tpi, cl, pair;
     int32_t cn;              // cluster_n: CTAs of a cluster on adjacent N tiles, A stages multicast (1 = none)
     int32_t ms;              // M-subtiles per CTA (tile_m = 128 * cta_group * ms; matmul: 1 or 2)
+    int32_t ovl;             // overlapped epilogue (two M-subtiles, bf16, tile_n 256): subtile 1 drained to a
+                             // 64 KB SMEM tile, subtile 0 to registers, TMEM released before the stores
     uint32_t patch_bytes, plane_bytes;
     // Diagnostics (XTC_TRACE): %globaltimer stamps for CTAs < kTraceCtas, laid out
     // [cta][kTraceSlots]: slot 0 kernel entry, 1 setup done; producer issue of k-block i at

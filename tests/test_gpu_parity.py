@@ -681,6 +681,7 @@ GATHER_CASES = [
     (dict(tile_n=256, stages=3, acc_buffers=2, persistent=1), 1, "bf16", 256),
     # the bench headline tile: CTA pair with two M-subtiles (512-row tiles)
     (dict(tile_m=512, cluster_m=2, tile_n=256, tile_k=64, stages=4, persistent=1, raster_group=8), 2, "bf16", 512),
+    (dict(tile_m=512, cluster_m=2, tile_n=256, tile_k=64, stages=3, persistent=1, raster_group=8), 2, "bf16", 512),
 ]
 
 
@@ -781,6 +782,9 @@ MSUB_SCHEDS = [
     dict(tile_m=512, cluster_m=2, tile_n=128, tile_k=64, stages=4, persistent=1, acc_buffers=2, pack_warps=2),
     dict(tile_m=256, tile_n=128, stages=3, split_k=2),
     dict(tile_m=256, tile_n=64, stages=4, buffer_c=0),
+    # overlapped epilogue (bf16 out, 256 columns, 3 stages leave room for the 64 KB SMEM tile)
+    dict(tile_m=512, cluster_m=2, tile_n=256, tile_k=64, stages=3, persistent=1, raster_group=8),
+    dict(tile_m=512, cluster_m=2, tile_n=256, tile_k=64, stages=3),
 ]
 
 
@@ -832,3 +836,12 @@ def test_conv_degenerate_single_pixel():
     run_conv(d, "bf16", "f32", tc(tile_n=64, stages=3), MODE_INT)
     d = xtc.conv2d_desc(1, 1, 1, 64, 128, 1, 1, 1, 0, "bf16", "bf16")
     run_conv(d, "bf16", "bf16", tc(tile_n=128, stages=2), MODE_INT)
+
+
+def test_tc_overlapped_epilogue_many_tiles_and_ragged():
+    """The overlapped epilogue across several tiles per CTA (persistent, TMEM released before the stores),
+    with ragged M and N, uniform data within 5e-3."""
+    sch = tc(tile_m=512, cluster_m=2, tile_n=256, tile_k=64, stages=3, persistent=1, raster_group=2)
+    run_matmul(2048 + 300, 2048 + 64, 512, "bf16", "bf16", sch, MODE_INT)
+    err, _ = run_matmul(3072, 2560, 1024, "bf16", "bf16", sch, MODE_UNIFORM)
+    assert err <= 5e-3

@@ -1,6 +1,6 @@
 # round-1 final (2): GPU parity, smoke, bench line, reference arm, launch list, headline ncu capture
 mkdir -p gpurun_out
-P='{"engine":1,"tile_m":512,"tile_n":256,"tile_k":64,"stages":4,"swizzle":128,"buffer_c":1,"acc_buffers":1,"persistent":1,"raster_group":8,"order":0,"cluster_m":2}'
+P='{"engine":1,"tile_m":512,"tile_n":256,"tile_k":64,"stages":3,"swizzle":128,"buffer_c":1,"acc_buffers":1,"persistent":1,"raster_group":8,"order":0,"cluster_m":2}'
 timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo rc=$? >> gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo rc=$? >> gpurun_out/smoke.log
 timeout 900 python bench.py > gpurun_out/bench.log 2> gpurun_out/bench.err; echo rc=$? >> gpurun_out/bench.err
