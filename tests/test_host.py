@@ -369,3 +369,18 @@ def test_bench_schedule_for_rows_wave_rule():
     for s in (bench.HEADLINE_SCHEDULE, bench.PAIR256_SCHEDULE):
         st, _, why = xtc.xtc_schedule_check(xtc.matmul_desc(8192, 8192, 8192), xtc.schedule(**s))
         assert st == xtc.XTC_OK, why
+
+
+def test_overlapped_epilogue_smem_placement():
+    """The headline plan reserves the 64 KB SMEM output tile of the overlapped epilogue (3 x 48 KB stages +
+    64 KB + 2 KB); 4 stages leave no room (32 KB staging, plain epilogue); f32 output never overlaps."""
+    import bench
+    d = xtc.matmul_desc(8192, 8192, 8192)
+    st, info, why = xtc.xtc_schedule_check(d, xtc.schedule(**bench.HEADLINE_SCHEDULE))
+    assert st == xtc.XTC_OK, why
+    assert info.smem_bytes == 3 * (256 * 64 * 2 + 64 * 128 * 2) + 65536 + 2048
+    st, info, why = xtc.xtc_schedule_check(d, xtc.schedule(**dict(bench.HEADLINE_SCHEDULE, stages=4)))
+    assert st == xtc.XTC_OK and info.smem_bytes == 4 * 49152 + 32768 + 2048, why
+    d32 = xtc.matmul_desc(8192, 8192, 8192, "bf16", "f32")
+    st, info, why = xtc.xtc_schedule_check(d32, xtc.schedule(**bench.HEADLINE_SCHEDULE))
+    assert st == xtc.XTC_OK and info.smem_bytes == 3 * 49152 + 32768 + 2048, why
