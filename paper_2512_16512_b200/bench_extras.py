@@ -13,7 +13,9 @@ MATMUL_SCHEDS = {
            dict(TC, tile_n=64, tile_k=128, stages=4, buffer_c=1, acc_buffers=2, persistent=0, raster_group=8),
            dict(TC, tile_n=64, tile_k=128, stages=4, buffer_c=1, acc_buffers=2, persistent=0, raster_group=8,
                 pack_warps=2),
-           dict(TC, tile_n=128, stages=6, buffer_c=1, acc_buffers=2, persistent=1, raster_group=4, pack_warps=2)],
+           dict(TC, tile_n=128, stages=6, buffer_c=1, acc_buffers=2, persistent=1, raster_group=4, pack_warps=2),
+           # best of the 4096-candidate sweep over the widened space (profiles/r01_sweep4096_widened_space.json)
+           dict(TC, tile_n=64, tile_k=128, stages=3, buffer_c=1, acc_buffers=2, persistent=0, raster_group=2)],
     512: [dict(TC, tile_n=64, stages=8, buffer_c=1, acc_buffers=1, pack_warps=2),
           dict(TC, tile_n=64, stages=4, buffer_c=1, acc_buffers=1, split_k=2, pack_warps=2),
           dict(TC, tile_n=64, tile_k=128, stages=4, buffer_c=1, acc_buffers=1, pack_warps=2)],
