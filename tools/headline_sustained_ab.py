@@ -13,6 +13,8 @@ c = torch.empty((n, n), dtype=torch.bfloat16, device="cuda")
 xtc.xtc_fill(a.data_ptr(), a.numel(), xtc.XTC_BF16, 1, 0, 0, st)
 xtc.xtc_fill(b.data_ptr(), b.numel(), xtc.XTC_BF16, 2, 0, 0, st)
 ops = {"pair512_ms2": xtc.Op(xtc.matmul_desc(n, n, n)).apply(xtc.schedule(**bench.HEADLINE_SCHEDULE)),
+       "pair512_ms2_4stage_plain_epilogue": xtc.Op(xtc.matmul_desc(n, n, n)).apply(
+           xtc.schedule(**dict(bench.HEADLINE_SCHEDULE, stages=4))),
        "pair256": xtc.Op(xtc.matmul_desc(n, n, n)).apply(xtc.schedule(**bench.PAIR256_SCHEDULE))}
 res = {k: [] for k in ops}
 for rnd in range(4):
