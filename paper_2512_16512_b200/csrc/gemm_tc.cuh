@@ -441,7 +441,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             if (trace && warp == 4 && lane == 0 && trace_k < kTraceTiles) trace[8 + 2 * kTraceK + 2 * trace_k] = ptx::globaltimer();
             ptx::tc_fence_after();
             if constexpr (MS == 2 && !CONV) {
-                if (p.ovl && p.n_gather == 0) {
+                if (p.ovl) {
                     // ---- overlapped epilogue: TMEM -> SMEM tile (subtile 1) + registers (subtile 0),
                     // TMEM released, then the TMA stores run while the next tile's MMAs do ----
                     uint8_t* big = sC + q * (4 * kTcEpiStageBytes);    // 4 boxes [32 rows][128 B] = 256 columns
@@ -482,10 +482,23 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                     }
                     ptx::fence_proxy_async_smem();
                     __syncwarp();
-                    if (lane == 0) {                                     // subtile 1: rows m0t + 128 + 32q
-                        for (int b = 0; b < 4; ++b)
-                            ptx::tma_store_3d(&tmC, big + b * kTcEpiStageBytes, n0 + 64 * b, m0t + 128 + 32 * q, 0);
+                    // the four 64-column boxes of 32 rows starting at `row`: to C, or (fused all-gather)
+                    // to every destination at gather_row0 + row
+                    auto store_rows = [&](int row) {
+                        if (p.n_gather) {
+                            const CUtensorMap* gm = reinterpret_cast<const CUtensorMap*>(p.gather);
+                            for (int d = 0; d < p.n_gather; ++d)
+                                for (int b = 0; b < 4; ++b)
+                                    ptx::tma_store_3d(gm + d, big + b * kTcEpiStageBytes, n0 + 64 * b,
+                                                      p.gather_row0 + row, 0);
+                        } else {
+                            for (int b = 0; b < 4; ++b)
+                                ptx::tma_store_3d(&tmC, big + b * kTcEpiStageBytes, n0 + 64 * b, row, 0);
+                        }
                         ptx::bulk_commit();
+                    };
+                    if (lane == 0) {                                     // subtile 1: rows m0t + 128 + 32q
+                        store_rows(m0t + 128 + 32 * q);
                         ptx::bulk_wait_read<0>();                        // ... have read the SMEM tile
                     }
                     __syncwarp();
@@ -501,11 +514,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                     }
                     ptx::fence_proxy_async_smem();
                     __syncwarp();
-                    if (lane == 0) {                                     // subtile 0: rows m0t + 32q
-                        for (int b = 0; b < 4; ++b)
-                            ptx::tma_store_3d(&tmC, big + b * kTcEpiStageBytes, n0 + 64 * b, m0t + 32 * q, 0);
-                        ptx::bulk_commit();
-                    }
+                    if (lane == 0) store_rows(m0t + 32 * q);              // subtile 0: rows m0t + 32q
                     if (trace && warp == 4 && lane == 0 && trace_k < kTraceTiles) trace[8 + 2 * kTraceK + 2 * trace_k++ + 1] = ptx::globaltimer();
                     if (++acc == p.acc_buffers) { acc = 0; aph ^= 1; }
                     continue;
