@@ -682,6 +682,8 @@ GATHER_CASES = [
     # the bench headline tile: CTA pair with two M-subtiles (512-row tiles)
     (dict(tile_m=512, cluster_m=2, tile_n=256, tile_k=64, stages=4, persistent=1, raster_group=8), 2, "bf16", 512),
     (dict(tile_m=512, cluster_m=2, tile_n=256, tile_k=64, stages=3, persistent=1, raster_group=8), 2, "bf16", 512),
+    # overlapped epilogue + gather with a ragged last N tile (576 = 2 x 256 + 64)
+    (dict(tile_m=512, cluster_m=2, tile_n=256, tile_k=64, stages=3, persistent=1, raster_group=2), 2, "bf16", 576),
 ]
 
 
@@ -845,3 +847,23 @@ def test_tc_overlapped_epilogue_many_tiles_and_ragged():
     run_matmul(2048 + 300, 2048 + 64, 512, "bf16", "bf16", sch, MODE_INT)
     err, _ = run_matmul(3072, 2560, 1024, "bf16", "bf16", sch, MODE_UNIFORM)
     assert err <= 5e-3
+
+
+def test_headline_schedule_with_consumers_takes_the_plain_epilogue():
+    """The headline schedule with fused relu / bias: the planner keeps the plain epilogue (consumers are
+    applied per 32-column chunk before rounding); results exact on integers."""
+    import bench
+    import oracle
+    M, N, K = 1024, 512, 256
+    for cons in ("relu", "relu+bias"):
+        d = xtc.matmul_desc(M, N, K, "bf16", "bf16", consumer=cons)
+        a = dev_tensor((M, K), "bf16", 41, MODE_INT)
+        b = dev_tensor((K, N), "bf16", 42, MODE_INT)
+        bias = torch.arange(N, dtype=torch.float32, device="cuda:0") % 7 - 3
+        c = torch.full((M, N), float("nan"), dtype=torch.bfloat16, device="cuda:0")
+        xtc.Op(d).apply(xtc.schedule(**dict(bench.HEADLINE_SCHEDULE, fuse=1))).run(
+            a, b, c, bias=bias if "bias" in cons else None)
+        torch.cuda.synchronize()
+        O, D = oracle_matmul(M, N, K, "bf16", MODE_INT, 41, 42)
+        O = oracle.consume(O, relu_=True, bias=bias.cpu().numpy().astype(np.float64) if "bias" in cons else None)
+        check_against_oracle(c, O, D, "bf16", exact=True, tol=0)
