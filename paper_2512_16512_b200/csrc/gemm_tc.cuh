@@ -445,6 +445,14 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                     // ---- overlapped epilogue: TMEM -> SMEM tile (subtile 1) + registers (subtile 0),
                     // TMEM released, then the TMA stores run while the next tile's MMAs do ----
                     uint8_t* big = sC + q * (4 * kTcEpiStageBytes);    // 4 boxes [32 rows][128 B] = 256 columns
+                    // fused relu / bias on a 32-column chunk of output row `r`, before the rounding
+                    auto consume = [&](uint32_t (&v)[32], int64_t r, int c) {
+                        if (p.cons && r < p.M) {
+                            const int64_t cc = (int64_t)n0 + c;
+                            const int nc = (int)((p.N - cc) < 32 ? (p.N - cc) : 32);
+                            if (nc > 0) apply_consumer32(v, p.cons, p.bias, p.C, true, r, p.ldc, cc, nc, true, true);
+                        }
+                    };
                     if (lane == 0) ptx::bulk_wait_read<0>();          // the previous tile's stores have read it
                     __syncwarp();
                     const uint32_t t_q = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * 2 * 256);
@@ -452,6 +460,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                         uint32_t v[32];
                         ptx::tmem_ld_32x32b_x32(t_q + (uint32_t)(256 + c), v);
                         ptx::tmem_ld_wait();
+                        consume(v, m0t + 128 + 32 * q + lane, c);
                         uint8_t* rowp = big + (c >> 6) * kTcEpiStageBytes + lane * 128;
                         const int cbase = (c & 63) ? 4 : 0;
 #pragma unroll
@@ -470,6 +479,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                         uint32_t v[32];
                         ptx::tmem_ld_32x32b_x32(t_q + (uint32_t)(32 * i), v);
                         ptx::tmem_ld_wait();
+                        consume(v, m0t + 32 * q + lane, 32 * i);
 #pragma unroll
                         for (int j = 0; j < 16; ++j)
                             R[i][j] = ptx::pack_bf16x2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));

@@ -316,7 +316,8 @@ static xtc_status plan_tc(const xtc_op_desc& d, const xtc_schedule& s, int num_s
         // bufferize, overlapped: with two M-subtiles, bf16 output and 256-column tiles, the epilogue drains
         // TMEM into a 64 KB SMEM tile + registers and releases it before its (slow) TMA stores, so the
         // next tile's MMAs overlap the stores -- when the 64 KB fit
-        if (ms == 2 && s.buffer_c && d.out_dtype == XTC_BF16 && p.split_k == 1 && s.tile_n == 256 && d.consumer == 0 &&
+        if (ms == 2 && s.buffer_c && d.out_dtype == XTC_BF16 && p.split_k == 1 && s.tile_n == 256 &&
+            !(d.consumer & XTC_CONSUMER_ACCUMULATE) && (d.consumer == 0 || s.fuse) &&
             accb == 1 && s.stages * per_stage + 2 * kTcEpiSmem + kSmemReserve <= kSmemMaxOptin &&
             getenv("XTC_NO_OVERLAP_EPILOGUE") == nullptr) {
             p.ovl = true;

@@ -849,9 +849,9 @@ def test_tc_overlapped_epilogue_many_tiles_and_ragged():
     assert err <= 5e-3
 
 
-def test_headline_schedule_with_consumers_takes_the_plain_epilogue():
-    """The headline schedule with fused relu / bias: the planner keeps the plain epilogue (consumers are
-    applied per 32-column chunk before rounding); results exact on integers."""
+def test_headline_schedule_with_fused_consumers():
+    """The headline schedule with fused relu / bias: applied per 32-column chunk before the rounding inside
+    the overlapped epilogue (both the SMEM-tile and the register-held subtile); exact on integers."""
     import bench
     import oracle
     M, N, K = 1024, 512, 256
