@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define XTC_ABI_VERSION 1
+#define XTC_ABI_VERSION 2
 
 typedef enum {
     XTC_OK = 0,
@@ -120,6 +120,10 @@ typedef enum { XTC_SPLITK_ORDERED = 0, XTC_SPLITK_ATOMIC = 1 } xtc_splitk_mode;
  *                                                   tcgen05: k-steps per stage, must be 0/1 (= fully unrolled)
  * vectorize    vector_n               : SIMT: 1 or 4 (float4 SMEM/global access along N); tcgen05: 0
  * parallelize  persistent             : 0 = one CTA per tile, 1 = #SM CTAs loop over tiles
+ *                          grid_sms               : persistent only: the number of SMs ("cores") the
+ *                                                   persistent grid spreads over, 0 = all of the device's;
+ *                                                   e.g. SMs left free for a concurrent collective, or few
+ *                                                   SMs so that every CTA strides over many tiles
  *                          cluster_m              : tcgen05: 1, or 2 = CTA pair (cta_group::2, tile_m = 256)
  *                          cluster_n              : tcgen05 matmul (cluster_m 1): 0/1, or 2 / 4 CTAs on adjacent
  *                                                   N tiles of one M tile form a cluster; each TMA-loads
@@ -166,6 +170,7 @@ typedef struct {
     int32_t fuse;
     int32_t pack_halo;
     int32_t cluster_n;
+    int32_t grid_sms;
 } xtc_schedule;
 
 /* What the planner derived for a legal schedule (for reports and tests). */

@@ -3,7 +3,7 @@
 Only ``tests/``, ``__graft_entry__.smoke()`` and the ``cpu_baseline`` /
 ``--impl reference`` legs of ``bench.py`` may import this package.  The
 product package ``paper_2512_16512_b200`` never imports it (checked by
-``tests/test_boundary.py``), and it shares no code with the CUDA path.
+``tests/test_host.py::test_product_never_imports_oracle``), and it shares no code with the CUDA path.
 
 The arithmetic lives in ``xtc_oracle.c`` (fp64 naive loop nests, PAPER.md
 Fig.2; conv2d P:251-253/P:1152 with the zero-padding reading of

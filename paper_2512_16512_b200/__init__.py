@@ -56,7 +56,7 @@ class xtc_op_desc(Structure):
 SCHEDULE_FIELDS = ["engine", "tile_m", "tile_n", "tile_k", "inner_m", "inner_n", "order", "raster_group",
                    "unroll_k", "vector_n", "stages", "swizzle", "buffer_c", "acc_buffers", "split_k",
                    "split_k_mode", "cluster_m", "persistent", "split_n_at", "pack_warps", "b_resident", "fuse",
-                   "pack_halo", "cluster_n"]
+                   "pack_halo", "cluster_n", "grid_sms"]
 
 
 class xtc_schedule(Structure):

@@ -393,6 +393,11 @@ xtc_status make_plan(const xtc_op_desc& d, const xtc_schedule& s, int num_sms, P
     if (s.order != XTC_ORDER_MN && s.order != XTC_ORDER_NM) ILLEGAL("interchange: order must be 0 (MN) or 1 (NM)");
     if (s.raster_group < 0 || s.raster_group > 64) ILLEGAL("raster_group must be in [0,64]");
     if (s.persistent != 0 && s.persistent != 1) ILLEGAL("persistent must be 0 or 1");
+    // parallelize over a number of cores: the persistent grid spreads over at most
+    // grid_sms SMs of the device (0 = all of them)
+    if (s.grid_sms < 0 || s.grid_sms > 4096) ILLEGAL("parallelize: grid_sms must be in [0,4096]");
+    if (s.grid_sms && !s.persistent) ILLEGAL("parallelize: grid_sms needs persistent 1 (one CTA per tile otherwise)");
+    if (s.grid_sms) num_sms = std::min(num_sms, (int)s.grid_sms);
     p.split_k = s.split_k == 0 ? 1 : s.split_k;
     if (p.split_k < 1 || p.split_k > 64) ILLEGAL("split_k must be in [1,64]");
     if (s.split_k_mode != XTC_SPLITK_ORDERED && s.split_k_mode != XTC_SPLITK_ATOMIC) ILLEGAL("unknown split_k_mode");
@@ -428,6 +433,8 @@ xtc_status make_plan(const xtc_op_desc& d, const xtc_schedule& s, int num_sms, P
     else if (s.engine == XTC_ENGINE_TCGEN05) st = plan_tc(d, s, num_sms, p, why);
     else ILLEGAL("unknown engine %d", s.engine);
     if (st != XTC_OK) return st;
+    if (p.grid_x < std::max(1, p.cluster))
+        ILLEGAL("parallelize: grid_sms %d leaves no room for one cluster of %d CTAs", s.grid_sms, p.cluster);
     if (p.split_k > 1 && !p.atomic) {
         p.ws_ld = cdiv(p.N, 4) * 4;
         p.workspace_bytes = (int64_t)p.split_k * p.M * p.ws_ld * 4;

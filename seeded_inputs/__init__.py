@@ -6,7 +6,7 @@ value, so that the CPU oracle (``oracle/``) and the GPU path
 (``xtc_fill`` in ``include/xtc.h``) can regenerate bit-identical operands
 without ever exchanging data.  The CUDA side implements the *same*
 counter-based generator independently in ``paper_2512_16512_b200/csrc``;
-``tests/test_inputs_gpu.py`` checks the two agree bit for bit.
+``tests/test_gpu_parity.py::test_gpu_generator_matches_seeded_inputs`` checks the two agree bit for bit.
 
 Generator (SURVEY.md §8(c) reading 9):
 

@@ -7,7 +7,7 @@ import torch
 
 import oracle
 import paper_2512_16512_b200 as xtc
-from seeded_inputs import gen_tensor
+from seeded_inputs import MODE_INT, gen_tensor
 
 TORCH_DT = {"bf16": torch.bfloat16, "f32": torch.float32, "tf32": torch.float32}
 
@@ -93,3 +93,20 @@ def run_matmul(M, N, K, in_dtype, out_dtype, sch, mode, seed=0, measure=True, ex
         if exact:
             assert m.n_mismatch == 0
     return err, m
+
+
+def run_conv(d, in_dtype, out_dtype, sch, mode, seed=10):
+    x = dev_tensor((d.batch, d.h, d.w, d.c), in_dtype, seed, mode)
+    w = dev_tensor((d.r, d.s, d.c, d.f), in_dtype, seed + 1, mode)
+    M, N, K = xtc.gemm_view(d)
+    y = torch.full((M, N), float("nan"), dtype=TORCH_DT[out_dtype], device="cuda:0")
+    op = xtc.Op(d).apply(sch)
+    op.run(x, w, y)
+    torch.cuda.synchronize()
+    O, D = oracle_conv(d, in_dtype, mode, seed, seed + 1)
+    exact = mode == MODE_INT
+    tol = 1e-5 if in_dtype == "f32" else 5e-3
+    err = check_against_oracle(y, O, D, out_dtype, exact, tol)
+    m = op.measure(x, w, y, xtc.measure_cfg(warmup=1, repeats=2, validate=1, exact=int(exact), tol=tol))
+    assert m.valid == 1, m.as_dict()
+    return err

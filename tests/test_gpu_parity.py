@@ -5,8 +5,8 @@ import torch
 
 import paper_2512_16512_b200 as xtc
 from seeded_inputs import MODE_INT, MODE_UNIFORM, gen_tensor
-from gpu_util import (TORCH_DT, check_against_oracle, dev_tensor, oracle_conv, oracle_matmul, out_as_f64, run_matmul,
-                      to_numpy_out)
+from gpu_util import (TORCH_DT, check_against_oracle, dev_tensor, oracle_conv, oracle_matmul, out_as_f64, run_conv,
+                      run_matmul, to_numpy_out)
 
 pytestmark = pytest.mark.gpu
 
@@ -147,23 +147,6 @@ def test_tc_tf32_integer_and_float(sch):
 
 
 # ------------------------------------------------------------------ conv --
-def run_conv(d, in_dtype, out_dtype, sch, mode, seed=10):
-    x = dev_tensor((d.batch, d.h, d.w, d.c), in_dtype, seed, mode)
-    w = dev_tensor((d.r, d.s, d.c, d.f), in_dtype, seed + 1, mode)
-    M, N, K = xtc.gemm_view(d)
-    y = torch.full((M, N), float("nan"), dtype=TORCH_DT[out_dtype], device="cuda:0")
-    op = xtc.Op(d).apply(sch)
-    op.run(x, w, y)
-    torch.cuda.synchronize()
-    O, D = oracle_conv(d, in_dtype, mode, seed, seed + 1)
-    exact = mode == MODE_INT
-    tol = 1e-5 if in_dtype == "f32" else 5e-3
-    err = check_against_oracle(y, O, D, out_dtype, exact, tol)
-    m = op.measure(x, w, y, xtc.measure_cfg(warmup=1, repeats=2, validate=1, exact=int(exact), tol=tol))
-    assert m.valid == 1, m.as_dict()
-    return err
-
-
 @pytest.mark.parametrize("shape", [(2, 56, 56, 64, 64), (3, 14, 14, 256, 256)])
 @pytest.mark.parametrize("mode", [MODE_INT, MODE_UNIFORM])
 def test_tc_conv_resnet_layers(shape, mode):
@@ -840,9 +823,10 @@ def test_conv_degenerate_single_pixel():
     run_conv(d, "bf16", "bf16", tc(tile_n=128, stages=2), MODE_INT)
 
 
-def test_tc_overlapped_epilogue_many_tiles_and_ragged():
-    """The overlapped epilogue across several tiles per CTA (persistent, TMEM released before the stores),
-    with ragged M and N, uniform data within 5e-3."""
+def test_tc_overlapped_epilogue_ragged():
+    """The overlapped epilogue (persistent, TMEM released before the stores) with ragged M and N; integer data
+    bit-exact, uniform data within 5e-3.  These shapes give 45 and 60 tiles to 74 CTA pairs, i.e. ONE tile per
+    pair: the cross-tile paths (SMEM tile reuse, TMEM phase flips) are covered by tests/test_gpu_multitile.py."""
     sch = tc(tile_m=512, cluster_m=2, tile_n=256, tile_k=64, stages=3, persistent=1, raster_group=2)
     run_matmul(2048 + 300, 2048 + 64, 512, "bf16", "bf16", sch, MODE_INT)
     err, _ = run_matmul(3072, 2560, 1024, "bf16", "bf16", sch, MODE_UNIFORM)

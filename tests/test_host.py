@@ -384,3 +384,18 @@ def test_overlapped_epilogue_smem_placement():
     d32 = xtc.matmul_desc(8192, 8192, 8192, "bf16", "f32")
     st, info, why = xtc.xtc_schedule_check(d32, xtc.schedule(**bench.HEADLINE_SCHEDULE))
     assert st == xtc.XTC_OK and info.smem_bytes == 3 * 49152 + 32768 + 2048, why
+
+
+# --------------------------------------------------------- the knob itself --
+def test_grid_sms_plan_and_legality():
+    import bench
+    HEADLINE = bench.HEADLINE_SCHEDULE
+    """grid_sms caps the persistent grid (parallelize over a number of cores, P:542-547)."""
+    d = xtc.matmul_desc(4096, 4096, 256)
+    st, info, _ = xtc.xtc_schedule_check(d, xtc.schedule(**HEADLINE), 148)
+    assert st == 0 and info.grid_x == 148 and info.num_tiles == 128
+    st, info, _ = xtc.xtc_schedule_check(d, xtc.schedule(**dict(HEADLINE, grid_sms=9)), 148)
+    assert st == 0 and info.grid_x == 8          # whole CTA pairs only
+    for bad in (dict(HEADLINE, grid_sms=1), dict(HEADLINE, grid_sms=8, persistent=0), dict(HEADLINE, grid_sms=-1)):
+        st, _, why = xtc.xtc_schedule_check(d, xtc.schedule(**bad), 148)
+        assert st == xtc.XTC_E_ILLEGAL_SCHEDULE and "grid_sms" in why
