@@ -71,7 +71,7 @@ def parse():
     ap.add_argument("--impl", default="xtc", choices=["xtc", "reference"])
     ap.add_argument("--no-extras", action="store_true", help="skip the secondary config lines (1024^3, conv, sweep)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--sweep-candidates", type=int, default=1024)
+    ap.add_argument("--sweep-candidates", type=int, default=4096, help="BASELINE config 4: 4096 candidates")
     ap.add_argument("--overlap-chunks", type=int, default=4,
                     help="N>1: block-cyclic row chunks per rank, each all-gathered while the next computes")
     ap.add_argument("--gather", default="fused", choices=["fused", "nccl"],
@@ -146,41 +146,62 @@ class ClockSampler:
 
 
 # --------------------------------------------------------- reference arm ---
-def cpu_oracle_sample(rows: int = 32, seed_a: int = 1, seed_b: int = 2):
-    """The oracle as it stands (fp64 naive loop nest) on `rows` sampled rows of
-    the 8192^3 workload.  Returns (TFLOP/s, seconds, threads, description)."""
+WORKLOAD = "matmul 8192x8192x8192 bf16->bf16 (BASELINE config 5: largest matmul)"
+METRIC = "matmul TFLOP/s (8192^3 bf16)"
+
+
+def sample_rows(rows: int):
+    """`rows` output rows spread evenly over the 8192 (every 512-row tile is visited)."""
+    return [int(i * (M // rows)) + (37 * i) % (M // rows) for i in range(rows)]
+
+
+def cpu_oracle_sample(rows: int = 32, seed_a: int = 1, seed_b: int = 2, mode: int = 0, B64=None):
+    """The oracle as it stands (fp64 naive loop nest) on `rows` sampled rows of the 8192^3 workload.
+    Returns (TFLOP/s, seconds, threads, description, (row ids, O, D))."""
     import oracle
     from seeded_inputs import gen_rows, gen_tensor
-    sel = [int(i * (M // rows)) for i in range(rows)]
-    A = oracle.to_f64(gen_rows(seed_a, (M, K), sel, "bf16"), "bf16")
-    B = oracle.to_f64(gen_tensor(seed_b, (K, N), "bf16"), "bf16")
+    sel = sample_rows(rows)
+    A = oracle.to_f64(gen_rows(seed_a, (M, K), sel, "bf16", mode), "bf16")
+    B = B64 if B64 is not None else oracle.to_f64(gen_tensor(seed_b, (K, N), "bf16", mode), "bf16")
     t0 = time.perf_counter()
-    oracle.matmul(A, B)
+    O, D = oracle.matmul(A, B)
     dt = time.perf_counter() - t0
     flops = 2.0 * rows * N * K
-    return flops / dt / 1e12, dt, oracle.num_threads(), f"{rows} of {M} output rows of the {M}x{N}x{K} matmul (full N, K)"
+    desc = f"{rows} of {M} output rows of the {M}x{N}x{K} matmul (full N, K), {'integer' if mode else 'uniform'} data"
+    return flops / dt / 1e12, dt, oracle.num_threads(), desc, (sel, O, D)
 
 
 def run_reference(args):
+    """The tier's reference arm: the CPU oracle, as it stands, on the host cores.  Each step is the
+    oracle on a bounded sample of the workload -- one output row per host thread (full N and K) --
+    and ms_per_step is the MEASURED time of that sample (nothing is extrapolated); value is the
+    sample's 2*rows*N*K FLOPs over that time.  Under torchrun only rank 0 runs."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     import oracle
+    from seeded_inputs import gen_tensor
     oracle.build()
-    vals = []
+    threads = oracle.num_threads()
+    rows = max(1, threads)
+    B64 = oracle.to_f64(gen_tensor(2, (K, N), "bf16"), "bf16")     # generated once, outside the steps
     for _ in range(max(0, args.warmup)):
-        pass   # the oracle has no warm state worth priming beyond one call below
+        cpu_oracle_sample(rows=rows, B64=B64)
+    secs, vals = [], []
     for _ in range(args.steps):
-        v, dt, threads, sample = cpu_oracle_sample(rows=8)
+        v, dt, threads, sample, _ = cpu_oracle_sample(rows=rows, B64=B64)
+        secs.append(dt)
         vals.append(v)
-    v = statistics.median(vals)
-    line = {"metric": "matmul TFLOP/s (8192^3 bf16)", "value": v, "unit": "TFLOP/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 2 * M * N * K / (v * 1e12) * 1e3,
+    total = sum(secs)
+    v = 2.0 * rows * N * K * args.steps / total / 1e12
+    line = {"metric": METRIC, "value": v, "unit": "TFLOP/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded counter-based generator)", "impl": "reference",
-            "config": {"workload": "matmul 8192x8192x8192 bf16->bf16 (BASELINE config 5)", "global_batch": 1,
-                       "parallelism": "host cores (OpenMP)"},
-            "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": threads, "kind": "oracle", "sample": sample},
+            "data": "synthetic (seeded counter-based generator, uniform[-1,1) bf16)", "impl": "reference",
+            "config": {"workload": WORKLOAD, "global_batch": 1, "parallelism": f"host cores (OpenMP, {threads} threads)",
+                       "step": f"one bounded sample: {sample}"},
+            "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": threads, "kind": "oracle", "sample": sample,
+                             "seconds_per_step": [round(x, 3) for x in secs]},
             "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -214,9 +235,23 @@ def sharded_sweep(xtc, torch, dist, dev, world, rank, n_cand, peak_tf):
     recs = unpack_gathered(gathered.cpu(), n_cand)
     ok = [r for r in recs if int(r["status"]) == 0 and int(r["valid"]) == 1]
     best = max(ok, key=lambda r: r["tflops_med"]) if ok else None
+    # the same candidates on integer data, each run once with exact = 1 (north_star: every legal schedule
+    # bit-identical), outside the timed region; counts reduced over the ranks
+    xtc.xtc_fill(a.data_ptr(), a.numel(), xtc.XTC_BF16, 1, 1, 0, sp)
+    xtc.xtc_fill(b.data_ptr(), b.numel(), xtc.XTC_BF16, 2, 1, 0, sp)
+    imets = op.sweep(scheds, a, b, c, xtc.measure_cfg(warmup=0, repeats=1, validate=1, exact=1), stream=sp)
+    cnt = torch.tensor([sum(int(m.status == 0 and m.valid == 1 and m.n_mismatch == 0) for m in imets),
+                        len(imets), sum(int(m.n_mismatch) for m in imets), sum(int(m.n_nan) for m in imets)],
+                       dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.all_reduce(cnt, op=dist.ReduceOp.SUM)
     return {"candidates": n_cand, "ranks": world, "seconds": float(t[0]), "schedules_per_s": n_cand / float(t[0]),
             "valid": len(ok), "invalid": n_cand - len(ok), "best_tflops": best["tflops_med"] if best else None,
-            "best_id": int(best["id"]) if best else None, "space": "GpuStrategy(TC_SLOTS) legal set, seed 0"}
+            "best_id": int(best["id"]) if best else None, "space": "GpuStrategy(TC_SLOTS) legal set, seed 0",
+            "timed": "uniform data: NaN-fill + validate (5e-3 of D) + 2 warmup + 10 timed reps per candidate",
+            "integer_exact": {"candidates": int(cnt[1]), "bit_exact": int(cnt[0]), "n_mismatch_total": int(cnt[2]),
+                              "n_nan_total": int(cnt[3]),
+                              "what": "every candidate once on integer data, exact = 1 vs RNE(fp64 GPU reference)"}}
 
 
 def sharded_conv(xtc, torch, dist, dev, world, rank, peak_tf, steps=10):
@@ -347,7 +382,12 @@ def main_xtc(args):
     # If the symmetric-memory rendezvous is unavailable the chunked NCCL overlap is used instead
     # (another GPU path, reported in config.parallelism).
     fused, fused_note = None, None
-    if world > 1 and args.gather == "fused":
+    tile_rows = schedule_for_rows(Mr)["tile_m"]
+    if world > 1 and args.gather == "fused" and (Mr % tile_rows or M % world):
+        # xtc_run_gather needs whole CTA tiles per shard (a ragged tile's zero rows would land in a neighbour's)
+        fused_note = (f"fused gather needs the {Mr}-row shard to be a multiple of the {tile_rows}-row tile; "
+                      "NCCL chunked overlap used")
+    elif world > 1 and args.gather == "fused":
         try:
             from paper_2512_16512_b200.parallel import SymmetricOutput
             fused = SymmetricOutput((M, N), torch.bfloat16, dev)
@@ -481,6 +521,11 @@ def main_xtc(args):
             if fused2 is not None:
                 fz = fused if j == 0 else fused2
                 dop.run_gather(da, db, fz.dests, r0, M, stream=sp)
+                if i >= 1:
+                    # this rank's D2H of step i-1 (from the other buffer) must finish before the barrier
+                    # of step i: a peer's step-(i+1) stores into that buffer follow its own barrier i,
+                    # so no peer can overwrite the buffer while it is still being copied out
+                    stream.wait_event(ev_out[j ^ 1])
                 fz.barrier()
             else:
                 dop.run(da, db, dc, stream=sp)
@@ -515,9 +560,38 @@ def main_xtc(args):
     validation = {"valid": int(min(vm.valid for vm in vms)), "max_norm_err": max(vm.max_norm_err for vm in vms),
                   "n_nan": int(sum(vm.n_nan for vm in vms)), "tol": 5e-3,
                   "n_mismatch_vs_rne_of_ref": int(sum(vm.n_mismatch for vm in vms)),
-                  "when": "after the timed region, same inputs"}
+                  "when": "after the timed region, same inputs (uniform data, every output vs the fp64 GPU reference)"}
+    # integer mode (DESIGN reading 8: tolerance runs cannot catch every bug at K = 8192): the same
+    # kernels on integer-valued A, B must be bit-exact -- every output against the on-chip fp64
+    # reference (exact = 1), and sampled rows against the CPU oracle in the cpu_baseline leg below
+    if CH > 1:
+        for j in range(CH):
+            xtc.xtc_fill(a[j * Mc].data_ptr(), Mc * K, xtc.XTC_BF16, 1, 1, (j * world + rank) * Mc * K, sp)
+    else:
+        xtc.xtc_fill(a.data_ptr(), Mr * K, xtc.XTC_BF16, 1, 1, r0 * K, sp)
+    xtc.xtc_fill(b.data_ptr(), K * N, xtc.XTC_BF16, 2, 1, 0, sp)
+    ivms = [o.measure(a[j * Mc:(j + 1) * Mc], b, c[j * Mc:(j + 1) * Mc],
+                      xtc.measure_cfg(warmup=0, repeats=1, validate=1, exact=1), stream=sp)
+            for j, o in enumerate(chunk_ops)]
+    validation["integer"] = {"valid": int(min(vm.valid for vm in ivms)),
+                             "n_mismatch": int(sum(vm.n_mismatch for vm in ivms)),
+                             "n_nan": int(sum(vm.n_nan for vm in ivms)), "exact": 1,
+                             "what": "integer data {-2..2}: every output bit-exact vs RNE(fp64 GPU reference)"}
+    int_rows_out = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rows_sel = sample_rows(128)
+        int_rows_out = c[rows_sel].cpu()
+    # back to the uniform operands for everything below (counters, the cuBLAS comparison)
+    if CH > 1:
+        for j in range(CH):
+            xtc.xtc_fill(a[j * Mc].data_ptr(), Mc * K, xtc.XTC_BF16, 1, 0, (j * world + rank) * Mc * K, sp)
+    else:
+        xtc.xtc_fill(a.data_ptr(), Mr * K, xtc.XTC_BF16, 1, 0, r0 * K, sp)
+    xtc.xtc_fill(b.data_ptr(), K * N, xtc.XTC_BF16, 2, 0, 0, sp)
     if world > 1:
         # the assembled C holds this rank's chunks at their global rows
+        for j, o in enumerate(chunk_ops):
+            o.run(a[j * Mc:(j + 1) * Mc], b, c[j * Mc:(j + 1) * Mc], stream=sp)
         compute_and_gather()
         torch.cuda.synchronize(dev)
         ok = all(torch.equal(full_c[(j * world + rank) * Mc:(j * world + rank + 1) * Mc] if CH > 1 else
@@ -578,9 +652,20 @@ def main_xtc(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, dt, threads, sample = cpu_oracle_sample(rows=128)
+        # the oracle on 128 sampled rows of the integer-data headline: timed (the baseline) and
+        # compared bit for bit with the GPU's rows of the same run (the full-size oracle check)
+        import numpy as np
+        import oracle
+        v, dt, threads, sample, (sel, O, _) = cpu_oracle_sample(rows=128, mode=1)
+        want = oracle.round_out(O, "bf16")
+        got = int_rows_out.view(torch.int16).numpy().view(np.uint16)
+        nbad = int((got != want).sum())
         cpu = {"value": v, "unit": "TFLOP/s", "cores": threads, "kind": "oracle", "sample": sample,
                "seconds": round(dt, 2)}
+        validation["integer"]["oracle_rows"] = {"rows": len(sel), "elements": int(want.size), "n_mismatch": nbad,
+                                                "what": "GPU rows vs RNE(CPU fp64 oracle), bit for bit"}
+        if nbad:
+            validation["integer"]["valid"] = 0
 
     traffic = None
     try:
@@ -592,11 +677,11 @@ def main_xtc(args):
     if rank == 0:
         clocks = clk.summary()
         line = {
-            "metric": "matmul TFLOP/s (8192^3 bf16)", "value": value, "unit": "TFLOP/s", "n_gpus": world,
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms_max / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (seeded counter-based generator, uniform[-1,1) bf16)",
-            "config": {"workload": "matmul 8192x8192x8192 bf16->bf16 (BASELINE config 5: largest matmul)",
+            "config": {"workload": WORKLOAD,
                        "model": None, "global_batch": 1, "seq_len": None,
                        "parallelism": ((f"M-sharded x{world}, all-gather fused into the GEMM epilogue "
                                         f"(xtc_run_gather: TMA stores into every rank's symmetric-memory C)"

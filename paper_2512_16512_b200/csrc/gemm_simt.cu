@@ -302,6 +302,10 @@ static cudaError_t launch_simt_u(int u, int vec, const SimtParams& p, int grid, 
 
 template <int TM>
 static cudaError_t launch_simt_n(int tn, int u, int vec, const SimtParams& p, int grid, int block, int smem, cudaStream_t st) {
+    // a 16-wide register row (e.g. the paper's J1 = 16 vector tile, Fig.4) for thin thread tiles only
+    if constexpr (TM <= 2) {
+        if (tn == 16) return launch_simt_u<TM, 16>(u, vec, p, grid, block, smem, st);
+    }
     switch (tn) {
         case 1: return launch_simt_u<TM, 1>(u, vec, p, grid, block, smem, st);
         case 2: return launch_simt_u<TM, 2>(u, vec, p, grid, block, smem, st);

@@ -70,7 +70,8 @@ xtc_status check_desc(const xtc_op_desc& d, std::string& why) {
 static xtc_status plan_simt(const xtc_op_desc& d, const xtc_schedule& s, int num_sms, Plan& p, std::string& why) {
     if (d.in_dtype != XTC_F32) ILLEGAL("SIMT engine computes fp32 inputs only (in_dtype must be F32)");
     int TM = s.inner_m, TN = s.inner_n;
-    if (!pow2_in(TM, 1, 8) || !pow2_in(TN, 1, 8)) ILLEGAL("SIMT inner_m/inner_n (thread tile) must be 1,2,4 or 8");
+    if (!pow2_in(TM, 1, 8) || !pow2_in(TN, 1, 16)) ILLEGAL("SIMT inner_m/inner_n (thread tile) must be 1,2,4 or 8 (inner_n 16 with inner_m <= 2)");
+    if (TN == 16 && TM > 2) ILLEGAL("SIMT inner_n 16 (a 16-wide register row) needs inner_m <= 2");
     if (s.tile_m < 1 || s.tile_n < 1 || s.tile_m > 256 || s.tile_n > 256) ILLEGAL("SIMT tile_m/tile_n must be in [1,256]");
     if (s.tile_m % TM || s.tile_n % TN) ILLEGAL("strip-mine: tile_m %% inner_m and tile_n %% inner_n must be 0");
     int threads = (s.tile_m / TM) * (s.tile_n / TN);

@@ -40,16 +40,20 @@ def rank_candidates(n: int, world: int, rank: int) -> List[int]:
 
 
 def pack_records(ids: Sequence[int], metrics: Sequence, rows: int) -> torch.Tensor:
-    """Fixed-size [rows, REC] float64 block; unused rows have id = -1."""
-    t = torch.full((rows, REC), -1.0, dtype=torch.float64)
-    for i, (cid, m) in enumerate(zip(ids, metrics)):
-        t[i, 0] = cid
-        if isinstance(m, dict):
-            vals = [m.get(f, 0.0) for f in REC_FIELDS[1:]]
+    """Fixed-size [rows, REC] float64 block; unused rows have id = -1.  One numpy pass over the
+    records (no per-row tensor construction: this runs inside the sweep's timed region)."""
+    import numpy as np
+    t = np.full((rows, REC), -1.0, dtype=np.float64)
+    n = min(len(ids), rows)
+    if n:
+        fields = REC_FIELDS[1:]
+        if isinstance(metrics[0], dict):
+            vals = [[m.get(f, 0.0) for f in fields] for m in metrics[:n]]
         else:
-            vals = [getattr(m, f) for f in REC_FIELDS[1:]]
-        t[i, 1:] = torch.tensor([float(v) for v in vals], dtype=torch.float64)
-    return t
+            vals = [[getattr(m, f) for f in fields] for m in metrics[:n]]
+        t[:n, 0] = np.asarray(ids[:n], dtype=np.float64)
+        t[:n, 1:] = np.asarray(vals, dtype=np.float64)
+    return torch.from_numpy(t)
 
 
 def unpack_gathered(gathered: torch.Tensor, n: int) -> List[dict]:

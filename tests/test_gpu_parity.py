@@ -851,3 +851,29 @@ def test_headline_schedule_with_fused_consumers():
         O, D = oracle_matmul(M, N, K, "bf16", MODE_INT, 41, 42)
         O = oracle.consume(O, relu_=True, bias=bias.cpu().numpy().astype(np.float64) if "bias" in cons else None)
         check_against_oracle(c, O, D, "bf16", exact=True, tol=0)
+
+
+# ------------------------------------- N3: descript / primitive-log front-ends --
+@pytest.mark.parametrize("mode", [MODE_INT, MODE_UNIFORM])
+def test_fig4_and_fig8_schedules_run_on_the_gpu(mode):
+    """The schedule built call for call from Fig.4 (imperative, primitive log) and from Fig.8 (descript)
+    lowers to ONE xtc_schedule (tests/test_host.py pins that); it runs on the SIMT engine -- a 1 x 16
+    register row with K1 = 4 unrolled and the [256, 258) remainder root -- against the oracle."""
+    import test_host
+    from paper_2512_16512_b200.scheduler import Scheduler
+    desc = xtc.matmul_desc(256, 258, 512, "f32", "f32")
+    s = Scheduler(desc)
+    s.descript(test_host.FIG8)
+    assert s.knobs() == test_host._fig4(desc).knobs()
+    err, _ = run_matmul(256, 258, 512, "f32", "f32", s.schedule(), mode)
+    assert err <= 1e-5
+
+
+def test_descript_headline_runs_on_the_gpu():
+    from paper_2512_16512_b200.scheduler import Scheduler
+    desc = xtc.matmul_desc(1024, 768, 320, "bf16", "bf16")
+    s = Scheduler(desc)
+    s.descript({"I": ["parallelize"], "J": ["parallelize"], "K": ["pack=3"], "K#64": [], "I#512": [],
+                "J#256": ["buffer"]})
+    run_matmul(1024, 768, 320, "bf16", "bf16", s.schedule(dict(cluster_m=2, persistent=1, raster_group=8)),
+               MODE_INT)

@@ -399,3 +399,102 @@ def test_grid_sms_plan_and_legality():
     for bad in (dict(HEADLINE, grid_sms=1), dict(HEADLINE, grid_sms=8, persistent=0), dict(HEADLINE, grid_sms=-1)):
         st, _, why = xtc.xtc_schedule_check(d, xtc.schedule(**bad), 148)
         assert st == xtc.XTC_E_ILLEGAL_SCHEDULE and "grid_sms" in why
+
+
+# --------------------------------------------- N3: descript + primitive log --
+def _fig4(desc):
+    """PAPER.md Fig.4, call for call."""
+    from paper_2512_16512_b200.scheduler import Scheduler
+    sch = Scheduler(desc)
+    sch.dims = ["I", "J", "K"]
+    sch.split(root="mm0", dim="J", segments={"J[0]": 0, "J[1]": 256})
+    sch.strip_mine(root="J[0]", dim="K", tiles={"K1": 4})
+    sch.strip_mine(root="J[0]", dim="J", tiles={"J1": 16})
+    sch.unroll(root="J[0]", unrolls={"J1": 16, "K1": 4})
+    sch.vectorize(root="J[0]", axes=["J1"])
+    sch.interchange(root="mm0", permutation=["I", "J[0]", "J[1]"])
+    sch.interchange(root="J[0]", permutation=["K", "K1", "J1"])
+    sch.interchange(root="J[1]", permutation=["K"])
+    return sch
+
+
+FIG8 = {"I": [], "J[0:256]": {"K": [], "K#4": ["unroll"], "J#16": ["vectorize"]}, "J[256:258]": {"K": []}}
+
+
+def test_fig4_primitive_log_and_fig8_descript_give_one_schedule():
+    """§V-A: Fig.8 is 'the reimplementation of the example in Fig.4'; both front-ends must build
+    the same loop nest and lower to the same legal schedule: the SIMT engine with the 1 x 16 register row
+    (J1 = 16, vectorized), K1 = 4 unrolled, and the [256, 258) remainder root."""
+    from paper_2512_16512_b200.scheduler import Scheduler
+    desc = xtc.matmul_desc(256, 258, 512, "f32", "f32")
+    imp = _fig4(desc)
+    dec = Scheduler(desc)
+    dec.dims = ["I", "J", "K"]
+    dec.descript(FIG8)
+    want_nest = (("I", 256, ()),
+                 ("split", "J", ((0, 256, (("K", 512, ()), ("K", 4, (("unroll", 4),)),
+                                           ("J", 16, (("unroll", 16), ("vectorize", 1))))),
+                                 (256, 258, (("K", 512, ()),)))))
+    assert imp.nest() == want_nest
+    assert dec.nest() == want_nest
+    kn = imp.knobs()
+    assert kn == dec.knobs()
+    assert kn == dict(engine=0, split_n_at=256, order=0, tile_m=1, tile_n=16, inner_m=1, inner_n=16, tile_k=4,
+                      unroll_k=4, stages=1, vector_n=4)
+    st, info, why = imp.check()
+    assert st == xtc.XTC_OK, why
+    assert info.tail_grid_x == 1 and info.num_tiles == 256 * 16      # 1 x 16 tiles of [0, 256) + the remainder
+    # the primitive log replays to the same state (P:751-755)
+    assert [p for p, _ in imp.log] == ["dims", "split", "strip_mine", "strip_mine", "unroll", "vectorize",
+                                        "interchange", "interchange", "interchange"]
+    again = Scheduler.replay(desc, imp.log)
+    assert again.nest() == want_nest and again.knobs() == kn
+
+
+def test_descript_and_primitives_lower_the_headline_schedule():
+    """The bench's tcgen05 schedule written as a loop nest: I, J parallelized over the grid with steps 512 x 256
+    (the CTA-pair tile), K staged in 64-deep blocks through a 3-stage pack, the output bufferized."""
+    import bench
+    from paper_2512_16512_b200.scheduler import Scheduler
+    desc = xtc.matmul_desc(8192, 8192, 8192, "bf16", "bf16")
+    target = dict(cluster_m=2, persistent=1, raster_group=8, acc_buffers=1)
+    dec = Scheduler(desc)
+    dec.descript({"I": ["parallelize"], "J": ["parallelize"], "K": ["pack=3"], "K#64": [], "I#512": [],
+                  "J#256": ["buffer"]})
+    imp = Scheduler(desc)
+    imp.strip_mine(root="mm0", dim="I", tiles={"I1": 512})
+    imp.strip_mine(root="mm0", dim="J", tiles={"J1": 256})
+    imp.strip_mine(root="mm0", dim="K", tiles={"K1": 64})
+    imp.interchange(root="mm0", permutation=["I", "J", "K", "K1", "I1", "J1"])
+    imp.parallelize(root="mm0", axes=["I", "J"])
+    imp.pack(root="mm0", at="K", stages=3)
+    imp.bufferize(root="mm0", at="J1")
+    assert imp.nest() == dec.nest()
+    want = {k: v for k, v in bench.HEADLINE_SCHEDULE.items()}
+    got = dec.knobs(target)
+    assert {k: got.get(k, 0) for k in want} == want
+    assert imp.knobs(target) == got
+    assert dec.check(target)[0] == xtc.XTC_OK
+    again = Scheduler.replay(desc, imp.log)
+    assert again.knobs(target) == got
+
+
+def test_scheduler_rejects_malformed_primitives():
+    from paper_2512_16512_b200.scheduler import Scheduler, ScheduleError
+    desc = xtc.matmul_desc(256, 258, 512, "f32", "f32")
+    s = Scheduler(desc)
+    with pytest.raises(ScheduleError):
+        s.interchange(root="mm0", permutation=["I", "K"])               # not a permutation
+    with pytest.raises(ScheduleError):
+        s.strip_mine(root="nope", dim="K", tiles={"K1": 4})              # unknown root
+    with pytest.raises(ScheduleError):
+        s.unroll(root="mm0", unrolls={"K": 3})                           # 3 does not divide 512 (S:271)
+    s.interchange(root="mm0", permutation=["K", "I", "J"])                # K outermost: no GPU lowering
+    with pytest.raises(ScheduleError):
+        s.knobs()
+    with pytest.raises(ScheduleError):
+        Scheduler(desc).descript({"I": [], "J": ["fuse"], "K": []})       # unknown annotation
+    with pytest.raises(ScheduleError):
+        Scheduler(desc).descript({"I": [], "J[0:100]": {"K": []}, "J[120:258]": {"K": []}})   # gap
+    with pytest.raises(ScheduleError):
+        Scheduler(xtc.conv2d_desc(1, 8, 8, 64, 64))
