@@ -99,7 +99,15 @@ typedef struct {
 
 typedef enum { XTC_ENGINE_SIMT = 0, XTC_ENGINE_TCGEN05 = 1 } xtc_engine;
 typedef enum { XTC_ORDER_MN = 0, XTC_ORDER_NM = 1 } xtc_order;
-typedef enum { XTC_SPLITK_ORDERED = 0, XTC_SPLITK_ATOMIC = 1 } xtc_splitk_mode;
+/* Reduction of the split K segments:
+ *   ORDERED  fp32 partials in a workspace, summed in ascending segment order by a second kernel
+ *   ATOMIC   fp32 atomics into C (fp32 output; exact on integer data only, order not fixed)
+ *   CLUSTER  tcgen05: the split_k segments of an output tile are the CTAs of one thread-block
+ *            cluster (split_k <= 16); after all partials are written each CTA sums 1/split_k of
+ *            the tile's rows in ascending segment order inside the same kernel -- bit-identical
+ *            to ORDERED, one launch, no second pass over the workspace.  Needs buffer_c 0,
+ *            cluster_m 1, cluster_n 0/1, tile_m 128 (matmul) and b_resident 0. */
+typedef enum { XTC_SPLITK_ORDERED = 0, XTC_SPLITK_ATOMIC = 1, XTC_SPLITK_CLUSTER = 2 } xtc_splitk_mode;
 
 /* A schedule: Table I primitives as GPU loop-nest knobs.  The
  * mapping, value ranges and legality rules are in DESIGN.md §4 (SURVEY.md

@@ -62,6 +62,19 @@ cudaError_t ensure_smem_attr_impl(const void* kernel, int smem) {
     if (e == cudaSuccess) have = smem;
     return e;
 }
+cudaError_t ensure_nonportable_cluster_impl(const void* kernel) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, bool> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(mu);
+    bool& d = done[{kernel, dev}];
+    if (d) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e == cudaSuccess) d = true;
+    return e;
+}
 }  // namespace xtc
 
 static xtc_status fail(xtc_status s, const std::string& why) {
@@ -559,6 +572,7 @@ static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cud
     const int64_t ldc = (d.kind == XTC_OP_MATMUL && d.ldc) ? d.ldc : p.n_total;
     const bool out_bf16 = d.out_dtype == XTC_BF16;
     const bool split_out = p.split_k > 1 && !p.atomic;
+    const bool split_cluster = p.split_cluster;      // the reduction runs inside the contraction kernel
     int launches = 0;
     if (p.atomic && !(d.consumer & XTC_CONSUMER_ACCUMULATE)) {
         // atomic split-K accumulates into C: clear the main root's columns first (unless the
@@ -567,7 +581,9 @@ static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cud
         CU_TRY(cudaMemset2DAsync(C, ldc * 4, 0, p.N * 4, rows, st), "memset C (atomic split-K)");
     }
     // cluster_n: the tile map walks cluster tiles (cluster_n adjacent N tiles of one M tile)
-    TileMap tm{p.tiles_m, p.tiles_n / (p.cluster_n > 1 ? p.cluster_n : 1), p.split_k, p.sch.order, p.sch.raster_group};
+    // split cluster: the tile map walks output tiles, the K segment is the CTA's cluster rank
+    TileMap tm{p.tiles_m, p.tiles_n / (p.cluster_n > 1 ? p.cluster_n : 1), split_cluster ? 1 : p.split_k, p.sch.order,
+               p.sch.raster_group};
     if (p.engine == XTC_ENGINE_SIMT) {
         SimtParams sp;
         memset(&sp, 0, sizeof sp);
@@ -640,6 +656,8 @@ static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cud
         tp.lo_off = p.split3 ? (uint32_t)(p.sch.stages * (tp.a_stage_bytes + tp.b_stage_bytes)) : 0u;
         tp.cg = conv_geom(d);
         tp.cn = p.cluster_n > 1 ? p.cluster_n : 1;
+        tp.ksc = split_cluster ? p.split_k : 1;
+        tp.cons_red = split_cluster ? p.cons_reduce : 0;
         if (ga) {
             tp.gather = ga->maps;
             tp.n_gather = ga->n;
@@ -685,7 +703,7 @@ static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cud
             }
         }
     }
-    if (split_out) {
+    if (split_out && !split_cluster) {
         CU_TRY(launch_splitk_reduce(op->ws, p.split_k, p.M, p.N, p.ws_ld, C, ldc, out_bf16, p.cons_reduce, op->bias, st),
                "splitk_reduce");
         ++launches;

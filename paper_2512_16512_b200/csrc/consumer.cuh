@@ -42,6 +42,17 @@ __device__ __forceinline__ void load_row32(const void* C, bool bf16, int64_t off
     }
 }
 
+// One complete sum v of output element `off` (column col): relu(C_old + v + bias[col]), the
+// same order as apply_consumer32 (used by the in-kernel split-K reduction).
+__device__ __forceinline__ float consume1(float v, int cons, const float* bias, const void* C, bool out_bf16,
+                                          int64_t off, int64_t col) {
+    if (cons & XTC_CONSUMER_ACCUMULATE)
+        v += out_bf16 ? bf16_bits_to_f32(reinterpret_cast<const uint16_t*>(C)[off]) : reinterpret_cast<const float*>(C)[off];
+    if (cons & XTC_CONSUMER_BIAS) v += __ldg(bias + col);
+    if (cons & XTC_CONSUMER_RELU) v = fmaxf(v, 0.f);
+    return v;
+}
+
 // v[j] (fp32 bits) for columns col0 + j, j < ncols, of output row `row`.  cons = XTC_CONSUMER_*
 // bits; add_old / add_bias let atomic split-K drop the terms that are not its segment's.
 __device__ __forceinline__ void apply_consumer32(uint32_t (&v)[32], int cons, const float* bias, const void* C,

@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 #include "consumer.cuh"
 #include "ptx.cuh"
+#include "splitk_cluster.cuh"
 #include "xtc_internal.h"
 
 namespace xtc {
@@ -51,7 +52,9 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
     uint64_t* tfull = pempty + kHaloMaxPatchBufs;
     uint64_t* tempty = tfull + 2;
     uint64_t* bfull = tempty + 2;                // resident filter: one barrier per k-block
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + kHaloMaxResidentKb);
+    uint64_t* ksig = bfull + kHaloMaxResidentKb; // cluster split-K: partials-written signals (2, by tile parity)
+    uint64_t* tready = ksig + 2;                 // TMEM allocated (its address is in tmem_slot)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tready + 1);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -65,8 +68,13 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
     static_assert(!PAIR || (CL == 2 && MSUB == 1), "the CTA pair is a 2-CTA cluster, one UMMA tile per CTA");
     constexpr int CG = PAIR ? 2 : 1;
     const uint32_t rank = (CL == 2) ? ptx::cluster_ctarank() : 0u;
-    const int64_t cluster_id = blockIdx.x / CL;
-    const int64_t num_clusters = gridDim.x / CL;
+    // cluster split-K (split_k_mode XTC_SPLITK_CLUSTER, CL = 1): the ksc CTAs of a cluster run
+    // the ksc K segments (runs of filter taps / channel planes) of one output tile
+    const int ksc = (CL == 1 && p.ksc > 1) ? p.ksc : 1;
+    const bool kclu = ksc > 1;
+    const uint32_t krank = kclu ? ptx::cluster_ctarank() : 0u;
+    const int64_t cluster_id = blockIdx.x / (CL * ksc);
+    const int64_t num_clusters = gridDim.x / (CL * ksc);
     // XTC_TRACE (diagnostics): slot 0 entry, 1 setup done, 2 exit; 8+j patch j issued,
     // 8+kTraceK+j patch j seen by the MMA warp, 8+2kTraceK+2j(+1) epilogue of tile j start/end
     uint64_t* const trace = (p.trace && blockIdx.x < kTraceCtas) ? p.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
@@ -88,27 +96,31 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
             ptx::mbar_init(&tempty[i], 4 * CG);
         }
         for (int i = 0; i < kHaloMaxResidentKb; ++i) ptx::mbar_init(&bfull[i], 1);
+        if (kclu) { ptx::mbar_init(&ksig[0], 4u * ksc); ptx::mbar_init(&ksig[1], 4u * ksc); }
+        ptx::mbar_init(tready, 1);
         ptx::fence_mbarrier_init();
     }
     // barriers first (peers' barriers exist before multicasts); the TMEM allocation is then
     // taken by warp 2 while warps 0 and 3 already issue the patch and filter loads, and only
-    // the TMEM users (warps 1, 4..7) wait for it on the named barrier kTmemBar
+    // the TMEM users (warps 1, 4..7) wait for it on the mbarrier tready
     if (warp == 2 && p.debug_late_alloc) {
         ptx::tmem_alloc<CG>(tmem_slot, p.tmem_cols);
         ptx::tmem_relinquish<CG>();
         ptx::tc_fence_before();
     }
-    if constexpr (CL == 2) ptx::cluster_sync(); else __syncthreads();
+    if (CL == 2 || kclu) ptx::cluster_sync(); else __syncthreads();
     if (warp == 2 && p.debug_late_alloc) {
-        ptx::named_bar_arrive(ptx::kTmemBar, ptx::kTmemBarThreads);
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(tready);
     } else if (warp == 2) {
         ptx::tmem_alloc<CG>(tmem_slot, p.tmem_cols);
         ptx::tmem_relinquish<CG>();
         ptx::tc_fence_before();
-        ptx::named_bar_arrive(ptx::kTmemBar, ptx::kTmemBarThreads);
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(tready);
     }
     auto tmem_address = [&]() -> uint32_t {
-        ptx::named_bar_sync(ptx::kTmemBar, ptx::kTmemBarThreads);
+        ptx::mbar_wait(tready, 0);
         ptx::tc_fence_after();
         return *reinterpret_cast<volatile uint32_t*>(tmem_slot);
     };
@@ -120,6 +132,7 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
     auto decode = [&](int64_t t, int& nimg, int& p0, int& n0, int& ks) {
         int mb, nb;
         tile_coords(p.tm, t, mb, nb, ks);
+        if (kclu) ks = (int)krank;
         mb = mb * CL + (int)rank;                    // CL = 2: the loop runs over M-tile pairs
         nimg = mb / p.tpi;
         p0 = (mb - nimg * p.tpi) * p.rt * MSUB;
@@ -281,6 +294,7 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
             {
                 int mb_, nb_, ks_;
                 tile_coords(p.tm, t, mb_, nb_, ks_);
+                if (kclu) ks_ = (int)krank;
                 kb0 = ks_ * p.kb_per_split;
                 kb1 = min(kb_total, kb0 + p.kb_per_split);
             }
@@ -351,6 +365,7 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
         const int q = warp & 3;
         int acc = 0, buf = 0;
         uint32_t aph = 0;
+        ClusterSplitState kst;
         uint8_t* stage = sC + q * (kTcEpiStageBytes * kTcEpiBuffers);
         const bool bf16_out = p.out_bf16 != 0;
         const int P = p.cg.P, Q = p.cg.Q;
@@ -424,7 +439,14 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
                         const int ncols = (int)((p.N - col0) < 32 ? (p.N - col0) : 32);
                         if (p.split_out) {                  // split_k: this segment's fp32 partial sums
                             float* dst = p.Wk + ((int64_t)ks * p.M + m) * p.ws_ld + col0;
-                            for (int j = 0; j < ncols; ++j) dst[j] = __uint_as_float(vals[j]);
+                            if (ncols == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+#pragma unroll
+                                for (int j = 0; j < 8; ++j)
+                                    reinterpret_cast<uint4*>(dst)[j] =
+                                        make_uint4(vals[4 * j], vals[4 * j + 1], vals[4 * j + 2], vals[4 * j + 3]);
+                            } else {
+                                for (int j = 0; j < ncols; ++j) dst[j] = __uint_as_float(vals[j]);
+                            }
                         } else if (bf16_out) {
                             uint16_t* dst = reinterpret_cast<uint16_t*>(p.C) + m * p.ldc + col0;
                             if (ncols == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
@@ -464,12 +486,19 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
                 else ptx::mbar_arrive(&tempty[acc]);
             }
             if (++acc == p.acc_buffers) { acc = 0; aph ^= 1u; }
+            if (kclu) {
+                // the tile's valid output rows are contiguous in y: image nimg, rows p0 .. p0+rt*MSUB-1 (< P)
+                const int p1 = min(P, p0 + p.rt * MSUB);
+                cluster_split_reduce(ksig, kst, ksc, (int)krank, p.Wk, p.M, p.ws_ld, ((int64_t)nimg * P + p0) * Q,
+                                     (p1 - p0) * Q, n0, (int)((p.N - n0) < p.tile_n ? (p.N - n0) : p.tile_n), p.C, p.ldc,
+                                     bf16_out, p.cons_red, p.bias, (int)threadIdx.x - 128);
+            }
         }
         if (p.buffer_c && lane == 0) ptx::bulk_wait<0>();
     }
 
     ptx::tc_fence_before();
-    if constexpr (CL == 2) ptx::cluster_sync(); else __syncthreads();   // no CTA exits while a peer may still signal it
+    if (CL == 2 || kclu) ptx::cluster_sync(); else __syncthreads();   // no CTA exits while a peer may still signal it
     if (trace && threadIdx.x == 0) trace[2] = ptx::globaltimer();
     if (warp == 2) {
         ptx::tc_fence_after();
@@ -483,9 +512,14 @@ static cudaError_t launch_halo_t(const CUtensorMap& x, const CUtensorMap& b, con
     auto k = tc_conv_halo_kernel<TF32, MSUB, CL, PAIR>;
     cudaError_t e = ensure_smem_attr(k, smem);
     if (e != cudaSuccess) return e;
-    if constexpr (CL == 1) {
+    const int ksc = (CL == 1 && p.ksc > 1) ? p.ksc : 1;
+    if (CL == 1 && ksc == 1) {
         k<<<grid, kTcThreads, smem, st>>>(x, b, y, p);
     } else {
+        if (ksc > 8) {
+            e = ensure_nonportable_cluster(k);
+            if (e != cudaSuccess) return e;
+        }
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(grid);
         cfg.blockDim = dim3(kTcThreads);
@@ -493,7 +527,7 @@ static cudaError_t launch_halo_t(const CUtensorMap& x, const CUtensorMap& b, con
         cfg.stream = st;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = CL;
+        attr[0].val.clusterDim.x = CL * ksc;
         attr[0].val.clusterDim.y = 1;
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;

@@ -32,6 +32,7 @@
 #include <type_traits>
 #include "consumer.cuh"
 #include "ptx.cuh"
+#include "splitk_cluster.cuh"
 #include "xtc_internal.h"
 
 namespace xtc {
@@ -65,7 +66,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     uint64_t* tempty = tfull + 2;
     uint64_t* bfull = tempty + 2;            // resident B landed
     uint64_t* split = bfull + 1;             // SPLIT3: lo parts of stage s written (warps 2 and 3)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(split + 8);
+    uint64_t* ksig = split + 8;              // cluster split-K: partials-written signals (2, by tile parity)
+    uint64_t* tready = ksig + 2;             // TMEM allocated (its address is in tmem_slot)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tready + 1);
 
     if (p.trace && blockIdx.x < kTraceCtas && threadIdx.x == 0)
         p.trace[(size_t)blockIdx.x * kTraceSlots] = ptx::globaltimer();
@@ -78,8 +81,13 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const bool mcast = cn > 1;
     const uint32_t crank = mcast ? ptx::cluster_ctarank() : 0u;
     const uint16_t cmask = (uint16_t)((1u << cn) - 1u);
-    const int64_t cluster_id = blockIdx.x / (CG * cn);
-    const int64_t num_clusters = gridDim.x / (CG * cn);
+    // cluster split-K (split_k_mode XTC_SPLITK_CLUSTER, CG = 1, cn = 1): the ksc CTAs of a
+    // cluster run the ksc K segments of one output tile; CTA rank = segment
+    const int ksc = (CG == 1 && cn == 1 && p.ksc > 1) ? p.ksc : 1;
+    const bool kclu = ksc > 1;
+    const uint32_t krank = kclu ? ptx::cluster_ctarank() : 0u;
+    const int64_t cluster_id = blockIdx.x / (CG * cn * ksc);
+    const int64_t num_clusters = gridDim.x / (CG * cn * ksc);
     const int bn_cta = p.tile_n / CG;        // B columns this CTA loads
 
     if (warp == 0 && lane == 0) {
@@ -93,28 +101,32 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         for (int a = 0; a < 2; ++a) { ptx::mbar_init(&tfull[a], 1); ptx::mbar_init(&tempty[a], 4 * CG); }
         ptx::mbar_init(bfull, 1);
         if constexpr (SPLIT3) for (int s = 0; s < S; ++s) ptx::mbar_init(&split[s], 2);
+        if (kclu) { ptx::mbar_init(&ksig[0], 4u * ksc); ptx::mbar_init(&ksig[1], 4u * ksc); }
+        ptx::mbar_init(tready, 1);
         ptx::fence_mbarrier_init();
     }
     // Barriers first; the TMEM allocation (the first tcgen05 instruction, ~0.5-1 us on a cold
     // SM) is then taken by warp 2 while the producers already issue the first (HBM-cold)
     // stages.  Only the MMA issuer and the epilogue read the TMEM address: they wait on the
-    // named barrier kTmemBar, which warp 2 arrives on after the allocation.
+    // mbarrier tready, which warp 2 arrives on after the allocation.
     if (warp == 2 && p.debug_late_alloc) {
         ptx::tmem_alloc<CG>(tmem_slot, p.tmem_cols);
         ptx::tmem_relinquish<CG>();
         ptx::tc_fence_before();
     }
-    if (CG == 2 || mcast) ptx::cluster_sync(); else __syncthreads();
+    if (CG == 2 || mcast || kclu) ptx::cluster_sync(); else __syncthreads();
     if (warp == 2 && p.debug_late_alloc) {
-        ptx::named_bar_arrive(ptx::kTmemBar, ptx::kTmemBarThreads);
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(tready);
     } else if (warp == 2) {
         ptx::tmem_alloc<CG>(tmem_slot, p.tmem_cols);
         ptx::tmem_relinquish<CG>();
         ptx::tc_fence_before();
-        ptx::named_bar_arrive(ptx::kTmemBar, ptx::kTmemBarThreads);
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(tready);
     }
     auto tmem_address = [&]() -> uint32_t {     // warps 1 and 4..7, once, before any TMEM use
-        ptx::named_bar_sync(ptx::kTmemBar, ptx::kTmemBarThreads);
+        ptx::mbar_wait(tready, 0);
         ptx::tc_fence_after();
         return *reinterpret_cast<volatile uint32_t*>(tmem_slot);
     };
@@ -165,6 +177,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters) {
                 int mb, nb, ks;
                 tile_coords(p.tm, t, mb, nb, ks);
+                if (kclu) ks = (int)krank;
                 const int kb0 = ks * p.kb_per_split;
                 const int kb1 = min(p.kb_total, kb0 + p.kb_per_split);
                 const int m0 = mb * TILE_M + 128 * MS * (int)rank;     // this CTA's 128*MS rows
@@ -295,6 +308,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters) {
             int mb, nb, ks;
             tile_coords(p.tm, t, mb, nb, ks);
+                if (kclu) ks = (int)krank;
             const int kb0 = ks * p.kb_per_split;
             const int kb1 = min(p.kb_total, kb0 + p.kb_per_split);
             for (int kb = kb0; kb < kb1; ++kb) {
@@ -345,6 +359,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters) {
                     int mb, nb, ks;
                     tile_coords(p.tm, t, mb, nb, ks);
+                if (kclu) ks = (int)krank;
                     const int kb0 = ks * kb_per;
                     const int kb1 = min(kb_tot, kb0 + kb_per);
                     ptx::mbar_wait(&tempty[acc], aph ^ 1);
@@ -428,6 +443,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         int acc = 0;
         uint32_t aph = 0;
         int buf = 0;
+        ClusterSplitState kst;
         uint8_t* stage = sC + q * (kTcEpiStageBytes * kTcEpiBuffers);
         if (p.n_gather && lane == 0)
             for (int d = 0; d < p.n_gather; ++d) ptx::tmap_acquire(reinterpret_cast<const CUtensorMap*>(p.gather) + d);
@@ -436,6 +452,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters) {
             int mb, nb, ks;
             tile_coords(p.tm, t, mb, nb, ks);
+                if (kclu) ks = (int)krank;
             const int m0t = mb * TILE_M + 128 * MS * (int)rank, n0 = (nb * cn + (int)crank) * p.tile_n;
             ptx::mbar_wait(&tfull[acc], aph);
             if (trace && warp == 4 && lane == 0 && trace_k < kTraceTiles) trace[8 + 2 * kTraceK + 2 * trace_k] = ptx::globaltimer();
@@ -647,13 +664,21 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 else ptx::mbar_arrive(&tempty[acc]);
             }
             if (++acc == p.acc_buffers) { acc = 0; aph ^= 1; }
+            if (kclu) {                                // the tile's K segments meet: ordered reduction
+                const int64_t r0 = (int64_t)mb * TILE_M;
+                const int64_t c0 = (int64_t)nb * p.tile_n;
+                cluster_split_reduce(ksig, kst, ksc, (int)krank, p.Wk, p.M, p.ws_ld, r0,
+                                     (int)(p.M - r0 < TILE_M ? p.M - r0 : TILE_M), c0,
+                                     (int)(p.N - c0 < p.tile_n ? p.N - c0 : p.tile_n),
+                                     p.C, p.ldc, p.out_bf16 != 0, p.cons_red, p.bias, (int)threadIdx.x - 128);
+            }
         }
         if (p.buffer_c && lane == 0) ptx::bulk_wait<0>();
     }
 
     ptx::tc_fence_before();
     // (cluster_n: no CTA may exit while a peer can still multicast into its SMEM / barriers)
-    if (CG == 2 || mcast) ptx::cluster_sync(); else __syncthreads();
+    if (CG == 2 || mcast || kclu) ptx::cluster_sync(); else __syncthreads();
     if (trace && threadIdx.x == 0) trace[2] = ptx::globaltimer();
     if (warp == 2) {
         ptx::tc_fence_after();
@@ -668,9 +693,14 @@ cudaError_t launch_tc_t(const CUtensorMap& a, const CUtensorMap& b, const CUtens
     auto k = tc_gemm_kernel<TF32, CONV, CG, SPLIT3, MS>;
     cudaError_t e = ensure_smem_attr(k, smem);
     if (e != cudaSuccess) return e;
-    if (CG == 1 && p.cn <= 1) {
+    const int ksc = (CG == 1 && p.cn <= 1 && p.ksc > 1) ? p.ksc : 1;
+    if (CG == 1 && p.cn <= 1 && ksc == 1) {
         k<<<grid, kTcThreads, smem, st>>>(a, b, c, p);
     } else {
+        if (ksc > 8) {
+            e = ensure_nonportable_cluster(k);
+            if (e != cudaSuccess) return e;
+        }
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(grid);
         cfg.blockDim = dim3(kTcThreads);
@@ -678,7 +708,7 @@ cudaError_t launch_tc_t(const CUtensorMap& a, const CUtensorMap& b, const CUtens
         cfg.stream = st;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = CG * (p.cn > 1 ? p.cn : 1);
+        attr[0].val.clusterDim.x = CG * (p.cn > 1 ? p.cn : 1) * ksc;
         attr[0].val.clusterDim.y = 1;
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;

@@ -133,7 +133,7 @@ static xtc_status plan_tc_halo(const xtc_op_desc& d, const xtc_schedule& s, int 
     if (hcl != 1 && hcl != 2) ILLEGAL("pack_halo: cluster_m must be 1 or 2 (filter multicast pair)");
     // split: K segments (runs of filter taps / channel planes) as their own CTAs; fp32 partials
     // written by direct stores, summed in ascending segment order by the reduction kernel
-    if (p.split_k > 1 && p.atomic) ILLEGAL("pack_halo: split_k needs the ordered reduction (split_k_mode 0)");
+    if (p.split_k > 1 && p.atomic) ILLEGAL("pack_halo: split_k needs an ordered reduction (split_k_mode 0 or 2)");
     if (p.split_k > 1 && s.buffer_c) ILLEGAL("pack_halo: split_k writes fp32 partials with direct stores (buffer_c 0)");
     if (s.pack_warps > 1) ILLEGAL("pack_halo: pack_warps must be 0 or 1 (warp 0 packs patches, warp 3 the B ring)");
     if (s.tile_m != 128 && s.tile_m != 256) ILLEGAL("pack_halo: tile_m must be 128 or 256 (1 or 2 UMMA M-tiles per patch)");
@@ -234,6 +234,18 @@ static xtc_status plan_tc_halo(const xtc_op_desc& d, const xtc_schedule& s, int 
     p.cta_group = pair ? 2 : 1;                         // UMMA M = 128 * cta_group (abi.cu idesc)
     p.block = kTcThreads;
     p.cluster = hcl;
+    if (p.split_cluster) {
+        // the split_k segments of a tile = the CTAs of one cluster, reduced in the kernel
+        if (hcl != 1) ILLEGAL("pack_halo: split_k_mode 2 needs cluster_m 1 (the cluster holds the K segments)");
+        if (s.b_resident) ILLEGAL("pack_halo: split_k_mode 2 needs b_resident 0");
+        p.num_tiles = (int64_t)p.tiles_m * p.tiles_n;
+        p.cluster = p.split_k;
+        const int64_t ctas = p.num_tiles * p.split_k;
+        const int64_t cap = (int64_t)(num_sms / p.split_k) * p.split_k;
+        if (s.persistent && cap < p.split_k) ILLEGAL("parallelize: %d SMs hold no cluster of %d CTAs", num_sms, p.split_k);
+        p.grid_x = s.persistent ? (int)std::min<int64_t>(ctas, cap) : (int)ctas;
+        return XTC_OK;
+    }
     const int64_t ctas = p.num_tiles * hcl;
     p.grid_x = s.persistent ? (int)std::min<int64_t>(ctas, num_sms - num_sms % hcl) : (int)ctas;
     return XTC_OK;
@@ -358,6 +370,19 @@ static xtc_status plan_tc(const xtc_op_desc& d, const xtc_schedule& s, int num_s
     if (p.atomic && s.buffer_c) ILLEGAL("atomic split-K uses direct red.global stores: buffer_c must be 0");
     p.block = kTcThreads;
     p.cluster = cg;
+    if (p.split_cluster) {
+        // one cluster of split_k CTAs per output tile; persistent: whole clusters on at most num_sms SMs
+        if (cg != 1 || ms != 1) ILLEGAL("split: split_k_mode 2 needs cluster_m 1 and tile_m 128 (one UMMA tile per CTA)");
+        if (s.cluster_n > 1) ILLEGAL("split: split_k_mode 2 needs cluster_n 0/1 (the cluster holds the K segments)");
+        if (s.b_resident) ILLEGAL("split: split_k_mode 2 needs b_resident 0");
+        p.num_tiles = (int64_t)p.tiles_m * p.tiles_n;
+        p.cluster = p.split_k;
+        const int64_t ctas = p.num_tiles * p.split_k;
+        const int64_t cap = (int64_t)(num_sms / p.split_k) * p.split_k;
+        if (s.persistent && cap < p.split_k) ILLEGAL("parallelize: %d SMs hold no cluster of %d CTAs", num_sms, p.split_k);
+        p.grid_x = s.persistent ? (int)std::min<int64_t>(ctas, cap) : (int)ctas;
+        return XTC_OK;
+    }
     // cluster_n: cn CTAs on adjacent N tiles of one M tile share every A stage by TMA multicast
     // (each loads 128/cn of its rows); a "tile" of the tile map is then a cluster tile
     const int cn = s.cluster_n == 0 ? 1 : s.cluster_n;
@@ -401,8 +426,17 @@ xtc_status make_plan(const xtc_op_desc& d, const xtc_schedule& s, int num_sms, P
     if (s.grid_sms) num_sms = std::min(num_sms, (int)s.grid_sms);
     p.split_k = s.split_k == 0 ? 1 : s.split_k;
     if (p.split_k < 1 || p.split_k > 64) ILLEGAL("split_k must be in [1,64]");
-    if (s.split_k_mode != XTC_SPLITK_ORDERED && s.split_k_mode != XTC_SPLITK_ATOMIC) ILLEGAL("unknown split_k_mode");
+    if (s.split_k_mode != XTC_SPLITK_ORDERED && s.split_k_mode != XTC_SPLITK_ATOMIC && s.split_k_mode != XTC_SPLITK_CLUSTER)
+        ILLEGAL("unknown split_k_mode");
     p.atomic = (p.split_k > 1 && s.split_k_mode == XTC_SPLITK_ATOMIC);
+    // the K segments of a tile as the CTAs of one cluster, reduced inside the kernel (splitk_cluster.cuh)
+    p.split_cluster = (p.split_k > 1 && s.split_k_mode == XTC_SPLITK_CLUSTER);
+    if (p.split_cluster) {
+        if (s.engine != XTC_ENGINE_TCGEN05) ILLEGAL("split: split_k_mode 2 (cluster reduction) needs the tcgen05 engine");
+        if (p.split_k > kSplitClusterMaxCtas) ILLEGAL("split: split_k_mode 2 puts the %d K segments in one cluster (<= %d CTAs)",
+                                                     p.split_k, kSplitClusterMaxCtas);
+        if (s.buffer_c) ILLEGAL("split: split_k_mode 2 writes partials and the reduced output with direct stores (buffer_c 0)");
+    }
     if (p.atomic && d.out_dtype != XTC_F32) ILLEGAL("atomic split-K needs fp32 output");
     if (s.split_n_at) {
         if (s.split_n_at < 0 || s.split_n_at >= N) ILLEGAL("split: split_n_at %d must be in (0, N=%lld)", s.split_n_at, (long long)N);

@@ -179,6 +179,30 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t saddr, uint32_t rank) {
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+// wait with cluster-scope acquire: pairs with mbar_arrive_cluster (release.cluster) of a peer CTA,
+// so the peer's writes before its arrive (incl. global memory) are visible after the wait
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    const uint32_t addr = smem_u32(bar);
+    uint64_t t0 = 0;
+    uint32_t n = 0;
+    while (true) {
+        uint32_t ok;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(addr), "r"(parity)
+            : "memory");
+        if (ok) return;
+        if (n == 0) t0 = globaltimer();
+        if ((++n & 1023u) == 0 && globaltimer() - t0 > XTC_WATCHDOG_NS) {
+            printf("xtc watchdog: cluster mbarrier wait timed out (block %d thread %d parity %u)\n",
+                   blockIdx.x, threadIdx.x, parity);
+            __trap();
+        }
+    }
+}
 
 // CTA-pair TMA: data lands in this CTA's SMEM, completion bytes are counted on
 // the mbarrier at `bar_cluster` (the leader CTA's barrier).
@@ -248,8 +272,6 @@ __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t n) {
 __device__ __forceinline__ void named_bar_arrive(uint32_t id, uint32_t n) {
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
-constexpr uint32_t kTmemBar = 1;            // allocator (warp 2) + warp 1 + warps 4..7
-constexpr uint32_t kTmemBarThreads = 6 * 32;
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 

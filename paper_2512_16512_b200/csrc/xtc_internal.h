@@ -25,6 +25,7 @@ constexpr int kTcEpiBuffers = 2;            // double-buffered per warp
 constexpr int kTcEpiSmem = 4 * kTcEpiStageBytes * kTcEpiBuffers;
 constexpr int kHaloMaxPatchBufs = 2;        // conv_halo: patch buffers (at most; the planner fits what SMEM allows)
 constexpr int kHaloMaxResidentKb = 32;      // conv_halo: resident-filter k-blocks (one mbarrier each)
+constexpr int kSplitClusterMaxCtas = 16;    // split_k_mode 2: K segments per cluster (> 8: non-portable size)
 
 // cudaFuncSetAttribute is a driver round trip: set the dynamic-SMEM opt-in once
 // per kernel variant and device, not on every launch (sweeps launch thousands).
@@ -33,6 +34,12 @@ cudaError_t ensure_smem_attr_impl(const void* kernel, int smem);   // keyed by (
 template <typename F>
 inline cudaError_t ensure_smem_attr(F* kernel, int smem) {
     return ensure_smem_attr_impl(reinterpret_cast<const void*>(kernel), smem);
+}
+// cluster sizes 9..16 need cudaFuncAttributeNonPortableClusterSizeAllowed (set once per kernel)
+cudaError_t ensure_nonportable_cluster_impl(const void* kernel);
+template <typename F>
+inline cudaError_t ensure_nonportable_cluster(F* kernel) {
+    return ensure_nonportable_cluster_impl(reinterpret_cast<const void*>(kernel));
 }
 
 // SIMT register budget: the TM x TN accumulator tile plus operands must fit
@@ -108,6 +115,8 @@ struct Plan {
     bool halo_pair = false;             // inner_m 256: cta_group::2 UMMAs (M = 256) over a CTA pair
     bool ovl = false;                   // overlapped epilogue (see TcParams::ovl); 64 KB epilogue SMEM
     int32_t msub = 1;                   // tcgen05 matmul: 128-row M-subtiles per CTA (tile_m = 128*cta_group*msub)
+    bool split_cluster = false;         // split_k_mode 2: the split_k K segments of a tile = one cluster's CTAs,
+                                        // reduced in-kernel; num_tiles then counts output tiles
     int32_t cluster_n = 1;              // tcgen05 matmul: CTAs on adjacent N tiles sharing A by multicast;
                                         // tiles (num_tiles) then count cluster tiles of cluster_n N tiles
     int64_t halo_patch_bytes = 0;
@@ -176,6 +185,9 @@ struct TcParams {
     // destination ([dest_rows][N] each); output tile rows land at gather_row0 + row
     const void* gather;
     int32_t n_gather, gather_row0;
+    // split_k_mode XTC_SPLITK_CLUSTER: the ksc K segments of a tile are the CTAs of one cluster
+    // (1 = off); cons_red = the consumer bits applied by that in-kernel reduction
+    int32_t ksc, cons_red;
 };
 constexpr int kTraceCtas = 160;          // >= #SMs: the whole persistent grid
 constexpr int kTraceK = 96;

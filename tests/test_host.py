@@ -401,6 +401,40 @@ def test_grid_sms_plan_and_legality():
         assert st == xtc.XTC_E_ILLEGAL_SCHEDULE and "grid_sms" in why
 
 
+# ------------------------------------------- split with the in-kernel reduction --
+def test_cluster_split_plan_and_legality():
+    """split_k_mode 2: one cluster of split_k CTAs per output tile, reduced in the kernel."""
+    CL = xtc.XTC_SPLITK_CLUSTER
+    base = dict(engine=1, tile_m=128, tile_n=64, tile_k=64, stages=4, buffer_c=0, acc_buffers=2, split_k_mode=CL)
+    d = xtc.matmul_desc(512, 512, 512)
+    st, info, why = xtc.xtc_schedule_check(d, xtc.schedule(**dict(base, split_k=8)), 148)
+    # 4 x 8 output tiles, each one cluster of 8 CTAs (one K segment of one k-block each)
+    assert st == 0 and info.num_tiles == 32 and info.cluster_x == 8 and info.grid_x == 256, why
+    assert info.k_blocks_per_split == 1 and info.workspace_bytes == 8 * 512 * 512 * 4
+    st, info, why = xtc.xtc_schedule_check(d, xtc.schedule(**dict(base, split_k=8, persistent=1)), 148)
+    assert st == 0 and info.grid_x == 144, why          # whole clusters only: 18 x 8
+    st, info, why = xtc.xtc_schedule_check(d, xtc.schedule(**dict(base, split_k=4, persistent=1, grid_sms=10)), 148)
+    assert st == 0 and info.grid_x == 8, why
+    for bad, frag in ((dict(buffer_c=1), "buffer_c"), (dict(tile_m=256, cluster_m=2, tile_n=128), "cluster_m"),
+                      (dict(split_k=17), "<= 16"), (dict(cluster_n=2), "cluster_n"), (dict(tile_m=256), "tile_m"),
+                      (dict(split_k=16), "empty K segment"), (dict(b_resident=1, split_k=2), "b_resident")):
+        kw = dict(base, split_k=4)
+        kw.update(bad)
+        st, _, why = xtc.xtc_schedule_check(d, xtc.schedule(**kw), 148)
+        assert st == xtc.XTC_E_ILLEGAL_SCHEDULE and frag in why, (bad, why)
+    simt = dict(engine=0, tile_m=64, tile_n=64, tile_k=16, inner_m=4, inner_n=4, stages=2, split_k=2,
+                split_k_mode=CL)
+    st, _, why = xtc.xtc_schedule_check(xtc.matmul_desc(256, 256, 256, "f32", "f32"), xtc.schedule(**simt), 148)
+    assert st == xtc.XTC_E_ILLEGAL_SCHEDULE and "tcgen05" in why
+    # the haloed-patch conv: L14 at batch 1 = 2 x 2 tiles, 9 segments of 2 k-blocks
+    dc = xtc.conv2d_desc(1, 14, 14, 256, 256, 3, 3, 1, 1)
+    halo = dict(base, pack_halo=1, tile_n=128, tile_k=128, stages=3, split_k=9)
+    st, info, why = xtc.xtc_schedule_check(dc, xtc.schedule(**halo), 148)
+    assert st == 0 and info.num_tiles == 4 and info.cluster_x == 9 and info.grid_x == 36, why
+    st, _, why = xtc.xtc_schedule_check(dc, xtc.schedule(**dict(halo, cluster_m=2)), 148)
+    assert st == xtc.XTC_E_ILLEGAL_SCHEDULE
+
+
 # --------------------------------------------- N3: descript + primitive log --
 def _fig4(desc):
     """PAPER.md Fig.4, call for call."""
