@@ -105,8 +105,8 @@ typedef enum { XTC_ORDER_MN = 0, XTC_ORDER_NM = 1 } xtc_order;
  *   CLUSTER  tcgen05: the split_k segments of an output tile are the CTAs of one thread-block
  *            cluster (split_k <= 16); after all partials are written each CTA sums 1/split_k of
  *            the tile's rows in ascending segment order inside the same kernel -- bit-identical
- *            to ORDERED, one launch, no second pass over the workspace.  Needs buffer_c 0,
- *            cluster_m 1, cluster_n 0/1, tile_m 128 (matmul) and b_resident 0. */
+ *            to ORDERED, one launch, no second pass over the workspace.  Needs cluster_m 1,
+ *            cluster_n 0/1, tile_m 128 (matmul), b_resident 0 (and buffer_c 0 for pack_halo). */
 typedef enum { XTC_SPLITK_ORDERED = 0, XTC_SPLITK_ATOMIC = 1, XTC_SPLITK_CLUSTER = 2 } xtc_splitk_mode;
 
 /* A schedule: Table I primitives as GPU loop-nest knobs.  The

@@ -150,6 +150,9 @@ def run_extras(xtc, torch, dev, peak):
                                                      split_k=sk, pack_warps=2) for sk in (2, 3)]
             if name == "L14":   # few tiles at small batch: narrower halo tiles spread over more SMs
                 cands.append(dict(HALO, tile_n=64, tile_k=128, stages=4))
+                # ... and the K segments of each tile over a cluster, reduced in the kernel (split_k_mode 2)
+                cands += [dict(HALO, tile_n=64, tile_k=128, stages=3, buffer_c=0, split_k=sk, split_k_mode=2)
+                          for sk in (6, 9)]
             r = _best(xtc, torch, dev, d, cands, [(nb, h, h, c), (3, 3, c, c)], peak)
             scan[f"{name}_n{nb}"] = {k: r.get(k) for k in ("tflops_med", "t_med_us", "warm_l2", "schedule", "error")}
     out["conv_batch_scan_bf16"] = scan

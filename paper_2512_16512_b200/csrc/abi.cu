@@ -60,6 +60,10 @@ cudaError_t ensure_smem_attr_impl(const void* kernel, int smem) {
     if (smem <= have) return cudaSuccess;
     e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e == cudaSuccess) have = smem;
+    // diagnostics (A/B): XTC_CARVEOUT=<0..100> sets the preferred L1/SMEM carveout of the kernels
+    if (e == cudaSuccess)
+        if (const char* c = getenv("XTC_CARVEOUT"))
+            e = cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(c));
     return e;
 }
 cudaError_t ensure_nonportable_cluster_impl(const void* kernel) {

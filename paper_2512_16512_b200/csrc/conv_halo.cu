@@ -482,7 +482,7 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
             if (trace && warp == 4 && lane == 0 && tj < kTraceTiles) trace[8 + 2 * kTraceK + 2 * tj + 1] = ptx::globaltimer();
             ++tj;
             if (lane == 0) {
-                if constexpr (PAIR) ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&tempty[acc]), 0));
+                if constexpr (PAIR) ptx::mbar_arrive_remote(ptx::mapa_shared(ptx::smem_u32(&tempty[acc]), 0));
                 else ptx::mbar_arrive(&tempty[acc]);
             }
             if (++acc == p.acc_buffers) { acc = 0; aph ^= 1u; }
@@ -491,10 +491,11 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
                 const int p1 = min(P, p0 + p.rt * MSUB);
                 cluster_split_reduce(ksig, kst, ksc, (int)krank, p.Wk, p.M, p.ws_ld, ((int64_t)nimg * P + p0) * Q,
                                      (p1 - p0) * Q, n0, (int)((p.N - n0) < p.tile_n ? (p.N - n0) : p.tile_n), p.C, p.ldc,
-                                     bf16_out, p.cons_red, p.bias, (int)threadIdx.x - 128);
+                                     bf16_out, p.cons_red, p.bias, (int)threadIdx.x - 128, false, trace);
             }
         }
         if (p.buffer_c && lane == 0) ptx::bulk_wait<0>();
+        if (trace && warp == 4 && lane == 0) trace[6] = ptx::globaltimer();   // XTC_TRACE: stores complete
     }
 
     ptx::tc_fence_before();
@@ -503,6 +504,7 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
     if (warp == 2) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc<CG>(*reinterpret_cast<volatile uint32_t*>(tmem_slot), p.tmem_cols);
+        if (trace && lane == 0) trace[7] = ptx::globaltimer();                // XTC_TRACE: TMEM released
     }
 }
 

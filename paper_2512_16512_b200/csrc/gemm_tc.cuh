@@ -504,7 +504,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                     ptx::tc_fence_before();
                     __syncwarp();
                     if (lane == 0) {                                     // TMEM free: the next tile's MMAs start
-                        if constexpr (CG == 2) ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&tempty[acc]), 0));
+                        if constexpr (CG == 2) ptx::mbar_arrive_remote(ptx::mapa_shared(ptx::smem_u32(&tempty[acc]), 0));
                         else ptx::mbar_arrive(&tempty[acc]);
                     }
                     ptx::fence_proxy_async_smem();
@@ -660,7 +660,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             __syncwarp();
             if (trace && warp == 4 && lane == 0 && trace_k < kTraceTiles) trace[8 + 2 * kTraceK + 2 * trace_k++ + 1] = ptx::globaltimer();
             if (lane == 0) {                           // TMEM buffer free for the next tile
-                if constexpr (CG == 2) ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&tempty[acc]), 0));
+                if constexpr (CG == 2) ptx::mbar_arrive_remote(ptx::mapa_shared(ptx::smem_u32(&tempty[acc]), 0));
                 else ptx::mbar_arrive(&tempty[acc]);
             }
             if (++acc == p.acc_buffers) { acc = 0; aph ^= 1; }
@@ -670,10 +670,11 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 cluster_split_reduce(ksig, kst, ksc, (int)krank, p.Wk, p.M, p.ws_ld, r0,
                                      (int)(p.M - r0 < TILE_M ? p.M - r0 : TILE_M), c0,
                                      (int)(p.N - c0 < p.tile_n ? p.N - c0 : p.tile_n),
-                                     p.C, p.ldc, p.out_bf16 != 0, p.cons_red, p.bias, (int)threadIdx.x - 128);
+                                     p.C, p.ldc, p.out_bf16 != 0, p.cons_red, p.bias, (int)threadIdx.x - 128, p.buffer_c != 0, trace);
             }
         }
         if (p.buffer_c && lane == 0) ptx::bulk_wait<0>();
+        if (trace && warp == 4 && lane == 0) trace[6] = ptx::globaltimer();   // XTC_TRACE: stores complete
     }
 
     ptx::tc_fence_before();
@@ -683,6 +684,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     if (warp == 2) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc<CG>(*reinterpret_cast<volatile uint32_t*>(tmem_slot), p.tmem_cols);
+        if (trace && lane == 0) trace[7] = ptx::globaltimer();                // XTC_TRACE: TMEM released
     }
 }
 

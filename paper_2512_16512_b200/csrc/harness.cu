@@ -341,6 +341,10 @@ cudaError_t launch_delay(uint64_t ns, cudaStream_t st) {
 }
 
 cudaError_t launch_flush(void* buf, int64_t bytes, uint32_t salt, cudaStream_t st) {
+    if (const char* c = getenv("XTC_CARVEOUT")) {     // diagnostics (A/B): same carveout as the GEMM kernels
+        static bool done = false;
+        if (!done) { cudaFuncSetAttribute(flush_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(c)); done = true; }
+    }
     // the last 16 bytes of the buffer serve as the (never written) sink
     flush_kernel<<<148 * 8, 512, 0, st>>>(static_cast<const uint4*>(buf), bytes / 16 - 1, salt,
                                           reinterpret_cast<uint32_t*>(static_cast<char*>(buf) + bytes - 16));

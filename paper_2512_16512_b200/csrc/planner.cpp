@@ -435,7 +435,6 @@ xtc_status make_plan(const xtc_op_desc& d, const xtc_schedule& s, int num_sms, P
         if (s.engine != XTC_ENGINE_TCGEN05) ILLEGAL("split: split_k_mode 2 (cluster reduction) needs the tcgen05 engine");
         if (p.split_k > kSplitClusterMaxCtas) ILLEGAL("split: split_k_mode 2 puts the %d K segments in one cluster (<= %d CTAs)",
                                                      p.split_k, kSplitClusterMaxCtas);
-        if (s.buffer_c) ILLEGAL("split: split_k_mode 2 writes partials and the reduced output with direct stores (buffer_c 0)");
     }
     if (p.atomic && d.out_dtype != XTC_F32) ILLEGAL("atomic split-K needs fp32 output");
     if (s.split_n_at) {

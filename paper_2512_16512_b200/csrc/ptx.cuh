@@ -157,6 +157,9 @@ __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.w
 template <int N>
 __device__ __forceinline__ void bulk_wait() { asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory"); }
 
+__device__ __forceinline__ void fence_proxy_async_global() {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -179,6 +182,18 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t saddr, uint32_t rank) {
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+// Remote arrive with the default (release.cta) semantics: a bare SYNCS.ARRIVE.  Enough where the
+// arrive only orders tcgen05 work (tcgen05.fence::before_thread_sync before it, e.g. TMEM drained
+// -> the pair leader's next MMA); release.cluster (above) costs a MEMBAR.ALL.GPU per arrive.
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// Relaxed cluster-scope arrive: the release is a preceding fence_acq_rel_gpu, paid once for
+// several arrives (fence + relaxed arrive = a release pattern at cluster scope)
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 // wait with cluster-scope acquire: pairs with mbar_arrive_cluster (release.cluster) of a peer CTA,
 // so the peer's writes before its arrive (incl. global memory) are visible after the wait
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {

@@ -24,85 +24,90 @@
 
 namespace xtc {
 
-constexpr int kSplitClusterMax = 16;        // cluster size limit (> 8 needs the non-portable opt-in)
 
 struct ClusterSplitState {
     uint32_t parity = 0;                    // bit b: phase parity of signal barrier b
     int which = 0;                          // barrier of the next tile
 };
 
-// Called by all 128 epilogue threads (tid = 0..127) after their partial stores of this tile.
+// Called by all 128 epilogue threads (tid = 0..127) after their partial stores of this tile
+// (direct stores, or -- tma_partials -- TMA stores issued by each warp's lane 0).
 // rows [row0, row0 + nrows) of the output are the tile's valid rows (contiguous in C and W),
 // cols [n0, n0 + ncols) its valid columns.
 __device__ __forceinline__ void cluster_split_reduce(uint64_t* sig, ClusterSplitState& st, int ksc, int krank,
                                                      const float* __restrict__ W, int64_t M, int64_t ws_ld,
                                                      int64_t row0, int nrows, int64_t n0, int ncols, void* C,
                                                      int64_t ldc, bool out_bf16, int cons, const float* bias,
-                                                     int tid) {
-    // the warp's partial stores precede the signal (__syncwarp orders them before lane 0's
-    // gpu-scope fence; the release arrive publishes them to the cluster)
+                                                     int tid, bool tma_partials, uint64_t* trace = nullptr) {
+    // the warp's partial stores precede the signal: __syncwarp orders them before lane 0's
+    // gpu-scope fence, and fence + relaxed cluster-scope arrives form the release (one fence for
+    // all split_k arrives: a release.cluster arrive would pay a MEMBAR.ALL.GPU each)
     __syncwarp();
     uint64_t* bar = sig + st.which;
     if ((tid & 31) == 0) {
-        __threadfence();
+        if (tma_partials) {                  // this warp's TMA stores of its partial rows: complete,
+            ptx::bulk_wait<0>();             // then ordered with the generic proxy of the readers
+            ptx::fence_proxy_async_global();
+        }
+        ptx::fence_acq_rel_gpu();
         const uint32_t a = ptx::smem_u32(bar);
-        for (int j = 0; j < ksc; ++j) ptx::mbar_arrive_cluster(ptx::mapa_shared(a, (uint32_t)j));
+        for (int j = 0; j < ksc; ++j) ptx::mbar_arrive_cluster_relaxed(ptx::mapa_shared(a, (uint32_t)j));
     }
+    if (trace && tid == 0) trace[3] = ptx::globaltimer();       // XTC_TRACE: signal sent, peers' seen, done
     ptx::mbar_wait_cluster(bar, (st.parity >> st.which) & 1u);
+    if (trace && tid == 0) trace[4] = ptx::globaltimer();
     st.parity ^= 1u << st.which;
     st.which ^= 1;
 
     const int rpc = (nrows + ksc - 1) / ksc;
     const int r_lo = krank * rpc;
     const int r_hi = min(nrows, r_lo + rpc);
-    if (r_lo >= r_hi) return;
-    const int groups = (ncols + 3) >> 2;               // 4-column groups per row
+    // 128 threads = (128 / gp) rows x gp four-column groups per pass, gp = pow2 >= groups: a warp
+    // reads and writes whole row segments (coalesced); the segment sums are one short loop
+    const int groups = (ncols + 3) >> 2;
+    int gp = 1;
+    while (gp < groups) gp <<= 1;
+    const int g = tid & (gp - 1);
+    const int rstep = 128 / gp;
     const int64_t plane = M * ws_ld;
-    const int items = (r_hi - r_lo) * groups;
-    for (int it = tid; it < items; it += 128) {
-        const int rr = it / groups;
-        const int g = it - rr * groups;
-        const int64_t row = row0 + r_lo + rr;
-        const int64_t col = n0 + 4 * g;
-        const int cnt = min(4, ncols - 4 * g);
-        const float* src = W + row * ws_ld + col;
-        float a[4];
-        if (cnt == 4) {
-            float4 v[kSplitClusterMax];
-#pragma unroll
-            for (int s = 0; s < kSplitClusterMax; ++s)
-                if (s < ksc) v[s] = __ldcg(reinterpret_cast<const float4*>(src + s * plane));
-            float4 acc = v[0];
-#pragma unroll
-            for (int s = 1; s < kSplitClusterMax; ++s)
-                if (s < ksc) { acc.x += v[s].x; acc.y += v[s].y; acc.z += v[s].z; acc.w += v[s].w; }
-            a[0] = acc.x; a[1] = acc.y; a[2] = acc.z; a[3] = acc.w;
-        } else {
-            for (int j = 0; j < cnt; ++j) {
-                float acc = __ldcg(src + j);
-                for (int s = 1; s < ksc; ++s) acc += __ldcg(src + s * plane + j);
-                a[j] = acc;
-            }
-        }
-        const int64_t off = row * ldc + col;
-        if (cons)
-            for (int j = 0; j < cnt; ++j) a[j] = consume1(a[j], cons, bias, C, out_bf16, off + j, col + j);
-        if (out_bf16) {
-            uint16_t* dst = reinterpret_cast<uint16_t*>(C) + off;
-            if (cnt == 4 && (reinterpret_cast<uintptr_t>(dst) & 7) == 0) {
-                *reinterpret_cast<uint2*>(dst) = make_uint2(ptx::pack_bf16x2(a[0], a[1]), ptx::pack_bf16x2(a[2], a[3]));
+    const int64_t col = n0 + 4 * g;
+    const int cnt = min(4, ncols - 4 * g);
+    const bool vec = ((ldc & 3) == 0) && ((n0 & 3) == 0) && cnt == 4 && (reinterpret_cast<uintptr_t>(C) & 15) == 0;
+    if (gp <= 128 && cnt > 0) {
+        for (int r = r_lo + tid / gp; r < r_hi; r += rstep) {
+            const int64_t row = row0 + r;
+            const float* src = W + row * ws_ld + col;
+            float a[4];
+            if (cnt == 4) {                                  // ws_ld is a multiple of 4: 16-byte loads
+                float4 acc = __ldcg(reinterpret_cast<const float4*>(src));
+#pragma unroll 4
+                for (int s = 1; s < ksc; ++s) {
+                    const float4 v = __ldcg(reinterpret_cast<const float4*>(src + s * plane));
+                    acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+                }
+                a[0] = acc.x; a[1] = acc.y; a[2] = acc.z; a[3] = acc.w;
             } else {
-                for (int j = 0; j < cnt; ++j) dst[j] = (uint16_t)(ptx::pack_bf16x2(a[j], 0.f) & 0xFFFFu);
+                for (int j = 0; j < cnt; ++j) {
+                    float acc = __ldcg(src + j);
+                    for (int s = 1; s < ksc; ++s) acc += __ldcg(src + s * plane + j);
+                    a[j] = acc;
+                }
             }
-        } else {
-            float* dst = reinterpret_cast<float*>(C) + off;
-            if (cnt == 4 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-                *reinterpret_cast<float4*>(dst) = make_float4(a[0], a[1], a[2], a[3]);
+            const int64_t off = row * ldc + col;
+            if (cons)
+                for (int j = 0; j < cnt; ++j) a[j] = consume1(a[j], cons, bias, C, out_bf16, off + j, col + j);
+            if (out_bf16) {
+                uint16_t* dst = reinterpret_cast<uint16_t*>(C) + off;
+                if (vec) *reinterpret_cast<uint2*>(dst) = make_uint2(ptx::pack_bf16x2(a[0], a[1]), ptx::pack_bf16x2(a[2], a[3]));
+                else for (int j = 0; j < cnt; ++j) dst[j] = (uint16_t)(ptx::pack_bf16x2(a[j], 0.f) & 0xFFFFu);
             } else {
-                for (int j = 0; j < cnt; ++j) dst[j] = a[j];
+                float* dst = reinterpret_cast<float*>(C) + off;
+                if (vec) *reinterpret_cast<float4*>(dst) = make_float4(a[0], a[1], a[2], a[3]);
+                else for (int j = 0; j < cnt; ++j) dst[j] = a[j];
             }
         }
     }
+    if (trace && tid == 0) trace[5] = ptx::globaltimer();
 }
 
 }  // namespace xtc

@@ -52,6 +52,10 @@ MATMUL_CASES = [
     ("s4-tf32", mm(tile_k=32, split_k=4), 256, 256, 512, "tf32", "f32"),
     ("s2-3xtf32", mm(tile_k=32, stages=3, split_k=2), 256, 256, 256, "f32", "f32"),
     ("s8-tile256", mm(tile_n=256, stages=3, split_k=8), 256, 512, 1024, "bf16", "bf16"),
+    # partials staged in SMEM and written by TMA stores (buffer_c 1), completed before the signal
+    ("s4-tma-partials", mm(split_k=4, buffer_c=1), 300, 256, 512, "bf16", "bf16"),
+    ("s3-tma-partials-persistent", mm(split_k=3, buffer_c=1, tile_n=64, persistent=1, grid_sms=6), 512, 320, 576,
+     "bf16", "f32"),
 ]
 
 

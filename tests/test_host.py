@@ -415,7 +415,9 @@ def test_cluster_split_plan_and_legality():
     assert st == 0 and info.grid_x == 144, why          # whole clusters only: 18 x 8
     st, info, why = xtc.xtc_schedule_check(d, xtc.schedule(**dict(base, split_k=4, persistent=1, grid_sms=10)), 148)
     assert st == 0 and info.grid_x == 8, why
-    for bad, frag in ((dict(buffer_c=1), "buffer_c"), (dict(tile_m=256, cluster_m=2, tile_n=128), "cluster_m"),
+    st, _, why = xtc.xtc_schedule_check(d, xtc.schedule(**dict(base, split_k=4, buffer_c=1)), 148)
+    assert st == 0, why                                  # partials through SMEM + TMA stores
+    for bad, frag in ((dict(tile_m=256, cluster_m=2, tile_n=128), "cluster_m"),
                       (dict(split_k=17), "<= 16"), (dict(cluster_n=2), "cluster_n"), (dict(tile_m=256), "tile_m"),
                       (dict(split_k=16), "empty K segment"), (dict(b_resident=1, split_k=2), "b_resident")):
         kw = dict(base, split_k=4)

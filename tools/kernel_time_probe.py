@@ -22,15 +22,16 @@ CASES = [
                                     split_k_mode=CL)),
     ("mm512", (512, 512, 512), dict(TC, tile_n=64, tile_k=64, stages=4, buffer_c=0, acc_buffers=1, split_k=8,
                                     split_k_mode=CL)),
-    ("mm512", (512, 512, 512), dict(TC, tile_n=64, tile_k=64, stages=4, buffer_c=0, acc_buffers=1, split_k=4)),
+    ("mm512", (512, 512, 512), dict(TC, tile_n=64, tile_k=64, stages=4, buffer_c=1, acc_buffers=1, split_k=4,
+                                    split_k_mode=CL)),
     ("mm1024", (1024, 1024, 1024), dict(TC, tile_n=64, tile_k=128, stages=4, buffer_c=1, acc_buffers=2,
                                         raster_group=8, pack_warps=2)),
     ("L14n1", (1, 14, 256), dict(HALO, tile_n=128, tile_k=128, stages=3, buffer_c=1)),
     ("L14n1", (1, 14, 256), dict(HALO, tile_n=64, tile_k=128, stages=3, buffer_c=0, split_k=6, split_k_mode=CL)),
     ("L14n1", (1, 14, 256), dict(HALO, tile_n=128, tile_k=128, stages=3, buffer_c=0, split_k=9, split_k_mode=CL)),
     ("L14n32", (32, 14, 256), dict(HALO, tile_n=128, tile_k=128, stages=3, buffer_c=1)),
-    ("L56n1", (1, 56, 64), dict(HALO, tile_n=64, stages=2, buffer_c=1, b_resident=1)),
-    ("L56n32", (32, 56, 64), dict(HALO, tile_n=64, stages=2, buffer_c=1, b_resident=1)),
+    ("L56n1", (1, 56, 64), dict(HALO, tile_n=64, tile_k=64, stages=2, buffer_c=1, b_resident=1)),
+    ("L56n32", (32, 56, 64), dict(HALO, tile_n=64, tile_k=64, stages=2, buffer_c=1, b_resident=1)),
 ]
 
 
