@@ -422,7 +422,10 @@ def main_xtc(args):
         if fused:
             if kev_pair is not None:
                 kev_pair[0].record(stream)
-            op.run_gather(a, b, fused.dests, r0, M, stream=sp)
+            if fused.multicast_ptr:                 # NVLS: one multimem store per vector, replicated by the switch
+                op.run_multicast(a, b, fused.multicast_ptr, r0, M, multimem=True, stream=sp)
+            else:                                   # unicast: one TMA store per destination
+                op.run_gather(a, b, fused.dests, r0, M, stream=sp)
             if kev_pair is not None:
                 kev_pair[1].record(stream)
             fused.barrier()                         # every rank's tiles have landed in every copy
@@ -520,7 +523,10 @@ def main_xtc(args):
                 stream.wait_event(ev_out[j])         # buffer j's result was copied out by step i-2
             if fused2 is not None:
                 fz = fused if j == 0 else fused2
-                dop.run_gather(da, db, fz.dests, r0, M, stream=sp)
+                if fz.multicast_ptr:
+                    dop.run_multicast(da, db, fz.multicast_ptr, r0, M, multimem=True, stream=sp)
+                else:
+                    dop.run_gather(da, db, fz.dests, r0, M, stream=sp)
                 if i >= 1:
                     # this rank's D2H of step i-1 (from the other buffer) must finish before the barrier
                     # of step i: a peer's step-(i+1) stores into that buffer follow its own barrier i,
@@ -684,7 +690,9 @@ def main_xtc(args):
             "config": {"workload": WORKLOAD,
                        "model": None, "global_batch": 1, "seq_len": None,
                        "parallelism": ((f"M-sharded x{world}, all-gather fused into the GEMM epilogue "
-                                        f"(xtc_run_gather: TMA stores into every rank's symmetric-memory C)"
+                                        + ("(xtc_run_multicast: multimem stores to the NVLS multicast address of "
+                                           "the symmetric-memory C)" if fused.multicast_ptr else
+                                           "(xtc_run_gather: TMA stores into every rank's symmetric-memory C)")
                                         + (f"; {fused_note}" if fused_note else ""))
                                        if fused else
                                        (f"M-sharded x{world}, {CH} block-cyclic chunks per rank, each NCCL "

@@ -285,6 +285,20 @@ xtc_status xtc_run(xtc_op op, const void* const* inputs, void* const* outputs, v
 xtc_status xtc_run_gather(xtc_op op, const void* const* inputs, void* const* dests, int32_t n_dest,
                           int64_t row_offset, int64_t dest_rows, void* stream);
 
+/* The same fused all-gather through ONE multicast destination (the NVLS form):
+ * `dest` is an NVLink-SHARP multicast address (CUDA multicast object bound to every rank's
+ * [dest_rows][N] buffer and mapped here, e.g. torch symmetric memory's multicast_ptr); the
+ * epilogue reads each staged output tile back from SMEM and writes it with
+ * multimem.st.global.v4 (16-byte vectors, whole 512-byte row segments per warp), and the
+ * NVSwitch replicates every store to all ranks -- each GPU sends its shard once instead of
+ * once per peer.  multimem = 0 writes the same vectors with ordinary st.global.v4 to a plain
+ * device pointer (one destination; the single-GPU form of the same write-out path).
+ * Row placement, requirements and ordering as xtc_run_gather, plus N (and the row pitch) a
+ * multiple of 8 bf16 / 4 fp32 elements.  A multimem address on a device without multicast
+ * support faults (the caller checks CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED). */
+xtc_status xtc_run_multicast(xtc_op op, const void* const* inputs, void* dest, int64_t row_offset,
+                             int64_t dest_rows, int32_t multimem, void* stream);
+
 /* a8 + a9 -- Executor + Evaluator.  Synchronous.  Sequence:
  *   1. if cfg->validate: fill outputs with NaN, run once, compute (or reuse)
  *      the fp64 GPU reference R and D, compare -> max_norm_err, n_mismatch, n_nan;

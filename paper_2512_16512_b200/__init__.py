@@ -134,6 +134,7 @@ def lib():
         L.xtc_schedule_default.argtypes = [P(xtc_op_desc), c_int32, P(xtc_schedule)]
         L.xtc_run.argtypes = [xtc_op, P(c_void_p), P(c_void_p), c_void_p]
         L.xtc_run_gather.argtypes = [xtc_op, P(c_void_p), P(c_void_p), c_int32, c_int64, c_int64, c_void_p]
+        L.xtc_run_multicast.argtypes = [xtc_op, P(c_void_p), c_void_p, c_int64, c_int64, c_int32, c_void_p]
         L.xtc_measure.argtypes = [xtc_op, P(c_void_p), P(c_void_p), P(xtc_measure_cfg), P(xtc_metrics), c_void_p]
         L.xtc_sweep.argtypes = [xtc_op, P(xtc_schedule), c_int32, P(c_void_p), P(c_void_p), P(xtc_measure_cfg),
                                 P(xtc_metrics), c_void_p]
@@ -213,6 +214,11 @@ def xtc_run_gather(op, inputs, dests, row_offset, dest_rows, stream=0) -> None:
     (the all-gather fused into the epilogue; include/xtc.h)."""
     _check(lib().xtc_run_gather(op, _ptrs(inputs), _ptrs(dests), len(dests), row_offset, dest_rows,
                                 c_void_p(stream)))
+
+
+def xtc_run_multicast(op, inputs, dest, row_offset, dest_rows, multimem, stream=0) -> None:
+    _check(lib().xtc_run_multicast(op, _ptrs(inputs), c_void_p(dest), c_int64(row_offset), c_int64(dest_rows),
+                                   c_int32(int(multimem)), c_void_p(stream)))
 
 
 def xtc_measure(op, inputs, outputs, cfg: xtc_measure_cfg, stream=0) -> xtc_metrics:
@@ -341,6 +347,11 @@ class Op:
         """dests: device pointers (ints) of [dest_rows][N] outputs, local or peer-mapped."""
         xtc_run_gather(self.handle, self._inputs(a, b, bias), list(dests), row_offset, dest_rows,
                        self._stream(stream))
+
+    def run_multicast(self, a, b, dest, row_offset, dest_rows, multimem=False, stream=None, bias=None) -> None:
+        """dest: an int device address -- an NVLS multicast address (multimem=True) or a plain pointer."""
+        xtc_run_multicast(self.handle, self._inputs(a, b, bias), int(dest), row_offset, dest_rows, multimem,
+                          self._stream(stream))
 
     def measure(self, a, b, c, cfg: xtc_measure_cfg = None, stream=None, bias=None) -> xtc_metrics:
         cfg = cfg or measure_cfg()

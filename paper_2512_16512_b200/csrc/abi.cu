@@ -567,6 +567,9 @@ static ConvGeom conv_geom(const xtc_op_desc& d) {
 struct GatherArgs {            // xtc_run_gather: device tensor maps of the destinations
     const void* maps;
     int32_t n, row0;
+    void* mc = nullptr;        // xtc_run_multicast: the destination and its store mode (1 plain, 2 multimem)
+    int64_t mc_ld = 0;
+    int32_t mc_mode = 0;
 };
 
 static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cudaStream_t st,
@@ -666,6 +669,9 @@ static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cud
             tp.gather = ga->maps;
             tp.n_gather = ga->n;
             tp.gather_row0 = ga->row0;
+            tp.mc = ga->mc;
+            tp.mc_ld = ga->mc_ld;
+            tp.mc_mode = ga->mc_mode;
         }
         const size_t trace_bytes = (size_t)kTraceCtas * kTraceSlots * 8;
         if (!op->trace_path.empty()) {
@@ -811,6 +817,51 @@ extern "C" xtc_status xtc_run_gather(xtc_op op, const void* const* inputs, void*
     void* c_local = static_cast<uint8_t*>(dests[0]) + row_offset * ld * os;
     GatherArgs ga{op->gmaps_dev, n_dest, (int32_t)row_offset};
     return run_impl(op, inputs[0], inputs[1], c_local, st, &ga);
+}
+
+extern "C" xtc_status xtc_run_multicast(xtc_op op, const void* const* inputs, void* dest, int64_t row_offset,
+                                        int64_t dest_rows, int32_t multimem, void* stream) {
+    if (!op || !inputs || !dest || !inputs[0] || !inputs[1]) return fail(XTC_E_INVALID_ARG, "null op or tensor pointer");
+    if (!op->has_plan) return fail(XTC_E_NO_SCHEDULE, "xtc_run_multicast before xtc_schedule_apply");
+    if (multimem != 0 && multimem != 1) return fail(XTC_E_INVALID_ARG, "xtc_run_multicast: multimem must be 0 or 1");
+    const Plan& p = op->plan;
+    const xtc_op_desc& d = op->d;
+    if (d.kind != XTC_OP_MATMUL || p.engine != XTC_ENGINE_TCGEN05 || !p.sch.buffer_c || p.split_k != 1 || p.halo ||
+        p.has_tail || p.cons_pass || p.split3 || (d.consumer & XTC_CONSUMER_ACCUMULATE) || p.cluster_n > 1)
+        return fail(XTC_E_UNSUPPORTED, "xtc_run_multicast: needs a tcgen05 matmul schedule with buffer_c=1, split_k=1, "
+                                       "cluster_n 1, no split_n_at root, fused consumers other than accumulate");
+    const int os = dsize(d.out_dtype);
+    const int64_t ld = d.ldc ? d.ldc : p.n_total;
+    const int64_t tile_rows = 128 * (int64_t)p.cta_group * p.msub;
+    if (p.M % tile_rows) return fail(XTC_E_UNSUPPORTED, "xtc_run_multicast: M must be a multiple of the CTA tile rows");
+    if ((p.N * os) % 16 || (ld * os) % 16)
+        return fail(XTC_E_UNSUPPORTED, "xtc_run_multicast: N and the row pitch must be multiples of 16 bytes");
+    if (row_offset < 0 || row_offset + p.M > dest_rows)
+        return fail(XTC_E_INVALID_ARG, "xtc_run_multicast: rows [row_offset, row_offset + M) must lie in [0, dest_rows)");
+    for (int i = 0; i < 2; ++i)
+        if (reinterpret_cast<uintptr_t>(inputs[i]) & 15) return fail(XTC_E_INVALID_ARG, "TMA needs 16-byte aligned inputs");
+    if (reinterpret_cast<uintptr_t>(dest) & 15) return fail(XTC_E_INVALID_ARG, "xtc_run_multicast: unaligned destination");
+    if (bind_bias(op, inputs) != XTC_OK) return XTC_E_INVALID_ARG;
+    DeviceGuard g(op->device);
+    if (multimem) {
+        typedef CUresult (*PFN_attr)(int*, CUdevice_attribute, CUdevice);
+        static PFN_attr get_attr = nullptr;
+        if (!get_attr) {
+            cudaDriverEntryPointQueryResult q;
+            void* fn = nullptr;
+            CU_TRY(cudaGetDriverEntryPoint("cuDeviceGetAttribute", &fn, cudaEnableDefault, &q), "cudaGetDriverEntryPoint");
+            if (!fn || q != cudaDriverEntryPointSuccess) return fail(XTC_E_CUDA, "cuDeviceGetAttribute unavailable");
+            get_attr = reinterpret_cast<PFN_attr>(fn);
+        }
+        int mc = 0;
+        if (get_attr(&mc, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, (CUdevice)op->device) != CUDA_SUCCESS || !mc)
+            return fail(XTC_E_UNSUPPORTED, "xtc_run_multicast: the device does not support multicast (NVLS)");
+    }
+    // the local C map is encoded on the shard's rows of the destination but never stored through:
+    // the epilogue writes every staged tile with 16-byte (multimem) stores
+    void* c_local = static_cast<uint8_t*>(dest) + row_offset * ld * os;
+    GatherArgs ga{nullptr, 0, (int32_t)row_offset, dest, ld, multimem ? 2 : 1};
+    return run_impl(op, inputs[0], inputs[1], c_local, (cudaStream_t)stream, &ga);
 }
 
 // --------------------------------------------------------------- measure --

@@ -37,6 +37,33 @@
 
 namespace xtc {
 
+// xtc_run_multicast write-out: `nboxes` (1 or 4) staged boxes of 32 rows x 128 bytes at box0 (box b
+// at box0 + b * kTcEpiStageBytes; row i at i * 128 with logical 16-byte chunk j at (j ^ (i & 7)) * 16,
+// the 128-byte swizzle of the TMA-store staging) are read back by the whole warp and written as
+// 16-byte vectors to rows row0.., columns col0.. of p.mc: with 4 boxes each warp instruction writes
+// one 512-byte row segment, with 1 box four 128-byte rows.
+__device__ __forceinline__ void mc_store_boxes(const TcParams& p, const uint8_t* box0, int nboxes, int64_t row0,
+                                               int64_t col0, int lane) {
+    const int os = p.out_bf16 ? 2 : 4;
+    const int j = lane & 7;
+    const int b = nboxes == 4 ? (lane >> 3) : 0;
+    const int sub = nboxes == 4 ? 0 : (lane >> 3);
+    const int step = nboxes == 4 ? 1 : 4;
+    const int64_t c = col0 + (int64_t)b * (128 / os) + j * (16 / os);
+    if (c >= p.N) return;
+    uint8_t* const base = static_cast<uint8_t*>(p.mc);
+    for (int i = sub; i < 32; i += step) {
+        const uint4 w = *reinterpret_cast<const uint4*>(box0 + b * kTcEpiStageBytes + i * 128 + ((j ^ (i & 7)) << 4));
+        void* dst = base + ((row0 + i) * p.mc_ld + c) * os;
+        if (p.mc_mode == 2) {
+            if (os == 2) ptx::multimem_st_v4_bf16x2(dst, w);
+            else ptx::multimem_st_v4_f32(dst, w);
+        } else {
+            ptx::st_global_v4(dst, w);
+        }
+    }
+}
+
 template <bool TF32, bool CONV, int CG, bool SPLIT3, int MS>
 __global__ void __launch_bounds__(kTcThreads, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -524,7 +551,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                         }
                         ptx::bulk_commit();
                     };
-                    if (lane == 0) {                                     // subtile 1: rows m0t + 128 + 32q
+                    if (p.mc_mode) {                                     // subtile 1: rows m0t + 128 + 32q
+                        mc_store_boxes(p, big, 4, p.gather_row0 + m0t + 128 + 32 * q, n0, lane);
+                    } else if (lane == 0) {
                         store_rows(m0t + 128 + 32 * q);
                         ptx::bulk_wait_read<0>();                        // ... have read the SMEM tile
                     }
@@ -541,7 +570,12 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                     }
                     ptx::fence_proxy_async_smem();
                     __syncwarp();
-                    if (lane == 0) store_rows(m0t + 32 * q);              // subtile 0: rows m0t + 32q
+                    if (p.mc_mode) {                                     // subtile 0: rows m0t + 32q
+                        mc_store_boxes(p, big, 4, p.gather_row0 + m0t + 32 * q, n0, lane);
+                        __syncwarp();                                    // read before the next tile's drain
+                    } else if (lane == 0) {
+                        store_rows(m0t + 32 * q);
+                    }
                     if (trace && warp == 4 && lane == 0 && trace_k < kTraceTiles) trace[8 + 2 * kTraceK + 2 * trace_k++ + 1] = ptx::globaltimer();
                     if (++acc == p.acc_buffers) { acc = 0; aph ^= 1; }
                     continue;
@@ -594,7 +628,11 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                     if (last_half) {
                         ptx::fence_proxy_async_smem();
                         __syncwarp();
-                        if (lane == 0) {
+                        if (p.mc_mode) {
+                            mc_store_boxes(p, stage + buf * kTcEpiStageBytes, 1, p.gather_row0 + m0 + 32 * q,
+                                           bf16_out ? (n0 + (c & ~63)) : (n0 + c), lane);
+                            __syncwarp();                        // read before the buffer is refilled
+                        } else if (lane == 0) {
                             const int col = bf16_out ? (n0 + (c & ~63)) : (n0 + c);
                             if (p.n_gather) {
                                 // fused all-gather: the staged chunk goes to every destination

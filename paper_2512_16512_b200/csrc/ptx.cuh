@@ -400,6 +400,23 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     return r;
 }
 
+// 16-byte global stores of the epilogue write-out: plain, or multimem (NVLS multicast address:
+// the switch replicates the store to every GPU bound to the multicast object)
+__device__ __forceinline__ void st_global_v4(void* p, uint4 v) {
+    asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ void multimem_st_v4_bf16x2(void* p, uint4 v) {
+    asm volatile("multimem.st.global.v4.bf16x2 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ void multimem_st_v4_f32(void* p, uint4 v) {
+    asm volatile("multimem.st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(__uint_as_float(v.x)),
+                 "f"(__uint_as_float(v.y)), "f"(__uint_as_float(v.z)), "f"(__uint_as_float(v.w))
+                 : "memory");
+}
+
 // Pin a loop-invariant value in a register: the compiler otherwise re-loads kernel
 // parameters from the constant bank inside hot loops (a dependent LDC -> compare -> branch
 // chain per use), which dominates a single-thread MMA-issue loop with short UMMAs.

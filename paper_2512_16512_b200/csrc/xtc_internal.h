@@ -188,6 +188,12 @@ struct TcParams {
     // split_k_mode XTC_SPLITK_CLUSTER: the ksc K segments of a tile are the CTAs of one cluster
     // (1 = off); cons_red = the consumer bits applied by that in-kernel reduction
     int32_t ksc, cons_red;
+    // xtc_run_multicast: the staged output tiles are read back from SMEM and written with 16-byte
+    // stores to mc ([rows][mc_ld] elements, tile rows at gather_row0 + row); mc_mode 1 = st.global,
+    // 2 = multimem.st (NVLS multicast address), 0 = off
+    void* mc;
+    int64_t mc_ld;
+    int32_t mc_mode;
 };
 constexpr int kTraceCtas = 160;          // >= #SMs: the whole persistent grid
 constexpr int kTraceK = 96;

@@ -127,6 +127,12 @@ class SymmetricOutput:
         self.tensor = symm.empty(*shape, dtype=dtype, device=device)
         self.handle = symm.rendezvous(self.tensor, group)
         self.dests = rotated_destinations(list(self.handle.buffer_ptrs), dist.get_rank(group))
+        # NVLS multicast address of the same buffer on every rank (0 when the allocator could not
+        # set one up): with it the epilogue stores each tile once and the switch replicates it
+        try:
+            self.multicast_ptr = int(self.handle.multicast_ptr)
+        except Exception:  # noqa: BLE001 -- older allocators have no multicast
+            self.multicast_ptr = 0
 
     def barrier(self):
         self.handle.barrier(channel=0)
