@@ -106,8 +106,15 @@ typedef enum { XTC_ORDER_MN = 0, XTC_ORDER_NM = 1 } xtc_order;
  *            cluster (split_k <= 16); after all partials are written each CTA sums 1/split_k of
  *            the tile's rows in ascending segment order inside the same kernel -- bit-identical
  *            to ORDERED, one launch, no second pass over the workspace.  Needs cluster_m 1,
- *            cluster_n 0/1, tile_m 128 (matmul), b_resident 0 (and buffer_c 0 for pack_halo). */
-typedef enum { XTC_SPLITK_ORDERED = 0, XTC_SPLITK_ATOMIC = 1, XTC_SPLITK_CLUSTER = 2 } xtc_splitk_mode;
+ *            cluster_n 0/1, tile_m 128 (matmul), b_resident 0 (and buffer_c 0 for pack_halo).
+ *   STREAM   tcgen05, persistent 1, split_k 0/1 ("stream-K"): the persistent grid of G CTAs splits
+ *            the flattened (output tile, k-block) loop into G equal contiguous ranges, so the split
+ *            points fall inside tiles wherever the tile count is not a multiple of G; a CTA whose
+ *            range ends inside a tile adds, in ascending k order, the fp32 partials that the CTAs
+ *            holding the rest of that tile wrote to the workspace (one launch, cooperative: all CTAs
+ *            resident).  Matmul: cluster_m 1, tile_m 128, cluster_n 0/1; pack_halo: cluster_m 1. */
+typedef enum { XTC_SPLITK_ORDERED = 0, XTC_SPLITK_ATOMIC = 1, XTC_SPLITK_CLUSTER = 2,
+               XTC_SPLITK_STREAM = 3 } xtc_splitk_mode;
 
 /* A schedule: Table I primitives as GPU loop-nest knobs.  The
  * mapping, value ranges and legality rules are in DESIGN.md §4 (SURVEY.md

@@ -27,7 +27,7 @@ XTC_OP_MATMUL, XTC_OP_CONV2D = 0, 1
 XTC_F32, XTC_BF16, XTC_TF32 = 0, 1, 2
 XTC_ENGINE_SIMT, XTC_ENGINE_TCGEN05 = 0, 1
 XTC_ORDER_MN, XTC_ORDER_NM = 0, 1
-XTC_SPLITK_ORDERED, XTC_SPLITK_ATOMIC, XTC_SPLITK_CLUSTER = 0, 1, 2
+XTC_SPLITK_ORDERED, XTC_SPLITK_ATOMIC, XTC_SPLITK_CLUSTER, XTC_SPLITK_STREAM = 0, 1, 2, 3
 XTC_CONSUMER_NONE, XTC_CONSUMER_RELU, XTC_CONSUMER_BIAS, XTC_CONSUMER_ACCUMULATE = 0, 1, 2, 4
 DTYPES = {"f32": XTC_F32, "bf16": XTC_BF16, "tf32": XTC_TF32}
 CONSUMERS = {None: XTC_CONSUMER_NONE, "none": XTC_CONSUMER_NONE, "relu": XTC_CONSUMER_RELU,

@@ -195,6 +195,8 @@ struct xtc_op_s {
     // bound to (dests, row count); re-encoded and re-uploaded only when these change
     alignas(64) CUtensorMap gmaps[8];
     void* gmaps_dev = nullptr;
+    uint32_t* sk_flags = nullptr;   // stream-K publish flags (kSkMaxCtas x 4) and the launch epoch
+    uint32_t sk_epoch = 0;
     const void* gbound[8] = {nullptr};
     int32_t n_gbound = 0;
     int64_t g_rows = 0;
@@ -219,6 +221,7 @@ static void release_op(xtc_op op) {
     if (op->c_old) cudaFree(op->c_old);
     if (op->trace_dev) cudaFree(op->trace_dev);
     if (op->gmaps_dev) cudaFree(op->gmaps_dev);
+    if (op->sk_flags) cudaFree(op->sk_flags);
     for (auto e : op->evs) cudaEventDestroy(e);
     cudaSetDevice(cur);
     delete op;
@@ -664,6 +667,20 @@ static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cud
         tp.cg = conv_geom(d);
         tp.cn = p.cluster_n > 1 ? p.cluster_n : 1;
         tp.ksc = split_cluster ? p.split_k : 1;
+        if (p.stream_k) {
+            if (!op->sk_flags) {            // per-CTA publish flags, zeroed once; epochs only grow
+                CU_TRY(cudaMalloc(&op->sk_flags, kSkMaxCtas * 4 * sizeof(uint32_t)), "stream-K flags alloc");
+                CU_TRY(cudaMemset(op->sk_flags, 0, kSkMaxCtas * 4 * sizeof(uint32_t)), "stream-K flags clear");
+                CU_TRY(cudaDeviceSynchronize(), "stream-K flags clear");
+            }
+            if (p.grid_x > kSkMaxCtas) return fail(XTC_E_UNSUPPORTED, "stream-K grid exceeds the flag array");
+            if (++op->sk_epoch == 0) ++op->sk_epoch;
+            tp.sk = 1;
+            tp.sk_iters = p.sk_iters;
+            tp.sk_slot = p.sk_slot;
+            tp.sk_flags = op->sk_flags;
+            tp.sk_epoch = op->sk_epoch;
+        }
         tp.cons_red = split_cluster ? p.cons_reduce : 0;
         if (ga) {
             tp.gather = ga->maps;

@@ -25,6 +25,7 @@
 #include "consumer.cuh"
 #include "ptx.cuh"
 #include "splitk_cluster.cuh"
+#include "stream_k.cuh"
 #include "xtc_internal.h"
 
 namespace xtc {
@@ -138,6 +139,31 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
         p0 = (mb - nimg * p.tpi) * p.rt * MSUB;
         n0 = nb * p.tile_n;
     };
+    // the tiles this CTA visits and the k-block range of each: data-parallel (strided over the tile
+    // map; K segment from the split or the cluster rank), or stream-K (stream_k.cuh)
+    const bool sk = p.sk != 0;
+    int64_t sk_s = 0, sk_e = 0;
+    if (sk) sk_range(p.sk_iters, num_clusters, cluster_id, sk_s, sk_e);
+    const int64_t n_walk = sk ? (sk_e > sk_s ? (sk_e - 1) / p.kb_total - sk_s / p.kb_total + 1 : 0)
+                              : (p.num_tiles > cluster_id ? (p.num_tiles - cluster_id + num_clusters - 1) / num_clusters
+                                                          : 0);
+    auto walk_at = [&](int64_t i, int& kb0, int& kb1) -> int64_t {
+        int64_t t;
+        if (sk) {
+            t = sk_s / p.kb_total + i;
+            const int64_t base = t * p.kb_total;
+            kb0 = (int)(sk_s > base ? sk_s - base : 0);
+            kb1 = (int)(sk_e - base < p.kb_total ? sk_e - base : p.kb_total);
+        } else {
+            t = cluster_id + i * num_clusters;
+            int mb, nb, ks;
+            tile_coords(p.tm, t, mb, nb, ks);
+            if (kclu) ks = (int)krank;
+            kb0 = ks * p.kb_per_split;
+            kb1 = min(p.kb_total, kb0 + p.kb_per_split);
+        }
+        return t;
+    };
     auto load_b = [&](uint8_t* dst, uint64_t* bar, int kb, int n0) {
         if (p.b3d) {
             ptx::tma_load_3d(&tmB, dst, bar, 0, kb * p.tile_k, n0 / ATOM);
@@ -162,7 +188,9 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
         int pb = 0;
         uint32_t use_par = 0;
         bool first_round = true;
-        for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters) {
+        for (int64_t it = 0; it < n_walk; ++it) {
+            int kb0_, kb1_;
+            const int64_t t = walk_at(it, kb0_, kb1_);
             int nimg, p0, n0;
             int ks;
             decode(t, nimg, p0, n0, ks);
@@ -218,11 +246,12 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
             int s = 0;
             uint32_t use_par = 0;
             bool first_round = true;
-            for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters) {
+            for (int64_t it = 0; it < n_walk; ++it) {
+                int kb0, kb1;
+                const int64_t t = walk_at(it, kb0, kb1);
                 int nimg, p0, n0;
                 int ks;
                 decode(t, nimg, p0, n0, ks);
-                const int kb0 = ks * p.kb_per_split, kb1 = min(p.kb_total, kb0 + p.kb_per_split);
                 for (int kb = kb0; kb < kb1; ++kb) {
                     const int cs = s;
                     const uint32_t cpar = use_par;
@@ -284,20 +313,15 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
         const int nbuf = p.nbuf, accb = p.acc_buffers;
         if (b_res && !(PAIR && rank != 0))            // the resident filter (per-k-block barriers)
             for (int kb = 0; kb < p.kb_total; ++kb) ptx::mbar_wait(&bfull[kb], 0);
-        for (int64_t t = cluster_id; t < ((PAIR && rank != 0) ? 0 : p.num_tiles); t += num_clusters) {
+        for (int64_t it = 0; it < ((PAIR && rank != 0) ? 0 : n_walk); ++it) {
             if (wait_tempty) ptx::mbar_wait(&tempty[acc], aph ^ 1u);
             ptx::mbar_wait(&pfull[pb], pph);
             if (trace && lane == 0 && tj < kTraceK) trace[8 + kTraceK + tj] = ptx::globaltimer();
             ++tj;
             ptx::tc_fence_after();
-            int kb0, kb1;                             // this tile's K segment (split_k)
-            {
-                int mb_, nb_, ks_;
-                tile_coords(p.tm, t, mb_, nb_, ks_);
-                if (kclu) ks_ = (int)krank;
-                kb0 = ks_ * p.kb_per_split;
-                kb1 = min(kb_total, kb0 + p.kb_per_split);
-            }
+            int kb0, kb1;                             // this tile's k-block range (split_k / stream-K)
+            walk_at(it, kb0, kb1);
+            kb1 = min(kb1, kb_total);                 // (kb_total 0: diagnostics without MMAs)
             if (ptx::elect_one()) {
                 const uint32_t d0 = tmem_base + (uint32_t)(acc * acc_cols);
                 const uint64_t apatch = adesc0 + (uint64_t)((uint32_t)pb * patch16);
@@ -369,7 +393,9 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
         uint8_t* stage = sC + q * (kTcEpiStageBytes * kTcEpiBuffers);
         const bool bf16_out = p.out_bf16 != 0;
         const int P = p.cg.P, Q = p.cg.Q;
-        for (int64_t t = cluster_id; t < ((p.debug_skip_mma & 64) ? 0 : p.num_tiles); t += num_clusters) {
+        for (int64_t it = 0; it < ((p.debug_skip_mma & 64) ? 0 : n_walk); ++it) {
+            int kb0, kb1;
+            const int64_t t = walk_at(it, kb0, kb1);
             int nimg, p0, n0;
             int ks;
             decode(t, nimg, p0, n0, ks);
@@ -377,6 +403,16 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
             else ptx::mbar_wait(&tfull[acc], aph);
             if (trace && warp == 4 && lane == 0 && tj < kTraceTiles) trace[8 + 2 * kTraceK + 2 * tj] = ptx::globaltimer();
             ptx::tc_fence_after();
+            // stream-K (stream_k.cuh): contribution -> this CTA's slot [128*MSUB virtual rows][tile_n];
+            // owned -> + the later k-ranges' partials (CTAs cluster_id+1 .. sk_last), ascending
+            const bool sk_contrib = sk && kb0 > 0;
+            const bool sk_own = sk && kb0 == 0 && kb1 < p.kb_total;
+            int64_t sk_last = 0;
+            if (sk_own) {
+                sk_last = sk_owner_of(p.sk_iters, num_clusters, (t + 1) * p.kb_total - 1);
+                if (lane == 0) sk_wait(p.sk_flags, cluster_id, sk_last, q, p.sk_epoch);
+                __syncwarp();
+            }
             for (int ms = 0; ms < ((p.debug_skip_mma & 8) ? 0 : MSUB); ++ms) {
                 const int v0 = ms * 128 + 32 * q;              // first virtual row of this warp
                 const int prow0 = p0 + v0 / p.wp, q0 = v0 % p.wp;
@@ -389,6 +425,27 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
                     uint32_t vals[32];
                     ptx::tmem_ld_32x32b_x32(t_row + c, vals);
                     ptx::tmem_ld_wait();
+                    if (sk_contrib) {
+                        uint4* dst = reinterpret_cast<uint4*>(p.Wk + cluster_id * p.sk_slot + (int64_t)v * p.tile_n + c);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j)
+                            dst[j] = make_uint4(vals[4 * j], vals[4 * j + 1], vals[4 * j + 2], vals[4 * j + 3]);
+                        continue;
+                    }
+                    if (sk_own) {
+                        for (int64_t g2 = cluster_id + 1; g2 <= sk_last; ++g2) {
+                            const float4* src =
+                                reinterpret_cast<const float4*>(p.Wk + g2 * p.sk_slot + (int64_t)v * p.tile_n + c);
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) {
+                                const float4 w = __ldcg(src + j);
+                                vals[4 * j] = __float_as_uint(__uint_as_float(vals[4 * j]) + w.x);
+                                vals[4 * j + 1] = __float_as_uint(__uint_as_float(vals[4 * j + 1]) + w.y);
+                                vals[4 * j + 2] = __float_as_uint(__uint_as_float(vals[4 * j + 2]) + w.z);
+                                vals[4 * j + 3] = __float_as_uint(__uint_as_float(vals[4 * j + 3]) + w.w);
+                            }
+                        }
+                    }
                     if (!any_valid || (p.debug_skip_mma & 4)) continue;   // warp-uniform
                     if (p.cons && valid) {            // fused consumer before the rounding
                         const int64_t m = ((int64_t)nimg * P + prow) * Q + qcol;
@@ -477,6 +534,10 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
                     }
                 }
             }
+            if (sk_contrib) {                          // publish this warp's rows of the partial
+                __syncwarp();
+                if (lane == 0) sk_publish(p.sk_flags, cluster_id, q, p.sk_epoch);
+            }
             ptx::tc_fence_before();
             __syncwarp();
             if (trace && warp == 4 && lane == 0 && tj < kTraceTiles) trace[8 + 2 * kTraceK + 2 * tj + 1] = ptx::globaltimer();
@@ -515,7 +576,7 @@ static cudaError_t launch_halo_t(const CUtensorMap& x, const CUtensorMap& b, con
     cudaError_t e = ensure_smem_attr(k, smem);
     if (e != cudaSuccess) return e;
     const int ksc = (CL == 1 && p.ksc > 1) ? p.ksc : 1;
-    if (CL == 1 && ksc == 1) {
+    if (CL == 1 && ksc == 1 && !p.sk) {
         k<<<grid, kTcThreads, smem, st>>>(x, b, y, p);
     } else {
         if (ksc > 8) {
@@ -528,10 +589,15 @@ static cudaError_t launch_halo_t(const CUtensorMap& x, const CUtensorMap& b, con
         cfg.dynamicSmemBytes = smem;
         cfg.stream = st;
         cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = CL * ksc;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
+        if (p.sk) {                 // stream-K owners wait for later CTAs: all of them must be resident
+            attr[0].id = cudaLaunchAttributeCooperative;
+            attr[0].val.cooperative = getenv("XTC_SK_NOCOOP") ? 0 : 1;   // (diagnostics: A/B of the attribute)
+        } else {
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = CL * ksc;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+        }
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         e = cudaLaunchKernelEx(&cfg, k, x, b, y, p);

@@ -33,6 +33,7 @@
 #include "consumer.cuh"
 #include "ptx.cuh"
 #include "splitk_cluster.cuh"
+#include "stream_k.cuh"
 #include "xtc_internal.h"
 
 namespace xtc {
@@ -115,6 +116,33 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const uint32_t krank = kclu ? ptx::cluster_ctarank() : 0u;
     const int64_t cluster_id = blockIdx.x / (CG * cn * ksc);
     const int64_t num_clusters = gridDim.x / (CG * cn * ksc);
+    // The tiles this CTA (cluster) visits and the k-block range of each: data-parallel (strided
+    // over the tile map; K segment from the split or the cluster rank), or stream-K (a contiguous
+    // range of the flattened (tile, k-block) space, stream_k.cuh).  Every role walks the same list.
+    const bool sk = p.sk != 0;
+    int64_t sk_s = 0, sk_e = 0;
+    if (sk) sk_range(p.sk_iters, num_clusters, cluster_id, sk_s, sk_e);
+    const int64_t n_walk = sk ? (sk_e > sk_s ? (sk_e - 1) / p.kb_total - sk_s / p.kb_total + 1 : 0)
+                              : (p.num_tiles > cluster_id ? (p.num_tiles - cluster_id + num_clusters - 1) / num_clusters
+                                                          : 0);
+    auto tile_at = [&](int64_t i, int& mb, int& nb, int& ks, int& kb0, int& kb1) -> int64_t {
+        int64_t t;
+        if (sk) {
+            t = sk_s / p.kb_total + i;
+            const int64_t base = t * p.kb_total;
+            kb0 = (int)(sk_s > base ? sk_s - base : 0);
+            kb1 = (int)(sk_e - base < p.kb_total ? sk_e - base : p.kb_total);
+            tile_coords(p.tm, t, mb, nb, ks);
+            ks = 0;
+        } else {
+            t = cluster_id + i * num_clusters;
+            tile_coords(p.tm, t, mb, nb, ks);
+            if (kclu) ks = (int)krank;
+            kb0 = ks * p.kb_per_split;
+            kb1 = min(p.kb_total, kb0 + p.kb_per_split);
+        }
+        return t;
+    };
     const int bn_cta = p.tile_n / CG;        // B columns this CTA loads
 
     if (warp == 0 && lane == 0) {
@@ -201,12 +229,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 }
                 __syncwarp();
             }
-            for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters) {
-                int mb, nb, ks;
-                tile_coords(p.tm, t, mb, nb, ks);
-                if (kclu) ks = (int)krank;
-                const int kb0 = ks * p.kb_per_split;
-                const int kb1 = min(p.kb_total, kb0 + p.kb_per_split);
+            for (int64_t it = 0; it < n_walk; ++it) {
+                int mb, nb, ks, kb0, kb1;
+                tile_at(it, mb, nb, ks, kb0, kb1);
                 const int m0 = mb * TILE_M + 128 * MS * (int)rank;     // this CTA's 128*MS rows
                 const int n0 = (nb * cn + (int)crank) * p.tile_n + bn_cta * (int)rank;  // this CTA's B columns
                 int wq = 0, hp = 0, nimg = 0;
@@ -332,12 +357,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 dst[i] = l;
             }
         };
-        for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters) {
-            int mb, nb, ks;
-            tile_coords(p.tm, t, mb, nb, ks);
-                if (kclu) ks = (int)krank;
-            const int kb0 = ks * p.kb_per_split;
-            const int kb1 = min(p.kb_total, kb0 + p.kb_per_split);
+        for (int64_t it = 0; it < n_walk; ++it) {
+            int mb, nb, ks, kb0, kb1;
+            tile_at(it, mb, nb, ks, kb0, kb1);
             for (int kb = kb0; kb < kb1; ++kb) {
                 ptx::mbar_wait(&full[s], ph);
                 split_buf(sA + (size_t)s * p.a_stage_bytes, p.a_stage_bytes);
@@ -370,7 +392,6 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             const uint32_t a_stage16 = ptx::pin(p.a_stage_bytes >> 4), b_stage16 = ptx::pin(p.b_stage_bytes >> 4);
             const uint32_t idesc = ptx::pin(p.idesc);
             const int Sring = ptx::pin(S), accb = ptx::pin(p.acc_buffers), tile_n = ptx::pin(p.tile_n);
-            const int kb_per = ptx::pin(p.kb_per_split), kb_tot = ptx::pin(p.kb_total);
             const uint32_t b_res_u = ptx::pin((uint32_t)(b_res ? 1 : 0));
             const uint32_t lo16 = ptx::pin(p.lo_off >> 4);     // SPLIT3: hi stage -> lo stage (16-byte units)
             if (b_res) ptx::mbar_wait(bfull, 0);     // resident B has landed (in both CTAs for a pair)
@@ -383,12 +404,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 const int n_a = NA >= 0 ? NA : ptx::pin(p.tile_k / ATOM);
                 int s = 0, acc = 0, tk = 0;
                 uint32_t ph = 0, aph = 0;
-                for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters) {
-                    int mb, nb, ks;
-                    tile_coords(p.tm, t, mb, nb, ks);
-                if (kclu) ks = (int)krank;
-                    const int kb0 = ks * kb_per;
-                    const int kb1 = min(kb_tot, kb0 + kb_per);
+                for (int64_t it = 0; it < n_walk; ++it) {
+                    int mb, nb, ks, kb0, kb1;
+                    tile_at(it, mb, nb, ks, kb0, kb1);
                     ptx::mbar_wait(&tempty[acc], aph ^ 1);
                     ptx::tc_fence_after();
                     if (ptx::elect_one()) {
@@ -476,14 +494,24 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             for (int d = 0; d < p.n_gather; ++d) ptx::tmap_acquire(reinterpret_cast<const CUtensorMap*>(p.gather) + d);
         const bool to_ws = p.split_out != 0;
         const bool bf16_out = p.out_bf16 && !to_ws;
-        for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters) {
-            int mb, nb, ks;
-            tile_coords(p.tm, t, mb, nb, ks);
-                if (kclu) ks = (int)krank;
+        for (int64_t it = 0; it < n_walk; ++it) {
+            int mb, nb, ks, kb0, kb1;
+            const int64_t t = tile_at(it, mb, nb, ks, kb0, kb1);
             const int m0t = mb * TILE_M + 128 * MS * (int)rank, n0 = (nb * cn + (int)crank) * p.tile_n;
             ptx::mbar_wait(&tfull[acc], aph);
             if (trace && warp == 4 && lane == 0 && trace_k < kTraceTiles) trace[8 + 2 * kTraceK + 2 * trace_k] = ptx::globaltimer();
             ptx::tc_fence_after();
+            // stream-K: a tile this CTA's range starts inside is a contribution (its partial goes to the
+            // CTA's workspace slot); one its range ends inside is owned (the later k-ranges' partials,
+            // held by CTAs cluster_id+1 .. sk_last, are added in k order before the consumer)
+            const bool sk_contrib = sk && kb0 > 0;
+            const bool sk_own = sk && kb0 == 0 && kb1 < p.kb_total;
+            int64_t sk_last = 0;
+            if (sk_own) {
+                sk_last = sk_owner_of(p.sk_iters, num_clusters, (t + 1) * p.kb_total - 1);
+                if (lane == 0) sk_wait(p.sk_flags, cluster_id, sk_last, q, p.sk_epoch);
+                __syncwarp();
+            }
             if constexpr (MS == 2 && !CONV) {
                 if (p.ovl) {
                     // ---- overlapped epilogue: TMEM -> SMEM tile (subtile 1) + registers (subtile 0),
@@ -589,6 +617,27 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 uint32_t v[32];
                 ptx::tmem_ld_32x32b_x32(t_row + c, v);
                 ptx::tmem_ld_wait();
+                if (sk_contrib) {                  // slot [128 rows][tile_n] fp32, row = TMEM lane
+                    uint4* dst = reinterpret_cast<uint4*>(p.Wk + cluster_id * p.sk_slot +
+                                                          (int64_t)(32 * q + lane) * p.tile_n + c);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) dst[j] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                    continue;
+                }
+                if (sk_own) {                      // + the later k-ranges, ascending
+                    for (int64_t g2 = cluster_id + 1; g2 <= sk_last; ++g2) {
+                        const float4* src = reinterpret_cast<const float4*>(
+                            p.Wk + g2 * p.sk_slot + (int64_t)(32 * q + lane) * p.tile_n + c);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const float4 w = __ldcg(src + j);
+                            v[4 * j] = __float_as_uint(__uint_as_float(v[4 * j]) + w.x);
+                            v[4 * j + 1] = __float_as_uint(__uint_as_float(v[4 * j + 1]) + w.y);
+                            v[4 * j + 2] = __float_as_uint(__uint_as_float(v[4 * j + 2]) + w.z);
+                            v[4 * j + 3] = __float_as_uint(__uint_as_float(v[4 * j + 3]) + w.w);
+                        }
+                    }
+                }
                 if (p.cons && row < p.M) {         // fused consumer before the rounding
                     const int64_t cc = (int64_t)n0 + c;
                     const int nc = (int)((p.N - cc) < 32 ? (p.N - cc) : 32);
@@ -694,6 +743,10 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 }
             }
             }   // M-subtiles
+            if (sk_contrib) {                      // publish this warp's rows of the partial
+                __syncwarp();
+                if (lane == 0) sk_publish(p.sk_flags, cluster_id, q, p.sk_epoch);
+            }
             ptx::tc_fence_before();
             __syncwarp();
             if (trace && warp == 4 && lane == 0 && trace_k < kTraceTiles) trace[8 + 2 * kTraceK + 2 * trace_k++ + 1] = ptx::globaltimer();
@@ -734,7 +787,7 @@ cudaError_t launch_tc_t(const CUtensorMap& a, const CUtensorMap& b, const CUtens
     cudaError_t e = ensure_smem_attr(k, smem);
     if (e != cudaSuccess) return e;
     const int ksc = (CG == 1 && p.cn <= 1 && p.ksc > 1) ? p.ksc : 1;
-    if (CG == 1 && p.cn <= 1 && ksc == 1) {
+    if (CG == 1 && p.cn <= 1 && ksc == 1 && !p.sk) {
         k<<<grid, kTcThreads, smem, st>>>(a, b, c, p);
     } else {
         if (ksc > 8) {
@@ -747,10 +800,15 @@ cudaError_t launch_tc_t(const CUtensorMap& a, const CUtensorMap& b, const CUtens
         cfg.dynamicSmemBytes = smem;
         cfg.stream = st;
         cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = CG * (p.cn > 1 ? p.cn : 1) * ksc;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
+        if (p.sk) {                 // stream-K owners wait for later CTAs: all of them must be resident
+            attr[0].id = cudaLaunchAttributeCooperative;
+            attr[0].val.cooperative = getenv("XTC_SK_NOCOOP") ? 0 : 1;   // (diagnostics: A/B of the attribute)
+        } else {
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = CG * (p.cn > 1 ? p.cn : 1) * ksc;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+        }
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         e = cudaLaunchKernelEx(&cfg, k, a, b, c, p);

@@ -234,6 +234,14 @@ static xtc_status plan_tc_halo(const xtc_op_desc& d, const xtc_schedule& s, int 
     p.cta_group = pair ? 2 : 1;                         // UMMA M = 128 * cta_group (abi.cu idesc)
     p.block = kTcThreads;
     p.cluster = hcl;
+    if (p.stream_k) {
+        if (hcl != 1) ILLEGAL("pack_halo: stream-K needs cluster_m 1");
+        p.sk_iters = p.num_tiles * (int64_t)p.kb_total;
+        p.grid_x = (int)std::min<int64_t>(p.sk_iters, num_sms);
+        p.sk_slot = 128LL * msub * s.tile_n;
+        p.workspace_bytes = (int64_t)p.grid_x * p.sk_slot * 4;
+        return XTC_OK;
+    }
     if (p.split_cluster) {
         // the split_k segments of a tile = the CTAs of one cluster, reduced in the kernel
         if (hcl != 1) ILLEGAL("pack_halo: split_k_mode 2 needs cluster_m 1 (the cluster holds the K segments)");
@@ -383,6 +391,15 @@ static xtc_status plan_tc(const xtc_op_desc& d, const xtc_schedule& s, int num_s
         p.grid_x = s.persistent ? (int)std::min<int64_t>(ctas, cap) : (int)ctas;
         return XTC_OK;
     }
+    if (p.stream_k) {
+        if (cg != 1 || ms != 1) ILLEGAL("split: stream-K needs cluster_m 1 and tile_m 128 (one UMMA tile per CTA)");
+        if (s.cluster_n > 1) ILLEGAL("split: stream-K needs cluster_n 0/1");
+        p.sk_iters = p.num_tiles * (int64_t)p.kb_total;
+        p.grid_x = (int)std::min<int64_t>(p.sk_iters, num_sms);
+        p.sk_slot = 128LL * s.tile_n;
+        p.workspace_bytes = (int64_t)p.grid_x * p.sk_slot * 4;
+        return XTC_OK;
+    }
     // cluster_n: cn CTAs on adjacent N tiles of one M tile share every A stage by TMA multicast
     // (each loads 128/cn of its rows); a "tile" of the tile map is then a cluster tile
     const int cn = s.cluster_n == 0 ? 1 : s.cluster_n;
@@ -426,8 +443,14 @@ xtc_status make_plan(const xtc_op_desc& d, const xtc_schedule& s, int num_sms, P
     if (s.grid_sms) num_sms = std::min(num_sms, (int)s.grid_sms);
     p.split_k = s.split_k == 0 ? 1 : s.split_k;
     if (p.split_k < 1 || p.split_k > 64) ILLEGAL("split_k must be in [1,64]");
-    if (s.split_k_mode != XTC_SPLITK_ORDERED && s.split_k_mode != XTC_SPLITK_ATOMIC && s.split_k_mode != XTC_SPLITK_CLUSTER)
-        ILLEGAL("unknown split_k_mode");
+    if (s.split_k_mode < XTC_SPLITK_ORDERED || s.split_k_mode > XTC_SPLITK_STREAM) ILLEGAL("unknown split_k_mode");
+    // stream-K: the split points of the flattened (tile, k-block) loop come from the persistent grid
+    p.stream_k = s.split_k_mode == XTC_SPLITK_STREAM;
+    if (p.stream_k) {
+        if (s.engine != XTC_ENGINE_TCGEN05) ILLEGAL("split: split_k_mode 3 (stream-K) needs the tcgen05 engine");
+        if (p.split_k != 1) ILLEGAL("split: stream-K derives the split points from the grid; split_k must be 0/1");
+        if (!s.persistent) ILLEGAL("split: stream-K needs persistent 1 (a fixed grid of co-resident CTAs)");
+    }
     p.atomic = (p.split_k > 1 && s.split_k_mode == XTC_SPLITK_ATOMIC);
     // the K segments of a tile as the CTAs of one cluster, reduced inside the kernel (splitk_cluster.cuh)
     p.split_cluster = (p.split_k > 1 && s.split_k_mode == XTC_SPLITK_CLUSTER);
@@ -473,6 +496,7 @@ xtc_status make_plan(const xtc_op_desc& d, const xtc_schedule& s, int num_sms, P
         p.ws_ld = cdiv(p.N, 4) * 4;
         p.workspace_bytes = (int64_t)p.split_k * p.M * p.ws_ld * 4;
     }
+    // (stream-K: per-CTA partial slots, sized by the planner above)
     return XTC_OK;
 }
 

@@ -26,6 +26,7 @@ constexpr int kTcEpiSmem = 4 * kTcEpiStageBytes * kTcEpiBuffers;
 constexpr int kHaloMaxPatchBufs = 2;        // conv_halo: patch buffers (at most; the planner fits what SMEM allows)
 constexpr int kHaloMaxResidentKb = 32;      // conv_halo: resident-filter k-blocks (one mbarrier each)
 constexpr int kSplitClusterMaxCtas = 16;    // split_k_mode 2: K segments per cluster (> 8: non-portable size)
+constexpr int kSkMaxCtas = 4096;            // split_k_mode 3: stream-K grid limit (publish flags per op)
 
 // cudaFuncSetAttribute is a driver round trip: set the dynamic-SMEM opt-in once
 // per kernel variant and device, not on every launch (sweeps launch thousands).
@@ -115,6 +116,8 @@ struct Plan {
     bool halo_pair = false;             // inner_m 256: cta_group::2 UMMAs (M = 256) over a CTA pair
     bool ovl = false;                   // overlapped epilogue (see TcParams::ovl); 64 KB epilogue SMEM
     int32_t msub = 1;                   // tcgen05 matmul: 128-row M-subtiles per CTA (tile_m = 128*cta_group*msub)
+    bool stream_k = false;              // split_k_mode 3: stream-K over the persistent grid (stream_k.cuh)
+    int64_t sk_iters = 0, sk_slot = 0;  // num_tiles x kb_total iterations; partial slot floats per CTA
     bool split_cluster = false;         // split_k_mode 2: the split_k K segments of a tile = one cluster's CTAs,
                                         // reduced in-kernel; num_tiles then counts output tiles
     int32_t cluster_n = 1;              // tcgen05 matmul: CTAs on adjacent N tiles sharing A by multicast;
@@ -194,6 +197,13 @@ struct TcParams {
     void* mc;
     int64_t mc_ld;
     int32_t mc_mode;
+    // split_k_mode XTC_SPLITK_STREAM (stream_k.cuh): stream-K over sk_iters = num_tiles x kb_total
+    // iterations; CTA g's partial slot is Wk + g * sk_slot floats, its flags sk_flags[4g .. 4g+3]
+    // (one per epilogue warp) hold the epoch of the launch that last published it
+    int32_t sk;
+    int64_t sk_iters, sk_slot;
+    uint32_t* sk_flags;
+    uint32_t sk_epoch;
 };
 constexpr int kTraceCtas = 160;          // >= #SMs: the whole persistent grid
 constexpr int kTraceK = 96;

@@ -93,7 +93,7 @@ TC_SLOTS = {
     "order": [0, 1],
     "raster_group": [1, 2, 4, 8],
     "split_k": [1, 2, 4, 8],
-    "split_k_mode": [0, 2],       # split: reduction by a second kernel, or in-kernel across a cluster
+    "split_k_mode": [0, 2, 3],    # split: reduction by a second kernel, in-kernel across a cluster, stream-K
     "buffer_c": [0, 1],
     "acc_buffers": [1, 2],
     "persistent": [0, 1],
@@ -160,8 +160,8 @@ class GpuStrategy:
                 kw = self._kw(names, combo)
                 if not self._divisible(kw):
                     continue
-                if kw.get("split_k", 1) <= 1 and kw.get("split_k_mode", 0):
-                    continue                      # no split: the reduction mode is moot (one schedule, not two)
+                if kw.get("split_k", 1) <= 1 and kw.get("split_k_mode", 0) == 2:
+                    continue                      # no split: the cluster reduction is moot (one schedule, not two)
                 st, _, _ = xtc_schedule_check(self.desc, schedule(**kw), self.num_sms)
                 if st == XTC_OK:
                     legal.append(tuple(combo))

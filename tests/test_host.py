@@ -437,6 +437,31 @@ def test_cluster_split_plan_and_legality():
     assert st == xtc.XTC_E_ILLEGAL_SCHEDULE
 
 
+def test_stream_k_plan_and_legality():
+    """split_k_mode 3: the persistent grid splits tiles x k-blocks into equal ranges."""
+    SK = xtc.XTC_SPLITK_STREAM
+    base = dict(engine=1, tile_m=128, tile_n=128, tile_k=64, stages=4, buffer_c=1, acc_buffers=2, persistent=1,
+                split_k_mode=SK)
+    d = xtc.matmul_desc(1280, 960, 576)                  # 10 x 8 = 80 tiles x 9 k-blocks = 720 iterations
+    st, info, why = xtc.xtc_schedule_check(d, xtc.schedule(**base), 148)
+    assert st == 0 and info.grid_x == 148 and info.num_tiles == 80, why
+    assert info.workspace_bytes == 148 * 128 * 128 * 4      # one fp32 partial slot per CTA
+    st, info, why = xtc.xtc_schedule_check(xtc.matmul_desc(256, 128, 256), xtc.schedule(**base), 148)
+    assert st == 0 and info.grid_x == 8, why                 # 2 tiles x 4 k-blocks: one iteration per CTA
+    for bad, frag in ((dict(persistent=0), "persistent"), (dict(split_k=2), "split_k"),
+                      (dict(tile_m=256, cluster_m=2), "cluster_m"), (dict(tile_m=256), "tile_m"),
+                      (dict(cluster_n=2), "cluster_n")):
+        st, _, why = xtc.xtc_schedule_check(d, xtc.schedule(**dict(base, **bad)), 148)
+        assert st == xtc.XTC_E_ILLEGAL_SCHEDULE and frag in why, (bad, why)
+    # the haloed-patch conv (L56 at batch 2: 56 tiles x 9 k-blocks over 148 CTAs)
+    dc = xtc.conv2d_desc(2, 56, 56, 64, 64, 3, 3, 1, 1)
+    halo = dict(base, pack_halo=1, tile_n=64, stages=2)
+    st, info, why = xtc.xtc_schedule_check(dc, xtc.schedule(**halo), 148)
+    assert st == 0 and info.grid_x == 148 and info.num_tiles == 56, why
+    st, _, why = xtc.xtc_schedule_check(dc, xtc.schedule(**dict(halo, cluster_m=2)), 148)
+    assert st == xtc.XTC_E_ILLEGAL_SCHEDULE
+
+
 # --------------------------------------------- N3: descript + primitive log --
 def _fig4(desc):
     """PAPER.md Fig.4, call for call."""

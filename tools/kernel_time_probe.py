@@ -32,6 +32,9 @@ CASES = [
     ("L14n32", (32, 14, 256), dict(HALO, tile_n=128, tile_k=128, stages=3, buffer_c=1)),
     ("L56n1", (1, 56, 64), dict(HALO, tile_n=64, tile_k=64, stages=2, buffer_c=1, b_resident=1)),
     ("L56n32", (32, 56, 64), dict(HALO, tile_n=64, tile_k=64, stages=2, buffer_c=1, b_resident=1)),
+    ("L56n32", (32, 56, 64), dict(HALO, tile_n=64, tile_k=64, stages=2, buffer_c=1, b_resident=1, split_k_mode=3)),
+    ("mm1024", (1024, 1024, 1024), dict(TC, tile_n=64, tile_k=128, stages=4, buffer_c=1, acc_buffers=2,
+                                        persistent=1, split_k_mode=3)),
 ]
 
 

@@ -28,12 +28,25 @@ def mm_cands(n):
                 if (n // 128) * (n // tn) * sk > 148 * 2:
                     continue
                 out.append(dict(TC, tile_n=tn, tile_k=tk, stages=4 if tk == 64 else 3, split_k=sk))
+        for tk in (64, 128):
+            out.append(dict(TC, tile_n=tn, tile_k=tk, stages=4, buffer_c=1, acc_buffers=2, persistent=1,
+                            split_k_mode=xtc.XTC_SPLITK_STREAM))
     return out
+
+
+SKM = xtc.XTC_SPLITK_STREAM
 
 
 def conv_cands(name, nb):
     halo = dict(TC, pack_halo=1, acc_buffers=2)
     out = []
+    # stream-K over the persistent grid: the same schedules as the data-parallel best, split points from the grid
+    if name == "L56":
+        out += [dict(halo, tile_n=64, tile_k=64, stages=2, buffer_c=1, b_resident=1, persistent=1, split_k_mode=SKM),
+                dict(halo, tile_n=64, tile_k=64, stages=2, buffer_c=1, persistent=1, split_k_mode=SKM)]
+    else:
+        out += [dict(halo, tile_n=128, tile_k=128, stages=3, buffer_c=1, persistent=1, split_k_mode=SKM),
+                dict(halo, tile_n=64, tile_k=128, stages=3, buffer_c=1, persistent=1, split_k_mode=SKM)]
     if name == "L14":
         for tn in (64, 128):
             for sk in (2, 3, 6, 9, 18):
