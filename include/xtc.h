@@ -97,7 +97,13 @@ typedef struct {
     int64_t stride_h, stride_w, pad_h, pad_w;               /* conv2d */
 } xtc_op_desc;
 
-typedef enum { XTC_ENGINE_SIMT = 0, XTC_ENGINE_TCGEN05 = 1 } xtc_engine;
+/* Engines (the instruction tier a schedule runs on):
+ *   SIMT     fp32 FFMA register tiles (fp32 inputs)
+ *   TCGEN05  tcgen05.mma, TMA-fed SMEM rings, TMEM accumulators (bf16 / tf32 / fp32 via 3xTF32)
+ *   MMA      warp-level tensor-core tiles (mma.sync m16n8k16 bf16 -> fp32) fed by an im2col
+ *            gather: conv2d / matmul whose operands TMA cannot address, e.g. the C = 3 stem conv
+ *            (P:1084).  tile_m 64|128, tile_n 16|32|64, tile_k 16|32|64, split_k 1, buffer_c 0. */
+typedef enum { XTC_ENGINE_SIMT = 0, XTC_ENGINE_TCGEN05 = 1, XTC_ENGINE_MMA = 2 } xtc_engine;
 typedef enum { XTC_ORDER_MN = 0, XTC_ORDER_NM = 1 } xtc_order;
 /* Reduction of the split K segments:
  *   ORDERED  fp32 partials in a workspace, summed in ascending segment order by a second kernel

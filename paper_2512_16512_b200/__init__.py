@@ -25,7 +25,7 @@ STATUS_NAMES = {0: "XTC_OK", 1: "XTC_E_INVALID_ARG", 2: "XTC_E_UNSUPPORTED", 3: 
                 4: "XTC_E_NO_SCHEDULE", 5: "XTC_E_CUDA", 6: "XTC_E_VALIDATION_FAILED", 7: "XTC_E_OOM"}
 XTC_OP_MATMUL, XTC_OP_CONV2D = 0, 1
 XTC_F32, XTC_BF16, XTC_TF32 = 0, 1, 2
-XTC_ENGINE_SIMT, XTC_ENGINE_TCGEN05 = 0, 1
+XTC_ENGINE_SIMT, XTC_ENGINE_TCGEN05, XTC_ENGINE_MMA = 0, 1, 2
 XTC_ORDER_MN, XTC_ORDER_NM = 0, 1
 XTC_SPLITK_ORDERED, XTC_SPLITK_ATOMIC, XTC_SPLITK_CLUSTER, XTC_SPLITK_STREAM = 0, 1, 2, 3
 XTC_CONSUMER_NONE, XTC_CONSUMER_RELU, XTC_CONSUMER_BIAS, XTC_CONSUMER_ACCUMULATE = 0, 1, 2, 4

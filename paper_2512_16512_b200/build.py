@@ -15,7 +15,7 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "--expt-re
          "-I" + os.path.join(HERE, "..", "include")]
 SOURCES = ["planner.cpp", "counters.cpp", "abi.cu", "harness.cu", "gemm_simt.cu", "gemm_simt_tm1.cu", "gemm_simt_tm2.cu",
            "gemm_simt_tm4.cu", "gemm_simt_tm8.cu", "gemm_tc.cu", "gemm_tc_mm_bf16.cu", "gemm_tc_conv_bf16.cu", "gemm_tc_mm_tf32.cu", "gemm_tc_conv_tf32.cu", "gemm_tc_split3.cu", "gemm_tc_ms2.cu",
-           "conv_halo.cu"]
+           "conv_halo.cu", "conv_mma.cu"]
 
 
 def _compile(src: str, verbose: bool) -> str:

@@ -19,6 +19,8 @@ cudaError_t launch_tc_gemm(bool tf32, bool conv, int cta_group, const CUtensorMa
                            const TcParams& p, int grid, int smem, cudaStream_t st);
 cudaError_t launch_tc_conv_halo(bool tf32, const CUtensorMap& x, const CUtensorMap& b, const CUtensorMap& y,
                                 const TcParams& p, int grid, int smem, cudaStream_t st);
+cudaError_t launch_conv_mma(const void* A, const void* B, void* C, const Plan& pl, const xtc_op_desc& d,
+                            const float* bias, int cons, cudaStream_t st);
 cudaError_t launch_simt_gemm(int tm, int tn, int u, int vec, const SimtParams& p, int grid, int block, int smem,
                              cudaStream_t st);
 cudaError_t launch_fill(void* dst, int64_t count, int bf16, uint64_t seed, int mode, int64_t first, cudaStream_t st);
@@ -594,7 +596,10 @@ static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cud
     // split cluster: the tile map walks output tiles, the K segment is the CTA's cluster rank
     TileMap tm{p.tiles_m, p.tiles_n / (p.cluster_n > 1 ? p.cluster_n : 1), split_cluster ? 1 : p.split_k, p.sch.order,
                p.sch.raster_group};
-    if (p.engine == XTC_ENGINE_SIMT) {
+    if (p.engine == XTC_ENGINE_MMA) {
+        CU_TRY(launch_conv_mma(A, B, C, p, d, op->bias, p.cons_epi, st), "conv_mma launch");
+        ++launches;
+    } else if (p.engine == XTC_ENGINE_SIMT) {
         SimtParams sp;
         memset(&sp, 0, sizeof sp);
         sp.A = A; sp.B = B; sp.C = C; sp.Wk = op->ws;

@@ -410,8 +410,10 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
             int64_t sk_last = 0;
             if (sk_own) {
                 sk_last = sk_owner_of(p.sk_iters, num_clusters, (t + 1) * p.kb_total - 1);
+                if (trace && warp == 4 && lane == 0) trace[3] = ptx::globaltimer();   // XTC_TRACE: owner waits
                 if (lane == 0) sk_wait(p.sk_flags, cluster_id, sk_last, q, p.sk_epoch);
                 __syncwarp();
+                if (trace && warp == 4 && lane == 0) trace[4] = ptx::globaltimer();
             }
             for (int ms = 0; ms < ((p.debug_skip_mma & 8) ? 0 : MSUB); ++ms) {
                 const int v0 = ms * 128 + 32 * q;              // first virtual row of this warp
@@ -537,6 +539,7 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
             if (sk_contrib) {                          // publish this warp's rows of the partial
                 __syncwarp();
                 if (lane == 0) sk_publish(p.sk_flags, cluster_id, q, p.sk_epoch);
+                if (trace && warp == 4 && lane == 0) trace[5] = ptx::globaltimer();   // XTC_TRACE: published
             }
             ptx::tc_fence_before();
             __syncwarp();

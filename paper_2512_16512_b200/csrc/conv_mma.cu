@@ -1,0 +1,188 @@
+// conv_mma.cu -- KB3s: implicit-GEMM conv2d (and matmul) for operands TMA and tcgen05 cannot
+// address: a channel count that is not a multiple of the 128-byte swizzle atom, e.g. the
+// paper's stem conv [112,112,16] x [7,7,3] step 2 (DESIGN reading 4: C = 3, a 6-byte
+// pixel).  Engine XTC_ENGINE_MMA: warp-level tensor-core tiles (mma.sync.m16n8k16 bf16 ->
+// fp32), the instruction tier that needs no TMA-addressable layout.
+//
+// The contraction is the paper's Fig.2 loop nest over the implicit-GEMM view M = N*P*Q,
+// N = F, K = R*S*C (c fastest), with
+//   strip_mine -> CTA tile tile_m x tile_n x tile_k (k padded to the 16-deep MMA step; the
+//                 pad reads zeros), warp tile 16 x tile_n (tile_m / 16 warps)
+//   pack       -> A gathered through the im2col index map (zero padding = the bounds test,
+//                 reading 3) and B transposed, both into SMEM, once per k-chunk
+//   bufferize  -> fp32 accumulators in registers; the consumer and the single rounding in
+//                 the epilogue (fuse)
+//   parallelize-> one CTA per tile or a persistent grid
+// For the stem, K = 147 -> 160 and N = 16: a 128 x 16 x 160 tile is 0.66 MFLOP, too small for
+// tcgen05 (a 128 x 16 UMMA is issue- and SMEM-port-bound), and the op is bound by its gather.
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include <string.h>
+#include "consumer.cuh"
+#include "xtc_internal.h"
+
+namespace xtc {
+
+struct MmaParams {
+    const uint16_t* A;           // conv: x NHWC; matmul: A [M][lda]
+    const uint16_t* B;           // conv: w RSCF = [K][F]; matmul: B [K][ldb]
+    void* C;                     // [M][ldc]
+    int64_t M, N, K, lda, ldb, ldc;
+    int32_t tile_m, tile_n, tile_k;
+    TileMap tm;
+    int64_t num_tiles;
+    int32_t out_bf16, cons;
+    const float* bias;
+    ConvGeom cg;
+};
+
+__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
+// NT = tile_n / 8 n8-blocks per warp; BK = k-chunk (multiple of 16)
+template <int NT, int BK>
+__global__ void __launch_bounds__(256) conv_mma_kernel(const MmaParams p) {
+    constexpr int LDS = BK + 8;                     // bf16 row pitch in SMEM (breaks bank aliasing)
+    __shared__ __align__(16) uint16_t As[128 * LDS];
+    __shared__ __align__(16) uint16_t Bs[NT * 8 * LDS];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int BM = p.tile_m;                        // 64 or 128: BM / 16 warps compute
+    const bool is_conv = p.cg.is_conv != 0;
+    const int C = p.cg.C, S = p.cg.S;
+    for (int64_t t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        int mb, nb, ks;
+        tile_coords(p.tm, t, mb, nb, ks);
+        const int64_t m0 = (int64_t)mb * BM, n0 = (int64_t)nb * (NT * 8);
+        // each thread gathers for one A row (tid % BM) a strided set of k (tid / BM + j * (256 / BM))
+        const int arow = tid % BM, akoff = tid / BM, astep = 256 / BM;
+        const int64_t m = m0 + arow;
+        int img = 0, h0 = 0, w0 = 0;
+        if (is_conv && m < p.M) {
+            const int pq = p.cg.P * p.cg.Q;
+            img = (int)(m / pq);
+            const int rem = (int)(m - (int64_t)img * pq);
+            const int pp = rem / p.cg.Q, qq = rem - pp * p.cg.Q;
+            h0 = pp * p.cg.sh - p.cg.ph;
+            w0 = qq * p.cg.sw - p.cg.pw;
+        }
+        float acc[NT][4];
+#pragma unroll
+        for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+        for (int64_t k0 = 0; k0 < p.K; k0 += BK) {
+            __syncthreads();                            // the previous chunk's fragments are read
+            // ---- pack A: im2col gather (zero outside the image, past K and past M) ----
+            for (int kk = akoff; kk < BK; kk += astep) {
+                const int64_t k = k0 + kk;
+                uint16_t v = 0;
+                if (m < p.M && k < p.K) {
+                    if (is_conv) {
+                        const int rs = (int)(k / C), c = (int)(k - (int64_t)rs * C);
+                        const int r = rs / S, s = rs - r * S;
+                        const int h = h0 + r, w = w0 + s;
+                        if (h >= 0 && h < p.cg.H && w >= 0 && w < p.cg.W)
+                            v = __ldg(p.A + (((int64_t)img * p.cg.H + h) * p.cg.W + w) * C + c);
+                    } else {
+                        v = __ldg(p.A + m * p.lda + k);
+                    }
+                }
+                As[arow * LDS + kk] = v;
+            }
+            // ---- pack B transposed: Bs[n][k] (k contiguous per column: the mma's col-major B) ----
+            for (int i = tid; i < NT * 8 * BK; i += 256) {
+                const int nn = i / BK, kk = i - nn * BK;
+                const int64_t k = k0 + kk, n = n0 + nn;
+                Bs[nn * LDS + kk] = (k < p.K && n < p.N) ? __ldg(p.B + k * p.ldb + n) : (uint16_t)0;
+            }
+            __syncthreads();
+            if (warp * 16 < BM) {
+#pragma unroll
+                for (int kk = 0; kk < BK; kk += 16) {
+                    // fragments of m16n8k16 (row.col): a0/a1 rows g / g+8 at k 2t.., a2/a3 at k 2t+8..
+                    const int g = lane >> 2, tq = lane & 3;
+                    const uint16_t* ar = As + (warp * 16 + g) * LDS + kk + 2 * tq;
+                    uint32_t a[4];
+                    a[0] = *reinterpret_cast<const uint32_t*>(ar);
+                    a[1] = *reinterpret_cast<const uint32_t*>(ar + 8 * LDS);
+                    a[2] = *reinterpret_cast<const uint32_t*>(ar + 8);
+                    a[3] = *reinterpret_cast<const uint32_t*>(ar + 8 * LDS + 8);
+#pragma unroll
+                    for (int j = 0; j < NT; ++j) {
+                        const uint16_t* br = Bs + (j * 8 + g) * LDS + kk + 2 * tq;
+                        uint32_t b[2];
+                        b[0] = *reinterpret_cast<const uint32_t*>(br);
+                        b[1] = *reinterpret_cast<const uint32_t*>(br + 8);
+                        mma_bf16_16816(acc[j], a, b);
+                    }
+                }
+            }
+        }
+        // ---- epilogue: d0,d1 at (row g, cols 2t, 2t+1), d2,d3 at row g + 8 ----
+        if (warp * 16 < BM) {
+            const int g = lane >> 2, tq = lane & 3;
+#pragma unroll
+            for (int j = 0; j < NT; ++j)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int64_t row = m0 + warp * 16 + g + (e >> 1) * 8;
+                    const int64_t col = n0 + j * 8 + 2 * tq + (e & 1);
+                    if (row >= p.M || col >= p.N) continue;
+                    const int64_t off = row * p.ldc + col;
+                    float v = acc[j][e];
+                    if (p.cons) v = consume1(v, p.cons, p.bias, p.C, p.out_bf16 != 0, off, col);
+                    if (p.out_bf16) reinterpret_cast<__nv_bfloat16*>(p.C)[off] = __float2bfloat16_rn(v);
+                    else reinterpret_cast<float*>(p.C)[off] = v;
+                }
+        }
+    }
+}
+
+template <int NT>
+static cudaError_t launch_mma_nt(int tile_k, const MmaParams& p, int grid, cudaStream_t st) {
+    switch (tile_k) {
+        case 16: conv_mma_kernel<NT, 16><<<grid, 256, 0, st>>>(p); break;
+        case 64: conv_mma_kernel<NT, 64><<<grid, 256, 0, st>>>(p); break;
+        default: conv_mma_kernel<NT, 32><<<grid, 256, 0, st>>>(p); break;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_conv_mma(const void* A, const void* B, void* C, const Plan& pl, const xtc_op_desc& d,
+                            const float* bias, int cons, cudaStream_t st) {
+    MmaParams p;
+    memset(&p, 0, sizeof p);
+    p.A = static_cast<const uint16_t*>(A);
+    p.B = static_cast<const uint16_t*>(B);
+    p.C = C;
+    p.M = pl.M; p.N = pl.N; p.K = pl.K;
+    const bool conv = d.kind == XTC_OP_CONV2D;
+    p.lda = conv ? 0 : (d.lda ? d.lda : d.k);
+    p.ldb = conv ? d.f : (d.ldb ? d.ldb : d.n);
+    p.ldc = conv ? d.f : (d.ldc ? d.ldc : d.n);
+    p.tile_m = pl.sch.tile_m; p.tile_n = pl.sch.tile_n; p.tile_k = pl.sch.tile_k;
+    p.tm = TileMap{pl.tiles_m, pl.tiles_n, 1, pl.sch.order, pl.sch.raster_group};
+    p.num_tiles = pl.num_tiles;
+    p.out_bf16 = d.out_dtype == XTC_BF16;
+    p.cons = cons;
+    p.bias = bias;
+    if (conv) {
+        int64_t M_, N_, K_, P, Q;
+        gemm_view(d, M_, N_, K_, P, Q);
+        p.cg.is_conv = 1;
+        p.cg.H = (int)d.h; p.cg.W = (int)d.w; p.cg.C = (int)d.c; p.cg.P = (int)P; p.cg.Q = (int)Q;
+        p.cg.R = (int)d.r; p.cg.S = (int)d.s; p.cg.sh = (int)d.stride_h; p.cg.sw = (int)d.stride_w;
+        p.cg.ph = (int)d.pad_h; p.cg.pw = (int)d.pad_w;
+    }
+    switch (pl.sch.tile_n) {
+        case 16: return launch_mma_nt<2>(p.tile_k, p, pl.grid_x, st);
+        case 32: return launch_mma_nt<4>(p.tile_k, p, pl.grid_x, st);
+        default: return launch_mma_nt<8>(p.tile_k, p, pl.grid_x, st);
+    }
+}
+
+}  // namespace xtc

@@ -509,8 +509,10 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             int64_t sk_last = 0;
             if (sk_own) {
                 sk_last = sk_owner_of(p.sk_iters, num_clusters, (t + 1) * p.kb_total - 1);
+                if (trace && warp == 4 && lane == 0) trace[3] = ptx::globaltimer();   // XTC_TRACE: owner waits
                 if (lane == 0) sk_wait(p.sk_flags, cluster_id, sk_last, q, p.sk_epoch);
                 __syncwarp();
+                if (trace && warp == 4 && lane == 0) trace[4] = ptx::globaltimer();
             }
             if constexpr (MS == 2 && !CONV) {
                 if (p.ovl) {
@@ -746,6 +748,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             if (sk_contrib) {                      // publish this warp's rows of the partial
                 __syncwarp();
                 if (lane == 0) sk_publish(p.sk_flags, cluster_id, q, p.sk_epoch);
+                if (trace && warp == 4 && lane == 0) trace[5] = ptx::globaltimer();   // XTC_TRACE: published
             }
             ptx::tc_fence_before();
             __syncwarp();

@@ -259,6 +259,31 @@ static xtc_status plan_tc_halo(const xtc_op_desc& d, const xtc_schedule& s, int 
     return XTC_OK;
 }
 
+// Warp-MMA engine (conv_mma.cu): mma.sync m16n8k16 tiles over an im2col gather, any channel count
+static xtc_status plan_mma(const xtc_op_desc& d, const xtc_schedule& s, int num_sms, Plan& p, std::string& why) {
+    if (d.in_dtype != XTC_BF16) ILLEGAL("MMA engine computes bf16 inputs (mma.sync m16n8k16 bf16 -> fp32)");
+    if (s.tile_m != 64 && s.tile_m != 128) ILLEGAL("MMA engine: tile_m must be 64 or 128 (16-row warp tiles)");
+    if (s.tile_n != 16 && s.tile_n != 32 && s.tile_n != 64) ILLEGAL("MMA engine: tile_n must be 16, 32 or 64");
+    if (s.tile_k != 16 && s.tile_k != 32 && s.tile_k != 64) ILLEGAL("MMA engine: tile_k must be 16, 32 or 64");
+    if (s.inner_m || s.inner_n) ILLEGAL("MMA engine: inner_m / inner_n must be 0 (the warp tile is 16 x tile_n)");
+    if (s.unroll_k > 1 || s.vector_n > 1 || s.stages > 1 || s.swizzle) ILLEGAL("MMA engine: unroll_k, vector_n, stages, swizzle must be 0/1");
+    if (p.split_k != 1) ILLEGAL("MMA engine: split_k must be 1");
+    if (s.buffer_c || s.acc_buffers > 1) ILLEGAL("MMA engine: buffer_c 0, acc_buffers 0/1 (register accumulators)");
+    if (s.cluster_m > 1 || s.cluster_n > 1 || s.pack_warps > 1 || s.b_resident || s.pack_halo)
+        ILLEGAL("MMA engine: cluster_m, cluster_n, pack_warps, b_resident, pack_halo must be 0/1");
+    p.block = 256;
+    p.smem = 0;
+    p.tiles_m = (int)cdiv(p.M, s.tile_m);
+    p.tiles_n = (int)cdiv(p.N, s.tile_n);
+    p.kb_total = (int)cdiv(p.K, s.tile_k);
+    p.kb_per_split = p.kb_total;
+    p.k_per_split = p.K;
+    p.num_tiles = (int64_t)p.tiles_m * p.tiles_n;
+    if (p.num_tiles >= (1ll << 31)) ILLEGAL("too many tiles");
+    p.grid_x = s.persistent ? (int)std::min<int64_t>(p.num_tiles, (int64_t)num_sms * 8) : (int)p.num_tiles;
+    return XTC_OK;
+}
+
 static xtc_status plan_tc(const xtc_op_desc& d, const xtc_schedule& s, int num_sms, Plan& p, std::string& why) {
     // F32 inputs on the tensor cores: the 3xTF32 split, fp32-accurate:
     // a = hi + lo with hi = a truncated to tf32 (what kind::tf32 reads) and lo = a - hi
@@ -488,6 +513,11 @@ xtc_status make_plan(const xtc_op_desc& d, const xtc_schedule& s, int num_sms, P
     }
     if (s.engine == XTC_ENGINE_SIMT) st = plan_simt(d, s, num_sms, p, why);
     else if (s.engine == XTC_ENGINE_TCGEN05) st = plan_tc(d, s, num_sms, p, why);
+    else if (s.engine == XTC_ENGINE_MMA) {
+        if (p.has_tail) ILLEGAL("MMA engine: split_n_at must be 0");
+        if (p.atomic) ILLEGAL("MMA engine: split_k must be 1");
+        st = plan_mma(d, s, num_sms, p, why);
+    }
     else ILLEGAL("unknown engine %d", s.engine);
     if (st != XTC_OK) return st;
     if (p.grid_x < std::max(1, p.cluster))

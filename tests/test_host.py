@@ -462,6 +462,24 @@ def test_stream_k_plan_and_legality():
     assert st == xtc.XTC_E_ILLEGAL_SCHEDULE
 
 
+def test_mma_engine_plan_and_legality():
+    """Engine 2 (warp-MMA tiles over an im2col gather): the paper's C = 3 stem conv plans on it."""
+    stem = xtc.conv2d_desc(1, 224, 224, 3, 16, 7, 7, 2, 3)
+    base = dict(engine=xtc.XTC_ENGINE_MMA, tile_m=128, tile_n=16, tile_k=32)
+    st, info, why = xtc.xtc_schedule_check(stem, xtc.schedule(**base), 148)
+    assert st == 0 and info.num_tiles == 98 and info.grid_x == 98, why      # 112*112/128 tiles, F = 16
+    assert xtc.xtc_schedule_check(stem, xtc.schedule(**dict(base, persistent=1)), 148)[0] == 0
+    # the same conv cannot take the tcgen05 engine (C = 3: no 128-byte channel block for TMA)
+    tc = dict(engine=1, tile_m=128, tile_n=64, tile_k=64, stages=4, swizzle=128)
+    assert xtc.xtc_schedule_check(stem, xtc.schedule(**tc), 148)[0] == xtc.XTC_E_ILLEGAL_SCHEDULE
+    for bad, frag in ((dict(tile_m=256), "tile_m"), (dict(tile_n=48), "tile_n"), (dict(tile_k=8), "tile_k"),
+                      (dict(split_k=2), "split_k"), (dict(buffer_c=1), "buffer_c"), (dict(inner_m=4), "inner_m")):
+        st, _, why = xtc.xtc_schedule_check(stem, xtc.schedule(**dict(base, **bad)), 148)
+        assert st == xtc.XTC_E_ILLEGAL_SCHEDULE and frag in why, (bad, why)
+    f32 = xtc.conv2d_desc(1, 224, 224, 3, 16, 7, 7, 2, 3, "f32", "f32")
+    assert xtc.xtc_schedule_check(f32, xtc.schedule(**base), 148)[0] == xtc.XTC_E_ILLEGAL_SCHEDULE
+
+
 # --------------------------------------------- N3: descript + primitive log --
 def _fig4(desc):
     """PAPER.md Fig.4, call for call."""
