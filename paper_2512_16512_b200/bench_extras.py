@@ -92,6 +92,25 @@ def _best(xtc, torch, dev, desc, scheds, in_shapes, peak, fill_seed=11, flush=1)
     return out
 
 
+# The paper's stem conv (reading 4): C = 3 -> bf16 on the warp-MMA tensor-core engine, fp32 on SIMT
+STEM_MMA_SCHEDS = [dict(engine=2, tile_m=128, tile_n=16, tile_k=32, persistent=p) for p in (0, 1)] + \
+                  [dict(engine=2, tile_m=64, tile_n=16, tile_k=k) for k in (16, 32, 64)]
+STEM_SIMT_SCHEDS = [dict(engine=0, tile_m=64, tile_n=16, tile_k=8, inner_m=4, inner_n=2, unroll_k=2, stages=1),
+                    dict(engine=0, tile_m=64, tile_n=16, tile_k=21, inner_m=4, inner_n=4, stages=2, vector_n=4,
+                         swizzle=4)]
+
+
+def stem_conv(xtc, torch, dev, peak):
+    out = {}
+    for nb in (1, 32):
+        for dt, scheds in (("bf16", STEM_MMA_SCHEDS), ("f32", STEM_SIMT_SCHEDS)):
+            d = xtc.conv2d_desc(nb, 224, 224, 3, 16, 7, 7, 2, 3, dt, dt)
+            r = _best(xtc, torch, dev, d, scheds, [(nb, 224, 224, 3), (7, 7, 3, 16)], peak)
+            out[f"n{nb}_{dt}_{'mma' if dt == 'bf16' else 'simt'}"] = {
+                k: r.get(k) for k in ("tflops_med", "t_med_us", "max_norm_err", "warm_l2", "schedule", "error")}
+    return out
+
+
 CONFIG1_SCHED = dict(engine=0, tile_m=8, tile_n=8, tile_k=8, inner_m=1, inner_n=1, unroll_k=1, stages=1, order=0)
 
 
@@ -157,4 +176,5 @@ def run_extras(xtc, torch, dev, peak):
             scan[f"{name}_n{nb}"] = {k: r.get(k) for k in ("tflops_med", "t_med_us", "warm_l2", "schedule", "error")}
     out["conv_batch_scan_bf16"] = scan
     out["matmul_32_f32_config1"] = config1_latency(xtc, torch, dev)
+    out["conv_stem_7x7s2_c3"] = stem_conv(xtc, torch, dev, peak)
     return out

@@ -236,7 +236,8 @@ def test_paper_tu_matmul_512x128x1024(mode):
 @pytest.mark.parametrize("mode", [MODE_INT, MODE_UNIFORM])
 def test_paper_stem_conv_7x7_stride2(mode):
     """[112,112,16] x [7,7,3] step 2 (reading 4): 224x224x3 -> 112x112x16, pad 3.  C = 3 gives a 6-byte
-    pixel pitch (no TMA), so it runs on the SIMT engine; K = 147 is ragged for every tile_k."""
+    pixel pitch (no TMA, no tcgen05 operand): fp32 runs on the SIMT engine (here), bf16 on the warp-MMA tensor-core
+    engine (tests/test_gpu_mma_engine.py); K = 147 is ragged for every tile_k."""
     d = xtc.conv2d_desc(1, 224, 224, 3, 16, 7, 7, 2, 3, "f32", "f32")
     assert xtc.gemm_view(d) == (112 * 112, 16, 147)
     for sch in (S(engine=0, tile_m=64, tile_n=16, tile_k=8, inner_m=4, inner_n=2, unroll_k=2, stages=1),

@@ -84,7 +84,8 @@ def main():
     js = os.path.join(os.path.dirname(prefix), "ncu_summary.json")
     allj = json.load(open(js)) if os.path.exists(js) else {}
     allj[os.path.basename(prefix)] = summ
-    allj["headline_kernel"] = summ
+    if "headline" in os.path.basename(prefix):
+        allj["headline_kernel"] = summ
     json.dump(allj, open(js, "w"), indent=1)
     print("\n".join(lines))
 

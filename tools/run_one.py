@@ -12,7 +12,8 @@ if a[0] == "matmul":
     d = xtc.matmul_desc(M, N, K, ind, outd); sa, sb = (M, K), (K, N)
 else:
     B, H, W, C, F = map(int, a[1:6]); ind, outd, sch = a[6], a[7], json.loads(a[8]); reps = int(a[9]) if len(a) > 9 else 3
-    d = xtc.conv2d_desc(B, H, W, C, F, 3, 3, 1, 1, ind, outd); sa, sb = (B, H, W, C), (3, 3, C, F)
+    R, S_, sd, pd = sch.pop("_geom", (3, 3, 1, 1))     # optional filter / stride / pad in the JSON
+    d = xtc.conv2d_desc(B, H, W, C, F, R, S_, sd, pd, ind, outd); sa, sb = (B, H, W, C), (R, S_, C, F)
 Mg, Ng, Kg = xtc.gemm_view(d)
 x = torch.empty(sa, dtype=T[ind], device="cuda"); w = torch.empty(sb, dtype=T[ind], device="cuda")
 y = torch.empty((Mg, Ng), dtype=T[outd], device="cuda")

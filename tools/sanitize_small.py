@@ -34,6 +34,12 @@ CASES = {
     "conv_halo_splitk_cluster": ("conv", (2, 14, 14, 64, 64), dict(engine=1, tile_m=128, tile_n=64, tile_k=64,
                                                                    stages=3, pack_halo=1, split_k=3, split_k_mode=2,
                                                                    acc_buffers=2)),
+    "tc_stream_k": ("mm", (384, 256, 512), dict(engine=1, tile_m=128, tile_n=128, tile_k=64, stages=3, buffer_c=1,
+                                                acc_buffers=2, persistent=1, grid_sms=7, split_k_mode=3)),
+    "conv_halo_stream_k": ("conv", (2, 14, 14, 64, 64), dict(engine=1, tile_m=128, tile_n=64, tile_k=64, stages=3,
+                                                            pack_halo=1, buffer_c=1, acc_buffers=2, persistent=1,
+                                                            grid_sms=5, split_k_mode=3)),
+    "conv_mma_stem": ("stem", (1, 64, 64, 3, 16), dict(engine=2, tile_m=128, tile_n=16, tile_k=32)),
     "tc_3xtf32": ("mm32", (256, 256, 256), dict(TC, tile_m=128, tile_n=128, tile_k=32, stages=3, acc_buffers=2,
                                                 persistent=1, grid_sms=2)),
     "conv_im2col": ("conv", (2, 14, 14, 64, 64), dict(TC, tile_m=128, tile_n=64, tile_k=64, stages=3, acc_buffers=2,
@@ -48,12 +54,13 @@ CASES = {
 def run(name):
     kind, shape, sch = CASES[name]
     st = torch.cuda.current_stream().cuda_stream
-    if kind == "conv":
+    if kind in ("conv", "stem"):
         n, h, w, c, f = shape
-        d = xtc.conv2d_desc(n, h, w, c, f, 3, 3, 1, 1, "bf16", "bf16")
+        r, sd, pd = (7, 2, 3) if kind == "stem" else (3, 1, 1)
+        d = xtc.conv2d_desc(n, h, w, c, f, r, r, sd, pd, "bf16", "bf16")
         M, N, K = xtc.gemm_view(d)
         a = torch.empty((n, h, w, c), dtype=torch.bfloat16, device="cuda")
-        b = torch.empty((3, 3, c, f), dtype=torch.bfloat16, device="cuda")
+        b = torch.empty((r, r, c, f), dtype=torch.bfloat16, device="cuda")
         out = torch.bfloat16
     else:
         M, N, K = shape
