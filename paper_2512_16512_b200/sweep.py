@@ -26,6 +26,32 @@ from .strategy import GpuStrategy
 TORCH_DT = {"bf16": torch.bfloat16, "f32": torch.float32, "tf32": torch.float32}
 
 
+def sweep_key(m, n, k, candidates, seed, in_dtype, out_dtype, engine):
+    """What a resume record must match: the candidate list is a function of all of these
+    (GpuStrategy(desc, engine).sample(candidates, seed)), so a record written under another
+    shape / dtype / engine / count is a different candidate with the same id."""
+    return {"seed": int(seed), "m": int(m), "n": int(n), "k": int(k), "candidates": int(candidates),
+            "in_dtype": str(in_dtype), "out_dtype": str(out_dtype), "engine": int(engine)}
+
+
+def load_resume(path, key):
+    """Finished records of `path` written under `key`; a file holding records of another key is
+    refused (ValueError) instead of silently merged."""
+    done = {}
+    if not path or not os.path.exists(path):
+        return done
+    with open(path) as f:
+        for ln in f:
+            if not ln.strip():
+                continue
+            r = json.loads(ln)
+            rk = r.get("key")
+            if rk != key:
+                raise ValueError(f"resume file {path} holds records of sweep {rk}, not {key}")
+            done[r["id"]] = r
+    return done
+
+
 def run_sweep(m, n, k, candidates, seed=0, world=1, rank=0, device=0, warmup=2, repeats=10, validate=1,
               peak_tflops=0.0, resume_path=None, in_dtype="bf16", out_dtype="bf16", engine=XTC_ENGINE_TCGEN05):
     """engine XTC_ENGINE_SIMT sweeps the fp32 register-tiled engine (in_dtype f32)."""
@@ -33,13 +59,7 @@ def run_sweep(m, n, k, candidates, seed=0, world=1, rank=0, device=0, warmup=2, 
     strat = GpuStrategy(desc, engine)
     samples = strat.sample(candidates, seed=seed)
     mine = rank_candidates(len(samples), world, rank)
-    done = {}
-    if resume_path and os.path.exists(resume_path):
-        with open(resume_path) as f:
-            for ln in f:
-                r = json.loads(ln)
-                if r.get("seed") == seed:
-                    done[r["id"]] = r
+    done = load_resume(resume_path, sweep_key(m, n, k, candidates, seed, in_dtype, out_dtype, engine))
     todo = [i for i in mine if i not in done]
     dev = torch.device("cuda", device)
     a = torch.empty((m, k), dtype=TORCH_DT[in_dtype], device=dev)
@@ -86,6 +106,7 @@ def main():
     desc, samples, mine, todo, scheds, op, (a, b, c), cfg, st, done = run_sweep(
         args.m, args.n, args.k, args.candidates, args.seed, world, rank, local, args.warmup, args.repeats,
         resume_path=args.resume, in_dtype=in_dt, out_dtype=out_dt, engine=engine)
+    key = sweep_key(args.m, args.n, args.k, args.candidates, args.seed, in_dt, out_dt, engine)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -105,7 +126,7 @@ def main():
     if args.resume:
         with open(args.resume, "a") as f:
             for i in todo:
-                r = dict(recs[i]); r.update(id=i, seed=args.seed)
+                r = dict(recs[i]); r.update(id=i, key=key)
                 f.write(json.dumps(r) + "\n")
     if rank == 0:
         ok = [r for r in all_recs if int(r["status"]) == 0 and int(r["valid"]) == 1]

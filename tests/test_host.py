@@ -577,3 +577,21 @@ def test_scheduler_rejects_malformed_primitives():
         Scheduler(desc).descript({"I": [], "J[0:100]": {"K": []}, "J[120:258]": {"K": []}})   # gap
     with pytest.raises(ScheduleError):
         Scheduler(xtc.conv2d_desc(1, 8, 8, 64, 64))
+
+
+def test_sweep_resume_matches_the_full_key(tmp_path):
+    """A resume file is matched on everything the candidate list depends on: records of
+    another shape / dtype / engine / count under the same seed are refused, not merged."""
+    import json
+    from paper_2512_16512_b200.sweep import load_resume, sweep_key
+    k1 = sweep_key(1024, 1024, 1024, 4096, 0, "bf16", "bf16", 1)
+    k2 = sweep_key(512, 512, 512, 4096, 0, "bf16", "bf16", 1)
+    p = tmp_path / "r.jsonl"
+    assert load_resume(str(p), k1) == {}
+    p.write_text("".join(json.dumps({"id": i, "key": k1, "tflops_med": 1.0}) + "\n" for i in (3, 7)))
+    assert sorted(load_resume(str(p), k1)) == [3, 7]
+    with pytest.raises(ValueError):
+        load_resume(str(p), k2)
+    p.write_text(json.dumps({"id": 0, "seed": 0, "tflops_med": 1.0}) + "\n")   # the round-1 format
+    with pytest.raises(ValueError):
+        load_resume(str(p), k1)
