@@ -93,8 +93,10 @@ def _best(xtc, torch, dev, desc, scheds, in_shapes, peak, fill_seed=11, flush=1)
 
 
 # The paper's stem conv (reading 4): C = 3 -> bf16 on the warp-MMA tensor-core engine, fp32 on SIMT
-STEM_MMA_SCHEDS = [dict(engine=2, tile_m=128, tile_n=16, tile_k=32, persistent=p) for p in (0, 1)] + \
-                  [dict(engine=2, tile_m=64, tile_n=16, tile_k=k) for k in (16, 32, 64)]
+# pack_halo = 1: the patch-staged kernel (tile_m / Q output rows per CTA); the im2col-gather kernel stays a candidate
+STEM_MMA_SCHEDS = [dict(engine=2, tile_m=tm, tile_n=16, tile_k=16, pack_halo=1, persistent=p)
+                   for tm in (128, 256, 512) for p in (0, 1)] + \
+                  [dict(engine=2, tile_m=128, tile_n=16, tile_k=32), dict(engine=2, tile_m=64, tile_n=16, tile_k=32)]
 STEM_SIMT_SCHEDS = [dict(engine=0, tile_m=64, tile_n=16, tile_k=8, inner_m=4, inner_n=2, unroll_k=2, stages=1),
                     dict(engine=0, tile_m=64, tile_n=16, tile_k=21, inner_m=4, inner_n=4, stages=2, vector_n=4,
                          swizzle=4)]

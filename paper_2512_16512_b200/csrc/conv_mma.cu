@@ -35,6 +35,8 @@ struct MmaParams {
     int32_t out_bf16, cons;
     const float* bias;
     ConvGeom cg;
+    MmaPatch pg;                 // pack_halo: the patch-staged conv (conv_mma_patch_kernel)
+    int32_t batch;
 };
 
 __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
@@ -142,6 +144,173 @@ __global__ void __launch_bounds__(256) conv_mma_kernel(const MmaParams p) {
     }
 }
 
+
+// ---- pack at the tile level (pack_halo = 1, conv only): the patch-staged kernel ----
+// A CTA tile = pg.tp whole output rows (p0 .. p0+tp) of image `img` x tile_n filters.  Its input
+// patch -- pg.pr input rows x pg.wpatch pixel slots x CP channels (channels >= C and pixels outside
+// the image are zeros: the zero padding, reading 3) -- is staged in SMEM ONCE per tile, the filter
+// slice transposed (Bs[n][k], k = (r, s, c) with s padded to pg.sp, c to CP; padded taps carry
+// zero weights).  Every 16-deep step (r, j) of pixel i then reads A from patch row
+// (i / Q) * sh + r at slot (i % Q) * sw + j * 16 / CP: a contiguous 32-byte run, so the m16n8k16
+// A fragments are four 32-bit LDS per 16 pixels (conflict-free for stride 2, CP = 4).  Each warp
+// owns 32 pixels (two m16 blocks) and all tile_n filters; the epilogue applies the consumer,
+// rounds once, stages the warp's 32 x tile_n block in SMEM and writes it with 16-byte stores.
+template <int NT, int CP>
+__global__ void __launch_bounds__(512) conv_mma_patch_kernel(const MmaParams p) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const MmaPatch g = p.pg;
+    uint8_t* const patch = smem;
+    uint8_t* const Bs = smem + g.smem_patch;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
+    const int nthr = blockDim.x;
+    const int os = p.out_bf16 ? 2 : 4;
+    uint8_t* const Os = smem + g.smem_patch + g.smem_b + warp * 32 * (NT * 8) * os;
+    const int H = p.cg.H, W = p.cg.W, C = p.cg.C, P = p.cg.P, Q = p.cg.Q, S = p.cg.S;
+    const int tiles_p = (P + g.tp - 1) / g.tp;
+    const int row_bytes = g.wpatch * CP * 2;
+    const int slots = g.pr * g.wpatch;
+    const int spc = g.sp * CP;                       // k per filter row r
+    for (int64_t t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        int mb, nb, ks;
+        tile_coords(p.tm, t, mb, nb, ks);
+        const int img = mb / tiles_p;
+        const int p0 = (mb - img * tiles_p) * g.tp;
+        const int n0 = nb * (NT * 8);
+        __syncthreads();                             // the previous tile's patch and filter are consumed
+        // ---- pack the patch: one CP-channel pixel slot per thread-iteration ----
+        const int h_base = p0 * p.cg.sh - p.cg.ph;
+        for (int sl = tid; sl < slots; sl += nthr) {
+            const int rr = sl / g.wpatch, ww = sl - rr * g.wpatch;
+            const int h = h_base + rr, w = ww - p.cg.pw;
+            uint16_t v[CP];
+#pragma unroll
+            for (int c = 0; c < CP; ++c) v[c] = 0;
+            if (h >= 0 && h < H && w >= 0 && w < W) {
+                const uint16_t* src = p.A + (((int64_t)img * H + h) * W + w) * C;
+#pragma unroll
+                for (int c = 0; c < CP; ++c)
+                    if (c < C) v[c] = __ldg(src + c);
+            }
+            uint32_t* dst = reinterpret_cast<uint32_t*>(patch + (size_t)sl * CP * 2);
+#pragma unroll
+            for (int c = 0; c < CP; c += 2) dst[c / 2] = (uint32_t)v[c] | ((uint32_t)v[c + 1] << 16);
+        }
+        // ---- pack the filter slice transposed: Bs[n][k] ----
+        for (int i = tid; i < NT * 8 * g.kp; i += nthr) {
+            const int nn = i % (NT * 8), kk = i / (NT * 8);
+            const int r = kk / spc, rem = kk - r * spc, s = rem / CP, c = rem - s * CP;
+            const int64_t n = n0 + nn;
+            uint16_t v = 0;
+            if (s < S && c < C && n < p.N) v = __ldg(p.B + ((int64_t)(r * S + s) * C + c) * p.ldb + n);
+            reinterpret_cast<uint16_t*>(Bs)[nn * g.b_pitch + kk] = v;
+        }
+        __syncthreads();
+        // ---- contraction: 2 m16 blocks x NT n8 blocks per warp ----
+        float acc[2][NT][4];
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) acc[b][j][0] = acc[b][j][1] = acc[b][j][2] = acc[b][j][3] = 0.f;
+        const uint8_t* abase[2][2];
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+                int i = warp * 32 + b * 16 + hh * 8 + gq;
+                if (i >= g.px) i = g.px - 1;         // rows past the tile compute a copy, never stored
+                const int pp = i / Q, qq = i - pp * Q;
+                abase[b][hh] = patch + (size_t)pp * p.cg.sh * row_bytes + (size_t)qq * p.cg.sw * CP * 2 + 4 * tq;
+            }
+        const uint8_t* bbase = Bs + (gq * g.b_pitch + 2 * tq) * 2;
+        if (warp * 32 < g.px) {
+            for (int r = 0; r < p.cg.R; ++r) {
+                for (int j = 0; j < g.ksr; ++j) {
+                    const int aoff = r * row_bytes + j * 32;
+                    const int boff = (r * g.ksr + j) * 32;
+                    uint32_t bf[NT][2];
+#pragma unroll
+                    for (int nt = 0; nt < NT; ++nt) {
+                        const uint8_t* bp = bbase + nt * 8 * g.b_pitch * 2 + boff;
+                        bf[nt][0] = *reinterpret_cast<const uint32_t*>(bp);
+                        bf[nt][1] = *reinterpret_cast<const uint32_t*>(bp + 16);
+                    }
+#pragma unroll
+                    for (int b = 0; b < 2; ++b) {
+                        uint32_t a[4];
+                        a[0] = *reinterpret_cast<const uint32_t*>(abase[b][0] + aoff);
+                        a[1] = *reinterpret_cast<const uint32_t*>(abase[b][1] + aoff);
+                        a[2] = *reinterpret_cast<const uint32_t*>(abase[b][0] + aoff + 16);
+                        a[3] = *reinterpret_cast<const uint32_t*>(abase[b][1] + aoff + 16);
+#pragma unroll
+                        for (int nt = 0; nt < NT; ++nt) mma_bf16_16816(acc[b][nt], a, bf[nt]);
+                    }
+                }
+            }
+        }
+        // ---- epilogue: consumer + one rounding, staged per warp, 16-byte stores ----
+        const int rows_valid = min(g.tp, P - p0) * Q;             // pixels of this tile that exist
+        const int64_t m_tile = ((int64_t)img * P + p0) * Q;
+        const int tn = NT * 8;
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    const int il = b * 16 + hh * 8 + gq;          // row within the warp's 32
+                    const int i = warp * 32 + il;
+                    const int cl = nt * 8 + 2 * tq;
+                    float v0 = acc[b][nt][hh * 2], v1 = acc[b][nt][hh * 2 + 1];
+                    if (p.cons && i < rows_valid) {
+                        const int64_t off = (m_tile + i) * p.ldc + n0 + cl;
+                        if (n0 + cl < p.N) v0 = consume1(v0, p.cons, p.bias, p.C, p.out_bf16 != 0, off, n0 + cl);
+                        if (n0 + cl + 1 < p.N) v1 = consume1(v1, p.cons, p.bias, p.C, p.out_bf16 != 0, off + 1, n0 + cl + 1);
+                    }
+                    if (p.out_bf16) {
+                        const uint32_t w = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(v0)) |
+                                           ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(v1)) << 16);
+                        *reinterpret_cast<uint32_t*>(Os + (il * tn + cl) * 2) = w;
+                    } else {
+                        *reinterpret_cast<float2*>(Os + (il * tn + cl) * 4) = make_float2(v0, v1);
+                    }
+                }
+        __syncwarp();
+        const int wrows = max(0, min(32, rows_valid - warp * 32));
+        const int64_t m_w = m_tile + warp * 32;
+        const int row_b = tn * os;                                 // staged bytes per row
+        const bool vec = (n0 + tn <= p.N) && ((p.ldc * os) % 16 == 0) && ((n0 * os) % 16 == 0);
+        uint8_t* const Cb = static_cast<uint8_t*>(p.C);
+        if (vec) {
+            const int vpr = row_b / 16;                            // 16-byte vectors per row
+            for (int e = lane; e < wrows * vpr; e += 32) {
+                const int rr = e / vpr, vv = e - rr * vpr;
+                const uint4 w = *reinterpret_cast<const uint4*>(Os + rr * row_b + vv * 16);
+                *reinterpret_cast<uint4*>(Cb + ((m_w + rr) * p.ldc + n0) * os + vv * 16) = w;
+            }
+        } else {
+            for (int e = lane; e < wrows * tn; e += 32) {
+                const int rr = e / tn, cc = e - rr * tn;
+                if (n0 + cc >= p.N) continue;
+                uint8_t* dst = Cb + ((m_w + rr) * p.ldc + n0 + cc) * os;
+                if (os == 2) *reinterpret_cast<uint16_t*>(dst) = *reinterpret_cast<const uint16_t*>(Os + (rr * tn + cc) * 2);
+                else *reinterpret_cast<float*>(dst) = *reinterpret_cast<const float*>(Os + (rr * tn + cc) * 4);
+            }
+        }
+    }
+}
+
+template <int NT>
+static cudaError_t launch_patch_nt(const MmaParams& p, int grid, int block, int smem, cudaStream_t st) {
+    auto k4 = conv_mma_patch_kernel<NT, 4>;
+    auto k8 = conv_mma_patch_kernel<NT, 8>;
+    auto k16 = conv_mma_patch_kernel<NT, 16>;
+    auto k = p.pg.cp == 4 ? k4 : (p.pg.cp == 8 ? k8 : k16);
+    cudaError_t e = ensure_smem_attr(k, smem);
+    if (e != cudaSuccess) return e;
+    k<<<grid, block, smem, st>>>(p);
+    return cudaGetLastError();
+}
+
 template <int NT>
 static cudaError_t launch_mma_nt(int tile_k, const MmaParams& p, int grid, cudaStream_t st) {
     switch (tile_k) {
@@ -177,6 +346,15 @@ cudaError_t launch_conv_mma(const void* A, const void* B, void* C, const Plan& p
         p.cg.H = (int)d.h; p.cg.W = (int)d.w; p.cg.C = (int)d.c; p.cg.P = (int)P; p.cg.Q = (int)Q;
         p.cg.R = (int)d.r; p.cg.S = (int)d.s; p.cg.sh = (int)d.stride_h; p.cg.sw = (int)d.stride_w;
         p.cg.ph = (int)d.pad_h; p.cg.pw = (int)d.pad_w;
+    }
+    if (pl.mma_patch) {
+        p.pg = pl.mp;
+        p.batch = (int)d.batch;
+        switch (pl.sch.tile_n) {
+            case 16: return launch_patch_nt<2>(p, pl.grid_x, pl.block, pl.smem, st);
+            case 32: return launch_patch_nt<4>(p, pl.grid_x, pl.block, pl.smem, st);
+            default: return launch_patch_nt<8>(p, pl.grid_x, pl.block, pl.smem, st);
+        }
     }
     switch (pl.sch.tile_n) {
         case 16: return launch_mma_nt<2>(p.tile_k, p, pl.grid_x, st);

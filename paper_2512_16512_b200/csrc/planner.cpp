@@ -262,15 +262,46 @@ static xtc_status plan_tc_halo(const xtc_op_desc& d, const xtc_schedule& s, int 
 // Warp-MMA engine (conv_mma.cu): mma.sync m16n8k16 tiles over an im2col gather, any channel count
 static xtc_status plan_mma(const xtc_op_desc& d, const xtc_schedule& s, int num_sms, Plan& p, std::string& why) {
     if (d.in_dtype != XTC_BF16) ILLEGAL("MMA engine computes bf16 inputs (mma.sync m16n8k16 bf16 -> fp32)");
-    if (s.tile_m != 64 && s.tile_m != 128) ILLEGAL("MMA engine: tile_m must be 64 or 128 (16-row warp tiles)");
+    if (s.tile_m != 64 && s.tile_m != 128 && !(s.pack_halo && (s.tile_m == 256 || s.tile_m == 512)))
+        ILLEGAL("MMA engine: tile_m must be 64 or 128 (16-row warp tiles; 256 / 512 with pack_halo)");
     if (s.tile_n != 16 && s.tile_n != 32 && s.tile_n != 64) ILLEGAL("MMA engine: tile_n must be 16, 32 or 64");
     if (s.tile_k != 16 && s.tile_k != 32 && s.tile_k != 64) ILLEGAL("MMA engine: tile_k must be 16, 32 or 64");
     if (s.inner_m || s.inner_n) ILLEGAL("MMA engine: inner_m / inner_n must be 0 (the warp tile is 16 x tile_n)");
     if (s.unroll_k > 1 || s.vector_n > 1 || s.stages > 1 || s.swizzle) ILLEGAL("MMA engine: unroll_k, vector_n, stages, swizzle must be 0/1");
     if (p.split_k != 1) ILLEGAL("MMA engine: split_k must be 1");
     if (s.buffer_c || s.acc_buffers > 1) ILLEGAL("MMA engine: buffer_c 0, acc_buffers 0/1 (register accumulators)");
-    if (s.cluster_m > 1 || s.cluster_n > 1 || s.pack_warps > 1 || s.b_resident || s.pack_halo)
-        ILLEGAL("MMA engine: cluster_m, cluster_n, pack_warps, b_resident, pack_halo must be 0/1");
+    if (s.cluster_m > 1 || s.cluster_n > 1 || s.pack_warps > 1 || s.b_resident)
+        ILLEGAL("MMA engine: cluster_m, cluster_n, pack_warps, b_resident must be 0/1");
+    if (s.pack_halo) {
+        // pack above the (r, s, c) loops: the tile's input patch staged once in SMEM
+        if (d.kind != XTC_OP_CONV2D) ILLEGAL("MMA engine: pack_halo is a conv2d placement");
+        if (s.tile_k != 16) ILLEGAL("MMA engine pack_halo: tile_k must be 16 (the whole K is resident; 16 = the step)");
+        if (d.c > 16) ILLEGAL("MMA engine pack_halo: C must be <= 16 (channels padded to 4/8/16 in the patch)");
+        int64_t M_, N_, K_, P, Q;
+        gemm_view(d, M_, N_, K_, P, Q);
+        if (Q > 512) ILLEGAL("MMA engine pack_halo: Q must be <= 512 (one output row per CTA at most 16 warps)");
+        MmaPatch g;
+        if (!mma_patch_geom((int)d.h, (int)d.w, (int)d.c, (int)P, (int)Q, (int)d.r, (int)d.s, (int)d.stride_h,
+                            (int)d.stride_w, s.tile_m, s.tile_n, dtype_size(d.out_dtype), g))
+            ILLEGAL("MMA engine pack_halo: tile_m %d gives %d pixels per CTA (> 512)", s.tile_m, (int)(Q * (s.tile_m / Q)));
+        if (g.smem > kSmemMaxOptin)
+            ILLEGAL("MMA engine pack_halo: SMEM %d B (patch %d + filter %d + staging %d) > %d", g.smem, g.smem_patch,
+                    g.smem_b, g.smem_out, kSmemMaxOptin);
+        p.mma_patch = true;
+        p.mp = g;
+        p.block = g.warps * 32;
+        p.smem = g.smem;
+        p.tiles_m = (int)(d.batch * cdiv(P, g.tp));
+        p.tiles_n = (int)cdiv(p.N, s.tile_n);
+        p.kb_total = g.kp / 16;
+        p.kb_per_split = p.kb_total;
+        p.k_per_split = p.K;
+        p.num_tiles = (int64_t)p.tiles_m * p.tiles_n;
+        if (p.num_tiles >= (1ll << 31)) ILLEGAL("too many tiles");
+        const int per_sm = std::max(1, std::min(2048 / p.block, kSmemMaxOptin / std::max(1, g.smem + 1024)));
+        p.grid_x = s.persistent ? (int)std::min<int64_t>(p.num_tiles, (int64_t)num_sms * per_sm) : (int)p.num_tiles;
+        return XTC_OK;
+    }
     p.block = 256;
     p.smem = 0;
     p.tiles_m = (int)cdiv(p.M, s.tile_m);

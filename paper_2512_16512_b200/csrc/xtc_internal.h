@@ -81,6 +81,38 @@ XTC_HD void tile_coords(const TileMap& t, int64_t id64, int& mb, int& nb, int& k
     if (t.order == XTC_ORDER_MN) { mb = (int)outer; nb = (int)inner; } else { nb = (int)outer; mb = (int)inner; }
 }
 
+// Warp-MMA engine with the pack at the tile level (engine 2, pack_halo = 1; conv_mma.cu): a CTA tile
+// is tp whole output rows of one image (px = tp*Q pixels, 32 per warp), its input patch
+// (pr rows x wpatch pixel slots x cp channels, c padded to cp with zeros) staged in SMEM once,
+// and K ordered (r, s, c) with s padded to sp so that every 16-deep MMA step is one contiguous
+// run of sp*cp/16-th of a patch row: A fragments are plain 32-bit LDS at pixel base + offset.
+// Padded taps (s >= S, c >= C) carry zero filter weights.  Returns false when illegal.
+struct MmaPatch {
+    int32_t tp, cp, sp, ksr, kp, pr, wpatch, px, warps, b_pitch;
+    int32_t smem_patch, smem_b, smem_out, smem;
+};
+XTC_HD bool mma_patch_geom(int H, int W, int C, int P, int Q, int R, int S, int sh, int sw, int tile_m,
+                           int tile_n, int out_size, MmaPatch& g) {
+    (void)H; (void)W;
+    g.cp = C <= 4 ? 4 : (C <= 8 ? 8 : (C <= 16 ? 16 : 0));
+    if (g.cp == 0 || Q <= 0 || P <= 0) return false;
+    const int spq = 16 / g.cp;                        // taps per 16-deep step
+    g.sp = (S + spq - 1) / spq * spq;
+    g.ksr = g.sp * g.cp / 16;
+    g.kp = R * g.sp * g.cp;
+    g.tp = tile_m / Q < 1 ? 1 : tile_m / Q;
+    if (g.tp > P) g.tp = P;
+    g.px = g.tp * Q;
+    g.warps = (g.px + 31) / 32;
+    g.pr = (g.tp - 1) * sh + R;
+    g.wpatch = (Q - 1) * sw + g.sp;
+    g.b_pitch = g.kp + 8;                             // elements; = 8 mod 16 -> conflict-free B fragments
+    g.smem_patch = (g.pr * g.wpatch * g.cp * 2 + 15) / 16 * 16;
+    g.smem_b = (tile_n * g.b_pitch * 2 + 15) / 16 * 16;
+    g.smem_out = g.warps * 32 * tile_n * out_size;
+    g.smem = g.smem_patch + g.smem_b + g.smem_out;
+    return g.warps <= 16;
+}
 // ------------------------------------------------------------------ plans --
 struct Plan {
     xtc_schedule sch{};
@@ -123,6 +155,8 @@ struct Plan {
     int32_t cluster_n = 1;              // tcgen05 matmul: CTAs on adjacent N tiles sharing A by multicast;
                                         // tiles (num_tiles) then count cluster tiles of cluster_n N tiles
     int64_t halo_patch_bytes = 0;
+    bool mma_patch = false;             // engine 2 with pack_halo: the patch-staged warp-MMA conv
+    MmaPatch mp{};
 };
 
 // Host-only: legality + plan derivation.  Returns XTC_OK or an error with reason.

@@ -36,6 +36,24 @@ CONV_CASES = [
 ]
 
 
+def patch(**kw):
+    """pack_halo = 1: the patch-staged kernel (tile_m / Q whole output rows per CTA, K resident)."""
+    return mma(pack_halo=1, tile_k=16, **kw)
+
+
+CONV_CASES += [
+    ("patch-stem-n1-tp1", (1, 224, 224, 3, 16, 7, 7, 2, 3), patch(), "bf16"),
+    ("patch-stem-n2-tp2-f32-persistent", (2, 224, 224, 3, 16, 7, 7, 2, 3), patch(tile_m=256, persistent=1), "f32"),
+    ("patch-stem-ragged-p-tp4", (2, 100, 224, 3, 16, 7, 7, 2, 3), patch(tile_m=512), "bf16"),
+    ("patch-stem-persistent-grid3", (1, 64, 96, 3, 16, 7, 7, 2, 3), patch(tile_m=256, persistent=1, grid_sms=3), "bf16"),
+    ("patch-c1-5x5", (2, 28, 28, 1, 32, 5, 5, 1, 2), patch(tile_n=32), "bf16"),
+    ("patch-c3-3x3-s1-ragged", (1, 33, 37, 3, 16, 3, 3, 1, 1), patch(tile_m=64), "f32"),
+    ("patch-c5-f24-ragged-n", (2, 19, 23, 5, 24, 3, 3, 1, 1), patch(tile_n=32), "bf16"),
+    ("patch-c8-f40-stride3", (1, 30, 31, 8, 40, 5, 5, 3, 2), patch(tile_n=64), "f32"),
+    ("patch-c16-f48-two-n-tiles", (1, 20, 20, 16, 48, 3, 3, 1, 1), patch(tile_n=32, tile_m=256), "bf16"),
+]
+
+
 @pytest.mark.parametrize("case", CONV_CASES, ids=[c[0] for c in CONV_CASES])
 @pytest.mark.parametrize("mode", MODES)
 def test_mma_engine_conv_vs_oracle(case, mode):
@@ -52,8 +70,9 @@ def test_mma_engine_matmul_vs_oracle(shape, mode):
     assert err <= 5e-3
 
 
+@pytest.mark.parametrize("pk", [0, 1])
 @pytest.mark.parametrize("cons", ["relu", "bias", "accumulate+bias+relu"])
-def test_mma_engine_stem_fused_consumers(cons):
+def test_mma_engine_stem_fused_consumers(cons, pk):
     d = xtc.conv2d_desc(1, 224, 224, 3, 16, 7, 7, 2, 3, "bf16", "f32", consumer=cons)
     M, N, K = xtc.gemm_view(d)
     x = dev_tensor((1, 224, 224, 3), "bf16", 95, MODE_INT)
@@ -61,7 +80,7 @@ def test_mma_engine_stem_fused_consumers(cons):
     bias = dev_tensor((16,), "f32", 97, MODE_INT)
     y = dev_tensor((M, N), "f32", 98, MODE_INT)
     y_old = y.double().cpu().numpy()
-    xtc.Op(d).apply(mma(fuse=1)).run(x, w, y, bias=bias)
+    xtc.Op(d).apply(patch(fuse=1, tile_m=256) if pk else mma(fuse=1)).run(x, w, y, bias=bias)
     torch.cuda.synchronize()
     O, D = oracle_conv(d, "bf16", MODE_INT, 95, 96)
     O = O.copy()

@@ -478,6 +478,23 @@ def test_mma_engine_plan_and_legality():
         assert st == xtc.XTC_E_ILLEGAL_SCHEDULE and frag in why, (bad, why)
     f32 = xtc.conv2d_desc(1, 224, 224, 3, 16, 7, 7, 2, 3, "f32", "f32")
     assert xtc.xtc_schedule_check(f32, xtc.schedule(**base), 148)[0] == xtc.XTC_E_ILLEGAL_SCHEDULE
+    # pack_halo = 1: tile_m / Q whole output rows per CTA, the patch staged once (tile_k = the 16-deep step)
+    pk = dict(base, pack_halo=1, tile_k=16)
+    for tm, rows in ((128, 1), (256, 2), (512, 4)):
+        st, info, why = xtc.xtc_schedule_check(stem, xtc.schedule(**dict(pk, tile_m=tm)), 148)
+        assert st == 0 and info.num_tiles == 112 // rows and info.block_x == 32 * (-(-112 * rows // 32)), why
+        # patch rows (rows-1)*2+7 x slots 111*2+8 x 4 channels + filter 16 x (7*8*4+8) + staging
+        px_w = -(-112 * rows // 32) * 32
+        assert info.smem_bytes == -(-((rows - 1) * 2 + 7) * 230 * 8 // 16) * 16 + 16 * 232 * 2 + px_w * 16 * 2, info.smem_bytes
+    for bad, frag in ((dict(tile_k=32), "tile_k"), (dict(tile_m=1024), "tile_m")):
+        st, _, why = xtc.xtc_schedule_check(stem, xtc.schedule(**dict(pk, **bad)), 148)
+        assert st == xtc.XTC_E_ILLEGAL_SCHEDULE and frag in why, (bad, why)
+    wide_c = xtc.conv2d_desc(1, 14, 14, 32, 16, 3, 3, 1, 1)
+    st, _, why = xtc.xtc_schedule_check(wide_c, xtc.schedule(**pk), 148)
+    assert st == xtc.XTC_E_ILLEGAL_SCHEDULE and "C must be" in why
+    mm = xtc.matmul_desc(256, 64, 128)
+    st, _, why = xtc.xtc_schedule_check(mm, xtc.schedule(**pk), 148)
+    assert st == xtc.XTC_E_ILLEGAL_SCHEDULE and "conv2d" in why
 
 
 # --------------------------------------------- N3: descript + primitive log --
