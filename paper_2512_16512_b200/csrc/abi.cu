@@ -20,7 +20,7 @@ cudaError_t launch_tc_gemm(bool tf32, bool conv, int cta_group, const CUtensorMa
 cudaError_t launch_tc_conv_halo(bool tf32, const CUtensorMap& x, const CUtensorMap& b, const CUtensorMap& y,
                                 const TcParams& p, int grid, int smem, cudaStream_t st);
 cudaError_t launch_conv_mma(const void* A, const void* B, void* C, const Plan& pl, const xtc_op_desc& d,
-                            const float* bias, int cons, cudaStream_t st);
+                            const float* bias, int cons, const CUtensorMap* tmX, cudaStream_t st);
 cudaError_t launch_simt_gemm(int tm, int tn, int u, int vec, const SimtParams& p, int grid, int block, int smem,
                              cudaStream_t st);
 cudaError_t launch_fill(void* dst, int64_t count, int bf16, uint64_t seed, int mode, int64_t first, cudaStream_t st);
@@ -597,7 +597,29 @@ static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cud
     TileMap tm{p.tiles_m, p.tiles_n / (p.cluster_n > 1 ? p.cluster_n : 1), split_cluster ? 1 : p.split_k, p.sch.order,
                p.sch.raster_group};
     if (p.engine == XTC_ENGINE_MMA) {
-        CU_TRY(launch_conv_mma(A, B, C, p, d, op->bias, p.cons_epi, st), "conv_mma launch");
+        const CUtensorMap* tmX = nullptr;
+        if (p.mma_patch && p.mp.tma) {
+            // the patch map: x viewed as {16-element chunk, W*C/16 chunks, H, N}; one box
+            // {16, chunks, pr, 1} per tile lands as the tile's [row][chunk][32 B] patch
+            if (!op->maps_valid || op->bound[0] != A) {
+                xtc_status s0 = load_driver_fns();
+                if (s0 != XTC_OK) return s0;
+                if (reinterpret_cast<uintptr_t>(A) & 15) return fail(XTC_E_INVALID_ARG, "MMA patch (TMA): x must be 16-byte aligned");
+                const cuuint64_t wc = (cuuint64_t)(d.w * d.c);
+                cuuint64_t dims[4] = {16, wc / 16, (cuuint64_t)d.h, (cuuint64_t)d.batch};
+                cuuint64_t strides[3] = {32, wc * 2, (cuuint64_t)d.h * wc * 2};
+                cuuint32_t box[4] = {16, (cuuint32_t)p.mp.chunks, (cuuint32_t)p.mp.pr, 1};
+                cuuint32_t estr[4] = {1, 1, 1, 1};
+                CUresult r = g_encode_tiled(&op->tmA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(A), dims,
+                                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                if (r != CUDA_SUCCESS) return fail(XTC_E_CUDA, "cuTensorMapEncodeTiled(MMA patch) failed: " + std::to_string((int)r));
+                op->bound[0] = A; op->bound[1] = B; op->bound[2] = C;
+                op->maps_valid = true;
+            }
+            tmX = &op->tmA;
+        }
+        CU_TRY(launch_conv_mma(A, B, C, p, d, op->bias, p.cons_epi, tmX, st), "conv_mma launch");
         ++launches;
     } else if (p.engine == XTC_ENGINE_SIMT) {
         SimtParams sp;

@@ -19,7 +19,9 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 #include <string.h>
+#include <cuda.h>
 #include "consumer.cuh"
+#include "ptx.cuh"
 #include "xtc_internal.h"
 
 namespace xtc {
@@ -145,66 +147,103 @@ __global__ void __launch_bounds__(256) conv_mma_kernel(const MmaParams p) {
 }
 
 
-// ---- pack at the tile level (pack_halo = 1, conv only): the patch-staged kernel ----
+// ---- pack at the tile level (pack_halo = 1/2, conv only): the patch-staged kernel ----
 // A CTA tile = pg.tp whole output rows (p0 .. p0+tp) of image `img` x tile_n filters.  Its input
-// patch -- pg.pr input rows x pg.wpatch pixel slots x CP channels (channels >= C and pixels outside
-// the image are zeros: the zero padding, reading 3) -- is staged in SMEM ONCE per tile, the filter
-// slice transposed (Bs[n][k], k = (r, s, c) with s padded to pg.sp, c to CP; padded taps carry
-// zero weights).  Every 16-deep step (r, j) of pixel i then reads A from patch row
-// (i / Q) * sh + r at slot (i % Q) * sw + j * 16 / CP: a contiguous 32-byte run, so the m16n8k16
-// A fragments are four 32-bit LDS per 16 pixels (conflict-free for stride 2, CP = 4).  Each warp
-// owns 32 pixels (two m16 blocks) and all tile_n filters; the epilogue applies the consumer,
-// rounds once, stages the warp's 32 x tile_n block in SMEM and writes it with 16-byte stores.
-template <int NT, int CP>
-__global__ void __launch_bounds__(512) conv_mma_patch_kernel(const MmaParams p) {
-    extern __shared__ __align__(16) uint8_t smem[];
+// patch (pg.pr input rows) is staged in SMEM once per tile -- by one 4-D TMA per tile into a double
+// buffer (TMA: the raw NHWC rows, prefetched one tile ahead, zero fill = the padding), or by the
+// threads into pixel slots of CP channels (PAD) -- and the filter slice transposed (Bs[n][k], k =
+// (r, run element kl), tap t = kl - delta; padded positions carry zero weights).  Every 16-deep
+// step (r, j) of pixel i then reads A from patch row (i / Q) * sh + r at element
+// (i % Q) * pix_stride + off0 + 16 j: a contiguous 32-byte run, so the m16n8k16 A fragments are
+// four 32-bit LDS per 16 pixels.  Each warp owns 32 pixels (two m16 blocks) and all tile_n
+// filters; the epilogue applies the consumer, rounds once, stages the warp's 32 x tile_n block in
+// SMEM and writes it with 16-byte stores.
+// MODE: 0 = TMA raw rows; 4 / 8 / 16 = thread-filled slots of that many channels.
+template <int NT, int MODE>
+__global__ void __launch_bounds__(512) conv_mma_patch_kernel(const __grid_constant__ CUtensorMap tmX, const MmaParams p) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    constexpr bool TMA = MODE == 0;
+    constexpr int CP = TMA ? 4 : MODE;                 // (unused in TMA mode)
     const MmaPatch g = p.pg;
-    uint8_t* const patch = smem;
-    uint8_t* const Bs = smem + g.smem_patch;
+    uint8_t* const Bs = smem + g.nbuf * g.smem_patch;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
     const int nthr = blockDim.x;
     const int os = p.out_bf16 ? 2 : 4;
-    uint8_t* const Os = smem + g.smem_patch + g.smem_b + warp * 32 * (NT * 8) * os;
+    constexpr int tn = NT * 8;
+    uint8_t* const Os = Bs + g.smem_b + warp * 32 * tn * os;
+    uint64_t* const full = reinterpret_cast<uint64_t*>(Bs + g.smem_b + g.smem_out);
     const int H = p.cg.H, W = p.cg.W, C = p.cg.C, P = p.cg.P, Q = p.cg.Q, S = p.cg.S;
     const int tiles_p = (P + g.tp - 1) / g.tp;
-    const int row_bytes = g.wpatch * CP * 2;
-    const int slots = g.pr * g.wpatch;
-    const int spc = g.sp * CP;                       // k per filter row r
-    for (int64_t t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-        int mb, nb, ks;
+    const uint32_t patch_tx = (uint32_t)(g.pr * g.rowpitch);
+    auto tile_pos = [&](int64_t t, int& img, int& p0, int& nb) {
+        int mb, ks;
         tile_coords(p.tm, t, mb, nb, ks);
-        const int img = mb / tiles_p;
-        const int p0 = (mb - img * tiles_p) * g.tp;
-        const int n0 = nb * (NT * 8);
-        __syncthreads();                             // the previous tile's patch and filter are consumed
-        // ---- pack the patch: one CP-channel pixel slot per thread-iteration ----
-        const int h_base = p0 * p.cg.sh - p.cg.ph;
-        for (int sl = tid; sl < slots; sl += nthr) {
-            const int rr = sl / g.wpatch, ww = sl - rr * g.wpatch;
-            const int h = h_base + rr, w = ww - p.cg.pw;
-            uint16_t v[CP];
+        img = mb / tiles_p;
+        p0 = (mb - img * tiles_p) * g.tp;
+    };
+    auto issue_patch = [&](int64_t t, int buf) {        // one thread: the whole patch of tile t
+        int img, p0, nb;
+        tile_pos(t, img, p0, nb);
+        ptx::mbar_arrive_expect_tx(&full[buf], patch_tx);
+        ptx::tma_load_4d(&tmX, smem + buf * g.smem_patch, &full[buf], 0, g.x0 / 16, p0 * p.cg.sh - p.cg.ph, img);
+    };
+    if (TMA && tid == 0) {
+        ptx::prefetch_tmap(&tmX);
+        ptx::mbar_init(&full[0], 1);
+        ptx::mbar_init(&full[1], 1);
+        ptx::fence_mbarrier_init();
+    }
+    __syncthreads();
+    if (TMA && tid == 0 && (int64_t)blockIdx.x < p.num_tiles) issue_patch(blockIdx.x, 0);
+    int cur_nb = -1;
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
+        int img, p0, nb;
+        tile_pos(t, img, p0, nb);
+        const int n0 = nb * tn;
+        const int buf = TMA ? (it & 1) : 0;
+        uint8_t* const patch = smem + buf * g.smem_patch;
+        // the next tile's patch into the other buffer: its last reader (tile it-1) passed the
+        // __syncthreads at the end of the previous iteration
+        if (TMA && tid == 0 && t + gridDim.x < p.num_tiles) issue_patch(t + gridDim.x, buf ^ 1);
+        if (!TMA) {
+            // ---- thread-filled patch: one CP-channel pixel slot per thread-iteration ----
+            const int h_base = p0 * p.cg.sh - p.cg.ph;
+            const int slots = g.pr * g.wpatch;
+            for (int sl = tid; sl < slots; sl += nthr) {
+                const int rr = sl / g.wpatch, ww = sl - rr * g.wpatch;
+                const int h = h_base + rr, w = ww - p.cg.pw;
+                uint16_t v[CP];
 #pragma unroll
-            for (int c = 0; c < CP; ++c) v[c] = 0;
-            if (h >= 0 && h < H && w >= 0 && w < W) {
-                const uint16_t* src = p.A + (((int64_t)img * H + h) * W + w) * C;
+                for (int c = 0; c < CP; ++c) v[c] = 0;
+                if (h >= 0 && h < H && w >= 0 && w < W) {
+                    const uint16_t* src = p.A + (((int64_t)img * H + h) * W + w) * C;
 #pragma unroll
-                for (int c = 0; c < CP; ++c)
-                    if (c < C) v[c] = __ldg(src + c);
+                    for (int c = 0; c < CP; ++c)
+                        if (c < C) v[c] = __ldg(src + c);
+                }
+                uint32_t* dst = reinterpret_cast<uint32_t*>(patch + (size_t)sl * CP * 2);
+#pragma unroll
+                for (int c = 0; c < CP; c += 2) dst[c / 2] = (uint32_t)v[c] | ((uint32_t)v[c + 1] << 16);
             }
-            uint32_t* dst = reinterpret_cast<uint32_t*>(patch + (size_t)sl * CP * 2);
-#pragma unroll
-            for (int c = 0; c < CP; c += 2) dst[c / 2] = (uint32_t)v[c] | ((uint32_t)v[c + 1] << 16);
         }
-        // ---- pack the filter slice transposed: Bs[n][k] ----
-        for (int i = tid; i < NT * 8 * g.kp; i += nthr) {
-            const int nn = i % (NT * 8), kk = i / (NT * 8);
-            const int r = kk / spc, rem = kk - r * spc, s = rem / CP, c = rem - s * CP;
-            const int64_t n = n0 + nn;
-            uint16_t v = 0;
-            if (s < S && c < C && n < p.N) v = __ldg(p.B + ((int64_t)(r * S + s) * C + c) * p.ldb + n);
-            reinterpret_cast<uint16_t*>(Bs)[nn * g.b_pitch + kk] = v;
+        const bool refill = nb != cur_nb;
+        if (refill) {
+            // ---- the filter slice transposed: Bs[n][k] (once per CTA when tiles_n == 1) ----
+            for (int i = tid; i < tn * g.kp; i += nthr) {
+                const int nn = i % tn, kk = i / tn;
+                const int r = kk / g.kpr, tap = kk - r * g.kpr - g.delta;
+                const int s = tap / g.bcp, c = tap - s * g.bcp;
+                const int64_t n = n0 + nn;
+                uint16_t v = 0;
+                if (tap >= 0 && s < S && c < C && n < p.N)
+                    v = __ldg(p.B + ((int64_t)(r * S + s) * C + c) * p.ldb + n);
+                reinterpret_cast<uint16_t*>(Bs)[nn * g.b_pitch + kk] = v;
+            }
+            cur_nb = nb;
         }
-        __syncthreads();
+        if (!TMA || refill) __syncthreads();          // thread-filled patch / (re)filled filter visible
+        if (TMA) ptx::mbar_wait(&full[buf], (uint32_t)((it >> 1) & 1));
         // ---- contraction: 2 m16 blocks x NT n8 blocks per warp ----
         float acc[2][NT][4];
 #pragma unroll
@@ -219,38 +258,35 @@ __global__ void __launch_bounds__(512) conv_mma_patch_kernel(const MmaParams p) 
                 int i = warp * 32 + b * 16 + hh * 8 + gq;
                 if (i >= g.px) i = g.px - 1;         // rows past the tile compute a copy, never stored
                 const int pp = i / Q, qq = i - pp * Q;
-                abase[b][hh] = patch + (size_t)pp * p.cg.sh * row_bytes + (size_t)qq * p.cg.sw * CP * 2 + 4 * tq;
+                abase[b][hh] = patch + (size_t)pp * p.cg.sh * g.rowpitch + (size_t)(qq * g.pix_stride + g.off0) * 2 + 4 * tq;
             }
         const uint8_t* bbase = Bs + (gq * g.b_pitch + 2 * tq) * 2;
-        if (warp * 32 < g.px) {
-            for (int r = 0; r < p.cg.R; ++r) {
-                for (int j = 0; j < g.ksr; ++j) {
-                    const int aoff = r * row_bytes + j * 32;
-                    const int boff = (r * g.ksr + j) * 32;
-                    uint32_t bf[NT][2];
+        for (int r = 0; r < p.cg.R; ++r) {
+            for (int j = 0; j < g.ksr; ++j) {
+                const int aoff = r * g.rowpitch + j * 32;
+                const int boff = (r * g.ksr + j) * 32;
+                uint32_t bf[NT][2];
 #pragma unroll
-                    for (int nt = 0; nt < NT; ++nt) {
-                        const uint8_t* bp = bbase + nt * 8 * g.b_pitch * 2 + boff;
-                        bf[nt][0] = *reinterpret_cast<const uint32_t*>(bp);
-                        bf[nt][1] = *reinterpret_cast<const uint32_t*>(bp + 16);
-                    }
+                for (int nt = 0; nt < NT; ++nt) {
+                    const uint8_t* bp = bbase + nt * 8 * g.b_pitch * 2 + boff;
+                    bf[nt][0] = *reinterpret_cast<const uint32_t*>(bp);
+                    bf[nt][1] = *reinterpret_cast<const uint32_t*>(bp + 16);
+                }
 #pragma unroll
-                    for (int b = 0; b < 2; ++b) {
-                        uint32_t a[4];
-                        a[0] = *reinterpret_cast<const uint32_t*>(abase[b][0] + aoff);
-                        a[1] = *reinterpret_cast<const uint32_t*>(abase[b][1] + aoff);
-                        a[2] = *reinterpret_cast<const uint32_t*>(abase[b][0] + aoff + 16);
-                        a[3] = *reinterpret_cast<const uint32_t*>(abase[b][1] + aoff + 16);
+                for (int b = 0; b < 2; ++b) {
+                    uint32_t a[4];
+                    a[0] = *reinterpret_cast<const uint32_t*>(abase[b][0] + aoff);
+                    a[1] = *reinterpret_cast<const uint32_t*>(abase[b][1] + aoff);
+                    a[2] = *reinterpret_cast<const uint32_t*>(abase[b][0] + aoff + 16);
+                    a[3] = *reinterpret_cast<const uint32_t*>(abase[b][1] + aoff + 16);
 #pragma unroll
-                        for (int nt = 0; nt < NT; ++nt) mma_bf16_16816(acc[b][nt], a, bf[nt]);
-                    }
+                    for (int nt = 0; nt < NT; ++nt) mma_bf16_16816(acc[b][nt], a, bf[nt]);
                 }
             }
         }
         // ---- epilogue: consumer + one rounding, staged per warp, 16-byte stores ----
         const int rows_valid = min(g.tp, P - p0) * Q;             // pixels of this tile that exist
         const int64_t m_tile = ((int64_t)img * P + p0) * Q;
-        const int tn = NT * 8;
 #pragma unroll
         for (int b = 0; b < 2; ++b)
 #pragma unroll
@@ -278,7 +314,8 @@ __global__ void __launch_bounds__(512) conv_mma_patch_kernel(const MmaParams p) 
         const int wrows = max(0, min(32, rows_valid - warp * 32));
         const int64_t m_w = m_tile + warp * 32;
         const int row_b = tn * os;                                 // staged bytes per row
-        const bool vec = (n0 + tn <= p.N) && ((p.ldc * os) % 16 == 0) && ((n0 * os) % 16 == 0);
+        const bool vec = (n0 + tn <= p.N) && ((p.ldc * os) % 16 == 0) && ((n0 * os) % 16 == 0) &&
+                         ((reinterpret_cast<uintptr_t>(p.C) & 15) == 0);
         uint8_t* const Cb = static_cast<uint8_t*>(p.C);
         if (vec) {
             const int vpr = row_b / 16;                            // 16-byte vectors per row
@@ -296,18 +333,21 @@ __global__ void __launch_bounds__(512) conv_mma_patch_kernel(const MmaParams p) 
                 else *reinterpret_cast<float*>(dst) = *reinterpret_cast<const float*>(Os + (rr * tn + cc) * 4);
             }
         }
+        __syncthreads();          // patch buffer, filter and staging free for the next tile
     }
 }
 
 template <int NT>
-static cudaError_t launch_patch_nt(const MmaParams& p, int grid, int block, int smem, cudaStream_t st) {
-    auto k4 = conv_mma_patch_kernel<NT, 4>;
-    auto k8 = conv_mma_patch_kernel<NT, 8>;
-    auto k16 = conv_mma_patch_kernel<NT, 16>;
-    auto k = p.pg.cp == 4 ? k4 : (p.pg.cp == 8 ? k8 : k16);
+static cudaError_t launch_patch_nt(const CUtensorMap* tmX, const MmaParams& p, int grid, int block, int smem,
+                                   cudaStream_t st) {
+    auto k = p.pg.tma ? conv_mma_patch_kernel<NT, 0>
+                      : (p.pg.cp == 4 ? conv_mma_patch_kernel<NT, 4>
+                                      : (p.pg.cp == 8 ? conv_mma_patch_kernel<NT, 8> : conv_mma_patch_kernel<NT, 16>));
     cudaError_t e = ensure_smem_attr(k, smem);
     if (e != cudaSuccess) return e;
-    k<<<grid, block, smem, st>>>(p);
+    CUtensorMap dummy;
+    memset(&dummy, 0, sizeof dummy);
+    k<<<grid, block, smem, st>>>(tmX ? *tmX : dummy, p);
     return cudaGetLastError();
 }
 
@@ -322,7 +362,7 @@ static cudaError_t launch_mma_nt(int tile_k, const MmaParams& p, int grid, cudaS
 }
 
 cudaError_t launch_conv_mma(const void* A, const void* B, void* C, const Plan& pl, const xtc_op_desc& d,
-                            const float* bias, int cons, cudaStream_t st) {
+                            const float* bias, int cons, const CUtensorMap* tmX, cudaStream_t st) {
     MmaParams p;
     memset(&p, 0, sizeof p);
     p.A = static_cast<const uint16_t*>(A);
@@ -351,9 +391,9 @@ cudaError_t launch_conv_mma(const void* A, const void* B, void* C, const Plan& p
         p.pg = pl.mp;
         p.batch = (int)d.batch;
         switch (pl.sch.tile_n) {
-            case 16: return launch_patch_nt<2>(p, pl.grid_x, pl.block, pl.smem, st);
-            case 32: return launch_patch_nt<4>(p, pl.grid_x, pl.block, pl.smem, st);
-            default: return launch_patch_nt<8>(p, pl.grid_x, pl.block, pl.smem, st);
+            case 16: return launch_patch_nt<2>(tmX, p, pl.grid_x, pl.block, pl.smem, st);
+            case 32: return launch_patch_nt<4>(tmX, p, pl.grid_x, pl.block, pl.smem, st);
+            default: return launch_patch_nt<8>(tmX, p, pl.grid_x, pl.block, pl.smem, st);
         }
     }
     switch (pl.sch.tile_n) {

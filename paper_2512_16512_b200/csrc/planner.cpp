@@ -281,8 +281,11 @@ static xtc_status plan_mma(const xtc_op_desc& d, const xtc_schedule& s, int num_
         gemm_view(d, M_, N_, K_, P, Q);
         if (Q > 512) ILLEGAL("MMA engine pack_halo: Q must be <= 512 (one output row per CTA at most 16 warps)");
         MmaPatch g;
-        if (!mma_patch_geom((int)d.h, (int)d.w, (int)d.c, (int)P, (int)Q, (int)d.r, (int)d.s, (int)d.stride_h,
-                            (int)d.stride_w, s.tile_m, s.tile_n, dtype_size(d.out_dtype), g))
+        // pack_halo 1: the TMA patch layout where it applies; 2: always the thread-filled padded layout
+        if (s.pack_halo > 2) ILLEGAL("MMA engine: pack_halo must be 0, 1 (TMA patch where legal) or 2 (thread-filled)");
+        const bool allow_tma = s.pack_halo == 1;
+        if (!mma_patch_geom((int)d.h, (int)d.w, (int)d.c, (int)P, (int)Q, (int)d.r, (int)d.s, (int)d.stride_w,
+                            (int)d.stride_h, (int)d.pad_w, s.tile_m, s.tile_n, dtype_size(d.out_dtype), allow_tma, g))
             ILLEGAL("MMA engine pack_halo: tile_m %d gives %d pixels per CTA (> 512)", s.tile_m, (int)(Q * (s.tile_m / Q)));
         if (g.smem > kSmemMaxOptin)
             ILLEGAL("MMA engine pack_halo: SMEM %d B (patch %d + filter %d + staging %d) > %d", g.smem, g.smem_patch,

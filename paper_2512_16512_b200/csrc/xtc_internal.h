@@ -82,35 +82,75 @@ XTC_HD void tile_coords(const TileMap& t, int64_t id64, int& mb, int& nb, int& k
 }
 
 // Warp-MMA engine with the pack at the tile level (engine 2, pack_halo = 1; conv_mma.cu): a CTA tile
-// is tp whole output rows of one image (px = tp*Q pixels, 32 per warp), its input patch
-// (pr rows x wpatch pixel slots x cp channels, c padded to cp with zeros) staged in SMEM once,
-// and K ordered (r, s, c) with s padded to sp so that every 16-deep MMA step is one contiguous
-// run of sp*cp/16-th of a patch row: A fragments are plain 32-bit LDS at pixel base + offset.
-// Padded taps (s >= S, c >= C) carry zero filter weights.  Returns false when illegal.
+// is tp whole output rows of one image (px = tp*Q pixels, 32 per warp); its input patch of pr input
+// rows is staged in SMEM once, K is ordered (r, then a contiguous run of kpr = ksr*16 elements of
+// patch row r), so every 16-deep MMA step of a pixel is one contiguous 32-byte run of its patch row
+// and the A fragments are plain 32-bit LDS at (pixel base + offset).  Two patch layouts:
+//  * tma (sw*C even, W*C % 16 == 0): the raw NHWC row, loaded by ONE 4-D TMA {16, chunks, pr, 1}
+//    over the input viewed as {16-element chunk, W*C/16 chunks, H, N}, double-buffered; the row
+//    starts at element x0 = 16*floor(-pw*C/16) (out-of-bounds chunks / rows are TMA zero fill =
+//    the zero padding, reading 3); pixel q's run starts at element q*sw*C - pw*C - x0 - delta,
+//    delta in {0,1} making every start even (4-byte aligned pairs); filter tap t = kl - delta.
+//  * padded (otherwise, C <= 16): pixel slots of cp = 4/8/16 channels filled by the threads
+//    (zeros past C and outside the image), taps s padded to sp; tap t = kl, s = t / cp.
+// Padded K positions carry zero filter weights.
 struct MmaPatch {
-    int32_t tp, cp, sp, ksr, kp, pr, wpatch, px, warps, b_pitch;
-    int32_t smem_patch, smem_b, smem_out, smem;
+    int32_t tma, tp, cp, sp, ksr, kpr, kp, pr, px, warps, b_pitch;
+    int32_t wpatch;          // padded: pixel slots per patch row
+    int32_t chunks, x0;      // tma: 16-element chunks per patch row, first element of the row
+    int32_t rowpitch;        // bytes per patch row in SMEM
+    int32_t pix_stride;      // elements between the runs of adjacent output pixels (sw*cp or sw*C)
+    int32_t off0;            // element offset of pixel 0's run in its patch row
+    int32_t bcp, delta;      // filter packing: tap t = kl - delta, s = t / bcp, c = t % bcp (c < C valid)
+    int32_t smem_patch;      // bytes per patch buffer (x nbuf)
+    int32_t nbuf, smem_b, smem_out, smem;
 };
-XTC_HD bool mma_patch_geom(int H, int W, int C, int P, int Q, int R, int S, int sh, int sw, int tile_m,
-                           int tile_n, int out_size, MmaPatch& g) {
-    (void)H; (void)W;
-    g.cp = C <= 4 ? 4 : (C <= 8 ? 8 : (C <= 16 ? 16 : 0));
-    if (g.cp == 0 || Q <= 0 || P <= 0) return false;
-    const int spq = 16 / g.cp;                        // taps per 16-deep step
-    g.sp = (S + spq - 1) / spq * spq;
-    g.ksr = g.sp * g.cp / 16;
-    g.kp = R * g.sp * g.cp;
+XTC_HD bool mma_patch_geom(int H, int W, int C, int P, int Q, int R, int S, int sw, int sh, int pw, int tile_m,
+                           int tile_n, int out_size, bool allow_tma, MmaPatch& g) {
+    (void)H;
+    if (Q <= 0 || P <= 0 || C > 16) return false;
     g.tp = tile_m / Q < 1 ? 1 : tile_m / Q;
     if (g.tp > P) g.tp = P;
     g.px = g.tp * Q;
     g.warps = (g.px + 31) / 32;
     g.pr = (g.tp - 1) * sh + R;
-    g.wpatch = (Q - 1) * sw + g.sp;
-    g.b_pitch = g.kp + 8;                             // elements; = 8 mod 16 -> conflict-free B fragments
-    g.smem_patch = (g.pr * g.wpatch * g.cp * 2 + 15) / 16 * 16;
-    g.smem_b = (tile_n * g.b_pitch * 2 + 15) / 16 * 16;
+    g.tma = allow_tma && (sw * C) % 2 == 0 && (W * C) % 16 == 0;
+    if (g.tma) {
+        g.cp = C;
+        g.x0 = -(((pw * C) + 15) / 16) * 16;                     // 16 * floor(-pw*C / 16)
+        g.delta = (-pw * C - g.x0) & 1;
+        g.kpr = (S * C + g.delta + 15) / 16 * 16;
+        g.off0 = -pw * C - g.x0 - g.delta;
+        g.pix_stride = sw * C;
+        const int last = (Q - 1) * g.pix_stride + g.off0 + g.kpr - 1;   // last element read, from x0
+        g.chunks = last / 16 + 1;
+        if (g.chunks > 256 || g.pr > 256) g.tma = 0;
+    }
+    if (g.tma) {
+        g.sp = 0; g.wpatch = 0;
+        g.rowpitch = g.chunks * 32;
+        g.bcp = C;
+        g.nbuf = 2;
+        g.smem_patch = (g.pr * g.rowpitch + 127) / 128 * 128;
+    } else {
+        g.cp = C <= 4 ? 4 : (C <= 8 ? 8 : 16);
+        const int spq = 16 / g.cp;                                 // taps per 16-deep step
+        g.sp = (S + spq - 1) / spq * spq;
+        g.kpr = g.sp * g.cp;
+        g.wpatch = (Q - 1) * sw + g.sp;
+        g.rowpitch = g.wpatch * g.cp * 2;
+        g.pix_stride = sw * g.cp;
+        g.off0 = 0; g.x0 = 0; g.chunks = 0;
+        g.bcp = g.cp; g.delta = 0;
+        g.nbuf = 1;
+        g.smem_patch = (g.pr * g.rowpitch + 127) / 128 * 128;
+    }
+    g.ksr = g.kpr / 16;
+    g.kp = R * g.kpr;
+    g.b_pitch = g.kp + 8;                                         // elements; = 8 mod 16 -> conflict-free B fragments
+    g.smem_b = (tile_n * g.b_pitch * 2 + 127) / 128 * 128;
     g.smem_out = g.warps * 32 * tile_n * out_size;
-    g.smem = g.smem_patch + g.smem_b + g.smem_out;
+    g.smem = g.nbuf * g.smem_patch + g.smem_b + g.smem_out + 16;  // + the two patch mbarriers
     return g.warps <= 16;
 }
 // ------------------------------------------------------------------ plans --

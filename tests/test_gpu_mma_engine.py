@@ -37,8 +37,11 @@ CONV_CASES = [
 
 
 def patch(**kw):
-    """pack_halo = 1: the patch-staged kernel (tile_m / Q whole output rows per CTA, K resident)."""
-    return mma(pack_halo=1, tile_k=16, **kw)
+    """pack_halo = 1: the patch-staged kernel (tile_m / Q whole output rows per CTA, K resident), the
+    input patch loaded by one TMA per tile where the layout allows; pack_halo = 2: filled by the threads."""
+    base = dict(pack_halo=1, tile_k=16)
+    base.update(kw)
+    return mma(**base)
 
 
 CONV_CASES += [
@@ -51,6 +54,14 @@ CONV_CASES += [
     ("patch-c5-f24-ragged-n", (2, 19, 23, 5, 24, 3, 3, 1, 1), patch(tile_n=32), "bf16"),
     ("patch-c8-f40-stride3", (1, 30, 31, 8, 40, 5, 5, 3, 2), patch(tile_n=64), "f32"),
     ("patch-c16-f48-two-n-tiles", (1, 20, 20, 16, 48, 3, 3, 1, 1), patch(tile_n=32, tile_m=256), "bf16"),
+    # TMA patch layout (sw*C even, W*C % 16 == 0) -- the stem cases above take it; these force or avoid it
+    ("tma-c8-s1-two-n-tiles-persistent", (2, 17, 18, 8, 40, 3, 3, 1, 1), patch(tile_n=32, persistent=1, grid_sms=2), "f32"),
+    ("tma-c16-5x5-pad2-ragged-p", (1, 21, 24, 16, 16, 5, 5, 1, 2), patch(tile_m=64), "bf16"),
+    ("tma-c4-stride2-pad0", (2, 31, 36, 4, 24, 3, 3, 2, 0), patch(tile_n=32, tile_m=256), "bf16"),
+    ("tma-c2-7x7-pad3-wide-row", (1, 12, 480, 2, 16, 7, 7, 2, 3), patch(), "bf16"),
+    ("thread-filled-stem-n2", (2, 224, 224, 3, 16, 7, 7, 2, 3), patch(pack_halo=2, tile_m=512), "bf16"),
+    ("thread-filled-c16-persistent", (2, 20, 20, 16, 48, 3, 3, 1, 1), patch(pack_halo=2, tile_n=64, persistent=1,
+                                                                             grid_sms=3), "f32"),
 ]
 
 

@@ -483,10 +483,18 @@ def test_mma_engine_plan_and_legality():
     for tm, rows in ((128, 1), (256, 2), (512, 4)):
         st, info, why = xtc.xtc_schedule_check(stem, xtc.schedule(**dict(pk, tile_m=tm)), 148)
         assert st == 0 and info.num_tiles == 112 // rows and info.block_x == 32 * (-(-112 * rows // 32)), why
-        # patch rows (rows-1)*2+7 x slots 111*2+8 x 4 channels + filter 16 x (7*8*4+8) + staging
+        # TMA layout (sw*C = 6 even, W*C = 672 = 42 chunks of 16): the row starts at element x0 = -16, delta = 1
+        # makes every pixel run start even, kpr = 32 (21 taps + 1), 44 chunks of 32 B per row; 2 patch buffers
+        # + filter 16 x (7*32 + 8) + staging + 2 mbarriers
+        pr = (rows - 1) * 2 + 7
         px_w = -(-112 * rows // 32) * 32
-        assert info.smem_bytes == -(-((rows - 1) * 2 + 7) * 230 * 8 // 16) * 16 + 16 * 232 * 2 + px_w * 16 * 2, info.smem_bytes
-    for bad, frag in ((dict(tile_k=32), "tile_k"), (dict(tile_m=1024), "tile_m")):
+        rnd = lambda b: -(-b // 128) * 128
+        assert info.smem_bytes == 2 * rnd(pr * 44 * 32) + rnd(16 * 232 * 2) + px_w * 16 * 2 + 16, info.smem_bytes
+        # pack_halo 2: thread-filled pixel slots of 4 channels, taps padded 7 -> 8, 230 slots per row, 1 buffer
+        st, info2, why = xtc.xtc_schedule_check(stem, xtc.schedule(**dict(pk, tile_m=tm, pack_halo=2)), 148)
+        assert st == 0 and info2.num_tiles == info.num_tiles, why
+        assert info2.smem_bytes == rnd(pr * 230 * 8) + rnd(16 * 232 * 2) + px_w * 16 * 2 + 16, info2.smem_bytes
+    for bad, frag in ((dict(tile_k=32), "tile_k"), (dict(tile_m=1024), "tile_m"), (dict(pack_halo=3), "pack_halo")):
         st, _, why = xtc.xtc_schedule_check(stem, xtc.schedule(**dict(pk, **bad)), 148)
         assert st == xtc.XTC_E_ILLEGAL_SCHEDULE and frag in why, (bad, why)
     wide_c = xtc.conv2d_desc(1, 14, 14, 32, 16, 3, 3, 1, 1)
