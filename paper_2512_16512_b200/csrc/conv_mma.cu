@@ -49,6 +49,12 @@ __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
 }
 
+__device__ __forceinline__ uint32_t lds32(uint32_t saddr) {
+    uint32_t v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(saddr));
+    return v;
+}
+
 // NT = tile_n / 8 n8-blocks per warp; BK = k-chunk (multiple of 16)
 template <int NT, int BK>
 __global__ void __launch_bounds__(256) conv_mma_kernel(const MmaParams p) {
@@ -175,18 +181,28 @@ __global__ void __launch_bounds__(512) conv_mma_patch_kernel(const __grid_consta
     const int H = p.cg.H, W = p.cg.W, C = p.cg.C, P = p.cg.P, Q = p.cg.Q, S = p.cg.S;
     const int tiles_p = (P + g.tp - 1) / g.tp;
     const uint32_t patch_tx = (uint32_t)(g.pr * g.rowpitch);
-    auto tile_pos = [&](int64_t t, int& img, int& p0, int& nb) {
-        int mb, ks;
-        tile_coords(p.tm, t, mb, nb, ks);
-        img = mb / tiles_p;
-        p0 = (mb - img * tiles_p) * g.tp;
-    };
-    auto issue_patch = [&](int64_t t, int buf) {        // one thread: the whole patch of tile t
-        int img, p0, nb;
-        tile_pos(t, img, p0, nb);
-        ptx::mbar_arrive_expect_tx(&full[buf], patch_tx);
-        ptx::tma_load_4d(&tmX, smem + buf * g.smem_patch, &full[buf], 0, g.x0 / 16, p0 * p.cg.sh - p.cg.ph, img);
-    };
+#define XTC_TILE_POS(t, img, p0, nb)                                   \
+    do {                                                               \
+        int mb_, ks_;                                                  \
+        tile_coords(p.tm, (t), mb_, nb, ks_);                          \
+        img = mb_ / tiles_p;                                           \
+        p0 = (mb_ - img * tiles_p) * g.tp;                             \
+    } while (0)
+#define XTC_ISSUE_PATCH(t, buf)                                                                          \
+    do {                                                                                                 \
+        int img_, p0_, nb_;                                                                              \
+        XTC_TILE_POS((t), img_, p0_, nb_);                                                               \
+        ptx::mbar_arrive_expect_tx(&full[(buf)], patch_tx);                                              \
+        ptx::tma_load_4d(&tmX, smem + (buf) * g.smem_patch, &full[(buf)], 0, g.x0 / 16,                  \
+                         p0_ * p.cg.sh - p.cg.ph, img_);                                                 \
+    } while (0)
+    // k -> row (r*S + s)*C + c of the RSCF filter, -1 for the zero-weight padding of K
+    int* const koff = reinterpret_cast<int*>(Bs + g.smem_b + g.smem_out + 16);
+    for (int kk = tid; kk < g.kp; kk += nthr) {
+        const int r = kk / g.kpr, tap = kk - r * g.kpr - g.delta;
+        const int s = tap / g.bcp, c = tap - s * g.bcp;
+        koff[kk] = (tap >= 0 && s < S && c < C) ? (r * S + s) * C + c : -1;
+    }
     if (TMA && tid == 0) {
         ptx::prefetch_tmap(&tmX);
         ptx::mbar_init(&full[0], 1);
@@ -194,18 +210,30 @@ __global__ void __launch_bounds__(512) conv_mma_patch_kernel(const __grid_consta
         ptx::fence_mbarrier_init();
     }
     __syncthreads();
-    if (TMA && tid == 0 && (int64_t)blockIdx.x < p.num_tiles) issue_patch(blockIdx.x, 0);
+    if (TMA && tid == 0 && (int64_t)blockIdx.x < p.num_tiles) XTC_ISSUE_PATCH((int64_t)blockIdx.x, 0);
+    // tile-invariant operand offsets (bytes within a patch buffer / the filter slice) of this lane
+    uint32_t a_off[2][2];
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+            int i = warp * 32 + b * 16 + hh * 8 + gq;
+            if (i >= g.px) i = g.px - 1;             // rows past the tile compute a copy, never stored
+            const int pp = i / Q, qq = i - pp * Q;
+            a_off[b][hh] = (uint32_t)(pp * p.cg.sh * g.rowpitch + (qq * g.pix_stride + g.off0) * 2 + 4 * tq);
+        }
+    const uint32_t b_lane = ptx::smem_u32(Bs) + (gq * g.b_pitch + 2 * tq) * 2;
     int cur_nb = -1;
     int it = 0;
     for (int64_t t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
         int img, p0, nb;
-        tile_pos(t, img, p0, nb);
+        XTC_TILE_POS(t, img, p0, nb);
         const int n0 = nb * tn;
         const int buf = TMA ? (it & 1) : 0;
         uint8_t* const patch = smem + buf * g.smem_patch;
         // the next tile's patch into the other buffer: its last reader (tile it-1) passed the
         // __syncthreads at the end of the previous iteration
-        if (TMA && tid == 0 && t + gridDim.x < p.num_tiles) issue_patch(t + gridDim.x, buf ^ 1);
+        if (TMA && tid == 0 && t + gridDim.x < p.num_tiles) XTC_ISSUE_PATCH(t + gridDim.x, buf ^ 1);
         if (!TMA) {
             // ---- thread-filled patch: one CP-channel pixel slot per thread-iteration ----
             const int h_base = p0 * p.cg.sh - p.cg.ph;
@@ -229,16 +257,27 @@ __global__ void __launch_bounds__(512) conv_mma_patch_kernel(const __grid_consta
         }
         const bool refill = nb != cur_nb;
         if (refill) {
-            // ---- the filter slice transposed: Bs[n][k] (once per CTA when tiles_n == 1) ----
-            for (int i = tid; i < tn * g.kp; i += nthr) {
-                const int nn = i % tn, kk = i / tn;
-                const int r = kk / g.kpr, tap = kk - r * g.kpr - g.delta;
-                const int s = tap / g.bcp, c = tap - s * g.bcp;
-                const int64_t n = n0 + nn;
-                uint16_t v = 0;
-                if (tap >= 0 && s < S && c < C && n < p.N)
-                    v = __ldg(p.B + ((int64_t)(r * S + s) * C + c) * p.ldb + n);
-                reinterpret_cast<uint16_t*>(Bs)[nn * g.b_pitch + kk] = v;
+            // ---- the filter slice transposed: Bs[n][k] (once per CTA when tiles_n == 1), through
+            // the k -> filter-row table built once per CTA ----
+            // 16 loads in flight per thread per batch (one L2 round trip for the stem's 3.6 K entries)
+            const int total = tn * g.kp;
+            for (int base = 0; base < total; base += 16 * nthr) {
+                uint16_t v[16];
+#pragma unroll
+                for (int u = 0; u < 16; ++u) {
+                    const int i = base + u * nthr + tid;
+                    v[u] = 0;
+                    if (i < total) {
+                        const int ko = koff[i / tn];
+                        const int64_t n = n0 + i % tn;
+                        if (ko >= 0 && n < p.N) v[u] = __ldg(p.B + (int64_t)ko * p.ldb + n);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 16; ++u) {
+                    const int i = base + u * nthr + tid;
+                    if (i < total) reinterpret_cast<uint16_t*>(Bs)[(i % tn) * g.b_pitch + i / tn] = v[u];
+                }
             }
             cur_nb = nb;
         }
@@ -250,39 +289,51 @@ __global__ void __launch_bounds__(512) conv_mma_patch_kernel(const __grid_consta
         for (int b = 0; b < 2; ++b)
 #pragma unroll
             for (int j = 0; j < NT; ++j) acc[b][j][0] = acc[b][j][1] = acc[b][j][2] = acc[b][j][3] = 0.f;
-        const uint8_t* abase[2][2];
+        // one flat loop over the R * ksr 16-deep steps; the fragments of step ks+1 are loaded before
+        // the MMAs of step ks issue (register double buffer), so LDS latency overlaps the MMA chain
+        const uint32_t pbase = ptx::smem_u32(patch);
+        const int nks = p.cg.R * g.ksr;
+        const uint32_t row_jump = (uint32_t)(g.rowpitch - g.ksr * 32 + 32);
+        uint32_t ar = pbase, br = b_lane;
+        int jj = 0;
+        uint32_t fa[2][4], fb[NT][2];
+        auto load_frags = [&](uint32_t (&xa)[2][4], uint32_t (&xb)[NT][2], uint32_t a_at, uint32_t b_at) {
 #pragma unroll
-        for (int b = 0; b < 2; ++b)
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-                int i = warp * 32 + b * 16 + hh * 8 + gq;
-                if (i >= g.px) i = g.px - 1;         // rows past the tile compute a copy, never stored
-                const int pp = i / Q, qq = i - pp * Q;
-                abase[b][hh] = patch + (size_t)pp * p.cg.sh * g.rowpitch + (size_t)(qq * g.pix_stride + g.off0) * 2 + 4 * tq;
+            for (int nt = 0; nt < NT; ++nt) {
+                xb[nt][0] = lds32(b_at + nt * 16 * g.b_pitch);
+                xb[nt][1] = lds32(b_at + nt * 16 * g.b_pitch + 16);
             }
-        const uint8_t* bbase = Bs + (gq * g.b_pitch + 2 * tq) * 2;
-        for (int r = 0; r < p.cg.R; ++r) {
-            for (int j = 0; j < g.ksr; ++j) {
-                const int aoff = r * g.rowpitch + j * 32;
-                const int boff = (r * g.ksr + j) * 32;
-                uint32_t bf[NT][2];
 #pragma unroll
-                for (int nt = 0; nt < NT; ++nt) {
-                    const uint8_t* bp = bbase + nt * 8 * g.b_pitch * 2 + boff;
-                    bf[nt][0] = *reinterpret_cast<const uint32_t*>(bp);
-                    bf[nt][1] = *reinterpret_cast<const uint32_t*>(bp + 16);
-                }
-#pragma unroll
-                for (int b = 0; b < 2; ++b) {
-                    uint32_t a[4];
-                    a[0] = *reinterpret_cast<const uint32_t*>(abase[b][0] + aoff);
-                    a[1] = *reinterpret_cast<const uint32_t*>(abase[b][1] + aoff);
-                    a[2] = *reinterpret_cast<const uint32_t*>(abase[b][0] + aoff + 16);
-                    a[3] = *reinterpret_cast<const uint32_t*>(abase[b][1] + aoff + 16);
-#pragma unroll
-                    for (int nt = 0; nt < NT; ++nt) mma_bf16_16816(acc[b][nt], a, bf[nt]);
-                }
+            for (int b = 0; b < 2; ++b) {
+                xa[b][0] = lds32(a_at + a_off[b][0]);
+                xa[b][1] = lds32(a_at + a_off[b][1]);
+                xa[b][2] = lds32(a_at + a_off[b][0] + 16);
+                xa[b][3] = lds32(a_at + a_off[b][1] + 16);
             }
+        };
+        load_frags(fa, fb, ar, br);
+#pragma unroll 1
+        for (int ks = 0; ks < nks; ++ks) {
+            // address of step ks+1 (the last iteration re-reads step ks: harmless)
+            if (ks + 1 < nks) {
+                ++jj;
+                const bool wrap = jj == g.ksr;
+                jj = wrap ? 0 : jj;
+                ar += wrap ? row_jump : 32u;
+                br += 32u;
+            }
+            uint32_t na[2][4], nbf[NT][2];
+            load_frags(na, nbf, ar, br);
+#pragma unroll
+            for (int b = 0; b < 2; ++b)
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) mma_bf16_16816(acc[b][nt], fa[b], fb[nt]);
+#pragma unroll
+            for (int b = 0; b < 2; ++b)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) fa[b][q] = na[b][q];
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) { fb[nt][0] = nbf[nt][0]; fb[nt][1] = nbf[nt][1]; }
         }
         // ---- epilogue: consumer + one rounding, staged per warp, 16-byte stores ----
         const int rows_valid = min(g.tp, P - p0) * Q;             // pixels of this tile that exist
@@ -318,9 +369,9 @@ __global__ void __launch_bounds__(512) conv_mma_patch_kernel(const __grid_consta
                          ((reinterpret_cast<uintptr_t>(p.C) & 15) == 0);
         uint8_t* const Cb = static_cast<uint8_t*>(p.C);
         if (vec) {
-            const int vpr = row_b / 16;                            // 16-byte vectors per row
-            for (int e = lane; e < wrows * vpr; e += 32) {
-                const int rr = e / vpr, vv = e - rr * vpr;
+            const int lv = __ffs(row_b / 16) - 1;                  // log2 of the 16-byte vectors per row
+            for (int e = lane; e < (wrows << lv); e += 32) {
+                const int rr = e >> lv, vv = e - (rr << lv);
                 const uint4 w = *reinterpret_cast<const uint4*>(Os + rr * row_b + vv * 16);
                 *reinterpret_cast<uint4*>(Cb + ((m_w + rr) * p.ldc + n0) * os + vv * 16) = w;
             }
@@ -336,6 +387,9 @@ __global__ void __launch_bounds__(512) conv_mma_patch_kernel(const __grid_consta
         __syncthreads();          // patch buffer, filter and staging free for the next tile
     }
 }
+
+#undef XTC_TILE_POS
+#undef XTC_ISSUE_PATCH
 
 template <int NT>
 static cudaError_t launch_patch_nt(const CUtensorMap* tmX, const MmaParams& p, int grid, int block, int smem,

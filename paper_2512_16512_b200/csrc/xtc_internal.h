@@ -150,7 +150,7 @@ XTC_HD bool mma_patch_geom(int H, int W, int C, int P, int Q, int R, int S, int 
     g.b_pitch = g.kp + 8;                                         // elements; = 8 mod 16 -> conflict-free B fragments
     g.smem_b = (tile_n * g.b_pitch * 2 + 127) / 128 * 128;
     g.smem_out = g.warps * 32 * tile_n * out_size;
-    g.smem = g.nbuf * g.smem_patch + g.smem_b + g.smem_out + 16;  // + the two patch mbarriers
+    g.smem = g.nbuf * g.smem_patch + g.smem_b + g.smem_out + 16 + 4 * g.kp;  // + 2 mbarriers + the k table
     return g.warps <= 16;
 }
 // ------------------------------------------------------------------ plans --

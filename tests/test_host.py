@@ -489,11 +489,11 @@ def test_mma_engine_plan_and_legality():
         pr = (rows - 1) * 2 + 7
         px_w = -(-112 * rows // 32) * 32
         rnd = lambda b: -(-b // 128) * 128
-        assert info.smem_bytes == 2 * rnd(pr * 44 * 32) + rnd(16 * 232 * 2) + px_w * 16 * 2 + 16, info.smem_bytes
+        assert info.smem_bytes == 2 * rnd(pr * 44 * 32) + rnd(16 * 232 * 2) + px_w * 16 * 2 + 16 + 4 * 224, info.smem_bytes
         # pack_halo 2: thread-filled pixel slots of 4 channels, taps padded 7 -> 8, 230 slots per row, 1 buffer
         st, info2, why = xtc.xtc_schedule_check(stem, xtc.schedule(**dict(pk, tile_m=tm, pack_halo=2)), 148)
         assert st == 0 and info2.num_tiles == info.num_tiles, why
-        assert info2.smem_bytes == rnd(pr * 230 * 8) + rnd(16 * 232 * 2) + px_w * 16 * 2 + 16, info2.smem_bytes
+        assert info2.smem_bytes == rnd(pr * 230 * 8) + rnd(16 * 232 * 2) + px_w * 16 * 2 + 16 + 4 * 224, info2.smem_bytes
     for bad, frag in ((dict(tile_k=32), "tile_k"), (dict(tile_m=1024), "tile_m"), (dict(pack_halo=3), "pack_halo")):
         st, _, why = xtc.xtc_schedule_check(stem, xtc.schedule(**dict(pk, **bad)), 148)
         assert st == xtc.XTC_E_ILLEGAL_SCHEDULE and frag in why, (bad, why)
