@@ -26,7 +26,8 @@ __device__ __forceinline__ void load_row32(const void* C, bool bf16, int64_t off
                 }
             }
         } else {
-            for (int j = 0; j < ncols; ++j) o[j] = bf16_bits_to_f32(s[j]);
+            #pragma unroll
+            for (int j = 0; j < 32; ++j) if (j < ncols) o[j] = bf16_bits_to_f32(s[j]);
         }
     } else {
         const float* s = reinterpret_cast<const float*>(C) + off;
@@ -37,7 +38,8 @@ __device__ __forceinline__ void load_row32(const void* C, bool bf16, int64_t off
                 o[4 * j] = w.x; o[4 * j + 1] = w.y; o[4 * j + 2] = w.z; o[4 * j + 3] = w.w;
             }
         } else {
-            for (int j = 0; j < ncols; ++j) o[j] = s[j];
+            #pragma unroll
+            for (int j = 0; j < 32; ++j) if (j < ncols) o[j] = s[j];
         }
     }
 }

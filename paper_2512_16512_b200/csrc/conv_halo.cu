@@ -109,26 +109,6 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
         ptx::tmem_relinquish<CG>();
         ptx::tc_fence_before();
     }
-    if (CL == 2 || kclu) ptx::cluster_sync(); else __syncthreads();
-    if (warp == 2 && p.debug_late_alloc) {
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(tready);
-    } else if (warp == 2) {
-        ptx::tmem_alloc<CG>(tmem_slot, p.tmem_cols);
-        ptx::tmem_relinquish<CG>();
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(tready);
-    }
-    auto tmem_address = [&]() -> uint32_t {
-        ptx::mbar_wait(tready, 0);
-        ptx::tc_fence_after();
-        return *reinterpret_cast<volatile uint32_t*>(tmem_slot);
-    };
-    const int acc_cols = MSUB * p.tile_n;        // TMEM columns of one accumulator buffer
-    if (trace && threadIdx.x == 0) trace[1] = ptx::globaltimer();
-    int tj = 0;                                  // per-role tile counter for the trace
-
     // tile id -> (image, first output row, first output channel)
     auto decode = [&](int64_t t, int& nimg, int& p0, int& n0, int& ks) {
         int mb, nb;
@@ -164,6 +144,45 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
         }
         return t;
     };
+    // The CTA's tile walk decoded ONCE into an SMEM table (first kTileTable tiles) before the setup
+    // barrier, every thread one entry: each role then reads a tile's (image, row, channel, K range)
+    // with two LDS instead of re-running the divisions of tile_coords / decode / walk_at per tile
+    // (measured ~1100 cycles per tile per role in XTC_TRACE phase totals).
+    TileInfo* const tinfo = reinterpret_cast<TileInfo*>((reinterpret_cast<uintptr_t>(tmem_slot) + 4 + 15) & ~uintptr_t(15));
+    for (int i = threadIdx.x; i < n_walk && i < kTileTable; i += blockDim.x) {
+        TileInfo ti;
+        ti.t = (int32_t)walk_at(i, ti.kb0, ti.kb1);
+        decode(ti.t, ti.nimg, ti.p0, ti.n0, ti.ks);
+        tinfo[i] = ti;
+    }
+    if (CL == 2 || kclu) ptx::cluster_sync(); else __syncthreads();
+    if (warp == 2 && p.debug_late_alloc) {
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(tready);
+    } else if (warp == 2) {
+        ptx::tmem_alloc<CG>(tmem_slot, p.tmem_cols);
+        ptx::tmem_relinquish<CG>();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(tready);
+    }
+    auto tmem_address = [&]() -> uint32_t {
+        ptx::mbar_wait(tready, 0);
+        ptx::tc_fence_after();
+        return *reinterpret_cast<volatile uint32_t*>(tmem_slot);
+    };
+    const int acc_cols = MSUB * p.tile_n;        // TMEM columns of one accumulator buffer
+    if (trace && threadIdx.x == 0) trace[1] = ptx::globaltimer();
+    int tj = 0;                                  // per-role tile counter for the trace
+
+    auto tile_at = [tinfo, &walk_at, &decode](int64_t it, TileInfo& ti) {
+        if (it < kTileTable) {
+            ti = tinfo[it];
+        } else {
+            ti.t = (int32_t)walk_at(it, ti.kb0, ti.kb1);
+            decode(ti.t, ti.nimg, ti.p0, ti.n0, ti.ks);
+        }
+    };
     auto load_b = [&](uint8_t* dst, uint64_t* bar, int kb, int n0) {
         if (p.b3d) {
             ptx::tma_load_3d(&tmB, dst, bar, 0, kb * p.tile_k, n0 / ATOM);
@@ -189,11 +208,9 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
         uint32_t use_par = 0;
         bool first_round = true;
         for (int64_t it = 0; it < n_walk; ++it) {
-            int kb0_, kb1_;
-            const int64_t t = walk_at(it, kb0_, kb1_);
-            int nimg, p0, n0;
-            int ks;
-            decode(t, nimg, p0, n0, ks);
+            TileInfo ti;
+            tile_at(it, ti);
+            const int nimg = ti.nimg, p0 = ti.p0;
             const int cb = pb;
             const uint32_t cpar = use_par;
             const bool fresh = first_round;
@@ -247,11 +264,9 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
             uint32_t use_par = 0;
             bool first_round = true;
             for (int64_t it = 0; it < n_walk; ++it) {
-                int kb0, kb1;
-                const int64_t t = walk_at(it, kb0, kb1);
-                int nimg, p0, n0;
-                int ks;
-                decode(t, nimg, p0, n0, ks);
+                TileInfo ti;
+                tile_at(it, ti);
+                const int kb0 = ti.kb0, kb1 = ti.kb1, n0 = ti.n0;
                 for (int kb = kb0; kb < kb1; ++kb) {
                     const int cs = s;
                     const uint32_t cpar = use_par;
@@ -319,8 +334,9 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
             if (trace && lane == 0 && tj < kTraceK) trace[8 + kTraceK + tj] = ptx::globaltimer();
             ++tj;
             ptx::tc_fence_after();
-            int kb0, kb1;                             // this tile's k-block range (split_k / stream-K)
-            walk_at(it, kb0, kb1);
+            TileInfo ti;                              // this tile's k-block range (split_k / stream-K)
+            tile_at(it, ti);
+            int kb0 = ti.kb0, kb1 = ti.kb1;
             kb1 = min(kb1, kb_total);                 // (kb_total 0: diagnostics without MMAs)
             if (ptx::elect_one()) {
                 const uint32_t d0 = tmem_base + (uint32_t)(acc * acc_cols);
@@ -331,8 +347,9 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
                 int pl = j0 - tap0 * planes, sx = tap0 % R_S;
                 uint32_t aoff = (uint32_t)pl * plane16 + (uint32_t)((tap0 / R_S) * p.wp + sx) * 8u;
                 uint32_t accf = 0;                    // 0 for the tile's first UMMA (overwrite)
+                const uint32_t aoff_mask = (p.debug_skip_mma & 256) ? 0u : 0xffffffffu;   // diagnostics: no tap shifts
                 auto atom = [&](uint64_t bd) {
-                    const uint64_t ad = apatch + (uint64_t)aoff;
+                    const uint64_t ad = apatch + (uint64_t)(aoff & aoff_mask);
 #pragma unroll
                     for (int ms = 0; ms < MSUB; ++ms)
 #pragma unroll
@@ -349,6 +366,8 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
                 };
                 if (b_res) {
                     // resident filter: k-block kb of B at kb * b_stage16, atom a at a*ATOM rows
+                    const int reps = (p.debug_skip_mma & 512) ? 2 : 1;   // diagnostics: every UMMA twice
+                    for (int rep = 0; rep < reps; ++rep)
                     for (int kb = kb0; kb < kb1; ++kb) {
                         const uint64_t bd = bdesc0 + (uint64_t)((uint32_t)kb * b_stage16);
                         for (int a = 0; a < n_atoms; ++a) atom(bd + (uint64_t)(a * ATOM * 8));
@@ -393,14 +412,27 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
         uint8_t* stage = sC + q * (kTcEpiStageBytes * kTcEpiBuffers);
         const bool bf16_out = p.out_bf16 != 0;
         const int P = p.cg.P, Q = p.cg.Q;
+        // tile-invariant virtual-row -> (row, slot) splits of this warp / thread (Wp is a power of two)
+        int e_row0[MSUB], e_q0[MSUB], e_row[MSUB], e_q[MSUB];
+#pragma unroll
+        for (int ms = 0; ms < MSUB; ++ms) {
+            const int v0 = ms * 128 + 32 * q, v = v0 + lane;
+            e_row0[ms] = v0 / p.wp; e_q0[ms] = v0 % p.wp;
+            e_row[ms] = v / p.wp; e_q[ms] = v % p.wp;
+        }
+        const bool phs = trace && warp == 4 && lane == 0;      // XTC_TRACE epilogue phase totals
+        uint64_t ph_t[6] = {0, 0, 0, 0, 0, 0};
+        uint64_t ck = phs ? clock64() : 0;
+        auto lap = [&](int k) { if (phs) { const uint64_t c2 = clock64(); ph_t[k] += c2 - ck; ck = c2; } };
         for (int64_t it = 0; it < ((p.debug_skip_mma & 64) ? 0 : n_walk); ++it) {
-            int kb0, kb1;
-            const int64_t t = walk_at(it, kb0, kb1);
-            int nimg, p0, n0;
-            int ks;
-            decode(t, nimg, p0, n0, ks);
+            TileInfo ti;
+            tile_at(it, ti);
+            const int kb0 = ti.kb0, kb1 = ti.kb1, nimg = ti.nimg, p0 = ti.p0, n0 = ti.n0, ks = ti.ks;
+            const int64_t t = ti.t;
+            lap(1);
             if (p.debug_skip_mma & 128) ptx::mbar_wait_sleep(&tfull[acc], aph);
             else ptx::mbar_wait(&tfull[acc], aph);
+            lap(0);
             if (trace && warp == 4 && lane == 0 && tj < kTraceTiles) trace[8 + 2 * kTraceK + 2 * tj] = ptx::globaltimer();
             ptx::tc_fence_after();
             // stream-K (stream_k.cuh): contribution -> this CTA's slot [128*MSUB virtual rows][tile_n];
@@ -416,17 +448,18 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
                 if (trace && warp == 4 && lane == 0) trace[4] = ptx::globaltimer();
             }
             for (int ms = 0; ms < ((p.debug_skip_mma & 8) ? 0 : MSUB); ++ms) {
-                const int v0 = ms * 128 + 32 * q;              // first virtual row of this warp
-                const int prow0 = p0 + v0 / p.wp, q0 = v0 % p.wp;
-                const int v = v0 + lane;
-                const int prow = p0 + v / p.wp, qcol = v % p.wp;
+                const int v = ms * 128 + 32 * q + lane;        // this thread's virtual row
+                const int prow0 = p0 + e_row0[ms], q0 = e_q0[ms];
+                const int prow = p0 + e_row[ms], qcol = e_q[ms];
                 const bool valid = prow < P && qcol < Q;
                 const bool any_valid = prow0 < P;              // rows grow with the lane index
                 const uint32_t t_row = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * acc_cols + ms * p.tile_n);
                 for (int c = 0; c < p.tile_n; c += 32) {
                     uint32_t vals[32];
+                    lap(4);
                     ptx::tmem_ld_32x32b_x32(t_row + c, vals);
                     ptx::tmem_ld_wait();
+                    lap(2);
                     if (sk_contrib) {
                         uint4* dst = reinterpret_cast<uint4*>(p.Wk + cluster_id * p.sk_slot + (int64_t)v * p.tile_n + c);
 #pragma unroll
@@ -462,6 +495,7 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
                         if (first_half) {
                             if (lane == 0) ptx::bulk_wait_read<1>();
                             __syncwarp();
+                            lap(3);
                         }
                         uint8_t* rowp = stage + buf * kTcEpiStageBytes + lane * 128;
                         if (bf16_out) {
@@ -504,7 +538,8 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
                                     reinterpret_cast<uint4*>(dst)[j] =
                                         make_uint4(vals[4 * j], vals[4 * j + 1], vals[4 * j + 2], vals[4 * j + 3]);
                             } else {
-                                for (int j = 0; j < ncols; ++j) dst[j] = __uint_as_float(vals[j]);
+                                #pragma unroll
+                                for (int j = 0; j < 32; ++j) if (j < ncols) dst[j] = __uint_as_float(vals[j]);
                             }
                         } else if (bf16_out) {
                             uint16_t* dst = reinterpret_cast<uint16_t*>(p.C) + m * p.ldc + col0;
@@ -519,7 +554,8 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
                                     reinterpret_cast<uint4*>(dst)[j] = w;
                                 }
                             } else {
-                                for (int j = 0; j < ncols; ++j)
+                                #pragma unroll
+                                for (int j = 0; j < 32; ++j) if (j < ncols)
                                     dst[j] = (uint16_t)(ptx::pack_bf16x2(__uint_as_float(vals[j]), 0.f) & 0xFFFFu);
                             }
                         } else {
@@ -530,7 +566,8 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
                                     reinterpret_cast<uint4*>(dst)[j] =
                                         make_uint4(vals[4 * j], vals[4 * j + 1], vals[4 * j + 2], vals[4 * j + 3]);
                             } else {
-                                for (int j = 0; j < ncols; ++j) dst[j] = __uint_as_float(vals[j]);
+                                #pragma unroll
+                                for (int j = 0; j < 32; ++j) if (j < ncols) dst[j] = __uint_as_float(vals[j]);
                             }
                         }
                     }
@@ -543,6 +580,7 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
             }
             ptx::tc_fence_before();
             __syncwarp();
+            lap(4);
             if (trace && warp == 4 && lane == 0 && tj < kTraceTiles) trace[8 + 2 * kTraceK + 2 * tj + 1] = ptx::globaltimer();
             ++tj;
             if (lane == 0) {
@@ -560,6 +598,11 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
         }
         if (p.buffer_c && lane == 0) ptx::bulk_wait<0>();
         if (trace && warp == 4 && lane == 0) trace[6] = ptx::globaltimer();   // XTC_TRACE: stores complete
+        if (phs) {
+            lap(4);
+            for (int k = 0; k < 5; ++k) trace[kTracePhase + k] = ph_t[k];
+            trace[kTracePhase + 5] = (uint64_t)tj;
+        }
     }
 
     ptx::tc_fence_before();

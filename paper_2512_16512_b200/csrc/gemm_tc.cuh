@@ -710,11 +710,13 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                                 for (int j = 0; j < 8; ++j)
                                     reinterpret_cast<uint4*>(dst)[j] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
                             } else {
-                                for (int j = 0; j < ncols; ++j) dst[j] = __uint_as_float(v[j]);
+                                #pragma unroll
+                                for (int j = 0; j < 32; ++j) if (j < ncols) dst[j] = __uint_as_float(v[j]);
                             }
                         } else if (p.atomic) {
                             float* dst = reinterpret_cast<float*>(p.C) + row * p.ldc + col0;
-                            for (int j = 0; j < ncols; ++j) atomicAdd(dst + j, __uint_as_float(v[j]));
+                            #pragma unroll
+                            for (int j = 0; j < 32; ++j) if (j < ncols) atomicAdd(dst + j, __uint_as_float(v[j]));
                         } else if (bf16_out) {
                             uint16_t* dst = reinterpret_cast<uint16_t*>(p.C) + row * p.ldc + col0;
                             if (ncols == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
@@ -728,7 +730,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                                     reinterpret_cast<uint4*>(dst)[j] = w;
                                 }
                             } else {
-                                for (int j = 0; j < ncols; ++j)
+                                #pragma unroll
+                                for (int j = 0; j < 32; ++j) if (j < ncols)
                                     dst[j] = (uint16_t)(ptx::pack_bf16x2(__uint_as_float(v[j]), 0.f) & 0xFFFFu);
                             }
                         } else {
@@ -738,7 +741,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                                 for (int j = 0; j < 8; ++j)
                                     reinterpret_cast<uint4*>(dst)[j] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
                             } else {
-                                for (int j = 0; j < ncols; ++j) dst[j] = __uint_as_float(v[j]);
+                                #pragma unroll
+                                for (int j = 0; j < 32; ++j) if (j < ncols) dst[j] = __uint_as_float(v[j]);
                             }
                         }
                     }

@@ -158,6 +158,11 @@ static xtc_status plan_tc_halo(const xtc_op_desc& d, const xtc_schedule& s, int 
     if (s.unroll_k > 1) ILLEGAL("tcgen05 unroll_k must be 0 or 1");
     if (s.vector_n > 1) ILLEGAL("tcgen05 vector_n must be 0");
     if (s.stages < 2 || s.stages > 8) ILLEGAL("tcgen05 stages must be in [2,8]");
+    // producer g % pack_warps fills slot g % stages after waiting for the slot's previous round
+    // (k-block g - stages) to be consumed; its own previous wait only guarantees k-block
+    // g - pack_warps - stages, so with pack_warps > stages the slot may still be two rounds behind
+    // and the mbarrier parity wait aliases (race found by the schedule-invariance sweep)
+    if (s.pack_warps > s.stages) ILLEGAL("pack: pack_warps %d > stages %d (ring slot parity would alias)", s.pack_warps, s.stages);
     if (s.swizzle != 0 && s.swizzle != 128) ILLEGAL("tcgen05 swizzle must be 128 (0 = default 128)");
     if (d.c % p.atom_k) ILLEGAL("tcgen05 conv2d needs C %% %d == 0", p.atom_k);
     if ((d.f * es) % 16 || (d.f * os) % 16) ILLEGAL("TMA needs 16-byte row pitch for the filter and the output");
@@ -192,10 +197,10 @@ static xtc_status plan_tc_halo(const xtc_op_desc& d, const xtc_schedule& s, int 
     } else {
         b_bytes = s.stages * b_stage;
     }
-    const int64_t fixed = b_bytes + (s.buffer_c ? kTcEpiSmem : 0) + kSmemReserve;
-    // two patch buffers when they fit: measured on B200, a third buffer in flight slows the
-    // tile (its TMA writes compete with the UMMA operand reads for the SMEM port)
-    int nbuf = 2;
+    const int64_t fixed = b_bytes + (s.buffer_c ? kTcEpiSmem : 0) + kSmemReserve + kTileTableBytes;
+    // three patch buffers when they fit (A/B on B200 after the epilogue de-spill, tools/halo_nbuf_ab.py:
+    // L56 N=32 22.06 -> 21.65 us, L14 N=32 19.44 -> 19.26 us), else two, else one
+    int nbuf = 3;
     if (const char* e = getenv("XTC_HALO_NBUF")) nbuf = std::max(1, std::min(kHaloMaxPatchBufs, atoi(e)));   // diagnostics
     while (nbuf > 1 && fixed + nbuf * patch > kSmemMaxOptin) --nbuf;
     if (fixed + nbuf * patch > kSmemMaxOptin)
@@ -366,6 +371,11 @@ static xtc_status plan_tc(const xtc_op_desc& d, const xtc_schedule& s, int num_s
     if (s.pack_warps < 0 || s.pack_warps > 3) ILLEGAL("pack: pack_warps (TMA-issuing warps) must be in [0,3]");
     if (s.vector_n > 1) ILLEGAL("tcgen05 vector_n must be 0 (the UMMA atom is the vector unit)");
     if (s.stages < 2 || s.stages > 8) ILLEGAL("tcgen05 stages must be in [2,8]");
+    // producer g % pack_warps fills slot g % stages after waiting for the slot's previous round
+    // (k-block g - stages) to be consumed; its own previous wait only guarantees k-block
+    // g - pack_warps - stages, so with pack_warps > stages the slot may still be two rounds behind
+    // and the mbarrier parity wait aliases (race found by the schedule-invariance sweep)
+    if (s.pack_warps > s.stages) ILLEGAL("pack: pack_warps %d > stages %d (ring slot parity would alias)", s.pack_warps, s.stages);
     if (s.swizzle != 0 && s.swizzle != 128) ILLEGAL("tcgen05 swizzle must be 128 (0 = default 128)");
     int accb = s.acc_buffers == 0 ? 1 : s.acc_buffers;
     if (accb < 1 || accb > 2) ILLEGAL("acc_buffers must be 1 or 2");

@@ -23,7 +23,7 @@ constexpr int kTcThreads = 256;             // warp0 TMA, warp1 MMA, warp2 TMEM 
 constexpr int kTcEpiStageBytes = 4096;      // one warp's 32 rows x 128 B output staging chunk
 constexpr int kTcEpiBuffers = 2;            // double-buffered per warp
 constexpr int kTcEpiSmem = 4 * kTcEpiStageBytes * kTcEpiBuffers;
-constexpr int kHaloMaxPatchBufs = 2;        // conv_halo: patch buffers (at most; the planner fits what SMEM allows)
+constexpr int kHaloMaxPatchBufs = 4;        // conv_halo: patch buffers (at most; the planner fits what SMEM allows)
 constexpr int kHaloMaxResidentKb = 32;      // conv_halo: resident-filter k-blocks (one mbarrier each)
 constexpr int kSplitClusterMaxCtas = 16;    // split_k_mode 2: K segments per cluster (> 8: non-portable size)
 constexpr int kSkMaxCtas = 4096;            // split_k_mode 3: stream-K grid limit (publish flags per op)
@@ -239,7 +239,8 @@ struct TcParams {
     int32_t debug_late_alloc;  // diagnostics (A/B): XTC_DEBUG_LATE_ALLOC=1 allocates TMEM before the
                                // prologue barrier, i.e. the producers wait for the allocation
     int32_t debug_skip_mma;  // diagnostics only, output invalid: XTC_DEBUG_SKIP_MMA, or XTC_DEBUG_SKIP=mask
-                             // (conv_halo: 1 no MMAs, 2 no patch TMA, 4 no output stores)
+                             // (conv_halo: 1 no MMAs, 2 no patch TMA, 4 no output stores, 8 no TMEM drain,
+                             // 256 no tap shifts, 512 every UMMA twice)
     int64_t ldc, ws_ld;
     void* C; float* Wk;
     uint32_t idesc;
@@ -279,10 +280,19 @@ struct TcParams {
     uint32_t* sk_flags;
     uint32_t sk_epoch;
 };
+// conv_halo: the first kTileTable tiles of a CTA's walk, decoded once into SMEM (after the barriers)
+struct TileInfo {
+    int32_t t, nimg, p0, n0, ks, kb0, kb1, pad;
+};
+constexpr int kTileTable = 64;
+constexpr int kTileTableBytes = kTileTable * (int)sizeof(TileInfo) + 16;
 constexpr int kTraceCtas = 160;          // >= #SMs: the whole persistent grid
 constexpr int kTraceK = 96;
 constexpr int kTraceTiles = 16;
-constexpr int kTraceSlots = 8 + 2 * kTraceK + 2 * kTraceTiles;
+constexpr int kTracePhase = 8 + 2 * kTraceK + 2 * kTraceTiles;   // conv_halo epilogue phase cycle totals (warp 4):
+                                                                   // +0 tfull wait, +1 tile decode, +2 TMEM ld+wait,
+                                                                   // +3 staging-buffer wait, +4 stage+store, +5 tiles
+constexpr int kTraceSlots = kTracePhase + 8;
 
 // Validation of the consumer (harness.cu compare_kernel): bits, bias, and the snapshot of
 // the output taken before the validated run (XTC_CONSUMER_ACCUMULATE; same layout as C).

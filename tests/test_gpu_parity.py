@@ -473,6 +473,9 @@ def test_schedule_invariance_tcgen05_sampled():
     for i, c in enumerate(cands[:32]):
         d = c.as_dict()
         d["pack_warps"] = 1 + i % 3
+        if d["pack_warps"] > d["stages"]:          # illegal: ring-slot parity aliasing (planner rule)
+            assert xtc.xtc_schedule_check(desc, xtc.schedule(**d), 148)[0] == xtc.XTC_E_ILLEGAL_SCHEDULE
+            d["pack_warps"] = d["stages"]
         extra.append(xtc.schedule(**d))
     n = _invariance(desc, "bf16", "bf16", cands + extra)
     assert n == 160

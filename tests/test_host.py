@@ -153,7 +153,8 @@ def test_pack_halo_plan():
     assert st == xtc.XTC_OK, why
     assert info.num_tiles == 32 * 28 and info.grid_x == 148 and info.tmem_cols == 128
     # resident filter 9 x 8 KiB + 2 patches of 4 rows x 64 slots x 128 B + epilogue staging
-    assert info.smem_bytes == 9 * 8192 + 2 * 4 * 64 * 128 + 32768 + 2048
+    # resident filter + 3 patch buffers + epilogue staging + barriers + the SMEM tile table (64 x 32 B + 16)
+    assert info.smem_bytes == 9 * 8192 + 3 * 4 * 64 * 128 + 32768 + 2048 + 64 * 32 + 16
     st, info, why = chk(l56, **dict(HALO, tile_m=256, b_resident=1))
     assert st == xtc.XTC_OK and info.num_tiles == 32 * 14 and info.tmem_cols == 256, why
     l14 = xtc.conv2d_desc(32, 14, 14, 256, 256)
@@ -620,3 +621,14 @@ def test_sweep_resume_matches_the_full_key(tmp_path):
     p.write_text(json.dumps({"id": 0, "seed": 0, "tflops_med": 1.0}) + "\n")   # the round-1 format
     with pytest.raises(ValueError):
         load_resume(str(p), k1)
+
+
+def test_pack_warps_bounded_by_stages():
+    """pack_warps producers rotate over the ring; a producer only knows k-block g - pack_warps - stages
+    was consumed, so pack_warps > stages could refill a slot two rounds behind (parity aliasing)."""
+    d = xtc.matmul_desc(512, 512, 512)
+    base = dict(engine=1, tile_m=256, tile_n=64, tile_k=64, swizzle=128, buffer_c=1, acc_buffers=2)
+    st, _, why = xtc.xtc_schedule_check(d, xtc.schedule(**dict(base, stages=2, pack_warps=3)), 148)
+    assert st == xtc.XTC_E_ILLEGAL_SCHEDULE and "pack_warps" in why, why
+    for stages, pw in ((2, 2), (3, 3), (4, 3)):
+        assert xtc.xtc_schedule_check(d, xtc.schedule(**dict(base, stages=stages, pack_warps=pw)), 148)[0] == 0

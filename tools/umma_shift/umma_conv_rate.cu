@@ -1,0 +1,97 @@
+// Microbenchmark: the conv_halo L56 UMMA stream in isolation -- M=128, N=64, K=16 bf16 UMMAs, 9 taps x 4
+// k-steps per "tile", A = a 4-row x 64-slot patch viewed at row shift r*64 + s, B = a resident 9 x 8 KB
+// filter (MN-major, SW128) -- with zero or random operand data, one CTA per SM, cycles per UMMA.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O2 -std=c++17 -I../../paper_2512_16512_b200/csrc umma_conv_rate.cu
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstdint>
+#include "ptx.cuh"
+using namespace xtc;
+constexpr int TILES = 64;
+__global__ void __launch_bounds__(256, 1) k_conv(int n, int random, int taps_mode, int commits, unsigned long long* cyc) {
+    extern __shared__ uint8_t raw[];
+    const uint32_t pad = (1024u - (ptx::smem_u32(raw) & 1023u)) & 1023u;
+    uint8_t* sm = raw + pad;
+    uint8_t* sA = sm;                          // 320 rows x 128 B
+    uint8_t* sB = sm + 320 * 128;              // 9 taps x 64 k x 128 B (N = 64 bf16)
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sB + 9 * 64 * 128);
+    uint64_t* tb = bar + 1;                    // per-tile commit barriers (2, by tile parity)
+    uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 4);
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int words = (320 * 128 + 9 * 64 * 128) / 4;
+    for (int i = tid; i < words; i += blockDim.x) {
+        uint32_t h = (uint32_t)i * 2654435761u ^ 0x9e3779b9u;
+        h ^= h >> 13; h *= 0x5bd1e995u; h ^= h >> 15;
+        // bf16 pairs with exponent near 1.0 and random mantissa/sign
+        const uint32_t lo = 0x3f00u | (h & 0x80ffu), hi = 0x3f00u | ((h >> 16) & 0x80ffu);
+        reinterpret_cast<uint32_t*>(sm)[i] = random ? (lo | (hi << 16)) : 0u;
+    }
+    ptx::fence_proxy_async_smem();
+    if (tid == 0) { ptx::mbar_init(bar, 1); ptx::mbar_init(&tb[0], 1); ptx::mbar_init(&tb[1], 1); ptx::fence_mbarrier_init(); }
+    if (warp == 0) { ptx::tmem_alloc<1>(slot, 256); ptx::tmem_relinquish<1>(); }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *slot;
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(n >> 3) << 17) | ((128u >> 4) << 24);
+    if (warp == 1) {
+        const uint64_t ad0 = ptx::smem_desc_sw128(ptx::smem_u32(sA), 16, 1024);
+        const uint64_t bd0 = ptx::smem_desc_sw128(ptx::smem_u32(sB), 64 * 128, 1024, 2);
+        __syncwarp();
+        const unsigned long long t0 = clock64();
+        if (ptx::elect_one()) {
+            for (int t = 0; t < TILES; ++t) {
+                const uint32_t d = tmem + (uint32_t)((t & 1) * 64);
+                for (int tap = 0; tap < 9; ++tap) {
+                    const int shift = taps_mode ? (tap / 3) * 64 + (tap % 3) : 0;
+                    const uint64_t ad = ad0 + (uint64_t)(shift * 8);
+                    const uint64_t bd = bd0 + (uint64_t)(tap * 64 * 128 / 16);
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk)
+                        ptx::umma<false, 1>(d, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 16 * 8), idesc,
+                                            (tap | kk) ? 1u : 0u);
+                }
+                if (commits) ptx::umma_commit<1>(&tb[t & 1]);   // like the conv kernel: pempty / tfull per tile
+                if (commits > 1) ptx::umma_commit<1>(&tb[t & 1]);
+            }
+            ptx::umma_commit<1>(bar);
+        }
+        __syncwarp();
+        ptx::mbar_wait(bar, 0);
+        const unsigned long long t1 = clock64();
+        if ((tid & 31) == 0) cyc[blockIdx.x] = t1 - t0;
+    } else if (commits && warp >= 4) {
+        // epilogue-like warps: poll the per-tile commit barriers (like the tfull waits) until the end
+        const uint32_t a0 = ptx::smem_u32(&tb[0]), a1 = ptx::smem_u32(&tb[1]), ab = ptx::smem_u32(bar);
+        while (!ptx::mbar_try_wait(ab, 0)) { ptx::mbar_try_wait(a0, 0); ptx::mbar_try_wait(a1, 0); }
+    } else {
+        ptx::mbar_wait(bar, 0);
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) { ptx::tc_fence_after(); ptx::tmem_dealloc<1>(tmem, 256); }
+}
+int main() {
+    unsigned long long* d;
+    cudaMalloc(&d, 148 * sizeof(unsigned long long));
+    const int smem = 320 * 128 + 9 * 64 * 128 + 128 + 1024;
+    cudaFuncSetAttribute(k_conv, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    unsigned long long h[148];
+    printf("N   data    taps        cycles/UMMA (median CTA over 148)   floor = 128*N/256\n");
+    for (int n : {64})
+        for (int rnd : {1})
+            for (int cm : {0, 1, 2})
+            for (int tm : {0, 1}) {
+                k_conv<<<148, 256, smem>>>(n, rnd, tm, cm, d);
+                cudaError_t e = cudaDeviceSynchronize();
+                if (e != cudaSuccess) { printf("CUDA error %s\n", cudaGetErrorString(e)); return 1; }
+                cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
+                for (int i = 0; i < 148; ++i)
+                    for (int j = i + 1; j < 148; ++j)
+                        if (h[j] < h[i]) { unsigned long long t = h[i]; h[i] = h[j]; h[j] = t; }
+                printf("%-3d %-7s %-11s commits/tile %d  %-20.1f %d\n", n, rnd ? "random" : "zeros", tm ? "conv shifts" : "no shift", cm,
+                       (double)h[74] / (TILES * 36), 128 * n / 256);
+            }
+    return 0;
+}
