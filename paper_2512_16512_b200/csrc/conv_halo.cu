@@ -30,7 +30,10 @@
 
 namespace xtc {
 
-template <bool TF32, int MSUB, int CL, bool PAIR = false>
+// LEAN: the split-free variant (no split_k partials, no cluster split-K, no stream-K): those paths
+// are compiled out, which shrinks the code the per-tile roles walk (ncu: 18 % of the L56 kernel's
+// warp samples were stalled on instruction fetch, 'no_instructions', in the full variant)
+template <bool TF32, int MSUB, int CL, bool PAIR = false, bool LEAN = false>
 __global__ void __launch_bounds__(kTcThreads, 1)
 tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmY, const TcParams p) {
@@ -71,7 +74,7 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
     const uint32_t rank = (CL == 2) ? ptx::cluster_ctarank() : 0u;
     // cluster split-K (split_k_mode XTC_SPLITK_CLUSTER, CL = 1): the ksc CTAs of a cluster run
     // the ksc K segments (runs of filter taps / channel planes) of one output tile
-    const int ksc = (CL == 1 && p.ksc > 1) ? p.ksc : 1;
+    const int ksc = (!LEAN && CL == 1 && p.ksc > 1) ? p.ksc : 1;
     const bool kclu = ksc > 1;
     const uint32_t krank = kclu ? ptx::cluster_ctarank() : 0u;
     const int64_t cluster_id = blockIdx.x / (CL * ksc);
@@ -121,7 +124,7 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
     };
     // the tiles this CTA visits and the k-block range of each: data-parallel (strided over the tile
     // map; K segment from the split or the cluster rank), or stream-K (stream_k.cuh)
-    const bool sk = p.sk != 0;
+    const bool sk = !LEAN && p.sk != 0;
     int64_t sk_s = 0, sk_e = 0;
     if (sk) sk_range(p.sk_iters, num_clusters, cluster_id, sk_s, sk_e);
     const int64_t n_walk = sk ? (sk_e > sk_s ? (sk_e - 1) / p.kb_total - sk_s / p.kb_total + 1 : 0)
@@ -171,7 +174,8 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
         ptx::tc_fence_after();
         return *reinterpret_cast<volatile uint32_t*>(tmem_slot);
     };
-    const int acc_cols = MSUB * p.tile_n;        // TMEM columns of one accumulator buffer
+    const int sfold = p.sfold > 1 ? p.sfold : 1;  // s-fold: accumulator blocks s = 0..S-1 of tile_n columns
+    const int acc_cols = MSUB * p.tile_n * sfold;  // TMEM columns of one accumulator buffer
     if (trace && threadIdx.x == 0) trace[1] = ptx::globaltimer();
     int tj = 0;                                  // per-role tile counter for the trace
 
@@ -328,9 +332,12 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
         const int nbuf = p.nbuf, accb = p.acc_buffers;
         if (b_res && !(PAIR && rank != 0))            // the resident filter (per-k-block barriers)
             for (int kb = 0; kb < p.kb_total; ++kb) ptx::mbar_wait(&bfull[kb], 0);
+        const bool mphs = trace && lane == 0;          // XTC_TRACE: MMA-warp wait / issue cycle totals
+        uint64_t m_wait = 0, m_issue = 0, mck = mphs ? clock64() : 0;
         for (int64_t it = 0; it < ((PAIR && rank != 0) ? 0 : n_walk); ++it) {
             if (wait_tempty) ptx::mbar_wait(&tempty[acc], aph ^ 1u);
             ptx::mbar_wait(&pfull[pb], pph);
+            if (mphs) { const uint64_t c2 = clock64(); m_wait += c2 - mck; mck = c2; }
             if (trace && lane == 0 && tj < kTraceK) trace[8 + kTraceK + tj] = ptx::globaltimer();
             ++tj;
             ptx::tc_fence_after();
@@ -364,7 +371,25 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
                     sx = sw ? 0 : sx;
                     aoff += pw ? (sw ? d_row : d_col) : d_plane;
                 };
-                if (b_res) {
+                if (sfold > 1 && kb1 > kb0) {
+                    // s-fold: per filter row r, channel plane pl and 16-deep step kk ONE UMMA of N = S x
+                    // tile_n on the patch view of row r (no s shift); its B operand is the row's S resident
+                    // taps, N blocks C x 128 bytes apart (row (r*S + s)*C + c of the RSCF filter)
+                    const uint64_t bfold = ptx::smem_desc_sw128(ptx::smem_u32(sB), (uint32_t)p.cg.C * 128u, 1024, 2);
+                    const int R_R = ptx::pin(p.cg.R), C_ = ptx::pin(p.cg.C);
+                    for (int r = 0; r < R_R; ++r) {
+                        const uint64_t ar = apatch + (uint64_t)((uint32_t)r * (uint32_t)p.wp * 8u);
+                        const uint64_t brow = bfold + (uint64_t)((uint32_t)(r * R_S * C_) * 8u);
+                        for (int pl2 = 0; pl2 < planes; ++pl2) {
+                            const uint64_t ad = ar + (uint64_t)((uint32_t)pl2 * plane16);
+                            const uint64_t bd = brow + (uint64_t)((uint32_t)(pl2 * ATOM) * 8u);
+#pragma unroll
+                            for (int kk = 0; kk < ATOM / UMMA_K; ++kk)
+                                ptx::umma<TF32, CG>(d0, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * UMMA_K * 8), idesc,
+                                                   (r | pl2 | kk) ? 1u : 0u);
+                        }
+                    }
+                } else if (b_res) {
                     // resident filter: k-block kb of B at kb * b_stage16, atom a at a*ATOM rows
                     const int reps = (p.debug_skip_mma & 512) ? 2 : 1;   // diagnostics: every UMMA twice
                     for (int rep = 0; rep < reps; ++rep)
@@ -395,6 +420,11 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
                 }
             }
             __syncwarp();
+            if (mphs) {
+                const uint64_t c2 = clock64();
+                m_issue += c2 - mck; mck = c2;
+                trace[kTracePhase + 6] = m_wait; trace[kTracePhase + 7] = m_issue;
+            }
             if (!b_res)                               // every lane advances the ring by the segment's slots
                 for (int kb = kb0; kb < kb1; ++kb)
                     if (++s == S) { s = 0; ph ^= 1u; }
@@ -412,6 +442,10 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
         uint8_t* stage = sC + q * (kTcEpiStageBytes * kTcEpiBuffers);
         const bool bf16_out = p.out_bf16 != 0;
         const int P = p.cg.P, Q = p.cg.Q;
+        // s-fold exchange: [round parity][warp][row s(s-1)/2 + i][32 fp32] after the SMEM tile table
+        float* const xbuf = reinterpret_cast<float*>(tinfo + kTileTable);
+        const int xrows = sfold * (sfold - 1) / 2;
+        uint32_t xround = 0;
         // tile-invariant virtual-row -> (row, slot) splits of this warp / thread (Wp is a power of two)
         int e_row0[MSUB], e_q0[MSUB], e_row[MSUB], e_q[MSUB];
 #pragma unroll
@@ -459,6 +493,54 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
                     lap(4);
                     ptx::tmem_ld_32x32b_x32(t_row + c, vals);
                     ptx::tmem_ld_wait();
+                    if (sfold > 1) {
+                        // s-fold: + block sx of virtual row v + sx, sx = 1..S-1 (S <= 4) in ascending order.
+                        // All blocks are loaded and the rows the warp below needs (its last lanes' v + sx =
+                        // this warp's rows 0..sx-1) published before ONE named barrier per chunk; rows of
+                        // this warp come by shuffle.  Only when an output row spans warps (Wp > 32); else
+                        // those lanes' slots are >= Q and never stored.
+                        const bool xchg = p.wp > 32;
+                        float* xb = xbuf + (size_t)(((xround & 1) * 4) * xrows) * 32;
+                        ++xround;
+                        uint32_t wb[3][32];
+#pragma unroll
+                        for (int sx = 1; sx < 4; ++sx)
+                            if (sx < sfold) ptx::tmem_ld_32x32b_x32(t_row + (uint32_t)(sx * p.tile_n) + c, wb[sx - 1]);
+                        ptx::tmem_ld_wait();
+                        if (xchg) {
+#pragma unroll
+                            for (int sx = 1; sx < 4; ++sx)
+                                if (sx < sfold && q > 0 && lane < sx) {
+                                    float4* dst = reinterpret_cast<float4*>(
+                                        xb + (size_t)(((q - 1) * xrows) + sx * (sx - 1) / 2 + lane) * 32);
+#pragma unroll
+                                    for (int j = 0; j < 8; ++j)
+                                        dst[j] = make_float4(__uint_as_float(wb[sx - 1][4 * j]), __uint_as_float(wb[sx - 1][4 * j + 1]),
+                                                             __uint_as_float(wb[sx - 1][4 * j + 2]), __uint_as_float(wb[sx - 1][4 * j + 3]));
+                                }
+                            ptx::named_bar_sync(3, 128);
+                        }
+#pragma unroll
+                        for (int sx = 1; sx < 4; ++sx) {
+                            if (sx >= sfold) break;
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                wb[sx - 1][j] = __float_as_uint(__shfl_down_sync(0xffffffffu, __uint_as_float(wb[sx - 1][j]), sx));
+                            if (xchg && q < 3 && lane >= 32 - sx) {          // divergent: the last sx lanes
+                                const float4* src = reinterpret_cast<const float4*>(
+                                    xb + (size_t)((q * xrows) + sx * (sx - 1) / 2 + (lane - (32 - sx))) * 32);
+#pragma unroll
+                                for (int j = 0; j < 8; ++j) {
+                                    const float4 o = src[j];
+                                    wb[sx - 1][4 * j] = __float_as_uint(o.x); wb[sx - 1][4 * j + 1] = __float_as_uint(o.y);
+                                    wb[sx - 1][4 * j + 2] = __float_as_uint(o.z); wb[sx - 1][4 * j + 3] = __float_as_uint(o.w);
+                                }
+                            }
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                vals[j] = __float_as_uint(__uint_as_float(vals[j]) + __uint_as_float(wb[sx - 1][j]));
+                        }
+                    }
                     lap(2);
                     if (sk_contrib) {
                         uint4* dst = reinterpret_cast<uint4*>(p.Wk + cluster_id * p.sk_slot + (int64_t)v * p.tile_n + c);
@@ -530,7 +612,7 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
                         const int64_t m = ((int64_t)nimg * P + prow) * Q + qcol;
                         const int64_t col0 = (int64_t)n0 + c;
                         const int ncols = (int)((p.N - col0) < 32 ? (p.N - col0) : 32);
-                        if (p.split_out) {                  // split_k: this segment's fp32 partial sums
+                        if (!LEAN && p.split_out) {         // split_k: this segment's fp32 partial sums
                             float* dst = p.Wk + ((int64_t)ks * p.M + m) * p.ws_ld + col0;
                             if (ncols == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
 #pragma unroll
@@ -618,7 +700,9 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
 template <bool TF32, int MSUB, int CL, bool PAIR = false>
 static cudaError_t launch_halo_t(const CUtensorMap& x, const CUtensorMap& b, const CUtensorMap& y, const TcParams& p,
                                  int grid, int smem, cudaStream_t st) {
-    auto k = tc_conv_halo_kernel<TF32, MSUB, CL, PAIR>;
+    // the lean variant for split-free bf16 plans (the BASELINE layers' schedules)
+    const bool lean = !TF32 && !p.sk && p.ksc <= 1 && !p.split_out && !p.atomic;
+    auto k = lean ? tc_conv_halo_kernel<TF32, MSUB, CL, PAIR, !TF32> : tc_conv_halo_kernel<TF32, MSUB, CL, PAIR, false>;
     cudaError_t e = ensure_smem_attr(k, smem);
     if (e != cudaSuccess) return e;
     const int ksc = (CL == 1 && p.ksc > 1) ? p.ksc : 1;

@@ -150,7 +150,24 @@ static xtc_status plan_tc_halo(const xtc_op_desc& d, const xtc_schedule& s, int 
             ILLEGAL("pack_halo: the CTA pair needs tile_n %% %d == 0 (a 128-byte filter block per CTA)", 2 * p.atom_n);
         if (d.f % p.atom_n) ILLEGAL("pack_halo: the CTA pair needs F %% %d == 0 (3-D filter TMA)", p.atom_n);
     }
-    if (s.inner_n != 0 && s.inner_n != s.tile_n) ILLEGAL("tcgen05 inner_n (UMMA N) must equal tile_n");
+    // inner_n = S * tile_n: the s-fold.  The S taps (r, 0..S-1) of a filter row are the N blocks of
+    // ONE UMMA on the patch view of row r (N = S * tile_n): accumulator block s of virtual row v
+    // holds sum_c x[v + r*Wp + s][c] w[r][s][c][:] minus the s shift, which the epilogue applies by
+    // adding block s of row v + s.  A is read once per filter row instead of once per tap.
+    int sfold = 1;
+    if (s.inner_n != 0 && s.inner_n != s.tile_n) {
+        if (s.inner_n != d.s * s.tile_n || d.s < 2)
+            ILLEGAL("pack_halo: inner_n (UMMA N) must be tile_n, or S x tile_n (s-fold, S >= 2)");
+        if (s.inner_n > 256) ILLEGAL("pack_halo s-fold: UMMA N = S x tile_n = %d exceeds 256", s.inner_n);
+        if (pair || hcl != 1 || s.tile_m != 128)
+            ILLEGAL("pack_halo s-fold: one CTA per 128-row tile (cluster_m 1, tile_m 128, inner_m 128)");
+        if (p.split_k > 1 || p.stream_k) ILLEGAL("pack_halo s-fold: split_k must be 1 (the fold sums whole filter rows)");
+        if (s.b_resident != 1) ILLEGAL("pack_halo s-fold: b_resident must be 1 (taps of a row are one strided B operand)");
+        if (s.tile_n != p.atom_n) ILLEGAL("pack_halo s-fold: tile_n must be %d (one 128-byte filter block per tap)", p.atom_n);
+        if (d.in_dtype != XTC_BF16) ILLEGAL("pack_halo s-fold: bf16 inputs (kind::f16)");
+        if (d.c % s.tile_k) ILLEGAL("pack_halo s-fold: tile_k must divide C (whole k-blocks per tap)");
+        sfold = (int)d.s;
+    }
     if (s.tile_n < p.atom_n || s.tile_n > 256 || s.tile_n % p.atom_n)
         ILLEGAL("tcgen05 tile_n must be a multiple of %d in [%d,256]", p.atom_n, p.atom_n);
     if (s.tile_k < p.atom_k || s.tile_k > 256 || s.tile_k % p.atom_k)
@@ -179,7 +196,7 @@ static xtc_status plan_tc_halo(const xtc_op_desc& d, const xtc_schedule& s, int 
     const int accb = s.acc_buffers == 0 ? 1 : s.acc_buffers;
     if (accb < 1 || accb > 2) ILLEGAL("acc_buffers must be 1 or 2");
     int alloc = 32;
-    while (alloc < accb * msub * s.tile_n) alloc *= 2;
+    while (alloc < accb * msub * s.tile_n * sfold) alloc *= 2;
     if (alloc > 512) ILLEGAL("bufferize: %d TMEM columns (acc_buffers x tile_m/128 x tile_n) exceed 512", alloc);
     p.tmem_cols = alloc;
     const int64_t planes = d.c / p.atom_k;
@@ -197,7 +214,10 @@ static xtc_status plan_tc_halo(const xtc_op_desc& d, const xtc_schedule& s, int 
     } else {
         b_bytes = s.stages * b_stage;
     }
-    const int64_t fixed = b_bytes + (s.buffer_c ? kTcEpiSmem : 0) + kSmemReserve + kTileTableBytes;
+    // s-fold: per epilogue warp and chunk parity, rows 0..s-1 of accumulator blocks s = 1..S-1 for the
+    // warp above (the rows v + s of its last lanes), 32 fp32 each
+    const int64_t xbytes = sfold > 1 ? 4LL * 2 * (sfold * (sfold - 1) / 2) * 128 : 0;
+    const int64_t fixed = b_bytes + (s.buffer_c ? kTcEpiSmem : 0) + kSmemReserve + kTileTableBytes + xbytes;
     // three patch buffers when they fit (A/B on B200 after the epilogue de-spill, tools/halo_nbuf_ab.py:
     // L56 N=32 22.06 -> 21.65 us, L14 N=32 19.44 -> 19.26 us), else two, else one
     int nbuf = 3;
@@ -236,6 +256,7 @@ static xtc_status plan_tc_halo(const xtc_op_desc& d, const xtc_schedule& s, int 
     p.num_tiles = (int64_t)p.tiles_m * p.tiles_n * p.split_k;
     if (p.num_tiles >= (1ll << 31)) ILLEGAL("too many tiles");
     p.halo_pair = pair;
+    p.halo_sfold = sfold;
     p.cta_group = pair ? 2 : 1;                         // UMMA M = 128 * cta_group (abi.cu idesc)
     p.block = kTcThreads;
     p.cluster = hcl;

@@ -186,6 +186,7 @@ struct Plan {
     int32_t halo_wp = 0, halo_rt = 0, halo_msub = 0, halo_pr = 0, halo_planes = 0, halo_nbuf = 0, halo_tpi = 0;
     int32_t halo_cl = 1;                // CTAs per cluster sharing the filter stream (TMA multicast, or a pair)
     bool halo_pair = false;             // inner_m 256: cta_group::2 UMMAs (M = 256) over a CTA pair
+    int32_t halo_sfold = 1;             // inner_n = S * tile_n: the filter row's S taps folded into the UMMA N
     bool ovl = false;                   // overlapped epilogue (see TcParams::ovl); 64 KB epilogue SMEM
     int32_t msub = 1;                   // tcgen05 matmul: 128-row M-subtiles per CTA (tile_m = 128*cta_group*msub)
     bool stream_k = false;              // split_k_mode 3: stream-K over the persistent grid (stream_k.cuh)
@@ -250,6 +251,8 @@ struct TcParams {
     ConvGeom cg;
     // pack_halo conv only (see Plan)
     int32_t wp, rt, msub, planes, nbuf, tpi, cl, pair;
+    int32_t sfold;           // pack_halo s-fold: the S taps of a filter row are the N blocks of one UMMA
+                             // (N = S * tile_n); the epilogue sums block s of row v + s (1 = off)
     int32_t cn;              // cluster_n: CTAs of a cluster on adjacent N tiles, A stages multicast (1 = none)
     int32_t ms;              // M-subtiles per CTA (tile_m = 128 * cta_group * ms; matmul: 1 or 2)
     int32_t ovl;             // overlapped epilogue (two M-subtiles, bf16, tile_n 256): subtile 1 drained to a
@@ -291,7 +294,8 @@ constexpr int kTraceK = 96;
 constexpr int kTraceTiles = 16;
 constexpr int kTracePhase = 8 + 2 * kTraceK + 2 * kTraceTiles;   // conv_halo epilogue phase cycle totals (warp 4):
                                                                    // +0 tfull wait, +1 tile decode, +2 TMEM ld+wait,
-                                                                   // +3 staging-buffer wait, +4 stage+store, +5 tiles
+                                                                   // +3 staging-buffer wait, +4 stage+store, +5 tiles;
+                                                                   // MMA warp: +6 wait cycles, +7 issue cycles
 constexpr int kTraceSlots = kTracePhase + 8;
 
 // Validation of the consumer (harness.cu compare_kernel): bits, bias, and the snapshot of

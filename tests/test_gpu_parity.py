@@ -189,6 +189,17 @@ HALO_CASES = [
     ((1, 14, 14, 256, 256, 3, 3, 1, "bf16", "bf16"), dict(tile_n=128, stages=4, split_k=3, buffer_c=0)),
     ((1, 14, 14, 256, 256, 3, 3, 1, "bf16", "bf16"), dict(tile_n=128, stages=4, split_k=9, buffer_c=0)),
     ((1, 56, 56, 64, 64, 3, 3, 1, "bf16", "f32"), dict(tile_n=64, stages=2, split_k=3, buffer_c=0, b_resident=1)),
+    # s-fold (inner_n = S x tile_n): a filter row's S taps as the N blocks of one UMMA, the s shift applied in
+    # the epilogue -- Wp 64 (output rows span two epilogue warps: cross-warp exchange), Wp 16 / 32 (no
+    # exchange), Wp 128, S = 2 and 4, 2 channel planes, ragged P / Q, direct stores, many tiles per CTA
+    ((4, 56, 56, 64, 64, 3, 3, 1, "bf16", "bf16"), dict(tile_n=64, inner_n=192, b_resident=1, stages=2)),
+    ((2, 30, 27, 64, 64, 3, 3, 1, "bf16", "f32"), dict(tile_n=64, inner_n=192, b_resident=1, stages=2, buffer_c=0)),
+    ((3, 14, 14, 128, 64, 3, 3, 1, "bf16", "bf16"), dict(tile_n=64, inner_n=192, b_resident=1, stages=2)),
+    ((2, 20, 21, 64, 64, 3, 4, 2, "bf16", "bf16"), dict(tile_n=64, inner_n=256, b_resident=1, stages=2)),
+    ((2, 12, 100, 64, 64, 2, 2, 0, "bf16", "f32"), dict(tile_n=64, inner_n=128, b_resident=1, stages=2,
+                                                        acc_buffers=1)),
+    ((2, 56, 56, 64, 64, 3, 3, 1, "bf16", "bf16"), dict(tile_n=64, inner_n=192, b_resident=1, stages=2,
+                                                        persistent=1, grid_sms=5)),
 ]
 
 

@@ -632,3 +632,22 @@ def test_pack_warps_bounded_by_stages():
     assert st == xtc.XTC_E_ILLEGAL_SCHEDULE and "pack_warps" in why, why
     for stages, pw in ((2, 2), (3, 3), (4, 3)):
         assert xtc.xtc_schedule_check(d, xtc.schedule(**dict(base, stages=stages, pack_warps=pw)), 148)[0] == 0
+
+
+def test_pack_halo_sfold_plan_and_legality():
+    """inner_n = S x tile_n folds a filter row's S taps into one UMMA (TMEM: S accumulator blocks)."""
+    d = xtc.conv2d_desc(32, 56, 56, 64, 64, 3, 3, 1, 1)
+    base = dict(engine=1, tile_m=128, tile_n=64, tile_k=64, stages=2, swizzle=128, pack_halo=1, buffer_c=1,
+                acc_buffers=2, persistent=1, b_resident=1)
+    st, info, why = xtc.xtc_schedule_check(d, xtc.schedule(**dict(base, inner_n=192)), 148)
+    assert st == 0 and info.tmem_cols == 512, why               # 2 buffers x 3 blocks x 64 columns -> 512
+    st0, info0, _ = xtc.xtc_schedule_check(d, xtc.schedule(**base), 148)
+    # the exchange rows for the warp above: 4 warps x 2 parities x 3 rows x 128 B
+    assert info.smem_bytes == info0.smem_bytes + 4 * 2 * 3 * 128
+    for bad, frag in ((dict(inner_n=128), "inner_n"), (dict(inner_n=192, b_resident=0), "b_resident"),
+                      (dict(inner_n=192, tile_m=256), "tile_m"), (dict(inner_n=192, split_k=3, buffer_c=0), "split_k")):
+        st, _, why = xtc.xtc_schedule_check(d, xtc.schedule(**dict(base, **bad)), 148)
+        assert st == xtc.XTC_E_ILLEGAL_SCHEDULE and frag in why, (bad, why)
+    d14 = xtc.conv2d_desc(32, 14, 14, 256, 256, 3, 3, 1, 1)       # S x tile_n must stay <= 256
+    st, _, why = xtc.xtc_schedule_check(d14, xtc.schedule(**dict(base, tile_n=128, inner_n=384, b_resident=0)), 148)
+    assert st == xtc.XTC_E_ILLEGAL_SCHEDULE

@@ -43,14 +43,16 @@ __global__ void __launch_bounds__(256, 1) k_conv(int n, int random, int taps_mod
         if (ptx::elect_one()) {
             for (int t = 0; t < TILES; ++t) {
                 const uint32_t d = tmem + (uint32_t)((t & 1) * 64);
-                for (int tap = 0; tap < 9; ++tap) {
-                    const int shift = taps_mode ? (tap / 3) * 64 + (tap % 3) : 0;
+                const int ntap = n == 192 ? 3 : 9;     // N = 192: the s-fold (3 taps of a filter row per UMMA)
+                for (int tap0 = 0; tap0 < ntap; ++tap0) {
+                    const int tap = n == 192 ? tap0 * 3 : tap0;
+                    const int shift = taps_mode ? (tap / 3) * 64 + (n == 192 ? 0 : tap % 3) : 0;
                     const uint64_t ad = ad0 + (uint64_t)(shift * 8);
                     const uint64_t bd = bd0 + (uint64_t)(tap * 64 * 128 / 16);
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk)
                         ptx::umma<false, 1>(d, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 16 * 8), idesc,
-                                            (tap | kk) ? 1u : 0u);
+                                            (tap0 | kk) ? 1u : 0u);
                 }
                 if (commits) ptx::umma_commit<1>(&tb[t & 1]);   // like the conv kernel: pempty / tfull per tile
                 if (commits > 1) ptx::umma_commit<1>(&tb[t & 1]);
@@ -79,9 +81,9 @@ int main() {
     cudaFuncSetAttribute(k_conv, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     unsigned long long h[148];
     printf("N   data    taps        cycles/UMMA (median CTA over 148)   floor = 128*N/256\n");
-    for (int n : {64})
+    for (int n : {64, 192})
         for (int rnd : {1})
-            for (int cm : {0, 1, 2})
+            for (int cm : {1})
             for (int tm : {0, 1}) {
                 k_conv<<<148, 256, smem>>>(n, rnd, tm, cm, d);
                 cudaError_t e = cudaDeviceSynchronize();
@@ -91,7 +93,7 @@ int main() {
                     for (int j = i + 1; j < 148; ++j)
                         if (h[j] < h[i]) { unsigned long long t = h[i]; h[i] = h[j]; h[j] = t; }
                 printf("%-3d %-7s %-11s commits/tile %d  %-20.1f %d\n", n, rnd ? "random" : "zeros", tm ? "conv shifts" : "no shift", cm,
-                       (double)h[74] / (TILES * 36), 128 * n / 256);
+                       (double)h[74] / (TILES * (n == 192 ? 12 : 36)), 128 * n / 256);
             }
     return 0;
 }
