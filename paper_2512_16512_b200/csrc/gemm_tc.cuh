@@ -65,7 +65,9 @@ __device__ __forceinline__ void mc_store_boxes(const TcParams& p, const uint8_t*
     }
 }
 
-template <bool TF32, bool CONV, int CG, bool SPLIT3, int MS>
+// LEAN: no stream-K, cluster split-K, cluster_n multicast, split partials, atomics or fused
+// gather / multicast write-out -- those paths compiled out (smaller code for the per-tile roles)
+template <bool TF32, bool CONV, int CG, bool SPLIT3, int MS, bool LEAN = false>
 __global__ void __launch_bounds__(kTcThreads, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmC, const TcParams p) {
@@ -105,13 +107,13 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const uint32_t rank = (CG == 2) ? ptx::cluster_ctarank() : 0u;
     // cluster_n (CG = 1): cn CTAs on adjacent N tiles of one M tile; CTA crank loads rows
     // [crank*128/cn, (crank+1)*128/cn) of every A stage and multicasts them to all cn CTAs
-    const int cn = CG == 1 ? p.cn : 1;
+    const int cn = (!LEAN && CG == 1) ? p.cn : 1;
     const bool mcast = cn > 1;
     const uint32_t crank = mcast ? ptx::cluster_ctarank() : 0u;
     const uint16_t cmask = (uint16_t)((1u << cn) - 1u);
     // cluster split-K (split_k_mode XTC_SPLITK_CLUSTER, CG = 1, cn = 1): the ksc CTAs of a
     // cluster run the ksc K segments of one output tile; CTA rank = segment
-    const int ksc = (CG == 1 && cn == 1 && p.ksc > 1) ? p.ksc : 1;
+    const int ksc = (!LEAN && CG == 1 && cn == 1 && p.ksc > 1) ? p.ksc : 1;
     const bool kclu = ksc > 1;
     const uint32_t krank = kclu ? ptx::cluster_ctarank() : 0u;
     const int64_t cluster_id = blockIdx.x / (CG * cn * ksc);
@@ -119,7 +121,10 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     // The tiles this CTA (cluster) visits and the k-block range of each: data-parallel (strided
     // over the tile map; K segment from the split or the cluster rank), or stream-K (a contiguous
     // range of the flattened (tile, k-block) space, stream_k.cuh).  Every role walks the same list.
-    const bool sk = p.sk != 0;
+    const bool sk = !LEAN && p.sk != 0;
+    const int n_gather = LEAN ? 0 : p.n_gather;    // fused all-gather destinations (xtc_run_gather)
+    const int mc_mode = LEAN ? 0 : p.mc_mode;      // multicast write-out (xtc_run_multicast)
+    const bool atomic_k = !LEAN && p.atomic != 0;    // atomic split-K
     int64_t sk_s = 0, sk_e = 0;
     if (sk) sk_range(p.sk_iters, num_clusters, cluster_id, sk_s, sk_e);
     const int64_t n_walk = sk ? (sk_e > sk_s ? (sk_e - 1) / p.kb_total - sk_s / p.kb_total + 1 : 0)
@@ -490,9 +495,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         int buf = 0;
         ClusterSplitState kst;
         uint8_t* stage = sC + q * (kTcEpiStageBytes * kTcEpiBuffers);
-        if (p.n_gather && lane == 0)
-            for (int d = 0; d < p.n_gather; ++d) ptx::tmap_acquire(reinterpret_cast<const CUtensorMap*>(p.gather) + d);
-        const bool to_ws = p.split_out != 0;
+        if (n_gather && lane == 0)
+            for (int d = 0; d < n_gather; ++d) ptx::tmap_acquire(reinterpret_cast<const CUtensorMap*>(p.gather) + d);
+        const bool to_ws = !LEAN && p.split_out != 0;
         const bool bf16_out = p.out_bf16 && !to_ws;
         for (int64_t it = 0; it < n_walk; ++it) {
             int mb, nb, ks, kb0, kb1;
@@ -569,9 +574,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                     // the four 64-column boxes of 32 rows starting at `row`: to C, or (fused all-gather)
                     // to every destination at gather_row0 + row
                     auto store_rows = [&](int row) {
-                        if (p.n_gather) {
+                        if (n_gather) {
                             const CUtensorMap* gm = reinterpret_cast<const CUtensorMap*>(p.gather);
-                            for (int d = 0; d < p.n_gather; ++d)
+                            for (int d = 0; d < n_gather; ++d)
                                 for (int b = 0; b < 4; ++b)
                                     ptx::tma_store_3d(gm + d, big + b * kTcEpiStageBytes, n0 + 64 * b,
                                                       p.gather_row0 + row, 0);
@@ -581,7 +586,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                         }
                         ptx::bulk_commit();
                     };
-                    if (p.mc_mode) {                                     // subtile 1: rows m0t + 128 + 32q
+                    if (mc_mode) {                                     // subtile 1: rows m0t + 128 + 32q
                         mc_store_boxes(p, big, 4, p.gather_row0 + m0t + 128 + 32 * q, n0, lane);
                     } else if (lane == 0) {
                         store_rows(m0t + 128 + 32 * q);
@@ -600,7 +605,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                     }
                     ptx::fence_proxy_async_smem();
                     __syncwarp();
-                    if (p.mc_mode) {                                     // subtile 0: rows m0t + 32q
+                    if (mc_mode) {                                     // subtile 0: rows m0t + 32q
                         mc_store_boxes(p, big, 4, p.gather_row0 + m0t + 32 * q, n0, lane);
                         __syncwarp();                                    // read before the next tile's drain
                     } else if (lane == 0) {
@@ -644,8 +649,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                     const int64_t cc = (int64_t)n0 + c;
                     const int nc = (int)((p.N - cc) < 32 ? (p.N - cc) : 32);
                     // atomic split-K: C is accumulated in place, the first segment adds the bias
-                    if (nc > 0) apply_consumer32(v, p.cons, p.bias, p.C, bf16_out, row, p.ldc, cc, nc, !p.atomic,
-                                                 !p.atomic || ks == 0);
+                    if (nc > 0) apply_consumer32(v, p.cons, p.bias, p.C, bf16_out, row, p.ldc, cc, nc, !atomic_k,
+                                                 !atomic_k || ks == 0);
                 }
                 if (p.buffer_c) {
                     // stage one 128-byte row per thread (swizzled), then one TMA store per warp
@@ -679,17 +684,17 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                     if (last_half) {
                         ptx::fence_proxy_async_smem();
                         __syncwarp();
-                        if (p.mc_mode) {
+                        if (mc_mode) {
                             mc_store_boxes(p, stage + buf * kTcEpiStageBytes, 1, p.gather_row0 + m0 + 32 * q,
                                            bf16_out ? (n0 + (c & ~63)) : (n0 + c), lane);
                             __syncwarp();                        // read before the buffer is refilled
                         } else if (lane == 0) {
                             const int col = bf16_out ? (n0 + (c & ~63)) : (n0 + c);
-                            if (p.n_gather) {
+                            if (n_gather) {
                                 // fused all-gather: the staged chunk goes to every destination
                                 // (this rank's C and its peers'), one bulk group for all
                                 const CUtensorMap* gm = reinterpret_cast<const CUtensorMap*>(p.gather);
-                                for (int d = 0; d < p.n_gather; ++d)
+                                for (int d = 0; d < n_gather; ++d)
                                     ptx::tma_store_3d(gm + d, stage + buf * kTcEpiStageBytes, col,
                                                       p.gather_row0 + m0 + 32 * q, 0);
                             } else {
@@ -713,7 +718,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                                 #pragma unroll
                                 for (int j = 0; j < 32; ++j) if (j < ncols) dst[j] = __uint_as_float(v[j]);
                             }
-                        } else if (p.atomic) {
+                        } else if (atomic_k) {
                             float* dst = reinterpret_cast<float*>(p.C) + row * p.ldc + col0;
                             #pragma unroll
                             for (int j = 0; j < 32; ++j) if (j < ncols) atomicAdd(dst + j, __uint_as_float(v[j]));
@@ -790,7 +795,11 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 template <bool TF32, bool CONV, int CG, bool SPLIT3, int MS>
 cudaError_t launch_tc_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
                                const TcParams& p, int grid, int smem, cudaStream_t st) {
-    auto k = tc_gemm_kernel<TF32, CONV, CG, SPLIT3, MS>;
+    // the lean variant for plain bf16 plans (no split / stream-K / multicast / gather)
+    const bool lean = !TF32 && !SPLIT3 && !p.sk && p.ksc <= 1 && p.cn <= 1 && !p.split_out && !p.atomic &&
+                      !p.n_gather && !p.mc_mode;
+    auto k = lean ? tc_gemm_kernel<TF32, CONV, CG, SPLIT3, MS, !TF32 && !SPLIT3>
+                  : tc_gemm_kernel<TF32, CONV, CG, SPLIT3, MS, false>;
     cudaError_t e = ensure_smem_attr(k, smem);
     if (e != cudaSuccess) return e;
     const int ksc = (CG == 1 && p.cn <= 1 && p.ksc > 1) ? p.ksc : 1;
