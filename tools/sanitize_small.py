@@ -40,6 +40,16 @@ CASES = {
                                                             pack_halo=1, buffer_c=1, acc_buffers=2, persistent=1,
                                                             grid_sms=5, split_k_mode=3)),
     "conv_mma_stem": ("stem", (1, 64, 64, 3, 16), dict(engine=2, tile_m=128, tile_n=16, tile_k=32)),
+    "conv_mma_patch_tma": ("stem", (2, 64, 64, 3, 16), dict(engine=2, tile_m=64, tile_n=16, tile_k=16, pack_halo=1,
+                                                           persistent=1, grid_sms=3)),
+    "conv_mma_patch_threads": ("stem", (2, 64, 64, 3, 16), dict(engine=2, tile_m=64, tile_n=16, tile_k=16,
+                                                               pack_halo=2, persistent=1, grid_sms=3)),
+    "conv_halo_sfold": ("conv", (2, 56, 56, 64, 64), dict(engine=1, tile_m=128, tile_n=64, tile_k=64, stages=2,
+                                                         pack_halo=1, b_resident=1, inner_n=192, acc_buffers=2,
+                                                         persistent=1, grid_sms=4)),
+    "conv_halo_lean": ("conv", (2, 56, 56, 64, 64), dict(engine=1, tile_m=128, tile_n=64, tile_k=64, stages=2,
+                                                        pack_halo=1, b_resident=1, acc_buffers=2, persistent=1,
+                                                        grid_sms=4)),
     "tc_3xtf32": ("mm32", (256, 256, 256), dict(TC, tile_m=128, tile_n=128, tile_k=32, stages=3, acc_buffers=2,
                                                 persistent=1, grid_sms=2)),
     "conv_im2col": ("conv", (2, 14, 14, 64, 64), dict(TC, tile_m=128, tile_n=64, tile_k=64, stages=3, acc_buffers=2,
