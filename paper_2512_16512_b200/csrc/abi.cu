@@ -733,10 +733,12 @@ static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cud
             tp.cl = p.halo_cl;
             tp.pair = p.halo_pair ? 1 : 0;
             tp.sfold = p.halo_sfold;
+            tp.compact = p.halo_compact ? 1 : 0;
             if (p.halo_sfold > 1)                     // UMMA N = S * tile_n
                 tp.idesc = (tp.idesc & ~(0x3Fu << 17)) | ((uint32_t)((p.halo_sfold * p.sch.tile_n) >> 3) << 17);
             tp.patch_bytes = (uint32_t)p.halo_patch_bytes;
             tp.plane_bytes = (uint32_t)(p.halo_patch_bytes / p.halo_planes);
+            tp.patch_tx = (uint32_t)((int64_t)p.halo_planes * p.halo_pr * p.halo_wp * 128);
             CU_TRY(launch_tc_conv_halo(tf32, op->tmA, op->tmB, op->tmC, tp, p.grid_x, p.smem, st), "conv_halo launch");
             ++launches;
         } else {

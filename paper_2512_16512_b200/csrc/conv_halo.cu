@@ -88,6 +88,13 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
         ptx::prefetch_tmap(&tmB);
         if (p.buffer_c) ptx::prefetch_tmap(&tmY);
     }
+    // early start (one CTA per cluster, CL = 1 and no cluster split): after the barrier inits the two
+    // producer warps (0: patches, 3: filter) start loading at once and walk their tiles without the
+    // SMEM tile table; only the TMEM users (warps 1, 2, 4..7) build the table and meet at a named
+    // barrier.  (Trace at L56 N=32 before: the setup barrier at 0.8 us, the first patch issued at
+    // 1.18 us, its data at 2.46 us.)  With CL = 2 / a cluster split the peers' barriers must exist
+    // before a multicast, so those keep the table-then-cluster-barrier order.
+    const bool early = CL == 1 && !kclu && !(p.debug_skip_mma & 8192);   // (8192: A/B diagnostics)
     if (warp == 1 && lane == 0) {
         // a multicast stage is free only when the MMAs of every CTA in the cluster have read it
         for (int s = 0; s < S; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], PAIR ? 1 : CL); }
@@ -113,13 +120,22 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
         ptx::tc_fence_before();
     }
     // tile id -> (image, first output row, first output channel)
-    auto decode = [&](int64_t t, int& nimg, int& p0, int& n0, int& ks) {
+    // (compact rows: tile j of an image = virtual rows v0 = j*128*MSUB ...; p0 = v0 / Wc is the output
+    // row whose padded window starts the patch, off = v0 - p0*Wc the tile's first slot in it)
+    auto decode = [&](int64_t t, int& nimg, int& p0, int& n0, int& ks, int& off) {
         int mb, nb;
         tile_coords(p.tm, t, mb, nb, ks);
         if (kclu) ks = (int)krank;
         mb = mb * CL + (int)rank;                    // CL = 2: the loop runs over M-tile pairs
         nimg = mb / p.tpi;
-        p0 = (mb - nimg * p.tpi) * p.rt * MSUB;
+        if (p.compact) {
+            const int v0 = (mb - nimg * p.tpi) * 128 * MSUB;
+            p0 = v0 / p.wp;
+            off = v0 - p0 * p.wp;
+        } else {
+            p0 = (mb - nimg * p.tpi) * p.rt * MSUB;
+            off = 0;
+        }
         n0 = nb * p.tile_n;
     };
     // the tiles this CTA visits and the k-block range of each: data-parallel (strided over the tile
@@ -147,18 +163,39 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
         }
         return t;
     };
+    auto load_b = [&](uint8_t* dst, uint64_t* bar, int kb, int n0) {
+        if (p.b3d) {
+            ptx::tma_load_3d(&tmB, dst, bar, 0, kb * p.tile_k, n0 / ATOM);
+        } else {
+            for (int b = 0; b < p.tile_n / ATOM; ++b)
+                ptx::tma_load_2d(&tmB, dst + (size_t)b * p.tile_k * 128, bar, n0 + b * ATOM, kb * p.tile_k);
+        }
+    };
     // The CTA's tile walk decoded ONCE into an SMEM table (first kTileTable tiles) before the setup
     // barrier, every thread one entry: each role then reads a tile's (image, row, channel, K range)
     // with two LDS instead of re-running the divisions of tile_coords / decode / walk_at per tile
     // (measured ~1100 cycles per tile per role in XTC_TRACE phase totals).
     TileInfo* const tinfo = reinterpret_cast<TileInfo*>((reinterpret_cast<uintptr_t>(tmem_slot) + 4 + 15) & ~uintptr_t(15));
-    for (int i = threadIdx.x; i < n_walk && i < kTileTable; i += blockDim.x) {
-        TileInfo ti;
-        ti.t = (int32_t)walk_at(i, ti.kb0, ti.kb1);
-        decode(ti.t, ti.nimg, ti.p0, ti.n0, ti.ks);
-        tinfo[i] = ti;
+    const bool producer = warp == 0 || warp == 3;
+    if (early) __syncthreads();                  // the barrier inits are visible; producers go
+    if (!(early && producer)) {
+        // early: the 192 threads of warps 1, 2, 4..7 fill the table; else all 256
+        const int ti0 = early ? (warp < 3 ? (int)threadIdx.x - 32 : (int)threadIdx.x - 64) : (int)threadIdx.x;
+        const int tstep = early ? (int)blockDim.x - 64 : (int)blockDim.x;
+        for (int i = ti0; i < n_walk && i < kTileTable; i += tstep) {
+            TileInfo ti;
+            ti.t = (int32_t)walk_at(i, ti.kb0, ti.kb1);
+            decode(ti.t, ti.nimg, ti.p0, ti.n0, ti.ks, ti.off);
+            tinfo[i] = ti;
+        }
     }
-    if (CL == 2 || kclu) ptx::cluster_sync(); else __syncthreads();
+    if (early) {
+        if (!producer) ptx::named_bar_sync(1, blockDim.x - 64);
+    } else if (CL == 2 || kclu) {
+        ptx::cluster_sync();
+    } else {
+        __syncthreads();
+    }
     if (warp == 2 && p.debug_late_alloc) {
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(tready);
@@ -179,20 +216,13 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
     if (trace && threadIdx.x == 0) trace[1] = ptx::globaltimer();
     int tj = 0;                                  // per-role tile counter for the trace
 
-    auto tile_at = [tinfo, &walk_at, &decode](int64_t it, TileInfo& ti) {
-        if (it < kTileTable) {
+    // the producers of an early start walk their tiles directly (the table may not be filled yet)
+    auto tile_at = [tinfo, &walk_at, &decode, early, producer](int64_t it, TileInfo& ti) {
+        if (it < kTileTable && !(early && producer)) {
             ti = tinfo[it];
         } else {
             ti.t = (int32_t)walk_at(it, ti.kb0, ti.kb1);
-            decode(ti.t, ti.nimg, ti.p0, ti.n0, ti.ks);
-        }
-    };
-    auto load_b = [&](uint8_t* dst, uint64_t* bar, int kb, int n0) {
-        if (p.b3d) {
-            ptx::tma_load_3d(&tmB, dst, bar, 0, kb * p.tile_k, n0 / ATOM);
-        } else {
-            for (int b = 0; b < p.tile_n / ATOM; ++b)
-                ptx::tma_load_2d(&tmB, dst + (size_t)b * p.tile_k * 128, bar, n0 + b * ATOM, kb * p.tile_k);
+            decode(ti.t, ti.nimg, ti.p0, ti.n0, ti.ks, ti.off);
         }
     };
     // PAIR: this CTA's half of the filter columns (128-byte blocks nblk0 ...), completing on the
@@ -211,7 +241,7 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
         int pb = 0;
         uint32_t use_par = 0;
         bool first_round = true;
-        for (int64_t it = 0; it < n_walk; ++it) {
+        for (int64_t it = 0; it < ((p.debug_skip_mma & 1024) ? 0 : n_walk); ++it) {
             TileInfo ti;
             tile_at(it, ti);
             const int nimg = ti.nimg, p0 = ti.p0;
@@ -232,13 +262,13 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
                 // box {ATOM channels, Wp slots, rows, 1} at (plane, -pad_w, p0 - pad_h, n): the zero
                 // padding and the slots beyond the image are TMA's out-of-bounds zero fill
                 if constexpr (PAIR) {                 // both patches complete on the leader's barrier
-                    if (rank == 0) ptx::mbar_arrive_expect_tx(&pfull[cb], 2 * p.patch_bytes);
+                    if (rank == 0) ptx::mbar_arrive_expect_tx(&pfull[cb], 2 * p.patch_tx);
                     const uint32_t bar_c = ptx::mapa_shared(ptx::smem_u32(&pfull[cb]), 0);
                     for (int pl = 0; pl < p.planes; ++pl)
                         ptx::tma_load_4d_pair(&tmX, dst + (size_t)pl * p.plane_bytes, bar_c, pl * ATOM, -p.cg.pw,
                                               p0 - p.cg.ph, nimg);
                 } else {
-                    ptx::mbar_arrive_expect_tx(&pfull[cb], p.patch_bytes);
+                    ptx::mbar_arrive_expect_tx(&pfull[cb], p.patch_tx);
                     for (int pl = 0; pl < p.planes; ++pl)
                         ptx::tma_load_4d(&tmX, dst + (size_t)pl * p.plane_bytes, &pfull[cb], pl * ATOM, -p.cg.pw,
                                          p0 - p.cg.ph, nimg);
@@ -299,19 +329,19 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
         }
     } else if (warp == 1) {
         // ===================== MMA issuer (contraction over r, s, c) =====================
+        // ONE elected lane runs the whole tile walk -- ring / patch / accumulator waits, UMMAs and
+        // commits.  Between two tiles it touches nothing but the two hand-off barriers: no tile-table
+        // reads (unless the tile has a K segment: split / stream-K / cluster split), no divisions, no
+        // warp reconvergence.  The UMMA queue holds only a few N = 64 UMMAs (~50 cycles each), so
+        // bookkeeping on this thread at a tile boundary idles the tensor pipe (measured at L56 N=32:
+        // ~860 cycles per tile when the warp reconverged and re-read the tile table per tile).
         const uint32_t tmem_base = tmem_address();
-        int s = 0, acc = 0, pb = 0;
-        uint32_t ph = 0, aph = 0, pph = 0;
         const uint32_t b_lbo = (uint32_t)p.tile_k * 128u;
         const uint64_t adesc0 = ptx::smem_desc_sw128(ptx::smem_u32(sP), 16, 1024);
         const uint64_t bdesc0 = TF32 ? ptx::smem_desc_sw128(ptx::smem_u32(sB), b_lbo, 512, 1)
                                      : ptx::smem_desc_sw128(ptx::smem_u32(sB), b_lbo, 1024, 2);
-        // Every loop bound and stride in registers, and ONE elected lane runs the whole tile
-        // (ring waits, UMMAs, commits) -- the warp reconverges once per tile, not per k-block.
-        // Every loop bound and stride is pinned in a register, ONE elected lane runs the whole
-        // tile (ring waits, UMMAs, commits), and an atom's MSUB x (ATOM/UMMA_K) UMMAs are
-        // straight-line code: the issue loop is a handful of instructions per 128-byte atom
-        // (short N=64 UMMAs take only ~48 cycles each, so issue overhead is exposed).
+        // every loop bound and stride pinned in a register; an atom's MSUB x (ATOM/UMMA_K) UMMAs
+        // are straight-line code
         const uint32_t b_stage16 = ptx::pin(p.b_stage_bytes >> 4);
         const uint32_t plane16 = ptx::pin(p.plane_bytes >> 4);
         const uint32_t patch16 = ptx::pin(p.patch_bytes >> 4);
@@ -329,30 +359,46 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
         const uint32_t idesc = ptx::pin(p.idesc);
         const bool plain_arrive = (p.debug_skip_mma & 16) != 0;
         const bool wait_tempty = !(p.debug_skip_mma & 64);
-        const int nbuf = p.nbuf, accb = p.acc_buffers;
-        if (b_res && !(PAIR && rank != 0))            // the resident filter (per-k-block barriers)
-            for (int kb = 0; kb < p.kb_total; ++kb) ptx::mbar_wait(&bfull[kb], 0);
-        const bool mphs = trace && lane == 0;          // XTC_TRACE: MMA-warp wait / issue cycle totals
-        uint64_t m_wait = 0, m_issue = 0, mck = mphs ? clock64() : 0;
-        for (int64_t it = 0; it < ((PAIR && rank != 0) ? 0 : n_walk); ++it) {
-            if (wait_tempty) ptx::mbar_wait(&tempty[acc], aph ^ 1u);
-            ptx::mbar_wait(&pfull[pb], pph);
-            if (mphs) { const uint64_t c2 = clock64(); m_wait += c2 - mck; mck = c2; }
-            if (trace && lane == 0 && tj < kTraceK) trace[8 + kTraceK + tj] = ptx::globaltimer();
-            ++tj;
-            ptx::tc_fence_after();
-            TileInfo ti;                              // this tile's k-block range (split_k / stream-K)
-            tile_at(it, ti);
-            int kb0 = ti.kb0, kb1 = ti.kb1;
-            kb1 = min(kb1, kb_total);                 // (kb_total 0: diagnostics without MMAs)
-            if (ptx::elect_one()) {
+        // diagnostics (1024, with 64): free run -- no per-tile waits or commits, one commit at the end
+        const bool free_run = (p.debug_skip_mma & 1024) != 0;
+        // every tile spans all k-blocks unless a split / stream-K / cluster split gives it a K segment
+        const bool fullk = !sk && !kclu && p.kb_per_split >= p.kb_total;
+        const int64_t n_mma = (PAIR && rank != 0) ? 0 : n_walk;
+        if (ptx::elect_one()) {
+            if (b_res && !(PAIR && rank != 0))        // the resident filter (per-k-block barriers)
+                for (int kb = 0; kb < p.kb_total; ++kb) ptx::mbar_wait(&bfull[kb], 0);
+            const bool mphs = trace != nullptr;        // XTC_TRACE: MMA-warp wait / issue cycle totals
+            uint64_t m_wait = 0, m_issue = 0, mck = mphs ? clock64() : 0;
+            int s = 0, acc = 0, pb = 0;
+            uint32_t ph = 0, aph = 0, pph = 0;
+            for (int64_t it = 0; it < n_mma; ++it) {
+                if (wait_tempty && !free_run) ptx::mbar_wait(&tempty[acc], aph ^ 1u);
+                if (!free_run) ptx::mbar_wait(&pfull[pb], pph);
+                if (mphs) { const uint64_t c2 = clock64(); m_wait += c2 - mck; mck = c2; }
+                if (trace && tj < kTraceK) trace[8 + kTraceK + tj] = ptx::globaltimer();
+                ++tj;
+                if (!(p.debug_skip_mma & 4096)) ptx::tc_fence_after();
+                int kb0 = 0, kb1 = kb_total, toff = 0;
+                if (!fullk || p.compact) {             // this tile's k-block range (split_k / stream-K), row offset
+                    TileInfo ti;
+                    tile_at(it, ti);
+                    kb0 = ti.kb0;
+                    kb1 = min(ti.kb1, kb_total);       // (kb_total 0: diagnostics without MMAs)
+                    toff = ti.off;
+                }
                 const uint32_t d0 = tmem_base + (uint32_t)(acc * acc_cols);
-                const uint64_t apatch = adesc0 + (uint64_t)((uint32_t)pb * patch16);
+                // compact rows: virtual row 0 of the tile is patch row toff (8 x 16 bytes per 128-byte row)
+                const uint64_t apatch = adesc0 + (uint64_t)((uint32_t)pb * patch16 + (uint32_t)toff * 8u);
                 // the next 128-byte atom: channel plane pl, filter column sx, A offset aoff
                 // (16-byte units) = pl*plane16 + (r*Wp + sx)*8, starting at the segment's first atom
-                const int j0 = kb0 * n_atoms, tap0 = j0 / planes;
-                int pl = j0 - tap0 * planes, sx = tap0 % R_S;
-                uint32_t aoff = (uint32_t)pl * plane16 + (uint32_t)((tap0 / R_S) * p.wp + sx) * 8u;
+                int pl = 0, sx = 0;
+                uint32_t aoff = 0;
+                if (kb0 > 0) {
+                    const int j0 = kb0 * n_atoms, tap0 = j0 / planes;
+                    pl = j0 - tap0 * planes;
+                    sx = tap0 % R_S;
+                    aoff = (uint32_t)pl * plane16 + (uint32_t)((tap0 / R_S) * p.wp + sx) * 8u;
+                }
                 uint32_t accf = 0;                    // 0 for the tile's first UMMA (overwrite)
                 const uint32_t aoff_mask = (p.debug_skip_mma & 256) ? 0u : 0xffffffffu;   // diagnostics: no tap shifts
                 auto atom = [&](uint64_t bd) {
@@ -398,40 +444,37 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
                         for (int a = 0; a < n_atoms; ++a) atom(bd + (uint64_t)(a * ATOM * 8));
                     }
                 } else {
-                    int s1 = s;
-                    uint32_t ph1 = ph;
                     for (int kb = kb0; kb < kb1; ++kb) {
-                        ptx::mbar_wait(&full[s1], ph1);
+                        ptx::mbar_wait(&full[s], ph);
                         ptx::tc_fence_after();
-                        const uint64_t bd = bdesc0 + (uint64_t)((uint32_t)s1 * b_stage16);
+                        const uint64_t bd = bdesc0 + (uint64_t)((uint32_t)s * b_stage16);
                         for (int a = 0; a < n_atoms; ++a) atom(bd + (uint64_t)(a * ATOM * 8));
-                        if constexpr (PAIR) ptx::umma_commit<2>(&empty[s1]);
-                        else if constexpr (CL == 2) ptx::umma_commit_multicast(&empty[s1], 0x3);
-                        else ptx::umma_commit<1>(&empty[s1]);
-                        if (++s1 == Sring) { s1 = 0; ph1 ^= 1u; }
+                        if constexpr (PAIR) ptx::umma_commit<2>(&empty[s]);
+                        else if constexpr (CL == 2) ptx::umma_commit_multicast(&empty[s], 0x3);
+                        else ptx::umma_commit<1>(&empty[s]);
+                        if (++s == Sring) { s = 0; ph ^= 1u; }
                     }
                 }
-                if (plain_arrive) {                   // diagnostics: plain arrives (valid only without MMAs)
+                if (free_run) {
+                    if (p.debug_skip_mma & 2048) { ptx::umma_commit<CG>(&pempty[pb]); ptx::umma_commit<CG>(&tempty[acc]); }
+                    if (it + 1 == n_mma) { ptx::umma_commit<CG>(&tfull[0]); ptx::mbar_wait(&tfull[0], 0); }
+                } else if (plain_arrive) {            // diagnostics: plain arrives (valid only without MMAs)
                     ptx::mbar_arrive(&pempty[pb]);
                     ptx::mbar_arrive(&tfull[acc]);
                 } else {
                     ptx::umma_commit<CG>(&pempty[pb]);    // patch buffer(s) free once these MMAs finish
                     ptx::umma_commit<CG>(&tfull[acc]);
                 }
+                if (mphs) {
+                    const uint64_t c2 = clock64();
+                    m_issue += c2 - mck; mck = c2;
+                    trace[kTracePhase + 6] = m_wait; trace[kTracePhase + 7] = m_issue;
+                }
+                if (++pb == p.nbuf) { pb = 0; pph ^= 1u; }
+                if (++acc == p.acc_buffers) { acc = 0; aph ^= 1u; }
             }
-            __syncwarp();
-            if (mphs) {
-                const uint64_t c2 = clock64();
-                m_issue += c2 - mck; mck = c2;
-                trace[kTracePhase + 6] = m_wait; trace[kTracePhase + 7] = m_issue;
-            }
-            if (!b_res)                               // every lane advances the ring by the segment's slots
-                for (int kb = kb0; kb < kb1; ++kb)
-                    if (++s == S) { s = 0; ph ^= 1u; }
-            (void)nbuf; (void)accb;
-            if (++pb == p.nbuf) { pb = 0; pph ^= 1u; }
-            if (++acc == p.acc_buffers) { acc = 0; aph ^= 1u; }
         }
+        __syncwarp();
     } else if (warp >= 4) {
         // ===================== epilogue (bufferize) =====================
         const uint32_t tmem_base = tmem_address();
@@ -483,8 +526,14 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
             }
             for (int ms = 0; ms < ((p.debug_skip_mma & 8) ? 0 : MSUB); ++ms) {
                 const int v = ms * 128 + 32 * q + lane;        // this thread's virtual row
-                const int prow0 = p0 + e_row0[ms], q0 = e_q0[ms];
-                const int prow = p0 + e_row[ms], qcol = e_q[ms];
+                int prow0 = p0 + e_row0[ms], q0 = e_q0[ms];
+                int prow = p0 + e_row[ms], qcol = e_q[ms];
+                if (p.compact) {                               // the tile starts at slot off of patch row 0
+                    const int w0 = ti.off + ms * 128 + 32 * q, w = w0 + lane;
+                    const int r0 = w0 / p.wp, r = w / p.wp;
+                    prow0 = p0 + r0; q0 = w0 - r0 * p.wp;
+                    prow = p0 + r; qcol = w - r * p.wp;
+                }
                 const bool valid = prow < P && qcol < Q;
                 const bool any_valid = prow0 < P;              // rows grow with the lane index
                 const uint32_t t_row = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * acc_cols + ms * p.tile_n);

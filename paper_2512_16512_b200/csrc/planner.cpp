@@ -125,7 +125,14 @@ static xtc_status plan_simt(const xtc_op_desc& d, const xtc_schedule& s, int num
 static xtc_status plan_tc_halo(const xtc_op_desc& d, const xtc_schedule& s, int num_sms, Plan& p, std::string& why) {
     const int es = dtype_size(d.in_dtype), os = dtype_size(d.out_dtype);
     if (d.kind != XTC_OP_CONV2D) ILLEGAL("pack_halo applies to conv2d only");
-    if (s.pack_halo != 1) ILLEGAL("pack_halo must be 0 or 1");
+    if (s.pack_halo != 1 && s.pack_halo != 2) ILLEGAL("pack_halo must be 0, 1 or 2");
+    // pack_halo = 2 (compact rows): output row p's slots sit at the padded row width Wc = Q + S - 1
+    // (not the power of two above it) and a tile is 128 x tile_m/128 CONSECUTIVE virtual rows of one
+    // image's P x Wc grid, so a tile starts mid-row: its patch starts at the padded input row of its
+    // first virtual row and every UMMA A view is advanced by the tile's offset into that row.  Fewer
+    // don't-care slots (L56: 58 of 64) and fewer tiles (L56 N=32: 832 instead of 896, 6 per SM
+    // instead of 7).  One CTA per tile (cluster_m 1), no s-fold, no split, direct stores.
+    const bool compact = s.pack_halo == 2;
     if (d.stride_h != 1 || d.stride_w != 1) ILLEGAL("pack_halo needs stride 1 (taps must be row shifts of one patch)");
     // cluster_m = 2: two CTAs on adjacent M tiles (same N tile) each fetch half of every filter
     // stage and TMA-multicast it to both (the filter stream per SM is halved)
@@ -188,10 +195,22 @@ static xtc_status plan_tc_halo(const xtc_op_desc& d, const xtc_schedule& s, int 
     gemm_view(d, M_, N_, K_, P, Q);
     int wp = 8;
     while (wp < Q + d.s - 1) wp *= 2;
+    if (compact) {
+        wp = (int)(Q + d.s - 1);
+        if (pair || hcl != 1) ILLEGAL("pack_halo 2 (compact rows): one CTA per tile (cluster_m 1, inner_m 128)");
+        if (sfold > 1) ILLEGAL("pack_halo 2 (compact rows): no s-fold (inner_n must be tile_n)");
+        if (p.split_k > 1 || p.stream_k) ILLEGAL("pack_halo 2 (compact rows): split_k must be 1");
+        // a warp's 32 rows start mid-row and wrap into the next output row; the TMA store box of
+        // whole-row slots cannot express that (a negative start slot faults), so direct stores
+        if (s.buffer_c) ILLEGAL("pack_halo 2 (compact rows): the epilogue stores directly (buffer_c 0)");
+    }
     if (wp > 128) ILLEGAL("pack_halo: Q + S - 1 = %lld pixel slots exceed one 128-row UMMA tile", (long long)(Q + d.s - 1));
     const int msub = pair ? 1 : s.tile_m / 128;            // the pair: one 128-row UMMA tile per CTA
-    const int rt = 128 / wp;                               // output rows per UMMA M-tile
-    const int64_t pr = (int64_t)msub * rt + d.r - 1;       // patch rows
+    const int rt = compact ? 0 : 128 / wp;                 // output rows per UMMA M-tile (pow2 rows)
+    // patch rows: pow2 rows: the tile's rows + R - 1; compact: the rows spanned by the largest patch
+    // index any virtual row of the tile reads, (Wc - 1) + 128*msub - 1 + (R-1)*Wc + S - 1, + 1
+    const int64_t pr = compact ? ((int64_t)wp - 1 + 128 * msub - 1 + (d.r - 1) * wp + d.s - 1) / wp + 1
+                               : (int64_t)msub * rt + d.r - 1;
     if (pr > 256) ILLEGAL("pack_halo: %lld patch rows exceed the 256-row TMA box", (long long)pr);
     const int accb = s.acc_buffers == 0 ? 1 : s.acc_buffers;
     if (accb < 1 || accb > 2) ILLEGAL("acc_buffers must be 1 or 2");
@@ -200,7 +219,9 @@ static xtc_status plan_tc_halo(const xtc_op_desc& d, const xtc_schedule& s, int 
     if (alloc > 512) ILLEGAL("bufferize: %d TMEM columns (acc_buffers x tile_m/128 x tile_n) exceed 512", alloc);
     p.tmem_cols = alloc;
     const int64_t planes = d.c / p.atom_k;
-    const int64_t patch = planes * pr * wp * 128;
+    // each channel plane starts 1024-byte aligned (the 128-byte swizzle atom; compact rows give
+    // pr * Wc * 128 bytes that are not a multiple of 1024)
+    const int64_t patch = planes * (((int64_t)pr * wp * 128 + 1023) / 1024 * 1024);
     const int64_t b_stage = (int64_t)s.tile_k * (pair ? s.tile_n / 2 : s.tile_n) * es;   // per CTA
     p.tiles_n = (int)cdiv(N_, s.tile_n);
     p.kb_total = (int)cdiv(K_, s.tile_k);
@@ -236,7 +257,8 @@ static xtc_status plan_tc_halo(const xtc_op_desc& d, const xtc_schedule& s, int 
     p.halo_planes = (int)planes;
     p.halo_nbuf = nbuf;
     p.halo_patch_bytes = patch;
-    p.halo_tpi = (int)cdiv(P, (int64_t)rt * msub);
+    p.halo_tpi = compact ? (int)cdiv(P * wp, 128LL * msub) : (int)cdiv(P, (int64_t)rt * msub);
+    p.halo_compact = compact;
     p.tiles_m = (int)(d.batch * p.halo_tpi);
     if (pair) {
         if (p.tiles_m % 2) ILLEGAL("pack_halo: the CTA pair needs an even number of M tiles (%d)", p.tiles_m);

@@ -187,6 +187,7 @@ struct Plan {
     int32_t halo_cl = 1;                // CTAs per cluster sharing the filter stream (TMA multicast, or a pair)
     bool halo_pair = false;             // inner_m 256: cta_group::2 UMMAs (M = 256) over a CTA pair
     int32_t halo_sfold = 1;             // inner_n = S * tile_n: the filter row's S taps folded into the UMMA N
+    bool halo_compact = false;          // pack_halo 2: rows at Wc = Q + S - 1 slots, tiles of consecutive rows
     bool ovl = false;                   // overlapped epilogue (see TcParams::ovl); 64 KB epilogue SMEM
     int32_t msub = 1;                   // tcgen05 matmul: 128-row M-subtiles per CTA (tile_m = 128*cta_group*msub)
     bool stream_k = false;              // split_k_mode 3: stream-K over the persistent grid (stream_k.cuh)
@@ -241,7 +242,8 @@ struct TcParams {
                                // prologue barrier, i.e. the producers wait for the allocation
     int32_t debug_skip_mma;  // diagnostics only, output invalid: XTC_DEBUG_SKIP_MMA, or XTC_DEBUG_SKIP=mask
                              // (conv_halo: 1 no MMAs, 2 no patch TMA, 4 no output stores, 8 no TMEM drain,
-                             // 256 no tap shifts, 512 every UMMA twice)
+                             // 256 no tap shifts, 512 every UMMA twice, 1024 (+64) free-run MMA warp:
+                             // no patch loads, no per-tile waits or commits)
     int64_t ldc, ws_ld;
     void* C; float* Wk;
     uint32_t idesc;
@@ -251,6 +253,8 @@ struct TcParams {
     ConvGeom cg;
     // pack_halo conv only (see Plan)
     int32_t wp, rt, msub, planes, nbuf, tpi, cl, pair;
+    int32_t compact;         // pack_halo 2: wp = Q + S - 1 and a tile = 128*msub consecutive virtual rows
+                             // of an image (starts mid-row at TileInfo::off)
     int32_t sfold;           // pack_halo s-fold: the S taps of a filter row are the N blocks of one UMMA
                              // (N = S * tile_n); the epilogue sums block s of row v + s (1 = off)
     int32_t cn;              // cluster_n: CTAs of a cluster on adjacent N tiles, A stages multicast (1 = none)
@@ -258,6 +262,7 @@ struct TcParams {
     int32_t ovl;             // overlapped epilogue (two M-subtiles, bf16, tile_n 256): subtile 1 drained to a
                              // 64 KB SMEM tile, subtile 0 to registers, TMEM released before the stores
     uint32_t patch_bytes, plane_bytes;
+    uint32_t patch_tx;       // bytes the patch TMAs deliver (planes x rows x Wp x 128; planes start 1024-aligned)
     // Diagnostics (XTC_TRACE): %globaltimer stamps for CTAs < kTraceCtas, laid out
     // [cta][kTraceSlots]: slot 0 kernel entry, 1 setup done; producer issue of k-block i at
     // 8+i, MMA full-wait done at 8+kTraceK+i, epilogue tile j start/end at 8+2kTraceK+2j(+1).
@@ -285,7 +290,7 @@ struct TcParams {
 };
 // conv_halo: the first kTileTable tiles of a CTA's walk, decoded once into SMEM (after the barriers)
 struct TileInfo {
-    int32_t t, nimg, p0, n0, ks, kb0, kb1, pad;
+    int32_t t, nimg, p0, n0, ks, kb0, kb1, off;   // off: pack_halo 2, the tile's first slot in patch row 0
 };
 constexpr int kTileTable = 64;
 constexpr int kTileTableBytes = kTileTable * (int)sizeof(TileInfo) + 16;

@@ -200,6 +200,18 @@ HALO_CASES = [
                                                         acc_buffers=1)),
     ((2, 56, 56, 64, 64, 3, 3, 1, "bf16", "bf16"), dict(tile_n=64, inner_n=192, b_resident=1, stages=2,
                                                         persistent=1, grid_sms=5)),
+    # pack_halo 2 (compact rows, Wc = Q + S - 1): tiles start mid-row, a warp's 32 rows wrap into the next
+    # output row (direct stores); Wc 58 / 41 / 34 / 104 / 15, tile_m 128 / 256, ragged image ends, fp32
+    # out, a 5x5 filter, 2 channel planes, tf32, several tiles per CTA (grid_sms)
+    ((2, 56, 56, 64, 64, 3, 3, 1, "bf16", "bf16"), dict(pack_halo=2, tile_n=64, b_resident=1, stages=2, buffer_c=0)),
+    ((2, 56, 56, 64, 64, 3, 3, 1, "bf16", "bf16"), dict(pack_halo=2, tile_n=64, b_resident=1, stages=2, buffer_c=0,
+                                                        grid_sms=7)),
+    ((3, 17, 39, 64, 128, 3, 3, 1, "bf16", "f32"), dict(pack_halo=2, tile_n=128, stages=3, buffer_c=0)),
+    ((2, 11, 30, 128, 64, 5, 5, 2, "bf16", "bf16"), dict(pack_halo=2, tile_m=256, tile_n=64, stages=3, buffer_c=0)),
+    ((2, 9, 102, 64, 64, 3, 3, 1, "bf16", "bf16"), dict(pack_halo=2, tile_n=64, b_resident=1, stages=2,
+                                                        buffer_c=0, grid_sms=3)),
+    ((2, 13, 13, 64, 64, 3, 3, 1, "bf16", "f32"), dict(pack_halo=2, tile_n=64, stages=2, buffer_c=0)),
+    ((2, 14, 14, 64, 64, 3, 3, 1, "tf32", "f32"), dict(pack_halo=2, tile_n=64, tile_k=32, stages=4, buffer_c=0)),
 ]
 
 
@@ -211,6 +223,12 @@ def test_tc_conv_pack_halo(case, mode):
     base = dict(pack_halo=1, tile_m=128, tile_k=64, persistent=1, acc_buffers=2, buffer_c=1)
     base.update(kw)
     run_conv(d, idt, odt, tc(**base), mode)
+
+
+def test_tc_conv_pack_halo_compact_fused_relu():
+    d = xtc.conv2d_desc(2, 56, 56, 64, 64, 3, 3, 1, 1, "bf16", "bf16", consumer="relu")
+    for extra in (dict(fuse=1), dict(fuse=1, acc_buffers=1)):
+        run_conv_relu(d, tc(pack_halo=2, tile_n=64, stages=2, b_resident=1, persistent=1, buffer_c=0, **extra))
 
 
 def run_conv_relu(d, sch, seed=30):

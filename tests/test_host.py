@@ -168,6 +168,28 @@ def test_pack_halo_plan():
     assert st == xtc.XTC_OK and info.num_tiles == 2, why
 
 
+def test_pack_halo_compact_plan():
+    """pack_halo 2: Wc = Q + S - 1 slots per row, tiles of 128 consecutive virtual rows per image
+    (ceil(P*Wc / 128) per image), patch rows = the rows spanned by a tile's largest read, + 1."""
+    l56 = xtc.conv2d_desc(32, 56, 56, 64, 64)
+    C = dict(HALO, pack_halo=2, buffer_c=0)
+    st, info, why = chk(l56, **dict(C, b_resident=1))
+    assert st == xtc.XTC_OK, why
+    tpi = -(-56 * 58 // 128)                                     # 26 tiles per image (25 full + 48 rows)
+    assert tpi == 26 and info.num_tiles == 32 * tpi and info.grid_x == 148
+    pr = (57 + 127 + 2 * 58 + 2) // 58 + 1                       # 6 patch rows of 58 slots
+    assert pr == 6 and pr * 58 * 128 == 44544
+    # resident filter + 3 patch planes rounded up to the 1024-byte swizzle atom (44544 -> 45056 bytes),
+    # no epilogue staging (direct stores), barriers + the SMEM tile table
+    assert info.smem_bytes == 9 * 8192 + 3 * 45056 + 2048 + 64 * 32 + 16
+    st, info, why = chk(l56, **dict(C, tile_m=256, b_resident=1))
+    assert st == xtc.XTC_OK and info.num_tiles == 32 * (-(-56 * 58 // 256)), why
+    # a power-of-two width gains nothing but stays legal: L14 (Wc = 16)
+    l14 = xtc.conv2d_desc(4, 14, 14, 256, 256)
+    st, info, why = chk(l14, **dict(C, tile_n=128, stages=4))
+    assert st == xtc.XTC_OK and info.num_tiles == 4 * 2 * 2, why
+
+
 @pytest.mark.parametrize("desc,kw,frag", [
     (xtc.conv2d_desc(2, 15, 17, 64, 128, 3, 3, 2, 1), {}, "stride 1"),
     (xtc.matmul_desc(256, 256, 256), {}, "conv2d only"),
@@ -186,7 +208,12 @@ def test_pack_halo_plan():
     (xtc.conv2d_desc(2, 56, 56, 64, 64), dict(pack_warps=2), "pack_warps"),
     (xtc.conv2d_desc(1, 4, 200, 64, 64), {}, "slots"),
     (xtc.conv2d_desc(2, 56, 56, 64, 64), dict(tile_m=384), "tile_m"),
-    (xtc.conv2d_desc(2, 56, 56, 64, 64), dict(pack_halo=2), "pack_halo"),
+    (xtc.conv2d_desc(2, 56, 56, 64, 64), dict(pack_halo=3), "pack_halo"),
+    # pack_halo 2 (compact rows): one CTA per tile, no s-fold, no split, TMA-store staging needs Wc >= 32
+    (xtc.conv2d_desc(2, 56, 56, 64, 128), dict(pack_halo=2, cluster_m=2, tile_n=128, buffer_c=0), "compact rows"),
+    (xtc.conv2d_desc(2, 56, 56, 64, 64), dict(pack_halo=2, inner_n=192, b_resident=1, buffer_c=0), "compact rows"),
+    (xtc.conv2d_desc(2, 56, 56, 64, 64), dict(pack_halo=2, split_k=3, buffer_c=0), "split_k must be 1"),
+    (xtc.conv2d_desc(2, 56, 56, 64, 64), dict(pack_halo=2, buffer_c=1), "buffer_c 0"),
     (xtc.conv2d_desc(2, 56, 56, 256, 256), dict(tile_m=256, tile_n=256, acc_buffers=1, stages=8), "SMEM"),
 ])
 def test_pack_halo_legality(desc, kw, frag):

@@ -7,14 +7,10 @@ from paper_2512_16512_b200.bench_extras import HALO, TC, _best
 dev = torch.device("cuda", 0)
 CANDS = {
     "L56": [dict(HALO, tile_n=64, stages=2, b_resident=1),
-            dict(HALO, tile_n=64, stages=2, b_resident=1, inner_n=192),
-            dict(HALO, tile_n=64, stages=2, b_resident=1, inner_n=192, buffer_c=0),
-            dict(HALO, tile_n=64, stages=2, b_resident=1, inner_n=192, acc_buffers=1)],
-    "L14": [dict(HALO, tile_m=256, cluster_m=2, inner_m=256, tile_n=128, tile_k=128, stages=3),
-            dict(HALO, tile_m=256, cluster_m=2, inner_m=256, tile_n=128, tile_k=128, stages=3, buffer_c=0),
-            dict(HALO, tile_n=128, tile_k=128, stages=3),
-            dict(HALO, tile_n=128, tile_k=128, stages=3, buffer_c=0),
-            dict(HALO, tile_n=64, tile_k=128, stages=4, buffer_c=0)],
+            dict(HALO, tile_n=64, stages=2, b_resident=1, buffer_c=0),
+            dict(HALO, tile_n=64, stages=2, b_resident=1, pack_halo=2, buffer_c=0),
+            dict(HALO, tile_m=256, tile_n=64, stages=2, b_resident=1, pack_halo=2, buffer_c=0)],
+    "L14": [dict(HALO, tile_n=128, tile_k=128, stages=3)],
 }
 LAYERS = {"L56": (56, 64), "L14": (14, 256)}
 for rnd in range(2):

@@ -16,7 +16,7 @@ st = torch.cuda.current_stream().cuda_stream
 xtc.xtc_fill(x.data_ptr(), x.numel(), xtc.XTC_BF16, 5, 0, 0, st)
 xtc.xtc_fill(w.data_ptr(), w.numel(), xtc.XTC_BF16, 6, 0, 0, st)
 op = xtc.Op(d).apply(xtc.schedule(**sch))
-for mask in (0, 1, 2, 4, 6, 3, 5, 7):
+for mask in [int(v) for v in os.environ.get("DIAG_MASKS", "0,1,2,4,6,3,5,7").split(",")]:
     os.environ["XTC_DEBUG_SKIP"] = str(mask)
     for flush in (1, 0):
         m = op.measure(x, w, y, xtc.measure_cfg(warmup=3, repeats=20, flush_l2=flush, validate=0))
