@@ -25,7 +25,8 @@ HALO = dict(TC, pack_halo=1, buffer_c=1, acc_buffers=2, persistent=1)
 
 CONV_SCHEDS = {
     # pack_halo (input packed once per output tile) first; the im2col schedules stay as candidates
-    "L56": [dict(HALO, tile_n=64, stages=2, b_resident=1),
+    "L56": [dict(HALO, tile_n=64, stages=2, b_resident=1, pack_halo=2, buffer_c=0),   # compact rows
+            dict(HALO, tile_n=64, stages=2, b_resident=1),
             dict(HALO, tile_m=256, tile_n=64, stages=2, b_resident=1),
             dict(TC, tile_n=64, stages=8, buffer_c=1, acc_buffers=2, persistent=1, raster_group=8, pack_warps=3),
             dict(TC, tile_n=64, stages=7, buffer_c=1, acc_buffers=2, persistent=1, pack_warps=3, b_resident=1)],
@@ -53,6 +54,66 @@ SIMT_SCHEDS = [
 ]
 
 
+REPS = 40   # timed launches per candidate (each after an L2 flush)
+
+
+def library_same_protocol(xtc, torch, dev, best, reps=200):
+    """Context only (library code, never on the product path): cuDNN (torch conv2d, channels_last bf16,
+    cudnn.benchmark) and cuBLAS (torch.matmul) on the BASELINE conv layers and small GEMMs, timed exactly
+    like our own best schedule here -- one launch between two events after an L2 flush, `reps` reps,
+    interleaved in blocks of 10 -- and reported as means (the event grid, see _best)."""
+    import torch.nn.functional as F
+    torch.backends.cudnn.benchmark = True
+    flush = torch.empty(512 * 1024 * 1024 // 4, device=dev, dtype=torch.float32)
+
+    def one(fn):
+        flush.add_(1.0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(); fn(); e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) * 1e3
+
+    out = {}
+    cases = [(f"conv_{name}_n{nb}", ("conv", nb, h, c)) for name, (h, c) in {"L56": (56, 64), "L14": (14, 256)}.items()
+             for nb in (1, 8, 32)] + [(f"matmul_{n}", ("mm", n)) for n in (512, 1024)]
+    for key, cs in cases:
+        sch = best.get(key)
+        if sch is None:
+            continue
+        if cs[0] == "conv":
+            _, nb, h, c = cs
+            x = torch.randn(nb, c, h, h, device=dev, dtype=torch.bfloat16).to(memory_format=torch.channels_last)
+            w = torch.randn(c, c, 3, 3, device=dev, dtype=torch.bfloat16).to(memory_format=torch.channels_last)
+            xn, wn = x.permute(0, 2, 3, 1).contiguous(), w.permute(2, 3, 1, 0).contiguous()
+            d = xtc.conv2d_desc(nb, h, h, c, c, 3, 3, 1, 1, "bf16", "bf16")
+            M, N, K = xtc.gemm_view(d)
+            y = torch.empty((M, N), dtype=torch.bfloat16, device=dev)
+            op = xtc.Op(d, dev.index).apply(xtc.schedule(**sch))
+            ours, lib, lib_name = (lambda: op.run(xn, wn, y)), (lambda: F.conv2d(x, w, padding=1)), "cudnn"
+            flops = 2.0 * M * N * K
+        else:
+            n = cs[1]
+            a = torch.randn(n, n, device=dev, dtype=torch.bfloat16)
+            b = torch.randn(n, n, device=dev, dtype=torch.bfloat16)
+            cc, cr = torch.empty_like(a), torch.empty_like(a)
+            op = xtc.Op(xtc.matmul_desc(n, n, n, "bf16", "bf16"), dev.index).apply(xtc.schedule(**sch))
+            ours, lib, lib_name = (lambda: op.run(a, b, cc)), (lambda: torch.matmul(a, b, out=cr)), "cublas"
+            flops = 2.0 * n ** 3
+        for _ in range(5):
+            ours(); lib()
+        t_o, t_l = [], []
+        for _ in range(reps // 10):
+            t_l += [one(lib) for _ in range(10)]
+            t_o += [one(ours) for _ in range(10)]
+        mo, ml = sum(t_o) / len(t_o), sum(t_l) / len(t_l)
+        out[key] = {"xtc_us_mean": round(mo, 3), f"{lib_name}_us_mean": round(ml, 3),
+                    "xtc_over_lib_speed": round(ml / mo, 3), "xtc_tflops_mean": round(flops / mo * 1e-6, 1),
+                    "schedule": sch}
+    out["protocol"] = (f"per launch: L2 flush (512 MB write), event pair around one launch; {reps} reps in "
+                       "interleaved blocks of 10 (library block first); means")
+    return out
+
+
 def _best(xtc, torch, dev, desc, scheds, in_shapes, peak, fill_seed=11, flush=1):
     M, N, K = xtc.gemm_view(desc)
     tdt = torch.bfloat16 if desc.in_dtype == xtc.XTC_BF16 else torch.float32
@@ -72,23 +133,27 @@ def _best(xtc, torch, dev, desc, scheds, in_shapes, peak, fill_seed=11, flush=1)
         except xtc.XtcError as e:                  # illegal for this shape: recorded, not measured
             rows.append({"illegal": str(e)[:160]})
             continue
-        m = op.measure(a, b, c, xtc.measure_cfg(warmup=3, repeats=20, flush_l2=flush, validate=1,
+        m = op.measure(a, b, c, xtc.measure_cfg(warmup=3, repeats=REPS, flush_l2=flush, validate=1,
                                                 reuse_reference=1, peak_tflops=peak), stream=st)
-        rows.append({"tflops_med": round(m.tflops_med, 1), "valid": int(m.valid), "t_med_us": round(m.t_med_ns / 1e3, 2)})
-        if m.valid == 1 and (best is None or m.tflops_med > best[0].tflops_med):
+        rows.append({"tflops_med": round(m.tflops_med, 1), "valid": int(m.valid), "t_med_us": round(m.t_med_ns / 1e3, 2),
+                     "t_mean_us": round(m.t_mean_ns / 1e3, 3)})
+        # ranked by the MEAN: single-launch event times snap to a ~1 us grid on these parts, so medians of
+        # short kernels tie (profiles/r02c_event_timer_quantisation.txt); the mean over reps resolves below it
+        if m.valid == 1 and (best is None or m.t_mean_ns < best[0].t_mean_ns):
             best = (m, s)
     if best is None:
         return {"error": "no valid schedule", "tried": rows}
     m, s = best
     out = {"tflops_med": m.tflops_med, "tflops_min_time": m.tflops_min, "t_med_us": m.t_med_ns / 1e3,
+           "t_mean_us": m.t_mean_ns / 1e3, "tflops_mean": m.tflops_med * m.t_med_ns / m.t_mean_ns,
            "frac_peak": m.tflops_med / peak, "max_norm_err": m.max_norm_err, "l2": "flushed" if flush else "warm",
            "schedule": s, "tried": rows}
     if flush:
         # the best schedule again with the operands left in L2 by the previous rep (warm L2)
         op.apply(xtc.schedule(**s))
-        w = op.measure(a, b, c, xtc.measure_cfg(warmup=3, repeats=20, flush_l2=0, validate=0, peak_tflops=peak),
+        w = op.measure(a, b, c, xtc.measure_cfg(warmup=3, repeats=REPS, flush_l2=0, validate=0, peak_tflops=peak),
                        stream=st)
-        out["warm_l2"] = {"tflops_med": w.tflops_med, "t_med_us": w.t_med_ns / 1e3}
+        out["warm_l2"] = {"tflops_med": w.tflops_med, "t_med_us": w.t_med_ns / 1e3, "t_mean_us": w.t_mean_ns / 1e3}
     return out
 
 
@@ -175,8 +240,11 @@ def run_extras(xtc, torch, dev, peak):
                 cands += [dict(HALO, tile_n=64, tile_k=128, stages=3, buffer_c=0, split_k=sk, split_k_mode=2)
                           for sk in (6, 9)]
             r = _best(xtc, torch, dev, d, cands, [(nb, h, h, c), (3, 3, c, c)], peak)
-            scan[f"{name}_n{nb}"] = {k: r.get(k) for k in ("tflops_med", "t_med_us", "warm_l2", "schedule", "error")}
+            scan[f"{name}_n{nb}"] = {k: r.get(k) for k in ("tflops_med", "t_med_us", "t_mean_us", "warm_l2", "schedule", "error")}
     out["conv_batch_scan_bf16"] = scan
+    best = {f"conv_{k}": v["schedule"] for k, v in scan.items() if v.get("schedule")}
+    best.update({f"matmul_{n}": out[f"matmul_{n}_bf16"].get("schedule") for n in (512, 1024)})
+    out["vs_library_same_protocol"] = library_same_protocol(xtc, torch, dev, best)
     out["matmul_32_f32_config1"] = config1_latency(xtc, torch, dev)
     out["conv_stem_7x7s2_c3"] = stem_conv(xtc, torch, dev, peak)
     return out

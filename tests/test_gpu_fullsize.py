@@ -83,15 +83,16 @@ def test_headline_8192_sampled_rows_and_random_elements(mode):
         assert m.n_mismatch == 0
 
 
-@pytest.mark.parametrize("layer", ["L56", "L14"])
+# (layer, index into the bench's candidate list, tiles per persistent CTA / pair at batch 32):
+# L56 compact rows: 32 x 26 = 832 tiles over 148 CTAs (6 per CTA); L56 power-of-two rows: 896 tiles (7);
+# L14's CTA-pair schedule: 64 pair tiles for 74 pairs (one each; its multi-tile form is in test_gpu_multitile.py)
+@pytest.mark.parametrize("layer,idx,per_cta", [("L56", 0, 6), ("L56", 1, 7), ("L14", 0, 1)])
 @pytest.mark.parametrize("mode", MODES)
-def test_conv_resnet_layers_batch32_bench_schedule(layer, mode):
+def test_conv_resnet_layers_batch32_bench_schedule(layer, idx, per_cta, mode):
     h, c = {"L56": (56, 64), "L14": (14, 256)}[layer]
     d = xtc.conv2d_desc(32, h, h, c, c, 3, 3, 1, 1, "bf16", "bf16")
-    sch = xtc.schedule(**CONV_SCHEDS[layer][0])
-    # L56: 896 halo tiles over 148 CTAs (7 per CTA); L14's CTA-pair schedule has 56 pair tiles for 74 pairs
-    # (one each; its multi-tile form is in test_gpu_multitile.py)
-    assert tiles_per_pair(d, sch) == (7 if layer == "L56" else 1)
+    sch = xtc.schedule(**CONV_SCHEDS[layer][idx])
+    assert tiles_per_pair(d, sch) == per_cta
     run_conv(d, "bf16", "bf16", sch, mode, seed=111)
 
 

@@ -10,7 +10,7 @@ import torch.nn.functional as F
 import paper_2512_16512_b200 as xtc
 from paper_2512_16512_b200.bench_extras import HALO
 
-REPS = 3
+REPS = int(os.environ.get("REPS", "3"))
 torch.backends.cudnn.benchmark = True
 VARIANTS = json.loads(os.environ.get("VARIANTS", "null")) or {
     "L56": {"pow2-tma": dict(HALO, tile_n=64, stages=2, b_resident=1),

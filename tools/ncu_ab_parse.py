@@ -13,7 +13,8 @@ for name, t in seq:
         groups.append(cur)
     elif cur is not None:
         cur.append((name, t))
-REPS = 3
+import os
+REPS = int(os.environ.get("REPS", "3"))
 for label, g in zip(order, groups):
     # the variant's own REPS launches: cuDNN's first REPS kernels, ours the first REPS xtc kernels (the
     # group also holds the next layer's setup kernels up to the next marker)
