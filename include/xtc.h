@@ -167,7 +167,12 @@ typedef enum { XTC_SPLITK_ORDERED = 0, XTC_SPLITK_ATOMIC = 1, XTC_SPLITK_CLUSTER
  *                                                   NHWC patch (tile rows + R-1 rows, Wp >= Q+S-1 pixel
  *                                                   slots) per tile, every filter tap (r, s) read as a
  *                                                   row-shifted view of it; tile_m = 128 or 256 virtual
- *                                                   rows (128/Wp output rows each), cluster_m 1, split_k 1
+ *                                                   rows (128/Wp output rows each), cluster_m 1, split_k 1;
+ *                                                   2 = the same with compact rows: Wc = Q+S-1 slots per
+ *                                                   row and tiles of consecutive virtual rows that may
+ *                                                   start mid-row (one CTA per tile, no s-fold, no split,
+ *                                                   buffer_c 0); the warp-MMA engine reads 1 / 2 as its
+ *                                                   TMA-staged / thread-filled patch
  * bufferize    buffer_c             : 1 = SMEM-staged output + TMA store, 0 = direct stores
  *                          acc_buffers            : tcgen05 TMEM accumulator buffers (1|2)
  * fuse         fuse                   : 1 = the op's consumer (relu) is applied in the producer's
