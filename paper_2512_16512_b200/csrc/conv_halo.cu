@@ -727,8 +727,14 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
                                      bf16_out, p.cons_red, p.bias, (int)threadIdx.x - 128, false, trace);
             }
         }
-        if (p.buffer_c && lane == 0) ptx::bulk_wait<0>();
-        if (trace && warp == 4 && lane == 0) trace[6] = ptx::globaltimer();   // XTC_TRACE: stores complete
+        // before the CTA exits its TMA stores must have READ the staging SMEM; their global writes complete
+        // with the grid (what a later kernel or the host sees).  Waiting for the writes themselves put the
+        // last tile's write latency on every launch's critical path.  (65536: A/B diagnostics, full wait.)
+        if (p.buffer_c && lane == 0) {
+            if (p.debug_skip_mma & 65536) ptx::bulk_wait<0>();
+            else ptx::bulk_wait_read<0>();
+        }
+        if (trace && warp == 4 && lane == 0) trace[6] = ptx::globaltimer();   // XTC_TRACE: stores read
         if (phs) {
             lap(4);
             for (int k = 0; k < 5; ++k) trace[kTracePhase + k] = ph_t[k];

@@ -480,7 +480,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             }
             if (issued) {
             } else if (trace) mma_loop(std::integral_constant<int, -1>{}, T1{}, T0{});
-            else if (p.debug_skip_mma) mma_loop(std::integral_constant<int, 0>{}, T0{}, T0{});
+            else if (p.debug_skip_mma & ~65536) mma_loop(std::integral_constant<int, 0>{}, T0{}, T0{});
             else if (n_a == 1) mma_loop(std::integral_constant<int, 1>{}, T0{}, T0{});
             else if (n_a == 2) mma_loop(std::integral_constant<int, 2>{}, T0{}, T0{});
             else if (n_a == 4) mma_loop(std::integral_constant<int, 4>{}, T0{}, T0{});
@@ -776,8 +776,14 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                                      p.C, p.ldc, p.out_bf16 != 0, p.cons_red, p.bias, (int)threadIdx.x - 128, p.buffer_c != 0, trace);
             }
         }
-        if (p.buffer_c && lane == 0) ptx::bulk_wait<0>();
-        if (trace && warp == 4 && lane == 0) trace[6] = ptx::globaltimer();   // XTC_TRACE: stores complete
+        // before the CTA exits its TMA stores must have READ the staging SMEM; their global writes complete
+        // with the grid (what a later kernel or the host sees).  Waiting for the writes themselves put the
+        // last tile's write latency on every launch's critical path.  (65536: A/B diagnostics, full wait.)
+        if (p.buffer_c && lane == 0) {
+            if (p.debug_skip_mma & 65536) ptx::bulk_wait<0>();
+            else ptx::bulk_wait_read<0>();
+        }
+        if (trace && warp == 4 && lane == 0) trace[6] = ptx::globaltimer();   // XTC_TRACE: stores read
     }
 
     ptx::tc_fence_before();

@@ -48,9 +48,10 @@ inline cudaError_t ensure_nonportable_cluster(F* kernel) {
 XTC_HD constexpr int simt_max_threads(int tm, int tn) {
     return tm * tn >= 32 ? 256 : (tm * tn >= 16 ? 512 : 1024);
 }
-// Register-tiled variants ask for two resident CTAs per SM (<= 128 regs/thread for the
-// 256-thread 8x8 tiles): one CTA leaves 2 warps per scheduler, too few to hide LDS latency.
-XTC_HD constexpr int simt_min_blocks(int tm, int tn) { return tm * tn >= 32 ? 2 : 1; }
+// Register-tiled variants ask for two resident CTAs per SM (<= 128 regs/thread): one CTA leaves 2 warps
+// per scheduler, too few to hide LDS latency -- except the 8x8 tile, whose 64 accumulators + 16 fragments
+// spilled to the stack at 128 registers (136 bytes, 3x slower); it gets the whole register file.
+XTC_HD constexpr int simt_min_blocks(int tm, int tn) { return tm * tn >= 64 ? 1 : (tm * tn >= 32 ? 2 : 1); }
 
 // Tile-order mapping: the schedule's interchange + grouped raster.
 // Linear tile id -> (split segment ks, tile row mb, tile col nb).

@@ -2,8 +2,9 @@
 the ~1 us event-timer grid (profiles/r02c_event_timer_quantisation.txt).  Usage:
   PYTHONPATH=. python tools/ab_mean.py conv B H C  'json-sched' ['json-sched' ...]   (3x3 s1 p1, C -> C, bf16)
   PYTHONPATH=. python tools/ab_mean.py matmul N 'json-sched' ...
-  a schedule string 'cudnn' / 'cublas' times the library call on the same operands (context only)."""
-import json, statistics, sys
+  a schedule string 'cudnn' / 'cublas' times the library call on the same operands (context only);
+  'env=MASK:json-sched' runs that schedule with XTC_DEBUG_SKIP=MASK (read by the library at each launch)."""
+import json, os, statistics, sys
 import torch
 import torch.nn.functional as F
 import paper_2512_16512_b200 as xtc
@@ -35,8 +36,9 @@ if a[0] == "conv":
         if s == "cudnn":
             fns.append(lambda: F.conv2d(x, w, padding=1))
         else:
-            op = xtc.Op(d).apply(xtc.schedule(**json.loads(s)))
-            fns.append(lambda op=op: op.run(xn, wn, y))
+            mask, js = (s[4:].split(":", 1) if s.startswith("env=") else ("0", s))
+            op = xtc.Op(d).apply(xtc.schedule(**json.loads(js)))
+            fns.append(lambda op=op, mask=mask: (os.environ.__setitem__("XTC_DEBUG_SKIP", mask), op.run(xn, wn, y)))
         labels.append(s)
 else:
     n = int(a[1])
@@ -47,8 +49,9 @@ else:
         if s == "cublas":
             fns.append(lambda: torch.matmul(A, Bm, out=Cm))
         else:
-            op = xtc.Op(xtc.matmul_desc(n, n, n, "bf16", "bf16")).apply(xtc.schedule(**json.loads(s)))
-            fns.append(lambda op=op: op.run(A, Bm, Cm))
+            mask, js = (s[4:].split(":", 1) if s.startswith("env=") else ("0", s))
+            op = xtc.Op(xtc.matmul_desc(n, n, n, "bf16", "bf16")).apply(xtc.schedule(**json.loads(js)))
+            fns.append(lambda op=op, mask=mask: (os.environ.__setitem__("XTC_DEBUG_SKIP", mask), op.run(A, Bm, Cm)))
         labels.append(s)
 for f in fns:
     for _ in range(5):
