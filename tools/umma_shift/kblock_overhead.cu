@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(256, 1) k(int n, int u, int mode, unsigned lon
                 if (mode == 1) { ptx::mbar_wait(&full[0], 0); ptx::tc_fence_after(); }
                 if (mode == 2) { ptx::mbar_wait(&full[s], ph); ptx::tc_fence_after(); }
                 if (u == 4) {                          // the kernels' form: k-steps unrolled, constant offsets
-                    const uint64_t bk = bd0 + (uint64_t)((v & 2) ? (kb % 9) * 512 : 0);
+                    const uint64_t bk = bd0 + (uint64_t)((v & 2) ? (kb % 8) * 512 : 0);
                     const uint32_t dk = tmem + (uint32_t)((v & 4) ? ((kb / 9) & 1) * 128 : 0);
                     const uint32_t acc0 = ((v & 4) && kb % 9 == 0) ? 0u : 1u;
 #pragma unroll
@@ -67,7 +67,9 @@ __global__ void __launch_bounds__(256, 1) k(int n, int u, int mode, unsigned lon
                         ptx::umma<false, 1>(tmem, ad0 + (uint64_t)((j & 3) * 2), bd0 + (uint64_t)((j & 3) * 128), idesc,
                                             (kb | j) ? 1u : 0u);
                 }
-                if (mode) ptx::umma_commit<1>(&empty[s]);
+                if (mode == 1 || mode == 2) ptx::umma_commit<1>(&empty[s]);
+                if (mode == 3 && kb % 9 == 8) ptx::umma_commit<1>(&empty[(kb / 9) & 1]);   // a commit per 36 UMMAs, no waits
+                if (mode == 4) ptx::umma_commit<1>(&empty[s]);                            // a commit per k-block, no waits
                 if (++s == S) { s = 0; ph ^= 1u; }
             }
             ptx::umma_commit<1>(done);
@@ -102,8 +104,8 @@ int main() {
     printf("N   U/kb  mode  cycles/UMMA  (floor 128*N/256)\n");
     for (int n : {64, 128})
         for (int u : {4})
-            for (int mode : {0})
-            for (int v = 0; v < 8; ++v) {
+            for (int mode : {0, 3, 4})
+            for (int v : {0, 1, 2, 6}) {
                 k<<<148, 256, smem>>>(n, u, mode, d, v);
                 cudaError_t e = cudaDeviceSynchronize();
                 if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); return 1; }
