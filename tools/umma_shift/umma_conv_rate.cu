@@ -57,8 +57,10 @@ __global__ void __launch_bounds__(256, 1) k_conv(int n, int random, int taps_mod
                     const uint64_t bd = bd0 + (uint64_t)(tap * 64 * 128 / 16);
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk)
-                        ptx::umma<false, 1>(d, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 16 * 8), idesc,
-                                            (tap0 | kk) ? 1u : 0u);
+                        // v&8: two independent accumulator chains (taps alternate between d and d + 128 columns)
+                        ptx::umma<false, 1>((v & 8) ? d + (uint32_t)((tap0 & 1) * 128) : d, ad + (uint64_t)(kk * 2),
+                                            bd + (uint64_t)(kk * 16 * 8), idesc,
+                                            ((v & 8) ? ((tap0 >> 1) | kk) : (tap0 | kk)) ? 1u : 0u);
                 }
                 if (commits) ptx::umma_commit<1>(&tb[t & 1]);   // like the conv kernel: pempty / tfull per tile
                 if (commits > 1) ptx::umma_commit<1>(&tb[t & 1]);
@@ -87,13 +89,13 @@ int main() {
     cudaFuncSetAttribute(k_conv, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     unsigned long long h[148];
     printf("N   data    taps        cycles/UMMA (median CTA over 148)   floor = 128*N/256\n");
-    for (int nt : {64, 7, 2})
+    for (int nt : {64, 7})
     for (int n : {64})
         for (int rnd : {1})
             for (int cm : {1})
             for (int tm : {1})
             for (int fe : {1})
-            for (int vv : {0, 3}) {
+            for (int vv : {0, 8}) {
                 cudaMemcpyToSymbol(g_tiles, &nt, sizeof nt);
                 printf("tiles %d: ", nt);
                 k_conv<<<148, 256, smem>>>(n, rnd, tm, cm, d, fe, vv);
