@@ -652,6 +652,9 @@ def main_xtc(args):
         extras["cublas_same_protocol"] = cublas_same_protocol(torch, stream, a, b, c, op, sp, args.steps, flops)
         try:
             from paper_2512_16512_b200.bench_extras import run_extras
+            # a cool-down after ~0.4 s of back-to-back 8192^3 launches at the power cap: the first small
+            # config measured right after them read 15-17 us at 1024^3 on some boxes instead of 12.3 us
+            time.sleep(2.0)
             extras.update(run_extras(xtc, torch, dev, peak_tf))
         except Exception as ex:   # extras are secondary: report, don't fail the headline
             extras = {"error": repr(ex)}

@@ -1058,9 +1058,13 @@ static xtc_status measure_impl(xtc_op op, const void* A, const void* B, void* C,
         CU_TRY(cudaEventCreate(&e), "cudaEventCreate");
         op->evs.push_back(e);
     }
-    // keep the GPU busy while the reps are enqueued (host enqueue is ~3-6 us per rep
-    // with cached launch attributes; budget 8 us per rep + 20 us)
-    CU_TRY(launch_delay(std::min<uint64_t>(8000ull * (uint64_t)R + 20000ull, 20000000ull), st), "delay");
+    // keep the GPU busy while the reps are enqueued: if the host falls behind, a rep's start event
+    // executes before its kernel is even submitted and the host's enqueue time lands inside the
+    // measurement.  Host enqueue is ~3-6 us per rep (flush + 2 events + the launch) on a quiet host;
+    // budget 30 us per rep + 20 us (XTC_MEASURE_DELAY_NS: per-rep budget, diagnostics)
+    uint64_t per_rep = 30000ull;
+    if (const char* e = getenv("XTC_MEASURE_DELAY_NS")) per_rep = strtoull(e, nullptr, 10);
+    CU_TRY(launch_delay(std::min<uint64_t>(per_rep * (uint64_t)R + 20000ull, 20000000ull), st), "delay");
     for (int i = 0; i < R; ++i) {
         if (cfg->flush_l2) CU_TRY(launch_flush(g_flush_buf[op->device], g_flush_bytes[op->device], (uint32_t)i, st), "flush");
         CU_TRY(cudaEventRecord(op->evs[2 * i], st), "event");
