@@ -510,6 +510,45 @@ def test_schedule_invariance_tcgen05_sampled():
     assert n == 160
 
 
+def test_schedule_invariance_conv_sampled():
+    """north_star's invariance property for the conv2d kernels: 96 random LEGAL schedules of one ragged
+    3x3 conv (Q + S - 1 = 25: power-of-two rows 32, compact rows 25) drawn over the halo patch layouts
+    (pack_halo 0 = TMA im2col, 1, 2), tile shapes, stages, epilogues, accumulator buffers, persistence and
+    grid size, resident / ring / multicast filters, the CTA pair, split-K (ordered and cluster-reduced) --
+    every one bit-exact on integer data against the on-chip fp64 reference, which equals the oracle."""
+    import random
+    d = xtc.conv2d_desc(3, 19, 23, 64, 128, 3, 3, 1, 1, "bf16", "bf16")
+    rng = random.Random(17)
+    cands, seen = [], set()
+    for _ in range(20000):
+        k = dict(engine=1, swizzle=128, pack_halo=rng.choice([0, 1, 2]), tile_m=rng.choice([128, 256]),
+                 tile_n=rng.choice([64, 128]), tile_k=rng.choice([64, 128]), stages=rng.choice([2, 3, 4]),
+                 buffer_c=rng.choice([0, 1]), acc_buffers=rng.choice([1, 2]), persistent=rng.choice([0, 1]),
+                 b_resident=rng.choice([0, 0, 1]), cluster_m=rng.choice([1, 1, 2]), inner_m=rng.choice([0, 0, 256]),
+                 split_k=rng.choice([1, 1, 1, 2, 3]), split_k_mode=rng.choice([0, 2]), grid_sms=rng.choice([0, 0, 7]))
+        key = tuple(sorted(k.items()))
+        if key in seen:
+            continue
+        seen.add(key)
+        sch = xtc.schedule(**k)
+        if xtc.xtc_schedule_check(d, sch, 148)[0] == xtc.XTC_OK:
+            cands.append(sch)
+        if len(cands) == 96:
+            break
+    assert len(cands) == 96
+    assert {c.pack_halo for c in cands} == {0, 1, 2}
+    M, N, K = xtc.gemm_view(d)
+    x = dev_tensor((d.batch, d.h, d.w, d.c), "bf16", 41, MODE_INT)
+    w = dev_tensor((d.r, d.s, d.c, d.f), "bf16", 42, MODE_INT)
+    y = torch.empty((M, N), dtype=torch.bfloat16, device="cuda:0")
+    recs = xtc.Op(d).sweep(cands, x, w, y, xtc.measure_cfg(warmup=0, repeats=1, validate=1, exact=1))
+    bad = [(i, cands[i].as_dict(), r.status, r.valid, r.n_mismatch) for i, r in enumerate(recs)
+           if r.status != 0 or r.valid != 1 or r.n_mismatch != 0]
+    assert not bad, bad[:3]
+    O, D = oracle_conv(d, "bf16", MODE_INT, 41, 42)
+    check_against_oracle(y, O, D, "bf16", True, 0.0)
+
+
 def test_schedule_invariance_simt_sampled():
     from paper_2512_16512_b200.strategy import GpuStrategy
     desc = xtc.matmul_desc(200, 136, 328, "f32", "f32")
