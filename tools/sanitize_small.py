@@ -47,6 +47,12 @@ CASES = {
     "conv_halo_sfold": ("conv", (2, 56, 56, 64, 64), dict(engine=1, tile_m=128, tile_n=64, tile_k=64, stages=2,
                                                          pack_halo=1, b_resident=1, inner_n=192, acc_buffers=2,
                                                          persistent=1, grid_sms=4)),
+    "conv_halo_compact": ("conv", (2, 56, 56, 64, 64), dict(engine=1, tile_m=128, tile_n=64, tile_k=64, stages=2,
+                                                           pack_halo=2, buffer_c=0, b_resident=1, acc_buffers=2,
+                                                           persistent=1, grid_sms=4)),
+    "conv_halo_compact_ring": ("conv", (2, 17, 39, 64, 128), dict(engine=1, tile_m=256, tile_n=128, tile_k=64,
+                                                                  stages=3, pack_halo=2, buffer_c=0, acc_buffers=2,
+                                                                  persistent=1, grid_sms=3)),
     "conv_halo_lean": ("conv", (2, 56, 56, 64, 64), dict(engine=1, tile_m=128, tile_n=64, tile_k=64, stages=2,
                                                         pack_halo=1, b_resident=1, acc_buffers=2, persistent=1,
                                                         grid_sms=4)),
