@@ -27,6 +27,8 @@ CONV_SCHEDS = {
     # pack_halo (input packed once per output tile) first; the im2col schedules stay as candidates
     "L56": [dict(HALO, tile_n=64, stages=2, b_resident=1, pack_halo=2, buffer_c=0),   # compact rows
             dict(HALO, tile_n=64, stages=2, b_resident=1),
+            # the CTA pair with 64-byte filter halves (per-tile MMA time -14 %, but 448 pair tiles = 7 rounds)
+            dict(HALO, tile_m=256, cluster_m=2, inner_m=256, tile_n=64, stages=2, b_resident=1, buffer_c=0),
             dict(HALO, tile_m=256, tile_n=64, stages=2, b_resident=1),
             dict(TC, tile_n=64, stages=8, buffer_c=1, acc_buffers=2, persistent=1, raster_group=8, pack_warps=3),
             dict(TC, tile_n=64, stages=7, buffer_c=1, acc_buffers=2, persistent=1, pack_warps=3, b_resident=1)],

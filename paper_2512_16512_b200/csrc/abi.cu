@@ -443,7 +443,17 @@ static xtc_status encode_maps(xtc_op op, const void* A, const void* B, void* C) 
         // tf32 MN-major operands must use 32-byte swizzle atoms (UMMA SWIZZLE_128B_BASE32B)
         const CUtensorMapSwizzle bsw = tf32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B;
         op->b3d = false;
-        if (allow3d && p.N % atom == 0) {
+        if (p.halo && p.halo_b64) {
+            // the CTA pair's 64-byte filter halves: box {32 columns, tile_k rows}, 64-byte swizzle
+            cuuint64_t dims[2] = {(cuuint64_t)p.N, (cuuint64_t)p.K};
+            cuuint64_t strides[1] = {(cuuint64_t)(ldb * es)};
+            cuuint32_t box[2] = {(cuuint32_t)(atom / 2), (cuuint32_t)tile_k};
+            cuuint32_t estr[2] = {1, 1};
+            r = g_encode_tiled(&op->tmB, in_t, 2, const_cast<void*>(B), dims, strides, box, estr,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) return fail(XTC_E_CUDA, "cuTensorMapEncodeTiled(B, 64-byte halves) failed: " + std::to_string((int)r));
+        } else if (allow3d && p.N % atom == 0) {
             cuuint64_t dims[3] = {(cuuint64_t)atom, (cuuint64_t)p.K, (cuuint64_t)(p.N / atom)};
             cuuint64_t strides[2] = {(cuuint64_t)(ldb * es), (cuuint64_t)(atom * es)};
             // each CTA of a pair (or of a halo multicast cluster) loads its share of the N blocks
@@ -455,7 +465,7 @@ static xtc_status encode_maps(xtc_op op, const void* A, const void* B, void* C) 
                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
             op->b3d = (r == CUDA_SUCCESS);
         }
-        if (!op->b3d) {
+        if (!op->b3d && !(p.halo && p.halo_b64)) {
             cuuint64_t dims[2] = {(cuuint64_t)p.N, (cuuint64_t)p.K};
             cuuint64_t strides[1] = {(cuuint64_t)(ldb * es)};
             cuuint32_t box[2] = {(cuuint32_t)atom, (cuuint32_t)tile_k};
@@ -734,6 +744,7 @@ static xtc_status run_impl(xtc_op op, const void* A, const void* B, void* C, cud
             tp.pair = p.halo_pair ? 1 : 0;
             tp.sfold = p.halo_sfold;
             tp.compact = p.halo_compact ? 1 : 0;
+            tp.b64 = p.halo_b64 ? 1 : 0;
             if (p.halo_sfold > 1)                     // UMMA N = S * tile_n
                 tp.idesc = (tp.idesc & ~(0x3Fu << 17)) | ((uint32_t)((p.halo_sfold * p.sch.tile_n) >> 3) << 17);
             tp.patch_bytes = (uint32_t)p.halo_patch_bytes;

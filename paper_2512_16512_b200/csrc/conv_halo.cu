@@ -228,7 +228,9 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
     // PAIR: this CTA's half of the filter columns (128-byte blocks nblk0 ...), completing on the
     // leader's barrier bar_c
     auto load_b_pair = [&](uint8_t* dst, uint32_t bar_c, int kb, int nblk0) {
-        if (p.b3d) {
+        if (p.b64) {                                 // tile_n = one atom: this CTA's 32-column, 64-byte half
+            ptx::tma_load_2d_pair(&tmB, dst, bar_c, nblk0 * ATOM + (int)rank * (ATOM / 2), kb * p.tile_k);
+        } else if (p.b3d) {
             ptx::tma_load_3d_pair(&tmB, dst, bar_c, 0, kb * p.tile_k, nblk0);
         } else {
             for (int b = 0; b < p.tile_n / ATOM / 2; ++b)
@@ -338,8 +340,12 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
         const uint32_t tmem_base = tmem_address();
         const uint32_t b_lbo = (uint32_t)p.tile_k * 128u;
         const uint64_t adesc0 = ptx::smem_desc_sw128(ptx::smem_u32(sP), 16, 1024);
+        // B (MN-major): 128-byte swizzle rows of one 64-column atom (8-row groups 1024 bytes apart), or
+        // for the pair's 64-byte halves the SW64 layout (layout type 4, 8-row groups 512 bytes apart)
         const uint64_t bdesc0 = TF32 ? ptx::smem_desc_sw128(ptx::smem_u32(sB), b_lbo, 512, 1)
-                                     : ptx::smem_desc_sw128(ptx::smem_u32(sB), b_lbo, 1024, 2);
+                              : p.b64 ? ptx::smem_desc_sw128(ptx::smem_u32(sB), b_lbo / 2, 512, 4)
+                                      : ptx::smem_desc_sw128(ptx::smem_u32(sB), b_lbo, 1024, 2);
+        const uint32_t brow16 = ptx::pin(p.b64 ? 4u : 8u);   // 16-byte units per filter k-row in SMEM
         // every loop bound and stride pinned in a register; an atom's MSUB x (ATOM/UMMA_K) UMMAs
         // are straight-line code
         const uint32_t b_stage16 = ptx::pin(p.b_stage_bytes >> 4);
@@ -408,7 +414,7 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
 #pragma unroll
                         for (int kk = 0; kk < ATOM / UMMA_K; ++kk)
                             ptx::umma<TF32, CG>(d0 + (uint32_t)ms * tile_n, ad + (uint64_t)(ms * 1024 + kk * 2),
-                                               bd + (uint64_t)(kk * UMMA_K * 8), idesc, kk ? 1u : accf);
+                                               bd + (uint64_t)((uint32_t)(kk * UMMA_K) * brow16), idesc, kk ? 1u : accf);
                     accf = 1u;
                     const bool pw = ++pl == planes;             // plane wraps: next filter column
                     pl = pw ? 0 : pl;
@@ -441,14 +447,14 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
                     for (int rep = 0; rep < reps; ++rep)
                     for (int kb = kb0; kb < kb1; ++kb) {
                         const uint64_t bd = bdesc0 + (uint64_t)((uint32_t)kb * b_stage16);
-                        for (int a = 0; a < n_atoms; ++a) atom(bd + (uint64_t)(a * ATOM * 8));
+                        for (int a = 0; a < n_atoms; ++a) atom(bd + (uint64_t)((uint32_t)(a * ATOM) * brow16));
                     }
                 } else {
                     for (int kb = kb0; kb < kb1; ++kb) {
                         ptx::mbar_wait(&full[s], ph);
                         ptx::tc_fence_after();
                         const uint64_t bd = bdesc0 + (uint64_t)((uint32_t)s * b_stage16);
-                        for (int a = 0; a < n_atoms; ++a) atom(bd + (uint64_t)(a * ATOM * 8));
+                        for (int a = 0; a < n_atoms; ++a) atom(bd + (uint64_t)((uint32_t)(a * ATOM) * brow16));
                         if constexpr (PAIR) ptx::umma_commit<2>(&empty[s]);
                         else if constexpr (CL == 2) ptx::umma_commit_multicast(&empty[s], 0x3);
                         else ptx::umma_commit<1>(&empty[s]);

@@ -153,9 +153,15 @@ static xtc_status plan_tc_halo(const xtc_op_desc& d, const xtc_schedule& s, int 
     if (pair) {
         if (hcl != 2 || s.tile_m != 256) ILLEGAL("pack_halo: inner_m 256 (CTA pair) needs cluster_m 2 and tile_m 256");
         if (p.split_k > 1) ILLEGAL("pack_halo: the CTA pair (inner_m 256) needs split_k 1");
-        if (s.tile_n % (2 * p.atom_n))
-            ILLEGAL("pack_halo: the CTA pair needs tile_n %% %d == 0 (a 128-byte filter block per CTA)", 2 * p.atom_n);
-        if (d.f % p.atom_n) ILLEGAL("pack_halo: the CTA pair needs F %% %d == 0 (3-D filter TMA)", p.atom_n);
+        // tile_n = one 128-byte atom (bf16: 64 filter columns): each CTA holds a 32-column, 64-byte half of
+        // every filter k-block in the UMMA's 64-byte-swizzle MN-major layout (TMA SWIZZLE_64B), so the pair
+        // halves the filter operand reads per SM at F = 64 too (L56)
+        const bool half64 = s.tile_n == p.atom_n && d.in_dtype == XTC_BF16;
+        if (s.tile_n % (2 * p.atom_n) && !half64)
+            ILLEGAL("pack_halo: the CTA pair needs tile_n %% %d == 0 (a 128-byte filter block per CTA), or tile_n %d "
+                    "with bf16 (64-byte filter halves)", 2 * p.atom_n, p.atom_n);
+        if (!half64 && d.f % p.atom_n) ILLEGAL("pack_halo: the CTA pair needs F %% %d == 0 (3-D filter TMA)", p.atom_n);
+        p.halo_b64 = half64;
     }
     // inner_n = S * tile_n: the s-fold.  The S taps (r, 0..S-1) of a filter row are the N blocks of
     // ONE UMMA on the patch view of row r (N = S * tile_n): accumulator block s of virtual row v

@@ -189,6 +189,7 @@ struct Plan {
     bool halo_pair = false;             // inner_m 256: cta_group::2 UMMAs (M = 256) over a CTA pair
     int32_t halo_sfold = 1;             // inner_n = S * tile_n: the filter row's S taps folded into the UMMA N
     bool halo_compact = false;          // pack_halo 2: rows at Wc = Q + S - 1 slots, tiles of consecutive rows
+    bool halo_b64 = false;              // CTA pair with tile_n = 64 (bf16): 64-byte-swizzle filter halves per CTA
     bool ovl = false;                   // overlapped epilogue (see TcParams::ovl); 64 KB epilogue SMEM
     int32_t msub = 1;                   // tcgen05 matmul: 128-row M-subtiles per CTA (tile_m = 128*cta_group*msub)
     bool stream_k = false;              // split_k_mode 3: stream-K over the persistent grid (stream_k.cuh)
@@ -254,6 +255,8 @@ struct TcParams {
     ConvGeom cg;
     // pack_halo conv only (see Plan)
     int32_t wp, rt, msub, planes, nbuf, tpi, cl, pair;
+    int32_t b64;             // pack_halo CTA pair, tile_n 64: each CTA's filter half is 32 columns x 64 bytes
+                             // (TMA SWIZZLE_64B, UMMA MN-major SW64 descriptor: 8-row groups 512 bytes apart)
     int32_t compact;         // pack_halo 2: wp = Q + S - 1 and a tile = 128*msub consecutive virtual rows
                              // of an image (starts mid-row at TileInfo::off)
     int32_t sfold;           // pack_halo s-fold: the S taps of a filter row are the N blocks of one UMMA

@@ -185,6 +185,12 @@ HALO_CASES = [
     ((2, 28, 28, 64, 128, 3, 3, 1, "bf16", "bf16"), dict(PAIR_H, tile_n=128, stages=2, b_resident=1)),     # 32  4
     ((2, 9, 13, 64, 128, 3, 3, 1, "bf16", "f32"), dict(PAIR_H, tile_n=128, stages=2, acc_buffers=1)),      # ragged
     ((2, 14, 14, 64, 128, 3, 3, 1, "tf32", "f32"), dict(PAIR_H, tile_n=64, tile_k=32, stages=4)),          # tf32
+    # the pair at tile_n = 64 (bf16): 64-byte-swizzle filter halves (32 columns per CTA), resident and ring,
+    # two N tiles (column offsets), ragged P / Q, direct stores, fp32 out
+    ((2, 56, 56, 64, 64, 3, 3, 1, "bf16", "bf16"), dict(PAIR_H, tile_n=64, b_resident=1, stages=2)),
+    ((2, 28, 28, 64, 128, 3, 3, 1, "bf16", "bf16"), dict(PAIR_H, tile_n=64, stages=3)),
+    ((2, 9, 13, 64, 64, 3, 3, 1, "bf16", "f32"), dict(PAIR_H, tile_n=64, stages=2, buffer_c=0, acc_buffers=1)),
+    ((2, 14, 14, 128, 64, 3, 3, 1, "bf16", "bf16"), dict(PAIR_H, tile_n=64, tile_k=128, b_resident=1, stages=2)),
     # split_k: K segments (runs of taps / channel planes) as CTAs, ordered reduction
     ((1, 14, 14, 256, 256, 3, 3, 1, "bf16", "bf16"), dict(tile_n=128, stages=4, split_k=3, buffer_c=0)),
     ((1, 14, 14, 256, 256, 3, 3, 1, "bf16", "bf16"), dict(tile_n=128, stages=4, split_k=9, buffer_c=0)),

@@ -168,6 +168,18 @@ def test_pack_halo_plan():
     assert st == xtc.XTC_OK and info.num_tiles == 2, why
 
 
+def test_pack_halo_pair_64byte_filter_halves():
+    """The CTA pair at tile_n = 64 (bf16): each CTA holds a 32-column half of every filter k-block
+    (64-byte rows), so the resident L56 filter takes 9 x 64 x 32 x 2 = 36 KiB per CTA."""
+    l56 = xtc.conv2d_desc(32, 56, 56, 64, 64)
+    P = dict(HALO, tile_m=256, cluster_m=2, inner_m=256, tile_n=64)
+    st, info, why = chk(l56, **dict(P, b_resident=1))
+    assert st == xtc.XTC_OK and info.num_tiles == 32 * 28 // 2 and info.cluster_x == 2, why
+    assert info.smem_bytes == 9 * 64 * 32 * 2 + 3 * 4 * 64 * 128 + 32768 + 2048 + 64 * 32 + 16
+    st, info, why = chk(xtc.conv2d_desc(2, 28, 28, 64, 128), **dict(P, stages=3))     # ring, two N tiles
+    assert st == xtc.XTC_OK and info.num_tiles == 2 * 7 * 2 // 2, why
+
+
 def test_pack_halo_compact_plan():
     """pack_halo 2: Wc = Q + S - 1 slots per row, tiles of 128 consecutive virtual rows per image
     (ceil(P*Wc / 128) per image), patch rows = the rows spanned by a tile's largest read, + 1."""
@@ -198,7 +210,9 @@ def test_pack_halo_compact_plan():
     (xtc.conv2d_desc(2, 56, 56, 64, 64), dict(cluster_m=2), "even number of 128-byte filter blocks"),
     (xtc.conv2d_desc(1, 14, 14, 256, 256), dict(cluster_m=2, tile_n=128, tile_m=256), "even number of M tiles"),
     (xtc.conv2d_desc(2, 14, 14, 256, 256), dict(inner_m=256, tile_n=128), "cluster_m 2 and tile_m 256"),
-    (xtc.conv2d_desc(2, 56, 56, 64, 64), dict(inner_m=256, cluster_m=2, tile_m=256, tile_n=64), "tile_n % 128"),
+    (xtc.conv2d_desc(2, 56, 56, 64, 256), dict(inner_m=256, cluster_m=2, tile_m=256, tile_n=192), "tile_n % 128"),
+    (xtc.conv2d_desc(2, 14, 14, 64, 64, 3, 3, 1, 1, "tf32", "f32"), dict(inner_m=256, cluster_m=2, tile_m=256, tile_n=32,
+                                                                      tile_k=32), "64-byte filter halves"),
     (xtc.conv2d_desc(1, 7, 7, 256, 256), dict(inner_m=256, cluster_m=2, tile_m=256, tile_n=128), "even number of M tiles"),
     (xtc.conv2d_desc(2, 14, 14, 256, 256), dict(inner_m=256, cluster_m=2, tile_m=256, tile_n=128, split_k=2,
                                                 buffer_c=0), "split_k 1"),
