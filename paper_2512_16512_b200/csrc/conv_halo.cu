@@ -88,13 +88,13 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
         ptx::prefetch_tmap(&tmB);
         if (p.buffer_c) ptx::prefetch_tmap(&tmY);
     }
-    // early start (one CTA per cluster, CL = 1 and no cluster split): after the barrier inits the two
+    // early start: after the barrier inits (made visible CTA-wide, or cluster-wide for a CTA pair /
+    // multicast cluster / cluster split, whose TMAs and arrives target the peers' barriers) the two
     // producer warps (0: patches, 3: filter) start loading at once and walk their tiles without the
     // SMEM tile table; only the TMEM users (warps 1, 2, 4..7) build the table and meet at a named
     // barrier.  (Trace at L56 N=32 before: the setup barrier at 0.8 us, the first patch issued at
-    // 1.18 us, its data at 2.46 us.)  With CL = 2 / a cluster split the peers' barriers must exist
-    // before a multicast, so those keep the table-then-cluster-barrier order.
-    const bool early = CL == 1 && !kclu && !(p.debug_skip_mma & 8192);   // (8192: A/B diagnostics)
+    // 1.18 us, its data at 2.46 us.)
+    const bool early = !(p.debug_skip_mma & 8192);   // (8192: A/B diagnostics)
     if (warp == 1 && lane == 0) {
         // a multicast stage is free only when the MMAs of every CTA in the cluster have read it
         for (int s = 0; s < S; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], PAIR ? 1 : CL); }
@@ -177,7 +177,10 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
     // (measured ~1100 cycles per tile per role in XTC_TRACE phase totals).
     TileInfo* const tinfo = reinterpret_cast<TileInfo*>((reinterpret_cast<uintptr_t>(tmem_slot) + 4 + 15) & ~uintptr_t(15));
     const bool producer = warp == 0 || warp == 3;
-    if (early) __syncthreads();                  // the barrier inits are visible; producers go
+    if (early) {                                 // the barrier inits are visible; producers go
+        if (CL == 2 || kclu) ptx::cluster_sync();
+        else __syncthreads();
+    }
     if (!(early && producer)) {
         // early: the 192 threads of warps 1, 2, 4..7 fill the table; else all 256
         const int ti0 = early ? (warp < 3 ? (int)threadIdx.x - 32 : (int)threadIdx.x - 64) : (int)threadIdx.x;
