@@ -126,6 +126,17 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
         int mb, nb;
         tile_coords(p.tm, t, mb, nb, ks);
         if (kclu) ks = (int)krank;
+        if (PAIR && p.compact) {
+            // compact rows + CTA pair: pair tile mb = (image pair i, tile j); rank r takes image 2i + r, tile j, so
+            // both CTAs' A views start at the same slot offset (the leader's descriptors address both patches)
+            const int ip = mb / p.tpi, j = mb - ip * p.tpi;
+            nimg = 2 * ip + (int)rank;
+            const int v0 = j * 128 * MSUB;
+            p0 = v0 / p.wp;
+            off = v0 - p0 * p.wp;
+            n0 = nb * p.tile_n;
+            return;
+        }
         mb = mb * CL + (int)rank;                    // CL = 2: the loop runs over M-tile pairs
         nimg = mb / p.tpi;
         if (p.compact) {

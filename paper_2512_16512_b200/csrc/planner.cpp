@@ -203,7 +203,10 @@ static xtc_status plan_tc_halo(const xtc_op_desc& d, const xtc_schedule& s, int 
     while (wp < Q + d.s - 1) wp *= 2;
     if (compact) {
         wp = (int)(Q + d.s - 1);
-        if (pair || hcl != 1) ILLEGAL("pack_halo 2 (compact rows): one CTA per tile (cluster_m 1, inner_m 128)");
+        // the CTA pair reads both CTAs' A views through the leader's descriptor, so both tiles must start at the
+        // same slot offset: the pair takes tile j of images 2i and 2i + 1 (an even batch)
+        if (hcl != 1 && !pair) ILLEGAL("pack_halo 2 (compact rows): cluster_m 2 only as the CTA pair (inner_m 256)");
+        if (pair && d.batch % 2) ILLEGAL("pack_halo 2 (compact rows) with the CTA pair needs an even batch (images 2i, 2i+1)");
         if (sfold > 1) ILLEGAL("pack_halo 2 (compact rows): no s-fold (inner_n must be tile_n)");
         if (p.split_k > 1 || p.stream_k) ILLEGAL("pack_halo 2 (compact rows): split_k must be 1");
         // a warp's 32 rows start mid-row and wrap into the next output row; the TMA store box of

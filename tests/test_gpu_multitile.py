@@ -170,6 +170,9 @@ CONV_CASES = [
     # the CTA pair with 64-byte filter halves (tile_n 64): 112 pair tiles over 5 pairs
     ("halo-pair64-L56-n8-10sm", (8, 56, 56, 64, 64), dict(HALO, tile_m=256, cluster_m=2, inner_m=256, tile_n=64,
                                                           stages=2, b_resident=1, grid_sms=10)),
+    ("halo-pair64-compact-L56-n8-10sm", (8, 56, 56, 64, 64), dict(HALO, tile_m=256, cluster_m=2, inner_m=256,
+                                                                  tile_n=64, stages=2, b_resident=1, pack_halo=2,
+                                                                  buffer_c=0, grid_sms=10)),
     # compact rows (pack_halo 2) at batch 8: 8 x 26 = 208 tiles over 148 CTAs, and 52 tiles on 11 SMs
     ("halo-compact-L56-n8", (8, 56, 56, 64, 64), dict(HALO, pack_halo=2, buffer_c=0, tile_n=64, stages=2,
                                                       b_resident=1)),

@@ -218,6 +218,12 @@ HALO_CASES = [
                                                         buffer_c=0, grid_sms=3)),
     ((2, 13, 13, 64, 64, 3, 3, 1, "bf16", "f32"), dict(pack_halo=2, tile_n=64, stages=2, buffer_c=0)),
     ((2, 14, 14, 64, 64, 3, 3, 1, "tf32", "f32"), dict(pack_halo=2, tile_n=64, tile_k=32, stages=4, buffer_c=0)),
+    # compact rows with the CTA pair (tile j of images 2i and 2i + 1): F = 64 halves, a two-N-tile ring, ragged
+    ((4, 56, 56, 64, 64, 3, 3, 1, "bf16", "bf16"), dict(PAIR_H, pack_halo=2, tile_n=64, b_resident=1, stages=2,
+                                                        buffer_c=0)),
+    ((2, 17, 39, 64, 256, 3, 3, 1, "bf16", "f32"), dict(PAIR_H, pack_halo=2, tile_n=128, stages=3, buffer_c=0)),
+    ((2, 9, 102, 64, 64, 3, 3, 1, "bf16", "bf16"), dict(PAIR_H, pack_halo=2, tile_n=64, stages=2, buffer_c=0,
+                                                        grid_sms=4)),
 ]
 
 

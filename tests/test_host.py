@@ -196,6 +196,9 @@ def test_pack_halo_compact_plan():
     assert info.smem_bytes == 9 * 8192 + 3 * 45056 + 2048 + 64 * 32 + 16
     st, info, why = chk(l56, **dict(C, tile_m=256, b_resident=1))
     assert st == xtc.XTC_OK and info.num_tiles == 32 * (-(-56 * 58 // 256)), why
+    # with the CTA pair (tile j of images 2i, 2i+1): 16 x 26 pair tiles
+    st, info, why = chk(l56, **dict(C, tile_m=256, cluster_m=2, inner_m=256, b_resident=1))
+    assert st == xtc.XTC_OK and info.num_tiles == 16 * 26 and info.cluster_x == 2, why
     # a power-of-two width gains nothing but stays legal: L14 (Wc = 16)
     l14 = xtc.conv2d_desc(4, 14, 14, 256, 256)
     st, info, why = chk(l14, **dict(C, tile_n=128, stages=4))
@@ -225,6 +228,8 @@ def test_pack_halo_compact_plan():
     (xtc.conv2d_desc(2, 56, 56, 64, 64), dict(pack_halo=3), "pack_halo"),
     # pack_halo 2 (compact rows): one CTA per tile, no s-fold, no split, TMA-store staging needs Wc >= 32
     (xtc.conv2d_desc(2, 56, 56, 64, 128), dict(pack_halo=2, cluster_m=2, tile_n=128, buffer_c=0), "compact rows"),
+    (xtc.conv2d_desc(3, 56, 56, 64, 64), dict(pack_halo=2, cluster_m=2, inner_m=256, tile_m=256, buffer_c=0),
+     "even batch"),
     (xtc.conv2d_desc(2, 56, 56, 64, 64), dict(pack_halo=2, inner_n=192, b_resident=1, buffer_c=0), "compact rows"),
     (xtc.conv2d_desc(2, 56, 56, 64, 64), dict(pack_halo=2, split_k=3, buffer_c=0), "split_k must be 1"),
     (xtc.conv2d_desc(2, 56, 56, 64, 64), dict(pack_halo=2, buffer_c=1), "buffer_c 0"),
