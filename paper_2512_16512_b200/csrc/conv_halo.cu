@@ -611,20 +611,23 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
                         }
                     }
                     lap(2);
+                    // stream-K partial slot, column-group major: float4 (col/4, virtual row v) at (col/4)*128*MSUB + v,
+                    // so a warp's 32 rows of one 4-column group are 512 contiguous bytes (coalesced both ways; a
+                    // row-major slot made every 16-byte access of a warp touch 32 lines)
                     if (sk_contrib) {
-                        uint4* dst = reinterpret_cast<uint4*>(p.Wk + cluster_id * p.sk_slot + (int64_t)v * p.tile_n + c);
+                        uint4* dst = reinterpret_cast<uint4*>(p.Wk + cluster_id * p.sk_slot) + (int64_t)(c / 4) * (128 * MSUB) + v;
 #pragma unroll
                         for (int j = 0; j < 8; ++j)
-                            dst[j] = make_uint4(vals[4 * j], vals[4 * j + 1], vals[4 * j + 2], vals[4 * j + 3]);
+                            dst[(int64_t)j * (128 * MSUB)] = make_uint4(vals[4 * j], vals[4 * j + 1], vals[4 * j + 2], vals[4 * j + 3]);
                         continue;
                     }
                     if (sk_own) {
                         for (int64_t g2 = cluster_id + 1; g2 <= sk_last; ++g2) {
-                            const float4* src =
-                                reinterpret_cast<const float4*>(p.Wk + g2 * p.sk_slot + (int64_t)v * p.tile_n + c);
+                            const float4* src = reinterpret_cast<const float4*>(p.Wk + g2 * p.sk_slot) +
+                                                (int64_t)(c / 4) * (128 * MSUB) + v;
 #pragma unroll
                             for (int j = 0; j < 8; ++j) {
-                                const float4 w = __ldcg(src + j);
+                                const float4 w = __ldcg(src + (int64_t)j * (128 * MSUB));
                                 vals[4 * j] = __float_as_uint(__uint_as_float(vals[4 * j]) + w.x);
                                 vals[4 * j + 1] = __float_as_uint(__uint_as_float(vals[4 * j + 1]) + w.y);
                                 vals[4 * j + 2] = __float_as_uint(__uint_as_float(vals[4 * j + 2]) + w.z);

@@ -624,20 +624,22 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 uint32_t v[32];
                 ptx::tmem_ld_32x32b_x32(t_row + c, v);
                 ptx::tmem_ld_wait();
-                if (sk_contrib) {                  // slot [128 rows][tile_n] fp32, row = TMEM lane
-                    uint4* dst = reinterpret_cast<uint4*>(p.Wk + cluster_id * p.sk_slot +
-                                                          (int64_t)(32 * q + lane) * p.tile_n + c);
+                // slot of tile_n/4 column groups x 128 rows (row = TMEM lane) of float4: a warp's 32 rows of one
+                // group are 512 contiguous bytes, so partial stores and the owner's loads are coalesced
+                if (sk_contrib) {
+                    uint4* dst = reinterpret_cast<uint4*>(p.Wk + cluster_id * p.sk_slot) + (int64_t)(c / 4) * 128 + 32 * q + lane;
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) dst[j] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                    for (int j = 0; j < 8; ++j)
+                        dst[(int64_t)j * 128] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
                     continue;
                 }
                 if (sk_own) {                      // + the later k-ranges, ascending
                     for (int64_t g2 = cluster_id + 1; g2 <= sk_last; ++g2) {
-                        const float4* src = reinterpret_cast<const float4*>(
-                            p.Wk + g2 * p.sk_slot + (int64_t)(32 * q + lane) * p.tile_n + c);
+                        const float4* src = reinterpret_cast<const float4*>(p.Wk + g2 * p.sk_slot) +
+                                            (int64_t)(c / 4) * 128 + 32 * q + lane;
 #pragma unroll
                         for (int j = 0; j < 8; ++j) {
-                            const float4 w = __ldcg(src + j);
+                            const float4 w = __ldcg(src + (int64_t)j * 128);
                             v[4 * j] = __float_as_uint(__uint_as_float(v[4 * j]) + w.x);
                             v[4 * j + 1] = __float_as_uint(__uint_as_float(v[4 * j + 1]) + w.y);
                             v[4 * j + 2] = __float_as_uint(__uint_as_float(v[4 * j + 2]) + w.z);
