@@ -715,6 +715,21 @@ def test_consumer_conv_simt_and_unfused(cons):
                      MODE_INT)
 
 
+@pytest.mark.parametrize("cons", CONS)
+def test_consumer_halo_compact_rows_and_pair64(cons):
+    """The round-2 halo layouts with every consumer combination (bias, relu, accumulate): compact rows
+    (direct stores at a mid-row tile start), the F = 64 CTA pair (64-byte filter halves; TMA store and direct),
+    and compact rows with the pair (images 2i, 2i+1)."""
+    L56 = lambda: xtc.conv2d_desc(2, 56, 56, 64, 64, 3, 3, 1, 1, "bf16", "bf16")
+    pair = dict(tile_m=256, cluster_m=2, inner_m=256, tile_n=64, stages=2, b_resident=1, persistent=1, fuse=1)
+    run_consumer(L56(), tc(pack_halo=2, tile_n=64, stages=2, b_resident=1, buffer_c=0, persistent=1, acc_buffers=2,
+                           fuse=1), cons, "bf16", "bf16", MODE_INT)
+    run_consumer(L56(), tc(pack_halo=1, acc_buffers=2, **pair), cons, "bf16", "bf16", MODE_INT)
+    run_consumer(xtc.conv2d_desc(2, 9, 13, 64, 64, 3, 3, 1, 1, "bf16", "f32"),
+                 tc(pack_halo=1, buffer_c=0, acc_buffers=1, **pair), cons, "bf16", "f32", MODE_INT)
+    run_consumer(L56(), tc(pack_halo=2, buffer_c=0, acc_buffers=2, **pair), cons, "bf16", "bf16", MODE_INT)
+
+
 def test_consumer_halo_split_k_in_the_reduction():
     run_consumer(xtc.conv2d_desc(1, 14, 14, 256, 256, 3, 3, 1, 1, "bf16", "bf16"),
                  tc(pack_halo=1, tile_n=128, stages=4, split_k=4, buffer_c=0, fuse=1), "bias+relu", "bf16", "bf16",
