@@ -242,10 +242,13 @@ struct TcParams {
     int32_t a3d, b3d;        // one 3-D TMA per stage for all 128-B atoms of A / B (tmA / tmB are 3-D maps)
     int32_t debug_late_alloc;  // diagnostics (A/B): XTC_DEBUG_LATE_ALLOC=1 allocates TMEM before the
                                // prologue barrier, i.e. the producers wait for the allocation
-    int32_t debug_skip_mma;  // diagnostics only, output invalid: XTC_DEBUG_SKIP_MMA, or XTC_DEBUG_SKIP=mask
-                             // (conv_halo: 1 no MMAs, 2 no patch TMA, 4 no output stores, 8 no TMEM drain,
-                             // 256 no tap shifts, 512 every UMMA twice, 1024 (+64) free-run MMA warp:
-                             // no patch loads, no per-tile waits or commits)
+    int32_t debug_skip_mma;  // diagnostics only: XTC_DEBUG_SKIP_MMA, or XTC_DEBUG_SKIP=mask.  conv_halo (output
+                             // invalid unless noted): 1 no MMAs, 2 no patch TMA, 4 no output stores, 8 no TMEM
+                             // drain, 16 plain arrives, 64 no epilogue, 128 sleeping waits, 256 no tap shifts,
+                             // 512 every UMMA twice, 1024 (+64) free-run MMA warp (no patch loads, no per-tile
+                             // waits or commits), 2048 (+1024) per-tile commits, 4096 no per-tile tcgen05
+                             // fence; valid output: 8192 no early producer start, 65536 full bulk wait at exit.
+                             // tc_gemm: any bit but 65536 = no MMAs; 65536 as above.
     int64_t ldc, ws_ld;
     void* C; float* Wk;
     uint32_t idesc;
