@@ -238,6 +238,8 @@ def run_extras(xtc, torch, dev, peak):
                                                      split_k=sk, pack_warps=2) for sk in (2, 3)]
             if name == "L14":   # few tiles at small batch: narrower halo tiles spread over more SMs
                 cands.append(dict(HALO, tile_n=64, tile_k=128, stages=4))
+                # ... with direct stores, so all 8 warps drain the (only) tile: -1.3 us at N=1
+                cands.append(dict(HALO, tile_n=64, tile_k=128, stages=4, buffer_c=0))
                 # ... and the K segments of each tile over a cluster, reduced in the kernel (split_k_mode 2)
                 cands += [dict(HALO, tile_n=64, tile_k=128, stages=3, buffer_c=0, split_k=sk, split_k_mode=2)
                           for sk in (6, 9)]

@@ -58,7 +58,9 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
     uint64_t* bfull = tempty + 2;                // resident filter: one barrier per k-block
     uint64_t* ksig = bfull + kHaloMaxResidentKb; // cluster split-K: partials-written signals (2, by tile parity)
     uint64_t* tready = ksig + 2;                 // TMEM allocated (its address is in tmem_slot)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tready + 1);
+    uint64_t* tlast = tready + 1;                // the CTA's last tile accumulated (one phase: warps 0..3 drain
+                                                 // half of it; tfull's parity would alias earlier tiles)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tlast + 1);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -109,6 +111,7 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
         for (int i = 0; i < kHaloMaxResidentKb; ++i) ptx::mbar_init(&bfull[i], 1);
         if (kclu) { ptx::mbar_init(&ksig[0], 4u * ksc); ptx::mbar_init(&ksig[1], 4u * ksc); }
         ptx::mbar_init(tready, 1);
+        ptx::mbar_init(tlast, 1);
         ptx::fence_mbarrier_init();
     }
     // barriers first (peers' barriers exist before multicasts); the TMEM allocation is then
@@ -227,6 +230,12 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
     };
     const int sfold = p.sfold > 1 ? p.sfold : 1;  // s-fold: accumulator blocks s = 0..S-1 of tile_n columns
     const int acc_cols = MSUB * p.tile_n * sfold;  // TMEM columns of one accumulator buffer
+    // the CTA's LAST tile is drained by all 8 warps: warps 4..7 take columns [0, tile_n/2), warps 0..3 --
+    // idle by then -- the upper half of the same TMEM lane quarters (warp w reads lanes 32(w%4)..).  Direct
+    // stores only (no staging SMEM for warps 0..3), one CTA per tile, no split / stream-K / s-fold.  The
+    // one-tile-per-CTA shapes (L14, small batches) pay their whole epilogue after the last MMA.
+    const bool split_last = !(p.debug_skip_mma & 0x20000) && CL == 1 && !kclu && !sk && sfold == 1 && p.buffer_c == 0 &&
+                            !p.split_out && !p.atomic && p.tile_n >= 64 && (p.tile_n & 63) == 0 && n_walk > 0;
     if (trace && threadIdx.x == 0) trace[1] = ptx::globaltimer();
     int tj = 0;                                  // per-role tile counter for the trace
 
@@ -481,9 +490,11 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
                 } else if (plain_arrive) {            // diagnostics: plain arrives (valid only without MMAs)
                     ptx::mbar_arrive(&pempty[pb]);
                     ptx::mbar_arrive(&tfull[acc]);
+                    if (split_last && it + 1 == n_mma) ptx::mbar_arrive(tlast);
                 } else {
                     ptx::umma_commit<CG>(&pempty[pb]);    // patch buffer(s) free once these MMAs finish
                     ptx::umma_commit<CG>(&tfull[acc]);
+                    if (split_last && it + 1 == n_mma) ptx::umma_commit<CG>(tlast);
                 }
                 if (mphs) {
                     const uint64_t c2 = clock64();
@@ -557,7 +568,8 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
                 const bool valid = prow < P && qcol < Q;
                 const bool any_valid = prow0 < P;              // rows grow with the lane index
                 const uint32_t t_row = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * acc_cols + ms * p.tile_n);
-                for (int c = 0; c < p.tile_n; c += 32) {
+                const int c_end = (split_last && it + 1 == n_walk) ? p.tile_n / 2 : p.tile_n;
+                for (int c = 0; c < c_end; c += 32) {
                     uint32_t vals[32];
                     lap(4);
                     ptx::tmem_ld_32x32b_x32(t_row + c, vals);
@@ -765,6 +777,67 @@ tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
         }
     }
 
+    if (split_last && warp < 4 && !(p.debug_skip_mma & (64 | 8))) {
+        const uint32_t tmem_base = tmem_address();
+        const int64_t it = n_walk - 1;
+        const int acc = (int)(it % p.acc_buffers);
+        const uint32_t aph = (uint32_t)((it / p.acc_buffers) & 1);
+        TileInfo ti;
+        tile_at(it, ti);
+        (void)aph;
+        ptx::mbar_wait(tlast, 0);                  // the last tile's MMAs are complete
+        ptx::tc_fence_after();
+        const int q = warp, P = p.cg.P, Q = p.cg.Q;
+        const bool bf16_out = p.out_bf16 != 0;
+#pragma unroll 1
+        for (int ms = 0; ms < MSUB; ++ms) {
+            const int w = ti.off + ms * 128 + 32 * q + lane;   // this thread's row (pow2 rows: off = 0)
+            const int r = w / p.wp;
+            const int prow = ti.p0 + r, qcol = w - r * p.wp;
+            const bool valid = prow < P && qcol < Q;
+            const int64_t m = ((int64_t)ti.nimg * P + prow) * Q + qcol;
+            const uint32_t t_row = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * acc_cols + ms * p.tile_n);
+#pragma unroll 1
+            for (int c = p.tile_n / 2; c < p.tile_n; c += 32) {
+                uint32_t vals[32];
+                ptx::tmem_ld_32x32b_x32(t_row + c, vals);
+                ptx::tmem_ld_wait();
+                if (!valid) continue;
+                const int64_t col0 = (int64_t)ti.n0 + c;
+                const int ncols = (int)((p.N - col0) < 32 ? (p.N - col0) : 32);
+                if (ncols <= 0) continue;
+                if (p.cons) apply_consumer32(vals, p.cons, p.bias, p.C, bf16_out, m, p.ldc, col0, ncols);
+                if (bf16_out) {
+                    uint16_t* dst = reinterpret_cast<uint16_t*>(p.C) + m * p.ldc + col0;
+                    if (ncols == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            uint4 o;
+                            o.x = ptx::pack_bf16x2(__uint_as_float(vals[8 * j + 0]), __uint_as_float(vals[8 * j + 1]));
+                            o.y = ptx::pack_bf16x2(__uint_as_float(vals[8 * j + 2]), __uint_as_float(vals[8 * j + 3]));
+                            o.z = ptx::pack_bf16x2(__uint_as_float(vals[8 * j + 4]), __uint_as_float(vals[8 * j + 5]));
+                            o.w = ptx::pack_bf16x2(__uint_as_float(vals[8 * j + 6]), __uint_as_float(vals[8 * j + 7]));
+                            reinterpret_cast<uint4*>(dst)[j] = o;
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) if (j < ncols)
+                            dst[j] = (uint16_t)(ptx::pack_bf16x2(__uint_as_float(vals[j]), 0.f) & 0xFFFFu);
+                    }
+                } else {
+                    float* dst = reinterpret_cast<float*>(p.C) + m * p.ldc + col0;
+                    if (ncols == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+#pragma unroll
+                        for (int j = 0; j < 8; ++j)
+                            reinterpret_cast<uint4*>(dst)[j] = make_uint4(vals[4 * j], vals[4 * j + 1], vals[4 * j + 2], vals[4 * j + 3]);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) if (j < ncols) dst[j] = __uint_as_float(vals[j]);
+                    }
+                }
+            }
+        }
+    }
     ptx::tc_fence_before();
     if (CL == 2 || kclu) ptx::cluster_sync(); else __syncthreads();   // no CTA exits while a peer may still signal it
     if (trace && threadIdx.x == 0) trace[2] = ptx::globaltimer();

@@ -247,7 +247,8 @@ struct TcParams {
                              // drain, 16 plain arrives, 64 no epilogue, 128 sleeping waits, 256 no tap shifts,
                              // 512 every UMMA twice, 1024 (+64) free-run MMA warp (no patch loads, no per-tile
                              // waits or commits), 2048 (+1024) per-tile commits, 4096 no per-tile tcgen05
-                             // fence; valid output: 8192 no early producer start, 65536 full bulk wait at exit.
+                             // fence; valid output: 8192 no early producer start, 65536 full bulk wait at exit,
+                             // 0x20000 last tile drained by warps 4..7 only.
                              // tc_gemm: any bit but 65536 = no MMAs; 65536 as above.
     int64_t ldc, ws_ld;
     void* C; float* Wk;
