@@ -218,6 +218,11 @@ HALO_CASES = [
                                                         buffer_c=0, grid_sms=3)),
     ((2, 13, 13, 64, 64, 3, 3, 1, "bf16", "f32"), dict(pack_halo=2, tile_n=64, stages=2, buffer_c=0)),
     ((2, 14, 14, 64, 64, 3, 3, 1, "tf32", "f32"), dict(pack_halo=2, tile_n=64, tile_k=32, stages=4, buffer_c=0)),
+    # ragged N tiles (F = 96 / 160: the last tile's upper half partly or wholly past F) with direct stores, where
+    # warps 0-3 drain the upper column half of each CTA's last tile; tile_m 256, compact rows, several tiles per CTA
+    ((2, 20, 21, 64, 96, 3, 3, 1, "bf16", "f32"), dict(tile_m=256, tile_n=64, stages=3, buffer_c=0)),
+    ((3, 17, 39, 64, 160, 3, 3, 1, "bf16", "bf16"), dict(pack_halo=2, tile_n=128, stages=3, buffer_c=0, grid_sms=5)),
+    ((2, 14, 14, 128, 96, 3, 3, 1, "bf16", "bf16"), dict(tile_n=64, tile_k=128, stages=3, buffer_c=0, grid_sms=3)),
     # compact rows with the CTA pair (tile j of images 2i and 2i + 1): F = 64 halves, a two-N-tile ring, ragged
     ((4, 56, 56, 64, 64, 3, 3, 1, "bf16", "bf16"), dict(PAIR_H, pack_halo=2, tile_n=64, b_resident=1, stages=2,
                                                         buffer_c=0)),
@@ -728,6 +733,16 @@ def test_consumer_halo_compact_rows_and_pair64(cons):
     run_consumer(xtc.conv2d_desc(2, 9, 13, 64, 64, 3, 3, 1, 1, "bf16", "f32"),
                  tc(pack_halo=1, buffer_c=0, acc_buffers=1, **pair), cons, "bf16", "f32", MODE_INT)
     run_consumer(L56(), tc(pack_halo=2, buffer_c=0, acc_buffers=2, **pair), cons, "bf16", "bf16", MODE_INT)
+
+
+def test_consumer_halo_split_last_ragged_n():
+    """bias + relu on a ragged N tile drained by both warp groups (warps 0-3 take the upper half of the last tile)."""
+    run_consumer(xtc.conv2d_desc(2, 20, 21, 64, 96, 3, 3, 1, 1, "bf16", "f32"),
+                 tc(pack_halo=1, tile_n=64, stages=3, buffer_c=0, persistent=1, acc_buffers=2, fuse=1, grid_sms=3),
+                 "bias+relu", "bf16", "f32", MODE_INT)
+    run_consumer(xtc.conv2d_desc(2, 20, 21, 64, 96, 3, 3, 1, 1, "bf16", "bf16"),
+                 tc(pack_halo=2, tile_n=64, stages=3, buffer_c=0, persistent=1, acc_buffers=1, fuse=1),
+                 "accumulate+bias+relu", "bf16", "bf16", MODE_INT)
 
 
 def test_consumer_halo_split_k_in_the_reduction():
